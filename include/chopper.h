@@ -1,0 +1,256 @@
+/*
+ * chopper.h -- C ABI of the B200-native Chopper analysis hot path.
+ *
+ * Chopper (arXiv 2512.08242) turns per-GPU kernel traces, serialized
+ * hardware-counter passes and 1 ms frequency / power samples of an FSDP LLM
+ * training run into multi-granularity attributions (kernel -> operation ->
+ * layer -> phase -> iteration -> GPU) and the paper's
+ * theoretical-vs-observed gap breakdown (Eqs. 4-8).
+ * This library implements that analysis as hand-written sm_100a CUDA; the
+ * readings of every silent / ambiguous point are DESIGN.md D1..D22.
+ *
+ * Conventions
+ *  - All timestamps are int64 nanoseconds.  t_l = host dispatch, t_ks =
+ *    device start, t_ke = device end.
+ *  - Every pointer documented "device" must be device memory of `device`
+ *    (e.g. a torch CUDA tensor); "host" pointers are host memory.
+ *  - Input buffers are BORROWED: they must stay alive and unmodified until
+ *    chopper_destroy (or the next chopper_load_columns).
+ *  - The library never allocates device memory: all intermediates live in
+ *    the caller's scratch buffer of chopper_scratch_bytes() bytes.
+ *  - Every call enqueues work on the ctx stream.  Host-detectable errors
+ *    (bad arguments, call order) are returned immediately; device-detected
+ *    errors latch into a status mask read by chopper_status_sync().  Some
+ *    calls synchronize the stream internally (documented per call).
+ *  - Nothing throws across the ABI.  chopper_last_error() holds a message.
+ *  - Calls must come in order: load_columns -> align -> attribute ->
+ *    overlap -> breakdown -> reduce_ranks (align may be skipped when there
+ *    are no counters and only one rank; otherwise CHOPPER_E_STATE).
+ */
+#ifndef CHOPPER_H
+#define CHOPPER_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHOPPER_ABI_VERSION 1
+
+typedef struct chopper_ctx chopper_ctx;
+typedef int32_t chopper_status;
+
+/* status codes; codes 1 and 3 mirror SPEC.md:544 exit codes */
+enum {
+    CHOPPER_OK = 0,
+    CHOPPER_E_VALIDATION = 1,        /* input invariant violated */
+    CHOPPER_E_INVALID_ARG = 2,
+    CHOPPER_E_ALIGNMENT = 3,         /* counter pass name sequence mismatch / conflict */
+    CHOPPER_E_AMBIGUOUS_SPANS = 4,   /* a dispatch falls where same-level spans cross */
+    CHOPPER_E_RANGE = 5,             /* a size exceeds a configured bound */
+    CHOPPER_E_INSUFFICIENT_DATA = 6,
+    CHOPPER_E_CUDA = 7,
+    CHOPPER_E_NCCL = 8,
+    CHOPPER_E_STATE = 9              /* call out of order */
+};
+
+/* event kinds (low 8 bits of meta) */
+enum { CK_COMPUTE = 0, CK_AG = 1, CK_RS = 2, CK_COMM_OTHER = 3, CK_COPY = 4, CK_MEMOP = 5, CK_OTHER = 6 };
+
+/* validation rules, index into chopper_report.val_count / val_first */
+enum {
+    CV_START_AFTER_END = 0,     /* t_ks > t_ke                                          (fatal) */
+    CV_GPU_NOT_GROUPED = 1,     /* events not grouped by gpu ascending                  (fatal) */
+    CV_DISPATCH_DECREASING = 2, /* t_l decreases within a gpu                           (fatal) */
+    CV_BAD_META = 3,            /* kind > 6, gpu >= n_traced_gpus, compute stream > 253 (fatal) */
+    CV_TS_RANGE = 4,            /* max - min over all event timestamps >= 2^52          (fatal) */
+    CV_STREAM_OVERLAP = 5,      /* same (gpu, compute stream) intervals overlap         (data)  */
+    CV_SPAN_BAD = 6,            /* span end < start, level > 3, gpu >= n_traced_gpus     (fatal) */
+    CV_SAMPLES_UNSORTED = 7,    /* samples not sorted by (gpu, ts) / bad gpu            (fatal) */
+    CV_COUNTER_NONFINITE = 8,   /* a counter pass holds a non-finite value (pass skipped)       */
+    CV_NRULES = 9
+};
+
+/* Kernel events, SoA, device.  Grouped by gpu ascending; within a gpu in
+ * dispatch order (t_l non-decreasing; ties keep input order = correlation
+ * order).  meta = (gpu << 24) | (stream << 8) | kind, stream dense
+ * per gpu.  A rank passes only the traced GPUs it owns. */
+typedef struct {
+    int64_t n;
+    const int64_t *dispatch_ns, *start_ns, *end_ns;
+    const uint32_t *meta;
+    const int32_t *name_id;
+} chopper_events;
+
+/* Annotation spans, SoA, device, any order.  gpu_level = (gpu << 8) | level,
+ * level 0 iteration, 1 phase, 2 layer, 3 operation.  Half-open [start, end)
+ * on the host (dispatch) timeline (D3).  label: iteration -> step number
+ * (joins iterations across GPUs, D5); operation -> op label id
+ * (0..n_labels-1); phase / layer -> free. */
+typedef struct {
+    int64_t n;
+    const uint32_t *gpu_level;
+    const int64_t *start_ns, *end_ns;
+    const int32_t *label;
+} chopper_spans;
+
+/* 1 ms frequency / power samples, SoA, device, sorted by (gpu, ts).
+ * Zero-order hold with extended ends (D10). */
+typedef struct {
+    int64_t n;
+    const int32_t *gpu;
+    const int64_t *ts_ns;
+    const int32_t *freq_mhz, *power_mw;
+} chopper_samples;
+
+/* One serialized counter pass of one gpu: the name ids of
+ * that gpu's non-MEMOP kernels in dispatch order (D2) and k counters per
+ * kernel.  name_id, values: device; slot: host. */
+typedef struct {
+    int32_t gpu;
+    int64_t n;
+    const int32_t *name_id;     /* [n] */
+    int32_t k;
+    const int32_t *slot;        /* host [k]: counter slot in 0..n_counters-1 */
+    const double *values;       /* [k][n] */
+} chopper_counter_pass;
+
+typedef struct {
+    int32_t n_traced_gpus;      /* traced GPUs in the whole run (all ranks) */
+    int32_t n_labels;           /* op label vocabulary size (identical on every rank) */
+    int32_t max_iters;          /* bound on iteration rank (fixed exchange shapes) */
+    int32_t max_coll_per_class; /* bound on AG (and RS) events per traced GPU */
+} chopper_config;
+
+/* Breakdown parameters.  Arrays are host memory. */
+typedef struct {
+    double tpt_peak;            /* TPT_peak, FLOP/s */
+    double freq_peak_hz;        /* Freq_peak, Hz */
+    int64_t batch, seq, ranks;  /* b, s, R: tokens per iteration = b*s*R */
+    int32_t warmup;             /* iterations with rank < warmup are not sampled */
+    int32_t slot_gpu_cycles, slot_perf_flops, slot_util_num, slot_util_den;  /* -1 = absent */
+    const double *f_gemm;       /* [n_labels] theoretical FLOPs per point (Eq. 4) */
+    const int32_t *op_type;     /* [n_labels] 1 gemm, 2 fa, 0 other */
+    int32_t n_ratios;           /* derived ratio-of-sums rates */
+    const int32_t *ratio_num;   /* [n_ratios] counter slot */
+    const int32_t *ratio_den;   /* [n_ratios] counter slot, or -1 = busy seconds */
+    const double *ratio_scale;  /* [n_ratios] */
+} chopper_bd_params;
+
+/* Row table (device SoA; pointers into ctx scratch; valid until the next
+ * chopper_load_columns / chopper_destroy).  Columns are [n] unless noted. */
+typedef struct {
+    int64_t n;
+    const int32_t *gpu, *it, *ph, *ly, *op;   /* caller span indices, -1 = none (unlabeled) */
+    const int32_t *label;                     /* op label (points, instances), -1 otherwise */
+    const int32_t *rank;                      /* iteration rank (iteration rows, points) else -1 */
+    const int64_t *n_events, *n_compute, *busy, *first_ks, *first_idx, *first_pred, *last_ke;
+    const int64_t *prep, *call, *ovl, *phi, *psi, *copy_ns, *ag_ns, *rs_ns;
+    const double *counters;                   /* [n_counters][n] */
+    const double *rates;                      /* [n_ratios][n] (points, iterations) or NULL */
+    /* iteration rows only (else NULL) */
+    const int64_t *wall, *comm_union, *aligned_first, *aligned_last;
+    const int32_t *step;
+} chopper_rows;
+
+typedef struct {
+    chopper_rows inst, layer, phase, iter, gpu, point;
+    int64_t n_bd;                             /* local breakdown rows */
+    const double *bd;                         /* device [n_bd][16], layout as chopper_global.bd */
+} chopper_tables;
+
+/* Host-visible global results (chopper_reduce_ranks). bd rows: 16 doubles:
+ * 0 n_points, 1 method (0 bucket, 1 fit), 2 D_act s, 3 D0 s, 4 D50 s,
+ * 5 D_thr, 6 Ovr_inst, 7 Ovr_util, 8 Ovr_overlap, 9 D_peak, 10 Ovr_freq,
+ * 11 Ovr_launch, 12 residual, 13 Ovr_freq_samples, 14 flags, 15 label. */
+typedef struct {
+    int64_t n_iters;                          /* iterations of the reference gpu */
+    int32_t step[4096], complete[4096], sampled[4096];
+    int64_t T[4096], aligned_first[4096], aligned_last[4096];
+    double throughput[4096];
+    double throughput_median;
+    int64_t n_bd;
+    double bd[256 * 16];
+    int64_t delta[256];                       /* clock offsets per traced gpu (D13) */
+    int32_t delta_flag[256];
+    int64_t max_skew_ag, max_skew_rs;
+} chopper_global;
+
+/* Device-side report read back by chopper_load_columns (host struct). */
+typedef struct {
+    int64_t val_count[CV_NRULES];
+    int64_t val_first[CV_NRULES];             /* smallest offending index, -1 none */
+    int64_t n_local_gpus;
+    int32_t local_gpu[256];
+    int64_t t_min, t_max;
+    int32_t full_sort_used;                   /* 1: timestamp radix sort ran (groups not start-monotone) */
+    int32_t non_laminar_lists;                /* (gpu, level) span lists needing the exact sweep path */
+} chopper_report;
+
+/* Worst-case scratch bytes for a ctx (all ranks may pass their own sizes). */
+size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_t n_spans, int64_t n_samples,
+                             int32_t n_counters);
+
+/* nccl_comm: ncclComm_t of the process group (borrowed), NULL when nranks == 1.
+ * cuda_stream: cudaStream_t (borrowed), NULL = legacy default stream. */
+chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int device, void *cuda_stream,
+                              void *nccl_comm, int rank, int nranks, void *scratch, size_t scratch_bytes);
+
+/* a1 pack + validate, a2 timestamp sort (stable by (gpu, group, t_ks), D1),
+ * same-stream disjointness and the launch chain predecessor.
+ * samples may be NULL.  Synchronizes the stream (reads the report). */
+chopper_status chopper_load_columns(chopper_ctx *ctx, const chopper_events *ev, const chopper_spans *sp,
+                                    const chopper_samples *smp);
+
+/* a3 counter alignment and a4 clock offsets (D13; NCCL
+ * all-gather #1 when nranks > 1).  counters_out: device [n_counters][n_events]
+ * in input order, or NULL (tables-only).  offsets_ns: host [n_traced_gpus] or
+ * NULL.  Synchronizes the stream. */
+chopper_status chopper_align(chopper_ctx *ctx, const chopper_counter_pass *passes, int32_t n_passes,
+                             int32_t n_counters, double *counters_out, int64_t *offsets_ns);
+
+/* a5 interval-containment attribution.
+ * span_idx: device [4][n_events] caller span index per level, -1 none,
+ * -2 ambiguous (D4), or NULL.  Synchronizes the stream. */
+chopper_status chopper_attribute(chopper_ctx *ctx, int32_t *span_idx);
+
+/* a6 overlap (D9), a7 launch overhead Eqs. 1-3 (D6-D8), a8 DVFS integrals
+ * (D10), fused with the time reductions of a9.  Each output is device [n]
+ * or NULL: ovl (COMPUTE: |[t_ks,t_ke) ∩ comm union|; comm: |∩ compute
+ * union|), prep, call, phi (MHz*ns), psi (mW*ns). */
+chopper_status chopper_overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_ns, int64_t *call_ns,
+                               int64_t *phi, int64_t *psi);
+
+/* a9 segmented reductions + roll-ups, a10 gap decomposition over this
+ * rank's points.  Fills *out with device table pointers.  Synchronizes. */
+chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, chopper_tables *out);
+
+/* a11: NCCL all-gather #2 of per-gpu rows, then global composition
+ * (throughput, medians, global breakdown).  Synchronizes. */
+chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
+
+/* report of the last chopper_load_columns (host copy) */
+chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out);
+/* synchronizes the ctx stream; returns the first latched error and fills the
+ * latched mask (bit c set for each latched status code c) if mask != NULL */
+chopper_status chopper_status_sync(chopper_ctx *ctx, uint32_t *mask);
+const char *chopper_last_error(const chopper_ctx *ctx);
+void chopper_destroy(chopper_ctx *ctx);
+
+/* number of device kernels this ctx launched since creation (bench evidence) */
+int64_t chopper_kernel_launches(const chopper_ctx *ctx);
+int32_t chopper_abi_version(void);
+
+/* introspection after chopper_align: first name-sequence divergence / first
+ * conflicting value index of pass p (-1 none), and slot presence per gpu */
+int64_t chopper_pass_mismatch(const chopper_ctx *ctx, int32_t p);
+int64_t chopper_pass_conflict(const chopper_ctx *ctx, int32_t p);
+int32_t chopper_counter_present(const chopper_ctx *ctx, int32_t gpu, int32_t slot);
+/* scratch bytes in use (high-water of the bump arena) */
+int64_t chopper_scratch_used(const chopper_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

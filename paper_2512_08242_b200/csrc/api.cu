@@ -1,0 +1,267 @@
+// api.cu -- the C ABI (include/chopper.h): argument checks, call order,
+// status latching.  Every compute step runs in the kernels of this directory.
+#include "common.cuh"
+
+chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &msg) {
+    ctx->err = msg;
+    ctx->latched_host |= 1u << s;
+    return s;
+}
+
+extern "C" {
+
+int32_t chopper_abi_version(void) { return CHOPPER_ABI_VERSION; }
+
+size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_t n_spans, int64_t n_samples,
+                             int32_t n_counters) {
+    if (!cfg) return 0;
+    int64_t N = n_events > 0 ? n_events : 1, S = n_spans > 0 ? n_spans : 1, M = n_samples > 0 ? n_samples : 1;
+    int64_t C = n_counters > 0 ? n_counters : 0;
+    int64_t G = cfg->n_traced_gpus > 0 ? cfg->n_traced_gpus : 1;
+    int64_t MI = cfg->max_iters > 0 ? cfg->max_iters : 1, L = cfg->n_labels > 0 ? cfg->n_labels : 1;
+    int64_t K = cfg->max_coll_per_class > 0 ? cfg->max_coll_per_class : 1;
+    size_t b = 0;
+    b += (size_t)N * (420 + 40 * C);         // sort buffers, chain, unions, sub-runs, instance tables
+    b += (size_t)S * 160;                    // push-order span arrays + sort buffers
+    b += (size_t)M * 64;                     // sample prefixes
+    b += (size_t)G * (4 + 4 * K) * 8 * 2;    // clock-offset exchange
+    b += (size_t)G * (8 + C + 8 * MI + 9 * MI * L) * 8 * 2;   // dense row exchange
+    b += (size_t)L * 10 * 8 * MI * G * 2;    // breakdown scratch
+    b += (size_t)256 << 20;
+    return b;
+}
+
+chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int device, void *cuda_stream,
+                              void *nccl_comm, int rank, int nranks, void *scratch, size_t scratch_bytes) {
+    if (!out || !cfg || !scratch) return CHOPPER_E_INVALID_ARG;
+    if (cfg->n_traced_gpus <= 0 || cfg->n_traced_gpus > CH_MAX_GPUS || cfg->n_labels < 0 || cfg->max_iters <= 0 ||
+        cfg->max_coll_per_class < 0 || nranks <= 0 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_comm))
+        return CHOPPER_E_INVALID_ARG;
+    chopper_ctx *c = new chopper_ctx();
+    c->cfg = *cfg;
+    c->device = device;
+    c->st = (cudaStream_t)cuda_stream;
+    c->nccl = nccl_comm;
+    c->rank = rank;
+    c->nranks = nranks;
+    c->scratch = (char *)scratch;
+    c->scratch_bytes = scratch_bytes;
+    if (cudaSetDevice(device) != cudaSuccess) {
+        delete c;
+        return CHOPPER_E_CUDA;
+    }
+    *out = c;
+    return CHOPPER_OK;
+}
+
+chopper_status chopper_load_columns(chopper_ctx *ctx, const chopper_events *ev, const chopper_spans *sp,
+                                    const chopper_samples *smp) {
+    if (!ctx || !ev || !sp) return CHOPPER_E_INVALID_ARG;
+    if (ev->n < 0 || ev->n > 0x7fffffffll || sp->n < 0 || sp->n > 0x7fffffffll)
+        return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "event / span count out of range");
+    if (ev->n > 0 && (!ev->dispatch_ns || !ev->start_ns || !ev->end_ns || !ev->meta || !ev->name_id))
+        return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "NULL event column");
+    if (sp->n > 0 && (!sp->gpu_level || !sp->start_ns || !sp->end_ns || !sp->label))
+        return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "NULL span column");
+    ctx->ev = *ev;
+    ctx->sp = *sp;
+    ctx->has_smp = smp && smp->n > 0;
+    if (ctx->has_smp && (!smp->gpu || !smp->ts_ns || !smp->freq_mhz || !smp->power_mw))
+        return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "NULL sample column");
+    ctx->smp = ctx->has_smp ? *smp : chopper_samples{};
+    ctx->N = ev->n;
+    ctx->S = sp->n;
+    ctx->M = ctx->has_smp ? smp->n : 0;
+    ctx->stage = 0;
+    ctx->latched_host = 0;
+    ctx->offsets_done = false;
+    ctx->C = 0;
+    ctx->d_col = nullptr;
+    ctx->d_nm_rank = nullptr;
+    ctx->present.clear();
+    ctx->err.clear();
+    memset(&ctx->rep, 0, sizeof(ctx->rep));
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return ch_fail(ctx, CHOPPER_E_CUDA, "cudaSetDevice");
+    chopper_status s = ch_load(ctx);
+    if (s != CHOPPER_OK) return s;
+    ctx->stage = 1;
+    return CHOPPER_OK;
+}
+
+chopper_status chopper_align(chopper_ctx *ctx, const chopper_counter_pass *passes, int32_t n_passes,
+                             int32_t n_counters, double *counters_out, int64_t *offsets_ns) {
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    if (ctx->stage != 1 || !ctx->loaded_ok) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_align before load");
+    if (n_passes < 0 || n_counters < 0 || (n_passes > 0 && !passes))
+        return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "bad counter passes");
+    CH_TRY(ch_align(ctx, passes, n_passes, n_counters, counters_out));
+    CH_TRY(ch_offsets(ctx));
+    ctx->offsets_done = true;
+    if (offsets_ns)
+        for (int g = 0; g < ctx->cfg.n_traced_gpus; g++) offsets_ns[g] = ctx->delta[g];
+    ctx->stage = 2;
+    return CHOPPER_OK;
+}
+
+chopper_status chopper_attribute(chopper_ctx *ctx, int32_t *span_idx) {
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    if (ctx->stage == 1 && ctx->nranks == 1) {
+        // align may be skipped on one rank without counters
+        CH_TRY(ch_align(ctx, nullptr, 0, 0, nullptr));
+        CH_TRY(ch_offsets(ctx));
+        ctx->offsets_done = true;
+        ctx->stage = 2;
+    }
+    if (ctx->stage != 2) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_attribute out of order");
+    CH_TRY(ch_build_spans(ctx));
+    CH_TRY(ch_attr_pass(ctx, span_idx));
+    ctx->stage = 3;
+    return CHOPPER_OK;
+}
+
+chopper_status chopper_overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_ns, int64_t *call_ns, int64_t *phi,
+                               int64_t *psi) {
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    if (ctx->stage != 3) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_overlap out of order");
+    CH_TRY(ch_overlap_prep(ctx));
+    CH_TRY(ch_event_pass(ctx, ovl_ns, prep_ns, call_ns, phi, psi));
+    ctx->stage = 4;
+    return CHOPPER_OK;
+}
+
+static void fill_rows(chopper_rows &r, const RowTable &t, bool iter, chopper_ctx *ctx) {
+    memset(&r, 0, sizeof(r));
+    r.n = t.n;
+    r.gpu = t.gpu; r.it = t.it; r.ph = t.ph; r.ly = t.ly; r.op = t.op; r.label = t.label; r.rank = t.rank;
+    r.n_events = t.f + (int64_t)RF_NEV * t.cap;
+    r.n_compute = t.f + (int64_t)RF_N * t.cap;
+    r.busy = t.f + (int64_t)RF_BUSY * t.cap;
+    r.first_ks = t.f + (int64_t)RF_FIRST_KS * t.cap;
+    r.first_idx = t.f + (int64_t)RF_FIRST_IDX * t.cap;
+    r.first_pred = t.first_pred;
+    r.last_ke = t.f + (int64_t)RF_LAST_KE * t.cap;
+    r.prep = t.f + (int64_t)RF_PREP * t.cap;
+    r.call = t.f + (int64_t)RF_CALL * t.cap;
+    r.ovl = t.f + (int64_t)RF_OVL * t.cap;
+    r.phi = t.f + (int64_t)RF_PHI * t.cap;
+    r.psi = t.f + (int64_t)RF_PSI * t.cap;
+    r.copy_ns = t.f + (int64_t)RF_COPY * t.cap;
+    r.ag_ns = t.f + (int64_t)RF_AG * t.cap;
+    r.rs_ns = t.f + (int64_t)RF_RS * t.cap;
+    r.counters = t.cnt;
+    r.rates = t.rates;
+    if (iter) {
+        r.wall = ctx->iter_wall;
+        r.comm_union = ctx->iter_cu;
+        r.aligned_first = ctx->iter_af;
+        r.aligned_last = ctx->iter_al;
+        r.step = ctx->iter_step;
+    }
+}
+
+chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, chopper_tables *out) {
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    if (ctx->stage != 4) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_breakdown out of order");
+    if (!p || !out || (ctx->cfg.n_labels > 0 && (!p->f_gemm || !p->op_type)) || p->n_ratios < 0 ||
+        (p->n_ratios > 0 && (!p->ratio_num || !p->ratio_den || !p->ratio_scale)))
+        return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "bad breakdown parameters");
+    const int C = ctx->C;
+    auto bad_slot = [&](int s) { return s >= C || s < -1; };
+    if (bad_slot(p->slot_gpu_cycles) || bad_slot(p->slot_perf_flops) || bad_slot(p->slot_util_num) ||
+        bad_slot(p->slot_util_den))
+        return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "breakdown counter slot out of range");
+    for (int q = 0; q < p->n_ratios; q++)
+        if (p->ratio_num[q] < 0 || p->ratio_num[q] >= C || p->ratio_den[q] < -1 || p->ratio_den[q] >= C)
+            return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "ratio slot out of range");
+    ctx->bd = *p;
+    const int L = ctx->cfg.n_labels;
+    ctx->f_gemm.assign(p->f_gemm, p->f_gemm + L);
+    ctx->op_type.assign(p->op_type, p->op_type + L);
+    ctx->n_ratios = p->n_ratios;
+    CH_ALLOC_BEGIN;
+    ctx->d_f_gemm = CH_ALLOC(ctx, double, std::max(L, 1));
+    ctx->d_op_type = CH_ALLOC(ctx, int32_t, std::max(L, 1));
+    ctx->d_ratio = CH_ALLOC(ctx, int32_t, 2 * std::max(p->n_ratios, 1));
+    ctx->d_ratio_scale = CH_ALLOC(ctx, double, std::max(p->n_ratios, 1));
+    CH_ALLOC_END(ctx);
+    if (L > 0) {
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_f_gemm, ctx->f_gemm.data(), 8 * L, cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_op_type, ctx->op_type.data(), 4 * L, cudaMemcpyHostToDevice, ctx->st));
+    }
+    if (p->n_ratios > 0) {
+        std::vector<int32_t> r(2 * p->n_ratios);
+        for (int q = 0; q < p->n_ratios; q++) { r[q] = p->ratio_num[q]; r[p->n_ratios + q] = p->ratio_den[q]; }
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_ratio, r.data(), 4 * r.size(), cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_ratio_scale, p->ratio_scale, 8 * p->n_ratios, cudaMemcpyHostToDevice,
+                                     ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    }
+    CH_TRY(ch_tables(ctx));
+    CH_TRY(ch_breakdown_local(ctx));
+    memset(out, 0, sizeof(*out));
+    fill_rows(out->inst, ctx->inst, false, ctx);
+    fill_rows(out->layer, ctx->layer, false, ctx);
+    fill_rows(out->phase, ctx->phase, false, ctx);
+    fill_rows(out->iter, ctx->iter, true, ctx);
+    fill_rows(out->gpu, ctx->gpurow, false, ctx);
+    fill_rows(out->point, ctx->point, false, ctx);
+    out->n_bd = ctx->n_bd;
+    out->bd = ctx->d_bd;
+    ctx->stage = 5;
+    return CHOPPER_OK;
+}
+
+chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
+    if (!ctx || !out) return CHOPPER_E_INVALID_ARG;
+    if (ctx->stage != 5) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_reduce_ranks out of order");
+    memset(out, 0, sizeof(*out));
+    CH_TRY(ch_reduce_ranks(ctx, out));
+    ctx->stage = 6;
+    return CHOPPER_OK;
+}
+
+chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out) {
+    if (!ctx || !out) return CHOPPER_E_INVALID_ARG;
+    *out = ctx->rep;
+    return CHOPPER_OK;
+}
+
+chopper_status chopper_status_sync(chopper_ctx *ctx, uint32_t *mask) {
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    uint32_t m = ctx->latched_host;
+    if (cudaStreamSynchronize(ctx->st) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;
+    if (ctx->d_rep) {
+        unsigned int dl = 0;
+        if (cudaMemcpy(&dl, &ctx->d_rep->latched, 4, cudaMemcpyDeviceToHost) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;
+        m |= dl;
+    }
+    if (mask) *mask = m;
+    const chopper_status order[] = {CHOPPER_E_CUDA, CHOPPER_E_NCCL, CHOPPER_E_VALIDATION, CHOPPER_E_ALIGNMENT,
+                                    CHOPPER_E_AMBIGUOUS_SPANS, CHOPPER_E_RANGE, CHOPPER_E_INSUFFICIENT_DATA,
+                                    CHOPPER_E_INVALID_ARG, CHOPPER_E_STATE};
+    for (chopper_status s : order)
+        if (m & (1u << s)) return s;
+    return CHOPPER_OK;
+}
+
+const char *chopper_last_error(const chopper_ctx *ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+void chopper_destroy(chopper_ctx *ctx) { delete ctx; }
+
+int64_t chopper_kernel_launches(const chopper_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+/* extra introspection used by the Python binding / tests */
+int64_t chopper_pass_mismatch(const chopper_ctx *ctx, int32_t p) {
+    return (ctx && p >= 0 && p < (int)ctx->pass_mismatch.size()) ? ctx->pass_mismatch[p] : -1;
+}
+int64_t chopper_pass_conflict(const chopper_ctx *ctx, int32_t p) {
+    return (ctx && p >= 0 && p < (int)ctx->pass_conflict.size()) ? ctx->pass_conflict[p] : -1;
+}
+int32_t chopper_counter_present(const chopper_ctx *ctx, int32_t gpu, int32_t slot) {
+    if (!ctx || gpu < 0 || gpu >= CH_MAX_GPUS || slot < 0 || slot >= ctx->C) return 0;
+    int lg = ctx->gpu_lg_h[gpu];
+    return lg >= 0 && (size_t)lg * ctx->C + slot < ctx->present.size() ? ctx->present[(size_t)lg * ctx->C + slot] : 0;
+}
+int64_t chopper_scratch_used(const chopper_ctx *ctx) { return ctx ? (int64_t)ctx->used : 0; }
+
+}  // extern "C"

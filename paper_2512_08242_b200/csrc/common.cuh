@@ -1,0 +1,373 @@
+// common.cuh -- internals of the B200 Chopper library (sm_100a only).
+// Context, scratch arena, error latching, warp / block primitives shared by
+// the kernels in this directory.  Nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/chopper.h"
+
+#define CH_MAX_GPUS 256
+#define CH_NONE_TS INT64_MIN
+#define CH_INVALID_KEY 0xFFFFFFFFFFFFFFFFull
+#define CH_FULL 0xFFFFFFFFu
+
+// ---------------------------------------------------------------------------
+// device report (a1 validation + ranges), mirrored on the host
+// ---------------------------------------------------------------------------
+struct DevReport {
+    unsigned long long val_count[CV_NRULES];
+    unsigned long long val_first[CV_NRULES];    // ULLONG_MAX = none
+    unsigned long long t_min_enc, t_max_enc;    // order-preserving encodings of int64
+    unsigned long long s_min_enc, s_max_enc;    // spans start min / end max
+    unsigned long long gbeg[CH_MAX_GPUS], gend[CH_MAX_GPUS];  // event ranges per traced gpu
+    unsigned long long sbeg[CH_MAX_GPUS], send[CH_MAX_GPUS];  // sample ranges per traced gpu
+    unsigned int max_stream[CH_MAX_GPUS];       // max compute stream id + 1 (0 = no compute)
+    unsigned int n_comm[CH_MAX_GPUS];
+    unsigned int flags;                         // bit0: non-monotone group in partition order
+    unsigned int latched;                       // latched status mask (bit = status code)
+    unsigned long long n_nonlaminar;
+};
+
+__host__ __device__ inline unsigned long long enc_i64(int64_t v) { return (unsigned long long)v ^ 0x8000000000000000ull; }
+__host__ __device__ inline int64_t dec_i64(unsigned long long u) { return (int64_t)(u ^ 0x8000000000000000ull); }
+
+// ---------------------------------------------------------------------------
+// row tables (SoA, int64 field-major) -- see tables.cu
+// ---------------------------------------------------------------------------
+enum RowField {
+    RF_NEV = 0, RF_N, RF_BUSY, RF_FIRST_IDX, RF_LAST_KE, RF_PREP, RF_CALL, RF_OVL, RF_PHI, RF_PSI, RF_COPY, RF_AG,
+    RF_RS, RF_FIRST_KS, RF_NFIELDS
+};
+
+struct RowTable {
+    int64_t cap = 0;
+    int64_t n = 0;                  // host copy after count read-back
+    unsigned long long *key = nullptr;
+    int64_t *first_event = nullptr;  // for sub-runs; row: first child
+    int64_t *f = nullptr;            // [RF_NFIELDS][cap]
+    double *cnt = nullptr;           // [C][cap]
+    int32_t *gpu = nullptr, *it = nullptr, *ph = nullptr, *ly = nullptr, *op = nullptr, *label = nullptr,
+            *rank = nullptr;         // decoded identity columns (outputs)
+    int64_t *first_ks = nullptr, *first_pred = nullptr;
+    double *rates = nullptr;
+};
+
+struct PassDesc {          // device copy of one counter pass
+    const int32_t *name_id;
+    const double *values;
+    int64_t n;
+    int32_t k;
+    int32_t lg;
+};
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct chopper_ctx {
+    chopper_config cfg{};
+    int device = 0;
+    cudaStream_t st = nullptr;
+    void *nccl = nullptr;
+    int rank = 0, nranks = 1;
+    char *scratch = nullptr;
+    size_t scratch_bytes = 0, used = 0;
+    int64_t launches = 0;
+    std::string err;
+    int stage = 0;                 // 1 loaded, 2 aligned, 3 attributed, 4 overlapped, 5 breakdown
+    bool loaded_ok = false;
+
+    // borrowed inputs
+    chopper_events ev{};
+    chopper_spans sp{};
+    chopper_samples smp{};
+    bool has_smp = false;
+    int64_t N = 0, S = 0, M = 0;
+
+    // report
+    chopper_report rep{};
+    DevReport *d_rep = nullptr;
+    DevReport h_rep{};
+
+    // local gpus
+    int n_lg = 0;
+    int lg_gpu[CH_MAX_GPUS];
+    int gpu_lg_h[CH_MAX_GPUS];
+    int32_t *d_gpu_lg = nullptr;     // [256] gpu -> lg or -1
+    int64_t g_beg[CH_MAX_GPUS + 1];  // input ranges per lg
+    int max_stream = 0;              // max compute stream id + 1 over local gpus
+    int NG = 0, n_buckets = 0;
+    int64_t t0 = 0, t_max = 0;
+    bool multi_stream = false;
+
+    // a2 sort
+    uint32_t *d_perm = nullptr;      // sorted position -> input index
+    int64_t *d_bucket_beg = nullptr; // [n_buckets + 1]
+    std::vector<int64_t> bucket_beg;
+    int64_t *d_pred_end = nullptr;   // [N] end of chain predecessor or NONE
+    bool full_sort = false;
+
+    // spans (push order)
+    int64_t S_loc = 0;               // spans of local gpus with positive length
+    int64_t *P_start = nullptr, *P_end = nullptr;
+    int32_t *P_orig = nullptr, *P_label = nullptr, *P_parent = nullptr;
+    int64_t *d_list_beg = nullptr;   // [n_lg*4 + 2] push-order begin of each (lg, level) list
+    std::vector<int64_t> list_beg;
+    int32_t *d_list_flags = nullptr; // [n_lg*4] 1 = non-laminar
+    std::vector<int32_t> list_flags;
+    int32_t *d_attr_pre = nullptr;   // [4][N] precomputed (non-laminar lists)
+    int kb[4] = {0, 0, 0, 0};        // key bits per level
+    int kg = 0;                      // key bits for lg
+
+    // samples
+    int64_t *d_smp_phi = nullptr, *d_smp_psi = nullptr;  // prefix integrals at sample k
+    int64_t *d_smp_lo = nullptr, *d_smp_hi = nullptr;    // [n_lg] sample ranges per lg
+    std::vector<int64_t> smp_lo, smp_hi;
+
+    // comm union per lg (merged intervals) and compute-union strategy
+    int64_t *U_s = nullptr, *U_e = nullptr, *U_P = nullptr;
+    int64_t *d_U_beg = nullptr, *d_U_cnt = nullptr;      // [n_lg]
+    int64_t *V_s = nullptr, *V_e = nullptr, *V_P = nullptr;
+    int64_t *d_V_beg = nullptr, *d_V_cnt = nullptr;      // [n_lg]
+    uint32_t *d_vperm = nullptr;     // compute events sorted by (lg, t_ks) (multi-stream only)
+    int v_general = 0;               // 1 = compute union built explicitly
+
+    // sub-runs (a9 time part), produced by the fused event pass
+    int64_t R = 0;
+    RowTable sub;
+    int32_t *d_run_id = nullptr;     // [N] sub-run of each event
+    unsigned long long *d_tile_state = nullptr;
+    unsigned int *d_tile_ticket = nullptr;
+
+    // alignment
+    int C = 0;
+    std::vector<PassDesc> passes;
+    PassDesc *d_passes = nullptr;
+    int32_t *d_slot_pass = nullptr;  // [n_lg][C] pass index providing the slot, -1 absent
+    int32_t *d_nm_rank = nullptr;    // [N] rank among non-MEMOP events of its gpu
+    int64_t *d_delta = nullptr;      // [n_traced]
+    int32_t *d_delta_flag = nullptr;
+    std::vector<int64_t> delta;
+    std::vector<int32_t> delta_flag;
+    int64_t max_skew[2] = {0, 0};
+    std::vector<int32_t> present;    // [n_lg][C]
+    int32_t *d_present = nullptr;    // [n_lg][C]
+    const double **d_col = nullptr;  // [n_lg][C] value column of the pass providing the slot
+    std::vector<int64_t> pass_mismatch, pass_conflict;
+    std::vector<int> gpu_present;    // [n_traced] gpu has events on some rank
+
+    // tables
+    RowTable inst, layer, phase, iter, gpurow, point;
+    int64_t *iter_wall = nullptr, *iter_cu = nullptr, *iter_af = nullptr, *iter_al = nullptr;
+    int32_t *iter_step = nullptr;
+    double *d_bd = nullptr;
+    int64_t n_bd = 0;
+    chopper_bd_params bd{};
+    std::vector<double> f_gemm;
+    std::vector<int32_t> op_type;
+    double *d_f_gemm = nullptr;
+    int32_t *d_op_type = nullptr;
+    int32_t *d_ratio = nullptr;      // [2][n_ratios]
+    double *d_ratio_scale = nullptr;
+    int n_ratios = 0;
+    int32_t *d_has_smp = nullptr;    // [n_lg]
+    int64_t *d_dense = nullptr;      // local dense exchange blocks [dense_slots][W]
+    int dense_slots = 0;
+    bool offsets_done = false;
+
+    size_t mark_after_load = 0;
+    uint32_t latched_host = 0;      // host-detected latched status bits
+};
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+#define CH_CUDA(ctx, call)                                                                 \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            (ctx)->err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #call;     \
+            return CHOPPER_E_CUDA;                                                         \
+        }                                                                                  \
+    } while (0)
+
+#define CH_TRY(expr)                          \
+    do {                                      \
+        chopper_status s_ = (expr);           \
+        if (s_ != CHOPPER_OK) return s_;      \
+    } while (0)
+
+#define CH_LAUNCHED(ctx)                                                                   \
+    do {                                                                                   \
+        (ctx)->launches++;                                                                 \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess) {                                                           \
+            (ctx)->err = std::string("CUDA launch: ") + cudaGetErrorString(e_) + " @" +      \
+                         std::to_string(__LINE__) + " " + __FILE__;                        \
+            return CHOPPER_E_CUDA;                                                         \
+        }                                                                                  \
+    } while (0)
+
+chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &msg);
+chopper_status ch_fill_u64(chopper_ctx *ctx, unsigned long long *p, int64_t n, unsigned long long v);
+
+// ---------------------------------------------------------------------------
+// scratch arena (256 B aligned bump allocator)
+// ---------------------------------------------------------------------------
+template <class T>
+inline T *ch_alloc(chopper_ctx *ctx, int64_t n, chopper_status *st) {
+    size_t bytes = (size_t)(n > 0 ? n : 1) * sizeof(T);
+    size_t off = (ctx->used + 255) & ~(size_t)255;
+    if (off + bytes > ctx->scratch_bytes) {
+        if (*st == CHOPPER_OK) {
+            *st = CHOPPER_E_RANGE;
+            ctx->err = "scratch exhausted (need " + std::to_string(off + bytes) + " of " +
+                       std::to_string(ctx->scratch_bytes) + " bytes)";
+        }
+        return nullptr;
+    }
+    ctx->used = off + bytes;
+    return reinterpret_cast<T *>(ctx->scratch + off);
+}
+#define CH_ALLOC(ctx, T, n) ch_alloc<T>((ctx), (n), &st_)
+#define CH_ALLOC_BEGIN chopper_status st_ = CHOPPER_OK
+#define CH_ALLOC_END(ctx)            \
+    do {                             \
+        if (st_ != CHOPPER_OK) return st_; \
+    } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int bits_for(uint64_t v) {  // bits needed to represent values 0..v
+    int b = 0;
+    while (b < 64 && (v >> b) != 0) b++;
+    return b;
+}
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int kind_of(uint32_t m) { return (int)(m & 0xFFu); }
+__device__ __forceinline__ int stream_of(uint32_t m) { return (int)((m >> 8) & 0xFFFFu); }
+__device__ __forceinline__ int gpu_of(uint32_t m) { return (int)(m >> 24); }
+__device__ __forceinline__ bool is_comm(int k) { return k == CK_AG || k == CK_RS || k == CK_COMM_OTHER; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// record a validation violation (count + smallest index)
+__device__ __forceinline__ void viol(DevReport *r, int rule, int64_t idx) {
+    atomicAdd(&r->val_count[rule], 1ull);
+    atomicMin(&r->val_first[rule], (unsigned long long)idx);
+}
+__device__ __forceinline__ void latch(DevReport *r, int code) { atomicOr(&r->latched, 1u << code); }
+
+// last index in [lo, hi) with a[idx] <= t, or lo - 1
+__device__ __forceinline__ int64_t last_le(const int64_t *__restrict__ a, int64_t lo, int64_t hi, int64_t t) {
+    int64_t l = lo, h = hi;
+    while (l < h) {
+        int64_t m = (l + h) >> 1;
+        if (__ldg(a + m) <= t) l = m + 1; else h = m;
+    }
+    return l - 1;
+}
+
+// warp inclusive scan (sum) of int64
+__device__ __forceinline__ int64_t warp_incl_sum(int64_t v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(CH_FULL, v, o);
+        if (lane_id() >= o) v += y;
+    }
+    return v;
+}
+// block exclusive scan (sum) of int64 for blockDim.x <= 1024; returns total via *total
+template <int NT>
+__device__ __forceinline__ int64_t block_excl_sum(int64_t v, int64_t *total, int64_t *smem /*[32]*/) {
+    int w = threadIdx.x >> 5, l = lane_id();
+    int64_t inc = warp_incl_sum(v);
+    if (l == 31) smem[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        int64_t x = (l < NT / 32) ? smem[l] : 0;
+        int64_t xi = warp_incl_sum(x);
+        if (l < NT / 32) smem[l] = xi - x;
+        if (l == NT / 32 - 1) smem[32] = xi;
+    }
+    __syncthreads();
+    int64_t r = smem[w] + inc - v;
+    if (total) *total = smem[32];
+    __syncthreads();
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// cross-file host entry points
+// ---------------------------------------------------------------------------
+// prims.cu
+chopper_status ch_scan_excl_i64(chopper_ctx *ctx, const int64_t *in, int64_t *out, int64_t n, int64_t *total_dev);
+chopper_status ch_seg_scan_i64(chopper_ctx *ctx, const int64_t *in, const uint8_t *head, int64_t *out, int64_t n,
+                               int op /*0 sum excl, 1 max incl, 2 sum incl*/);
+chopper_status ch_radix_sort(chopper_ctx *ctx, unsigned long long *keys, uint32_t *vals, unsigned long long *keys_alt,
+                             uint32_t *vals_alt, int64_t n, int bit_lo, int bit_hi, bool *result_in_alt);
+chopper_status ch_radix_partition_meta(chopper_ctx *ctx, const uint32_t *meta, const int32_t *gpu_lg, int NG,
+                                       int other_group, uint32_t *vals_out, int64_t n);
+// load.cu
+chopper_status ch_load(chopper_ctx *ctx);
+// spans.cu
+chopper_status ch_build_spans(chopper_ctx *ctx);
+chopper_status ch_attr_pass(chopper_ctx *ctx, int32_t *span_idx);
+// events.cu
+chopper_status ch_overlap_prep(chopper_ctx *ctx);
+chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int64_t *call, int64_t *phi, int64_t *psi);
+// align.cu
+chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, int32_t n_passes, int32_t n_counters,
+                        double *counters_out);
+chopper_status ch_offsets(chopper_ctx *ctx);
+// tables.cu
+chopper_status ch_tables(chopper_ctx *ctx);
+// compose.cu
+chopper_status ch_breakdown_local(chopper_ctx *ctx);
+chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
+chopper_status ch_nccl_allgather(chopper_ctx *ctx, const void *send, void *recv, size_t bytes_per_rank);
+
+// lookup of an event's innermost span per level (spans.cu; used by events.cu)
+struct SpanView {
+    const int64_t *P_start, *P_end;
+    const int32_t *P_parent;
+    const int64_t *list_beg;     // [n_lg*4 + 1]
+    const int32_t *list_flags;   // non-laminar lists
+    const int32_t *attr_pre;     // [4][N] for non-laminar lists
+    int64_t N;
+};
+
+// innermost span (push-order global index) containing t in list (lg, lv), -1 none, -2 ambiguous
+__device__ __forceinline__ int64_t span_lookup(const SpanView &v, int lg, int lv, int64_t t, int64_t i, int64_t *cursor) {
+    int list = lg * 4 + lv;
+    if (v.list_flags[list]) {
+        int32_t a = v.attr_pre[(int64_t)lv * v.N + i];
+        return a;   // already a push-order global index, -1 or -2
+    }
+    int64_t lb = v.list_beg[list], le = v.list_beg[list + 1];
+    if (le <= lb) return -1;
+    int64_t c = *cursor;
+    // seeded search: walk forward a few steps from the previous answer, else binary search
+    if (c >= lb - 1 && c < le && (c < lb || __ldg(v.P_start + c) <= t)) {
+        int steps = 0;
+        while (c + 1 < le && __ldg(v.P_start + c + 1) <= t && steps < 8) { c++; steps++; }
+        if (c + 1 < le && __ldg(v.P_start + c + 1) <= t) c = last_le(v.P_start, c + 1, le, t);
+    } else {
+        c = last_le(v.P_start, lb, le, t);
+    }
+    *cursor = c;
+    while (c >= lb && __ldg(v.P_end + c) <= t) c = __ldg(v.P_parent + c);
+    return c >= lb ? c : -1;
+}

@@ -1,0 +1,584 @@
+// compose.cu -- a10 gap decomposition and a11 cross-rank reduce
+// (chopper_breakdown part 2, chopper_reduce_ranks).
+//
+// Per-gpu rows are laid into a fixed-shape dense exchange block (iteration rows
+// [max_iters], points [max_iters][n_labels]) so that the cross-rank exchange is
+// exactly one ncclAllGather (#2) and every rank composes the global result in
+// the same order, re-indexed by gpu id (identical for any rank count).
+//
+// a10 (Eqs. 4-8; readings D14-D20): one block per gemm / fa
+// op label.  Medians by block bitonic sort; the least-squares fallback and the
+// final factors are evaluated by one thread in (gpu, iteration) order with the
+// same operation order as DESIGN.md O13 (compiled with -fmad=false).
+// a11: T(it) = max over gpus of (busy + launch),
+// throughput = b*s*R / T, median over sampled iterations.
+#include "common.cuh"
+
+namespace {
+// exchange block layout (int64 words; doubles bit-cast)
+constexpr int HDR = 4;          // gpu, present, has_samples, C
+constexpr int IT_W = 8;         // valid, step, busy, prep, call, n, first_ks, last_ke
+constexpr int PT_W = 9;         // valid, busy, launch, ovl, phi, cg, fp, un, ud
+
+struct Layout {
+    int64_t MI, L, C, W;
+    __host__ __device__ int64_t it_off() const { return HDR + C; }
+    __host__ __device__ int64_t pt_off() const { return HDR + C + IT_W * MI; }
+};
+
+__device__ __forceinline__ int64_t dbits(double d) { return __double_as_longlong(d); }
+__device__ __forceinline__ double bitsd(int64_t v) { return __longlong_as_double(v); }
+
+__global__ void k_dense_header(int64_t *blk, Layout Ly, int n_lg, const int32_t *__restrict__ lg_gpu,
+                               const int32_t *__restrict__ has_smp, const int32_t *__restrict__ present) {
+    int l = blockIdx.x;
+    if (l >= n_lg) return;
+    int64_t *b = blk + (int64_t)l * Ly.W;
+    if (threadIdx.x == 0) {
+        b[0] = lg_gpu[l];
+        b[1] = 1;
+        b[2] = has_smp[l];
+        b[3] = Ly.C;
+    }
+    for (int s = threadIdx.x; s < Ly.C; s += blockDim.x) b[HDR + s] = present[(int64_t)l * Ly.C + s];
+}
+
+__global__ void k_dense_iters(int64_t *blk, Layout Ly, int64_t n, const int32_t *__restrict__ gpu,
+                              const int32_t *__restrict__ rank, const int32_t *__restrict__ step,
+                              const int64_t *__restrict__ f, int64_t cap, const int32_t *__restrict__ gpu_lg,
+                              unsigned int *ovf) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int64_t r = rank[j];
+    if (r < 0 || r >= Ly.MI) { atomicOr(ovf, 1u); return; }
+    int64_t *b = blk + (int64_t)gpu_lg[gpu[j]] * Ly.W + Ly.it_off() + r * IT_W;
+    b[0] = 1;
+    b[1] = step[j];
+    b[2] = f[(int64_t)RF_BUSY * cap + j];
+    b[3] = f[(int64_t)RF_PREP * cap + j];
+    b[4] = f[(int64_t)RF_CALL * cap + j];
+    b[5] = f[(int64_t)RF_N * cap + j];
+    b[6] = f[(int64_t)RF_FIRST_KS * cap + j];
+    b[7] = f[(int64_t)RF_LAST_KE * cap + j];
+}
+
+__global__ void k_dense_points(int64_t *blk, Layout Ly, int64_t n, const int32_t *__restrict__ gpu,
+                               const int32_t *__restrict__ rank, const int32_t *__restrict__ label,
+                               const int64_t *__restrict__ f, const double *__restrict__ cnt, int64_t cap,
+                               const int32_t *__restrict__ gpu_lg, int s_cyc, int s_fl, int s_un, int s_ud,
+                               unsigned int *ovf) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int64_t r = rank[j];
+    int lab = label[j];
+    if (r < 0 || r >= Ly.MI || lab < 0 || lab >= Ly.L) { atomicOr(ovf, 1u); return; }
+    int64_t *b = blk + (int64_t)gpu_lg[gpu[j]] * Ly.W + Ly.pt_off() + (r * Ly.L + lab) * PT_W;
+    b[0] = 1;
+    b[1] = f[(int64_t)RF_BUSY * cap + j];
+    b[2] = f[(int64_t)RF_PREP * cap + j] + f[(int64_t)RF_CALL * cap + j];
+    b[3] = f[(int64_t)RF_OVL * cap + j];
+    b[4] = f[(int64_t)RF_PHI * cap + j];
+    b[5] = dbits(s_cyc >= 0 ? cnt[(int64_t)s_cyc * cap + j] : 0.0);
+    b[6] = dbits(s_fl >= 0 ? cnt[(int64_t)s_fl * cap + j] : 0.0);
+    b[7] = dbits(s_un >= 0 ? cnt[(int64_t)s_un * cap + j] : 0.0);
+    b[8] = dbits(s_ud >= 0 ? cnt[(int64_t)s_ud * cap + j] : 0.0);
+}
+
+// ---- block-level helpers ----
+template <class T>
+__device__ void block_bitonic(T *a, int n2) {
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                int x = i ^ j;
+                if (x > i) {
+                    bool up = (i & k) == 0;
+                    T p = a[i], q = a[x];
+                    if ((p > q) == up) { a[i] = q; a[x] = p; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+__device__ __forceinline__ int pow2ceil(int n) {
+    int p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+// median of a[0..n) (sorted in place); even count = mean of the two central values (D21)
+__device__ double med_i64(int64_t *a, int n) {
+    int n2 = pow2ceil(n);
+    for (int i = n + threadIdx.x; i < n2; i += blockDim.x) a[i] = INT64_MAX;
+    __syncthreads();
+    block_bitonic<int64_t>(a, n2);
+    double m = (n % 2) ? (double)a[n / 2] : 0.5 * ((double)a[n / 2 - 1] + (double)a[n / 2]);
+    __syncthreads();
+    return m;
+}
+__device__ double med_f64(double *a, int n) {
+    int n2 = pow2ceil(n);
+    for (int i = n + threadIdx.x; i < n2; i += blockDim.x) a[i] = INFINITY;
+    __syncthreads();
+    block_bitonic<double>(a, n2);
+    double m = (n % 2) ? a[n / 2] : 0.5 * (a[n / 2 - 1] + a[n / 2]);
+    __syncthreads();
+    return m;
+}
+
+enum { BD_FIT = 1, BD_NO_FLOPS = 2, BD_NO_UTIL = 4, BD_UTIL_RANGE = 8, BD_D0_ZERO = 16, BD_NO_CYCLES = 32,
+       BD_NO_SAMPLES = 64, BD_INSUFFICIENT = 128 };
+
+struct BdArgs {
+    const int64_t *blk;
+    int nslots;
+    Layout Ly;
+    const int32_t *slot_order;   // slots sorted by gpu id, -1 terminated
+    const int32_t *labels;       // gemm / fa labels, one per block
+    const double *f_gemm;
+    double tpt, freq;
+    int warmup;
+    int s_cyc, s_fl, s_un, s_ud;
+    int64_t maxp2;               // scratch capacity per array (pow2)
+    int64_t *wi;                 // [nblocks][5][maxp2] int64 scratch
+    double *wd;                  // [nblocks][5][maxp2] double scratch
+    double *out;                 // [nblocks][16]
+};
+
+__global__ void __launch_bounds__(256) k_breakdown(BdArgs A) {
+    __shared__ int s_n;
+    __shared__ int s_flags_in;   // bit0 cyc, bit1 fl, bit2 util, bit3 smp
+    const int L = A.labels[blockIdx.x];
+    double *out = A.out + (int64_t)blockIdx.x * 16;
+    int64_t *busy = A.wi + (int64_t)blockIdx.x * 5 * A.maxp2;
+    int64_t *launch = busy + A.maxp2, *ovl = busy + 2 * A.maxp2, *phi = busy + 3 * A.maxp2, *ti = busy + 4 * A.maxp2;
+    double *cg = A.wd + (int64_t)blockIdx.x * 5 * A.maxp2;
+    double *fp = cg + A.maxp2, *un = cg + 2 * A.maxp2, *ud = cg + 3 * A.maxp2, *td = cg + 4 * A.maxp2;
+    const Layout Ly = A.Ly;
+    if (threadIdx.x == 0) {
+        // gather sampled points of L in (gpu, iteration) order; slot presence over contributing gpus
+        int n = 0;
+        int cyc = A.s_cyc >= 0, fl = A.s_fl >= 0, ut = A.s_un >= 0 && A.s_ud >= 0, sm = 1;
+        for (int q = 0; q < A.nslots; q++) {
+            int sl = A.slot_order[q];
+            if (sl < 0) break;
+            const int64_t *b = A.blk + (int64_t)sl * Ly.W;
+            if (b[1] == 0) continue;
+            for (int64_t r = A.warmup > 0 ? A.warmup : 0; r < Ly.MI; r++) {
+                const int64_t *p = b + Ly.pt_off() + (r * Ly.L + L) * PT_W;
+                if (p[0] == 0 || p[1] <= 0) continue;
+                if (n >= A.maxp2) continue;
+                busy[n] = p[1]; launch[n] = p[2]; ovl[n] = p[3]; phi[n] = p[4];
+                cg[n] = bitsd(p[5]); fp[n] = bitsd(p[6]); un[n] = bitsd(p[7]); ud[n] = bitsd(p[8]);
+                if (cyc && !b[HDR + A.s_cyc]) cyc = 0;
+                if (fl && !b[HDR + A.s_fl]) fl = 0;
+                if (ut && !(b[HDR + A.s_un] && b[HDR + A.s_ud])) ut = 0;
+                if (!b[2]) sm = 0;
+                n++;
+            }
+        }
+        s_n = n;
+        s_flags_in = cyc | (fl << 1) | (ut << 2) | ((sm && n > 0) << 3);
+    }
+    __syncthreads();
+    const int n = s_n;
+    const int fin = s_flags_in;
+    const bool has_cyc = fin & 1, has_fl = fin & 2, has_util = fin & 4, has_smp = fin & 8;
+    if (threadIdx.x < 16) out[threadIdx.x] = NAN;
+    __syncthreads();
+    if (n < 2) {
+        if (threadIdx.x == 0) { out[0] = n; out[1] = 0; out[14] = BD_INSUFFICIENT; out[15] = L; }
+        return;
+    }
+    int flags = 0;
+    // D_act = median busy (D14)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ti[i] = busy[i];
+    __syncthreads();
+    double d_act = med_i64(ti, n);
+    // D0 / D50 buckets (integer tests, D15)
+    __shared__ int s_n0, s_n50;
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int i = 0; i < n; i++) if (20 * ovl[i] <= busy[i]) ti[a++] = busy[i];
+        s_n0 = a;
+    }
+    __syncthreads();
+    int n0 = s_n0;
+    double d0 = 0.0, d50 = 0.0;
+    bool bucket = false;
+    if (n0 > 0) {
+        double m0 = med_i64(ti, n0);
+        if (threadIdx.x == 0) {
+            int a = 0;
+            for (int i = 0; i < n; i++) if (2 * busy[i] <= 5 * ovl[i] && 5 * ovl[i] <= 3 * busy[i]) ti[a++] = busy[i];
+            s_n50 = a;
+        }
+        __syncthreads();
+        int n50 = s_n50;
+        if (n50 > 0) {
+            d0 = m0;
+            d50 = med_i64(ti, n50);
+            bucket = true;
+        }
+    }
+    __shared__ double s_d0, s_d50;
+    if (!bucket) {
+        if (threadIdx.x == 0) {
+            double sr = 0.0, sb = 0.0;
+            for (int i = 0; i < n; i++) { sr += (double)ovl[i] / (double)busy[i]; sb += (double)busy[i]; }
+            double mr = sr / (double)n, mb = sb / (double)n, sxx = 0.0, sxy = 0.0;
+            for (int i = 0; i < n; i++) {
+                double dr = (double)ovl[i] / (double)busy[i] - mr, db = (double)busy[i] - mb;
+                sxx += dr * dr;
+                sxy += dr * db;
+            }
+            if (sxx == 0.0) { s_d0 = d_act; s_d50 = d_act; }
+            else { double c = sxy / sxx, a = mb - c * mr; s_d0 = a; s_d50 = a + c * 0.5; }
+        }
+        __syncthreads();
+        d0 = s_d0;
+        d50 = s_d50;
+        flags |= BD_FIT;
+    }
+    // remaining medians
+    double med_fp = 0.0, med_u = 0.0, med_cg = 0.0, med_bl, med_v = 0.0;
+    if (has_fl) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) td[i] = fp[i];
+        __syncthreads();
+        med_fp = med_f64(td, n);
+    }
+    if (has_util || (has_fl && has_cyc)) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            td[i] = has_util ? un[i] / ud[i] : (fp[i] / cg[i]) * (A.freq / A.tpt);
+        __syncthreads();
+        med_u = med_f64(td, n);
+    }
+    if (has_cyc) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) td[i] = cg[i];
+        __syncthreads();
+        med_cg = med_f64(td, n);
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) ti[i] = busy[i] + launch[i];
+    __syncthreads();
+    med_bl = med_i64(ti, n);
+    if (has_smp) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) td[i] = (double)phi[i] / (double)busy[i] * 1e6;
+        __syncthreads();
+        med_v = med_f64(td, n);
+    }
+    if (threadIdx.x == 0) {
+        out[0] = n;
+        out[1] = bucket ? 0 : 1;
+        out[2] = d_act * 1e-9;
+        out[3] = d0 * 1e-9;
+        out[4] = d50 * 1e-9;
+        double d_thr = A.f_gemm[L] / A.tpt;                                   // Eq. 4
+        out[5] = d_thr;
+        double ovr_inst = 1.0;                                               // Eq. 5
+        if (has_fl) ovr_inst = med_fp / A.f_gemm[L]; else flags |= BD_NO_FLOPS;
+        out[6] = ovr_inst;
+        double ovr_util = 1.0;                                               // Eq. 6
+        if (has_util || (has_fl && has_cyc)) {
+            if (!(med_u > 0.0 && med_u <= 1.0)) flags |= BD_UTIL_RANGE;
+            ovr_util = 1.0 / med_u;
+        } else flags |= BD_NO_UTIL;
+        out[7] = ovr_util;
+        double ovr_ovl = d50 / d0;                                           // Eq. 7
+        if (!(d0 > 0.0)) flags |= BD_D0_ZERO;
+        out[8] = ovr_ovl;
+        if (has_cyc) {                                                       // Eq. 8
+            double d_peak = med_cg / A.freq;
+            out[9] = d_peak;
+            out[10] = (d_act * 1e-9 / d_peak) / ovr_ovl;
+        } else flags |= BD_NO_CYCLES;
+        out[11] = med_bl / d_act;                                            // launch term (D20)
+        out[12] = d_act * 1e-9 / (d_thr * ovr_inst * ovr_util * ovr_ovl * out[10]);
+        if (has_smp) out[13] = A.freq / med_v; else flags |= BD_NO_SAMPLES;
+        out[14] = flags;
+        out[15] = L;
+    }
+}
+
+// global iteration rows (a11): one thread per iteration rank of the reference gpu
+struct GlobArgs {
+    const int64_t *blk;
+    int nslots;
+    Layout Ly;
+    const int32_t *slot_order;
+    const int64_t *delta;
+    int64_t tokens;              // b*s*R
+    int warmup;
+    int32_t *step, *complete, *sampled;
+    int64_t *T, *af, *al;
+    double *tp;
+    int64_t *n_out;
+    double *med;
+    double *work;                // [pow2(MI)]
+};
+
+__global__ void __launch_bounds__(256) k_global(GlobArgs A) {
+    const Layout Ly = A.Ly;
+    __shared__ int s_ref;
+    __shared__ int s_nst;
+    if (threadIdx.x == 0) {
+        s_ref = A.slot_order[0];
+        s_nst = 0;
+    }
+    __syncthreads();
+    const int ref = s_ref;
+    if (ref < 0) { if (threadIdx.x == 0) { *A.n_out = 0; *A.med = NAN; } return; }
+    const int64_t *rb = A.blk + (int64_t)ref * Ly.W;
+    // reference rows are the valid ranks of the reference gpu in rank order; output index = count before
+    for (int64_t r = threadIdx.x; r < Ly.MI; r += blockDim.x) {
+        const int64_t *row = rb + Ly.it_off() + r * IT_W;
+        if (!row[0]) continue;
+        int64_t w = 0;
+        for (int64_t q = 0; q < r; q++) w += rb[Ly.it_off() + q * IT_W] != 0;
+        int64_t step = row[1];
+        bool complete = true, samp = true;
+        int64_t T = INT64_MIN, lo = INT64_MAX, hi = INT64_MIN;
+        for (int q = 0; q < A.nslots; q++) {
+            int sl = A.slot_order[q];
+            if (sl < 0) break;
+            const int64_t *b = A.blk + (int64_t)sl * Ly.W;
+            if (!b[1]) continue;
+            int g = (int)b[0];
+            int64_t f = -1;
+            // first iteration (rank order) of gpu g with the same step label (D5)
+            for (int64_t x = 0; x < Ly.MI; x++)
+                if (b[Ly.it_off() + x * IT_W] && b[Ly.it_off() + x * IT_W + 1] == step) { f = x; break; }
+            if (f < 0) { complete = false; continue; }
+            const int64_t *x = b + Ly.it_off() + f * IT_W;
+            if (f < A.warmup) samp = false;
+            int64_t t = x[2] + x[3] + x[4];
+            if (t > T) T = t;
+            if (x[5] > 0) {
+                int64_t a = x[6] - A.delta[g], c = x[7] - A.delta[g];
+                if (a < lo) lo = a;
+                if (c > hi) hi = c;
+            }
+        }
+        A.step[w] = (int32_t)step;
+        A.complete[w] = complete;
+        A.sampled[w] = complete && samp;
+        A.T[w] = complete ? T : 0;
+        A.af[w] = lo;
+        A.al[w] = hi;
+        A.tp[w] = complete ? (double)A.tokens / ((double)T * 1e-9) : NAN;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t nref = 0;
+        int nst = 0;
+        for (int64_t r = 0; r < Ly.MI; r++) if (rb[Ly.it_off() + r * IT_W]) nref++;
+        for (int64_t w = 0; w < nref; w++) if (A.sampled[w]) A.work[nst++] = A.tp[w];
+        *A.n_out = nref;
+        s_nst = nst;
+    }
+    __syncthreads();
+    int nst = s_nst;
+    double m = NAN;
+    if (nst > 0) m = med_f64(A.work, nst);
+    if (threadIdx.x == 0) *A.med = m;
+}
+}  // namespace
+
+static Layout layout_of(chopper_ctx *ctx) {
+    Layout Ly;
+    Ly.MI = std::max(1, ctx->cfg.max_iters);
+    Ly.L = std::max(1, ctx->cfg.n_labels);
+    Ly.C = ctx->C;
+    Ly.W = HDR + Ly.C + IT_W * Ly.MI + PT_W * Ly.MI * Ly.L;
+    return Ly;
+}
+
+// dense local exchange blocks [slots][W]
+static chopper_status densify(chopper_ctx *ctx, int64_t **blk_out, int *slots_out) {
+    const Layout Ly = layout_of(ctx);
+    const int slots = (int)ceil_div(ctx->cfg.n_traced_gpus, ctx->nranks);
+    if (ctx->n_lg > slots) return ch_fail(ctx, CHOPPER_E_RANGE, "more local gpus than ceil(n_traced_gpus / nranks)");
+    CH_ALLOC_BEGIN;
+    int64_t *blk = CH_ALLOC(ctx, int64_t, (int64_t)slots * Ly.W);
+    int32_t *lgg = CH_ALLOC(ctx, int32_t, ctx->n_lg + 1);
+    int32_t *pres = CH_ALLOC(ctx, int32_t, (int64_t)std::max(ctx->n_lg, 1) * std::max(ctx->C, 1));
+    unsigned int *ovf = CH_ALLOC(ctx, unsigned int, 1);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemsetAsync(blk, 0, 8 * (size_t)slots * Ly.W, ctx->st));
+    CH_CUDA(ctx, cudaMemsetAsync(ovf, 0, 4, ctx->st));
+    std::vector<int32_t> h(ctx->lg_gpu, ctx->lg_gpu + ctx->n_lg);
+    std::vector<int32_t> hp((size_t)std::max(ctx->n_lg, 1) * std::max(ctx->C, 1), 0);
+    for (size_t q = 0; q < ctx->present.size() && q < hp.size(); q++) hp[q] = ctx->present[q];
+    if (ctx->n_lg) CH_CUDA(ctx, cudaMemcpyAsync(lgg, h.data(), 4 * ctx->n_lg, cudaMemcpyHostToDevice, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(pres, hp.data(), 4 * hp.size(), cudaMemcpyHostToDevice, ctx->st));
+    if (ctx->n_lg > 0) {
+        k_dense_header<<<ctx->n_lg, 64, 0, ctx->st>>>(blk, Ly, ctx->n_lg, lgg, ctx->d_has_smp, pres);
+        CH_LAUNCHED(ctx);
+    }
+    if (ctx->iter.n > 0) {
+        k_dense_iters<<<(unsigned)ceil_div(ctx->iter.n, 256), 256, 0, ctx->st>>>(
+            blk, Ly, ctx->iter.n, ctx->iter.gpu, ctx->iter.rank, ctx->iter_step, ctx->iter.f, ctx->iter.cap,
+            ctx->d_gpu_lg, ovf);
+        CH_LAUNCHED(ctx);
+    }
+    if (ctx->point.n > 0) {
+        const chopper_bd_params &p = ctx->bd;
+        k_dense_points<<<(unsigned)ceil_div(ctx->point.n, 256), 256, 0, ctx->st>>>(
+            blk, Ly, ctx->point.n, ctx->point.gpu, ctx->point.rank, ctx->point.label, ctx->point.f, ctx->point.cnt,
+            ctx->point.cap, ctx->d_gpu_lg, p.slot_gpu_cycles, p.slot_perf_flops, p.slot_util_num, p.slot_util_den,
+            ovf);
+        CH_LAUNCHED(ctx);
+    }
+    unsigned int hovf = 0;
+    CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "iteration rank >= max_iters or op label >= n_labels");
+    *blk_out = blk;
+    *slots_out = slots;
+    return CHOPPER_OK;
+}
+
+static chopper_status run_breakdown(chopper_ctx *ctx, const int64_t *blk, int nslots, const int32_t *slot_order,
+                                    double **out_dev, int64_t *n_out) {
+    const Layout Ly = layout_of(ctx);
+    std::vector<int32_t> labs;
+    for (int L = 0; L < (int)ctx->op_type.size(); L++)
+        if (ctx->op_type[L] == 1 || ctx->op_type[L] == 2) labs.push_back(L);
+    int nb = (int)labs.size();
+    *n_out = nb;
+    CH_ALLOC_BEGIN;
+    double *out = CH_ALLOC(ctx, double, (int64_t)std::max(nb, 1) * 16);
+    int32_t *dl = CH_ALLOC(ctx, int32_t, std::max(nb, 1));
+    int64_t maxp = (int64_t)Ly.MI * ctx->cfg.n_traced_gpus;
+    int64_t maxp2 = 1;
+    while (maxp2 < maxp) maxp2 <<= 1;
+    int64_t *wi = CH_ALLOC(ctx, int64_t, (int64_t)std::max(nb, 1) * 5 * maxp2);
+    double *wd = CH_ALLOC(ctx, double, (int64_t)std::max(nb, 1) * 5 * maxp2);
+    CH_ALLOC_END(ctx);
+    *out_dev = out;
+    if (nb == 0) return CHOPPER_OK;
+    CH_CUDA(ctx, cudaMemcpyAsync(dl, labs.data(), 4 * nb, cudaMemcpyHostToDevice, ctx->st));
+    BdArgs A;
+    A.blk = blk;
+    A.nslots = nslots;
+    A.Ly = Ly;
+    A.slot_order = slot_order;
+    A.labels = dl;
+    A.f_gemm = ctx->d_f_gemm;
+    A.tpt = ctx->bd.tpt_peak;
+    A.freq = ctx->bd.freq_peak_hz;
+    A.warmup = ctx->bd.warmup;
+    A.s_cyc = ctx->bd.slot_gpu_cycles;
+    A.s_fl = ctx->bd.slot_perf_flops;
+    A.s_un = ctx->bd.slot_util_num;
+    A.s_ud = ctx->bd.slot_util_den;
+    A.maxp2 = maxp2;
+    A.wi = wi;
+    A.wd = wd;
+    A.out = out;
+    k_breakdown<<<nb, 256, 0, ctx->st>>>(A);
+    CH_LAUNCHED(ctx);
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    return CHOPPER_OK;
+}
+
+// slot order by gpu id (host, from the exchange headers)
+static chopper_status slot_order(chopper_ctx *ctx, const int64_t *blk, int nslots, int64_t W, int32_t **out) {
+    std::vector<int64_t> hdr(2);
+    std::vector<std::pair<int64_t, int>> v;
+    for (int b = 0; b < nslots; b++) {
+        CH_CUDA(ctx, cudaMemcpyAsync(hdr.data(), blk + (int64_t)b * W, 16, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        if (hdr[1]) v.push_back({hdr[0], b});
+    }
+    std::sort(v.begin(), v.end());
+    std::vector<int32_t> o(nslots + 1, -1);
+    for (size_t q = 0; q < v.size(); q++) o[q] = v[q].second;
+    CH_ALLOC_BEGIN;
+    int32_t *d = CH_ALLOC(ctx, int32_t, nslots + 1);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemcpyAsync(d, o.data(), 4 * (nslots + 1), cudaMemcpyHostToDevice, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    *out = d;
+    return CHOPPER_OK;
+}
+
+chopper_status ch_breakdown_local(chopper_ctx *ctx) {
+    int64_t *blk;
+    int slots;
+    CH_TRY(densify(ctx, &blk, &slots));
+    ctx->d_dense = blk;
+    ctx->dense_slots = slots;
+    int32_t *ord;
+    CH_TRY(slot_order(ctx, blk, slots, layout_of(ctx).W, &ord));
+    CH_TRY(run_breakdown(ctx, blk, slots, ord, &ctx->d_bd, &ctx->n_bd));
+    return CHOPPER_OK;
+}
+
+chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
+    const Layout Ly = layout_of(ctx);
+    const int slots = ctx->dense_slots;
+    const int nslots = slots * ctx->nranks;
+    CH_ALLOC_BEGIN;
+    int64_t *all = CH_ALLOC(ctx, int64_t, (int64_t)nslots * Ly.W);
+    CH_ALLOC_END(ctx);
+    if (ctx->nranks > 1) {
+        CH_TRY(ch_nccl_allgather(ctx, ctx->d_dense, all, sizeof(int64_t) * (size_t)slots * Ly.W));
+    } else {
+        CH_CUDA(ctx, cudaMemcpyAsync(all, ctx->d_dense, 8 * (size_t)slots * Ly.W, cudaMemcpyDeviceToDevice, ctx->st));
+    }
+    int32_t *ord;
+    CH_TRY(slot_order(ctx, all, nslots, Ly.W, &ord));
+    // global iterations + throughput
+    int64_t MI = Ly.MI;
+    int64_t mi2 = 1;
+    while (mi2 < MI) mi2 <<= 1;
+    int32_t *step = CH_ALLOC(ctx, int32_t, MI), *comp = CH_ALLOC(ctx, int32_t, MI), *samp = CH_ALLOC(ctx, int32_t, MI);
+    int64_t *T = CH_ALLOC(ctx, int64_t, MI), *af = CH_ALLOC(ctx, int64_t, MI), *al = CH_ALLOC(ctx, int64_t, MI);
+    double *tp = CH_ALLOC(ctx, double, MI), *work = CH_ALLOC(ctx, double, mi2), *med = CH_ALLOC(ctx, double, 1);
+    int64_t *nref = CH_ALLOC(ctx, int64_t, 1);
+    int64_t *dd = CH_ALLOC(ctx, int64_t, ctx->cfg.n_traced_gpus);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemcpyAsync(dd, ctx->delta.data(), 8 * ctx->cfg.n_traced_gpus, cudaMemcpyHostToDevice, ctx->st));
+    GlobArgs G;
+    G.blk = all;
+    G.nslots = nslots;
+    G.Ly = Ly;
+    G.slot_order = ord;
+    G.delta = dd;
+    G.tokens = ctx->bd.batch * ctx->bd.seq * ctx->bd.ranks;
+    G.warmup = ctx->bd.warmup;
+    G.step = step; G.complete = comp; G.sampled = samp; G.T = T; G.af = af; G.al = al; G.tp = tp;
+    G.n_out = nref; G.med = med; G.work = work;
+    k_global<<<1, 256, 0, ctx->st>>>(G);
+    CH_LAUNCHED(ctx);
+    double *bd;
+    int64_t nbd;
+    CH_TRY(run_breakdown(ctx, all, nslots, ord, &bd, &nbd));
+    // host copies
+    int64_t n = 0;
+    CH_CUDA(ctx, cudaMemcpyAsync(&n, nref, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    if (n > 4096) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 4096 iterations in chopper_global");
+    out->n_iters = n;
+    if (n > 0) {
+        CH_CUDA(ctx, cudaMemcpyAsync(out->step, step, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(out->complete, comp, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(out->sampled, samp, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(out->T, T, 8 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(out->aligned_first, af, 8 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(out->aligned_last, al, 8 * n, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(out->throughput, tp, 8 * n, cudaMemcpyDeviceToHost, ctx->st));
+    }
+    CH_CUDA(ctx, cudaMemcpyAsync(&out->throughput_median, med, 8, cudaMemcpyDeviceToHost, ctx->st));
+    if (nbd > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 breakdown rows");
+    out->n_bd = nbd;
+    if (nbd > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->bd, bd, 8 * 16 * nbd, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    for (int g = 0; g < ctx->cfg.n_traced_gpus && g < 256; g++) {
+        out->delta[g] = ctx->delta[g];
+        out->delta_flag[g] = ctx->delta_flag[g];
+    }
+    out->max_skew_ag = ctx->max_skew[0];
+    out->max_skew_rs = ctx->max_skew[1];
+    return CHOPPER_OK;
+}

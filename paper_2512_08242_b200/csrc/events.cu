@@ -1,0 +1,637 @@
+// events.cu -- the per-event hot pass (chopper_overlap).
+//
+// One fused, tiled pass over the event columns in dispatch (input) order:
+//   a5  attribution key per event: innermost span per level (spans.cu),
+//   a6  overlap: COMPUTE -> |[t_ks,t_ke) ∩ U_g| with U_g the union of the
+//       gpu's communication intervals (D9), as
+//       cov(t_ke) - cov(t_ks) over prefix lengths of the merged union;
+//       communication -> |[t_ks,t_ke) ∩ V_g| (compute union),
+//   a7  launch overhead Eqs. 1-3 with the chain
+//       predecessor from a2 and dispatch clamped to start (D6),
+//   a8  frequency / power integrals over a zero-order hold (D10) as
+//       differences of prefix integrals,
+//   a9  (time part) reduction of each maximal run of equal instance key into
+//       a sub-run row: thread-sequential folding, in-tile completion through
+//       shared memory, sub-run ids from a decoupled look-back chained scan.
+// Each 2048-event tile is cut at its boundary so sub-runs never cross tiles;
+// sub-runs with equal keys are merged into instances in tables.cu.
+#include "common.cuh"
+
+SpanView ch_span_view(chopper_ctx *ctx);
+
+namespace {
+constexpr int NT = 256;
+constexpr int EV_NT = 256, EV_IPT = 8, EV_TILE = EV_NT * EV_IPT;
+constexpr int NACC = RF_NFIELDS;
+constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
+
+// ---- comm / compute unions: one block per local gpu ----------------------------------------------
+// positions pos[lo..hi) index events sorted by t_ks; output merged intervals at out[lo + m].
+__global__ void __launch_bounds__(1024) k_union_block(const uint32_t *__restrict__ pos, const int64_t *__restrict__ seg_lo,
+                                                      const int64_t *__restrict__ seg_hi, const int64_t *__restrict__ ks,
+                                                      const int64_t *__restrict__ ke, int64_t *__restrict__ Us,
+                                                      int64_t *__restrict__ Ue, int64_t *__restrict__ UP,
+                                                      int64_t *__restrict__ Ubeg, int64_t *__restrict__ Ucnt) {
+    __shared__ int64_t sm[33];
+    __shared__ int64_t smax[32];
+    __shared__ int64_t s_carry_max;
+    __shared__ int64_t s_m;
+    __shared__ unsigned char shead[1024 + 1];
+    int lg = blockIdx.x;
+    int64_t lo = seg_lo[lg], hi = seg_hi[lg];
+    int tid = threadIdx.x, w = tid >> 5, l = lane_id();
+    if (tid == 0) { s_carry_max = INT64_MIN; s_m = 0; }
+    __syncthreads();
+    for (int64_t base = lo; base < hi; base += 1024) {
+        int64_t j = base + tid;
+        bool valid = j < hi;
+        int64_t s = 0, e = INT64_MIN;
+        if (valid) { uint32_t i = pos[j]; s = ks[i]; e = ke[i]; }
+        // inclusive prefix max of e across the block
+        int64_t v = e;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(CH_FULL, v, o);
+            if (l >= o && y > v) v = y;
+        }
+        if (l == 31) smax[w] = v;
+        __syncthreads();
+        if (w == 0) {
+            int64_t x = smax[l];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int64_t y = __shfl_up_sync(CH_FULL, x, o);
+                if (l >= o && y > x) x = y;
+            }
+            smax[l] = x;   // inclusive over warps
+        }
+        __syncthreads();
+        int64_t carry = s_carry_max;
+        int64_t wpre = w > 0 ? smax[w - 1] : INT64_MIN;
+        int64_t Mi = v;
+        if (wpre > Mi) Mi = wpre;
+        if (carry > Mi) Mi = carry;
+        // exclusive (previous element's inclusive max)
+        int64_t Mprev = __shfl_up_sync(CH_FULL, Mi, 1);
+        if (l == 0) {
+            Mprev = wpre > carry ? wpre : carry;
+            if (w > 0) {
+                // previous warp's last inclusive = max(carry, smax[w-1])
+            }
+        }
+        bool head = valid && (s > Mprev);   // Mprev = INT64_MIN for the very first element
+        shead[tid] = head;
+        int64_t tot;
+        int64_t ex = block_excl_sum<1024>(head ? 1 : 0, &tot, sm);
+        int64_t m0 = s_m;
+        if (head) Us[lo + m0 + ex] = s;
+        // last element of its run: next element is a head, or end of segment
+        bool nexthead;
+        if (tid < 1023) nexthead = (j + 1 < hi) ? (bool)shead[tid + 1] : true;
+        else {
+            if (j + 1 < hi) { uint32_t i2 = pos[j + 1]; nexthead = ks[i2] > Mi; }
+            else nexthead = true;
+        }
+        if (valid && nexthead) Ue[lo + m0 + ex + (head ? 0 : -1)] = Mi;
+        __syncthreads();
+        if (tid == 1023) s_carry_max = Mi;
+        if (tid == 0) s_m = m0 + tot;
+        __syncthreads();
+    }
+    int64_t mcount = s_m;
+    // prefix lengths
+    int64_t run = 0;
+    for (int64_t base = 0; base < mcount; base += 1024) {
+        int64_t m = base + tid;
+        int64_t len = m < mcount ? Ue[lo + m] - Us[lo + m] : 0;
+        int64_t tot;
+        int64_t ex = block_excl_sum<1024>(len, &tot, sm);
+        if (m < mcount) UP[lo + m] = run + ex;
+        run += tot;
+    }
+    if (tid == 0) { Ubeg[lg] = lo; Ucnt[lg] = mcount; }
+}
+
+// sample prefix inputs: f_k * (tau_{k+1} - tau_k) within a gpu, 0 at a gpu's last sample
+__global__ void k_smp_terms(const int32_t *__restrict__ g, const int64_t *__restrict__ ts,
+                            const int32_t *__restrict__ f, const int32_t *__restrict__ p, int64_t n,
+                            int64_t *__restrict__ tf, int64_t *__restrict__ tp, uint8_t *__restrict__ head) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    bool last = (k == n - 1) || g[k + 1] != g[k];
+    int64_t dt = last ? 0 : ts[k + 1] - ts[k];
+    tf[k] = (int64_t)f[k] * dt;
+    tp[k] = (int64_t)p[k] * dt;
+    head[k] = (k == 0) || g[k - 1] != g[k];
+}
+
+// ---- compute-union keys for multi-stream gpus -----------------------------------------------------
+__global__ void k_vkeys(const uint32_t *__restrict__ meta, const int64_t *__restrict__ ks, int64_t n,
+                        const int32_t *__restrict__ gpu_lg, int64_t t0, int tsbits, int lgbits,
+                        unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t m = meta[i];
+    unsigned long long k;
+    if (kind_of(m) == CK_COMPUTE)
+        k = ((unsigned long long)gpu_lg[gpu_of(m)] << tsbits) | (unsigned long long)(ks[i] - t0);
+    else
+        k = ((1ull << lgbits) - 1) << tsbits;    // sorts after every gpu
+    keys[i] = k;
+    vals[i] = (uint32_t)i;
+}
+
+// ---- fused event pass ---------------------------------------------------------------------------
+struct EvParams {
+    const int64_t *tl, *ks, *ke;
+    const uint32_t *meta;
+    int64_t N;
+    const int32_t *gpu_lg;
+    SpanView sv;
+    int sh_op, sh_ly, sh_ph, sh_it, sh_lg;
+    const int64_t *pred_end;
+    const int64_t *Us, *Ue, *UP, *Ubeg, *Ucnt;
+    int v_general;
+    const int64_t *Vs, *Ve, *VP, *Vbeg, *Vcnt;
+    const uint32_t *perm;
+    const int64_t *bucket_beg;
+    int NG;
+    const int64_t *smp_ts;
+    const int32_t *smp_f, *smp_p;
+    const int64_t *phi_pre, *psi_pre, *smp_lo, *smp_hi;
+    int64_t *o_ovl, *o_prep, *o_call, *o_phi, *o_psi;
+    int32_t *o_run;
+    unsigned long long *sr_key;
+    int64_t *sr_first;
+    int64_t *sr_f;
+    int64_t cap;
+    unsigned long long *tile_state;
+    unsigned int *ticket;
+};
+
+__device__ __forceinline__ unsigned long long event_key(const EvParams &P, int64_t i, int lg, int64_t t, int64_t *cur) {
+    int64_t r[4];
+    bool ok = true;
+#pragma unroll
+    for (int lv = 0; lv < 4; lv++) {
+        int64_t c = span_lookup(P.sv, lg, lv, t, i, &cur[lv]);
+        if (c == -2) ok = false;
+        r[lv] = c >= 0 ? c - P.sv.list_beg[lg * 4 + lv] + 1 : 0;
+    }
+    if (!ok || r[0] == 0) return CH_INVALID_KEY;
+    return ((unsigned long long)lg << P.sh_lg) | ((unsigned long long)r[0] << P.sh_it) |
+           ((unsigned long long)r[1] << P.sh_ph) | ((unsigned long long)r[2] << P.sh_ly) | (unsigned long long)r[3];
+}
+
+// last index in [lo, hi) with a[idx] <= t, seeded by the previous answer (t mostly non-decreasing)
+__device__ __forceinline__ int64_t seek(const int64_t *__restrict__ a, int64_t lo, int64_t hi, int64_t t, int64_t *cur) {
+    int64_t c = *cur;
+    if (c >= lo - 1 && c < hi && (c < lo || __ldg(a + c) <= t)) {
+        int steps = 0;
+        while (c + 1 < hi && __ldg(a + c + 1) <= t && steps < 4) { c++; steps++; }
+        if (c + 1 < hi && __ldg(a + c + 1) <= t) c = last_le(a, c + 1, hi, t);
+    } else {
+        c = last_le(a, lo, hi, t);
+    }
+    *cur = c;
+    return c;
+}
+
+// coverage of (-inf, t) by a merged union with prefix lengths
+__device__ __forceinline__ int64_t cov(const int64_t *Us, const int64_t *Ue, const int64_t *UP, int64_t lo, int64_t hi,
+                                       int64_t t, int64_t *cur) {
+    if (hi <= lo) return 0;
+    int64_t u = seek(Us, lo, hi, t, cur);
+    if (u < lo) return 0;
+    int64_t s = __ldg(Us + u), e = __ldg(Ue + u);
+    int64_t x = t - s;
+    if (x > e - s) x = e - s;
+    return __ldg(UP + u) + x;
+}
+
+// |[a, b) ∩ compute intervals| for the single-stream fast path: intervals sorted and disjoint
+__device__ int64_t covl_fast(const EvParams &P, int lg, int64_t a, int64_t b) {
+    int64_t lo = P.bucket_beg[lg * P.NG + 1], hi = P.bucket_beg[lg * P.NG + 2];
+    // first compute interval with end > a (ends are sorted for disjoint sorted intervals)
+    int64_t l = lo, h = hi;
+    while (l < h) {
+        int64_t m = (l + h) >> 1;
+        if (__ldg(P.ke + P.perm[m]) > a) h = m; else l = m + 1;
+    }
+    int64_t tot = 0;
+    for (int64_t j = l; j < hi; j++) {
+        uint32_t i = P.perm[j];
+        int64_t s = __ldg(P.ks + i);
+        if (s >= b) break;
+        int64_t e = __ldg(P.ke + i);
+        int64_t x = s > a ? s : a, y = e < b ? e : b;
+        if (y > x) tot += y - x;
+    }
+    return tot;
+}
+
+struct Acc {
+    int64_t v[NACC];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int f = 0; f < NACC; f++) v[f] = 0;
+        v[RF_FIRST_IDX] = INT64_MAX;
+        v[RF_FIRST_KS] = INT64_MAX;
+        v[RF_LAST_KE] = INT64_MIN;
+    }
+    __device__ __forceinline__ void add(const Acc &b) {
+#pragma unroll
+        for (int f = 0; f < NACC; f++)
+            if (f != RF_FIRST_IDX && f != RF_FIRST_KS && f != RF_LAST_KE) v[f] += b.v[f];
+        if (b.v[RF_FIRST_KS] < v[RF_FIRST_KS] ||
+            (b.v[RF_FIRST_KS] == v[RF_FIRST_KS] && b.v[RF_FIRST_IDX] < v[RF_FIRST_IDX])) {
+            v[RF_FIRST_KS] = b.v[RF_FIRST_KS];
+            v[RF_FIRST_IDX] = b.v[RF_FIRST_IDX];
+        }
+        if (b.v[RF_LAST_KE] > v[RF_LAST_KE]) v[RF_LAST_KE] = b.v[RF_LAST_KE];
+    }
+    __device__ __forceinline__ void store(int64_t *sm, int t) const {
+#pragma unroll
+        for (int f = 0; f < NACC; f++) sm[f * EV_NT + t] = v[f];
+    }
+    __device__ __forceinline__ void load(const int64_t *sm, int t) {
+#pragma unroll
+        for (int f = 0; f < NACC; f++) v[f] = sm[f * EV_NT + t];
+    }
+};
+
+__device__ __forceinline__ void write_subrun(const EvParams &P, int64_t id, const Acc &a) {
+#pragma unroll
+    for (int f = 0; f < NACC; f++) P.sr_f[(int64_t)f * P.cap + id] = a.v[f];
+}
+
+__global__ void __launch_bounds__(EV_NT) k_events(EvParams P) {
+    extern __shared__ int64_t dsm[];
+    int64_t *fp = dsm;                    // [NACC][EV_NT] first piece per thread
+    int64_t *lp = dsm + NACC * EV_NT;     // [NACC][EV_NT] last piece per thread
+    __shared__ unsigned long long lastkey[EV_NT];
+    __shared__ unsigned char hh[EV_NT];
+    __shared__ int64_t scan_sm[33];
+    __shared__ int64_t s_tile, s_excl;
+    __shared__ unsigned long long s_prevkey;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_tile = (int64_t)atomicAdd(P.ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * EV_TILE;
+    const int64_t i0 = base + (int64_t)tid * EV_IPT;
+    const int64_t N = P.N;
+
+    // ---- phase A: instance keys (attribution) ----
+    unsigned long long key[EV_IPT];
+    {
+        int64_t cur[4] = {-2, -2, -2, -2};
+        int lgp = -1;
+#pragma unroll
+        for (int k = 0; k < EV_IPT; k++) {
+            int64_t i = i0 + k;
+            key[k] = CH_INVALID_KEY;
+            if (i < N) {
+                int lg = P.gpu_lg[gpu_of(P.meta[i])];
+                if (lg != lgp) { cur[0] = cur[1] = cur[2] = cur[3] = -2; lgp = lg; }
+                key[k] = event_key(P, i, lg, P.tl[i], cur);
+            }
+        }
+    }
+    lastkey[tid] = key[EV_IPT - 1];
+    if (tid == 0) {
+        s_prevkey = 0;
+        if (base > 0 && base < N) {
+            int64_t i = base - 1;
+            int64_t c2[4] = {-2, -2, -2, -2};
+            s_prevkey = event_key(P, i, P.gpu_lg[gpu_of(P.meta[i])], P.tl[i], c2);
+        }
+    }
+    __syncthreads();
+    unsigned hmask = 0;
+    {
+        unsigned long long prev = tid > 0 ? lastkey[tid - 1] : s_prevkey;
+#pragma unroll
+        for (int k = 0; k < EV_IPT; k++) {
+            int64_t i = i0 + k;
+            if (i < N && (i == base || key[k] != prev)) hmask |= 1u << k;
+            prev = key[k];
+        }
+    }
+    int64_t tot;
+    int64_t ex = block_excl_sum<EV_NT>(__popc(hmask), &tot, scan_sm);
+    // ---- decoupled look-back: global sub-run id of this tile's first head ----
+    if (tid == 0) {
+        int64_t excl = 0;
+        if (tile == 0) {
+            atomicExch(&P.tile_state[0], FLAG_P | (unsigned long long)tot);
+        } else {
+            atomicExch(&P.tile_state[tile], FLAG_A | (unsigned long long)tot);
+            int64_t p = tile - 1;
+            while (true) {
+                unsigned long long s = *((volatile unsigned long long *)&P.tile_state[p]);
+                unsigned long long fl = s >> 62;
+                if (fl == 0) continue;
+                excl += (int64_t)(s & VAL_MASK);
+                if (fl == 2) break;
+                p--;
+            }
+            atomicExch(&P.tile_state[tile], FLAG_P | (unsigned long long)(excl + tot));
+        }
+        s_excl = excl;
+    }
+    __syncthreads();
+    const int64_t run0 = s_excl + ex;
+
+    // ---- phase B: per-event values, outputs, thread-sequential folding ----
+    Acc acc;
+    acc.zero();
+    bool has = false;
+    int64_t curid = run0 - 1;
+    int64_t cu_s = -2, cu_e = -2, cs_s = -2, cs_e = -2;
+    int lgp = -1;
+#pragma unroll 1
+    for (int k = 0; k < EV_IPT; k++) {
+        int64_t i = i0 + k;
+        if (i >= N) break;
+        uint32_t m = P.meta[i];
+        int lg = P.gpu_lg[gpu_of(m)];
+        if (lg != lgp) { cu_s = cu_e = cs_s = cs_e = -2; lgp = lg; }
+        if ((hmask >> k) & 1u) {
+            if (!has) { acc.store(fp, tid); has = true; }
+            else write_subrun(P, curid, acc);
+            curid++;
+            acc.zero();
+            P.sr_key[curid] = key[k];
+            P.sr_first[curid] = i;
+        }
+        int kd = kind_of(m);
+        int64_t ks = P.ks[i], ke = P.ke[i];
+        int64_t dur = ke - ks;
+        int64_t ovl = 0, prep = 0, call = 0, phi = 0, psi = 0;
+        acc.v[RF_NEV] += 1;
+        if (kd == CK_COMPUTE) {
+            int64_t pe = P.pred_end[i];
+            if (pe != CH_NONE_TS) {
+                int64_t tl = P.tl[i];
+                int64_t t2 = tl < ks ? tl : ks;                       // D6: dispatch clamped to start
+                int64_t a = t2 - pe;
+                prep = a > 0 ? a : 0;                                  // Eq. 1
+                int64_t c1 = ks - t2, c2 = ks - pe;
+                int64_t c = c1 < c2 ? c1 : c2;                         // Eq. 2
+                call = c > 0 ? c : 0;
+            }
+            int64_t ulo = P.Ubeg[lg], uhi = ulo + P.Ucnt[lg];
+            ovl = cov(P.Us, P.Ue, P.UP, ulo, uhi, ke, &cu_e) - cov(P.Us, P.Ue, P.UP, ulo, uhi, ks, &cu_s);
+            int64_t slo = P.smp_lo[lg], shi = P.smp_hi[lg];
+            if (shi > slo) {
+                int64_t Fa, Fb, Pa, Pb;
+                {
+                    int64_t q = seek(P.smp_ts, slo, shi, ks, &cs_s);
+                    if (q < slo) q = slo;
+                    int64_t dt = ks - P.smp_ts[q];
+                    Fa = P.phi_pre[q] + (int64_t)P.smp_f[q] * dt;
+                    Pa = P.psi_pre[q] + (int64_t)P.smp_p[q] * dt;
+                }
+                {
+                    int64_t q = seek(P.smp_ts, slo, shi, ke, &cs_e);
+                    if (q < slo) q = slo;
+                    int64_t dt = ke - P.smp_ts[q];
+                    Fb = P.phi_pre[q] + (int64_t)P.smp_f[q] * dt;
+                    Pb = P.psi_pre[q] + (int64_t)P.smp_p[q] * dt;
+                }
+                phi = Fb - Fa;
+                psi = Pb - Pa;
+            }
+            acc.v[RF_N] += 1;
+            acc.v[RF_BUSY] += dur;
+            acc.v[RF_PREP] += prep;
+            acc.v[RF_CALL] += call;
+            acc.v[RF_OVL] += ovl;
+            acc.v[RF_PHI] += phi;
+            acc.v[RF_PSI] += psi;
+            if (ks < acc.v[RF_FIRST_KS] || (ks == acc.v[RF_FIRST_KS] && i < acc.v[RF_FIRST_IDX])) {
+                acc.v[RF_FIRST_KS] = ks;
+                acc.v[RF_FIRST_IDX] = i;
+            }
+            if (ke > acc.v[RF_LAST_KE]) acc.v[RF_LAST_KE] = ke;
+        } else {
+            if (kd == CK_COPY || kd == CK_OTHER) acc.v[RF_COPY] += dur;
+            else if (kd == CK_AG) acc.v[RF_AG] += dur;
+            else if (kd == CK_RS) acc.v[RF_RS] += dur;
+            if (is_comm(kd)) {
+                if (P.v_general) {
+                    int64_t vlo = P.Vbeg[lg], vhi = vlo + P.Vcnt[lg];
+                    int64_t c1 = -2, c2 = -2;
+                    ovl = cov(P.Vs, P.Ve, P.VP, vlo, vhi, ke, &c1) - cov(P.Vs, P.Ve, P.VP, vlo, vhi, ks, &c2);
+                } else {
+                    ovl = covl_fast(P, lg, ks, ke);
+                }
+            }
+        }
+        if (P.o_ovl) P.o_ovl[i] = ovl;
+        if (P.o_prep) P.o_prep[i] = prep;
+        if (P.o_call) P.o_call[i] = call;
+        if (P.o_phi) P.o_phi[i] = phi;
+        if (P.o_psi) P.o_psi[i] = psi;
+        if (P.o_run) P.o_run[i] = (int32_t)curid;
+    }
+    if (has) acc.store(lp, tid);
+    else acc.store(fp, tid);
+    hh[tid] = has;
+    __syncthreads();
+    // ---- in-tile completion of sub-runs that span threads ----
+    if (has && tid > 0) {
+        Acc s, t;
+        s.load(fp, tid);
+        int u = tid - 1;
+        while (!hh[u]) { t.load(fp, u); s.add(t); u--; }
+        t.load(lp, u);
+        s.add(t);
+        write_subrun(P, run0 - 1, s);
+    }
+    if (tid == EV_NT - 1 && base < N) {
+        int64_t last_id = s_excl + tot - 1;
+        if (has) {
+            Acc s;
+            s.load(lp, tid);
+            write_subrun(P, last_id, s);
+        } else {
+            Acc s, t;
+            s.load(fp, tid);
+            int u = tid - 1;
+            while (!hh[u]) { t.load(fp, u); s.add(t); u--; }
+            t.load(lp, u);
+            s.add(t);
+            write_subrun(P, last_id, s);
+        }
+    }
+}
+}  // namespace
+
+chopper_status ch_overlap_prep(chopper_ctx *ctx) {
+    const int n_lg = ctx->n_lg, NG = ctx->NG;
+    const int64_t N = ctx->N;
+    CH_ALLOC_BEGIN;
+    ctx->d_U_beg = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    ctx->d_U_cnt = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    ctx->d_V_beg = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    ctx->d_V_cnt = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    ctx->U_s = CH_ALLOC(ctx, int64_t, N);
+    ctx->U_e = CH_ALLOC(ctx, int64_t, N);
+    ctx->U_P = CH_ALLOC(ctx, int64_t, N);
+    ctx->d_smp_lo = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    ctx->d_smp_hi = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    int64_t *seg_lo = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    int64_t *seg_hi = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    CH_ALLOC_END(ctx);
+    // comm union U_g over the communication bucket of each gpu (all comm streams, D9)
+    std::vector<int64_t> lo(n_lg), hi(n_lg);
+    for (int l = 0; l < n_lg; l++) { lo[l] = ctx->bucket_beg[l * NG]; hi[l] = ctx->bucket_beg[l * NG + 1]; }
+    CH_CUDA(ctx, cudaMemcpyAsync(seg_lo, lo.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(seg_hi, hi.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+    if (n_lg > 0) {
+        k_union_block<<<n_lg, 1024, 0, ctx->st>>>(ctx->d_perm, seg_lo, seg_hi, ctx->ev.start_ns, ctx->ev.end_ns, ctx->U_s,
+                                                  ctx->U_e, ctx->U_P, ctx->d_U_beg, ctx->d_U_cnt);
+        CH_LAUNCHED(ctx);
+    }
+    // compute union V_g: explicit only with several compute streams or same-stream overlaps
+    ctx->v_general = (ctx->multi_stream || ctx->h_rep.val_count[CV_STREAM_OVERLAP] > 0) ? 1 : 0;
+    if (ctx->v_general && n_lg > 0) {
+        ctx->V_s = CH_ALLOC(ctx, int64_t, N);
+        ctx->V_e = CH_ALLOC(ctx, int64_t, N);
+        ctx->V_P = CH_ALLOC(ctx, int64_t, N);
+        ctx->d_vperm = CH_ALLOC(ctx, uint32_t, N);
+        int64_t *vlo = CH_ALLOC(ctx, int64_t, n_lg + 1), *vhi = CH_ALLOC(ctx, int64_t, n_lg + 1);
+        CH_ALLOC_END(ctx);
+        size_t mark = ctx->used;
+        unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, N), *k2 = CH_ALLOC(ctx, unsigned long long, N);
+        uint32_t *v2 = CH_ALLOC(ctx, uint32_t, N);
+        CH_ALLOC_END(ctx);
+        int tsbits = bits_for((uint64_t)(ctx->t_max - ctx->t0));
+        int lgbits = bits_for((uint64_t)n_lg);
+        if (tsbits + lgbits > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "compute-union key exceeds 64 bits");
+        k_vkeys<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, N, ctx->d_gpu_lg, ctx->t0,
+                                                               tsbits, lgbits, k1, ctx->d_vperm);
+        CH_LAUNCHED(ctx);
+        bool alt;
+        CH_TRY(ch_radix_sort(ctx, k1, ctx->d_vperm, k2, v2, N, 0, tsbits + lgbits, &alt));
+        if (alt) CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_vperm, v2, 4 * N, cudaMemcpyDeviceToDevice, ctx->st));
+        ctx->used = mark;
+        // compute events of lg are contiguous in vperm: counts per gpu from the buckets
+        std::vector<int64_t> a(n_lg), b(n_lg);
+        int64_t off = 0;
+        for (int l = 0; l < n_lg; l++) {
+            int64_t c = ctx->bucket_beg[l * NG + NG - 1] - ctx->bucket_beg[l * NG + 1];
+            a[l] = off; b[l] = off + c; off += c;
+        }
+        CH_CUDA(ctx, cudaMemcpyAsync(vlo, a.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(vhi, b.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+        k_union_block<<<n_lg, 1024, 0, ctx->st>>>(ctx->d_vperm, vlo, vhi, ctx->ev.start_ns, ctx->ev.end_ns, ctx->V_s,
+                                                  ctx->V_e, ctx->V_P, ctx->d_V_beg, ctx->d_V_cnt);
+        CH_LAUNCHED(ctx);
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));   // host vectors a/b go out of scope
+    }
+    // sample prefix integrals (D10)
+    ctx->smp_lo.assign(n_lg, 0);
+    ctx->smp_hi.assign(n_lg, 0);
+    for (int l = 0; l < n_lg; l++) {
+        int g = ctx->lg_gpu[l];
+        if (ctx->has_smp && ctx->h_rep.send[g] > 0 && ctx->h_rep.sbeg[g] != ~0ull) {
+            ctx->smp_lo[l] = (int64_t)ctx->h_rep.sbeg[g];
+            ctx->smp_hi[l] = (int64_t)ctx->h_rep.send[g];
+        }
+    }
+    CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_smp_lo, ctx->smp_lo.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_smp_hi, ctx->smp_hi.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+    if (ctx->has_smp && ctx->M > 0) {
+        const int64_t M = ctx->M;
+        ctx->d_smp_phi = CH_ALLOC(ctx, int64_t, M);
+        ctx->d_smp_psi = CH_ALLOC(ctx, int64_t, M);
+        CH_ALLOC_END(ctx);
+        size_t mark = ctx->used;
+        int64_t *tf = CH_ALLOC(ctx, int64_t, M), *tp = CH_ALLOC(ctx, int64_t, M);
+        uint8_t *hd = CH_ALLOC(ctx, uint8_t, M);
+        CH_ALLOC_END(ctx);
+        k_smp_terms<<<(unsigned)ceil_div(M, NT), NT, 0, ctx->st>>>(ctx->smp.gpu, ctx->smp.ts_ns, ctx->smp.freq_mhz,
+                                                                   ctx->smp.power_mw, M, tf, tp, hd);
+        CH_LAUNCHED(ctx);
+        CH_TRY(ch_seg_scan_i64(ctx, tf, hd, ctx->d_smp_phi, M, 0));
+        CH_TRY(ch_seg_scan_i64(ctx, tp, hd, ctx->d_smp_psi, M, 0));
+        ctx->used = mark;
+    }
+    // lg -> has samples (breakdown flag)
+    ctx->d_has_smp = CH_ALLOC(ctx, int32_t, n_lg + 1);
+    CH_ALLOC_END(ctx);
+    {
+        std::vector<int32_t> hs(n_lg + 1, 0);
+        for (int l = 0; l < n_lg; l++) hs[l] = ctx->smp_hi[l] > ctx->smp_lo[l] ? 1 : 0;
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_has_smp, hs.data(), 4 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    }
+    return CHOPPER_OK;
+}
+
+chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int64_t *call, int64_t *phi, int64_t *psi) {
+    const int64_t N = ctx->N;
+    ctx->R = 0;
+    if (N == 0) return CHOPPER_OK;
+    int64_t ntile = ceil_div(N, EV_TILE);
+    CH_ALLOC_BEGIN;
+    ctx->sub.cap = N;
+    ctx->sub.key = CH_ALLOC(ctx, unsigned long long, N + 1);
+    ctx->sub.first_event = CH_ALLOC(ctx, int64_t, N + 1);
+    ctx->sub.f = CH_ALLOC(ctx, int64_t, (int64_t)NACC * N);
+    ctx->d_run_id = CH_ALLOC(ctx, int32_t, N);
+    ctx->d_tile_state = CH_ALLOC(ctx, unsigned long long, ntile);
+    ctx->d_tile_ticket = CH_ALLOC(ctx, unsigned int, 1);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemsetAsync(ctx->d_tile_state, 0, 8 * ntile, ctx->st));
+    CH_CUDA(ctx, cudaMemsetAsync(ctx->d_tile_ticket, 0, 4, ctx->st));
+    EvParams P;
+    P.tl = ctx->ev.dispatch_ns;
+    P.ks = ctx->ev.start_ns;
+    P.ke = ctx->ev.end_ns;
+    P.meta = ctx->ev.meta;
+    P.N = N;
+    P.gpu_lg = ctx->d_gpu_lg;
+    P.sv = ch_span_view(ctx);
+    P.sh_op = 0;
+    P.sh_ly = ctx->kb[3];
+    P.sh_ph = P.sh_ly + ctx->kb[2];
+    P.sh_it = P.sh_ph + ctx->kb[1];
+    P.sh_lg = P.sh_it + ctx->kb[0];
+    P.pred_end = ctx->d_pred_end;
+    P.Us = ctx->U_s; P.Ue = ctx->U_e; P.UP = ctx->U_P; P.Ubeg = ctx->d_U_beg; P.Ucnt = ctx->d_U_cnt;
+    P.v_general = ctx->v_general;
+    P.Vs = ctx->V_s; P.Ve = ctx->V_e; P.VP = ctx->V_P; P.Vbeg = ctx->d_V_beg; P.Vcnt = ctx->d_V_cnt;
+    P.perm = ctx->d_perm;
+    P.bucket_beg = ctx->d_bucket_beg;
+    P.NG = ctx->NG;
+    P.smp_ts = ctx->smp.ts_ns; P.smp_f = ctx->smp.freq_mhz; P.smp_p = ctx->smp.power_mw;
+    P.phi_pre = ctx->d_smp_phi; P.psi_pre = ctx->d_smp_psi; P.smp_lo = ctx->d_smp_lo; P.smp_hi = ctx->d_smp_hi;
+    P.o_ovl = ovl; P.o_prep = prep; P.o_call = call; P.o_phi = phi; P.o_psi = psi;
+    P.o_run = ctx->d_run_id;
+    P.sr_key = ctx->sub.key; P.sr_first = ctx->sub.first_event; P.sr_f = ctx->sub.f; P.cap = N;
+    P.tile_state = ctx->d_tile_state; P.ticket = ctx->d_tile_ticket;
+    size_t dsm = sizeof(int64_t) * 2 * NACC * EV_NT;
+    static bool attr_set = false;
+    if (!attr_set) {
+        CH_CUDA(ctx, cudaFuncSetAttribute(k_events, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        attr_set = true;
+    }
+    k_events<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P);
+    CH_LAUNCHED(ctx);
+    unsigned long long last = 0;
+    CH_CUDA(ctx, cudaMemcpyAsync(&last, ctx->d_tile_state + ntile - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    ctx->R = (int64_t)(last & VAL_MASK);
+    // sentinel: sub-run R begins at N
+    int64_t nv = N;
+    CH_CUDA(ctx, cudaMemcpyAsync(ctx->sub.first_event + ctx->R, &nv, 8, cudaMemcpyHostToDevice, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    return CHOPPER_OK;
+}
+
+// event-pass launch geometry (for the bench's algorithmic-bytes accounting)
+int64_t ch_event_tile() { return EV_TILE; }

@@ -1,0 +1,347 @@
+// load.cu -- a1 pack + validate and a2 timestamp sort (chopper_load_columns).
+//
+// a1: one streaming pass over the event columns
+//   checks t_ks <= t_ke, gpu grouping, non-decreasing dispatch per gpu, meta
+//   ranges, and collects per-gpu ranges, the max compute stream and the
+//   global timestamp range (< 2^52).
+// a2 (D1): stable sort of events by (gpu, group, t_ks) with group = 0 for
+//   communication, 1 + stream for COMPUTE, "other" last.  B200 path: one
+//   stable counting pass keyed by (gpu, group) straight from meta; if any
+//   communication or compute group is then not start-monotone, a full LSD
+//   radix sort on (bucket, t_ks - t0) replaces it.  The same pass derives the
+//   launch chain predecessor (previous COMPUTE kernel on the
+//   same stream) and the same-stream disjointness check.
+#include "common.cuh"
+
+namespace {
+constexpr int NT = 256;
+
+__global__ void k_validate_events(const int64_t *__restrict__ tl, const int64_t *__restrict__ ks,
+                                  const int64_t *__restrict__ ke, const uint32_t *__restrict__ meta, int64_t n,
+                                  int G, DevReport *rep) {
+    __shared__ unsigned int smax[CH_MAX_GPUS];
+    for (int g = threadIdx.x; g < CH_MAX_GPUS; g += blockDim.x) smax[g] = 0;
+    __syncthreads();
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t m = meta[i];
+        int g = gpu_of(m), k = kind_of(m), s = stream_of(m);
+        int64_t a = tl[i], b = ks[i], c = ke[i];
+        if (b > c) viol(rep, CV_START_AFTER_END, i);
+        if (i > 0) {
+            uint32_t mp = meta[i - 1];
+            int gp = gpu_of(mp);
+            if (g < gp) viol(rep, CV_GPU_NOT_GROUPED, i);
+            if (g == gp && a < tl[i - 1]) viol(rep, CV_DISPATCH_DECREASING, i);
+        }
+        bool bad = k > CK_OTHER || g >= G || (k == CK_COMPUTE && s > 253);
+        if (bad) {
+            viol(rep, CV_BAD_META, i);
+        } else {
+            if (i == 0 || gpu_of(meta[i - 1]) != g) atomicMin(&rep->gbeg[g], (unsigned long long)i);
+            if (i == n - 1 || gpu_of(meta[i + 1]) != g) atomicMax(&rep->gend[g], (unsigned long long)(i + 1));
+            if (k == CK_COMPUTE) atomicMax(&smax[g], (unsigned)(s + 1));
+        }
+        unsigned long long ea = enc_i64(a), eb = enc_i64(b), ec = enc_i64(c);
+        unsigned long long mn = ea < eb ? ea : eb, mx = ea > eb ? ea : eb;
+        mn = mn < ec ? mn : ec;
+        mx = mx > ec ? mx : ec;
+        lo = lo < mn ? lo : mn;
+        hi = hi > mx ? hi : mx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long a = __shfl_xor_sync(CH_FULL, lo, o), b = __shfl_xor_sync(CH_FULL, hi, o);
+        lo = lo < a ? lo : a;
+        hi = hi > b ? hi : b;
+    }
+    if (lane_id() == 0) {
+        atomicMin(&rep->t_min_enc, lo);
+        atomicMax(&rep->t_max_enc, hi);
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < G; g += blockDim.x)
+        if (smax[g]) atomicMax(&rep->max_stream[g], smax[g]);
+}
+
+__global__ void k_validate_spans(const uint32_t *__restrict__ gl, const int64_t *__restrict__ s,
+                                 const int64_t *__restrict__ e, int64_t n, int G, DevReport *rep) {
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t x = gl[j];
+        if (e[j] < s[j] || (x & 0xFFu) > 3 || (int)(x >> 8) >= G) {
+            viol(rep, CV_SPAN_BAD, j);
+            continue;
+        }
+        unsigned long long a = enc_i64(s[j]), b = enc_i64(e[j]);
+        lo = lo < a ? lo : a;
+        hi = hi > b ? hi : b;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long a = __shfl_xor_sync(CH_FULL, lo, o), b = __shfl_xor_sync(CH_FULL, hi, o);
+        lo = lo < a ? lo : a;
+        hi = hi > b ? hi : b;
+    }
+    if (lane_id() == 0) {
+        atomicMin(&rep->s_min_enc, lo);
+        atomicMax(&rep->s_max_enc, hi);
+    }
+}
+
+__global__ void k_validate_samples(const int32_t *__restrict__ g, const int64_t *__restrict__ ts, int64_t n, int G,
+                                   DevReport *rep) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        int x = g[k];
+        if (x < 0 || x >= G) { viol(rep, CV_SAMPLES_UNSORTED, k); continue; }
+        if (k > 0 && (x < g[k - 1] || (x == g[k - 1] && ts[k] < ts[k - 1]))) viol(rep, CV_SAMPLES_UNSORTED, k);
+        if (k == 0 || g[k - 1] != x) atomicMin(&rep->sbeg[x], (unsigned long long)k);
+        if (k == n - 1 || g[k + 1] != x) atomicMax(&rep->send[x], (unsigned long long)(k + 1));
+    }
+}
+
+__device__ __forceinline__ int bucket_of(uint32_t m, const int32_t *gpu_lg, int NG, int other) {
+    int k = kind_of(m), g;
+    if (is_comm(k)) g = 0;
+    else if (k == CK_COMPUTE) g = 1 + stream_of(m);
+    else g = other;
+    return gpu_lg[gpu_of(m)] * NG + g;
+}
+
+__global__ void k_make_keys(const uint32_t *__restrict__ meta, const int64_t *__restrict__ ks, int64_t n,
+                            const int32_t *__restrict__ gpu_lg, int NG, int other, int64_t t0, int tsbits,
+                            unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    unsigned long long b = (unsigned long long)bucket_of(meta[i], gpu_lg, NG, other);
+    keys[i] = tsbits ? (b << tsbits) | (unsigned long long)(ks[i] - t0) : b;
+    vals[i] = (uint32_t)i;
+}
+
+// chain predecessor + monotonicity + same-stream disjointness, in sorted order
+__global__ void k_chain(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ meta,
+                        const int64_t *__restrict__ ks, const int64_t *__restrict__ ke, int64_t n,
+                        const int32_t *__restrict__ gpu_lg, int NG, int other, int64_t *__restrict__ pred_end,
+                        DevReport *rep) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    uint32_t i = perm[j];
+    uint32_t m = meta[i];
+    int b = bucket_of(m, gpu_lg, NG, other);
+    int grp = b % NG;
+    bool same = false;
+    uint32_t ip = 0;
+    if (j > 0) {
+        ip = perm[j - 1];
+        same = bucket_of(meta[ip], gpu_lg, NG, other) == b;
+    }
+    int64_t pe = CH_NONE_TS;
+    if (same && grp != other) {
+        int64_t a = ks[i];
+        if (a < ks[ip]) atomicOr(&rep->flags, 1u);   // not start-monotone: full sort needed
+        if (grp >= 1) {
+            pe = ke[ip];
+            if (a < pe) viol(rep, CV_STREAM_OVERLAP, i);
+        }
+    }
+    if (kind_of(m) == CK_COMPUTE) pred_end[i] = pe;
+}
+
+__global__ void k_bucket_begins(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ meta, int64_t n,
+                                const int32_t *__restrict__ gpu_lg, int NG, int other,
+                                unsigned long long *__restrict__ beg) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    int b = bucket_of(meta[perm[j]], gpu_lg, NG, other);
+    if (j == 0 || bucket_of(meta[perm[j - 1]], gpu_lg, NG, other) != b) atomicMin(&beg[b], (unsigned long long)j);
+}
+
+__global__ void k_init_report(DevReport *r) {
+    int t = threadIdx.x;
+    if (t < CV_NRULES) { r->val_count[t] = 0; r->val_first[t] = ~0ull; }
+    for (int g = t; g < CH_MAX_GPUS; g += blockDim.x) {
+        r->gbeg[g] = ~0ull; r->gend[g] = 0; r->sbeg[g] = ~0ull; r->send[g] = 0; r->max_stream[g] = 0; r->n_comm[g] = 0;
+    }
+    if (t == 0) {
+        r->t_min_enc = ~0ull; r->t_max_enc = 0; r->s_min_enc = ~0ull; r->s_max_enc = 0; r->flags = 0; r->latched = 0;
+        r->n_nonlaminar = 0;
+    }
+}
+
+__global__ void k_fill_u64(unsigned long long *p, int64_t n, unsigned long long v) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+}  // namespace
+
+chopper_status ch_fill_u64(chopper_ctx *ctx, unsigned long long *p, int64_t n, unsigned long long v) {
+    if (n <= 0) return CHOPPER_OK;
+    k_fill_u64<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(p, n, v);
+    CH_LAUNCHED(ctx);
+    return CHOPPER_OK;
+}
+
+static chopper_status read_report(chopper_ctx *ctx) {
+    CH_CUDA(ctx, cudaMemcpyAsync(&ctx->h_rep, ctx->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    return CHOPPER_OK;
+}
+
+static void fill_public_report(chopper_ctx *ctx) {
+    DevReport &h = ctx->h_rep;
+    chopper_report &r = ctx->rep;
+    for (int q = 0; q < CV_NRULES; q++) {
+        r.val_count[q] = (int64_t)h.val_count[q];
+        r.val_first[q] = h.val_first[q] == ~0ull ? -1 : (int64_t)h.val_first[q];
+    }
+    r.n_local_gpus = ctx->n_lg;
+    for (int l = 0; l < ctx->n_lg; l++) r.local_gpu[l] = ctx->lg_gpu[l];
+    r.t_min = ctx->t0;
+    r.t_max = ctx->t_max;
+    r.full_sort_used = ctx->full_sort ? 1 : 0;
+}
+
+chopper_status ch_load(chopper_ctx *ctx) {
+    const int G = ctx->cfg.n_traced_gpus;
+    const int64_t n = ctx->N;
+    ctx->used = 0;
+    CH_ALLOC_BEGIN;
+    ctx->d_rep = CH_ALLOC(ctx, DevReport, 1);
+    ctx->d_gpu_lg = CH_ALLOC(ctx, int32_t, CH_MAX_GPUS);
+    CH_ALLOC_END(ctx);
+    k_init_report<<<1, 256, 0, ctx->st>>>(ctx->d_rep);
+    CH_LAUNCHED(ctx);
+    unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, NT), 1), 148 * 16);
+    if (n > 0) {
+        k_validate_events<<<grid, NT, 0, ctx->st>>>(ctx->ev.dispatch_ns, ctx->ev.start_ns, ctx->ev.end_ns, ctx->ev.meta,
+                                                    n, G, ctx->d_rep);
+        CH_LAUNCHED(ctx);
+    }
+    if (ctx->S > 0) {
+        unsigned gs = (unsigned)std::min<int64_t>(ceil_div(ctx->S, NT), 148 * 8);
+        k_validate_spans<<<gs, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, ctx->S, G,
+                                                 ctx->d_rep);
+        CH_LAUNCHED(ctx);
+    }
+    if (ctx->has_smp && ctx->M > 0) {
+        unsigned gs = (unsigned)std::min<int64_t>(ceil_div(ctx->M, NT), 148 * 8);
+        k_validate_samples<<<gs, NT, 0, ctx->st>>>(ctx->smp.gpu, ctx->smp.ts_ns, ctx->M, G, ctx->d_rep);
+        CH_LAUNCHED(ctx);
+    }
+    CH_TRY(read_report(ctx));
+    DevReport &h = ctx->h_rep;
+    ctx->t0 = n > 0 ? dec_i64(h.t_min_enc) : 0;
+    ctx->t_max = n > 0 ? dec_i64(h.t_max_enc) : 0;
+    if (n > 0 && (uint64_t)ctx->t_max - (uint64_t)ctx->t0 >= (1ull << 52)) {
+        h.val_count[CV_TS_RANGE] = 1;
+        h.val_first[CV_TS_RANGE] = 0;
+    }
+    // local gpus (events grouped ascending)
+    ctx->n_lg = 0;
+    for (int g = 0; g < CH_MAX_GPUS; g++) ctx->gpu_lg_h[g] = -1;
+    int ms = 0;
+    for (int g = 0; g < G; g++) {
+        if (h.gend[g] > 0 && h.gbeg[g] != ~0ull) {
+            ctx->gpu_lg_h[g] = ctx->n_lg;
+            ctx->lg_gpu[ctx->n_lg] = g;
+            ctx->g_beg[ctx->n_lg] = (int64_t)h.gbeg[g];
+            ctx->n_lg++;
+            ms = std::max(ms, (int)h.max_stream[g]);
+        }
+    }
+    ctx->g_beg[ctx->n_lg] = n;
+    ctx->max_stream = ms;
+    ctx->multi_stream = ms > 1;
+    ctx->NG = ms + 2;
+    ctx->n_buckets = ctx->n_lg * ctx->NG;
+    fill_public_report(ctx);
+    const int fatal[] = {CV_START_AFTER_END, CV_GPU_NOT_GROUPED, CV_DISPATCH_DECREASING, CV_BAD_META, CV_TS_RANGE,
+                         CV_SPAN_BAD, CV_SAMPLES_UNSORTED};
+    for (int q : fatal)
+        if (h.val_count[q]) {
+            ctx->loaded_ok = false;
+            return ch_fail(ctx, CHOPPER_E_VALIDATION, "input validation failed (rule " + std::to_string(q) + ")");
+        }
+    if (ctx->n_lg == 0) {
+        ctx->loaded_ok = true;
+        return CHOPPER_OK;
+    }
+    CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_gpu_lg, ctx->gpu_lg_h, sizeof(int32_t) * CH_MAX_GPUS, cudaMemcpyHostToDevice,
+                                 ctx->st));
+    // a2: partition by (lg, dense group); full radix sort only if a group is not start-monotone
+    ctx->d_perm = CH_ALLOC(ctx, uint32_t, n);
+    ctx->d_pred_end = CH_ALLOC(ctx, int64_t, n);
+    ctx->d_bucket_beg = CH_ALLOC(ctx, int64_t, ctx->n_buckets + 1);
+    CH_ALLOC_END(ctx);
+    const int NG = ctx->NG, other = NG - 1;
+    size_t mark = ctx->used;
+    if (ctx->n_buckets <= 256) {
+        CH_TRY(ch_radix_partition_meta(ctx, ctx->ev.meta, ctx->d_gpu_lg, NG, other, ctx->d_perm, n));
+    } else {
+        unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, n), *k2 = CH_ALLOC(ctx, unsigned long long, n);
+        uint32_t *v2 = CH_ALLOC(ctx, uint32_t, n);
+        CH_ALLOC_END(ctx);
+        k_make_keys<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, n, ctx->d_gpu_lg,
+                                                                   NG, other, 0, 0, k1, ctx->d_perm);
+        CH_LAUNCHED(ctx);
+        bool alt;
+        CH_TRY(ch_radix_sort(ctx, k1, ctx->d_perm, k2, v2, n, 0, bits_for((uint64_t)ctx->n_buckets), &alt));
+        if (alt) CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_perm, v2, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->st));
+    }
+    ctx->used = mark;
+    ctx->full_sort = false;
+    k_chain<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
+                                                           ctx->ev.end_ns, n, ctx->d_gpu_lg, NG, other,
+                                                           ctx->d_pred_end, ctx->d_rep);
+    CH_LAUNCHED(ctx);
+    CH_TRY(read_report(ctx));
+    if (ctx->h_rep.flags & 1u) {
+        // full stable sort by (bucket, t_ks - t0), D1
+        int tsbits = bits_for((uint64_t)(ctx->t_max - ctx->t0));
+        int bb = bits_for((uint64_t)ctx->n_buckets);
+        if (tsbits + bb > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "sort key exceeds 64 bits");
+        unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, n), *k2 = CH_ALLOC(ctx, unsigned long long, n);
+        uint32_t *v2 = CH_ALLOC(ctx, uint32_t, n);
+        CH_ALLOC_END(ctx);
+        k_make_keys<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, n, ctx->d_gpu_lg,
+                                                                   NG, other, ctx->t0, tsbits, k1, ctx->d_perm);
+        CH_LAUNCHED(ctx);
+        bool alt;
+        CH_TRY(ch_radix_sort(ctx, k1, ctx->d_perm, k2, v2, n, 0, tsbits + bb, &alt));
+        if (alt) CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_perm, v2, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->st));
+        ctx->used = mark;
+        ctx->full_sort = true;
+        // reset the disjointness counters and recompute the chain in the true sorted order
+        unsigned long long zero = 0, none = ~0ull;
+        CH_CUDA(ctx, cudaMemcpyAsync(&ctx->d_rep->val_count[CV_STREAM_OVERLAP], &zero, 8, cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(&ctx->d_rep->val_first[CV_STREAM_OVERLAP], &none, 8, cudaMemcpyHostToDevice, ctx->st));
+        k_chain<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
+                                                               ctx->ev.end_ns, n, ctx->d_gpu_lg, NG, other,
+                                                               ctx->d_pred_end, ctx->d_rep);
+        CH_LAUNCHED(ctx);
+    }
+    // bucket begins in sorted order
+    {
+        unsigned long long *beg = reinterpret_cast<unsigned long long *>(ctx->d_bucket_beg);
+        CH_TRY(ch_fill_u64(ctx, beg, ctx->n_buckets + 1, ~0ull));
+        k_bucket_begins<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, n, ctx->d_gpu_lg, NG,
+                                                                       other, beg);
+        CH_LAUNCHED(ctx);
+        ctx->bucket_beg.assign(ctx->n_buckets + 1, 0);
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->bucket_beg.data(), beg, 8 * (ctx->n_buckets + 1), cudaMemcpyDeviceToHost,
+                                     ctx->st));
+        CH_TRY(read_report(ctx));
+        // empty buckets begin where the next non-empty one does
+        ctx->bucket_beg[ctx->n_buckets] = n;
+        for (int b = ctx->n_buckets - 1; b >= 0; b--)
+            if ((unsigned long long)ctx->bucket_beg[b] == ~0ull) ctx->bucket_beg[b] = ctx->bucket_beg[b + 1];
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_bucket_beg, ctx->bucket_beg.data(), 8 * (ctx->n_buckets + 1),
+                                     cudaMemcpyHostToDevice, ctx->st));
+    }
+    // same-stream overlaps are data: reported, processing continues
+    fill_public_report(ctx);
+    if (ctx->h_rep.val_count[CV_STREAM_OVERLAP]) ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
+    ctx->loaded_ok = true;
+    ctx->mark_after_load = ctx->used;
+    return CHOPPER_OK;
+}

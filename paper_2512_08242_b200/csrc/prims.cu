@@ -1,0 +1,329 @@
+// prims.cu -- device-wide primitives written for this library: exclusive /
+// segmented scans and a stable LSD radix sort (8-bit digits, warp-match
+// ranking).  Used by the a2 timestamp sort, span push-order sort, sub-run
+// grouping and the union / sample prefix builders.
+#include "common.cuh"
+
+namespace {
+constexpr int SC_NT = 256, SC_IPT = 8, SC_TILE = SC_NT * SC_IPT;
+
+__global__ void k_tile_sums(const int64_t *__restrict__ in, int64_t n, int64_t *__restrict__ sums) {
+    __shared__ int64_t sm[33];
+    int64_t base = (int64_t)blockIdx.x * SC_TILE;
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SC_IPT; k++) {
+        int64_t i = base + (int64_t)k * SC_NT + threadIdx.x;
+        if (i < n) s += in[i];
+    }
+    int64_t tot;
+    block_excl_sum<SC_NT>(s, &tot, sm);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void k_tile_apply(const int64_t *__restrict__ in, int64_t n, const int64_t *__restrict__ offs,
+                             int64_t *__restrict__ out, int64_t *total_dev) {
+    __shared__ int64_t sm[33];
+    int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_IPT;
+    int64_t v[SC_IPT];
+    int64_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SC_IPT; k++) {
+        int64_t i = base + k;
+        v[k] = i < n ? in[i] : 0;
+        s += v[k];
+    }
+    int64_t tot;
+    int64_t ex = block_excl_sum<SC_NT>(s, &tot, sm) + (offs ? offs[blockIdx.x] : 0);
+#pragma unroll
+    for (int k = 0; k < SC_IPT; k++) {
+        int64_t i = base + k;
+        if (i < n) out[i] = ex;
+        ex += v[k];
+    }
+    if (total_dev && blockIdx.x == gridDim.x - 1 && threadIdx.x == SC_NT - 1) *total_dev = ex;
+}
+
+// ---- segmented scans: aggregate (head seen, value since last head) ------------------------------
+template <int OP>
+__device__ __forceinline__ int64_t op_comb(int64_t a, int64_t b) {
+    if (OP == 1) return a > b ? a : b;
+    return a + b;
+}
+template <int OP>
+__device__ __forceinline__ int64_t op_id() { return OP == 1 ? INT64_MIN : 0; }
+
+template <int OP>
+__global__ void k_seg_tile_agg(const int64_t *__restrict__ in, const uint8_t *__restrict__ head, int64_t n,
+                               int64_t *__restrict__ agg_v, uint8_t *__restrict__ agg_h) {
+    // one thread per tile is enough here: tile aggregates are tiny compared to the apply pass
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t ntile = (n + SC_TILE - 1) / SC_TILE;
+    if (t >= ntile) return;
+    int64_t lo = t * SC_TILE, hi = lo + SC_TILE < n ? lo + SC_TILE : n;
+    int64_t v = op_id<OP>();
+    uint8_t h = 0;
+    for (int64_t i = lo; i < hi; i++) {
+        if (head[i]) { v = op_id<OP>(); h = 1; }
+        v = op_comb<OP>(v, in[i]);
+    }
+    agg_v[t] = v;
+    agg_h[t] = h;
+}
+
+// exclusive carry per tile, single thread sequential (tiles are few)
+template <int OP>
+__global__ void k_seg_carry(const int64_t *__restrict__ agg_v, const uint8_t *__restrict__ agg_h, int64_t ntile,
+                            int64_t *__restrict__ carry) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t c = op_id<OP>();
+    for (int64_t t = 0; t < ntile; t++) {
+        carry[t] = c;
+        c = agg_h[t] ? agg_v[t] : op_comb<OP>(c, agg_v[t]);
+    }
+}
+
+// per-thread sequential segment inside the tile with a warp/block carry of (head, value)
+template <int OP, bool EXCL>
+__global__ void k_seg_apply(const int64_t *__restrict__ in, const uint8_t *__restrict__ head, int64_t n,
+                            const int64_t *__restrict__ carry, int64_t *__restrict__ out) {
+    __shared__ int64_t sv[SC_NT];
+    __shared__ uint8_t sh[SC_NT];
+    int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_IPT;
+    int64_t v = op_id<OP>();
+    uint8_t h = 0;
+    for (int k = 0; k < SC_IPT; k++) {
+        int64_t i = base + k;
+        if (i >= n) break;
+        if (head[i]) { v = op_id<OP>(); h = 1; }
+        v = op_comb<OP>(v, in[i]);
+    }
+    sv[threadIdx.x] = v;
+    sh[threadIdx.x] = h;
+    __syncthreads();
+    // sequential exclusive carry across threads (thread 0), simple and deterministic
+    if (threadIdx.x == 0) {
+        int64_t c = carry[blockIdx.x];
+        for (int t = 0; t < SC_NT; t++) {
+            int64_t a = sv[t];
+            uint8_t hh = sh[t];
+            sv[t] = c;
+            c = hh ? a : op_comb<OP>(c, a);
+        }
+    }
+    __syncthreads();
+    int64_t c = sv[threadIdx.x];
+    for (int k = 0; k < SC_IPT; k++) {
+        int64_t i = base + k;
+        if (i >= n) break;
+        if (head[i]) c = op_id<OP>();
+        if (EXCL) { out[i] = c; c = op_comb<OP>(c, in[i]); }
+        else { c = op_comb<OP>(c, in[i]); out[i] = c; }
+    }
+}
+
+// ---- radix sort ---------------------------------------------------------------------------------
+constexpr int RX_NT = 256, RX_WARPS = RX_NT / 32, RX_ROUNDS = 8, RX_TILE = RX_NT * RX_ROUNDS;
+
+struct KeyArr {
+    const unsigned long long *k;
+    int shift;
+    __device__ __forceinline__ int digit(int64_t i) const { return (int)((k[i] >> shift) & 0xFFu); }
+};
+struct KeyMeta {  // partition digit: bucket = lg * NG + dense group (a2 fast path)
+    const uint32_t *meta;
+    const int32_t *gpu_lg;
+    int NG, other;
+    __device__ __forceinline__ int digit(int64_t i) const {
+        uint32_t m = meta[i];
+        int k = kind_of(m), g;
+        if (is_comm(k)) g = 0;
+        else if (k == CK_COMPUTE) g = 1 + stream_of(m);
+        else g = other;
+        return gpu_lg[gpu_of(m)] * NG + g;
+    }
+};
+
+template <class KS>
+__global__ void __launch_bounds__(RX_NT) k_rx_upsweep(KS ks, int64_t n, unsigned int *__restrict__ counts,
+                                                      int64_t ntile) {
+    __shared__ unsigned int h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    int64_t base = (int64_t)blockIdx.x * RX_TILE;
+    for (int r = 0; r < RX_ROUNDS; r++) {
+        int64_t i = base + (int64_t)r * RX_NT + threadIdx.x;
+        if (i < n) atomicAdd(&h[ks.digit(i)], 1u);
+    }
+    __syncthreads();
+    counts[(int64_t)threadIdx.x * ntile + blockIdx.x] = h[threadIdx.x];
+}
+
+template <class KS, bool HAS_KEYS, bool HAS_VALS>
+__global__ void __launch_bounds__(RX_NT) k_rx_downsweep(KS ks, const unsigned long long *__restrict__ keys_in,
+                                                        const uint32_t *__restrict__ vals_in, int64_t n,
+                                                        const int64_t *__restrict__ offs, int64_t ntile,
+                                                        unsigned long long *__restrict__ keys_out,
+                                                        uint32_t *__restrict__ vals_out) {
+    __shared__ unsigned int wh[RX_WARPS][256];
+    __shared__ int64_t goff[256];
+    int w = threadIdx.x >> 5, l = lane_id();
+    for (int d = threadIdx.x; d < 256 * RX_WARPS; d += RX_NT) (&wh[0][0])[d] = 0;
+    goff[threadIdx.x] = offs[(int64_t)threadIdx.x * ntile + blockIdx.x];
+    __syncthreads();
+    int64_t base = (int64_t)blockIdx.x * RX_TILE + (int64_t)w * (32 * RX_ROUNDS);
+    int dg[RX_ROUNDS];
+    unsigned int rk[RX_ROUNDS];
+    unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < RX_ROUNDS; r++) {
+        int64_t i = base + r * 32 + l;
+        bool valid = i < n;
+        int d = valid ? ks.digit(i) : 256 + l;
+        unsigned mm = __match_any_sync(CH_FULL, d);
+        unsigned int before = valid ? wh[w][d] : 0;
+        __syncwarp();
+        if (valid && (mm & lt) == 0) wh[w][d] = before + __popc(mm);
+        __syncwarp();
+        dg[r] = d;
+        rk[r] = before + __popc(mm & lt);
+    }
+    __syncthreads();
+    {   // exclusive prefix over warps, per digit (thread = digit)
+        unsigned int run = 0;
+        for (int q = 0; q < RX_WARPS; q++) {
+            unsigned int c = wh[q][threadIdx.x];
+            wh[q][threadIdx.x] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RX_ROUNDS; r++) {
+        int64_t i = base + r * 32 + l;
+        if (i < n) {
+            int d = dg[r];
+            int64_t pos = goff[d] + wh[w][d] + rk[r];
+            if (HAS_KEYS) keys_out[pos] = keys_in[i];
+            vals_out[pos] = HAS_VALS ? vals_in[i] : (uint32_t)i;
+        }
+    }
+}
+__global__ void k_u32_to_i64(const unsigned int *a, int64_t *b, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+}
+}  // namespace
+
+chopper_status ch_scan_excl_i64(chopper_ctx *ctx, const int64_t *in, int64_t *out, int64_t n, int64_t *total_dev) {
+    if (n <= 0) {
+        if (total_dev) CH_CUDA(ctx, cudaMemsetAsync(total_dev, 0, 8, ctx->st));
+        return CHOPPER_OK;
+    }
+    int64_t ntile = ceil_div(n, SC_TILE);
+    size_t mark = ctx->used;
+    CH_ALLOC_BEGIN;
+    int64_t *offs = nullptr;
+    if (ntile > 1) {
+        int64_t *sums = CH_ALLOC(ctx, int64_t, ntile);
+        offs = CH_ALLOC(ctx, int64_t, ntile);
+        CH_ALLOC_END(ctx);
+        k_tile_sums<<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, n, sums);
+        CH_LAUNCHED(ctx);
+        CH_TRY(ch_scan_excl_i64(ctx, sums, offs, ntile, nullptr));
+    }
+    k_tile_apply<<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, n, offs, out, total_dev);
+    CH_LAUNCHED(ctx);
+    ctx->used = mark;
+    return CHOPPER_OK;
+}
+
+chopper_status ch_seg_scan_i64(chopper_ctx *ctx, const int64_t *in, const uint8_t *head, int64_t *out, int64_t n,
+                               int op) {
+    if (n <= 0) return CHOPPER_OK;
+    int64_t ntile = ceil_div(n, SC_TILE);
+    size_t mark = ctx->used;
+    CH_ALLOC_BEGIN;
+    int64_t *agg = CH_ALLOC(ctx, int64_t, ntile);
+    uint8_t *aggh = CH_ALLOC(ctx, uint8_t, ntile);
+    int64_t *carry = CH_ALLOC(ctx, int64_t, ntile);
+    CH_ALLOC_END(ctx);
+    unsigned g1 = (unsigned)ceil_div(ntile, 128);
+    if (op == 1) {
+        k_seg_tile_agg<1><<<g1, 128, 0, ctx->st>>>(in, head, n, agg, aggh);
+        CH_LAUNCHED(ctx);
+        k_seg_carry<1><<<1, 32, 0, ctx->st>>>(agg, aggh, ntile, carry);
+        CH_LAUNCHED(ctx);
+        k_seg_apply<1, false><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
+        CH_LAUNCHED(ctx);
+    } else {
+        k_seg_tile_agg<0><<<g1, 128, 0, ctx->st>>>(in, head, n, agg, aggh);
+        CH_LAUNCHED(ctx);
+        k_seg_carry<0><<<1, 32, 0, ctx->st>>>(agg, aggh, ntile, carry);
+        CH_LAUNCHED(ctx);
+        if (op == 0) k_seg_apply<0, true><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
+        else k_seg_apply<0, false><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
+        CH_LAUNCHED(ctx);
+    }
+    ctx->used = mark;
+    return CHOPPER_OK;
+}
+
+// stable LSD radix sort of (key, value) pairs over bits [bit_lo, bit_hi).  Each pass reads
+// (keys, vals) and writes (keys_alt, vals_alt), then the roles swap; *result_in_alt tells the
+// caller which pair holds the sorted result.
+chopper_status ch_radix_sort(chopper_ctx *ctx, unsigned long long *keys, uint32_t *vals, unsigned long long *keys_alt,
+                             uint32_t *vals_alt, int64_t n, int bit_lo, int bit_hi, bool *result_in_alt) {
+    *result_in_alt = false;
+    if (n <= 0 || bit_hi <= bit_lo) return CHOPPER_OK;
+    int64_t ntile = ceil_div(n, RX_TILE);
+    size_t mark = ctx->used;
+    CH_ALLOC_BEGIN;
+    unsigned int *counts = CH_ALLOC(ctx, unsigned int, 256 * ntile);
+    int64_t *cnt64 = CH_ALLOC(ctx, int64_t, 256 * ntile);
+    int64_t *offs = CH_ALLOC(ctx, int64_t, 256 * ntile);
+    CH_ALLOC_END(ctx);
+    unsigned long long *ki = keys, *ko = keys_alt;
+    uint32_t *vi = vals, *vo = vals_alt;
+    bool alt = false;
+    for (int b = bit_lo; b < bit_hi; b += 8) {
+        KeyArr ks{ki, b};
+        k_rx_upsweep<KeyArr><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, n, counts, ntile);
+        CH_LAUNCHED(ctx);
+        k_u32_to_i64<<<(unsigned)ceil_div(256 * ntile, 256), 256, 0, ctx->st>>>(counts, cnt64, 256 * ntile);
+        CH_LAUNCHED(ctx);
+        CH_TRY(ch_scan_excl_i64(ctx, cnt64, offs, 256 * ntile, nullptr));
+        k_rx_downsweep<KeyArr, true, true><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, ki, vi, n, offs, ntile, ko, vo);
+        CH_LAUNCHED(ctx);
+        std::swap(ki, ko);
+        std::swap(vi, vo);
+        alt = !alt;
+    }
+    *result_in_alt = alt;
+    ctx->used = mark;
+    return CHOPPER_OK;
+}
+
+// a2 fast path: one stable counting pass keyed by (lg, dense group) straight from meta
+chopper_status ch_radix_partition_meta(chopper_ctx *ctx, const uint32_t *meta, const int32_t *gpu_lg, int NG,
+                                       int other_group, uint32_t *vals_out, int64_t n) {
+    if (n <= 0) return CHOPPER_OK;
+    int64_t ntile = ceil_div(n, RX_TILE);
+    size_t mark = ctx->used;
+    CH_ALLOC_BEGIN;
+    unsigned int *counts = CH_ALLOC(ctx, unsigned int, 256 * ntile);
+    int64_t *cnt64 = CH_ALLOC(ctx, int64_t, 256 * ntile);
+    int64_t *offs = CH_ALLOC(ctx, int64_t, 256 * ntile);
+    CH_ALLOC_END(ctx);
+    KeyMeta ks{meta, gpu_lg, NG, other_group};
+    k_rx_upsweep<KeyMeta><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, n, counts, ntile);
+    CH_LAUNCHED(ctx);
+    k_u32_to_i64<<<(unsigned)ceil_div(256 * ntile, 256), 256, 0, ctx->st>>>(counts, cnt64, 256 * ntile);
+    CH_LAUNCHED(ctx);
+    CH_TRY(ch_scan_excl_i64(ctx, cnt64, offs, 256 * ntile, nullptr));
+    k_rx_downsweep<KeyMeta, false, false><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, nullptr, nullptr, n, offs, ntile,
+                                                                                 nullptr, vals_out);
+    CH_LAUNCHED(ctx);
+    ctx->used = mark;
+    return CHOPPER_OK;
+}

@@ -1,0 +1,358 @@
+// spans.cu -- a5 interval-containment attribution structures (chopper_attribute).
+//
+// PAPER.md:100-102, 211-214; readings D3 (half-open spans,
+// containment on dispatch time t_l) and D4 (innermost wins; ambiguity only
+// where crossing spans both contain a dispatch).
+//
+// Spans of each (gpu, level) list are radix-sorted into "push order"
+// (start asc, end desc, index desc): the innermost span containing t is then
+// the last span with start <= t, walked up its parent chain while end <= t.
+// parent(q) = nearest earlier span of the list with end >= end(q) (previous
+// greater-or-equal element), computed per 256-span chunk with a stack and
+// resolved across chunks with a sparse table of chunk maxima.  A list is
+// laminar iff no span between parent(q) and q ends after start(q); lists
+// that are not laminar use an exact sequential sweep on the device
+// (k_attr_sweep) instead of the parent walk.
+#include "common.cuh"
+
+namespace {
+constexpr int NT = 256;
+constexpr int CHUNK = 256;
+constexpr int UNRES = -3;
+constexpr int SWEEP_MAX_ACTIVE = 64;
+
+__device__ __forceinline__ bool span_valid(uint32_t gl, int64_t s, int64_t e, const int32_t *gpu_lg) {
+    int g = (int)(gl >> 8), lv = (int)(gl & 0xFFu);
+    return lv <= 3 && g < CH_MAX_GPUS && gpu_lg[g] >= 0 && e > s;
+}
+
+// sort 1: end descending, ties index descending (initial order = reversed index)
+__global__ void k_span_key1(const uint32_t *__restrict__ gl, const int64_t *__restrict__ s,
+                            const int64_t *__restrict__ e, int64_t S, int64_t emax,
+                            unsigned long long *__restrict__ key, uint32_t *__restrict__ val) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= S) return;
+    int64_t j = S - 1 - q;
+    int64_t ee = e[j];
+    key[q] = (ee <= emax) ? (unsigned long long)(emax - ee) : 0ull;
+    val[q] = (uint32_t)j;
+}
+
+// sort 2: (list, start) with list = lg*4 + level, excluded spans -> list n_lg*4
+__global__ void k_span_key2(const uint32_t *__restrict__ gl, const int64_t *__restrict__ s,
+                            const int64_t *__restrict__ e, const uint32_t *__restrict__ val, int64_t S,
+                            const int32_t *__restrict__ gpu_lg, int n_lg, int64_t smin, int sbits,
+                            unsigned long long *__restrict__ key) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= S) return;
+    uint32_t j = val[q];
+    uint32_t x = gl[j];
+    int64_t a = s[j], b = e[j];
+    unsigned long long list;
+    unsigned long long off = 0;
+    if (span_valid(x, a, b, gpu_lg)) {
+        list = (unsigned long long)(gpu_lg[x >> 8] * 4 + (int)(x & 0xFFu));
+        off = (unsigned long long)(a - smin);
+    } else {
+        list = (unsigned long long)(n_lg * 4);
+    }
+    key[q] = (list << sbits) | off;
+}
+
+__global__ void k_span_gather(const uint32_t *__restrict__ order, const uint32_t *__restrict__ gl,
+                              const int64_t *__restrict__ s, const int64_t *__restrict__ e,
+                              const int32_t *__restrict__ lab, int64_t S, const int32_t *__restrict__ gpu_lg, int n_lg,
+                              int64_t *__restrict__ Ps, int64_t *__restrict__ Pe, int32_t *__restrict__ Po,
+                              int32_t *__restrict__ Pl, int32_t *__restrict__ Plist,
+                              unsigned long long *__restrict__ lbeg) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= S) return;
+    uint32_t j = order[q];
+    uint32_t x = gl[j];
+    int64_t a = s[j], b = e[j];
+    int list = span_valid(x, a, b, gpu_lg) ? gpu_lg[x >> 8] * 4 + (int)(x & 0xFFu) : n_lg * 4;
+    Ps[q] = a;
+    Pe[q] = b;
+    Po[q] = (int32_t)j;
+    Pl[q] = lab[j];
+    Plist[q] = list;
+    int prev = -1;
+    if (q > 0) {
+        uint32_t jp = order[q - 1];
+        uint32_t xp = gl[jp];
+        prev = span_valid(xp, s[jp], e[jp], gpu_lg) ? gpu_lg[xp >> 8] * 4 + (int)(xp & 0xFFu) : n_lg * 4;
+    }
+    if (list != prev) lbeg[list] = (unsigned long long)q;   // sorted: first q of each list is unique
+}
+
+// per-chunk sequential stack: previous greater-or-equal end inside the chunk
+__global__ void k_chunk_stack(const int64_t *__restrict__ Pe, const int32_t *__restrict__ Plist, int64_t S,
+                              int32_t *__restrict__ parent, int32_t *__restrict__ cstack, int32_t *__restrict__ csp,
+                              int64_t *__restrict__ cmax, const int64_t *__restrict__ list_beg) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t lo = c * CHUNK;
+    if (lo >= S) return;
+    int64_t hi = lo + CHUNK < S ? lo + CHUNK : S;
+    int32_t *stk = cstack + lo;
+    int sp = 0;
+    int cur = -1;
+    for (int64_t q = lo; q < hi; q++) {
+        int list = Plist[q];
+        if (list != cur) { sp = 0; cur = list; }
+        int64_t e = Pe[q];
+        while (sp > 0 && Pe[stk[sp - 1]] < e) sp--;
+        if (sp > 0) parent[q] = stk[sp - 1];
+        else parent[q] = (list_beg[list] >= lo) ? -1 : UNRES;
+        stk[sp++] = (int32_t)q;
+    }
+    csp[c] = sp;
+    cmax[c] = sp > 0 ? Pe[stk[0]] : INT64_MIN;   // bottom of the final stack = max end of the last list
+}
+
+__global__ void k_sparse_level(const int64_t *__restrict__ prev, int64_t *__restrict__ next, int64_t nch, int64_t w) {
+    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nch) return;
+    int64_t a = prev[c];
+    int64_t b = c - w >= 0 ? prev[c - w] : INT64_MIN;
+    next[c] = a > b ? a : b;
+}
+
+__global__ void k_resolve(const int64_t *__restrict__ Pe, const int32_t *__restrict__ Plist, int64_t S,
+                          int32_t *__restrict__ parent, const int32_t *__restrict__ cstack,
+                          const int32_t *__restrict__ csp, const int64_t *__restrict__ sparse, int levels,
+                          int64_t nch, const int64_t *__restrict__ list_beg) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= S || parent[q] != UNRES) return;
+    int64_t x = Pe[q];
+    int64_t lbc = list_beg[Plist[q]] / CHUNK;
+    int64_t c = q / CHUNK - 1;
+    // largest chunk index c >= lbc whose max >= x: skip blocks of chunks entirely below x
+    for (int k = levels - 1; k >= 0; k--) {
+        int64_t w = 1ll << k;
+        if (c - w + 1 >= lbc && sparse[(int64_t)k * nch + c] < x) c -= w;
+    }
+    int32_t res = -1;
+    if (c >= lbc && sparse[c] >= x) {
+        const int32_t *stk = cstack + c * CHUNK;
+        int n = csp[c];
+        // topmost stack entry with end >= x (ends non-increasing bottom -> top)
+        int l = 0, h = n;
+        while (l < h) {
+            int m = (l + h) >> 1;
+            if (Pe[stk[m]] >= x) l = m + 1; else h = m;
+        }
+        if (l > 0) res = stk[l - 1];
+    }
+    parent[q] = res;
+}
+
+// laminarity: no span strictly between parent(q) and q (push order) ends after start(q)
+__global__ void k_laminar(const int64_t *__restrict__ Ps, const int64_t *__restrict__ Pe,
+                          const int32_t *__restrict__ Plist, const int32_t *__restrict__ parent, int64_t S,
+                          const int64_t *__restrict__ list_beg, int n_lists, int32_t *__restrict__ flags) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= S) return;
+    int list = Plist[q];
+    if (list >= n_lists) return;
+    int64_t lb = list_beg[list];
+    int64_t p = parent[q] >= 0 ? parent[q] : lb - 1;
+    int64_t sq = Ps[q];
+    int64_t j = q - 1;
+    int steps = 0;
+    while (j > p) {
+        if (Pe[j] > sq || ++steps > 64) { flags[list] = 1; return; }
+        int32_t pj = parent[j];
+        j = pj >= 0 ? pj : lb - 1;
+    }
+}
+
+// exact sequential sweep for a non-laminar (gpu, level) list: active set in push order
+__global__ void k_attr_sweep(const int *__restrict__ lists, int n_sweep, const int64_t *__restrict__ list_beg,
+                             const int64_t *__restrict__ Ps, const int64_t *__restrict__ Pe,
+                             const int64_t *__restrict__ gbeg, const int64_t *__restrict__ tl, int64_t N,
+                             int32_t *__restrict__ attr_pre, DevReport *rep) {
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= n_sweep) return;
+    int list = lists[w];
+    int lg = list / 4, lv = list % 4;
+    int64_t lb = list_beg[list], le = list_beg[list + 1];
+    int64_t act[SWEEP_MAX_ACTIVE];
+    int na = 0;
+    int64_t nxt = lb;
+    for (int64_t i = gbeg[lg]; i < gbeg[lg + 1]; i++) {
+        int64_t t = tl[i];
+        while (nxt < le && Ps[nxt] <= t) {
+            if (na == SWEEP_MAX_ACTIVE) { latch(rep, CHOPPER_E_RANGE); break; }
+            act[na++] = nxt++;
+        }
+        int k = 0;
+        for (int a = 0; a < na; a++) if (Pe[act[a]] > t) act[k++] = act[a];
+        na = k;
+        int32_t r = -1;
+        if (na > 0) {
+            bool chain = true;
+            for (int a = 1; a < na; a++) if (Pe[act[a]] > Pe[act[a - 1]]) chain = false;
+            if (chain) r = (int32_t)act[na - 1];
+            else { r = -2; latch(rep, CHOPPER_E_AMBIGUOUS_SPANS); }
+        }
+        attr_pre[(int64_t)lv * N + i] = r;
+    }
+}
+
+__global__ void k_attr_out(SpanView v, const int64_t *__restrict__ tl, const uint32_t *__restrict__ meta, int64_t N,
+                           const int32_t *__restrict__ gpu_lg, const int32_t *__restrict__ Po,
+                           int32_t *__restrict__ out) {
+    // blocked: each thread handles 8 consecutive events so the seeded search walks forward
+    int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    int64_t cur[4] = {-2, -2, -2, -2};
+    int lgp = -1;
+    for (int k = 0; k < 8; k++) {
+        int64_t i = base + k;
+        if (i >= N) break;
+        int lg = gpu_lg[gpu_of(meta[i])];
+        if (lg != lgp) { cur[0] = cur[1] = cur[2] = cur[3] = -2; lgp = lg; }
+        int64_t t = tl[i];
+#pragma unroll
+        for (int lv = 0; lv < 4; lv++) {
+            int64_t c = span_lookup(v, lg, lv, t, i, &cur[lv]);
+            out[(int64_t)lv * N + i] = c >= 0 ? Po[c] : (int32_t)c;
+        }
+    }
+}
+}  // namespace
+
+chopper_status ch_build_spans(chopper_ctx *ctx) {
+    const int64_t S = ctx->S;
+    const int n_lg = ctx->n_lg;
+    const int n_lists = n_lg * 4;
+    CH_ALLOC_BEGIN;
+    ctx->d_list_beg = CH_ALLOC(ctx, int64_t, n_lists + 2);
+    ctx->d_list_flags = CH_ALLOC(ctx, int32_t, n_lists + 1);
+    ctx->P_start = CH_ALLOC(ctx, int64_t, S);
+    ctx->P_end = CH_ALLOC(ctx, int64_t, S);
+    ctx->P_orig = CH_ALLOC(ctx, int32_t, S);
+    ctx->P_label = CH_ALLOC(ctx, int32_t, S);
+    ctx->P_parent = CH_ALLOC(ctx, int32_t, S);
+    int32_t *Plist = CH_ALLOC(ctx, int32_t, S);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemsetAsync(ctx->d_list_flags, 0, sizeof(int32_t) * (n_lists + 1), ctx->st));
+    ctx->list_beg.assign(n_lists + 2, 0);
+    ctx->S_loc = 0;
+    if (S > 0) {
+        int64_t smin = dec_i64(ctx->h_rep.s_min_enc), emax = dec_i64(ctx->h_rep.s_max_enc);
+        if (ctx->h_rep.s_min_enc == ~0ull) { smin = 0; emax = 0; }
+        int rbits = bits_for((uint64_t)(emax - smin));
+        int lbits = bits_for((uint64_t)n_lists);
+        if (rbits + lbits > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "span sort key exceeds 64 bits");
+        size_t mark = ctx->used;
+        unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, S), *k2 = CH_ALLOC(ctx, unsigned long long, S);
+        uint32_t *v1 = CH_ALLOC(ctx, uint32_t, S), *v2 = CH_ALLOC(ctx, uint32_t, S);
+        unsigned long long *lb = CH_ALLOC(ctx, unsigned long long, n_lists + 1);
+        CH_ALLOC_END(ctx);
+        unsigned g = (unsigned)ceil_div(S, NT);
+        k_span_key1<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, S, emax, k1, v1);
+        CH_LAUNCHED(ctx);
+        bool alt;
+        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, S, 0, rbits, &alt));
+        uint32_t *vs = alt ? v2 : v1;
+        unsigned long long *ks = alt ? k2 : k1, *ko = alt ? k1 : k2;
+        uint32_t *vo = alt ? v1 : v2;
+        k_span_key2<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, vs, S, ctx->d_gpu_lg,
+                                           n_lg, smin, rbits, ks);
+        CH_LAUNCHED(ctx);
+        CH_TRY(ch_radix_sort(ctx, ks, vs, ko, vo, S, 0, rbits + lbits, &alt));
+        uint32_t *order = alt ? vo : vs;
+        CH_TRY(ch_fill_u64(ctx, lb, n_lists + 1, ~0ull));
+        k_span_gather<<<g, NT, 0, ctx->st>>>(order, ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, ctx->sp.label,
+                                             S, ctx->d_gpu_lg, n_lg, ctx->P_start, ctx->P_end, ctx->P_orig,
+                                             ctx->P_label, Plist, lb);
+        CH_LAUNCHED(ctx);
+        std::vector<unsigned long long> hb(n_lists + 1);
+        CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), lb, 8 * (n_lists + 1), cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        ctx->used = mark;
+        ctx->list_beg[n_lists + 1] = S;
+        for (int l = n_lists; l >= 0; l--) ctx->list_beg[l] = hb[l] == ~0ull ? ctx->list_beg[l + 1] : (int64_t)hb[l];
+        ctx->S_loc = ctx->list_beg[n_lists];
+    }
+    CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_list_beg, ctx->list_beg.data(), 8 * (n_lists + 2), cudaMemcpyHostToDevice,
+                                 ctx->st));
+    // key bit widths: component = rank + 1 in [0, list size]; never all-ones
+    int64_t mx[4] = {0, 0, 0, 0};
+    for (int l = 0; l < n_lists; l++) mx[l % 4] = std::max(mx[l % 4], ctx->list_beg[l + 1] - ctx->list_beg[l]);
+    ctx->kg = bits_for((uint64_t)n_lg);
+    int tot = ctx->kg;
+    for (int lv = 0; lv < 4; lv++) { ctx->kb[lv] = bits_for((uint64_t)mx[lv] + 1); tot += ctx->kb[lv]; }
+    if (tot > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "instance key exceeds 64 bits");
+
+    const int64_t SL = ctx->S_loc;
+    ctx->list_flags.assign(n_lists, 0);
+    if (SL > 0) {
+        int64_t nch = ceil_div(SL, CHUNK);
+        int levels = 1;
+        while ((1ll << levels) < nch) levels++;
+        size_t mark = ctx->used;
+        int32_t *cstack = CH_ALLOC(ctx, int32_t, nch * CHUNK);
+        int32_t *csp = CH_ALLOC(ctx, int32_t, nch);
+        int64_t *sparse = CH_ALLOC(ctx, int64_t, (int64_t)levels * nch);
+        CH_ALLOC_END(ctx);
+        k_chunk_stack<<<(unsigned)ceil_div(nch, 32), 32, 0, ctx->st>>>(ctx->P_end, Plist, SL, ctx->P_parent, cstack, csp,
+                                                                      sparse, ctx->d_list_beg);
+        CH_LAUNCHED(ctx);
+        for (int k = 1; k < levels; k++) {
+            k_sparse_level<<<(unsigned)ceil_div(nch, NT), NT, 0, ctx->st>>>(sparse + (int64_t)(k - 1) * nch,
+                                                                            sparse + (int64_t)k * nch, nch, 1ll << (k - 1));
+            CH_LAUNCHED(ctx);
+        }
+        unsigned g = (unsigned)ceil_div(SL, NT);
+        k_resolve<<<g, NT, 0, ctx->st>>>(ctx->P_end, Plist, SL, ctx->P_parent, cstack, csp, sparse, levels, nch,
+                                         ctx->d_list_beg);
+        CH_LAUNCHED(ctx);
+        k_laminar<<<g, NT, 0, ctx->st>>>(ctx->P_start, ctx->P_end, Plist, ctx->P_parent, SL, ctx->d_list_beg, n_lists,
+                                         ctx->d_list_flags);
+        CH_LAUNCHED(ctx);
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->list_flags.data(), ctx->d_list_flags, 4 * n_lists, cudaMemcpyDeviceToHost,
+                                     ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        ctx->used = mark;
+    }
+    // exact sweep for non-laminar lists
+    std::vector<int> sweep;
+    for (int l = 0; l < n_lists; l++) if (ctx->list_flags[l]) sweep.push_back(l);
+    ctx->rep.non_laminar_lists = (int32_t)sweep.size();
+    ctx->d_attr_pre = nullptr;
+    if (!sweep.empty()) {
+        ctx->d_attr_pre = CH_ALLOC(ctx, int32_t, 4 * ctx->N);
+        int *dl = CH_ALLOC(ctx, int, (int64_t)sweep.size());
+        int64_t *dg = CH_ALLOC(ctx, int64_t, n_lg + 1);
+        CH_ALLOC_END(ctx);
+        CH_CUDA(ctx, cudaMemcpyAsync(dl, sweep.data(), 4 * sweep.size(), cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(dg, ctx->g_beg, 8 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
+        k_attr_sweep<<<(unsigned)ceil_div((int64_t)sweep.size(), 32), 32, 0, ctx->st>>>(
+            dl, (int)sweep.size(), ctx->d_list_beg, ctx->P_start, ctx->P_end, dg, ctx->ev.dispatch_ns, ctx->N,
+            ctx->d_attr_pre, ctx->d_rep);
+        CH_LAUNCHED(ctx);
+    }
+    return CHOPPER_OK;
+}
+
+SpanView ch_span_view(chopper_ctx *ctx) {
+    SpanView v;
+    v.P_start = ctx->P_start;
+    v.P_end = ctx->P_end;
+    v.P_parent = ctx->P_parent;
+    v.list_beg = ctx->d_list_beg;
+    v.list_flags = ctx->d_list_flags;
+    v.attr_pre = ctx->d_attr_pre;
+    v.N = ctx->N;
+    return v;
+}
+
+chopper_status ch_attr_pass(chopper_ctx *ctx, int32_t *span_idx) {
+    if (!span_idx || ctx->N == 0) return CHOPPER_OK;
+    int64_t threads = ceil_div(ctx->N, 8);
+    k_attr_out<<<(unsigned)ceil_div(threads, NT), NT, 0, ctx->st>>>(ch_span_view(ctx), ctx->ev.dispatch_ns, ctx->ev.meta,
+                                                                    ctx->N, ctx->d_gpu_lg, ctx->P_orig, span_idx);
+    CH_LAUNCHED(ctx);
+    return CHOPPER_OK;
+}

@@ -1,0 +1,230 @@
+"""Pipeline driver over the C ABI: upload columns into torch CUDA tensors, run
+chopper_load_columns -> align -> attribute -> overlap -> breakdown ->
+reduce_ranks, and read results back.  Marshalling only -- no analysis here.
+
+flops_table() is the host-side Eq. 4 parameter table (theoretical FLOPs of an
+op label from the workload shapes, D19).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Dict, Optional
+
+import numpy as np
+
+from . import (chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
+               chopper_create, chopper_destroy, chopper_events, chopper_get_report, chopper_global,
+               chopper_kernel_launches, chopper_load_columns, chopper_overlap, chopper_reduce_ranks,
+               chopper_samples, chopper_scratch_bytes, chopper_spans, chopper_status_sync, chopper_tables,
+               _check, bd_params, dev_to_numpy, load_library, rows_to_numpy)
+
+_GEMM = {"qkv_ip", "attn_op", "mlp_gp", "mlp_up", "mlp_dp", "lp"}
+
+
+def flops_table(labels, shapes: Dict[str, int], bwd_gemm: float = 2.0, bwd_fa: float = 2.5) -> np.ndarray:
+    """F_gemm per op label (Eq. 4): GEMM m x n x k -> 2mnk; attention -> 4*b*h*s^2*d; per-layer ops are
+    summed over the layers because a point sums an op across layers."""
+    b, s, H, F = shapes["b"], shapes["s"], shapes["hidden"], shapes["ffn"]
+    h, kvh, d, V, L = shapes["heads"], shapes["kv_heads"], shapes["head_dim"], shapes["vocab"], shapes["layers"]
+    tok = b * s
+    shape = {"qkv_ip": (tok, H + 2 * kvh * d, H), "attn_op": (tok, H, H), "mlp_gp": (tok, F, H),
+             "mlp_up": (tok, F, H), "mlp_dp": (tok, H, F), "lp": (tok, V, H)}
+    out = np.zeros(len(labels))
+    for i, lab in enumerate(labels):
+        pre, base = (lab[:2], lab[2:]) if lab[:2] in ("f_", "b_") else ("", lab)
+        if base in shape:
+            m, n, k = shape[base]
+            v = 2.0 * m * n * k
+            mult = bwd_gemm
+        elif base == "attn_fa":
+            v = 4.0 * b * h * s * s * d
+            mult = bwd_fa
+        else:
+            continue
+        if base != "lp":
+            v *= L
+        out[i] = v * (mult if pre == "b_" else 1.0)
+    return out
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+class Pipeline:
+    """One rank's chopper context.  `cols` is any object with the column attributes of the ABI
+    (t_l, t_ks, t_ke, meta, name_id, span_*, smp_*, passes)."""
+
+    def __init__(self, n_traced_gpus: int, n_labels: int, max_iters: int, max_coll_per_class: int,
+                 device: int = 0, pg=None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2512_08242_b200 needs a CUDA device (no CPU fallback)")
+        load_library()
+        self.torch = torch
+        self.device = device
+        self.cfg = chopper_config(n_traced_gpus=n_traced_gpus, n_labels=n_labels, max_iters=max_iters,
+                                  max_coll_per_class=max_coll_per_class)
+        self.stream = stream or torch.cuda.current_stream(device)
+        self.pg = pg
+        self.rank, self.nranks = 0, 1
+        self.comm = 0
+        if pg is not None:
+            import torch.distributed as dist
+            self.rank, self.nranks = dist.get_rank(pg), dist.get_world_size(pg)
+            if self.nranks > 1:
+                be = pg._get_backend(torch.device("cuda", device))
+                self.comm = int(be._comm_ptr())
+        self.ctx = None
+        self.scratch = None
+        self.d = {}
+
+    # ---- inputs ----
+    def upload(self, cols, n_counters: int, pinned_host: Optional[dict] = None) -> None:
+        """Copy input columns to the device (from pinned host tensors if given)."""
+        torch = self.torch
+        dev = torch.device("cuda", self.device)
+        src = {
+            "t_l": _i64(cols.t_l), "t_ks": _i64(cols.t_ks), "t_ke": _i64(cols.t_ke),
+            "meta": np.ascontiguousarray(cols.meta, np.uint32).view(np.int32),
+            "name_id": np.ascontiguousarray(cols.name_id, np.int32),
+            "span_gl": np.ascontiguousarray(cols.span_gl, np.uint32).view(np.int32),
+            "span_start": _i64(cols.span_start), "span_end": _i64(cols.span_end),
+            "span_label": np.ascontiguousarray(cols.span_label, np.int32),
+            "smp_gpu": np.ascontiguousarray(cols.smp_gpu, np.int32), "smp_ts": _i64(cols.smp_ts),
+            "smp_freq": np.ascontiguousarray(cols.smp_freq, np.int32),
+            "smp_power": np.ascontiguousarray(cols.smp_power, np.int32),
+        }
+        d = {}
+        with torch.cuda.stream(self.stream):
+            for k, v in src.items():
+                if pinned_host is not None and k in pinned_host:
+                    d[k] = pinned_host[k].to(dev, non_blocking=True)
+                else:
+                    d[k] = torch.from_numpy(v).to(dev, non_blocking=False)
+            self.passes_dev = []
+            for (g, names, slots, vals) in cols.passes:
+                self.passes_dev.append((int(g), torch.from_numpy(np.ascontiguousarray(names, np.int32)).to(dev),
+                                        np.ascontiguousarray(slots, np.int32),
+                                        torch.from_numpy(np.ascontiguousarray(vals, np.float64)).to(dev)))
+        self.d = d
+        self.n_counters = n_counters
+        self.N, self.S, self.M = len(src["t_l"]), len(src["span_gl"]), len(src["smp_gpu"])
+        need = chopper_scratch_bytes(self.cfg, self.N, self.S, self.M, n_counters)
+        if self.scratch is None or self.scratch.numel() < need:
+            self.scratch = None
+            if self.ctx:
+                chopper_destroy(self.ctx)
+                self.ctx = None
+            self.scratch = torch.empty(need, dtype=torch.uint8, device=dev)
+        if self.ctx is None:
+            self.ctx = chopper_create(self.cfg, self.device, self.stream.cuda_stream, self.comm, self.rank,
+                                      self.nranks, self.scratch)
+
+    # ---- run ----
+    def run(self, params: dict, full: bool = False, check: bool = True) -> dict:
+        """All six ABI calls.  full=True also writes the per-event outputs (parity mode)."""
+        torch = self.torch
+        d, N = self.d, self.N
+        ev = chopper_events(n=N, dispatch_ns=d["t_l"].data_ptr(), start_ns=d["t_ks"].data_ptr(),
+                            end_ns=d["t_ke"].data_ptr(), meta=d["meta"].data_ptr(), name_id=d["name_id"].data_ptr())
+        sp = chopper_spans(n=self.S, gpu_level=d["span_gl"].data_ptr(), start_ns=d["span_start"].data_ptr(),
+                           end_ns=d["span_end"].data_ptr(), label=d["span_label"].data_ptr())
+        smp = chopper_samples(n=self.M, gpu=d["smp_gpu"].data_ptr(), ts_ns=d["smp_ts"].data_ptr(),
+                              freq_mhz=d["smp_freq"].data_ptr(), power_mw=d["smp_power"].data_ptr()) \
+            if self.M > 0 else None
+        res = {"full": full}
+        allow = () if check else tuple(range(1, 10))
+        s = chopper_load_columns(self.ctx, ev, sp, smp)
+        res["load_status"] = s
+        res["report"] = chopper_get_report(self.ctx)
+        if s != 0:
+            _check(self.ctx, s, "chopper_load_columns", allow=allow)
+            return res
+        C = self.n_counters
+        passes = []
+        self._slot_keep = []
+        for (g, names, slots, vals) in self.passes_dev:
+            self._slot_keep.append(slots)
+            passes.append(chopper_counter_pass(gpu=g, n=names.numel(), name_id=names.data_ptr(), k=len(slots),
+                                               slot=slots.ctypes.data, values=vals.data_ptr()))
+        dev = torch.device("cuda", self.device)
+        out = {}
+        if full:
+            out["counters"] = torch.zeros((max(C, 1), max(N, 1)), dtype=torch.float64, device=dev)
+            out["span_idx"] = torch.empty((4, max(N, 1)), dtype=torch.int32, device=dev)
+            for k in ("ovl", "prep", "call", "phi", "psi"):
+                out[k] = torch.empty(max(N, 1), dtype=torch.int64, device=dev)
+        offs = np.zeros(self.cfg.n_traced_gpus, dtype=np.int64)
+        _check(self.ctx, chopper_align(self.ctx, passes, C, out.get("counters") if C else None, offs), "chopper_align")
+        _check(self.ctx, chopper_attribute(self.ctx, out.get("span_idx")), "chopper_attribute")
+        _check(self.ctx, chopper_overlap(self.ctx, out.get("ovl"), out.get("prep"), out.get("call"), out.get("phi"),
+                                         out.get("psi")), "chopper_overlap")
+        self._bd = bd_params(params)
+        tabs = chopper_tables()
+        _check(self.ctx, chopper_breakdown(self.ctx, self._bd, tabs), "chopper_breakdown")
+        glob = chopper_global()
+        _check(self.ctx, chopper_reduce_ranks(self.ctx, glob), "chopper_reduce_ranks")
+        st, mask = chopper_status_sync(self.ctx)
+        res.update(status=st, mask=mask, offsets=offs, tables=tabs, glob=glob, out=out)
+        return res
+
+    def to_numpy(self, res: dict, n_ratios: int = 0) -> Dict[str, np.ndarray]:
+        """Results in the oracle's naming (tests compare these element by element)."""
+        o: Dict[str, np.ndarray] = {}
+        N, C = self.N, self.n_counters
+        if res.get("full"):
+            out = res["out"]
+            o["ev.span_idx"] = out["span_idx"][:, :N].reshape(-1).cpu().numpy()
+            for k in ("ovl", "prep", "call", "phi", "psi"):
+                o["ev." + k] = out[k][:N].cpu().numpy()
+            o["ev.counters"] = out["counters"][:C, :N].reshape(-1).cpu().numpy() if C else np.zeros(0)
+        tabs = res["tables"]
+        for name, attr in (("inst", "inst"), ("layer", "layer"), ("phase", "phase"), ("iter", "iter"), ("gpu", "gpu"),
+                           ("point", "point")):
+            r = rows_to_numpy(getattr(tabs, attr), C, n_ratios)
+            for k, v in r.items():
+                key = {"n_compute": "n", "step": "step"}.get(k, k)
+                if k == "counters":
+                    o[f"{name}.counters"] = v.reshape(-1)
+                elif k == "rates":
+                    o[f"{name}.rates"] = v.reshape(-1)
+                else:
+                    o[f"{name}.{key}"] = v
+        nbd = int(tabs.n_bd)
+        o["bd.local"] = dev_to_numpy(tabs.bd, nbd * 16, np.float64)
+        g = res["glob"]
+        n = int(g.n_iters)
+        o["glob.step"] = np.array(g.step[:n], np.int32)
+        o["glob.complete"] = np.array(g.complete[:n], np.int32)
+        o["glob.sampled"] = np.array(g.sampled[:n], np.int32)
+        o["glob.T"] = np.array(g.T[:n], np.int64)
+        o["glob.aligned_first"] = np.array(g.aligned_first[:n], np.int64)
+        o["glob.aligned_last"] = np.array(g.aligned_last[:n], np.int64)
+        o["glob.throughput"] = np.array(g.throughput[:n], np.float64)
+        o["glob.throughput_median"] = np.array([g.throughput_median])
+        o["bd.rows"] = np.array(g.bd[:int(g.n_bd) * 16], np.float64)
+        G = self.cfg.n_traced_gpus
+        o["gpu.delta"] = np.array(g.delta[:G], np.int64)
+        o["gpu.delta_flag"] = np.array(g.delta_flag[:G], np.int32)
+        o["skew.max_ag"] = np.array([g.max_skew_ag])
+        o["skew.max_rs"] = np.array([g.max_skew_rs])
+        rep = res["report"]
+        o["val.count"] = np.array(rep.val_count[:], np.int64)
+        o["val.first"] = np.array(rep.val_first[:], np.int64)
+        o["status_mask"] = np.array([res.get("mask", 0)], np.int64)
+        return o
+
+    def launches(self) -> int:
+        return chopper_kernel_launches(self.ctx) if self.ctx else 0
+
+    def close(self):
+        if self.ctx:
+            chopper_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,278 @@
+"""GPU parity: the CUDA path through the C ABI vs the oracle, element by element.
+
+Integer outputs (span indices, overlap, launch components, DVFS integrals,
+every integer table column, clock offsets, iteration joins) must be bit-exact;
+fp64 counter sums, rates and breakdown factors within 1e-9 relative
+(BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+import oracle
+import tracegen
+from parity import assert_parity, run_both
+from tinytrace import AG, COMPUTE, COPY, MEMOP, OTHER, RS, TinyTrace, params
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_08242_b200 as ch
+    ch.build()
+    ch.load_library()
+
+
+def _check_status(ref, got):
+    assert int(ref["status"][0]) == int(got["status_mask"][0]), (ref["status"], got["status_mask"])
+
+
+def test_config1_toy_full():
+    b = tracegen.generate(tracegen.config(1))
+    ref, got, res, pipe = run_both(b)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+    np.testing.assert_array_equal(ref["val.count"], got["val.count"])
+
+
+def test_small_counters_samples_full():
+    cfg = tracegen.config(3)
+    cfg.n_iters, cfg.n_layers, cfg.n_gpus, cfg.opt_kernels, cfg.warmup = 3, 4, 3, 600, 1
+    b = tracegen.generate(cfg)
+    ref, got, res, pipe = run_both(b)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+
+
+def test_config2_llama_full():
+    """BASELINE configs[1]: Llama 3 8B FSDP-shaped, 8 GPUs x 10 iterations (~0.9M events)."""
+    b = tracegen.generate(tracegen.config(2))
+    ref, got, res, pipe = run_both(b)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+
+
+@pytest.mark.slow
+def test_config3_counters_dvfs_full():
+    """BASELINE configs[2]: 20 counters per kernel + 1 ms frequency / power samples."""
+    b = tracegen.generate(tracegen.config(3))
+    ref, got, res, pipe = run_both(b)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+
+
+@pytest.mark.slow
+def test_config4_long_run_full():
+    """BASELINE configs[3] at full size (~17.6M events, 8 counters, samples): the bench workload, same launch path."""
+    b = tracegen.generate(tracegen.config(4))
+    ref, got, res, pipe = run_both(b, max_iters=256)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+
+
+def test_tables_only_mode_matches_full():
+    """per-event outputs NULL (the bench path) gives the same tables as full mode."""
+    import paper_2512_08242_b200 as ch
+    b = tracegen.generate(tracegen.config(1))
+    p = oracle.default_params(b)
+    pipe = ch.Pipeline(b.cfg.n_gpus, len(b.labels), 16, 4096)
+    pipe.upload(b, b.n_counters)
+    full = pipe.to_numpy(pipe.run(p, full=True), len(p["ratio_num"]))
+    lean = pipe.to_numpy(pipe.run(p, full=False), len(p["ratio_num"]))
+    for k in lean:
+        if k.startswith("ev."):
+            continue
+        np.testing.assert_array_equal(np.nan_to_num(full[k]), np.nan_to_num(lean[k]), err_msg=k)
+
+
+# ---------------------------------------------------------------------------
+# edge cases
+# ---------------------------------------------------------------------------
+def _tiny(tt, **kw):
+    b = tt.bundle()
+    p = params(b, **kw)
+    return run_both(b, p)
+
+
+def test_no_spans_all_unannotated():
+    tt = TinyTrace().ev(0, 0, 10, 20).ev(0, 1, 25, 40).ev(0, 2, 5, 50, kind=AG, stream=1)
+    ref, got, _, _ = _tiny(tt)
+    assert_parity(ref, got)
+    assert len(got["inst.gpu"]) == 0
+
+
+def test_single_event():
+    tt = TinyTrace().span(0, 0, 0, 100, 3).span(0, 3, 0, 100, 1).ev(0, 5, 10, 20)
+    ref, got, _, _ = _tiny(tt)
+    assert_parity(ref, got)
+
+
+def test_crossing_spans_ambiguous_sweep_path():
+    """crossing op spans: exact device sweep path; dispatch in the crossing region -> -2 + E_AMBIGUOUS_SPANS."""
+    tt = TinyTrace().span(0, 0, 0, 1000, 7).span(0, 3, 100, 200, 0).span(0, 3, 150, 250, 1)
+    for t in (50, 120, 160, 220, 300):
+        tt.ev(0, t, t + 1, t + 2)
+    ref, got, res, pipe = _tiny(tt)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+    assert res["report"].non_laminar_lists == 1
+
+
+def test_crossing_without_dispatch_is_harmless():
+    tt = TinyTrace().span(0, 0, 0, 1000, 7).span(0, 3, 100, 200, 0).span(0, 3, 150, 250, 1)
+    for t in (50, 120, 220, 300):
+        tt.ev(0, t, t + 1, t + 2)
+    ref, got, _, _ = _tiny(tt)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+
+
+def test_deep_nesting_and_identical_spans():
+    tt = TinyTrace().span(0, 0, 0, 10_000, 1)
+    # depth-8 nest of op spans, identical duplicates, zero-length spans, siblings
+    for d in range(8):
+        tt.span(0, 3, 100 * d, 9000 - 100 * d, d % 4)
+    tt.span(0, 3, 300, 8700, 2)                         # identical to the depth-3 span
+    tt.span(0, 3, 5000, 5000, 1)                        # zero length: never contains anything
+    for s in range(1000, 8000, 700):
+        tt.span(0, 3, s, s + 300, 3)
+    for t in range(0, 10_000, 97):
+        tt.ev(0, t, t + 10, t + 50)
+    ref, got, res, _ = _tiny(tt)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+    assert res["report"].non_laminar_lists == 0
+
+
+def test_multi_stream_compute_and_comm_order():
+    """two compute streams (compute union built explicitly) and comm events whose start order
+    differs from dispatch order (full radix sort path)."""
+    tt = TinyTrace(n_gpus=2).span(0, 0, 0, 10 ** 6, 1).span(1, 0, 0, 10 ** 6, 1)
+    for g in range(2):
+        t = 0
+        for k in range(60):
+            tt.ev(g, 10 * k, 100 + 37 * k, 100 + 37 * k + 30, stream=k % 2)
+        tt.ev(g, 5, 3000, 3500, kind=AG, stream=2)
+        tt.ev(g, 6, 1000, 1200, kind=RS, stream=3)          # dispatched later, starts earlier
+        tt.ev(g, 7, 900, 950, kind=AG, stream=2)
+        del t
+    b = tt.bundle()
+    ref, got, res, _ = run_both(b, params(b))
+    _check_status(ref, got)
+    assert_parity(ref, got)
+    assert res["report"].full_sort_used == 1
+
+
+def test_same_stream_overlap_is_data():
+    tt = TinyTrace().span(0, 0, 0, 1000, 1).ev(0, 0, 10, 50).ev(0, 1, 40, 80).ev(0, 2, 30, 90, kind=AG, stream=1)
+    ref, got, _, _ = _tiny(tt)
+    _check_status(ref, got)
+    np.testing.assert_array_equal(ref["val.count"], got["val.count"])
+    np.testing.assert_array_equal(ref["val.first"], got["val.first"])
+    assert_parity(ref, got)
+
+
+@pytest.mark.parametrize("case", ["start_after_end", "not_grouped", "dispatch_dec", "bad_meta", "span_bad"])
+def test_fatal_validation(case):
+    import paper_2512_08242_b200 as ch
+    tt = TinyTrace(n_gpus=2)
+    keep = False
+    if case == "start_after_end":
+        tt.ev(0, 0, 10, 5).ev(0, 1, 20, 30)
+    elif case == "not_grouped":
+        tt.ev(1, 0, 10, 15).ev(0, 1, 20, 30); keep = True
+    elif case == "dispatch_dec":
+        tt.ev(0, 5, 10, 15).ev(0, 1, 20, 30); keep = True
+    elif case == "bad_meta":
+        tt.ev(0, 0, 10, 15).ev(0, 1, 20, 30, kind=9)
+    elif case == "span_bad":
+        tt.ev(0, 0, 10, 15).span(0, 0, 10, 5)
+    b = tt.bundle(keep_order=keep)
+    p = params(b)
+    ref = oracle.run(b, p)
+    pipe = ch.Pipeline(2, len(b.labels), 8, 16)
+    pipe.upload(b, 0)
+    res = pipe.run(p, check=False)
+    assert res["load_status"] == 1
+    rep = res["report"]
+    np.testing.assert_array_equal(ref["val.count"], np.array(rep.val_count[:]))
+    np.testing.assert_array_equal(ref["val.first"], np.array(rep.val_first[:]))
+
+
+def test_counter_alignment_mismatch_and_conflict():
+    tt = TinyTrace(n_counters=2).span(0, 0, 0, 1000, 1).span(0, 3, 0, 1000, 0)
+    names = [1, 2, 1]
+    for k, nm in enumerate(names):
+        tt.ev(0, 10 * k, 10 * k + 1, 10 * k + 5, name=nm)
+    tt.ev(0, 100, 101, 102, kind=MEMOP, stream=3, name=9)
+    tt.counter_pass(0, names, [0], [[1, 2, 3]]).counter_pass(0, [1, 1], [1], [[5, 6]])
+    tt.counter_pass(0, names, [0], [[1, 2.5, 3]])
+    b = tt.bundle()
+    p = params(b, slot_unum=-1, slot_uden=-1)
+    ref, got, res, pipe = run_both(b, p)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+    import paper_2512_08242_b200 as ch
+    lib = ch.load_library()
+    for q in range(3):
+        assert lib.chopper_pass_mismatch(pipe.ctx, q) == ref["pass.mismatch"][q]
+        assert lib.chopper_pass_conflict(pipe.ctx, q) == ref["pass.conflict"][q]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_traces(seed):
+    """random multi-gpu traces with nested / crossing spans, skewed dispatch, comm on two streams, copies,
+    memops, samples and counters."""
+    rng = np.random.default_rng(1000 + seed)
+    G = int(rng.integers(1, 4))
+    C = 4
+    tt = TinyTrace(n_gpus=G, n_counters=C, labels=["l%d" % i for i in range(6)])
+    for g in range(G):
+        T = 200_000
+        for it in range(3):
+            tt.span(g, 0, it * T, (it + 1) * T, 100 + it)
+            tt.span(g, 1, it * T, it * T + T // 2, 0).span(g, 1, it * T + T // 2, (it + 1) * T, 1)
+            for ly in range(3):
+                tt.span(g, 2, it * T + ly * 50_000, it * T + ly * 50_000 + 40_000, ly)
+        for _ in range(int(rng.integers(20, 60))):
+            s = int(rng.integers(0, 3 * T))
+            e = s + int(rng.integers(0, 30_000))
+            tt.span(g, 3, s, e, int(rng.integers(0, 6)))
+        t_dev = 0
+        t_host = 0
+        names = []
+        kinds = []
+        for k in range(int(rng.integers(200, 600))):
+            kind = int(rng.choice([COMPUTE] * 8 + [AG, RS, COPY, MEMOP, OTHER]))
+            d = int(rng.integers(0, 3000))
+            if kind == COMPUTE:
+                t_dev += int(rng.integers(0, 800))
+                ks = t_dev
+                t_dev += d
+                st = 0
+            else:
+                ks = int(rng.integers(0, 3 * T))
+                st = {AG: 1, RS: 2, COPY: 0, MEMOP: 3, OTHER: 4}[kind]
+                if kind == COPY:
+                    t_dev += int(rng.integers(0, 800)); ks = t_dev; t_dev += d
+            t_host += int(rng.integers(1, 1500))
+            tl = t_host if rng.random() > 0.05 else t_host
+            nm = int(rng.integers(0, 5))
+            tt.ev(g, tl, ks, ks + d, kind=kind, stream=st, name=nm)
+            if kind != MEMOP:
+                names.append(nm)
+            kinds.append(kind)
+        vals = rng.integers(0, 1000, size=(2, len(names))).astype(float)
+        tt.counter_pass(g, names, [0, 1], vals)
+        tt.counter_pass(g, names, [2, 3], np.vstack([rng.integers(1, 100, len(names)), rng.random(len(names)) + 1]))
+        ts = 0
+        while ts < 3 * T:
+            tt.sample(g, ts, int(rng.integers(1300, 2100)), int(rng.integers(500, 1000)))
+            ts += int(rng.integers(5_000, 20_000))
+    b = tt.bundle()
+    p = params(b, f_gemm=np.full(6, 1e9), op_type=np.array([1, 2, 0, 1, 1, 2], np.int32), warmup=1)
+    ref, got, res, _ = run_both(b, p)
+    _check_status(ref, got)
+    assert_parity(ref, got)
