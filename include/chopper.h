@@ -250,6 +250,14 @@ int32_t chopper_counter_present(const chopper_ctx *ctx, int32_t gpu, int32_t slo
 /* scratch bytes in use (high-water of the bump arena) */
 int64_t chopper_scratch_used(const chopper_ctx *ctx);
 
+/* Device timing of pipeline phases with CUDA events recorded on the ctx
+ * stream (off by default).  phase: 0 load, 1 align, 2 attribute,
+ * 3 overlap prep, 4 fused event pass kernel, 5 tables, 6 breakdown,
+ * 7 reduce_ranks.  chopper_phase_time returns 0 and *ms for the most recent
+ * run of that phase, CHOPPER_E_STATE if it was not timed. */
+void chopper_set_timing(chopper_ctx *ctx, int32_t on);
+chopper_status chopper_phase_time(chopper_ctx *ctx, int32_t phase, float *ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -126,7 +126,7 @@ EXPORTS = ["chopper_scratch_bytes", "chopper_create", "chopper_load_columns", "c
            "chopper_overlap", "chopper_breakdown", "chopper_reduce_ranks", "chopper_get_report",
            "chopper_status_sync", "chopper_last_error", "chopper_destroy", "chopper_kernel_launches",
            "chopper_abi_version", "chopper_pass_mismatch", "chopper_pass_conflict", "chopper_counter_present",
-           "chopper_scratch_used"]
+           "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time"]
 
 _lib = None
 
@@ -161,6 +161,8 @@ def load_library() -> ctypes.CDLL:
         "chopper_pass_conflict": (I64, [P, I32]),
         "chopper_counter_present": (I32, [P, I32, I32]),
         "chopper_scratch_used": (I64, [P]),
+        "chopper_set_timing": (None, [P, I32]),
+        "chopper_phase_time": (I32, [P, I32, ctypes.POINTER(ctypes.c_float)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -252,6 +254,19 @@ def chopper_destroy(ctx) -> None:
 
 def chopper_kernel_launches(ctx) -> int:
     return int(load_library().chopper_kernel_launches(ctx))
+
+
+def chopper_set_timing(ctx, on: bool) -> None:
+    load_library().chopper_set_timing(ctx, 1 if on else 0)
+
+
+PHASES = ["load", "align", "attribute", "overlap_prep", "event_pass", "tables", "breakdown", "reduce_ranks"]
+
+
+def chopper_phase_time(ctx, phase: int) -> Optional[float]:
+    ms = ctypes.c_float()
+    s = load_library().chopper_phase_time(ctx, phase, ctypes.byref(ms))
+    return float(ms.value) if s == 0 else None
 
 
 # ---------------------------------------------------------------------------

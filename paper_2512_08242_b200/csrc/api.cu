@@ -82,8 +82,10 @@ chopper_status chopper_load_columns(chopper_ctx *ctx, const chopper_events *ev, 
     ctx->err.clear();
     memset(&ctx->rep, 0, sizeof(ctx->rep));
     if (cudaSetDevice(ctx->device) != cudaSuccess) return ch_fail(ctx, CHOPPER_E_CUDA, "cudaSetDevice");
+    ch_tick(ctx, 0, 0);
     chopper_status s = ch_load(ctx);
     if (s != CHOPPER_OK) return s;
+    ch_tick(ctx, 0, 1);
     ctx->stage = 1;
     return CHOPPER_OK;
 }
@@ -94,8 +96,10 @@ chopper_status chopper_align(chopper_ctx *ctx, const chopper_counter_pass *passe
     if (ctx->stage != 1 || !ctx->loaded_ok) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_align before load");
     if (n_passes < 0 || n_counters < 0 || (n_passes > 0 && !passes))
         return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "bad counter passes");
+    ch_tick(ctx, 1, 0);
     CH_TRY(ch_align(ctx, passes, n_passes, n_counters, counters_out));
     CH_TRY(ch_offsets(ctx));
+    ch_tick(ctx, 1, 1);
     ctx->offsets_done = true;
     if (offsets_ns)
         for (int g = 0; g < ctx->cfg.n_traced_gpus; g++) offsets_ns[g] = ctx->delta[g];
@@ -113,8 +117,10 @@ chopper_status chopper_attribute(chopper_ctx *ctx, int32_t *span_idx) {
         ctx->stage = 2;
     }
     if (ctx->stage != 2) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_attribute out of order");
+    ch_tick(ctx, 2, 0);
     CH_TRY(ch_build_spans(ctx));
     CH_TRY(ch_attr_pass(ctx, span_idx));
+    ch_tick(ctx, 2, 1);
     ctx->stage = 3;
     return CHOPPER_OK;
 }
@@ -123,7 +129,9 @@ chopper_status chopper_overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_
                                int64_t *psi) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
     if (ctx->stage != 3) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_overlap out of order");
+    ch_tick(ctx, 3, 0);
     CH_TRY(ch_overlap_prep(ctx));
+    ch_tick(ctx, 3, 1);
     CH_TRY(ch_event_pass(ctx, ovl_ns, prep_ns, call_ns, phi, psi));
     ctx->stage = 4;
     return CHOPPER_OK;
@@ -196,8 +204,12 @@ chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, c
                                      ctx->st));
         CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     }
+    ch_tick(ctx, 5, 0);
     CH_TRY(ch_tables(ctx));
+    ch_tick(ctx, 5, 1);
+    ch_tick(ctx, 6, 0);
     CH_TRY(ch_breakdown_local(ctx));
+    ch_tick(ctx, 6, 1);
     memset(out, 0, sizeof(*out));
     fill_rows(out->inst, ctx->inst, false, ctx);
     fill_rows(out->layer, ctx->layer, false, ctx);
@@ -215,7 +227,9 @@ chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     if (!ctx || !out) return CHOPPER_E_INVALID_ARG;
     if (ctx->stage != 5) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_reduce_ranks out of order");
     memset(out, 0, sizeof(*out));
+    ch_tick(ctx, 7, 0);
     CH_TRY(ch_reduce_ranks(ctx, out));
+    ch_tick(ctx, 7, 1);
     ctx->stage = 6;
     return CHOPPER_OK;
 }
@@ -246,7 +260,13 @@ chopper_status chopper_status_sync(chopper_ctx *ctx, uint32_t *mask) {
 
 const char *chopper_last_error(const chopper_ctx *ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
-void chopper_destroy(chopper_ctx *ctx) { delete ctx; }
+void chopper_destroy(chopper_ctx *ctx) {
+    if (!ctx) return;
+    for (auto &p : ctx->tev)
+        for (auto &e : p)
+            if (e) cudaEventDestroy(e);
+    delete ctx;
+}
 
 int64_t chopper_kernel_launches(const chopper_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
@@ -263,5 +283,17 @@ int32_t chopper_counter_present(const chopper_ctx *ctx, int32_t gpu, int32_t slo
     return lg >= 0 && (size_t)lg * ctx->C + slot < ctx->present.size() ? ctx->present[(size_t)lg * ctx->C + slot] : 0;
 }
 int64_t chopper_scratch_used(const chopper_ctx *ctx) { return ctx ? (int64_t)ctx->used : 0; }
+
+void chopper_set_timing(chopper_ctx *ctx, int32_t on) {
+    if (ctx) ctx->timing = on != 0;
+}
+
+chopper_status chopper_phase_time(chopper_ctx *ctx, int32_t phase, float *ms) {
+    if (!ctx || !ms || phase < 0 || phase >= 8) return CHOPPER_E_INVALID_ARG;
+    if (!ctx->timed[phase]) return CHOPPER_E_STATE;
+    if (cudaEventSynchronize(ctx->tev[phase][1]) != cudaSuccess) return CHOPPER_E_CUDA;
+    if (cudaEventElapsedTime(ms, ctx->tev[phase][0], ctx->tev[phase][1]) != cudaSuccess) return CHOPPER_E_CUDA;
+    return CHOPPER_OK;
+}
 
 }  // extern "C"

@@ -177,6 +177,10 @@ struct chopper_ctx {
     double *d_ratio_scale = nullptr;
     int n_ratios = 0;
     int32_t *d_has_smp = nullptr;    // [n_lg]
+    // phase timing (chopper_set_timing)
+    bool timing = false;
+    cudaEvent_t tev[8][2] = {};
+    bool timed[8] = {};
     int64_t *d_dense = nullptr;      // local dense exchange blocks [dense_slots][W]
     int dense_slots = 0;
     bool offsets_done = false;
@@ -215,6 +219,12 @@ struct chopper_ctx {
     } while (0)
 
 chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &msg);
+inline void ch_tick(chopper_ctx *ctx, int phase, int end) {
+    if (!ctx->timing) return;
+    if (!ctx->tev[phase][end]) cudaEventCreate(&ctx->tev[phase][end]);
+    cudaEventRecord(ctx->tev[phase][end], ctx->st);
+    if (end) ctx->timed[phase] = true;
+}
 chopper_status ch_fill_u64(chopper_ctx *ctx, unsigned long long *p, int64_t n, unsigned long long v);
 
 // ---------------------------------------------------------------------------

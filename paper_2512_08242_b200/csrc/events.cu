@@ -620,8 +620,10 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         CH_CUDA(ctx, cudaFuncSetAttribute(k_events, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
         attr_set = true;
     }
+    ch_tick(ctx, 4, 0);
     k_events<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P);
     CH_LAUNCHED(ctx);
+    ch_tick(ctx, 4, 1);
     unsigned long long last = 0;
     CH_CUDA(ctx, cudaMemcpyAsync(&last, ctx->d_tile_state + ntile - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));

@@ -166,7 +166,8 @@ class Pipeline:
         glob = chopper_global()
         _check(self.ctx, chopper_reduce_ranks(self.ctx, glob), "chopper_reduce_ranks")
         st, mask = chopper_status_sync(self.ctx)
-        res.update(status=st, mask=mask, offsets=offs, tables=tabs, glob=glob, out=out)
+        res.update(status=st, mask=mask, offsets=offs, tables=tabs, glob=glob, out=out,
+                   report=chopper_get_report(self.ctx))
         return res
 
     def to_numpy(self, res: dict, n_ratios: int = 0) -> Dict[str, np.ndarray]:
