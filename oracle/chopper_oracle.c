@@ -450,7 +450,13 @@ or_result *or_run(const or_input *in) {
                 for (int64_t i = gbeg[g]; i < gend[g]; i++) {
                     if (kind_of(in->meta[i]) != K_COMPUTE) continue;
                     int64_t a = in->t_ks[i], b = in->t_ke[i], F = 0, P = 0;
-                    for (int64_t k = 0; k < K; k++) {  /* piece k: [lo, hi) with value sample k */
+                    /* pieces ending at or before a contribute nothing: start at the first piece with hi > a */
+                    int64_t kl = 0, kh = K - 1;
+                    while (kl < kh) {
+                        int64_t m = (kl + kh) / 2;
+                        if (in->smp_ts[k0 + m + 1] > a) kh = m; else kl = m + 1;
+                    }
+                    for (int64_t k = kl; k < K; k++) {  /* piece k: [lo, hi) with value sample k */
                         int64_t lo = (k == 0) ? INT64_MIN : in->smp_ts[k0 + k];
                         int64_t hi = (k == K - 1) ? INT64_MAX : in->smp_ts[k0 + k + 1];
                         int64_t x = i64max(a, lo), y = i64min(b, hi);
