@@ -53,11 +53,20 @@ __global__ void k_pass_check(const uint32_t *__restrict__ meta, const int32_t *_
     }
 }
 
-__global__ void k_pass_finite(const PassDesc *__restrict__ passes, int p, unsigned int *__restrict__ bad) {
+// non-finite values in any pass (blockIdx.y = pass): streaming read, 4 doubles per thread step
+__global__ void k_pass_finite(const PassDesc *__restrict__ passes, unsigned int *__restrict__ bad) {
+    const int p = blockIdx.y;
     const PassDesc d = passes[p];
-    int64_t tot = d.n * d.k;
-    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x)
-        if (!isfinite(d.values[x])) { atomicOr(&bad[p], 1u); return; }
+    const int64_t tot = d.n * d.k;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool ok = true;
+    int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; x + 3 * stride < tot; x += 4 * stride) {
+        double a = d.values[x], b = d.values[x + stride], c = d.values[x + 2 * stride], e = d.values[x + 3 * stride];
+        ok &= isfinite(a) && isfinite(b) && isfinite(c) && isfinite(e);
+    }
+    for (; x < tot; x += stride) ok &= (bool)isfinite(d.values[x]);
+    if (__any_sync(CH_FULL, !ok) && lane_id() == 0) atomicOr(&bad[p], 1u);
 }
 
 // values of the same slot from two passes must agree within 1e-9 relative
@@ -297,10 +306,8 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
             k_pass_check<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.name_id, N, ctx->d_gpu_lg,
                                                                         ctx->d_nm_rank, ctx->d_passes, doff, didx, mis);
             CH_LAUNCHED(ctx);
-            for (int p = 0; p < n_passes; p++) {
-                k_pass_finite<<<64, NT, 0, ctx->st>>>(ctx->d_passes, p, bad);
-                CH_LAUNCHED(ctx);
-            }
+            k_pass_finite<<<dim3(148 * 2, n_passes), NT, 0, ctx->st>>>(ctx->d_passes, bad);
+            CH_LAUNCHED(ctx);
             std::vector<unsigned long long> hmis(n_passes);
             std::vector<unsigned int> hbad(n_passes);
             CH_CUDA(ctx, cudaMemcpyAsync(hmis.data(), mis, 8 * n_passes, cudaMemcpyDeviceToHost, ctx->st));

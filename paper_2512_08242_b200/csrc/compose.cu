@@ -106,22 +106,25 @@ __device__ __forceinline__ int pow2ceil(int n) {
     while (p < n) p <<= 1;
     return p;
 }
-// median of a[0..n) (sorted in place); even count = mean of the two central values (D21)
-__device__ double med_i64(int64_t *a, int n) {
+// median of a[0..n) (D21: even count = mean of the two central values).  The values are sorted in
+// shared memory when they fit (sh != nullptr), else in place in global memory.
+__device__ double med_i64(int64_t *a, int n, int64_t *sh) {
     int n2 = pow2ceil(n);
-    for (int i = n + threadIdx.x; i < n2; i += blockDim.x) a[i] = INT64_MAX;
+    int64_t *w = sh ? sh : a;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) w[i] = i < n ? a[i] : INT64_MAX;
     __syncthreads();
-    block_bitonic<int64_t>(a, n2);
-    double m = (n % 2) ? (double)a[n / 2] : 0.5 * ((double)a[n / 2 - 1] + (double)a[n / 2]);
+    block_bitonic<int64_t>(w, n2);
+    double m = (n % 2) ? (double)w[n / 2] : 0.5 * ((double)w[n / 2 - 1] + (double)w[n / 2]);
     __syncthreads();
     return m;
 }
-__device__ double med_f64(double *a, int n) {
+__device__ double med_f64(double *a, int n, double *sh) {
     int n2 = pow2ceil(n);
-    for (int i = n + threadIdx.x; i < n2; i += blockDim.x) a[i] = INFINITY;
+    double *w = sh ? sh : a;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) w[i] = i < n ? a[i] : INFINITY;
     __syncthreads();
-    block_bitonic<double>(a, n2);
-    double m = (n % 2) ? a[n / 2] : 0.5 * (a[n / 2 - 1] + a[n / 2]);
+    block_bitonic<double>(w, n2);
+    double m = (n % 2) ? w[n / 2] : 0.5 * (w[n / 2 - 1] + w[n / 2]);
     __syncthreads();
     return m;
 }
@@ -143,9 +146,13 @@ struct BdArgs {
     int64_t *wi;                 // [nblocks][5][maxp2] int64 scratch
     double *wd;                  // [nblocks][5][maxp2] double scratch
     double *out;                 // [nblocks][16]
+    int use_smem;
 };
 
-__global__ void __launch_bounds__(256) k_breakdown(BdArgs A) {
+__global__ void __launch_bounds__(512) k_breakdown(BdArgs A) {
+    extern __shared__ int64_t bsh[];
+    int64_t *shi = A.use_smem ? bsh : nullptr;
+    double *shd = A.use_smem ? reinterpret_cast<double *>(bsh) : nullptr;
     __shared__ int s_n;
     __shared__ int s_flags_in;   // bit0 cyc, bit1 fl, bit2 util, bit3 smp
     const int L = A.labels[blockIdx.x];
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(256) k_breakdown(BdArgs A) {
     // D_act = median busy (D14)
     for (int i = threadIdx.x; i < n; i += blockDim.x) ti[i] = busy[i];
     __syncthreads();
-    double d_act = med_i64(ti, n);
+    double d_act = med_i64(ti, n, shi);
     // D0 / D50 buckets (integer tests, D15)
     __shared__ int s_n0, s_n50;
     if (threadIdx.x == 0) {
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(256) k_breakdown(BdArgs A) {
     double d0 = 0.0, d50 = 0.0;
     bool bucket = false;
     if (n0 > 0) {
-        double m0 = med_i64(ti, n0);
+        double m0 = med_i64(ti, n0, shi);
         if (threadIdx.x == 0) {
             int a = 0;
             for (int i = 0; i < n; i++) if (2 * busy[i] <= 5 * ovl[i] && 5 * ovl[i] <= 3 * busy[i]) ti[a++] = busy[i];
@@ -217,7 +224,7 @@ __global__ void __launch_bounds__(256) k_breakdown(BdArgs A) {
         int n50 = s_n50;
         if (n50 > 0) {
             d0 = m0;
-            d50 = med_i64(ti, n50);
+            d50 = med_i64(ti, n50, shi);
             bucket = true;
         }
     }
@@ -245,26 +252,26 @@ __global__ void __launch_bounds__(256) k_breakdown(BdArgs A) {
     if (has_fl) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) td[i] = fp[i];
         __syncthreads();
-        med_fp = med_f64(td, n);
+        med_fp = med_f64(td, n, shd);
     }
     if (has_util || (has_fl && has_cyc)) {
         for (int i = threadIdx.x; i < n; i += blockDim.x)
             td[i] = has_util ? un[i] / ud[i] : (fp[i] / cg[i]) * (A.freq / A.tpt);
         __syncthreads();
-        med_u = med_f64(td, n);
+        med_u = med_f64(td, n, shd);
     }
     if (has_cyc) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) td[i] = cg[i];
         __syncthreads();
-        med_cg = med_f64(td, n);
+        med_cg = med_f64(td, n, shd);
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) ti[i] = busy[i] + launch[i];
     __syncthreads();
-    med_bl = med_i64(ti, n);
+    med_bl = med_i64(ti, n, shi);
     if (has_smp) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) td[i] = (double)phi[i] / (double)busy[i] * 1e6;
         __syncthreads();
-        med_v = med_f64(td, n);
+        med_v = med_f64(td, n, shd);
     }
     if (threadIdx.x == 0) {
         out[0] = n;
@@ -378,7 +385,7 @@ __global__ void __launch_bounds__(256) k_global(GlobArgs A) {
     __syncthreads();
     int nst = s_nst;
     double m = NAN;
-    if (nst > 0) m = med_f64(A.work, nst);
+    if (nst > 0) m = med_f64(A.work, nst, nullptr);
     if (threadIdx.x == 0) *A.med = m;
 }
 }  // namespace
@@ -475,7 +482,14 @@ static chopper_status run_breakdown(chopper_ctx *ctx, const int64_t *blk, int ns
     A.wi = wi;
     A.wd = wd;
     A.out = out;
-    k_breakdown<<<nb, 256, 0, ctx->st>>>(A);
+    size_t shb = (size_t)8 * maxp2;
+    A.use_smem = shb <= 64 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        CH_CUDA(ctx, cudaFuncSetAttribute(k_breakdown, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        attr = true;
+    }
+    k_breakdown<<<nb, 512, A.use_smem ? shb : 0, ctx->st>>>(A);
     CH_LAUNCHED(ctx);
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return CHOPPER_OK;
@@ -483,13 +497,13 @@ static chopper_status run_breakdown(chopper_ctx *ctx, const int64_t *blk, int ns
 
 // slot order by gpu id (host, from the exchange headers)
 static chopper_status slot_order(chopper_ctx *ctx, const int64_t *blk, int nslots, int64_t W, int32_t **out) {
-    std::vector<int64_t> hdr(2);
+    // one strided copy of the (gpu, present) header words of every slot
+    std::vector<int64_t> hdr(2 * (size_t)nslots);
     std::vector<std::pair<int64_t, int>> v;
-    for (int b = 0; b < nslots; b++) {
-        CH_CUDA(ctx, cudaMemcpyAsync(hdr.data(), blk + (int64_t)b * W, 16, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-        if (hdr[1]) v.push_back({hdr[0], b});
-    }
+    CH_CUDA(ctx, cudaMemcpy2DAsync(hdr.data(), 16, blk, 8 * (size_t)W, 16, nslots, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    for (int b = 0; b < nslots; b++)
+        if (hdr[2 * b + 1]) v.push_back({hdr[2 * b], b});
     std::sort(v.begin(), v.end());
     std::vector<int32_t> o(nslots + 1, -1);
     for (size_t q = 0; q < v.size(); q++) o[q] = v[q].second;

@@ -230,6 +230,25 @@ __device__ int64_t covl_fast(const EvParams &P, int lg, int64_t a, int64_t b) {
     return tot;
 }
 
+// per-event overlap of communication kernels with the compute union (R6), one thread per comm event;
+// comm events are the first bucket of each gpu in sorted order
+__global__ void k_covl(EvParams P, int n_lg) {
+    int lg = blockIdx.y;
+    int64_t lo = P.bucket_beg[lg * P.NG], hi = P.bucket_beg[lg * P.NG + 1];
+    for (int64_t j = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < hi; j += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t i = P.perm[j];
+        int64_t ks = P.ks[i], ke = P.ke[i], ovl;
+        if (P.v_general) {
+            int64_t vlo = P.Vbeg[lg], vhi = vlo + P.Vcnt[lg];
+            int64_t c1 = -2, c2 = -2;
+            ovl = cov(P.Vs, P.Ve, P.VP, vlo, vhi, ke, &c1) - cov(P.Vs, P.Ve, P.VP, vlo, vhi, ks, &c2);
+        } else {
+            ovl = covl_fast(P, lg, ks, ke);
+        }
+        P.o_ovl[i] = ovl;
+    }
+}
+
 struct Acc {
     int64_t v[NACC];
     __device__ __forceinline__ void zero() {
@@ -273,7 +292,6 @@ __global__ void __launch_bounds__(EV_NT) k_events(EvParams P) {
     __shared__ unsigned char hh[EV_NT];
     __shared__ int64_t scan_sm[33];
     __shared__ int64_t s_tile, s_excl;
-    __shared__ unsigned long long s_prevkey;
     const int tid = threadIdx.x;
     if (tid == 0) s_tile = (int64_t)atomicAdd(P.ticket, 1u);
     __syncthreads();
@@ -299,18 +317,11 @@ __global__ void __launch_bounds__(EV_NT) k_events(EvParams P) {
         }
     }
     lastkey[tid] = key[EV_IPT - 1];
-    if (tid == 0) {
-        s_prevkey = 0;
-        if (base > 0 && base < N) {
-            int64_t i = base - 1;
-            int64_t c2[4] = {-2, -2, -2, -2};
-            s_prevkey = event_key(P, i, P.gpu_lg[gpu_of(P.meta[i])], P.tl[i], c2);
-        }
-    }
     __syncthreads();
     unsigned hmask = 0;
     {
-        unsigned long long prev = tid > 0 ? lastkey[tid - 1] : s_prevkey;
+        // the tile start is always a head (sub-runs never cross tiles), so thread 0 needs no previous key
+        unsigned long long prev = tid > 0 ? lastkey[tid - 1] : CH_INVALID_KEY;
 #pragma unroll
         for (int k = 0; k < EV_IPT; k++) {
             int64_t i = i0 + k;
@@ -419,17 +430,9 @@ __global__ void __launch_bounds__(EV_NT) k_events(EvParams P) {
             if (kd == CK_COPY || kd == CK_OTHER) acc.v[RF_COPY] += dur;
             else if (kd == CK_AG) acc.v[RF_AG] += dur;
             else if (kd == CK_RS) acc.v[RF_RS] += dur;
-            if (is_comm(kd)) {
-                if (P.v_general) {
-                    int64_t vlo = P.Vbeg[lg], vhi = vlo + P.Vcnt[lg];
-                    int64_t c1 = -2, c2 = -2;
-                    ovl = cov(P.Vs, P.Ve, P.VP, vlo, vhi, ke, &c1) - cov(P.Vs, P.Ve, P.VP, vlo, vhi, ks, &c2);
-                } else {
-                    ovl = covl_fast(P, lg, ks, ke);
-                }
-            }
+            // communication overlap with the compute union feeds no table: k_covl writes it (full mode)
         }
-        if (P.o_ovl) P.o_ovl[i] = ovl;
+        if (P.o_ovl && !is_comm(kd)) P.o_ovl[i] = ovl;
         if (P.o_prep) P.o_prep[i] = prep;
         if (P.o_call) P.o_call[i] = call;
         if (P.o_phi) P.o_phi[i] = phi;
@@ -624,6 +627,10 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     k_events<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P);
     CH_LAUNCHED(ctx);
     ch_tick(ctx, 4, 1);
+    if (ovl && ctx->n_lg > 0) {
+        k_covl<<<dim3(64, ctx->n_lg), 128, 0, ctx->st>>>(P, ctx->n_lg);
+        CH_LAUNCHED(ctx);
+    }
     unsigned long long last = 0;
     CH_CUDA(ctx, cudaMemcpyAsync(&last, ctx->d_tile_state + ntile - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));

@@ -53,66 +53,96 @@ __device__ __forceinline__ int64_t op_comb(int64_t a, int64_t b) {
 template <int OP>
 __device__ __forceinline__ int64_t op_id() { return OP == 1 ? INT64_MIN : 0; }
 
+// (head, value) pair scan: (h1,v1) (+) (h2,v2) = (h1|h2, h2 ? v2 : v1 op v2)
 template <int OP>
-__global__ void k_seg_tile_agg(const int64_t *__restrict__ in, const uint8_t *__restrict__ head, int64_t n,
-                               int64_t *__restrict__ agg_v, uint8_t *__restrict__ agg_h) {
-    // one thread per tile is enough here: tile aggregates are tiny compared to the apply pass
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t ntile = (n + SC_TILE - 1) / SC_TILE;
-    if (t >= ntile) return;
-    int64_t lo = t * SC_TILE, hi = lo + SC_TILE < n ? lo + SC_TILE : n;
-    int64_t v = op_id<OP>();
-    uint8_t h = 0;
-    for (int64_t i = lo; i < hi; i++) {
-        if (head[i]) { v = op_id<OP>(); h = 1; }
-        v = op_comb<OP>(v, in[i]);
+__device__ __forceinline__ void pair_comb(uint32_t &h, int64_t &v, uint32_t h2, int64_t v2) {
+    v = h2 ? v2 : op_comb<OP>(v, v2);
+    h |= h2;
+}
+// block-wide exclusive pair scan (blockDim = SC_NT); returns the exclusive prefix of this thread,
+// *tot_h / *tot_v get the block aggregate
+template <int OP>
+__device__ __forceinline__ void block_pair_excl(uint32_t h, int64_t v, uint32_t *eh, int64_t *ev, uint32_t *th,
+                                                int64_t *tv) {
+    __shared__ int64_t wv[SC_NT / 32];
+    __shared__ uint32_t wh[SC_NT / 32];
+    int l = lane_id(), w = threadIdx.x >> 5;
+    uint32_t ih = h;
+    int64_t iv = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t yh = __shfl_up_sync(CH_FULL, ih, o);
+        int64_t yv = __shfl_up_sync(CH_FULL, iv, o);
+        if (l >= o) {   // (y) (+) (this)
+            uint32_t nh = yh;
+            int64_t nv = yv;
+            pair_comb<OP>(nh, nv, ih, iv);
+            ih = nh;
+            iv = nv;
+        }
     }
-    agg_v[t] = v;
-    agg_h[t] = h;
+    if (l == 31) { wh[w] = ih; wv[w] = iv; }
+    __syncthreads();
+    uint32_t ph = 0;
+    int64_t pv = op_id<OP>();
+    for (int q = 0; q < w; q++) pair_comb<OP>(ph, pv, wh[q], wv[q]);
+    // exclusive of this thread = (warp prefix) (+) (lanes before)
+    uint32_t xh = __shfl_up_sync(CH_FULL, ih, 1);
+    int64_t xv = __shfl_up_sync(CH_FULL, iv, 1);
+    uint32_t eh2 = ph;
+    int64_t ev2 = pv;
+    if (l > 0) pair_comb<OP>(eh2, ev2, xh, xv);
+    *eh = eh2;
+    *ev = ev2;
+    uint32_t ah = 0;
+    int64_t av = op_id<OP>();
+    for (int q = 0; q < SC_NT / 32; q++) pair_comb<OP>(ah, av, wh[q], wv[q]);
+    *th = ah;
+    *tv = av;
+    __syncthreads();
 }
 
-// exclusive carry per tile, single thread sequential (tiles are few)
 template <int OP>
-__global__ void k_seg_carry(const int64_t *__restrict__ agg_v, const uint8_t *__restrict__ agg_h, int64_t ntile,
-                            int64_t *__restrict__ carry) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    int64_t c = op_id<OP>();
-    for (int64_t t = 0; t < ntile; t++) {
-        carry[t] = c;
-        c = agg_h[t] ? agg_v[t] : op_comb<OP>(c, agg_v[t]);
-    }
-}
-
-// per-thread sequential segment inside the tile with a warp/block carry of (head, value)
-template <int OP, bool EXCL>
-__global__ void k_seg_apply(const int64_t *__restrict__ in, const uint8_t *__restrict__ head, int64_t n,
-                            const int64_t *__restrict__ carry, int64_t *__restrict__ out) {
-    __shared__ int64_t sv[SC_NT];
-    __shared__ uint8_t sh[SC_NT];
+__global__ void __launch_bounds__(SC_NT) k_seg_tile_agg(const int64_t *__restrict__ in, const uint8_t *__restrict__ head,
+                                                        int64_t n, int64_t *__restrict__ agg_v, uint8_t *__restrict__ agg_h) {
     int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_IPT;
     int64_t v = op_id<OP>();
-    uint8_t h = 0;
+    uint32_t h = 0;
     for (int k = 0; k < SC_IPT; k++) {
         int64_t i = base + k;
         if (i >= n) break;
         if (head[i]) { v = op_id<OP>(); h = 1; }
         v = op_comb<OP>(v, in[i]);
     }
-    sv[threadIdx.x] = v;
-    sh[threadIdx.x] = h;
-    __syncthreads();
-    // sequential exclusive carry across threads (thread 0), simple and deterministic
-    if (threadIdx.x == 0) {
-        int64_t c = carry[blockIdx.x];
-        for (int t = 0; t < SC_NT; t++) {
-            int64_t a = sv[t];
-            uint8_t hh = sh[t];
-            sv[t] = c;
-            c = hh ? a : op_comb<OP>(c, a);
-        }
+    uint32_t eh, th;
+    int64_t ev, tv;
+    block_pair_excl<OP>(h, v, &eh, &ev, &th, &tv);
+    if (threadIdx.x == 0) { agg_v[blockIdx.x] = tv; agg_h[blockIdx.x] = (uint8_t)th; }
+}
+
+// carry of tile t = inclusive pair scan of the aggregates up to t-1
+__global__ void k_shift_carry(const int64_t *__restrict__ incl, int64_t ntile, int64_t ident, int64_t *__restrict__ carry) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < ntile) carry[t] = t > 0 ? incl[t - 1] : ident;
+}
+
+template <int OP, bool EXCL>
+__global__ void __launch_bounds__(SC_NT) k_seg_apply(const int64_t *__restrict__ in, const uint8_t *__restrict__ head,
+                                                     int64_t n, const int64_t *__restrict__ carry,
+                                                     int64_t *__restrict__ out) {
+    int64_t base = (int64_t)blockIdx.x * SC_TILE + (int64_t)threadIdx.x * SC_IPT;
+    int64_t v = op_id<OP>();
+    uint32_t h = 0;
+    for (int k = 0; k < SC_IPT; k++) {
+        int64_t i = base + k;
+        if (i >= n) break;
+        if (head[i]) { v = op_id<OP>(); h = 1; }
+        v = op_comb<OP>(v, in[i]);
     }
-    __syncthreads();
-    int64_t c = sv[threadIdx.x];
+    uint32_t eh, th;
+    int64_t ev, tv;
+    block_pair_excl<OP>(h, v, &eh, &ev, &th, &tv);
+    int64_t c = eh ? ev : op_comb<OP>(carry ? carry[blockIdx.x] : op_id<OP>(), ev);
     for (int k = 0; k < SC_IPT; k++) {
         int64_t i = base + k;
         if (i >= n) break;
@@ -243,28 +273,26 @@ chopper_status ch_seg_scan_i64(chopper_ctx *ctx, const int64_t *in, const uint8_
     if (n <= 0) return CHOPPER_OK;
     int64_t ntile = ceil_div(n, SC_TILE);
     size_t mark = ctx->used;
-    CH_ALLOC_BEGIN;
-    int64_t *agg = CH_ALLOC(ctx, int64_t, ntile);
-    uint8_t *aggh = CH_ALLOC(ctx, uint8_t, ntile);
-    int64_t *carry = CH_ALLOC(ctx, int64_t, ntile);
-    CH_ALLOC_END(ctx);
-    unsigned g1 = (unsigned)ceil_div(ntile, 128);
-    if (op == 1) {
-        k_seg_tile_agg<1><<<g1, 128, 0, ctx->st>>>(in, head, n, agg, aggh);
+    int64_t *carry = nullptr;
+    if (ntile > 1) {
+        CH_ALLOC_BEGIN;
+        int64_t *agg = CH_ALLOC(ctx, int64_t, ntile);
+        uint8_t *aggh = CH_ALLOC(ctx, uint8_t, ntile);
+        int64_t *incl = CH_ALLOC(ctx, int64_t, ntile);
+        carry = CH_ALLOC(ctx, int64_t, ntile);
+        CH_ALLOC_END(ctx);
+        if (op == 1) k_seg_tile_agg<1><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, agg, aggh);
+        else k_seg_tile_agg<0><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, agg, aggh);
         CH_LAUNCHED(ctx);
-        k_seg_carry<1><<<1, 32, 0, ctx->st>>>(agg, aggh, ntile, carry);
-        CH_LAUNCHED(ctx);
-        k_seg_apply<1, false><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
-        CH_LAUNCHED(ctx);
-    } else {
-        k_seg_tile_agg<0><<<g1, 128, 0, ctx->st>>>(in, head, n, agg, aggh);
-        CH_LAUNCHED(ctx);
-        k_seg_carry<0><<<1, 32, 0, ctx->st>>>(agg, aggh, ntile, carry);
-        CH_LAUNCHED(ctx);
-        if (op == 0) k_seg_apply<0, true><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
-        else k_seg_apply<0, false><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
+        // inclusive pair scan of the tile aggregates (recursive), then shift by one tile
+        CH_TRY(ch_seg_scan_i64(ctx, agg, aggh, incl, ntile, op == 1 ? 1 : 2));
+        k_shift_carry<<<(unsigned)ceil_div(ntile, 256), 256, 0, ctx->st>>>(incl, ntile, op == 1 ? INT64_MIN : 0, carry);
         CH_LAUNCHED(ctx);
     }
+    if (op == 1) k_seg_apply<1, false><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
+    else if (op == 0) k_seg_apply<0, true><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
+    else k_seg_apply<0, false><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
+    CH_LAUNCHED(ctx);
     ctx->used = mark;
     return CHOPPER_OK;
 }

@@ -14,25 +14,52 @@
 namespace {
 constexpr int NT = 256;
 
-// counter sums of each sub-run over its COMPUTE events: one warp per sub-run
-__global__ void k_subrun_counters(const int64_t *__restrict__ first, int64_t R, const uint32_t *__restrict__ meta,
-                                  const int32_t *__restrict__ gpu_lg, const int32_t *__restrict__ nm_rank,
-                                  const double *const *__restrict__ col, int C, double *__restrict__ out,
-                                  int64_t cap) {
-    int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int l = lane_id();
-    if (r >= R) return;
-    int64_t lo = first[r], hi = first[r + 1];
-    int lg = gpu_lg[gpu_of(meta[lo])];
-    for (int s0 = 0; s0 < C; s0 += 8) {
-        double acc[8];
+// counter sums of each sub-run over its COMPUTE events, tiled like the event pass (2048 events per
+// block, 8 consecutive per thread; sub-runs never cross tiles).  Slots are processed SG at a time.
+// Pieces spanning threads are completed through shared memory in forward (input) order.
+constexpr int CT_NT = 256, CT_IPT = 8, CT_TILE = CT_NT * CT_IPT, CT_SG = 8;
+__global__ void __launch_bounds__(CT_NT) k_counters_tiled(const uint32_t *__restrict__ meta,
+                                                          const int32_t *__restrict__ run_id,
+                                                          const int32_t *__restrict__ nm_rank,
+                                                          const int32_t *__restrict__ gpu_lg,
+                                                          const double *const *__restrict__ col, int C, int s0,
+                                                          int64_t N, double *__restrict__ out, int64_t cap) {
+    __shared__ double fp[CT_SG][CT_NT], lp[CT_SG][CT_NT];
+    __shared__ unsigned char hh[CT_NT];
+    const int tid = threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * CT_TILE, i0 = base + (int64_t)tid * CT_IPT;
+    double acc[CT_SG];
 #pragma unroll
-        for (int q = 0; q < 8; q++) acc[q] = 0.0;
-        for (int64_t i = lo + l; i < hi; i += 32) {
-            if (kind_of(meta[i]) != CK_COMPUTE) continue;
+    for (int q = 0; q < CT_SG; q++) acc[q] = 0.0;
+    bool has = false;
+    int32_t cur = -1, first_head = -1;
+    int32_t prev = (i0 > base && i0 < N) ? run_id[i0 - 1] : -1;
+    for (int k = 0; k < CT_IPT; k++) {
+        int64_t i = i0 + k;
+        if (i >= N) break;
+        int32_t rid = run_id[i];
+        if (i == base || rid != prev) {
+            if (!has) {
+#pragma unroll
+                for (int q = 0; q < CT_SG; q++) fp[q][tid] = acc[q];
+                has = true;
+                first_head = rid;
+            } else {
+#pragma unroll
+                for (int q = 0; q < CT_SG; q++)
+                    if (s0 + q < C) out[(int64_t)(s0 + q) * cap + cur] = acc[q];
+            }
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++) acc[q] = 0.0;
+            cur = rid;
+        }
+        prev = rid;
+        uint32_t m = meta[i];
+        if (kind_of(m) == CK_COMPUTE) {
+            int lg = gpu_lg[gpu_of(m)];
             int64_t j = nm_rank[i];
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
+            for (int q = 0; q < CT_SG; q++) {
                 int s = s0 + q;
                 if (s < C) {
                     const double *c = col[lg * C + s];
@@ -40,12 +67,35 @@ __global__ void k_subrun_counters(const int64_t *__restrict__ first, int64_t R, 
                 }
             }
         }
+    }
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
-            double v = acc[q];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CH_FULL, v, o);
-            if (l == 0 && s0 + q < C) out[(int64_t)(s0 + q) * cap + r] = v;
+    for (int q = 0; q < CT_SG; q++) {
+        if (has) lp[q][tid] = acc[q];
+        else fp[q][tid] = acc[q];
+    }
+    hh[tid] = has;
+    __syncthreads();
+    // a sub-run ending inside this thread's first piece started at the nearest earlier thread with a head
+    auto complete = [&](int upto, bool own_last, int32_t id) {
+        int u = upto - 1;
+        while (!hh[u]) u--;
+        for (int q = 0; q < CT_SG; q++) {
+            if (s0 + q >= C) break;
+            double s = lp[q][u];
+            for (int v = u + 1; v < upto; v++) s += fp[q][v];
+            s += own_last ? lp[q][upto] : fp[q][upto];
+            out[(int64_t)(s0 + q) * cap + id] = s;
+        }
+    };
+    if (has && tid > 0 && base < N) complete(tid, false, first_head - 1);
+    if (tid == CT_NT - 1 && base < N) {
+        int64_t last = base + CT_TILE - 1 < N ? base + CT_TILE - 1 : N - 1;
+        int32_t id = run_id[last];
+        if (has) {
+            for (int q = 0; q < CT_SG; q++)
+                if (s0 + q < C) out[(int64_t)(s0 + q) * cap + id] = lp[q][tid];
+        } else {
+            complete(tid, false, id);
         }
     }
 }
@@ -350,9 +400,12 @@ chopper_status ch_tables(chopper_ctx *ctx) {
     // sub-run fields were written with capacity N; re-point the table view at that layout
     TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, ctx->N, std::max<int64_t>(R, 1)};
     if (C > 0 && R > 0) {
-        k_subrun_counters<<<(unsigned)ceil_div(R * 32, NT), NT, 0, ctx->st>>>(
-            ctx->sub.first_event, R, ctx->ev.meta, ctx->d_gpu_lg, ctx->d_nm_rank, ctx->d_col, C, subv.cnt, subv.ccap);
-        CH_LAUNCHED(ctx);
+        for (int s0 = 0; s0 < C; s0 += CT_SG) {
+            k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, 0, ctx->st>>>(
+                ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, s0, ctx->N, subv.cnt,
+                subv.ccap);
+            CH_LAUNCHED(ctx);
+        }
     }
     // instances: stable sort of sub-runs by key, then group equal keys
     unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, R + 1), *k2 = CH_ALLOC(ctx, unsigned long long, R + 1);
