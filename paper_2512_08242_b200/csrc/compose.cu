@@ -162,30 +162,50 @@ __global__ void __launch_bounds__(512) k_breakdown(BdArgs A) {
     double *cg = A.wd + (int64_t)blockIdx.x * 5 * A.maxp2;
     double *fp = cg + A.maxp2, *un = cg + 2 * A.maxp2, *ud = cg + 3 * A.maxp2, *td = cg + 4 * A.maxp2;
     const Layout Ly = A.Ly;
+    // gather the sampled points of L in (gpu, iteration) order: ordered block compaction over the
+    // candidate (gpu slot, iteration rank) grid; slot presence is AND-ed over contributing gpus
+    __shared__ int64_t scan_sm[33];
+    __shared__ int s_count;
     if (threadIdx.x == 0) {
-        // gather sampled points of L in (gpu, iteration) order; slot presence over contributing gpus
-        int n = 0;
-        int cyc = A.s_cyc >= 0, fl = A.s_fl >= 0, ut = A.s_un >= 0 && A.s_ud >= 0, sm = 1;
-        for (int q = 0; q < A.nslots; q++) {
-            int sl = A.slot_order[q];
-            if (sl < 0) break;
-            const int64_t *b = A.blk + (int64_t)sl * Ly.W;
-            if (b[1] == 0) continue;
-            for (int64_t r = A.warmup > 0 ? A.warmup : 0; r < Ly.MI; r++) {
-                const int64_t *p = b + Ly.pt_off() + (r * Ly.L + L) * PT_W;
-                if (p[0] == 0 || p[1] <= 0) continue;
-                if (n >= A.maxp2) continue;
-                busy[n] = p[1]; launch[n] = p[2]; ovl[n] = p[3]; phi[n] = p[4];
-                cg[n] = bitsd(p[5]); fp[n] = bitsd(p[6]); un[n] = bitsd(p[7]); ud[n] = bitsd(p[8]);
-                if (cyc && !b[HDR + A.s_cyc]) cyc = 0;
-                if (fl && !b[HDR + A.s_fl]) fl = 0;
-                if (ut && !(b[HDR + A.s_un] && b[HDR + A.s_ud])) ut = 0;
-                if (!b[2]) sm = 0;
-                n++;
+        s_count = 0;
+        s_flags_in = (A.s_cyc >= 0) | ((A.s_fl >= 0) << 1) | ((A.s_un >= 0 && A.s_ud >= 0) << 2) | (1 << 3);
+    }
+    __syncthreads();
+    {
+        int nq = 0;
+        while (nq < A.nslots && A.slot_order[nq] >= 0) nq++;
+        const int64_t r0 = A.warmup > 0 ? A.warmup : 0;
+        const int64_t nr = Ly.MI > r0 ? Ly.MI - r0 : 0;
+        const int64_t total = (int64_t)nq * nr;
+        for (int64_t c0 = 0; c0 < total; c0 += blockDim.x) {
+            int64_t c = c0 + threadIdx.x;
+            bool ok = false;
+            const int64_t *b = nullptr, *p = nullptr;
+            if (c < total) {
+                b = A.blk + (int64_t)A.slot_order[c / nr] * Ly.W;
+                p = b + Ly.pt_off() + ((r0 + c % nr) * Ly.L + L) * PT_W;
+                ok = b[1] != 0 && p[0] != 0 && p[1] > 0;
             }
+            int64_t tot;
+            int64_t pos = block_excl_sum<512>(ok ? 1 : 0, &tot, scan_sm) + s_count;
+            if (ok && pos < A.maxp2) {
+                busy[pos] = p[1]; launch[pos] = p[2]; ovl[pos] = p[3]; phi[pos] = p[4];
+                cg[pos] = bitsd(p[5]); fp[pos] = bitsd(p[6]); un[pos] = bitsd(p[7]); ud[pos] = bitsd(p[8]);
+                int drop = 0;
+                if (A.s_cyc >= 0 && !b[HDR + A.s_cyc]) drop |= 1;
+                if (A.s_fl >= 0 && !b[HDR + A.s_fl]) drop |= 2;
+                if (A.s_un >= 0 && A.s_ud >= 0 && !(b[HDR + A.s_un] && b[HDR + A.s_ud])) drop |= 4;
+                if (!b[2]) drop |= 8;
+                if (drop) atomicAnd(&s_flags_in, ~drop);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) s_count += (int)tot;
+            __syncthreads();
         }
-        s_n = n;
-        s_flags_in = cyc | (fl << 1) | (ut << 2) | ((sm && n > 0) << 3);
+    }
+    if (threadIdx.x == 0) {
+        s_n = s_count < A.maxp2 ? s_count : (int)A.maxp2;
+        if (s_n == 0) s_flags_in &= ~8;
     }
     __syncthreads();
     const int n = s_n;
@@ -203,23 +223,22 @@ __global__ void __launch_bounds__(512) k_breakdown(BdArgs A) {
     __syncthreads();
     double d_act = med_i64(ti, n, shi);
     // D0 / D50 buckets (integer tests, D15)
+    // bucket members (order irrelevant: only their medians are used)
     __shared__ int s_n0, s_n50;
-    if (threadIdx.x == 0) {
-        int a = 0;
-        for (int i = 0; i < n; i++) if (20 * ovl[i] <= busy[i]) ti[a++] = busy[i];
-        s_n0 = a;
-    }
+    if (threadIdx.x == 0) s_n0 = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        if (20 * ovl[i] <= busy[i]) ti[atomicAdd(&s_n0, 1)] = busy[i];
     __syncthreads();
     int n0 = s_n0;
     double d0 = 0.0, d50 = 0.0;
     bool bucket = false;
     if (n0 > 0) {
         double m0 = med_i64(ti, n0, shi);
-        if (threadIdx.x == 0) {
-            int a = 0;
-            for (int i = 0; i < n; i++) if (2 * busy[i] <= 5 * ovl[i] && 5 * ovl[i] <= 3 * busy[i]) ti[a++] = busy[i];
-            s_n50 = a;
-        }
+        if (threadIdx.x == 0) s_n50 = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            if (2 * busy[i] <= 5 * ovl[i] && 5 * ovl[i] <= 3 * busy[i]) ti[atomicAdd(&s_n50, 1)] = busy[i];
         __syncthreads();
         int n50 = s_n50;
         if (n50 > 0) {
@@ -336,11 +355,16 @@ __global__ void __launch_bounds__(256) k_global(GlobArgs A) {
     if (ref < 0) { if (threadIdx.x == 0) { *A.n_out = 0; *A.med = NAN; } return; }
     const int64_t *rb = A.blk + (int64_t)ref * Ly.W;
     // reference rows are the valid ranks of the reference gpu in rank order; output index = count before
-    for (int64_t r = threadIdx.x; r < Ly.MI; r += blockDim.x) {
+    __shared__ int widx[4096];
+    if (threadIdx.x == 0) {
+        int c = 0;
+        for (int64_t r = 0; r < Ly.MI && r < 4096; r++) { widx[r] = c; c += rb[Ly.it_off() + r * IT_W] != 0; }
+    }
+    __syncthreads();
+    for (int64_t r = threadIdx.x; r < Ly.MI && r < 4096; r += blockDim.x) {
         const int64_t *row = rb + Ly.it_off() + r * IT_W;
         if (!row[0]) continue;
-        int64_t w = 0;
-        for (int64_t q = 0; q < r; q++) w += rb[Ly.it_off() + q * IT_W] != 0;
+        int64_t w = widx[r];
         int64_t step = row[1];
         bool complete = true, samp = true;
         int64_t T = INT64_MIN, lo = INT64_MAX, hi = INT64_MIN;

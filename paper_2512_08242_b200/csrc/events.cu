@@ -279,16 +279,120 @@ struct Acc {
     }
 };
 
+// sub-run rows are AoS: 16 int64 (14 fields + pad) = one 128 B line per row
+constexpr int SR_W = 16;
 __device__ __forceinline__ void write_subrun(const EvParams &P, int64_t id, const Acc &a) {
+    longlong2 *dst = reinterpret_cast<longlong2 *>(P.sr_f + id * SR_W);
 #pragma unroll
-    for (int f = 0; f < NACC; f++) P.sr_f[(int64_t)f * P.cap + id] = a.v[f];
+    for (int f = 0; f < SR_W / 2; f++)
+        dst[f] = make_longlong2(2 * f < NACC ? a.v[2 * f] : 0, 2 * f + 1 < NACC ? a.v[2 * f + 1] : 0);
 }
 
-__global__ void __launch_bounds__(EV_NT) k_events(EvParams P) {
+// ---- register caches for the per-event lookups (events of a gpu come in dispatch order) ----
+// innermost span of one (gpu, level) list: unchanged while t < start of the next span in push order
+// and t < end of the current answer (descendants on the chain already ended before the previous t)
+struct LvCache {
+    int32_t lb, le, c0, res;
+    int64_t next_start, res_end;
+    bool pre;
+};
+__device__ __forceinline__ void lv_reset(LvCache &c, const SpanView &v, int list) {
+    c.lb = (int32_t)v.list_beg[list];
+    c.le = (int32_t)v.list_beg[list + 1];
+    c.pre = v.list_flags[list] != 0;
+    c.c0 = -2;
+    c.res = -1;
+}
+__device__ __forceinline__ int32_t lv_lookup(LvCache &c, const SpanView &v, int lv, int64_t t, int64_t i) {
+    if (c.pre) return v.attr_pre[(int64_t)lv * v.N + i];
+    if (c.le <= c.lb) return -1;
+    if (c.c0 != -2 && t < c.next_start && (c.res < 0 || t < c.res_end)) return c.res;
+    int64_t c0 = c.c0;
+    if (c0 == -2) {
+        c0 = last_le(v.P_start, c.lb, c.le, t);
+    } else {
+        int steps = 0;
+        while (c0 + 1 < c.le && __ldg(v.P_start + c0 + 1) <= t && steps < 4) { c0++; steps++; }
+        if (c0 + 1 < c.le && __ldg(v.P_start + c0 + 1) <= t) c0 = last_le(v.P_start, c0 + 1, c.le, t);
+    }
+    int64_t r = c0;
+    while (r >= c.lb && __ldg(v.P_end + r) <= t) r = __ldg(v.P_parent + r);
+    if (r < c.lb) r = -1;
+    c.c0 = (int32_t)c0;
+    c.res = (int32_t)r;
+    c.next_start = c0 + 1 < c.le ? __ldg(v.P_start + c0 + 1) : INT64_MAX;
+    c.res_end = r >= 0 ? __ldg(v.P_end + r) : 0;
+    return (int32_t)r;
+}
+
+// coverage of (-inf, t) by the gpu's merged comm union, caching the current merged interval
+struct CovCache {
+    int32_t lo, hi, u;
+    int64_t us, len, up, next_s;
+};
+__device__ __forceinline__ void cov_reset(CovCache &c, int64_t lo, int64_t cnt) {
+    c.lo = (int32_t)lo;
+    c.hi = (int32_t)(lo + cnt);
+    c.u = -2;
+}
+__device__ __forceinline__ int64_t cov_c(CovCache &c, const int64_t *Us, const int64_t *Ue, const int64_t *UP, int64_t t) {
+    if (c.hi <= c.lo) return 0;
+    if (!(c.u != -2 && t < c.next_s && (c.u < c.lo || t >= c.us))) {
+        int64_t u;
+        if (c.u != -2 && c.u >= c.lo && t >= c.us) {     // forward from the cached interval
+            u = c.u;
+            int steps = 0;
+            while (u + 1 < c.hi && __ldg(Us + u + 1) <= t && steps < 4) { u++; steps++; }
+            if (u + 1 < c.hi && __ldg(Us + u + 1) <= t) u = last_le(Us, u + 1, c.hi, t);
+        } else {
+            u = last_le(Us, c.lo, c.hi, t);
+        }
+        c.u = (int32_t)u;
+        c.next_s = u + 1 < c.hi ? __ldg(Us + u + 1) : INT64_MAX;
+        if (u >= c.lo) {
+            c.us = __ldg(Us + u);
+            c.len = __ldg(Ue + u) - c.us;
+            c.up = __ldg(UP + u);
+        }
+    }
+    if (c.u < c.lo) return 0;
+    int64_t x = t - c.us;
+    return c.up + (x < c.len ? x : c.len);
+}
+
+// prefix integral F(t) of a zero-order-hold sample stream, caching the current sample window
+struct SmpCache {
+    int32_t lo, hi, q;
+    int64_t ts, next, phi, psi;
+    int32_t f, p;
+};
+__device__ __forceinline__ void smp_reset(SmpCache &c, int64_t lo, int64_t hi) {
+    c.lo = (int32_t)lo;
+    c.hi = (int32_t)hi;
+    c.q = -2;
+}
+__device__ __forceinline__ void smp_F(SmpCache &c, const EvParams &P, int64_t t, int64_t *F, int64_t *Pw) {
+    if (!(c.q != -2 && t < c.next && (c.q == c.lo || t >= c.ts))) {
+        int64_t q = last_le(P.smp_ts, c.lo, c.hi, t);
+        if (q < c.lo) q = c.lo;            // before the first sample: f_0 extended backwards (D10)
+        c.q = (int32_t)q;
+        c.ts = __ldg(P.smp_ts + q);
+        c.next = q + 1 < c.hi ? __ldg(P.smp_ts + q + 1) : INT64_MAX;
+        c.phi = __ldg(P.phi_pre + q);
+        c.psi = __ldg(P.psi_pre + q);
+        c.f = __ldg(P.smp_f + q);
+        c.p = __ldg(P.smp_p + q);
+    }
+    int64_t dt = t - c.ts;
+    *F = c.phi + (int64_t)c.f * dt;
+    *Pw = c.psi + (int64_t)c.p * dt;
+}
+
+__global__ void __launch_bounds__(EV_NT, 3) k_events(EvParams P) {
     extern __shared__ int64_t dsm[];
     int64_t *fp = dsm;                    // [NACC][EV_NT] first piece per thread
     int64_t *lp = dsm + NACC * EV_NT;     // [NACC][EV_NT] last piece per thread
-    __shared__ unsigned long long lastkey[EV_NT];
+    unsigned long long *keys_s = reinterpret_cast<unsigned long long *>(dsm + 2 * NACC * EV_NT);  // [EV_IPT][EV_NT]
     __shared__ unsigned char hh[EV_NT];
     __shared__ int64_t scan_sm[33];
     __shared__ int64_t s_tile, s_excl;
@@ -300,35 +404,45 @@ __global__ void __launch_bounds__(EV_NT) k_events(EvParams P) {
     const int64_t i0 = base + (int64_t)tid * EV_IPT;
     const int64_t N = P.N;
 
-    // ---- phase A: instance keys (attribution) ----
-    unsigned long long key[EV_IPT];
-    {
-        int64_t cur[4] = {-2, -2, -2, -2};
-        int lgp = -1;
-#pragma unroll
-        for (int k = 0; k < EV_IPT; k++) {
-            int64_t i = i0 + k;
-            key[k] = CH_INVALID_KEY;
-            if (i < N) {
-                int lg = P.gpu_lg[gpu_of(P.meta[i])];
-                if (lg != lgp) { cur[0] = cur[1] = cur[2] = cur[3] = -2; lgp = lg; }
-                key[k] = event_key(P, i, lg, P.tl[i], cur);
-            }
-        }
-    }
-    lastkey[tid] = key[EV_IPT - 1];
-    __syncthreads();
+    // ---- phase A: instance keys (attribution), staged in shared memory ----
     unsigned hmask = 0;
     {
-        // the tile start is always a head (sub-runs never cross tiles), so thread 0 needs no previous key
-        unsigned long long prev = tid > 0 ? lastkey[tid - 1] : CH_INVALID_KEY;
-#pragma unroll
+        LvCache lc[4];
+        int lgp = -1;
+        unsigned long long prevk = CH_INVALID_KEY;
+#pragma unroll 1
         for (int k = 0; k < EV_IPT; k++) {
             int64_t i = i0 + k;
-            if (i < N && (i == base || key[k] != prev)) hmask |= 1u << k;
-            prev = key[k];
+            unsigned long long kk = CH_INVALID_KEY;
+            if (i < N) {
+                int lg = P.gpu_lg[gpu_of(__ldg(P.meta + i))];
+                if (lg != lgp) {
+#pragma unroll
+                    for (int lv = 0; lv < 4; lv++) lv_reset(lc[lv], P.sv, lg * 4 + lv);
+                    lgp = lg;
+                }
+                int64_t t = __ldg(P.tl + i);
+                int32_t r[4];
+                bool ok = true;
+#pragma unroll
+                for (int lv = 0; lv < 4; lv++) {
+                    int32_t c = lv_lookup(lc[lv], P.sv, lv, t, i);
+                    ok &= c != -2;
+                    r[lv] = c >= 0 ? c - lc[lv].lb + 1 : 0;
+                }
+                if (ok && r[0] != 0)
+                    kk = ((unsigned long long)lg << P.sh_lg) | ((unsigned long long)r[0] << P.sh_it) |
+                         ((unsigned long long)r[1] << P.sh_ph) | ((unsigned long long)r[2] << P.sh_ly) |
+                         (unsigned long long)r[3];
+                if (k > 0 && kk != prevk) hmask |= 1u << k;
+            }
+            keys_s[k * EV_NT + tid] = kk;
+            prevk = kk;
         }
     }
+    __syncthreads();
+    // the tile start is always a head (sub-runs never cross tiles)
+    if (i0 < N && (i0 == base || keys_s[tid] != keys_s[(EV_IPT - 1) * EV_NT + tid - 1])) hmask |= 1u;
     int64_t tot;
     int64_t ex = block_excl_sum<EV_NT>(__popc(hmask), &tot, scan_sm);
     // ---- decoupled look-back: global sub-run id of this tile's first head ----
@@ -359,32 +473,40 @@ __global__ void __launch_bounds__(EV_NT) k_events(EvParams P) {
     acc.zero();
     bool has = false;
     int64_t curid = run0 - 1;
-    int64_t cu_s = -2, cu_e = -2, cs_s = -2, cs_e = -2;
+    CovCache cc;
+    SmpCache sc;
+    bool smp = false;
     int lgp = -1;
 #pragma unroll 1
     for (int k = 0; k < EV_IPT; k++) {
         int64_t i = i0 + k;
         if (i >= N) break;
-        uint32_t m = P.meta[i];
+        uint32_t m = __ldg(P.meta + i);
         int lg = P.gpu_lg[gpu_of(m)];
-        if (lg != lgp) { cu_s = cu_e = cs_s = cs_e = -2; lgp = lg; }
+        if (lg != lgp) {
+            cov_reset(cc, P.Ubeg[lg], P.Ucnt[lg]);
+            int64_t slo = P.smp_lo[lg], shi = P.smp_hi[lg];
+            smp = shi > slo;
+            smp_reset(sc, slo, shi);
+            lgp = lg;
+        }
         if ((hmask >> k) & 1u) {
             if (!has) { acc.store(fp, tid); has = true; }
             else write_subrun(P, curid, acc);
             curid++;
             acc.zero();
-            P.sr_key[curid] = key[k];
+            P.sr_key[curid] = keys_s[k * EV_NT + tid];
             P.sr_first[curid] = i;
         }
         int kd = kind_of(m);
-        int64_t ks = P.ks[i], ke = P.ke[i];
+        int64_t ks = __ldg(P.ks + i), ke = __ldg(P.ke + i);
         int64_t dur = ke - ks;
         int64_t ovl = 0, prep = 0, call = 0, phi = 0, psi = 0;
         acc.v[RF_NEV] += 1;
         if (kd == CK_COMPUTE) {
-            int64_t pe = P.pred_end[i];
+            int64_t pe = __ldg(P.pred_end + i);
             if (pe != CH_NONE_TS) {
-                int64_t tl = P.tl[i];
+                int64_t tl = __ldg(P.tl + i);
                 int64_t t2 = tl < ks ? tl : ks;                       // D6: dispatch clamped to start
                 int64_t a = t2 - pe;
                 prep = a > 0 ? a : 0;                                  // Eq. 1
@@ -392,27 +514,15 @@ __global__ void __launch_bounds__(EV_NT) k_events(EvParams P) {
                 int64_t c = c1 < c2 ? c1 : c2;                         // Eq. 2
                 call = c > 0 ? c : 0;
             }
-            int64_t ulo = P.Ubeg[lg], uhi = ulo + P.Ucnt[lg];
-            ovl = cov(P.Us, P.Ue, P.UP, ulo, uhi, ke, &cu_e) - cov(P.Us, P.Ue, P.UP, ulo, uhi, ks, &cu_s);
-            int64_t slo = P.smp_lo[lg], shi = P.smp_hi[lg];
-            if (shi > slo) {
-                int64_t Fa, Fb, Pa, Pb;
-                {
-                    int64_t q = seek(P.smp_ts, slo, shi, ks, &cs_s);
-                    if (q < slo) q = slo;
-                    int64_t dt = ks - P.smp_ts[q];
-                    Fa = P.phi_pre[q] + (int64_t)P.smp_f[q] * dt;
-                    Pa = P.psi_pre[q] + (int64_t)P.smp_p[q] * dt;
-                }
-                {
-                    int64_t q = seek(P.smp_ts, slo, shi, ke, &cs_e);
-                    if (q < slo) q = slo;
-                    int64_t dt = ke - P.smp_ts[q];
-                    Fb = P.phi_pre[q] + (int64_t)P.smp_f[q] * dt;
-                    Pb = P.psi_pre[q] + (int64_t)P.smp_p[q] * dt;
-                }
-                phi = Fb - Fa;
-                psi = Pb - Pa;
+            int64_t c_ks = cov_c(cc, P.Us, P.Ue, P.UP, ks);
+            int64_t c_ke = cov_c(cc, P.Us, P.Ue, P.UP, ke);
+            ovl = c_ke - c_ks;                                         // |[t_ks, t_ke) ∩ U_g| (D9)
+            if (smp) {
+                int64_t Fa, Pa, Fb, Pb;
+                smp_F(sc, P, ks, &Fa, &Pa);
+                smp_F(sc, P, ke, &Fb, &Pb);
+                phi = Fb - Fa;                                         // MHz*ns
+                psi = Pb - Pa;                                         // mW*ns
             }
             acc.v[RF_N] += 1;
             acc.v[RF_BUSY] += dur;
@@ -584,7 +694,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     ctx->sub.cap = N;
     ctx->sub.key = CH_ALLOC(ctx, unsigned long long, N + 1);
     ctx->sub.first_event = CH_ALLOC(ctx, int64_t, N + 1);
-    ctx->sub.f = CH_ALLOC(ctx, int64_t, (int64_t)NACC * N);
+    ctx->sub.f = CH_ALLOC(ctx, int64_t, (int64_t)SR_W * N);
     ctx->d_run_id = CH_ALLOC(ctx, int32_t, N);
     ctx->d_tile_state = CH_ALLOC(ctx, unsigned long long, ntile);
     ctx->d_tile_ticket = CH_ALLOC(ctx, unsigned int, 1);
@@ -617,7 +727,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     P.o_run = ctx->d_run_id;
     P.sr_key = ctx->sub.key; P.sr_first = ctx->sub.first_event; P.sr_f = ctx->sub.f; P.cap = N;
     P.tile_state = ctx->d_tile_state; P.ticket = ctx->d_tile_ticket;
-    size_t dsm = sizeof(int64_t) * 2 * NACC * EV_NT;
+    size_t dsm = sizeof(int64_t) * (2 * NACC * EV_NT + EV_IPT * EV_NT);
     static bool attr_set = false;
     if (!attr_set) {
         CH_CUDA(ctx, cudaFuncSetAttribute(k_events, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));

@@ -219,24 +219,42 @@ __global__ void __launch_bounds__(RX_NT) k_rx_downsweep(KS ks, const unsigned lo
         rk[r] = before + __popc(mm & lt);
     }
     __syncthreads();
+    unsigned int run = 0;
     {   // exclusive prefix over warps, per digit (thread = digit)
-        unsigned int run = 0;
         for (int q = 0; q < RX_WARPS; q++) {
             unsigned int c = wh[q][threadIdx.x];
             wh[q][threadIdx.x] = run;
             run += c;
         }
     }
+    // tile-local start of every digit: exclusive scan of the per-digit tile counts
+    __shared__ int64_t sc[33];
+    __shared__ int tstart[256];
+    int64_t ttot;
+    tstart[threadIdx.x] = (int)block_excl_sum<RX_NT>((int64_t)run, &ttot, sc);
     __syncthreads();
+    // stage the tile in shared memory in (digit, input) order, then write each digit bucket coalesced
+    __shared__ unsigned long long sk[HAS_KEYS ? RX_TILE : 1];
+    __shared__ uint32_t sv[RX_TILE];
+    __shared__ uint8_t sd[RX_TILE];
 #pragma unroll
     for (int r = 0; r < RX_ROUNDS; r++) {
         int64_t i = base + r * 32 + l;
         if (i < n) {
             int d = dg[r];
-            int64_t pos = goff[d] + wh[w][d] + rk[r];
-            if (HAS_KEYS) keys_out[pos] = keys_in[i];
-            vals_out[pos] = HAS_VALS ? vals_in[i] : (uint32_t)i;
+            int loc = tstart[d] + (int)wh[w][d] + (int)rk[r];
+            if (HAS_KEYS) sk[loc] = keys_in[i];
+            sv[loc] = HAS_VALS ? vals_in[i] : (uint32_t)i;
+            sd[loc] = (uint8_t)d;
         }
+    }
+    __syncthreads();
+    const int tn = (int)ttot;
+    for (int j = threadIdx.x; j < tn; j += RX_NT) {
+        int d = sd[j];
+        int64_t pos = goff[d] + (j - tstart[d]);
+        if (HAS_KEYS) keys_out[pos] = sk[j];
+        vals_out[pos] = sv[j];
     }
 }
 __global__ void k_u32_to_i64(const unsigned int *a, int64_t *b, int64_t n) {

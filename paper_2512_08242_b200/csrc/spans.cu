@@ -59,6 +59,54 @@ __global__ void k_span_key2(const uint32_t *__restrict__ gl, const int64_t *__re
     key[q] = (list << sbits) | off;
 }
 
+// (list, start) keys straight from the caller's arrays, identity values
+__global__ void k_span_key_fast(const uint32_t *__restrict__ gl, const int64_t *__restrict__ s,
+                                const int64_t *__restrict__ e, int64_t S, const int32_t *__restrict__ gpu_lg, int n_lg,
+                                int64_t smin, int sbits, unsigned long long *__restrict__ key,
+                                uint32_t *__restrict__ val) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= S) return;
+    uint32_t x = gl[q];
+    int64_t a = s[q], b = e[q];
+    unsigned long long list, off = 0;
+    if (span_valid(x, a, b, gpu_lg)) {
+        list = (unsigned long long)(gpu_lg[x >> 8] * 4 + (int)(x & 0xFFu));
+        off = (unsigned long long)(a - smin);
+    } else {
+        list = (unsigned long long)(n_lg * 4);
+    }
+    key[q] = (list << sbits) | off;
+    val[q] = (uint32_t)q;
+}
+
+// runs of equal (list, start) are in index-ascending order after the stable sort: reorder each run by
+// (end desc, index desc) with an insertion sort; runs longer than 256 set *big (two-sort fallback)
+__global__ void k_fix_ties(const unsigned long long *__restrict__ key, uint32_t *__restrict__ order,
+                           const int64_t *__restrict__ e, int64_t S, unsigned long long excl_key, unsigned int *big) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= S - 1) return;
+    unsigned long long k = key[q];
+    if (k >= excl_key) return;                       // excluded spans: order irrelevant
+    if (key[q + 1] != k || (q > 0 && key[q - 1] == k)) return;
+    int64_t hi = q + 1;
+    while (hi < S && key[hi] == k && hi - q <= 256) hi++;
+    if (hi - q > 256) { atomicOr(big, 1u); return; }
+    for (int64_t a = q + 1; a < hi; a++) {
+        uint32_t v = order[a];
+        int64_t ev = e[v];
+        int64_t b = a - 1;
+        // element v goes before order[b] if (end desc, index desc) ranks it first
+        while (b >= q) {
+            uint32_t w = order[b];
+            int64_t ew = e[w];
+            if (ew > ev || (ew == ev && w > v)) break;
+            order[b + 1] = w;
+            b--;
+        }
+        order[b + 1] = v;
+    }
+}
+
 __global__ void k_span_gather(const uint32_t *__restrict__ order, const uint32_t *__restrict__ gl,
                               const int64_t *__restrict__ s, const int64_t *__restrict__ e,
                               const int32_t *__restrict__ lab, int64_t S, const int32_t *__restrict__ gpu_lg, int n_lg,
@@ -250,18 +298,36 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         unsigned long long *lb = CH_ALLOC(ctx, unsigned long long, n_lists + 1);
         CH_ALLOC_END(ctx);
         unsigned g = (unsigned)ceil_div(S, NT);
-        k_span_key1<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, S, emax, k1, v1);
-        CH_LAUNCHED(ctx);
+        unsigned int *big = reinterpret_cast<unsigned int *>(lb + n_lists);   // reuses the EXCL slot until gather
         bool alt;
-        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, S, 0, rbits, &alt));
-        uint32_t *vs = alt ? v2 : v1;
-        unsigned long long *ks = alt ? k2 : k1, *ko = alt ? k1 : k2;
-        uint32_t *vo = alt ? v1 : v2;
-        k_span_key2<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, vs, S, ctx->d_gpu_lg,
-                                           n_lg, smin, rbits, ks);
+        // one stable (list, start) sort with input order as tie-break, then equal-start runs are reordered
+        // by (end desc, index desc) in place
+        k_span_key_fast<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, S, ctx->d_gpu_lg,
+                                               n_lg, smin, rbits, k1, v1);
         CH_LAUNCHED(ctx);
-        CH_TRY(ch_radix_sort(ctx, ks, vs, ko, vo, S, 0, rbits + lbits, &alt));
-        uint32_t *order = alt ? vo : vs;
+        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, S, 0, rbits + lbits, &alt));
+        uint32_t *order = alt ? v2 : v1;
+        unsigned long long *okeys = alt ? k2 : k1;
+        CH_CUDA(ctx, cudaMemsetAsync(big, 0, 4, ctx->st));
+        k_fix_ties<<<g, NT, 0, ctx->st>>>(okeys, order, ctx->sp.end_ns, S, (unsigned long long)n_lists << rbits, big);
+        CH_LAUNCHED(ctx);
+        unsigned int hbig = 0;
+        CH_CUDA(ctx, cudaMemcpyAsync(&hbig, big, 4, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        if (hbig) {
+            // very long runs of equal starts: exact two-sort path (end desc, then (list, start) stable)
+            k_span_key1<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, S, emax, k1, v1);
+            CH_LAUNCHED(ctx);
+            CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, S, 0, rbits, &alt));
+            uint32_t *vs = alt ? v2 : v1;
+            unsigned long long *ks = alt ? k2 : k1, *ko = alt ? k1 : k2;
+            uint32_t *vo = alt ? v1 : v2;
+            k_span_key2<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, vs, S,
+                                               ctx->d_gpu_lg, n_lg, smin, rbits, ks);
+            CH_LAUNCHED(ctx);
+            CH_TRY(ch_radix_sort(ctx, ks, vs, ko, vo, S, 0, rbits + lbits, &alt));
+            order = alt ? vo : vs;
+        }
         CH_TRY(ch_fill_u64(ctx, lb, n_lists + 1, ~0ull));
         k_span_gather<<<g, NT, 0, ctx->st>>>(order, ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, ctx->sp.label,
                                              S, ctx->d_gpu_lg, n_lg, ctx->P_start, ctx->P_end, ctx->P_orig,

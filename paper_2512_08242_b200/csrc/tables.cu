@@ -128,8 +128,9 @@ struct TabView {
     unsigned long long *key;
     int64_t *f;
     double *cnt;
-    int64_t cap;     // field-column capacity
+    int64_t cap;     // field stride (field-major tables: capacity; AoS sub-runs: 1)
     int64_t ccap;    // counter-column capacity
+    int64_t rs;      // row stride (field-major: 1; AoS sub-runs: 16)
 };
 
 // parent row p = sum of children [starts[p], starts[p+1]) visited in order (through perm if given)
@@ -150,12 +151,12 @@ __global__ void k_sum_rows(TabView ch, const uint32_t *__restrict__ perm, const 
         if (j == lo) k0 = ch.key[c];
 #pragma unroll
         for (int f = 0; f < RF_NFIELDS; f++) {
-            int64_t x = ch.f[(int64_t)f * ch.cap + c];
+            int64_t x = ch.f[(int64_t)f * ch.cap + c * ch.rs];
             if (f == RF_FIRST_IDX || f == RF_FIRST_KS) continue;
             if (f == RF_LAST_KE) { if (x > v[f]) v[f] = x; continue; }
             v[f] += x;
         }
-        int64_t cks = ch.f[(int64_t)RF_FIRST_KS * ch.cap + c], cidx = ch.f[(int64_t)RF_FIRST_IDX * ch.cap + c];
+        int64_t cks = ch.f[(int64_t)RF_FIRST_KS * ch.cap + c * ch.rs], cidx = ch.f[(int64_t)RF_FIRST_IDX * ch.cap + c * ch.rs];
         if (cks < v[RF_FIRST_KS] || (cks == v[RF_FIRST_KS] && cidx < v[RF_FIRST_IDX])) {
             v[RF_FIRST_KS] = cks;
             v[RF_FIRST_IDX] = cidx;
@@ -353,7 +354,7 @@ static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sor
     return CHOPPER_OK;
 }
 
-static TabView view(RowTable &t) { return TabView{t.key, t.f, t.cnt, t.cap, t.cap}; }
+static TabView view(RowTable &t) { return TabView{t.key, t.f, t.cnt, t.cap, t.cap, 1}; }
 
 static chopper_status rollup(chopper_ctx *ctx, RowTable &child, RowTable &parent, int shift, int depth,
                              const KeyLayout &L, int32_t *lg_gpu_d) {
@@ -398,7 +399,7 @@ chopper_status ch_tables(chopper_ctx *ctx) {
     }
     ctx->sub.cap = std::max<int64_t>(R, 1);
     // sub-run fields were written with capacity N; re-point the table view at that layout
-    TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, ctx->N, std::max<int64_t>(R, 1)};
+    TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, 1, std::max<int64_t>(R, 1), 16};   // AoS sub-run rows
     if (C > 0 && R > 0) {
         for (int s0 = 0; s0 < C; s0 += CT_SG) {
             k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, 0, ctx->st>>>(
