@@ -17,23 +17,6 @@
 namespace {
 constexpr int NT = 256;
 
-__global__ void k_flag_nonmemop(const uint32_t *__restrict__ meta, int64_t n, int64_t *__restrict__ f) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) f[i] = kind_of(meta[i]) != CK_MEMOP ? 1 : 0;
-}
-__global__ void k_flag_kind(const uint32_t *__restrict__ meta, int64_t n, int kind, int64_t *__restrict__ f) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) f[i] = kind_of(meta[i]) == kind ? 1 : 0;
-}
-// rank within the gpu: global exclusive prefix minus the prefix at the gpu's first event
-__global__ void k_rank_in_gpu(const int64_t *__restrict__ ex, const uint32_t *__restrict__ meta, int64_t n,
-                              const int32_t *__restrict__ gpu_lg, const int64_t *__restrict__ gbeg,
-                              int32_t *__restrict__ rank) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int lg = gpu_lg[gpu_of(meta[i])];
-    rank[i] = (int32_t)(ex[i] - ex[gbeg[lg]]);
-}
 
 // name-sequence check of every pass of the event's gpu
 __global__ void k_pass_check(const uint32_t *__restrict__ meta, const int32_t *__restrict__ name_id, int64_t n,
@@ -93,35 +76,102 @@ __global__ void k_counters_out(const uint32_t *__restrict__ meta, int64_t n, con
     }
 }
 
-// ---- clock offsets -------------------------------------------------------------------------------
-// exchange block per gpu slot: [gpu, present, cnt_ag, cnt_rs, ks_ag[K], ke_ag[K], ks_rs[K], ke_rs[K]]
-__global__ void k_coll_scatter(const uint32_t *__restrict__ meta, const int64_t *__restrict__ ks,
-                               const int64_t *__restrict__ ke, int64_t n, const int32_t *__restrict__ gpu_lg,
-                               const int32_t *__restrict__ r_ag, const int32_t *__restrict__ r_rs, int64_t K,
-                               int64_t W, int64_t *__restrict__ blk, unsigned int *__restrict__ overflow) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    uint32_t m = meta[i];
+// ---- per-gpu ranks from meta: non-MEMOP (counter-pass position), AG and RS (collective index) -------
+// tile = 2048 events; counts of the three predicates packed 21 bits apart
+constexpr int MR_NT = 256, MR_IPT = 8, MR_TILE = MR_NT * MR_IPT;
+__device__ __forceinline__ unsigned long long pred3(uint32_t m) {
     int k = kind_of(m);
-    if (k != CK_AG && k != CK_RS) return;
-    int lg = gpu_lg[gpu_of(m)];
-    int64_t j = k == CK_AG ? r_ag[i] : r_rs[i];
-    if (j >= K) { atomicOr(overflow, 1u); return; }
-    int64_t *b = blk + (int64_t)lg * W + 4 + (k == CK_AG ? 0 : 2 * K);
-    b[j] = ks[i];
-    b[K + j] = ke[i];
+    return (k != CK_MEMOP ? 1ull : 0ull) | (k == CK_AG ? 1ull << 21 : 0ull) | (k == CK_RS ? 1ull << 42 : 0ull);
+}
+__global__ void __launch_bounds__(MR_NT) k_meta_tiles(const uint32_t *__restrict__ meta, int64_t n,
+                                                      int64_t *__restrict__ tc, int64_t ntile) {
+    __shared__ int64_t sm[33];
+    int64_t i0 = (int64_t)blockIdx.x * MR_TILE + (int64_t)threadIdx.x * MR_IPT;
+    unsigned long long c = 0;
+    for (int k = 0; k < MR_IPT; k++)
+        if (i0 + k < n) c += pred3(meta[i0 + k]);
+    int64_t tot;
+    block_excl_sum<MR_NT>((int64_t)c, &tot, sm);
+    if (threadIdx.x == 0) {
+        unsigned long long t = (unsigned long long)tot;
+        tc[blockIdx.x] = (int64_t)(t & 0x1FFFFF);
+        tc[ntile + blockIdx.x] = (int64_t)((t >> 21) & 0x1FFFFF);
+        tc[2 * ntile + blockIdx.x] = (int64_t)(t >> 42);
+    }
+}
+// base[c][lg] = global exclusive count of predicate c at the gpu's first event (lg = n_lg -> N);
+// also writes the exchange header (gpu, present, #AG, #RS) of every local gpu
+__global__ void k_gpu_bases(const uint32_t *__restrict__ meta, int64_t n, const int64_t *__restrict__ tex,
+                            int64_t ntile, const int64_t *__restrict__ gbeg, int n_lg, int64_t *__restrict__ base,
+                            const int32_t *__restrict__ lg_gpu, int64_t *__restrict__ xsend, int64_t W) {
+    int t = threadIdx.x;
+    if (t < 3 * (n_lg + 1)) {
+        int c = t / (n_lg + 1), lg = t % (n_lg + 1);
+        int64_t pos = gbeg[lg];
+        int64_t tile = pos / MR_TILE;
+        int64_t b = 0;
+        if (tile < ntile) {
+            b = tex[c * ntile + tile];
+            for (int64_t i = tile * MR_TILE; i < pos; i++) b += (int64_t)((pred3(meta[i]) >> (21 * c)) & 0x1FFFFF);
+        } else {
+            b = tex[c * ntile + ntile - 1];
+            for (int64_t i = (ntile - 1) * MR_TILE; i < n; i++) b += (int64_t)((pred3(meta[i]) >> (21 * c)) & 0x1FFFFF);
+        }
+        base[c * (n_lg + 1) + lg] = b;
+    }
+    __syncthreads();
+    if (t < n_lg && xsend) {
+        int64_t *h = xsend + (int64_t)t * W;
+        h[0] = lg_gpu[t];
+        h[1] = 1;
+        h[2] = base[1 * (n_lg + 1) + t + 1] - base[1 * (n_lg + 1) + t];
+        h[3] = base[2 * (n_lg + 1) + t + 1] - base[2 * (n_lg + 1) + t];
+    }
+}
+__global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict__ meta, const int64_t *__restrict__ ks,
+                                                      const int64_t *__restrict__ ke, int64_t n,
+                                                      const int32_t *__restrict__ gpu_lg, const int64_t *__restrict__ tex,
+                                                      int64_t ntile, const int64_t *__restrict__ base, int n_lg,
+                                                      int32_t *__restrict__ nm_rank, int64_t *__restrict__ xsend,
+                                                      int64_t K, int64_t W, unsigned int *__restrict__ ovf) {
+    __shared__ int64_t sm[33];
+    int64_t i0 = (int64_t)blockIdx.x * MR_TILE + (int64_t)threadIdx.x * MR_IPT;
+    uint32_t mm[MR_IPT];
+    unsigned long long c = 0;
+#pragma unroll
+    for (int k = 0; k < MR_IPT; k++) {
+        mm[k] = i0 + k < n ? meta[i0 + k] : (uint32_t)CK_MEMOP;
+        if (i0 + k < n) c += pred3(mm[k]);
+    }
+    int64_t tot;
+    unsigned long long ex = (unsigned long long)block_excl_sum<MR_NT>((int64_t)c, &tot, sm);
+    int64_t r0 = tex[blockIdx.x] + (int64_t)(ex & 0x1FFFFF);
+    int64_t r1 = tex[ntile + blockIdx.x] + (int64_t)((ex >> 21) & 0x1FFFFF);
+    int64_t r2 = tex[2 * ntile + blockIdx.x] + (int64_t)(ex >> 42);
+#pragma unroll
+    for (int k = 0; k < MR_IPT; k++) {
+        int64_t i = i0 + k;
+        if (i >= n) break;
+        uint32_t m = mm[k];
+        int lg = gpu_lg[gpu_of(m)];
+        int kd = kind_of(m);
+        nm_rank[i] = (int32_t)(r0 - base[lg]);
+        if (kd == CK_AG || kd == CK_RS) {
+            int64_t j = kd == CK_AG ? r1 - base[(n_lg + 1) + lg] : r2 - base[2 * (n_lg + 1) + lg];
+            if (j >= K) atomicOr(ovf, 1u);
+            else if (xsend) {
+                int64_t *b = xsend + (int64_t)lg * W + 4 + (kd == CK_AG ? 0 : 2 * K);
+                b[j] = ks[i];
+                b[K + j] = ke[i];
+            }
+        }
+        if (kd != CK_MEMOP) r0++;
+        if (kd == CK_AG) r1++;
+        if (kd == CK_RS) r2++;
+    }
 }
 
-__global__ void k_coll_header(int64_t *__restrict__ blk, int64_t W, int n_lg, const int32_t *__restrict__ lg_gpu,
-                              const int32_t *__restrict__ r_ag_last, const int32_t *__restrict__ r_rs_last) {
-    int l = threadIdx.x;
-    if (l >= n_lg) return;
-    int64_t *b = blk + (int64_t)l * W;
-    b[0] = lg_gpu[l];
-    b[1] = 1;
-    b[2] = r_ag_last[l];
-    b[3] = r_rs_last[l];
-}
+
 
 // one block per gathered gpu slot: lower median of collective-end differences (radix select)
 __global__ void __launch_bounds__(256) k_delta(const int64_t *__restrict__ all, int nslots, int64_t W, int64_t K,
@@ -261,28 +311,46 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
     ctx->present.assign((size_t)n_lg * (C > 0 ? C : 1), 0);
     std::vector<const double *> hcol((size_t)n_lg * (C > 0 ? C : 1), nullptr);
     CH_CUDA(ctx, cudaMemcpyAsync(dgbeg, ctx->g_beg, 8 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
-    if (N > 0 && n_lg > 0) {
-        size_t mark = ctx->used;
-        int64_t *f = CH_ALLOC(ctx, int64_t, N), *ex = CH_ALLOC(ctx, int64_t, N);
+    // clock-offset exchange block of this rank (filled by the rank pass, consumed by ch_offsets)
+    {
+        const int64_t K = std::max(1, ctx->cfg.max_coll_per_class);
+        ctx->xW = 4 + 4 * K;
+        ctx->xslots = (int)ceil_div(ctx->cfg.n_traced_gpus, ctx->nranks);
+        if (n_lg > ctx->xslots) return ch_fail(ctx, CHOPPER_E_RANGE, "more local gpus than ceil(n_traced_gpus / nranks)");
+        ctx->d_xsend = CH_ALLOC(ctx, int64_t, (int64_t)ctx->xslots * ctx->xW);
+        ctx->d_xovf = CH_ALLOC(ctx, unsigned int, 1);
         CH_ALLOC_END(ctx);
-        k_flag_nonmemop<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, N, f);
+        CH_CUDA(ctx, cudaMemsetAsync(ctx->d_xsend, 0, 8 * (size_t)ctx->xslots * ctx->xW, ctx->st));
+        CH_CUDA(ctx, cudaMemsetAsync(ctx->d_xovf, 0, 4, ctx->st));
+    }
+    if (N > 0 && n_lg > 0) {
+        // one tile-count pass and one apply pass over meta: non-MEMOP rank (counter-pass position, D2),
+        // AG / RS collective index (D13) written straight into the exchange block
+        const int64_t K = ctx->xW / 4 - 1;
+        int64_t ntile = ceil_div(N, MR_TILE);
+        size_t mark = ctx->used;
+        int64_t *tc = CH_ALLOC(ctx, int64_t, 3 * ntile), *tex = CH_ALLOC(ctx, int64_t, 3 * ntile);
+        int64_t *base = CH_ALLOC(ctx, int64_t, 3 * (n_lg + 1));
+        int32_t *dlg = CH_ALLOC(ctx, int32_t, n_lg + 1);
+        CH_ALLOC_END(ctx);
+        std::vector<int32_t> hlg(ctx->lg_gpu, ctx->lg_gpu + n_lg);
+        CH_CUDA(ctx, cudaMemcpyAsync(dlg, hlg.data(), 4 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+        k_meta_tiles<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, N, tc, ntile);
         CH_LAUNCHED(ctx);
-        CH_TRY(ch_scan_excl_i64(ctx, f, ex, N, nullptr));
-        k_rank_in_gpu<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ex, ctx->ev.meta, N, ctx->d_gpu_lg, dgbeg,
-                                                                     ctx->d_nm_rank);
+        for (int c = 0; c < 3; c++) CH_TRY(ch_scan_excl_i64(ctx, tc + c * ntile, tex + c * ntile, ntile, nullptr));
+        k_gpu_bases<<<1, 3 * (n_lg + 1) > 32 ? 3 * (n_lg + 1) : 32, 0, ctx->st>>>(
+            ctx->ev.meta, N, tex, ntile, dgbeg, n_lg, base, dlg, ctx->d_xsend, ctx->xW);
         CH_LAUNCHED(ctx);
-        // number of non-MEMOP events per gpu
-        std::vector<int64_t> exb(n_lg + 1, 0);
-        for (int l = 0; l < n_lg; l++)
-            CH_CUDA(ctx, cudaMemcpyAsync(&exb[l], ex + ctx->g_beg[l], 8, cudaMemcpyDeviceToHost, ctx->st));
-        int64_t lastf = 0, lastex = 0;
-        CH_CUDA(ctx, cudaMemcpyAsync(&lastf, f + N - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(&lastex, ex + N - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
+        k_meta_apply<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, ctx->ev.end_ns, N,
+                                                             ctx->d_gpu_lg, tex, ntile, base, n_lg, ctx->d_nm_rank,
+                                                             ctx->d_xsend, K, ctx->xW, ctx->d_xovf);
+        CH_LAUNCHED(ctx);
+        std::vector<int64_t> hb(3 * (n_lg + 1));
+        CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), base, 8 * hb.size(), cudaMemcpyDeviceToHost, ctx->st));
         CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-        exb[n_lg] = lastex + lastf;
         ctx->used = mark;
         std::vector<int64_t> m_g(n_lg);
-        for (int l = 0; l < n_lg; l++) m_g[l] = exb[l + 1] - exb[l];
+        for (int l = 0; l < n_lg; l++) m_g[l] = hb[l + 1] - hb[l];
 
         if (n_passes > 0) {
             std::vector<int32_t> off(n_lg + 1, 0), idx;
@@ -376,69 +444,24 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
 }
 
 chopper_status ch_offsets(chopper_ctx *ctx) {
-    const int64_t N = ctx->N;
     const int n_lg = ctx->n_lg, G = ctx->cfg.n_traced_gpus;
-    const int64_t K = std::max(1, ctx->cfg.max_coll_per_class);
-    const int64_t W = 4 + 4 * K;
-    const int slots = (int)ceil_div(G, ctx->nranks);
-    if (n_lg > slots) return ch_fail(ctx, CHOPPER_E_RANGE, "more local gpus than ceil(n_traced_gpus / nranks)");
+    const int64_t W = ctx->xW, K = W / 4 - 1;
+    const int slots = ctx->xslots;
+    (void)n_lg;
     CH_ALLOC_BEGIN;
-    int64_t *send = CH_ALLOC(ctx, int64_t, (int64_t)slots * W);
     int64_t *all = CH_ALLOC(ctx, int64_t, (int64_t)slots * W * ctx->nranks);
     ctx->d_delta = CH_ALLOC(ctx, int64_t, G);
     ctx->d_delta_flag = CH_ALLOC(ctx, int32_t, G);
     unsigned long long *mskew = CH_ALLOC(ctx, unsigned long long, 2);
-    unsigned int *ovf = CH_ALLOC(ctx, unsigned int, 1);
-    int32_t *dlg_gpu = CH_ALLOC(ctx, int32_t, n_lg + 1);
-    int32_t *lastag = CH_ALLOC(ctx, int32_t, n_lg + 1), *lastrs = CH_ALLOC(ctx, int32_t, n_lg + 1);
-    int64_t *dgbeg = CH_ALLOC(ctx, int64_t, n_lg + 1);
     CH_ALLOC_END(ctx);
-    CH_CUDA(ctx, cudaMemsetAsync(send, 0, 8 * slots * W, ctx->st));
     CH_CUDA(ctx, cudaMemsetAsync(ctx->d_delta, 0, 8 * G, ctx->st));
     CH_CUDA(ctx, cudaMemsetAsync(ctx->d_delta_flag, 0, 4 * G, ctx->st));
     CH_CUDA(ctx, cudaMemsetAsync(mskew, 0, 16, ctx->st));
-    CH_CUDA(ctx, cudaMemsetAsync(ovf, 0, 4, ctx->st));
-    std::vector<int32_t> lgg(ctx->lg_gpu, ctx->lg_gpu + n_lg);
-    if (n_lg > 0) CH_CUDA(ctx, cudaMemcpyAsync(dlg_gpu, lgg.data(), 4 * n_lg, cudaMemcpyHostToDevice, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(dgbeg, ctx->g_beg, 8 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
-    if (N > 0 && n_lg > 0) {
-        size_t mark = ctx->used;
-        int64_t *f = CH_ALLOC(ctx, int64_t, N), *ex = CH_ALLOC(ctx, int64_t, N);
-        int32_t *rag = CH_ALLOC(ctx, int32_t, N), *rrs = CH_ALLOC(ctx, int32_t, N);
-        CH_ALLOC_END(ctx);
-        std::vector<int32_t> la(n_lg), lr(n_lg);
-        for (int cls = 0; cls < 2; cls++) {
-            int32_t *r = cls == 0 ? rag : rrs;
-            k_flag_kind<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, N, cls == 0 ? CK_AG : CK_RS, f);
-            CH_LAUNCHED(ctx);
-            CH_TRY(ch_scan_excl_i64(ctx, f, ex, N, nullptr));
-            k_rank_in_gpu<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ex, ctx->ev.meta, N, ctx->d_gpu_lg, dgbeg, r);
-            CH_LAUNCHED(ctx);
-            // count per gpu = rank at gpu end
-            std::vector<int64_t> exb(n_lg + 1, 0);
-            for (int l = 0; l < n_lg; l++)
-                CH_CUDA(ctx, cudaMemcpyAsync(&exb[l], ex + ctx->g_beg[l], 8, cudaMemcpyDeviceToHost, ctx->st));
-            int64_t lf = 0, le = 0;
-            CH_CUDA(ctx, cudaMemcpyAsync(&lf, f + N - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaMemcpyAsync(&le, ex + N - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-            exb[n_lg] = le + lf;
-            for (int l = 0; l < n_lg; l++) (cls == 0 ? la : lr)[l] = (int32_t)(exb[l + 1] - exb[l]);
-        }
-        CH_CUDA(ctx, cudaMemcpyAsync(lastag, la.data(), 4 * n_lg, cudaMemcpyHostToDevice, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(lastrs, lr.data(), 4 * n_lg, cudaMemcpyHostToDevice, ctx->st));
-        k_coll_scatter<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, ctx->ev.end_ns, N,
-                                                                      ctx->d_gpu_lg, rag, rrs, K, W, send, ovf);
-        CH_LAUNCHED(ctx);
-        k_coll_header<<<1, 256, 0, ctx->st>>>(send, W, n_lg, dlg_gpu, lastag, lastrs);
-        CH_LAUNCHED(ctx);
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-        ctx->used = mark;
-    }
+    // NCCL all-gather #1: every rank's collective-end vectors (D13)
     if (ctx->nranks > 1) {
-        CH_TRY(ch_nccl_allgather(ctx, send, all, sizeof(int64_t) * slots * W));
+        CH_TRY(ch_nccl_allgather(ctx, ctx->d_xsend, all, sizeof(int64_t) * slots * W));
     } else {
-        CH_CUDA(ctx, cudaMemcpyAsync(all, send, 8 * slots * W, cudaMemcpyDeviceToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(all, ctx->d_xsend, 8 * slots * W, cudaMemcpyDeviceToDevice, ctx->st));
     }
     int nslots = slots * ctx->nranks;
     k_delta<<<nslots, 256, 0, ctx->st>>>(all, nslots, W, K, ctx->d_delta, ctx->d_delta_flag);
@@ -449,18 +472,17 @@ chopper_status ch_offsets(chopper_ctx *ctx) {
     ctx->delta_flag.assign(G, 1);
     unsigned long long hs[2] = {0, 0};
     unsigned int hovf = 0;
+    std::vector<int64_t> hdr(2 * (size_t)nslots);
     CH_CUDA(ctx, cudaMemcpyAsync(ctx->delta.data(), ctx->d_delta, 8 * G, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(ctx->delta_flag.data(), ctx->d_delta_flag, 4 * G, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(hs, mskew, 16, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ctx->d_xovf, 4, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpy2DAsync(hdr.data(), 16, all, 8 * (size_t)W, 16, nslots, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-    // gpus absent from every rank keep flag 1 (no events): mark present ones from the headers
-    std::vector<int64_t> hdr((size_t)nslots * W);
-    CH_CUDA(ctx, cudaMemcpyAsync(hdr.data(), all, 8 * (size_t)nslots * W, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    // gpus absent from every rank keep flag 1 (no events)
     ctx->gpu_present.assign(G, 0);
     for (int b = 0; b < nslots; b++)
-        if (hdr[(size_t)b * W + 1]) ctx->gpu_present[hdr[(size_t)b * W]] = 1;
+        if (hdr[2 * (size_t)b + 1]) ctx->gpu_present[hdr[2 * (size_t)b]] = 1;
     for (int g = 0; g < G; g++) if (!ctx->gpu_present[g]) { ctx->delta_flag[g] = 1; ctx->delta[g] = 0; }
     ctx->max_skew[0] = (int64_t)hs[0];
     ctx->max_skew[1] = (int64_t)hs[1];

@@ -161,6 +161,10 @@ struct chopper_ctx {
     const double **d_col = nullptr;  // [n_lg][C] value column of the pass providing the slot
     std::vector<int64_t> pass_mismatch, pass_conflict;
     std::vector<int> gpu_present;    // [n_traced] gpu has events on some rank
+    int64_t *d_xsend = nullptr;      // clock-offset exchange block of this rank [xslots][xW]
+    unsigned int *d_xovf = nullptr;
+    int64_t xW = 0;
+    int xslots = 0;
 
     // tables
     RowTable inst, layer, phase, iter, gpurow, point;

@@ -169,19 +169,6 @@ struct EvParams {
     unsigned int *ticket;
 };
 
-__device__ __forceinline__ unsigned long long event_key(const EvParams &P, int64_t i, int lg, int64_t t, int64_t *cur) {
-    int64_t r[4];
-    bool ok = true;
-#pragma unroll
-    for (int lv = 0; lv < 4; lv++) {
-        int64_t c = span_lookup(P.sv, lg, lv, t, i, &cur[lv]);
-        if (c == -2) ok = false;
-        r[lv] = c >= 0 ? c - P.sv.list_beg[lg * 4 + lv] + 1 : 0;
-    }
-    if (!ok || r[0] == 0) return CH_INVALID_KEY;
-    return ((unsigned long long)lg << P.sh_lg) | ((unsigned long long)r[0] << P.sh_it) |
-           ((unsigned long long)r[1] << P.sh_ph) | ((unsigned long long)r[2] << P.sh_ly) | (unsigned long long)r[3];
-}
 
 // last index in [lo, hi) with a[idx] <= t, seeded by the previous answer (t mostly non-decreasing)
 __device__ __forceinline__ int64_t seek(const int64_t *__restrict__ a, int64_t lo, int64_t hi, int64_t t, int64_t *cur) {
@@ -373,7 +360,15 @@ __device__ __forceinline__ void smp_reset(SmpCache &c, int64_t lo, int64_t hi) {
 }
 __device__ __forceinline__ void smp_F(SmpCache &c, const EvParams &P, int64_t t, int64_t *F, int64_t *Pw) {
     if (!(c.q != -2 && t < c.next && (c.q == c.lo || t >= c.ts))) {
-        int64_t q = last_le(P.smp_ts, c.lo, c.hi, t);
+        int64_t q;
+        if (c.q != -2 && t >= c.next) {    // forward from the cached window (t mostly increases)
+            q = c.q + 1;
+            int steps = 0;
+            while (q + 1 < c.hi && __ldg(P.smp_ts + q + 1) <= t && steps < 4) { q++; steps++; }
+            if (q + 1 < c.hi && __ldg(P.smp_ts + q + 1) <= t) q = last_le(P.smp_ts, q + 1, c.hi, t);
+        } else {
+            q = last_le(P.smp_ts, c.lo, c.hi, t);
+        }
         if (q < c.lo) q = c.lo;            // before the first sample: f_0 extended backwards (D10)
         c.q = (int32_t)q;
         c.ts = __ldg(P.smp_ts + q);

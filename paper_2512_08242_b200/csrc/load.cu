@@ -122,7 +122,7 @@ __global__ void k_make_keys(const uint32_t *__restrict__ meta, const int64_t *__
 __global__ void k_chain(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ meta,
                         const int64_t *__restrict__ ks, const int64_t *__restrict__ ke, int64_t n,
                         const int32_t *__restrict__ gpu_lg, int NG, int other, int64_t *__restrict__ pred_end,
-                        DevReport *rep) {
+                        DevReport *rep, unsigned int *__restrict__ bflag) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     uint32_t i = perm[j];
@@ -138,13 +138,34 @@ __global__ void k_chain(const uint32_t *__restrict__ perm, const uint32_t *__res
     int64_t pe = CH_NONE_TS;
     if (same && grp != other) {
         int64_t a = ks[i];
-        if (a < ks[ip]) atomicOr(&rep->flags, 1u);   // not start-monotone: full sort needed
+        if (a < ks[ip]) bflag[b] = 1u;                 // bucket not start-monotone: sort it
         if (grp >= 1) {
             pe = ke[ip];
             if (a < pe) viol(rep, CV_STREAM_OVERLAP, i);
         }
     }
     if (kind_of(m) == CK_COMPUTE) pred_end[i] = pe;
+}
+
+// keys of the events in the flagged bucket segments: (segment, t_ks - t0), value = input index
+__global__ void k_seg_keys(const uint32_t *__restrict__ perm, const int64_t *__restrict__ ks,
+                           const int64_t *__restrict__ lo, const int64_t *__restrict__ pre, int nseg, int64_t M,
+                           int64_t t0, int tsbits, unsigned long long *__restrict__ key, uint32_t *__restrict__ val) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M) return;
+    int a = 0, b = nseg;                       // segment: last pre[s] <= t
+    while (b - a > 1) { int m = (a + b) >> 1; if (pre[m] <= t) a = m; else b = m; }
+    uint32_t i = perm[lo[a] + (t - pre[a])];
+    key[t] = ((unsigned long long)a << tsbits) | (unsigned long long)(ks[i] - t0);
+    val[t] = i;
+}
+__global__ void k_seg_scatter(const uint32_t *__restrict__ sorted, const int64_t *__restrict__ lo,
+                              const int64_t *__restrict__ pre, int nseg, int64_t M, uint32_t *__restrict__ perm) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M) return;
+    int a = 0, b = nseg;
+    while (b - a > 1) { int m = (a + b) >> 1; if (pre[m] <= t) a = m; else b = m; }
+    perm[lo[a] + (t - pre[a])] = sorted[t];
 }
 
 __global__ void k_bucket_begins(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ meta, int64_t n,
@@ -290,53 +311,79 @@ chopper_status ch_load(chopper_ctx *ctx) {
     }
     ctx->used = mark;
     ctx->full_sort = false;
+    const int nb = ctx->n_buckets;
+    unsigned int *bflag = CH_ALLOC(ctx, unsigned int, nb + 1);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemsetAsync(bflag, 0, 4 * (nb + 1), ctx->st));
+    // bucket begins (unchanged by the per-bucket timestamp sort below)
+    unsigned long long *beg = reinterpret_cast<unsigned long long *>(ctx->d_bucket_beg);
+    CH_TRY(ch_fill_u64(ctx, beg, nb + 1, ~0ull));
+    k_bucket_begins<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, n, ctx->d_gpu_lg, NG,
+                                                                   other, beg);
+    CH_LAUNCHED(ctx);
     k_chain<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
                                                            ctx->ev.end_ns, n, ctx->d_gpu_lg, NG, other,
-                                                           ctx->d_pred_end, ctx->d_rep);
+                                                           ctx->d_pred_end, ctx->d_rep, bflag);
     CH_LAUNCHED(ctx);
+    ctx->bucket_beg.assign(nb + 1, 0);
+    std::vector<unsigned int> hflag(nb + 1, 0);
+    CH_CUDA(ctx, cudaMemcpyAsync(ctx->bucket_beg.data(), beg, 8 * (nb + 1), cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(hflag.data(), bflag, 4 * (nb + 1), cudaMemcpyDeviceToHost, ctx->st));
     CH_TRY(read_report(ctx));
-    if (ctx->h_rep.flags & 1u) {
-        // full stable sort by (bucket, t_ks - t0), D1
+    ctx->bucket_beg[nb] = n;
+    for (int b = nb - 1; b >= 0; b--)
+        if ((unsigned long long)ctx->bucket_beg[b] == ~0ull) ctx->bucket_beg[b] = ctx->bucket_beg[b + 1];
+    CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_bucket_beg, ctx->bucket_beg.data(), 8 * (nb + 1), cudaMemcpyHostToDevice,
+                                 ctx->st));
+    // buckets that are not start-monotone in dispatch order: stable timestamp sort of just those segments (D1)
+    std::vector<int64_t> seg_lo, seg_pre;
+    bool compute_resorted = false;
+    int64_t Mseg = 0;
+    for (int b = 0; b < nb; b++)
+        if (hflag[b]) {
+            seg_lo.push_back(ctx->bucket_beg[b]);
+            seg_pre.push_back(Mseg);
+            Mseg += ctx->bucket_beg[b + 1] - ctx->bucket_beg[b];
+            if (b % NG >= 1 && b % NG != other) compute_resorted = true;
+        }
+    if (Mseg > 0) {
+        const int nseg = (int)seg_lo.size();
+        seg_pre.push_back(Mseg);
         int tsbits = bits_for((uint64_t)(ctx->t_max - ctx->t0));
-        int bb = bits_for((uint64_t)ctx->n_buckets);
-        if (tsbits + bb > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "sort key exceeds 64 bits");
-        unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, n), *k2 = CH_ALLOC(ctx, unsigned long long, n);
-        uint32_t *v2 = CH_ALLOC(ctx, uint32_t, n);
+        int sb = bits_for((uint64_t)nseg);
+        if (tsbits + sb > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "sort key exceeds 64 bits");
+        size_t mk = ctx->used;
+        unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, Mseg), *k2 = CH_ALLOC(ctx, unsigned long long, Mseg);
+        uint32_t *v1 = CH_ALLOC(ctx, uint32_t, Mseg), *v2 = CH_ALLOC(ctx, uint32_t, Mseg);
+        int64_t *dlo = CH_ALLOC(ctx, int64_t, nseg + 1), *dpre = CH_ALLOC(ctx, int64_t, nseg + 1);
         CH_ALLOC_END(ctx);
-        k_make_keys<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, n, ctx->d_gpu_lg,
-                                                                   NG, other, ctx->t0, tsbits, k1, ctx->d_perm);
+        seg_lo.push_back(n);
+        CH_CUDA(ctx, cudaMemcpyAsync(dlo, seg_lo.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(dpre, seg_pre.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
+        k_seg_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.start_ns, dlo, dpre, nseg, Mseg,
+                                                                     ctx->t0, tsbits, k1, v1);
         CH_LAUNCHED(ctx);
         bool alt;
-        CH_TRY(ch_radix_sort(ctx, k1, ctx->d_perm, k2, v2, n, 0, tsbits + bb, &alt));
-        if (alt) CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_perm, v2, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, ctx->st));
-        ctx->used = mark;
+        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, tsbits + sb, &alt));
+        k_seg_scatter<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(alt ? v2 : v1, dlo, dpre, nseg, Mseg,
+                                                                        ctx->d_perm);
+        CH_LAUNCHED(ctx);
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));   // host vectors above go out of scope
+        ctx->used = mk;
         ctx->full_sort = true;
-        // reset the disjointness counters and recompute the chain in the true sorted order
-        unsigned long long zero = 0, none = ~0ull;
-        CH_CUDA(ctx, cudaMemcpyAsync(&ctx->d_rep->val_count[CV_STREAM_OVERLAP], &zero, 8, cudaMemcpyHostToDevice, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(&ctx->d_rep->val_first[CV_STREAM_OVERLAP], &none, 8, cudaMemcpyHostToDevice, ctx->st));
-        k_chain<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
-                                                               ctx->ev.end_ns, n, ctx->d_gpu_lg, NG, other,
-                                                               ctx->d_pred_end, ctx->d_rep);
-        CH_LAUNCHED(ctx);
-    }
-    // bucket begins in sorted order
-    {
-        unsigned long long *beg = reinterpret_cast<unsigned long long *>(ctx->d_bucket_beg);
-        CH_TRY(ch_fill_u64(ctx, beg, ctx->n_buckets + 1, ~0ull));
-        k_bucket_begins<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, n, ctx->d_gpu_lg, NG,
-                                                                       other, beg);
-        CH_LAUNCHED(ctx);
-        ctx->bucket_beg.assign(ctx->n_buckets + 1, 0);
-        CH_CUDA(ctx, cudaMemcpyAsync(ctx->bucket_beg.data(), beg, 8 * (ctx->n_buckets + 1), cudaMemcpyDeviceToHost,
-                                     ctx->st));
-        CH_TRY(read_report(ctx));
-        // empty buckets begin where the next non-empty one does
-        ctx->bucket_beg[ctx->n_buckets] = n;
-        for (int b = ctx->n_buckets - 1; b >= 0; b--)
-            if ((unsigned long long)ctx->bucket_beg[b] == ~0ull) ctx->bucket_beg[b] = ctx->bucket_beg[b + 1];
-        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_bucket_beg, ctx->bucket_beg.data(), 8 * (ctx->n_buckets + 1),
-                                     cudaMemcpyHostToDevice, ctx->st));
+        if (compute_resorted) {
+            // chain predecessors and the disjointness check depend on the corrected order
+            unsigned long long zero = 0, none = ~0ull;
+            CH_CUDA(ctx, cudaMemcpyAsync(&ctx->d_rep->val_count[CV_STREAM_OVERLAP], &zero, 8, cudaMemcpyHostToDevice,
+                                         ctx->st));
+            CH_CUDA(ctx, cudaMemcpyAsync(&ctx->d_rep->val_first[CV_STREAM_OVERLAP], &none, 8, cudaMemcpyHostToDevice,
+                                         ctx->st));
+            k_chain<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
+                                                                   ctx->ev.end_ns, n, ctx->d_gpu_lg, NG, other,
+                                                                   ctx->d_pred_end, ctx->d_rep, bflag);
+            CH_LAUNCHED(ctx);
+            CH_TRY(read_report(ctx));
+        }
     }
     // same-stream overlaps are data: reported, processing continues
     fill_public_report(ctx);
