@@ -101,25 +101,26 @@ __global__ void __launch_bounds__(MR_NT) k_meta_tiles(const uint32_t *__restrict
 }
 // base[c][lg] = global exclusive count of predicate c at the gpu's first event (lg = n_lg -> N);
 // also writes the exchange header (gpu, present, #AG, #RS) of every local gpu
+// one warp per (predicate, gpu boundary): tile prefix + the packed counts of the partial tile before it
 __global__ void k_gpu_bases(const uint32_t *__restrict__ meta, int64_t n, const int64_t *__restrict__ tex,
                             int64_t ntile, const int64_t *__restrict__ gbeg, int n_lg, int64_t *__restrict__ base,
                             const int32_t *__restrict__ lg_gpu, int64_t *__restrict__ xsend, int64_t W) {
-    int t = threadIdx.x;
-    if (t < 3 * (n_lg + 1)) {
-        int c = t / (n_lg + 1), lg = t % (n_lg + 1);
+    const int w = threadIdx.x >> 5, l = lane_id();
+    for (int job = w; job < 3 * (n_lg + 1); job += blockDim.x >> 5) {
+        int c = job / (n_lg + 1), lg = job % (n_lg + 1);
         int64_t pos = gbeg[lg];
         int64_t tile = pos / MR_TILE;
-        int64_t b = 0;
-        if (tile < ntile) {
-            b = tex[c * ntile + tile];
-            for (int64_t i = tile * MR_TILE; i < pos; i++) b += (int64_t)((pred3(meta[i]) >> (21 * c)) & 0x1FFFFF);
-        } else {
-            b = tex[c * ntile + ntile - 1];
-            for (int64_t i = (ntile - 1) * MR_TILE; i < n; i++) b += (int64_t)((pred3(meta[i]) >> (21 * c)) & 0x1FFFFF);
-        }
-        base[c * (n_lg + 1) + lg] = b;
+        int64_t lo, hi, b;
+        if (tile < ntile) { b = tex[c * ntile + tile]; lo = tile * MR_TILE; hi = pos; }
+        else { b = tex[c * ntile + ntile - 1]; lo = (ntile - 1) * MR_TILE; hi = n; }
+        int64_t part = 0;
+        for (int64_t i = lo + l; i < hi; i += 32) part += (int64_t)((pred3(meta[i]) >> (21 * c)) & 0x1FFFFF);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(CH_FULL, part, o);
+        if (l == 0) base[c * (n_lg + 1) + lg] = b + part;
     }
     __syncthreads();
+    const int t = threadIdx.x;
     if (t < n_lg && xsend) {
         int64_t *h = xsend + (int64_t)t * W;
         h[0] = lg_gpu[t];
@@ -174,16 +175,21 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
 
 
 // one block per gathered gpu slot: lower median of collective-end differences (radix select)
-__global__ void __launch_bounds__(256) k_delta(const int64_t *__restrict__ all, int nslots, int64_t W, int64_t K,
-                                               int64_t *__restrict__ delta, int32_t *__restrict__ dflag) {
-    __shared__ unsigned int hist[256];
+// one 1024-thread block per gathered gpu slot: lower median of the collective-end differences by radix
+// select on (d - min d): a min/max pass first, so only the bytes in which the differences vary are
+// selected on (differences are microseconds: 2-3 passes instead of 8), with per-warp histograms.
+constexpr int DL_NT = 1024, DL_W = DL_NT / 32;
+__global__ void __launch_bounds__(DL_NT) k_delta(const int64_t *__restrict__ all, int nslots, int64_t W, int64_t K,
+                                                 int64_t *__restrict__ delta, int32_t *__restrict__ dflag) {
+    __shared__ unsigned int hist[DL_W][256];
     __shared__ int s_ref;
     __shared__ int64_t s_m[2];
-    __shared__ unsigned long long s_prefix;
+    __shared__ unsigned long long s_prefix, s_lo[DL_W], s_hi[DL_W];
     __shared__ int64_t s_k;
     const int64_t *me = all + (int64_t)blockIdx.x * W;
     if (me[1] == 0) return;
-    int g = (int)me[0];
+    const int g = (int)me[0];
+    const int w = threadIdx.x >> 5, l = lane_id();
     if (threadIdx.x == 0) {
         int ref = -1, refg = 1 << 30;
         int64_t m0 = -1, m1 = -1;
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(256) k_delta(const int64_t *__restrict__ all, 
     }
     __syncthreads();
     const int64_t *rf = all + (int64_t)s_ref * W;
-    int64_t m0 = s_m[0], m1 = s_m[1], nd = m0 + m1;
+    const int64_t m0 = s_m[0], m1 = s_m[1], nd = m0 + m1;
     if (nd == 0) {
         if (threadIdx.x == 0) { delta[g] = 0; dflag[g] = 1; }
         return;
@@ -211,31 +217,62 @@ __global__ void __launch_bounds__(256) k_delta(const int64_t *__restrict__ all, 
         else d = me[4 + 3 * K + (q - m0)] - rf[4 + 3 * K + (q - m0)];
         return enc_i64(d);
     };
-    if (threadIdx.x == 0) { s_prefix = 0; s_k = (nd - 1) / 2; }
+    // range of the (order-preserving encoded) differences
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int64_t q = threadIdx.x; q < nd; q += DL_NT) {
+        unsigned long long v = dval(q);
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long a2 = __shfl_xor_sync(CH_FULL, lo, o), b2 = __shfl_xor_sync(CH_FULL, hi, o);
+        lo = a2 < lo ? a2 : lo;
+        hi = b2 > hi ? b2 : hi;
+    }
+    if (l == 0) { s_lo[w] = lo; s_hi[w] = hi; }
     __syncthreads();
-    for (int byte = 7; byte >= 0; byte--) {
-        hist[threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+        unsigned long long a2 = ~0ull, b2 = 0ull;
+        for (int x = 0; x < DL_W; x++) { a2 = s_lo[x] < a2 ? s_lo[x] : a2; b2 = s_hi[x] > b2 ? s_hi[x] : b2; }
+        s_lo[0] = a2;
+        s_hi[0] = b2;
+        s_prefix = 0;
+        s_k = (nd - 1) / 2;
+    }
+    __syncthreads();
+    const unsigned long long vmin = s_lo[0], span = s_hi[0] - vmin;
+    int top = 0;
+    while (top < 8 && (span >> (8 * top)) != 0) top++;      // bytes of (v - vmin) that vary
+    for (int byte = top - 1; byte >= 0; byte--) {
+        for (int d = threadIdx.x; d < DL_W * 256; d += DL_NT) (&hist[0][0])[d] = 0;
         __syncthreads();
-        unsigned long long pre = s_prefix;
-        unsigned long long hmask = byte == 7 ? 0ull : (~0ull << (8 * (byte + 1)));
-        for (int64_t q = threadIdx.x; q < nd; q += blockDim.x) {
-            unsigned long long v = dval(q);
-            if ((v & hmask) == (pre & hmask)) atomicAdd(&hist[(v >> (8 * byte)) & 0xFF], 1u);
+        const unsigned long long pre = s_prefix;
+        const unsigned long long hmask = ~0ull << (8 * (byte + 1));
+        for (int64_t q = threadIdx.x; q < nd; q += DL_NT) {
+            unsigned long long v = dval(q) - vmin;
+            if ((v & hmask) == (pre & hmask)) atomicAdd(&hist[w][(v >> (8 * byte)) & 0xFF], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 256) {        // fold the per-warp histograms
+            unsigned int c = 0;
+            for (int x = 0; x < DL_W; x++) c += hist[x][threadIdx.x];
+            hist[0][threadIdx.x] = c;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             int64_t k = s_k;
             int d = 0;
             for (; d < 256; d++) {
-                if (k < (int64_t)hist[d]) break;
-                k -= hist[d];
+                if (k < (int64_t)hist[0][d]) break;
+                k -= hist[0][d];
             }
             s_k = k;
             s_prefix = pre | ((unsigned long long)d << (8 * byte));
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) { delta[g] = dec_i64(s_prefix); dflag[g] = 0; }
+    if (threadIdx.x == 0) { delta[g] = dec_i64(s_prefix + vmin); dflag[g] = 0; }
 }
 
 __global__ void k_skew(const int64_t *__restrict__ all, int nslots, int64_t W, int64_t K,
@@ -291,6 +328,7 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
     const int n_lg = ctx->n_lg, C = n_counters;
     ctx->C = C;
     ctx->passes.clear();
+    ctx->pass_slots.clear();
     std::vector<std::vector<int>> by_lg(n_lg);
     for (int p = 0; p < n_passes; p++) {
         const chopper_counter_pass &q = passes[p];
@@ -299,17 +337,18 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         for (int kk = 0; kk < q.k; kk++)
             if (q.slot[kk] < 0 || q.slot[kk] >= C) return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "counter slot out of range");
         ctx->passes.push_back(PassDesc{q.name_id, q.values, q.n, q.k, lg});
+        ctx->pass_slots.push_back(std::vector<int32_t>(q.slot, q.slot + q.k));
         by_lg[lg].push_back(p);
     }
     CH_ALLOC_BEGIN;
     ctx->d_nm_rank = CH_ALLOC(ctx, int32_t, N);
     ctx->d_passes = CH_ALLOC(ctx, PassDesc, n_passes + 1);
-    ctx->d_present = CH_ALLOC(ctx, int32_t, (int64_t)n_lg * (C > 0 ? C : 1));
-    const double **col = CH_ALLOC(ctx, const double *, (int64_t)n_lg * (C > 0 ? C : 1));
     int64_t *dgbeg = CH_ALLOC(ctx, int64_t, n_lg + 1);
     CH_ALLOC_END(ctx);
-    ctx->present.assign((size_t)n_lg * (C > 0 ? C : 1), 0);
-    std::vector<const double *> hcol((size_t)n_lg * (C > 0 ? C : 1), nullptr);
+    ctx->d_conf = nullptr;
+    ctx->h_col_dev = nullptr;
+    ctx->d_present = nullptr;
+    ctx->pass_mismatch.assign(n_passes, -1);
     CH_CUDA(ctx, cudaMemcpyAsync(dgbeg, ctx->g_beg, 8 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
     // clock-offset exchange block of this rank (filled by the rank pass, consumed by ch_offsets)
     {
@@ -338,7 +377,7 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         k_meta_tiles<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, N, tc, ntile);
         CH_LAUNCHED(ctx);
         for (int c = 0; c < 3; c++) CH_TRY(ch_scan_excl_i64(ctx, tc + c * ntile, tex + c * ntile, ntile, nullptr));
-        k_gpu_bases<<<1, 3 * (n_lg + 1) > 32 ? 3 * (n_lg + 1) : 32, 0, ctx->st>>>(
+        k_gpu_bases<<<1, 1024, 0, ctx->st>>>(
             ctx->ev.meta, N, tex, ntile, dgbeg, n_lg, base, dlg, ctx->d_xsend, ctx->xW);
         CH_LAUNCHED(ctx);
         k_meta_apply<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, ctx->ev.end_ns, N,
@@ -361,85 +400,132 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
             off[n_lg] = (int32_t)idx.size();
             int32_t *doff = CH_ALLOC(ctx, int32_t, n_lg + 1), *didx = CH_ALLOC(ctx, int32_t, n_passes);
             unsigned long long *mis = CH_ALLOC(ctx, unsigned long long, n_passes);
-            unsigned int *bad = CH_ALLOC(ctx, unsigned int, n_passes);
-            unsigned long long *conf = CH_ALLOC(ctx, unsigned long long, n_passes);
             CH_ALLOC_END(ctx);
             CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_passes, ctx->passes.data(), sizeof(PassDesc) * n_passes,
                                          cudaMemcpyHostToDevice, ctx->st));
             CH_CUDA(ctx, cudaMemcpyAsync(doff, off.data(), 4 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
             CH_CUDA(ctx, cudaMemcpyAsync(didx, idx.data(), 4 * n_passes, cudaMemcpyHostToDevice, ctx->st));
             CH_TRY(ch_fill_u64(ctx, mis, n_passes, ~0ull));
-            CH_TRY(ch_fill_u64(ctx, conf, n_passes, ~0ull));
-            CH_CUDA(ctx, cudaMemsetAsync(bad, 0, 4 * n_passes, ctx->st));
             k_pass_check<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.name_id, N, ctx->d_gpu_lg,
                                                                         ctx->d_nm_rank, ctx->d_passes, doff, didx, mis);
             CH_LAUNCHED(ctx);
-            k_pass_finite<<<dim3(148 * 2, n_passes), NT, 0, ctx->st>>>(ctx->d_passes, bad);
-            CH_LAUNCHED(ctx);
             std::vector<unsigned long long> hmis(n_passes);
-            std::vector<unsigned int> hbad(n_passes);
             CH_CUDA(ctx, cudaMemcpyAsync(hmis.data(), mis, 8 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaMemcpyAsync(hbad.data(), bad, 4 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
             CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
             ctx->pass_mismatch.assign(n_passes, -1);
-            ctx->pass_conflict.assign(n_passes, -1);
-            // slot assignment: first valid pass wins; later passes checked for conflicts
-            std::vector<std::pair<int, int>> first((size_t)n_lg * (C > 0 ? C : 1), {-1, -1});
             for (int p = 0; p < n_passes; p++) {
                 const PassDesc &d = ctx->passes[p];
                 int64_t mg = m_g[d.lg];
                 int64_t lim = d.n < mg ? d.n : mg;
                 int64_t mj = hmis[p] == ~0ull ? -1 : (int64_t)hmis[p];
                 if (mj < 0 && d.n != mg) mj = lim;
-                if (mj >= 0) {
-                    ctx->pass_mismatch[p] = mj;
-                    ctx->latched_host |= 1u << CHOPPER_E_ALIGNMENT;
-                    continue;
-                }
-                if (hbad[p]) {
-                    ctx->rep.val_count[CV_COUNTER_NONFINITE]++;
-                    if (ctx->rep.val_first[CV_COUNTER_NONFINITE] < 0 || p < ctx->rep.val_first[CV_COUNTER_NONFINITE])
-                        ctx->rep.val_first[CV_COUNTER_NONFINITE] = p;
-                    ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
-                    continue;
-                }
-                for (int kk = 0; kk < d.k; kk++) {
-                    int s = passes[p].slot[kk];
-                    auto &f0 = first[(size_t)d.lg * C + s];
-                    if (f0.first < 0) {
-                        f0 = {p, kk};
-                        hcol[(size_t)d.lg * C + s] = d.values + (int64_t)kk * d.n;
-                        ctx->present[(size_t)d.lg * C + s] = 1;
-                    } else {
-                        const PassDesc &a = ctx->passes[f0.first];
-                        k_pass_conflict<<<64, NT, 0, ctx->st>>>(a.values + (int64_t)f0.second * a.n,
-                                                                d.values + (int64_t)kk * d.n, d.n, conf + p);
-                        CH_LAUNCHED(ctx);
-                    }
-                }
+                ctx->pass_mismatch[p] = mj;
             }
-            std::vector<unsigned long long> hconf(n_passes);
-            CH_CUDA(ctx, cudaMemcpyAsync(hconf.data(), conf, 8 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-            for (int p = 0; p < n_passes; p++)
-                if (hconf[p] != ~0ull) {
-                    ctx->pass_conflict[p] = (int64_t)hconf[p];
-                    ctx->latched_host |= 1u << CHOPPER_E_ALIGNMENT;
-                }
         }
     }
-    if (C > 0) {
-        CH_CUDA(ctx, cudaMemcpyAsync(col, hcol.data(), sizeof(double *) * hcol.size(), cudaMemcpyHostToDevice, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_present, ctx->present.data(), 4 * ctx->present.size(),
-                                     cudaMemcpyHostToDevice, ctx->st));
+    // slot assignment, speculatively treating every name-matching pass as finite: the columns that feed
+    // a slot are checked for finiteness by the counter pass itself (ch_tables), which then redoes the
+    // assignment if one was not; name-matching passes with a column feeding no slot are checked here.
+    ctx->pass_bad.assign(n_passes, 0);
+    CH_TRY(ch_assign_slots(ctx));
+    if (n_passes > 0) {
+        ctx->d_pass_bad = CH_ALLOC(ctx, unsigned int, n_passes);
+        CH_ALLOC_END(ctx);
+        CH_CUDA(ctx, cudaMemsetAsync(ctx->d_pass_bad, 0, 4 * n_passes, ctx->st));
+        bool any = false;
+        for (int p = 0; p < n_passes; p++) any |= ctx->pass_mismatch[p] < 0 && !ctx->pass_covered[p];
+        if (any) {
+            // every pass gets a grid row; covered / mismatched ones exit at once
+            std::vector<PassDesc> pd(ctx->passes);
+            for (int p = 0; p < n_passes; p++)
+                if (ctx->pass_mismatch[p] >= 0 || ctx->pass_covered[p]) pd[p].n = 0;
+            PassDesc *dpd = CH_ALLOC(ctx, PassDesc, n_passes);
+            CH_ALLOC_END(ctx);
+            CH_CUDA(ctx, cudaMemcpyAsync(dpd, pd.data(), sizeof(PassDesc) * n_passes, cudaMemcpyHostToDevice, ctx->st));
+            k_pass_finite<<<dim3(148 * 2, n_passes), NT, 0, ctx->st>>>(dpd, ctx->d_pass_bad);
+            CH_LAUNCHED(ctx);
+            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));   // pd goes out of scope
+        }
     }
-    ctx->d_col = col;
-    if (counters_out && C > 0 && N > 0) {
-        k_counters_out<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, N, ctx->d_gpu_lg, ctx->d_nm_rank, col,
-                                                                      C, counters_out);
-        CH_LAUNCHED(ctx);
-    }
+    ctx->counters_out = (counters_out && C > 0 && N > 0) ? counters_out : nullptr;
+    CH_TRY(ch_counters_full(ctx));
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    return CHOPPER_OK;
+}
+
+chopper_status ch_counters_full(chopper_ctx *ctx) {
+    if (!ctx->counters_out) return CHOPPER_OK;
+    k_counters_out<<<(unsigned)ceil_div(ctx->N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->N, ctx->d_gpu_lg, ctx->d_nm_rank,
+                                                                       ctx->d_col, ctx->C, ctx->counters_out);
+    CH_LAUNCHED(ctx);
+    return CHOPPER_OK;
+}
+
+// slot -> value column: in pass order, the first pass that matches the name sequence and is not known
+// to be non-finite provides each slot (O3); later passes with the same slot are checked for conflicts.
+chopper_status ch_assign_slots(chopper_ctx *ctx) {
+    const int n_lg = ctx->n_lg, C = ctx->C;
+    const int n_passes = (int)ctx->passes.size();
+    const size_t nc = (size_t)std::max(n_lg, 1) * (C > 0 ? C : 1);
+    ctx->present.assign(nc, 0);
+    ctx->sel_pass.assign(nc, -1);
+    ctx->pass_conflict.assign(n_passes, -1);
+    ctx->pass_covered.assign(n_passes, 0);
+    std::vector<int> sel_k(nc, -1);
+    std::vector<const double *> hcol(nc, nullptr);
+    if (!ctx->d_conf && n_passes > 0) {
+        CH_ALLOC_BEGIN;
+        ctx->d_conf = CH_ALLOC(ctx, unsigned long long, n_passes);
+        CH_ALLOC_END(ctx);
+    }
+    if (n_passes > 0) CH_TRY(ch_fill_u64(ctx, ctx->d_conf, n_passes, ~0ull));
+    bool conflicts = false;
+    for (int p = 0; p < n_passes; p++) {
+        const PassDesc &d = ctx->passes[p];
+        if (ctx->pass_mismatch[p] >= 0 || ctx->pass_bad[p]) continue;
+        int cov = 1;
+        for (int kk = 0; kk < d.k; kk++) {
+            int s = ctx->pass_slots[p][kk];
+            size_t q = (size_t)d.lg * C + s;
+            if (ctx->sel_pass[q] < 0) {
+                ctx->sel_pass[q] = p;
+                sel_k[q] = kk;
+                hcol[q] = d.values + (int64_t)kk * d.n;
+                ctx->present[q] = 1;
+            } else {
+                cov = 0;
+                const PassDesc &a = ctx->passes[ctx->sel_pass[q]];
+                k_pass_conflict<<<64, NT, 0, ctx->st>>>(a.values + (int64_t)sel_k[q] * a.n, d.values + (int64_t)kk * d.n,
+                                                        d.n, ctx->d_conf + p);
+                CH_LAUNCHED(ctx);
+                conflicts = true;
+            }
+        }
+        ctx->pass_covered[p] = cov;
+    }
+    if (conflicts) {
+        std::vector<unsigned long long> hconf(n_passes);
+        CH_CUDA(ctx, cudaMemcpyAsync(hconf.data(), ctx->d_conf, 8 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        for (int p = 0; p < n_passes; p++)
+            if (hconf[p] != ~0ull) ctx->pass_conflict[p] = (int64_t)hconf[p];
+    }
+    // E_ALIGNMENT from name mismatches and conflicts of this assignment
+    ctx->latched_host &= ~(1u << CHOPPER_E_ALIGNMENT);
+    for (int p = 0; p < n_passes; p++)
+        if (ctx->pass_mismatch[p] >= 0 || ctx->pass_conflict[p] >= 0) ctx->latched_host |= 1u << CHOPPER_E_ALIGNMENT;
+    if (C > 0) {
+        if (!ctx->h_col_dev) {
+            CH_ALLOC_BEGIN;
+            ctx->h_col_dev = CH_ALLOC(ctx, const double *, (int64_t)nc);
+            ctx->d_present = CH_ALLOC(ctx, int32_t, (int64_t)nc);
+            CH_ALLOC_END(ctx);
+        }
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->h_col_dev, hcol.data(), sizeof(double *) * nc, cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_present, ctx->present.data(), 4 * nc, cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));   // hcol goes out of scope
+    }
+    ctx->d_col = ctx->h_col_dev;
     return CHOPPER_OK;
 }
 
@@ -464,7 +550,7 @@ chopper_status ch_offsets(chopper_ctx *ctx) {
         CH_CUDA(ctx, cudaMemcpyAsync(all, ctx->d_xsend, 8 * slots * W, cudaMemcpyDeviceToDevice, ctx->st));
     }
     int nslots = slots * ctx->nranks;
-    k_delta<<<nslots, 256, 0, ctx->st>>>(all, nslots, W, K, ctx->d_delta, ctx->d_delta_flag);
+    k_delta<<<nslots, DL_NT, 0, ctx->st>>>(all, nslots, W, K, ctx->d_delta, ctx->d_delta_flag);
     CH_LAUNCHED(ctx);
     k_skew<<<64, 256, 0, ctx->st>>>(all, nslots, W, K, ctx->d_delta, mskew);
     CH_LAUNCHED(ctx);

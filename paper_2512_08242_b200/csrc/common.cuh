@@ -124,6 +124,7 @@ struct chopper_ctx {
     int32_t *d_attr_pre = nullptr;   // [4][N] precomputed (non-laminar lists)
     int kb[4] = {0, 0, 0, 0};        // key bits per level
     int kg = 0;                      // key bits for lg
+    int64_t max_it_list = 0;         // longest iteration-span list of a local gpu (iteration ranks < this)
 
     // samples
     int64_t *d_smp_phi = nullptr, *d_smp_psi = nullptr;  // prefix integrals at sample k
@@ -160,6 +161,17 @@ struct chopper_ctx {
     int32_t *d_present = nullptr;    // [n_lg][C]
     const double **d_col = nullptr;  // [n_lg][C] value column of the pass providing the slot
     std::vector<int64_t> pass_mismatch, pass_conflict;
+    // counter-pass bookkeeping kept across calls (the caller's slot arrays are only valid in chopper_align)
+    std::vector<std::vector<int32_t>> pass_slots;   // [n_passes][k]
+    std::vector<int> pass_bad;                      // 1 = pass holds a non-finite value (known)
+    std::vector<int> pass_covered;                  // 1 = every column feeds a slot: finiteness checked by
+                                                    //     the counter pass in ch_tables, else k_pass_finite
+    std::vector<int32_t> sel_pass;                  // [n_lg][C] pass providing the slot, -1 absent
+    unsigned int *d_colbad = nullptr;               // [n_lg][C] non-finite value seen by the counter pass
+    unsigned int *d_pass_bad = nullptr;             // [n_passes] k_pass_finite result (uncovered passes)
+    unsigned long long *d_conf = nullptr;           // [n_passes] first conflicting position
+    double *counters_out = nullptr;                 // full-mode [C][N] output (rewritten if slots change)
+    const double **h_col_dev = nullptr;             // device array behind d_col (mutable)
     std::vector<int> gpu_present;    // [n_traced] gpu has events on some rank
     int64_t *d_xsend = nullptr;      // clock-offset exchange block of this rank [xslots][xW]
     unsigned int *d_xovf = nullptr;
@@ -345,6 +357,8 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
 // align.cu
 chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, int32_t n_passes, int32_t n_counters,
                         double *counters_out);
+chopper_status ch_assign_slots(chopper_ctx *ctx);          // slot -> column from the passes' known state
+chopper_status ch_counters_full(chopper_ctx *ctx);         // full-mode [C][N] counter matrix
 chopper_status ch_offsets(chopper_ctx *ctx);
 // tables.cu
 chopper_status ch_tables(chopper_ctx *ctx);

@@ -111,7 +111,8 @@ __device__ __forceinline__ int pow2ceil(int n) {
 __device__ double med_i64(int64_t *a, int n, int64_t *sh) {
     int n2 = pow2ceil(n);
     int64_t *w = sh ? sh : a;
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) w[i] = i < n ? a[i] : INT64_MAX;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x)
+        if (w != a || i >= n) w[i] = i < n ? a[i] : INT64_MAX;
     __syncthreads();
     block_bitonic<int64_t>(w, n2);
     double m = (n % 2) ? (double)w[n / 2] : 0.5 * ((double)w[n / 2 - 1] + (double)w[n / 2]);
@@ -121,7 +122,8 @@ __device__ double med_i64(int64_t *a, int n, int64_t *sh) {
 __device__ double med_f64(double *a, int n, double *sh) {
     int n2 = pow2ceil(n);
     double *w = sh ? sh : a;
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) w[i] = i < n ? a[i] : INFINITY;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x)
+        if (w != a || i >= n) w[i] = i < n ? a[i] : INFINITY;
     __syncthreads();
     block_bitonic<double>(w, n2);
     double m = (n % 2) ? w[n / 2] : 0.5 * (w[n / 2 - 1] + w[n / 2]);
@@ -137,40 +139,41 @@ struct BdArgs {
     int nslots;
     Layout Ly;
     const int32_t *slot_order;   // slots sorted by gpu id, -1 terminated
-    const int32_t *labels;       // gemm / fa labels, one per block
+    const int32_t *labels;       // gemm / fa labels, one per block row
     const double *f_gemm;
     double tpt, freq;
     int warmup;
     int s_cyc, s_fl, s_un, s_ud;
-    int64_t maxp2;               // scratch capacity per array (pow2)
-    int64_t *wi;                 // [nblocks][5][maxp2] int64 scratch
-    double *wd;                  // [nblocks][5][maxp2] double scratch
+    int64_t maxp2;               // capacity per work array (pow2)
+    int64_t *wi;                 // [nblocks][BD_TASKS][maxp2] int64 / double work arrays (global fallback)
+    double *res;                 // [nblocks][BD_TASKS][4] task results
     double *out;                 // [nblocks][16]
     int use_smem;
 };
 
+// one block per (gemm / fa label, task): every median of O13 runs in its own block (the points are few,
+// the blocks many); k_bd_compose then evaluates Eqs. 4-8 per label in the fixed order of DESIGN.md O13.
+enum { BT_ACT = 0, BT_D0, BT_D50, BT_FP, BT_U, BT_CG, BT_BL, BT_V, BT_FIT, BD_TASKS };
+
 __global__ void __launch_bounds__(512) k_breakdown(BdArgs A) {
     extern __shared__ int64_t bsh[];
-    int64_t *shi = A.use_smem ? bsh : nullptr;
-    double *shd = A.use_smem ? reinterpret_cast<double *>(bsh) : nullptr;
-    __shared__ int s_n;
-    __shared__ int s_flags_in;   // bit0 cyc, bit1 fl, bit2 util, bit3 smp
+    const int task = blockIdx.y;
     const int L = A.labels[blockIdx.x];
-    double *out = A.out + (int64_t)blockIdx.x * 16;
-    int64_t *busy = A.wi + (int64_t)blockIdx.x * 5 * A.maxp2;
-    int64_t *launch = busy + A.maxp2, *ovl = busy + 2 * A.maxp2, *phi = busy + 3 * A.maxp2, *ti = busy + 4 * A.maxp2;
-    double *cg = A.wd + (int64_t)blockIdx.x * 5 * A.maxp2;
-    double *fp = cg + A.maxp2, *un = cg + 2 * A.maxp2, *ud = cg + 3 * A.maxp2, *td = cg + 4 * A.maxp2;
+    double *res = A.res + ((int64_t)blockIdx.x * BD_TASKS + task) * 4;
+    int64_t *w = A.use_smem ? bsh : A.wi + ((int64_t)blockIdx.x * BD_TASKS + task) * 2 * A.maxp2;
+    int64_t *w2 = w + A.maxp2;                   // second operand (LS fit)
+    double *wd = reinterpret_cast<double *>(w), *wd2 = reinterpret_cast<double *>(w2);
     const Layout Ly = A.Ly;
-    // gather the sampled points of L in (gpu, iteration) order: ordered block compaction over the
-    // candidate (gpu slot, iteration rank) grid; slot presence is AND-ed over contributing gpus
     __shared__ int64_t scan_sm[33];
-    __shared__ int s_count;
+    __shared__ int s_count, s_all, s_flags_in;
     if (threadIdx.x == 0) {
         s_count = 0;
+        s_all = 0;
         s_flags_in = (A.s_cyc >= 0) | ((A.s_fl >= 0) << 1) | ((A.s_un >= 0 && A.s_ud >= 0) << 2) | (1 << 3);
     }
     __syncthreads();
+    // sampled points of L in (gpu, iteration) order (ordered block compaction over the candidate grid);
+    // each task keeps the members and the value it needs.  Slot presence is AND-ed over contributing gpus.
     {
         int nq = 0;
         while (nq < A.nslots && A.slot_order[nq] >= 0) nq++;
@@ -179,18 +182,19 @@ __global__ void __launch_bounds__(512) k_breakdown(BdArgs A) {
         const int64_t total = (int64_t)nq * nr;
         for (int64_t c0 = 0; c0 < total; c0 += blockDim.x) {
             int64_t c = c0 + threadIdx.x;
-            bool ok = false;
+            bool ok = false, keep = false;
             const int64_t *b = nullptr, *p = nullptr;
             if (c < total) {
                 b = A.blk + (int64_t)A.slot_order[c / nr] * Ly.W;
                 p = b + Ly.pt_off() + ((r0 + c % nr) * Ly.L + L) * PT_W;
                 ok = b[1] != 0 && p[0] != 0 && p[1] > 0;
             }
-            int64_t tot;
-            int64_t pos = block_excl_sum<512>(ok ? 1 : 0, &tot, scan_sm) + s_count;
-            if (ok && pos < A.maxp2) {
-                busy[pos] = p[1]; launch[pos] = p[2]; ovl[pos] = p[3]; phi[pos] = p[4];
-                cg[pos] = bitsd(p[5]); fp[pos] = bitsd(p[6]); un[pos] = bitsd(p[7]); ud[pos] = bitsd(p[8]);
+            int64_t busy = 0, launch = 0, ovl = 0, phi = 0;
+            if (ok) {
+                busy = p[1]; launch = p[2]; ovl = p[3]; phi = p[4];
+                keep = true;
+                if (task == BT_D0) keep = 20 * ovl <= busy;                                   // D15 buckets
+                if (task == BT_D50) keep = 2 * busy <= 5 * ovl && 5 * ovl <= 3 * busy;
                 int drop = 0;
                 if (A.s_cyc >= 0 && !b[HDR + A.s_cyc]) drop |= 1;
                 if (A.s_fl >= 0 && !b[HDR + A.s_fl]) drop |= 2;
@@ -198,131 +202,118 @@ __global__ void __launch_bounds__(512) k_breakdown(BdArgs A) {
                 if (!b[2]) drop |= 8;
                 if (drop) atomicAnd(&s_flags_in, ~drop);
             }
+            int64_t tot, tall;
+            int64_t pos = block_excl_sum<512>(keep ? 1 : 0, &tot, scan_sm) + s_count;
+            block_excl_sum<512>(ok ? 1 : 0, &tall, scan_sm);
+            if (keep && pos < A.maxp2) {
+                switch (task) {
+                    case BT_ACT: case BT_D0: case BT_D50: w[pos] = busy; break;
+                    case BT_FP: wd[pos] = bitsd(p[6]); break;
+                    case BT_U:      // both readings; presence (known after the gather) picks one (D18)
+                        wd[pos] = bitsd(p[7]) / bitsd(p[8]);
+                        wd2[pos] = (bitsd(p[6]) / bitsd(p[5])) * (A.freq / A.tpt);
+                        break;
+                    case BT_CG: wd[pos] = bitsd(p[5]); break;
+                    case BT_BL: w[pos] = busy + launch; break;
+                    case BT_V: wd[pos] = (double)phi / (double)busy * 1e6; break;
+                    case BT_FIT: wd[pos] = (double)ovl / (double)busy; wd2[pos] = (double)busy; break;
+                }
+            }
             __syncthreads();
-            if (threadIdx.x == 0) s_count += (int)tot;
+            if (threadIdx.x == 0) { s_count += (int)tot; s_all += (int)tall; }
             __syncthreads();
         }
+    }
+    const int n = s_count < A.maxp2 ? s_count : (int)A.maxp2;
+    const int n_all = s_all < A.maxp2 ? s_all : (int)A.maxp2;
+    const int fin = n_all == 0 ? (s_flags_in & ~8) : s_flags_in;
+    const bool has_cyc = fin & 1, has_fl = fin & 2, has_util = fin & 4, has_smp = fin & 8;
+    bool run = n_all >= 2 && n > 0;
+    if (task == BT_FP) run &= has_fl;
+    if (task == BT_U) run &= has_util || (has_fl && has_cyc);
+    if (task == BT_CG) run &= has_cyc;
+    if (task == BT_V) run &= has_smp;
+    if (run && task == BT_U && !has_util) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) wd[i] = wd2[i];
+        __syncthreads();
+    }
+    double m = 0.0;
+    if (run && task != BT_FIT) {
+        if (task == BT_ACT || task == BT_D0 || task == BT_D50 || task == BT_BL) m = med_i64(w, n, nullptr);
+        else m = med_f64(wd, n, nullptr);
+    }
+    if (run && task == BT_FIT && threadIdx.x == 0) {
+        // least-squares busy ~ a + c*r over all points, two sequential passes in (gpu, iteration) order
+        double sr = 0.0, sb = 0.0;
+        for (int i = 0; i < n; i++) { sr += wd[i]; sb += wd2[i]; }
+        double mr = sr / (double)n, mb = sb / (double)n, sxx = 0.0, sxy = 0.0;
+        for (int i = 0; i < n; i++) {
+            double dr = wd[i] - mr, db = wd2[i] - mb;
+            sxx += dr * dr;
+            sxy += dr * db;
+        }
+        if (sxx == 0.0) { res[1] = 0.0; res[2] = 0.0; res[3] = 1.0; }   // all r equal: D0 = D50 = D_act
+        else { double c = sxy / sxx, a = mb - c * mr; res[1] = a; res[2] = a + c * 0.5; res[3] = 0.0; }
     }
     if (threadIdx.x == 0) {
-        s_n = s_count < A.maxp2 ? s_count : (int)A.maxp2;
-        if (s_n == 0) s_flags_in &= ~8;
+        res[0] = m;
+        if (task == BT_ACT) { res[1] = n_all; res[2] = fin; }
+        if (task == BT_D0 || task == BT_D50) res[1] = n;
     }
-    __syncthreads();
-    const int n = s_n;
-    const int fin = s_flags_in;
+}
+
+__global__ void k_bd_compose(BdArgs A, int nb) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= nb) return;
+    const int L = A.labels[q];
+    const double *r = A.res + (int64_t)q * BD_TASKS * 4;
+    double *out = A.out + (int64_t)q * 16;
+    for (int k = 0; k < 16; k++) out[k] = NAN;
+    const int n = (int)r[BT_ACT * 4 + 1], fin = (int)r[BT_ACT * 4 + 2];
+    if (n < 2) { out[0] = n; out[1] = 0; out[14] = BD_INSUFFICIENT; out[15] = L; return; }
     const bool has_cyc = fin & 1, has_fl = fin & 2, has_util = fin & 4, has_smp = fin & 8;
-    if (threadIdx.x < 16) out[threadIdx.x] = NAN;
-    __syncthreads();
-    if (n < 2) {
-        if (threadIdx.x == 0) { out[0] = n; out[1] = 0; out[14] = BD_INSUFFICIENT; out[15] = L; }
-        return;
-    }
     int flags = 0;
-    // D_act = median busy (D14)
-    for (int i = threadIdx.x; i < n; i += blockDim.x) ti[i] = busy[i];
-    __syncthreads();
-    double d_act = med_i64(ti, n, shi);
-    // D0 / D50 buckets (integer tests, D15)
-    // bucket members (order irrelevant: only their medians are used)
-    __shared__ int s_n0, s_n50;
-    if (threadIdx.x == 0) s_n0 = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x)
-        if (20 * ovl[i] <= busy[i]) ti[atomicAdd(&s_n0, 1)] = busy[i];
-    __syncthreads();
-    int n0 = s_n0;
-    double d0 = 0.0, d50 = 0.0;
-    bool bucket = false;
-    if (n0 > 0) {
-        double m0 = med_i64(ti, n0, shi);
-        if (threadIdx.x == 0) s_n50 = 0;
-        __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            if (2 * busy[i] <= 5 * ovl[i] && 5 * ovl[i] <= 3 * busy[i]) ti[atomicAdd(&s_n50, 1)] = busy[i];
-        __syncthreads();
-        int n50 = s_n50;
-        if (n50 > 0) {
-            d0 = m0;
-            d50 = med_i64(ti, n50, shi);
-            bucket = true;
-        }
-    }
-    __shared__ double s_d0, s_d50;
-    if (!bucket) {
-        if (threadIdx.x == 0) {
-            double sr = 0.0, sb = 0.0;
-            for (int i = 0; i < n; i++) { sr += (double)ovl[i] / (double)busy[i]; sb += (double)busy[i]; }
-            double mr = sr / (double)n, mb = sb / (double)n, sxx = 0.0, sxy = 0.0;
-            for (int i = 0; i < n; i++) {
-                double dr = (double)ovl[i] / (double)busy[i] - mr, db = (double)busy[i] - mb;
-                sxx += dr * dr;
-                sxy += dr * db;
-            }
-            if (sxx == 0.0) { s_d0 = d_act; s_d50 = d_act; }
-            else { double c = sxy / sxx, a = mb - c * mr; s_d0 = a; s_d50 = a + c * 0.5; }
-        }
-        __syncthreads();
-        d0 = s_d0;
-        d50 = s_d50;
+    const double d_act = r[BT_ACT * 4];
+    const int n0 = (int)r[BT_D0 * 4 + 1], n50 = (int)r[BT_D50 * 4 + 1];
+    double d0, d50;
+    const bool bucket = n0 > 0 && n50 > 0;
+    if (bucket) { d0 = r[BT_D0 * 4]; d50 = r[BT_D50 * 4]; }
+    else {
+        if (r[BT_FIT * 4 + 3] != 0.0) { d0 = d_act; d50 = d_act; }
+        else { d0 = r[BT_FIT * 4 + 1]; d50 = r[BT_FIT * 4 + 2]; }
         flags |= BD_FIT;
     }
-    // remaining medians
-    double med_fp = 0.0, med_u = 0.0, med_cg = 0.0, med_bl, med_v = 0.0;
-    if (has_fl) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) td[i] = fp[i];
-        __syncthreads();
-        med_fp = med_f64(td, n, shd);
-    }
+    const double med_fp = r[BT_FP * 4], med_u = r[BT_U * 4], med_cg = r[BT_CG * 4], med_bl = r[BT_BL * 4],
+                 med_v = r[BT_V * 4];
+    out[0] = n;
+    out[1] = bucket ? 0 : 1;
+    out[2] = d_act * 1e-9;
+    out[3] = d0 * 1e-9;
+    out[4] = d50 * 1e-9;
+    double d_thr = A.f_gemm[L] / A.tpt;                                   // Eq. 4
+    out[5] = d_thr;
+    double ovr_inst = 1.0;                                               // Eq. 5
+    if (has_fl) ovr_inst = med_fp / A.f_gemm[L]; else flags |= BD_NO_FLOPS;
+    out[6] = ovr_inst;
+    double ovr_util = 1.0;                                               // Eq. 6
     if (has_util || (has_fl && has_cyc)) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            td[i] = has_util ? un[i] / ud[i] : (fp[i] / cg[i]) * (A.freq / A.tpt);
-        __syncthreads();
-        med_u = med_f64(td, n, shd);
-    }
-    if (has_cyc) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) td[i] = cg[i];
-        __syncthreads();
-        med_cg = med_f64(td, n, shd);
-    }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) ti[i] = busy[i] + launch[i];
-    __syncthreads();
-    med_bl = med_i64(ti, n, shi);
-    if (has_smp) {
-        for (int i = threadIdx.x; i < n; i += blockDim.x) td[i] = (double)phi[i] / (double)busy[i] * 1e6;
-        __syncthreads();
-        med_v = med_f64(td, n, shd);
-    }
-    if (threadIdx.x == 0) {
-        out[0] = n;
-        out[1] = bucket ? 0 : 1;
-        out[2] = d_act * 1e-9;
-        out[3] = d0 * 1e-9;
-        out[4] = d50 * 1e-9;
-        double d_thr = A.f_gemm[L] / A.tpt;                                   // Eq. 4
-        out[5] = d_thr;
-        double ovr_inst = 1.0;                                               // Eq. 5
-        if (has_fl) ovr_inst = med_fp / A.f_gemm[L]; else flags |= BD_NO_FLOPS;
-        out[6] = ovr_inst;
-        double ovr_util = 1.0;                                               // Eq. 6
-        if (has_util || (has_fl && has_cyc)) {
-            if (!(med_u > 0.0 && med_u <= 1.0)) flags |= BD_UTIL_RANGE;
-            ovr_util = 1.0 / med_u;
-        } else flags |= BD_NO_UTIL;
-        out[7] = ovr_util;
-        double ovr_ovl = d50 / d0;                                           // Eq. 7
-        if (!(d0 > 0.0)) flags |= BD_D0_ZERO;
-        out[8] = ovr_ovl;
-        if (has_cyc) {                                                       // Eq. 8
-            double d_peak = med_cg / A.freq;
-            out[9] = d_peak;
-            out[10] = (d_act * 1e-9 / d_peak) / ovr_ovl;
-        } else flags |= BD_NO_CYCLES;
-        out[11] = med_bl / d_act;                                            // launch term (D20)
-        out[12] = d_act * 1e-9 / (d_thr * ovr_inst * ovr_util * ovr_ovl * out[10]);
-        if (has_smp) out[13] = A.freq / med_v; else flags |= BD_NO_SAMPLES;
-        out[14] = flags;
-        out[15] = L;
-    }
+        if (!(med_u > 0.0 && med_u <= 1.0)) flags |= BD_UTIL_RANGE;
+        ovr_util = 1.0 / med_u;
+    } else flags |= BD_NO_UTIL;
+    out[7] = ovr_util;
+    double ovr_ovl = d50 / d0;                                           // Eq. 7
+    if (!(d0 > 0.0)) flags |= BD_D0_ZERO;
+    out[8] = ovr_ovl;
+    if (has_cyc) {                                                       // Eq. 8
+        double d_peak = med_cg / A.freq;
+        out[9] = d_peak;
+        out[10] = (d_act * 1e-9 / d_peak) / ovr_ovl;
+    } else flags |= BD_NO_CYCLES;
+    out[11] = med_bl / d_act;                                            // launch term (D20)
+    out[12] = d_act * 1e-9 / (d_thr * ovr_inst * ovr_util * ovr_ovl * out[10]);
+    if (has_smp) out[13] = A.freq / med_v; else flags |= BD_NO_SAMPLES;
+    out[14] = flags;
+    out[15] = L;
 }
 
 // global iteration rows (a11): one thread per iteration rank of the reference gpu
@@ -354,13 +345,39 @@ __global__ void __launch_bounds__(256) k_global(GlobArgs A) {
     const int ref = s_ref;
     if (ref < 0) { if (threadIdx.x == 0) { *A.n_out = 0; *A.med = NAN; } return; }
     const int64_t *rb = A.blk + (int64_t)ref * Ly.W;
-    // reference rows are the valid ranks of the reference gpu in rank order; output index = count before
-    __shared__ int widx[4096];
-    if (threadIdx.x == 0) {
-        int c = 0;
-        for (int64_t r = 0; r < Ly.MI && r < 4096; r++) { widx[r] = c; c += rb[Ly.it_off() + r * IT_W] != 0; }
+    // per slot: are the step labels strictly increasing over its valid ranks?
+    __shared__ int s_sorted[CH_MAX_GPUS];
+    for (int q = threadIdx.x; q < A.nslots && q < CH_MAX_GPUS; q += blockDim.x) s_sorted[q] = 1;
+    __syncthreads();
+    for (int q = 0; q < A.nslots && q < CH_MAX_GPUS; q++) {
+        int sl = A.slot_order[q];
+        if (sl < 0) break;
+        const int64_t *b = A.blk + (int64_t)sl * Ly.W + Ly.it_off();
+        for (int64_t x = threadIdx.x; x < Ly.MI; x += blockDim.x) {
+            if (!b[x * IT_W]) continue;
+            int64_t y = x + 1;
+            while (y < Ly.MI && !b[y * IT_W]) y++;
+            if (y < Ly.MI && b[y * IT_W + 1] <= b[x * IT_W + 1]) s_sorted[q] = 0;
+        }
     }
     __syncthreads();
+    // reference rows are the valid ranks of the reference gpu in rank order; output index = count before
+    __shared__ int widx[4096];
+    __shared__ int64_t scan_sm[33];
+    __shared__ int64_t s_base;
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    for (int64_t r0 = 0; r0 < Ly.MI && r0 < 4096; r0 += blockDim.x) {     // ordered compaction (block scan)
+        int64_t r = r0 + threadIdx.x;
+        bool v = r < Ly.MI && r < 4096 && rb[Ly.it_off() + r * IT_W] != 0;
+        int64_t tot;
+        int64_t ex = block_excl_sum<256>(v ? 1 : 0, &tot, scan_sm);
+        if (r < Ly.MI && r < 4096) widx[r] = (int)(s_base + ex);
+        __syncthreads();
+        if (threadIdx.x == 0) s_base += tot;
+        __syncthreads();
+    }
+    const int64_t nref_all = s_base;
     for (int64_t r = threadIdx.x; r < Ly.MI && r < 4096; r += blockDim.x) {
         const int64_t *row = rb + Ly.it_off() + r * IT_W;
         if (!row[0]) continue;
@@ -375,9 +392,16 @@ __global__ void __launch_bounds__(256) k_global(GlobArgs A) {
             if (!b[1]) continue;
             int g = (int)b[0];
             int64_t f = -1;
-            // first iteration (rank order) of gpu g with the same step label (D5)
-            for (int64_t x = 0; x < Ly.MI; x++)
-                if (b[Ly.it_off() + x * IT_W] && b[Ly.it_off() + x * IT_W + 1] == step) { f = x; break; }
+            // first iteration (rank order) of gpu g with the same step label (D5); iterations are
+            // normally rank-aligned across gpus, so the scan is entered only when rank r differs
+            // or an earlier rank carries the same step
+            const int64_t *xr = b + Ly.it_off() + r * IT_W;
+            if (q < CH_MAX_GPUS && s_sorted[q] && xr[0] && xr[1] == step) {
+                f = r;      // steps strictly increasing over the gpu's ranks: rank r is the first match
+            } else {
+                for (int64_t x = 0; x < Ly.MI; x++)
+                    if (b[Ly.it_off() + x * IT_W] && b[Ly.it_off() + x * IT_W + 1] == step) { f = x; break; }
+            }
             if (f < 0) { complete = false; continue; }
             const int64_t *x = b + Ly.it_off() + f * IT_W;
             if (f < A.warmup) samp = false;
@@ -398,13 +422,21 @@ __global__ void __launch_bounds__(256) k_global(GlobArgs A) {
         A.tp[w] = complete ? (double)A.tokens / ((double)T * 1e-9) : NAN;
     }
     __syncthreads();
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    for (int64_t w0 = 0; w0 < nref_all; w0 += blockDim.x) {                 // sampled throughputs, in order
+        int64_t w = w0 + threadIdx.x;
+        bool v = w < nref_all && A.sampled[w];
+        int64_t tot;
+        int64_t ex = block_excl_sum<256>(v ? 1 : 0, &tot, scan_sm);
+        if (v) A.work[s_base + ex] = A.tp[w];
+        __syncthreads();
+        if (threadIdx.x == 0) s_base += tot;
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
-        int64_t nref = 0;
-        int nst = 0;
-        for (int64_t r = 0; r < Ly.MI; r++) if (rb[Ly.it_off() + r * IT_W]) nref++;
-        for (int64_t w = 0; w < nref; w++) if (A.sampled[w]) A.work[nst++] = A.tp[w];
-        *A.n_out = nref;
-        s_nst = nst;
+        *A.n_out = nref_all;
+        s_nst = (int)s_base;
     }
     __syncthreads();
     int nst = s_nst;
@@ -482,8 +514,10 @@ static chopper_status run_breakdown(chopper_ctx *ctx, const int64_t *blk, int ns
     int64_t maxp = (int64_t)Ly.MI * ctx->cfg.n_traced_gpus;
     int64_t maxp2 = 1;
     while (maxp2 < maxp) maxp2 <<= 1;
-    int64_t *wi = CH_ALLOC(ctx, int64_t, (int64_t)std::max(nb, 1) * 5 * maxp2);
-    double *wd = CH_ALLOC(ctx, double, (int64_t)std::max(nb, 1) * 5 * maxp2);
+    size_t shb = (size_t)16 * maxp2;     // work array + second operand of the fit
+    bool use_smem = shb <= 64 * 1024;
+    int64_t *wi = use_smem ? nullptr : CH_ALLOC(ctx, int64_t, (int64_t)std::max(nb, 1) * BD_TASKS * 2 * maxp2);
+    double *res = CH_ALLOC(ctx, double, (int64_t)std::max(nb, 1) * BD_TASKS * 4);
     CH_ALLOC_END(ctx);
     *out_dev = out;
     if (nb == 0) return CHOPPER_OK;
@@ -504,16 +538,17 @@ static chopper_status run_breakdown(chopper_ctx *ctx, const int64_t *blk, int ns
     A.s_ud = ctx->bd.slot_util_den;
     A.maxp2 = maxp2;
     A.wi = wi;
-    A.wd = wd;
+    A.res = res;
     A.out = out;
-    size_t shb = (size_t)8 * maxp2;
-    A.use_smem = shb <= 64 * 1024;
+    A.use_smem = use_smem;
     static bool attr = false;
     if (!attr) {
         CH_CUDA(ctx, cudaFuncSetAttribute(k_breakdown, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
         attr = true;
     }
-    k_breakdown<<<nb, 512, A.use_smem ? shb : 0, ctx->st>>>(A);
+    k_breakdown<<<dim3(nb, BD_TASKS), 512, use_smem ? shb : 0, ctx->st>>>(A);
+    CH_LAUNCHED(ctx);
+    k_bd_compose<<<(unsigned)ceil_div(nb, 64), 64, 0, ctx->st>>>(A, nb);
     CH_LAUNCHED(ctx);
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return CHOPPER_OK;

@@ -22,7 +22,6 @@ SpanView ch_span_view(chopper_ctx *ctx);
 namespace {
 constexpr int NT = 256;
 constexpr int EV_NT = 256, EV_IPT = 8, EV_TILE = EV_NT * EV_IPT;
-constexpr int NACC = RF_NFIELDS;
 constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62, VAL_MASK = (1ull << 62) - 1;
 
 // ---- comm / compute unions: one block per local gpu ----------------------------------------------
@@ -236,43 +235,53 @@ __global__ void k_covl(EvParams P, int n_lg) {
     }
 }
 
+// ---- sub-run aggregate ----------------------------------------------------------------------------
+// Counts and the first-event offset are tile-local 32-bit (a tile holds 2048 events); the rest are the
+// int64 row fields.  merge() is commutative and associative: sums, max(last_ke) and the lexicographic
+// min of (first_ks, first offset) -- so the segmented scan below may combine in any grouping.
 struct Acc {
-    int64_t v[NACC];
+    int32_t nev, n, foff;
+    int64_t busy, prep, call, ovl, phi, psi, copy, ag, rs, fks, lke;
     __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int f = 0; f < NACC; f++) v[f] = 0;
-        v[RF_FIRST_IDX] = INT64_MAX;
-        v[RF_FIRST_KS] = INT64_MAX;
-        v[RF_LAST_KE] = INT64_MIN;
+        nev = 0; n = 0; foff = INT32_MAX;
+        busy = prep = call = ovl = phi = psi = copy = ag = rs = 0;
+        fks = INT64_MAX; lke = INT64_MIN;
     }
-    __device__ __forceinline__ void add(const Acc &b) {
-#pragma unroll
-        for (int f = 0; f < NACC; f++)
-            if (f != RF_FIRST_IDX && f != RF_FIRST_KS && f != RF_LAST_KE) v[f] += b.v[f];
-        if (b.v[RF_FIRST_KS] < v[RF_FIRST_KS] ||
-            (b.v[RF_FIRST_KS] == v[RF_FIRST_KS] && b.v[RF_FIRST_IDX] < v[RF_FIRST_IDX])) {
-            v[RF_FIRST_KS] = b.v[RF_FIRST_KS];
-            v[RF_FIRST_IDX] = b.v[RF_FIRST_IDX];
-        }
-        if (b.v[RF_LAST_KE] > v[RF_LAST_KE]) v[RF_LAST_KE] = b.v[RF_LAST_KE];
+    __device__ __forceinline__ void merge(const Acc &b) {
+        nev += b.nev; n += b.n;
+        busy += b.busy; prep += b.prep; call += b.call; ovl += b.ovl; phi += b.phi; psi += b.psi;
+        copy += b.copy; ag += b.ag; rs += b.rs;
+        if (b.lke > lke) lke = b.lke;
+        if (b.fks < fks || (b.fks == fks && b.foff < foff)) { fks = b.fks; foff = b.foff; }
     }
-    __device__ __forceinline__ void store(int64_t *sm, int t) const {
-#pragma unroll
-        for (int f = 0; f < NACC; f++) sm[f * EV_NT + t] = v[f];
-    }
-    __device__ __forceinline__ void load(const int64_t *sm, int t) {
-#pragma unroll
-        for (int f = 0; f < NACC; f++) v[f] = sm[f * EV_NT + t];
+    __device__ __forceinline__ Acc shfl_up(int o) const {
+        Acc r;
+        r.nev = __shfl_up_sync(CH_FULL, nev, o); r.n = __shfl_up_sync(CH_FULL, n, o);
+        r.foff = __shfl_up_sync(CH_FULL, foff, o);
+        r.busy = __shfl_up_sync(CH_FULL, busy, o); r.prep = __shfl_up_sync(CH_FULL, prep, o);
+        r.call = __shfl_up_sync(CH_FULL, call, o); r.ovl = __shfl_up_sync(CH_FULL, ovl, o);
+        r.phi = __shfl_up_sync(CH_FULL, phi, o); r.psi = __shfl_up_sync(CH_FULL, psi, o);
+        r.copy = __shfl_up_sync(CH_FULL, copy, o); r.ag = __shfl_up_sync(CH_FULL, ag, o);
+        r.rs = __shfl_up_sync(CH_FULL, rs, o); r.fks = __shfl_up_sync(CH_FULL, fks, o);
+        r.lke = __shfl_up_sync(CH_FULL, lke, o);
+        return r;
     }
 };
 
-// sub-run rows are AoS: 16 int64 (14 fields + pad) = one 128 B line per row
+// sub-run rows are AoS: 16 int64 (14 fields in RowField order + pad) = one 128 B line per row
 constexpr int SR_W = 16;
-__device__ __forceinline__ void write_subrun(const EvParams &P, int64_t id, const Acc &a) {
+__device__ __forceinline__ void write_subrun(const EvParams &P, int64_t id, const Acc &a, int64_t base) {
     longlong2 *dst = reinterpret_cast<longlong2 *>(P.sr_f + id * SR_W);
-#pragma unroll
-    for (int f = 0; f < SR_W / 2; f++)
-        dst[f] = make_longlong2(2 * f < NACC ? a.v[2 * f] : 0, 2 * f + 1 < NACC ? a.v[2 * f + 1] : 0);
+    const int64_t fidx = a.foff == INT32_MAX ? INT64_MAX : base + a.foff;
+    // RowField: NEV N BUSY FIRST_IDX LAST_KE PREP CALL OVL PHI PSI COPY AG RS FIRST_KS
+    dst[0] = make_longlong2(a.nev, a.n);
+    dst[1] = make_longlong2(a.busy, fidx);
+    dst[2] = make_longlong2(a.lke, a.prep);
+    dst[3] = make_longlong2(a.call, a.ovl);
+    dst[4] = make_longlong2(a.phi, a.psi);
+    dst[5] = make_longlong2(a.copy, a.ag);
+    dst[6] = make_longlong2(a.rs, a.fks);
+    dst[7] = make_longlong2(0, 0);
 }
 
 // ---- register caches for the per-event lookups (events of a gpu come in dispatch order) ----
@@ -283,12 +292,15 @@ struct LvCache {
     int64_t next_start, res_end;
     bool pre;
 };
-__device__ __forceinline__ void lv_reset(LvCache &c, const SpanView &v, int list) {
+// seed = last push-order index with start <= the thread's first dispatch (warp_seeds), or -2 (none): the
+// first lookup then walks forward / up from the seed instead of binary-searching the whole list
+__device__ __forceinline__ void lv_reset(LvCache &c, const SpanView &v, int list, int32_t seed = -2) {
     c.lb = (int32_t)v.list_beg[list];
     c.le = (int32_t)v.list_beg[list + 1];
     c.pre = v.list_flags[list] != 0;
-    c.c0 = -2;
+    c.c0 = seed >= c.lb - 1 && seed < c.le ? seed : -2;
     c.res = -1;
+    c.next_start = INT64_MIN;      // forces the first lookup through the walk
 }
 __device__ __forceinline__ int32_t lv_lookup(LvCache &c, const SpanView &v, int lv, int64_t t, int64_t i) {
     if (c.pre) return v.attr_pre[(int64_t)lv * v.N + i];
@@ -321,6 +333,18 @@ __device__ __forceinline__ void cov_reset(CovCache &c, int64_t lo, int64_t cnt) 
     c.lo = (int32_t)lo;
     c.hi = (int32_t)(lo + cnt);
     c.u = -2;
+}
+// position the cache at merged interval u (last start <= the thread's first query), loading its fields
+__device__ __forceinline__ void cov_seed(CovCache &c, const int64_t *Us, const int64_t *Ue, const int64_t *UP,
+                                         int32_t u) {
+    if (c.hi <= c.lo || u < c.lo - 1 || u >= c.hi) return;
+    c.u = u;
+    c.next_s = u + 1 < c.hi ? __ldg(Us + u + 1) : INT64_MAX;
+    if (u >= c.lo) {
+        c.us = __ldg(Us + u);
+        c.len = __ldg(Ue + u) - c.us;
+        c.up = __ldg(UP + u);
+    }
 }
 __device__ __forceinline__ int64_t cov_c(CovCache &c, const int64_t *Us, const int64_t *Ue, const int64_t *UP, int64_t t) {
     if (c.hi <= c.lo) return 0;
@@ -358,6 +382,99 @@ __device__ __forceinline__ void smp_reset(SmpCache &c, int64_t lo, int64_t hi) {
     c.hi = (int32_t)hi;
     c.q = -2;
 }
+__device__ __forceinline__ void smp_seed(SmpCache &c, const EvParams &P, int32_t q) {
+    if (c.hi <= c.lo || q < c.lo - 1 || q >= c.hi) return;
+    if (q < c.lo) q = c.lo;            // before the first sample: f_0 extended backwards (D10)
+    c.q = q;
+    c.ts = __ldg(P.smp_ts + q);
+    c.next = q + 1 < c.hi ? __ldg(P.smp_ts + q + 1) : INT64_MAX;
+    c.phi = __ldg(P.phi_pre + q);
+    c.psi = __ldg(P.psi_pre + q);
+    c.f = __ldg(P.smp_f + q);
+    c.p = __ldg(P.smp_p + q);
+}
+
+// ---- warp-cooperative seeding of the per-thread caches -------------------------------------------
+// For NQ sorted tables a[lo, hi) (warp-uniform) and one query t per lane, every lane gets the last
+// index with a[idx] <= t (lo - 1 if none; -2 for lanes that do not take part).  A 32-ary descent on the
+// warp's smallest query (one probe per lane per round, all tables in lockstep) replaces each lane's
+// ~18-step dependent binary search; lanes then resolve their own query in 32-element register chunks
+// (shuffle binary search), walking forward chunk by chunk.
+struct SeedQ {
+    const int64_t *a;
+    int64_t lo, hi;
+    int64_t t;
+    bool on;
+};
+template <int NQ>
+__device__ __forceinline__ void warp_seeds(const SeedQ (&q)[NQ], int32_t (&ans)[NQ]) {
+    const int lane = lane_id();
+    int64_t l[NQ], h[NQ], qmin[NQ];
+    bool act[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; j++) {
+        act[j] = __any_sync(CH_FULL, q[j].on) && q[j].hi > q[j].lo;
+        int64_t x = q[j].on ? q[j].t : INT64_MAX;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            int64_t y = __shfl_xor_sync(CH_FULL, x, o);
+            x = y < x ? y : x;
+        }
+        qmin[j] = x;
+        l[j] = q[j].lo;
+        h[j] = q[j].hi;
+        ans[j] = -2;
+    }
+    while (true) {
+        bool any = false;
+        int64_t v[NQ], step[NQ];
+#pragma unroll
+        for (int j = 0; j < NQ; j++) {
+            v[j] = INT64_MAX;
+            step[j] = 0;
+            if (act[j] && h[j] - l[j] > 32) {
+                step[j] = (h[j] - l[j] + 31) >> 5;
+                int64_t p = l[j] + lane * step[j];
+                if (p < h[j]) v[j] = __ldg(q[j].a + p);
+                any = true;
+            }
+        }
+        if (!any) break;
+#pragma unroll
+        for (int j = 0; j < NQ; j++) {
+            if (step[j] == 0) continue;
+            int c = __popc(__ballot_sync(CH_FULL, v[j] <= qmin[j]));
+            if (c == 0) {
+                h[j] = l[j];                  // answer l - 1
+            } else {
+                int64_t nl = l[j] + (int64_t)(c - 1) * step[j];
+                h[j] = nl + step[j] < h[j] ? nl + step[j] : h[j];
+                l[j] = nl + 1;                // answer in [nl, h - 1]
+            }
+        }
+    }
+    // chunks from l: every element before l is <= the smallest query
+#pragma unroll
+    for (int j = 0; j < NQ; j++) {
+        if (!act[j]) continue;
+        const int64_t t = q[j].on ? q[j].t : INT64_MIN;
+        bool done = !q[j].on;
+        int64_t c0 = l[j];
+        while (__any_sync(CH_FULL, !done)) {
+            int64_t val = c0 + lane < q[j].hi ? __ldg(q[j].a + c0 + lane) : INT64_MAX;
+            int pos = 0;
+#pragma unroll
+            for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                int64_t x = __shfl_sync(CH_FULL, val, pos + s2 - 1);
+                if (x <= t) pos += s2;
+            }
+            if (__shfl_sync(CH_FULL, val, 31) <= t) pos = 32;
+            if (!done && pos < 32) { ans[j] = (int32_t)(c0 - 1 + pos); done = true; }
+            if (!done && c0 + 32 >= q[j].hi) { ans[j] = (int32_t)(q[j].hi - 1); done = true; }
+            c0 += 32;
+        }
+    }
+}
 __device__ __forceinline__ void smp_F(SmpCache &c, const EvParams &P, int64_t t, int64_t *F, int64_t *Pw) {
     if (!(c.q != -2 && t < c.next && (c.q == c.lo || t >= c.ts))) {
         int64_t q;
@@ -383,89 +500,227 @@ __device__ __forceinline__ void smp_F(SmpCache &c, const EvParams &P, int64_t t,
     *Pw = c.psi + (int64_t)c.p * dt;
 }
 
-__global__ void __launch_bounds__(EV_NT, 3) k_events(EvParams P) {
-    extern __shared__ int64_t dsm[];
-    int64_t *fp = dsm;                    // [NACC][EV_NT] first piece per thread
-    int64_t *lp = dsm + NACC * EV_NT;     // [NACC][EV_NT] last piece per thread
-    unsigned long long *keys_s = reinterpret_cast<unsigned long long *>(dsm + 2 * NACC * EV_NT);  // [EV_IPT][EV_NT]
-    __shared__ unsigned char hh[EV_NT];
-    __shared__ int64_t scan_sm[33];
-    __shared__ int64_t s_tile, s_excl;
+
+// ---- tile staging: cp.async 16 B units into an XOR-swizzled thread-blocked layout ------------------
+// Thread t owns events [8t, 8t+8) of the tile.  An int64 column keeps thread t's 64 B as four 16 B
+// units, unit j stored at slot t*4 + (j ^ ((t >> 1) & 3)); a u32 column keeps 32 B as two units at
+// t*2 + (j ^ ((t >> 2) & 1)).  Both the coalesced cp.async writes (consecutive units) and the per-thread
+// 128-bit reads (unit j of 8 consecutive threads) then touch all 32 banks once.
+__device__ __forceinline__ int sw64(int t, int j) { return t * 4 + (j ^ ((t >> 1) & 3)); }
+__device__ __forceinline__ int sw32(int t, int j) { return t * 2 + (j ^ ((t >> 2) & 1)); }
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+constexpr int EV_WARPS = EV_NT / 32;
+struct EvSmem {
+    longlong2 col[4][EV_TILE / 2];        // t_l, t_ks, t_ke, pred_end (64 KB)
+    uint4 meta[EV_TILE / 4];              // 8 KB
+    unsigned long long key[EV_IPT][EV_NT];  // instance key per event, [k][thread] (16 KB)
+    Acc wagg[EV_WARPS], wcarry[EV_WARPS];
+    int wflag[EV_WARPS], wcflag[EV_WARPS];
+    int wheads[EV_WARPS];
+    int64_t tile, excl;
+    int tot;
+};
+
+__device__ __forceinline__ void stage_tile(EvSmem &S, const EvParams &P, int64_t base, bool vec) {
     const int tid = threadIdx.x;
-    if (tid == 0) s_tile = (int64_t)atomicAdd(P.ticket, 1u);
+    const int64_t *src[4] = {P.tl, P.ks, P.ke, P.pred_end};
+    if (vec) {
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                int u = tid + r * EV_NT;    // 16 B unit of the column: events 2u, 2u+1
+                cp_async16(&S.col[c][sw64(u >> 2, u & 3)], src[c] + base + 2 * u);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            int u = tid + r * EV_NT;        // events 4u .. 4u+3
+            cp_async16(&S.meta[sw32(u >> 1, u & 1)], P.meta + base + 4 * u);
+        }
+        cp_async_wait_all();
+    } else {
+        // partial or unaligned tile: element-wise, same layout
+        for (int e = tid; e < EV_TILE; e += EV_NT) {
+            int64_t i = base + e;
+            int t = e >> 3, k = e & 7;
+            int64_t *dst;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                dst = reinterpret_cast<int64_t *>(&S.col[c][sw64(t, k >> 1)]) + (k & 1);
+                *dst = i < P.N ? src[c][i] : 0;
+            }
+            reinterpret_cast<uint32_t *>(&S.meta[sw32(t, k >> 2)])[k & 3] = i < P.N ? P.meta[i] : 0u;
+        }
+    }
     __syncthreads();
-    const int64_t tile = s_tile;
+}
+
+// the fused pass: one 2048-event tile per block, 8 consecutive events per thread
+__global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
+    extern __shared__ __align__(16) unsigned char ev_dsm[];
+    EvSmem &S = *reinterpret_cast<EvSmem *>(ev_dsm);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) S.tile = (int64_t)atomicAdd(P.ticket, 1u);
+    __syncthreads();
+    const int64_t tile = S.tile;
     const int64_t base = tile * EV_TILE;
     const int64_t i0 = base + (int64_t)tid * EV_IPT;
     const int64_t N = P.N;
+    stage_tile(S, P, base, vec_ok && base + EV_TILE <= N);
+    const int nv = i0 >= N ? 0 : (int)min((int64_t)EV_IPT, N - i0);    // valid events of this thread
 
-    // ---- phase A: instance keys (attribution), staged in shared memory ----
+    // ---- phase 0: seeds for the span, comm-union and sample caches (lanes of one gpu) ----
+    int32_t seed[6];
+    int seed_lg;
+    {
+        int64_t t0 = 0, ksc = 0;
+        bool hc = false;
+        int lg0 = -1;
+        if (nv > 0) {
+            t0 = reinterpret_cast<const int64_t *>(&S.col[0][sw64(tid, 0)])[0];
+            lg0 = P.gpu_lg[gpu_of(reinterpret_cast<const uint32_t *>(&S.meta[sw32(tid, 0)])[0])];
+            for (int k = 0; k < nv && !hc; k++) {
+                uint32_t m = reinterpret_cast<const uint32_t *>(&S.meta[sw32(tid, k >> 2)])[k & 3];
+                if (kind_of(m) == CK_COMPUTE && P.gpu_lg[gpu_of(m)] == lg0) {
+                    ksc = reinterpret_cast<const int64_t *>(&S.col[1][sw64(tid, k >> 1)])[k & 1];
+                    hc = true;
+                }
+            }
+        }
+        const int lgw = __shfl_sync(CH_FULL, lg0, 0);
+        const bool mine = nv > 0 && lg0 == lgw && lgw >= 0;
+        SeedQ qs[6];
+        const int64_t *lb = P.sv.list_beg;
+#pragma unroll
+        for (int lv = 0; lv < 4; lv++) {
+            qs[lv].a = P.sv.P_start;
+            qs[lv].lo = lgw >= 0 ? lb[lgw * 4 + lv] : 0;
+            qs[lv].hi = lgw >= 0 ? lb[lgw * 4 + lv + 1] : 0;
+            qs[lv].t = t0;
+            qs[lv].on = mine && lgw >= 0 && !P.sv.list_flags[lgw * 4 + lv];
+        }
+        qs[4].a = P.Us;
+        qs[4].lo = lgw >= 0 ? P.Ubeg[lgw] : 0;
+        qs[4].hi = lgw >= 0 ? P.Ubeg[lgw] + P.Ucnt[lgw] : 0;
+        qs[4].t = ksc;
+        qs[4].on = mine && hc;
+        qs[5].a = P.smp_ts;
+        qs[5].lo = lgw >= 0 ? P.smp_lo[lgw] : 0;
+        qs[5].hi = lgw >= 0 ? P.smp_hi[lgw] : 0;
+        qs[5].t = ksc;
+        qs[5].on = mine && hc;
+        warp_seeds<6>(qs, seed);
+        seed_lg = mine ? lgw : -1;
+    }
+
+    // ---- phase A: instance key of every event (attribution, a5) ----
     unsigned hmask = 0;
     {
         LvCache lc[4];
         int lgp = -1;
         unsigned long long prevk = CH_INVALID_KEY;
 #pragma unroll 1
-        for (int k = 0; k < EV_IPT; k++) {
-            int64_t i = i0 + k;
-            unsigned long long kk = CH_INVALID_KEY;
-            if (i < N) {
-                int lg = P.gpu_lg[gpu_of(__ldg(P.meta + i))];
-                if (lg != lgp) {
+        for (int j = 0; j < EV_IPT / 2; j++) {
+            const longlong2 tv = S.col[0][sw64(tid, j)];
+            const uint2 mv = reinterpret_cast<const uint2 *>(&S.meta[sw32(tid, j >> 1)])[j & 1];
 #pragma unroll
-                    for (int lv = 0; lv < 4; lv++) lv_reset(lc[lv], P.sv, lg * 4 + lv);
-                    lgp = lg;
-                }
-                int64_t t = __ldg(P.tl + i);
-                int32_t r[4];
-                bool ok = true;
+            for (int h = 0; h < 2; h++) {
+                const int k = 2 * j + h;
+                unsigned long long kk = CH_INVALID_KEY;
+                if (k < nv) {
+                    const int64_t i = i0 + k;
+                    const int64_t t = h ? tv.y : tv.x;
+                    const int lg = P.gpu_lg[gpu_of(h ? mv.y : mv.x)];
+                    if (lg != lgp) {
 #pragma unroll
-                for (int lv = 0; lv < 4; lv++) {
-                    int32_t c = lv_lookup(lc[lv], P.sv, lv, t, i);
-                    ok &= c != -2;
-                    r[lv] = c >= 0 ? c - lc[lv].lb + 1 : 0;
+                        for (int lv = 0; lv < 4; lv++)
+                            lv_reset(lc[lv], P.sv, lg * 4 + lv, lgp < 0 && lg == seed_lg ? seed[lv] : -2);
+                        lgp = lg;
+                    }
+                    int32_t r[4];
+                    bool ok = true;
+#pragma unroll
+                    for (int lv = 0; lv < 4; lv++) {
+                        int32_t c = lv_lookup(lc[lv], P.sv, lv, t, i);
+                        ok &= c != -2;
+                        r[lv] = c >= 0 ? c - lc[lv].lb + 1 : 0;
+                    }
+                    if (ok && r[0] != 0)
+                        kk = ((unsigned long long)lg << P.sh_lg) | ((unsigned long long)r[0] << P.sh_it) |
+                             ((unsigned long long)r[1] << P.sh_ph) | ((unsigned long long)r[2] << P.sh_ly) |
+                             (unsigned long long)r[3];
+                    if (k > 0 && kk != prevk) hmask |= 1u << k;
                 }
-                if (ok && r[0] != 0)
-                    kk = ((unsigned long long)lg << P.sh_lg) | ((unsigned long long)r[0] << P.sh_it) |
-                         ((unsigned long long)r[1] << P.sh_ph) | ((unsigned long long)r[2] << P.sh_ly) |
-                         (unsigned long long)r[3];
-                if (k > 0 && kk != prevk) hmask |= 1u << k;
+                S.key[k][tid] = kk;
+                prevk = kk;
             }
-            keys_s[k * EV_NT + tid] = kk;
-            prevk = kk;
         }
     }
     __syncthreads();
     // the tile start is always a head (sub-runs never cross tiles)
-    if (i0 < N && (i0 == base || keys_s[tid] != keys_s[(EV_IPT - 1) * EV_NT + tid - 1])) hmask |= 1u;
-    int64_t tot;
-    int64_t ex = block_excl_sum<EV_NT>(__popc(hmask), &tot, scan_sm);
-    // ---- decoupled look-back: global sub-run id of this tile's first head ----
-    if (tid == 0) {
+    if (nv > 0 && (tid == 0 || S.key[0][tid] != S.key[EV_IPT - 1][tid - 1])) hmask |= 1u;
+    const int nh = __popc(hmask);
+    // block exclusive scan of head counts (int32)
+    int wex = nh;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(CH_FULL, wex, o);
+        if (lane >= o) wex += y;
+    }
+    if (lane == 31) S.wheads[warp] = wex;
+    wex -= nh;
+    __syncthreads();
+    int wbase = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < EV_WARPS; w++) {
+        int c = S.wheads[w];
+        if (w < warp) wbase += c;
+        tot += c;
+    }
+    const int ex = wbase + wex;           // heads before this thread in the tile
+    // ---- decoupled look-back (warp 0, 32 predecessors per probe): global id of the tile's first head ----
+    if (warp == 0) {
         int64_t excl = 0;
         if (tile == 0) {
-            atomicExch(&P.tile_state[0], FLAG_P | (unsigned long long)tot);
+            if (lane == 0) atomicExch(&P.tile_state[0], FLAG_P | (unsigned long long)tot);
         } else {
-            atomicExch(&P.tile_state[tile], FLAG_A | (unsigned long long)tot);
-            int64_t p = tile - 1;
+            if (lane == 0) atomicExch(&P.tile_state[tile], FLAG_A | (unsigned long long)tot);
+            int64_t p = tile - 1 - lane;
             while (true) {
-                unsigned long long s = *((volatile unsigned long long *)&P.tile_state[p]);
-                unsigned long long fl = s >> 62;
-                if (fl == 0) continue;
-                excl += (int64_t)(s & VAL_MASK);
-                if (fl == 2) break;
-                p--;
+                unsigned long long s = (unsigned long long)FLAG_P;
+                if (p >= 0) s = *((volatile unsigned long long *)&P.tile_state[p]);
+                unsigned fl = (unsigned)(s >> 62);
+                unsigned pm = __ballot_sync(CH_FULL, fl == 2u), zm = __ballot_sync(CH_FULL, fl == 0u);
+                int fp = pm ? __ffs(pm) - 1 : 32;
+                unsigned need = fp >= 31 ? CH_FULL : ((2u << fp) - 1u);
+                if (zm & need) continue;                       // a predecessor has not published yet
+                int64_t v = lane <= fp ? (int64_t)(s & VAL_MASK) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CH_FULL, v, o);
+                excl += v;
+                if (fp < 32) break;
+                p -= 32;
             }
-            atomicExch(&P.tile_state[tile], FLAG_P | (unsigned long long)(excl + tot));
+            if (lane == 0) atomicExch(&P.tile_state[tile], FLAG_P | (unsigned long long)(excl + tot));
         }
-        s_excl = excl;
+        if (lane == 0) { S.excl = excl; S.tot = tot; }
     }
     __syncthreads();
-    const int64_t run0 = s_excl + ex;
+    const int64_t run0 = S.excl + ex;     // global id of this thread's first head
 
-    // ---- phase B: per-event values, outputs, thread-sequential folding ----
-    Acc acc;
-    acc.zero();
+    // ---- phase B: per-event values (a6-a8), outputs, thread-sequential folding (a9) ----
+    Acc cur, p0;
+    cur.zero();
+    p0.zero();
     bool has = false;
     int64_t curid = run0 - 1;
     CovCache cc;
@@ -473,106 +728,141 @@ __global__ void __launch_bounds__(EV_NT, 3) k_events(EvParams P) {
     bool smp = false;
     int lgp = -1;
 #pragma unroll 1
-    for (int k = 0; k < EV_IPT; k++) {
-        int64_t i = i0 + k;
-        if (i >= N) break;
-        uint32_t m = __ldg(P.meta + i);
-        int lg = P.gpu_lg[gpu_of(m)];
-        if (lg != lgp) {
-            cov_reset(cc, P.Ubeg[lg], P.Ucnt[lg]);
-            int64_t slo = P.smp_lo[lg], shi = P.smp_hi[lg];
-            smp = shi > slo;
-            smp_reset(sc, slo, shi);
-            lgp = lg;
-        }
-        if ((hmask >> k) & 1u) {
-            if (!has) { acc.store(fp, tid); has = true; }
-            else write_subrun(P, curid, acc);
-            curid++;
-            acc.zero();
-            P.sr_key[curid] = keys_s[k * EV_NT + tid];
-            P.sr_first[curid] = i;
-        }
-        int kd = kind_of(m);
-        int64_t ks = __ldg(P.ks + i), ke = __ldg(P.ke + i);
-        int64_t dur = ke - ks;
-        int64_t ovl = 0, prep = 0, call = 0, phi = 0, psi = 0;
-        acc.v[RF_NEV] += 1;
-        if (kd == CK_COMPUTE) {
-            int64_t pe = __ldg(P.pred_end + i);
-            if (pe != CH_NONE_TS) {
-                int64_t tl = __ldg(P.tl + i);
-                int64_t t2 = tl < ks ? tl : ks;                       // D6: dispatch clamped to start
-                int64_t a = t2 - pe;
-                prep = a > 0 ? a : 0;                                  // Eq. 1
-                int64_t c1 = ks - t2, c2 = ks - pe;
-                int64_t c = c1 < c2 ? c1 : c2;                         // Eq. 2
-                call = c > 0 ? c : 0;
+    for (int j = 0; j < EV_IPT / 2; j++) {
+        if (2 * j >= nv) break;
+        const longlong2 tlv = S.col[0][sw64(tid, j)], ksv = S.col[1][sw64(tid, j)], kev = S.col[2][sw64(tid, j)],
+                        pev = S.col[3][sw64(tid, j)];
+        const uint2 mv = reinterpret_cast<const uint2 *>(&S.meta[sw32(tid, j >> 1)])[j & 1];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int k = 2 * j + h;
+            if (k >= nv) break;
+            const int64_t i = i0 + k;
+            const uint32_t m = h ? mv.y : mv.x;
+            const int lg = P.gpu_lg[gpu_of(m)];
+            if (lg != lgp) {
+                cov_reset(cc, P.Ubeg[lg], P.Ucnt[lg]);
+                int64_t slo = P.smp_lo[lg], shi = P.smp_hi[lg];
+                smp = shi > slo;
+                smp_reset(sc, slo, shi);
+                if (lgp < 0 && lg == seed_lg) {
+                    if (seed[4] != -2) cov_seed(cc, P.Us, P.Ue, P.UP, seed[4]);
+                    if (seed[5] != -2 && smp) smp_seed(sc, P, seed[5]);
+                }
+                lgp = lg;
             }
-            int64_t c_ks = cov_c(cc, P.Us, P.Ue, P.UP, ks);
-            int64_t c_ke = cov_c(cc, P.Us, P.Ue, P.UP, ke);
-            ovl = c_ke - c_ks;                                         // |[t_ks, t_ke) ∩ U_g| (D9)
-            if (smp) {
-                int64_t Fa, Pa, Fb, Pb;
-                smp_F(sc, P, ks, &Fa, &Pa);
-                smp_F(sc, P, ke, &Fb, &Pb);
-                phi = Fb - Fa;                                         // MHz*ns
-                psi = Pb - Pa;                                         // mW*ns
+            if ((hmask >> k) & 1u) {
+                if (!has) { p0 = cur; has = true; }
+                else write_subrun(P, curid, cur, base);
+                curid++;
+                cur.zero();
+                P.sr_key[curid] = S.key[k][tid];
+                P.sr_first[curid] = i;
             }
-            acc.v[RF_N] += 1;
-            acc.v[RF_BUSY] += dur;
-            acc.v[RF_PREP] += prep;
-            acc.v[RF_CALL] += call;
-            acc.v[RF_OVL] += ovl;
-            acc.v[RF_PHI] += phi;
-            acc.v[RF_PSI] += psi;
-            if (ks < acc.v[RF_FIRST_KS] || (ks == acc.v[RF_FIRST_KS] && i < acc.v[RF_FIRST_IDX])) {
-                acc.v[RF_FIRST_KS] = ks;
-                acc.v[RF_FIRST_IDX] = i;
+            const int kd = kind_of(m);
+            const int64_t ks = h ? ksv.y : ksv.x, ke = h ? kev.y : kev.x;
+            const int64_t dur = ke - ks;
+            int64_t ovl = 0, prep = 0, call = 0, phi = 0, psi = 0;
+            cur.nev += 1;
+            if (kd == CK_COMPUTE) {
+                const int64_t pe = h ? pev.y : pev.x;
+                if (pe != CH_NONE_TS) {
+                    const int64_t tl = h ? tlv.y : tlv.x;
+                    const int64_t t2 = tl < ks ? tl : ks;                  // D6: dispatch clamped to start
+                    const int64_t a = t2 - pe;
+                    prep = a > 0 ? a : 0;                                   // Eq. 1
+                    const int64_t c1 = ks - t2, c2 = ks - pe;
+                    const int64_t c = c1 < c2 ? c1 : c2;                    // Eq. 2
+                    call = c > 0 ? c : 0;
+                }
+                const int64_t c_ks = cov_c(cc, P.Us, P.Ue, P.UP, ks);
+                const int64_t c_ke = cov_c(cc, P.Us, P.Ue, P.UP, ke);
+                ovl = c_ke - c_ks;                                          // |[t_ks, t_ke) ∩ U_g| (D9)
+                if (smp) {
+                    int64_t Fa, Pa, Fb, Pb;
+                    smp_F(sc, P, ks, &Fa, &Pa);
+                    smp_F(sc, P, ke, &Fb, &Pb);
+                    phi = Fb - Fa;                                          // MHz*ns
+                    psi = Pb - Pa;                                          // mW*ns
+                }
+                cur.n += 1;
+                cur.busy += dur;
+                cur.prep += prep;
+                cur.call += call;
+                cur.ovl += ovl;
+                cur.phi += phi;
+                cur.psi += psi;
+                if (ks < cur.fks || (ks == cur.fks && tid * EV_IPT + k < cur.foff)) {
+                    cur.fks = ks;
+                    cur.foff = tid * EV_IPT + k;
+                }
+                if (ke > cur.lke) cur.lke = ke;
+            } else {
+                if (kd == CK_COPY || kd == CK_OTHER) cur.copy += dur;
+                else if (kd == CK_AG) cur.ag += dur;
+                else if (kd == CK_RS) cur.rs += dur;
+                // communication overlap with the compute union feeds no table: k_covl writes it (full mode)
             }
-            if (ke > acc.v[RF_LAST_KE]) acc.v[RF_LAST_KE] = ke;
-        } else {
-            if (kd == CK_COPY || kd == CK_OTHER) acc.v[RF_COPY] += dur;
-            else if (kd == CK_AG) acc.v[RF_AG] += dur;
-            else if (kd == CK_RS) acc.v[RF_RS] += dur;
-            // communication overlap with the compute union feeds no table: k_covl writes it (full mode)
+            if (P.o_ovl && !is_comm(kd)) P.o_ovl[i] = ovl;
+            if (P.o_prep) P.o_prep[i] = prep;
+            if (P.o_call) P.o_call[i] = call;
+            if (P.o_phi) P.o_phi[i] = phi;
+            if (P.o_psi) P.o_psi[i] = psi;
+            if (P.o_run) P.o_run[i] = (int32_t)curid;
         }
-        if (P.o_ovl && !is_comm(kd)) P.o_ovl[i] = ovl;
-        if (P.o_prep) P.o_prep[i] = prep;
-        if (P.o_call) P.o_call[i] = call;
-        if (P.o_phi) P.o_phi[i] = phi;
-        if (P.o_psi) P.o_psi[i] = psi;
-        if (P.o_run) P.o_run[i] = (int32_t)curid;
     }
-    if (has) acc.store(lp, tid);
-    else acc.store(fp, tid);
-    hh[tid] = has;
+
+    // ---- runs that span threads: segmented inclusive scan of (has, tail-or-whole) over the tile ----
+    bool f = has;
+    Acc v = cur;
+    if (!__all_sync(CH_FULL, has)) {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            Acc pv = v.shfl_up(o);
+            bool pf = __shfl_up_sync(CH_FULL, f, o);
+            if (lane >= o) {
+                if (!f) { pv.merge(v); v = pv; }
+                f = f || pf;
+            }
+        }
+    }
+    if (lane == 31) { S.wagg[warp] = v; S.wflag[warp] = f; }
     __syncthreads();
-    // ---- in-tile completion of sub-runs that span threads ----
-    if (has && tid > 0) {
-        Acc s, t;
-        s.load(fp, tid);
-        int u = tid - 1;
-        while (!hh[u]) { t.load(fp, u); s.add(t); u--; }
-        t.load(lp, u);
-        s.add(t);
-        write_subrun(P, run0 - 1, s);
-    }
-    if (tid == EV_NT - 1 && base < N) {
-        int64_t last_id = s_excl + tot - 1;
-        if (has) {
-            Acc s;
-            s.load(lp, tid);
-            write_subrun(P, last_id, s);
-        } else {
-            Acc s, t;
-            s.load(fp, tid);
-            int u = tid - 1;
-            while (!hh[u]) { t.load(fp, u); s.add(t); u--; }
-            t.load(lp, u);
-            s.add(t);
-            write_subrun(P, last_id, s);
+    if (tid < EV_WARPS) {                 // carry into warp tid: segmented combine of earlier warps
+        Acc c;
+        c.zero();
+        int cf = 0;
+        for (int w = 0; w < tid; w++) {
+            if (S.wflag[w]) { c = S.wagg[w]; cf = 1; }
+            else c.merge(S.wagg[w]);
         }
+        S.wcarry[tid] = c;
+        S.wcflag[tid] = cf;
+    }
+    __syncthreads();
+    // exclusive value at this thread: warp-exclusive, completed with the warp carry if no head precedes
+    Acc e = v.shfl_up(1);
+    bool ef = __shfl_up_sync(CH_FULL, f, 1);
+    if (lane == 0) { e.zero(); ef = false; }
+    if (!ef) {
+        Acc c = S.wcarry[warp];
+        c.merge(e);
+        e = c;
+    }
+    // the run that ends in this thread's first piece (or at the end of the previous thread)
+    if (has && tid > 0) {
+        e.merge(p0);
+        write_subrun(P, run0 - 1, e, base);
+    }
+    // the run open at the end of the tile
+    if (tid == EV_NT - 1 && base < N) {
+        Acc last = v;
+        if (!f) {
+            Acc c = S.wcarry[warp];
+            c.merge(v);
+            last = c;
+        }
+        write_subrun(P, S.excl + S.tot - 1, last, base);
     }
 }
 }  // namespace
@@ -722,14 +1012,17 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     P.o_run = ctx->d_run_id;
     P.sr_key = ctx->sub.key; P.sr_first = ctx->sub.first_event; P.sr_f = ctx->sub.f; P.cap = N;
     P.tile_state = ctx->d_tile_state; P.ticket = ctx->d_tile_ticket;
-    size_t dsm = sizeof(int64_t) * (2 * NACC * EV_NT + EV_IPT * EV_NT);
+    size_t dsm = sizeof(EvSmem);
     static bool attr_set = false;
     if (!attr_set) {
         CH_CUDA(ctx, cudaFuncSetAttribute(k_events, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
         attr_set = true;
     }
+    // 16 B cp.async staging needs 16 B aligned event columns (tile bases are multiples of 2048 events)
+    auto al16 = [](const void *p) { return ((uintptr_t)p & 15u) == 0; };
+    int vec_ok = al16(P.tl) && al16(P.ks) && al16(P.ke) && al16(P.pred_end) && al16(P.meta);
     ch_tick(ctx, 4, 0);
-    k_events<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P);
+    k_events<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P, vec_ok);
     CH_LAUNCHED(ctx);
     ch_tick(ctx, 4, 1);
     if (ovl && ctx->n_lg > 0) {

@@ -23,6 +23,8 @@ __global__ void k_validate_events(const int64_t *__restrict__ tl, const int64_t 
     for (int g = threadIdx.x; g < CH_MAX_GPUS; g += blockDim.x) smax[g] = 0;
     __syncthreads();
     unsigned long long lo = ~0ull, hi = 0ull;
+    int sg = -1;
+    unsigned smx = 0;                      // max compute stream + 1 of gpu sg (flushed on change: few atomics)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         uint32_t m = meta[i];
         int g = gpu_of(m), k = kind_of(m), s = stream_of(m);
@@ -40,7 +42,14 @@ __global__ void k_validate_events(const int64_t *__restrict__ tl, const int64_t 
         } else {
             if (i == 0 || gpu_of(meta[i - 1]) != g) atomicMin(&rep->gbeg[g], (unsigned long long)i);
             if (i == n - 1 || gpu_of(meta[i + 1]) != g) atomicMax(&rep->gend[g], (unsigned long long)(i + 1));
-            if (k == CK_COMPUTE) atomicMax(&smax[g], (unsigned)(s + 1));
+            if (k == CK_COMPUTE) {
+                if (g != sg) {
+                    if (sg >= 0 && smx) atomicMax(&smax[sg], smx);
+                    sg = g;
+                    smx = 0;
+                }
+                smx = smx > (unsigned)(s + 1) ? smx : (unsigned)(s + 1);
+            }
         }
         unsigned long long ea = enc_i64(a), eb = enc_i64(b), ec = enc_i64(c);
         unsigned long long mn = ea < eb ? ea : eb, mx = ea > eb ? ea : eb;
@@ -49,6 +58,7 @@ __global__ void k_validate_events(const int64_t *__restrict__ tl, const int64_t 
         lo = lo < mn ? lo : mn;
         hi = hi > mx ? hi : mx;
     }
+    if (sg >= 0 && smx) atomicMax(&smax[sg], smx);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         unsigned long long a = __shfl_xor_sync(CH_FULL, lo, o), b = __shfl_xor_sync(CH_FULL, hi, o);
@@ -122,7 +132,7 @@ __global__ void k_make_keys(const uint32_t *__restrict__ meta, const int64_t *__
 __global__ void k_chain(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ meta,
                         const int64_t *__restrict__ ks, const int64_t *__restrict__ ke, int64_t n,
                         const int32_t *__restrict__ gpu_lg, int NG, int other, int64_t *__restrict__ pred_end,
-                        DevReport *rep, unsigned int *__restrict__ bflag) {
+                        DevReport *rep, unsigned int *__restrict__ bflag, unsigned long long *__restrict__ beg) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     uint32_t i = perm[j];
@@ -135,6 +145,7 @@ __global__ void k_chain(const uint32_t *__restrict__ perm, const uint32_t *__res
         ip = perm[j - 1];
         same = bucket_of(meta[ip], gpu_lg, NG, other) == b;
     }
+    if (!same) beg[b] = (unsigned long long)j;     // first sorted position of the bucket
     int64_t pe = CH_NONE_TS;
     if (same && grp != other) {
         int64_t a = ks[i];
@@ -166,15 +177,6 @@ __global__ void k_seg_scatter(const uint32_t *__restrict__ sorted, const int64_t
     int a = 0, b = nseg;
     while (b - a > 1) { int m = (a + b) >> 1; if (pre[m] <= t) a = m; else b = m; }
     perm[lo[a] + (t - pre[a])] = sorted[t];
-}
-
-__global__ void k_bucket_begins(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ meta, int64_t n,
-                                const int32_t *__restrict__ gpu_lg, int NG, int other,
-                                unsigned long long *__restrict__ beg) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    int b = bucket_of(meta[perm[j]], gpu_lg, NG, other);
-    if (j == 0 || bucket_of(meta[perm[j - 1]], gpu_lg, NG, other) != b) atomicMin(&beg[b], (unsigned long long)j);
 }
 
 __global__ void k_init_report(DevReport *r) {
@@ -318,12 +320,9 @@ chopper_status ch_load(chopper_ctx *ctx) {
     // bucket begins (unchanged by the per-bucket timestamp sort below)
     unsigned long long *beg = reinterpret_cast<unsigned long long *>(ctx->d_bucket_beg);
     CH_TRY(ch_fill_u64(ctx, beg, nb + 1, ~0ull));
-    k_bucket_begins<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, n, ctx->d_gpu_lg, NG,
-                                                                   other, beg);
-    CH_LAUNCHED(ctx);
     k_chain<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
                                                            ctx->ev.end_ns, n, ctx->d_gpu_lg, NG, other,
-                                                           ctx->d_pred_end, ctx->d_rep, bflag);
+                                                           ctx->d_pred_end, ctx->d_rep, bflag, beg);
     CH_LAUNCHED(ctx);
     ctx->bucket_beg.assign(nb + 1, 0);
     std::vector<unsigned int> hflag(nb + 1, 0);
@@ -380,7 +379,7 @@ chopper_status ch_load(chopper_ctx *ctx) {
                                          ctx->st));
             k_chain<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
                                                                    ctx->ev.end_ns, n, ctx->d_gpu_lg, NG, other,
-                                                                   ctx->d_pred_end, ctx->d_rep, bflag);
+                                                                   ctx->d_pred_end, ctx->d_rep, bflag, beg);
             CH_LAUNCHED(ctx);
             CH_TRY(read_report(ctx));
         }

@@ -17,7 +17,7 @@
 
 namespace {
 constexpr int NT = 256;
-constexpr int CHUNK = 256;
+constexpr int CHUNK = 64;
 constexpr int UNRES = -3;
 constexpr int SWEEP_MAX_ACTIVE = 64;
 
@@ -141,20 +141,26 @@ __global__ void k_chunk_stack(const int64_t *__restrict__ Pe, const int32_t *__r
     int64_t lo = c * CHUNK;
     if (lo >= S) return;
     int64_t hi = lo + CHUNK < S ? lo + CHUNK : S;
-    int32_t *stk = cstack + lo;
+    int32_t si[CHUNK];                 // the stack (indices and ends) stays thread-local
+    int64_t se[CHUNK];
     int sp = 0;
     int cur = -1;
+    int64_t lbeg = 0;
     for (int64_t q = lo; q < hi; q++) {
         int list = Plist[q];
-        if (list != cur) { sp = 0; cur = list; }
+        if (list != cur) { sp = 0; cur = list; lbeg = list_beg[list]; }
         int64_t e = Pe[q];
-        while (sp > 0 && Pe[stk[sp - 1]] < e) sp--;
-        if (sp > 0) parent[q] = stk[sp - 1];
-        else parent[q] = (list_beg[list] >= lo) ? -1 : UNRES;
-        stk[sp++] = (int32_t)q;
+        while (sp > 0 && se[sp - 1] < e) sp--;
+        if (sp > 0) parent[q] = si[sp - 1];
+        else parent[q] = (lbeg >= lo) ? -1 : UNRES;
+        si[sp] = (int32_t)q;
+        se[sp] = e;
+        sp++;
     }
+    int32_t *stk = cstack + lo;
+    for (int k = 0; k < sp; k++) stk[k] = si[k];
     csp[c] = sp;
-    cmax[c] = sp > 0 ? Pe[stk[0]] : INT64_MIN;   // bottom of the final stack = max end of the last list
+    cmax[c] = sp > 0 ? se[0] : INT64_MIN;   // bottom of the final stack = max end of the last list
 }
 
 __global__ void k_sparse_level(const int64_t *__restrict__ prev, int64_t *__restrict__ next, int64_t nch, int64_t w) {
@@ -347,6 +353,7 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
     int64_t mx[4] = {0, 0, 0, 0};
     for (int l = 0; l < n_lists; l++) mx[l % 4] = std::max(mx[l % 4], ctx->list_beg[l + 1] - ctx->list_beg[l]);
     ctx->kg = bits_for((uint64_t)n_lg);
+    ctx->max_it_list = mx[0];
     int tot = ctx->kg;
     for (int lv = 0; lv < 4; lv++) { ctx->kb[lv] = bits_for((uint64_t)mx[lv] + 1); tot += ctx->kb[lv]; }
     if (tot > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "instance key exceeds 64 bits");
@@ -362,7 +369,7 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         int32_t *csp = CH_ALLOC(ctx, int32_t, nch);
         int64_t *sparse = CH_ALLOC(ctx, int64_t, (int64_t)levels * nch);
         CH_ALLOC_END(ctx);
-        k_chunk_stack<<<(unsigned)ceil_div(nch, 32), 32, 0, ctx->st>>>(ctx->P_end, Plist, SL, ctx->P_parent, cstack, csp,
+        k_chunk_stack<<<(unsigned)ceil_div(nch, 64), 64, 0, ctx->st>>>(ctx->P_end, Plist, SL, ctx->P_parent, cstack, csp,
                                                                       sparse, ctx->d_list_beg);
         CH_LAUNCHED(ctx);
         for (int k = 1; k < levels; k++) {

@@ -14,90 +14,239 @@
 namespace {
 constexpr int NT = 256;
 
-// counter sums of each sub-run over its COMPUTE events, tiled like the event pass (2048 events per
-// block, 8 consecutive per thread; sub-runs never cross tiles).  Slots are processed SG at a time.
-// Pieces spanning threads are completed through shared memory in forward (input) order.
-constexpr int CT_NT = 256, CT_IPT = 8, CT_TILE = CT_NT * CT_IPT, CT_SG = 8;
+// counter sums of each sub-run over its COMPUTE events, CT_SG slots per launch.  Lane = event: warp w of
+// a block walks events [base + 256w, base + 256w + 256) 32 at a time, so every load (meta, run id, pass
+// position, and the counter values at consecutive pass positions) is coalesced.  Sums within a warp come
+// from a segmented warp scan keyed by the sub-run id; a run still open at the end of a warp is finished
+// by thread 0 from the per-warp edge pieces (sub-runs never cross 2048-event tiles).  The pass also
+// checks every value it reads -- the slot's column at every non-MEMOP event, i.e. the whole column --
+// for finiteness (R8), so a counter pass is read once.
+constexpr int CT_NT = 256, CT_TILE = 2048, CT_SG = 8, CT_WARPS = CT_NT / 32, CT_WEV = CT_TILE / CT_WARPS;
 __global__ void __launch_bounds__(CT_NT) k_counters_tiled(const uint32_t *__restrict__ meta,
                                                           const int32_t *__restrict__ run_id,
                                                           const int32_t *__restrict__ nm_rank,
                                                           const int32_t *__restrict__ gpu_lg,
                                                           const double *const *__restrict__ col, int C, int s0,
-                                                          int64_t N, double *__restrict__ out, int64_t cap) {
-    __shared__ double fp[CT_SG][CT_NT], lp[CT_SG][CT_NT];
-    __shared__ unsigned char hh[CT_NT];
-    const int tid = threadIdx.x;
-    const int64_t base = (int64_t)blockIdx.x * CT_TILE, i0 = base + (int64_t)tid * CT_IPT;
-    double acc[CT_SG];
+                                                          int64_t N, double *__restrict__ out, int64_t cap,
+                                                          unsigned int *__restrict__ colbad) {
+    __shared__ double s_lead[CT_WARPS][CT_SG], s_tail[CT_WARPS][CT_SG];
+    __shared__ int32_t s_tail_id[CT_WARPS], s_has[CT_WARPS];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * CT_TILE;
+    const int64_t w0 = base + (int64_t)w * CT_WEV;
+    const int ns = min(CT_SG, C - s0);
+    if (lane < CT_SG) s_lead[w][lane] = 0.0;
+    // the open run of this warp: running sum, id, and whether its head lies in this warp
+    double carry[CT_SG];
 #pragma unroll
-    for (int q = 0; q < CT_SG; q++) acc[q] = 0.0;
-    bool has = false;
-    int32_t cur = -1, first_head = -1;
-    int32_t prev = (i0 > base && i0 < N) ? run_id[i0 - 1] : -1;
-    for (int k = 0; k < CT_IPT; k++) {
-        int64_t i = i0 + k;
-        if (i >= N) break;
-        int32_t rid = run_id[i];
-        if (i == base || rid != prev) {
-            if (!has) {
+    for (int q = 0; q < CT_SG; q++) carry[q] = 0.0;
+    bool open = false, open_here = false, seen_head = false;
+    int32_t open_id = -1;
+    int32_t prev_last = (w0 > base && w0 < N) ? run_id[w0 - 1] : -1;   // -1: the tile start is a head
+    if (w0 > base && w0 < N) { open = true; open_id = prev_last; }      // continuing a run from the left
+    int lgc = -1;
+    const double *cp[CT_SG];
 #pragma unroll
-                for (int q = 0; q < CT_SG; q++) fp[q][tid] = acc[q];
-                has = true;
-                first_head = rid;
-            } else {
+    for (int q = 0; q < CT_SG; q++) cp[q] = nullptr;
+    for (int it = 0; it < CT_WEV / 32; it++) {
+        const int64_t e = w0 + it * 32 + lane;
+        const bool valid = e < N;
+        const uint32_t m = valid ? meta[e] : (uint32_t)CK_MEMOP;
+        const int32_t rid = valid ? run_id[e] : -2;
+        const int32_t nm = valid ? nm_rank[e] : 0;
+        int32_t rprev = __shfl_up_sync(CH_FULL, rid, 1);
+        if (lane == 0) rprev = prev_last;
+        const bool head = valid && rid != rprev;
+        const int kd = kind_of(m);
+        const bool rd = valid && kd != CK_MEMOP;
+        const int lg = rd ? gpu_lg[gpu_of(m)] : -1;
+        const int lgw = __shfl_sync(CH_FULL, lg, 31);
+        if (lgw != lgc && lgw >= 0) {
 #pragma unroll
-                for (int q = 0; q < CT_SG; q++)
-                    if (s0 + q < C) out[(int64_t)(s0 + q) * cap + cur] = acc[q];
-            }
-#pragma unroll
-            for (int q = 0; q < CT_SG; q++) acc[q] = 0.0;
-            cur = rid;
+            for (int q = 0; q < CT_SG; q++) cp[q] = q < ns ? col[lgw * C + s0 + q] : nullptr;
+            lgc = lgw;
         }
-        prev = rid;
-        uint32_t m = meta[i];
-        if (kind_of(m) == CK_COMPUTE) {
-            int lg = gpu_lg[gpu_of(m)];
-            int64_t j = nm_rank[i];
+        double v[CT_SG];
 #pragma unroll
-            for (int q = 0; q < CT_SG; q++) {
-                int s = s0 + q;
-                if (s < C) {
-                    const double *c = col[lg * C + s];
-                    if (c) acc[q] += c[j];
+        for (int q = 0; q < CT_SG; q++) {
+            v[q] = 0.0;
+            if (q < ns && rd) {
+                const double *c = lg == lgc ? cp[q] : col[lg * C + s0 + q];
+                if (c) {
+                    const double x = __ldg(c + nm);
+                    if (!isfinite(x)) atomicOr(&colbad[lg * C + s0 + q], 1u);
+                    if (kd == CK_COMPUTE) v[q] = x;
                 }
             }
         }
-    }
+        const unsigned hm = __ballot_sync(CH_FULL, head), vm = __ballot_sync(CH_FULL, valid);
+        if (vm == 0) break;                                   // past the end of the events (warp-uniform)
+        bool f = head;
 #pragma unroll
-    for (int q = 0; q < CT_SG; q++) {
-        if (has) lp[q][tid] = acc[q];
-        else fp[q][tid] = acc[q];
+        for (int o = 1; o < 32; o <<= 1) {
+            const bool pf = __shfl_up_sync(CH_FULL, f, o);
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++) {
+                const double pv = __shfl_up_sync(CH_FULL, v[q], o);
+                if (lane >= o && !f) v[q] = pv + v[q];
+            }
+            if (lane >= o) f = f || pf;
+        }
+        const int last_valid = 31 - __clz(vm);               // valid lanes are a prefix
+        const int first_head = hm ? __ffs(hm) - 1 : 32;
+        // 1) the open run: continues through lanes [0, first_head) and ends before first_head / at the end
+        if (open) {
+            const int endl = min(first_head, last_valid + 1) - 1;   // its last lane in this batch (-1: none)
+            double tot[CT_SG];
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++) {
+                const double x = __shfl_sync(CH_FULL, v[q], endl < 0 ? 0 : endl);
+                tot[q] = carry[q] + (endl >= 0 ? x : 0.0);
+            }
+            const bool ends = first_head < 32 || last_valid < 31;
+            if (ends) {
+                if (lane == 0) {
+                    if (open_here) {
+                        for (int q = 0; q < ns; q++) out[(int64_t)(s0 + q) * cap + open_id] = tot[q];
+                    } else {
+                        for (int q = 0; q < ns; q++) s_lead[w][q] = tot[q];   // edge piece of a run from the left
+                    }
+                }
+                open = false;
+            } else {
+#pragma unroll
+                for (int q = 0; q < CT_SG; q++) carry[q] = tot[q];
+            }
+        }
+        // 2) runs starting at heads of this batch: closed ones are written by their last lane
+        if (hm) {
+            const bool nxt_head = lane < 31 && ((hm >> (lane + 1)) & 1u);
+            const bool is_last = lane == last_valid;
+            if (f && head == false) {}                          // (f marks lanes at/after a head)
+            const bool closes = valid && f && (nxt_head || (is_last && last_valid < 31));
+            if (closes)
+                for (int q = 0; q < ns; q++) out[(int64_t)(s0 + q) * cap + rid] = v[q];
+            // the last head's run is open at lane 31
+            if (last_valid == 31) {
+                const int lh = 31 - __clz(hm);
+                (void)lh;
+#pragma unroll
+                for (int q = 0; q < CT_SG; q++) carry[q] = __shfl_sync(CH_FULL, v[q], 31);
+                open = true;
+                open_here = true;
+                open_id = __shfl_sync(CH_FULL, rid, 31);
+            }
+            seen_head = true;
+        }
+        prev_last = __shfl_sync(CH_FULL, rid, 31);
+        if (last_valid < 31) break;
     }
-    hh[tid] = has;
+    if (lane == 0) {
+        s_has[w] = seen_head;
+        s_tail_id[w] = open ? open_id : -1;
+#pragma unroll
+        for (int q = 0; q < CT_SG; q++) s_tail[w][q] = open ? carry[q] : 0.0;
+    }
     __syncthreads();
-    // a sub-run ending inside this thread's first piece started at the nearest earlier thread with a head
-    auto complete = [&](int upto, bool own_last, int32_t id) {
-        int u = upto - 1;
-        while (!hh[u]) u--;
-        for (int q = 0; q < CT_SG; q++) {
-            if (s0 + q >= C) break;
-            double s = lp[q][u];
-            for (int v = u + 1; v < upto; v++) s += fp[q][v];
-            s += own_last ? lp[q][upto] : fp[q][upto];
-            out[(int64_t)(s0 + q) * cap + id] = s;
-        }
-    };
-    if (has && tid > 0 && base < N) complete(tid, false, first_head - 1);
-    if (tid == CT_NT - 1 && base < N) {
-        int64_t last = base + CT_TILE - 1 < N ? base + CT_TILE - 1 : N - 1;
-        int32_t id = run_id[last];
-        if (has) {
-            for (int q = 0; q < CT_SG; q++)
-                if (s0 + q < C) out[(int64_t)(s0 + q) * cap + id] = lp[q][tid];
-        } else {
-            complete(tid, false, id);
+    // a run open at the end of warp wa (head inside wa): + whole warps without a head + the lead of the next
+    if (tid == 0) {
+        for (int wa = 0; wa < CT_WARPS; wa++) {
+            if (s_tail_id[wa] < 0 || !s_has[wa]) continue;
+            const int32_t id = s_tail_id[wa];
+            double acc[CT_SG];
+            for (int q = 0; q < ns; q++) acc[q] = s_tail[wa][q];
+            for (int wb = wa + 1; wb < CT_WARPS; wb++) {
+                if (s_has[wb]) {                                  // ends in wb's lead piece (maybe empty)
+                    for (int q = 0; q < ns; q++) acc[q] += s_lead[wb][q];
+                    break;
+                }
+                if (s_tail_id[wb] != id) {                        // wb had no events of this run: it ended
+                    for (int q = 0; q < ns; q++) acc[q] += s_lead[wb][q];
+                    break;
+                }
+                for (int q = 0; q < ns; q++) acc[q] += s_tail[wb][q];
+            }
+            for (int q = 0; q < ns; q++) out[(int64_t)(s0 + q) * cap + id] = acc[q];
         }
     }
+}
+
+// ---- instance sort: sub-run keys are produced in dispatch order, so their (gpu, iteration) prefixes
+// come in non-decreasing order; only the order inside an iteration is to be established.  Segments of
+// equal prefix are sorted in shared memory by (key, sub-run index) -- the order a stable sort gives --
+// one block per segment; a full radix sort remains the fallback when the prefix check fails.
+constexpr int SS_MAX = 4096, SS_NT = 512;
+__global__ void k_prefix_heads(const unsigned long long *__restrict__ key, int64_t n, int sh,
+                               int64_t *__restrict__ head) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    head[j] = (j == 0 || (key[j] >> sh) != (key[j - 1] >> sh)) ? 1 : 0;
+}
+// valid segments must have strictly increasing prefixes; invalid keys (all ones) form their own segments
+__global__ void k_prefix_check(const unsigned long long *__restrict__ key, const int64_t *__restrict__ starts,
+                               int64_t nseg, int sh, unsigned int *__restrict__ bad) {
+    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nseg) return;
+    const unsigned long long inv = CH_INVALID_KEY >> sh;
+    const unsigned long long p = key[starts[s]] >> sh;
+    if (starts[s + 1] - starts[s] > SS_MAX) atomicOr(bad, 2u);
+    if (p == inv) return;
+    for (int64_t t = s - 1; t >= 0 && t >= s - 2; t--) {
+        const unsigned long long q = key[starts[t]] >> sh;
+        if (q == inv) continue;
+        if (q >= p) atomicOr(bad, 1u);
+        break;
+    }
+}
+__global__ void __launch_bounds__(SS_NT) k_seg_sort(unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
+                                                    const int64_t *__restrict__ starts, int64_t nseg) {
+    __shared__ unsigned long long sk[SS_MAX];
+    __shared__ uint32_t sv[SS_MAX];
+    const int64_t lo = starts[blockIdx.x], hi = starts[blockIdx.x + 1];
+    const int n = (int)(hi - lo);
+    if (n <= 1 || n > SS_MAX) return;
+    bool sorted = true;   // fast exit for an already ordered segment
+    for (int i = threadIdx.x + 1; i < n; i += blockDim.x)
+        if (keys[lo + i] < keys[lo + i - 1]) sorted = false;
+    if (__syncthreads_and(sorted)) return;
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        sk[i] = i < n ? keys[lo + i] : ~0ull;
+        sv[i] = i < n ? vals[lo + i] : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int x = i ^ j;
+                if (x > i) {
+                    const bool up = (i & k) == 0;
+                    const unsigned long long a = sk[i], b = sk[x];
+                    const uint32_t va = sv[i], vb = sv[x];
+                    const bool gt = a > b || (a == b && va > vb);
+                    if (gt == up) { sk[i] = b; sk[x] = a; sv[i] = vb; sv[x] = va; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { keys[lo + i] = sk[i]; vals[lo + i] = sv[i]; }
+}
+// stable partition: valid keys first (in order), invalid keys after
+__global__ void k_valid_flags(const unsigned long long *__restrict__ key, int64_t n, int64_t *__restrict__ f) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n) f[j] = key[j] != CH_INVALID_KEY ? 1 : 0;
+}
+__global__ void k_partition(const unsigned long long *__restrict__ ki, const uint32_t *__restrict__ vi, int64_t n,
+                            const int64_t *__restrict__ ex, const int64_t *__restrict__ nvalid,
+                            unsigned long long *__restrict__ ko, uint32_t *__restrict__ vo) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const bool v = ki[j] != CH_INVALID_KEY;
+    const int64_t p = v ? ex[j] : *nvalid + (j - ex[j]);
+    ko[p] = ki[j];
+    vo[p] = vi[j];
 }
 
 __global__ void k_copy_keys(const unsigned long long *__restrict__ k, int64_t n, unsigned long long *__restrict__ out,
@@ -133,45 +282,146 @@ struct TabView {
     int64_t rs;      // row stride (field-major: 1; AoS sub-runs: 16)
 };
 
-// parent row p = sum of children [starts[p], starts[p+1]) visited in order (through perm if given)
-__global__ void k_sum_rows(TabView ch, const uint32_t *__restrict__ perm, const int64_t *__restrict__ starts,
-                           int64_t ng, int shift, int C, TabView pa) {
-    int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= ng) return;
-    int64_t lo = starts[p], hi = starts[p + 1];
+// parent row p = sum of children [starts[p], starts[p+1]) (through perm if given).  Integer fields are
+// exact in any order; first = lexicographic min of (first_ks, first_idx), last_ke = max.  One lane per
+// parent for small groups (children in ascending order); groups of more than SR_SMALL children are
+// summed by the whole warp (lanes stride the children, then a butterfly), which keeps a 200-child
+// iteration->gpu group off a single thread's dependent load chain.  fp64 counter sums of big groups
+// are tree-ordered (within the 1e-9 budget, D12/D22).
+constexpr int SR_SMALL = 8;
+struct RowAcc {
     int64_t v[RF_NFIELDS];
+    __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int f = 0; f < RF_NFIELDS; f++) v[f] = 0;
-    v[RF_FIRST_IDX] = INT64_MAX;
-    v[RF_FIRST_KS] = INT64_MAX;
-    v[RF_LAST_KE] = INT64_MIN;
-    unsigned long long k0 = 0;
-    for (int64_t j = lo; j < hi; j++) {
-        int64_t c = perm ? (int64_t)perm[j] : j;
-        if (j == lo) k0 = ch.key[c];
+        for (int f = 0; f < RF_NFIELDS; f++) v[f] = 0;
+        v[RF_FIRST_IDX] = INT64_MAX;
+        v[RF_FIRST_KS] = INT64_MAX;
+        v[RF_LAST_KE] = INT64_MIN;
+    }
+    __device__ __forceinline__ void add_child(const TabView &ch, int64_t c) {
+        const int64_t *b = ch.f + c * ch.rs;
+        int64_t x[RF_NFIELDS];
 #pragma unroll
-        for (int f = 0; f < RF_NFIELDS; f++) {
-            int64_t x = ch.f[(int64_t)f * ch.cap + c * ch.rs];
-            if (f == RF_FIRST_IDX || f == RF_FIRST_KS) continue;
-            if (f == RF_LAST_KE) { if (x > v[f]) v[f] = x; continue; }
-            v[f] += x;
-        }
-        int64_t cks = ch.f[(int64_t)RF_FIRST_KS * ch.cap + c * ch.rs], cidx = ch.f[(int64_t)RF_FIRST_IDX * ch.cap + c * ch.rs];
-        if (cks < v[RF_FIRST_KS] || (cks == v[RF_FIRST_KS] && cidx < v[RF_FIRST_IDX])) {
-            v[RF_FIRST_KS] = cks;
-            v[RF_FIRST_IDX] = cidx;
+        for (int f = 0; f < RF_NFIELDS; f++) x[f] = b[(int64_t)f * ch.cap];
+        merge(x);
+    }
+    __device__ __forceinline__ void merge(const int64_t *x) {
+#pragma unroll
+        for (int f = 0; f < RF_NFIELDS; f++)
+            if (f != RF_FIRST_IDX && f != RF_FIRST_KS && f != RF_LAST_KE) v[f] += x[f];
+        if (x[RF_LAST_KE] > v[RF_LAST_KE]) v[RF_LAST_KE] = x[RF_LAST_KE];
+        if (x[RF_FIRST_KS] < v[RF_FIRST_KS] || (x[RF_FIRST_KS] == v[RF_FIRST_KS] && x[RF_FIRST_IDX] < v[RF_FIRST_IDX])) {
+            v[RF_FIRST_KS] = x[RF_FIRST_KS];
+            v[RF_FIRST_IDX] = x[RF_FIRST_IDX];
         }
     }
+    __device__ __forceinline__ void warp_all() {
 #pragma unroll
-    for (int f = 0; f < RF_NFIELDS; f++) pa.f[(int64_t)f * pa.cap + p] = v[f];
-    pa.key[p] = shift >= 64 ? 0ull : ((k0 >> shift) << shift);
-    for (int s = 0; s < C; s++) {
-        double acc = 0.0;
-        for (int64_t j = lo; j < hi; j++) {
-            int64_t c = perm ? (int64_t)perm[j] : j;
-            acc += ch.cnt[(int64_t)s * ch.ccap + c];
+        for (int o = 16; o > 0; o >>= 1) {
+            int64_t y[RF_NFIELDS];
+#pragma unroll
+            for (int f = 0; f < RF_NFIELDS; f++) y[f] = __shfl_xor_sync(CH_FULL, v[f], o);
+            merge(y);
         }
-        pa.cnt[(int64_t)s * pa.ccap + p] = acc;
+    }
+};
+
+__global__ void __launch_bounds__(256) k_sum_rows(TabView ch, const uint32_t *__restrict__ perm,
+                                                  const int64_t *__restrict__ starts, int64_t ng, int shift, int C,
+                                                  TabView pa) {
+    const int lane = lane_id();
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = p < ng;
+    int64_t lo = 0, hi = 0;
+    if (valid) { lo = starts[p]; hi = starts[p + 1]; }
+    const bool big = valid && hi - lo > SR_SMALL;
+    if (valid && !big) {
+        RowAcc a;
+        a.zero();
+        for (int64_t j = lo; j < hi; j++) a.add_child(ch, perm ? (int64_t)perm[j] : j);
+#pragma unroll
+        for (int f = 0; f < RF_NFIELDS; f++) pa.f[(int64_t)f * pa.cap + p] = a.v[f];
+        unsigned long long k0 = hi > lo ? ch.key[perm ? (int64_t)perm[lo] : lo] : 0ull;
+        pa.key[p] = shift >= 64 ? 0ull : ((k0 >> shift) << shift);
+        for (int s = 0; s < C; s++) {
+            double acc = 0.0;
+            for (int64_t j = lo; j < hi; j++) acc += ch.cnt[(int64_t)s * ch.ccap + (perm ? (int64_t)perm[j] : j)];
+            pa.cnt[(int64_t)s * pa.ccap + p] = acc;
+        }
+    }
+    // big groups: the warp works through them one at a time
+    unsigned bm = __ballot_sync(CH_FULL, big);
+    while (bm) {
+        const int src = __ffs(bm) - 1;
+        bm &= bm - 1;
+        const int64_t q = __shfl_sync(CH_FULL, p, src);
+        const int64_t qlo = __shfl_sync(CH_FULL, lo, src), qhi = __shfl_sync(CH_FULL, hi, src);
+        RowAcc a;
+        a.zero();
+        for (int64_t j = qlo + lane; j < qhi; j += 32) a.add_child(ch, perm ? (int64_t)perm[j] : j);
+        a.warp_all();
+        if (lane < RF_NFIELDS) {
+            int64_t x = a.v[0];
+#pragma unroll
+            for (int f = 1; f < RF_NFIELDS; f++) if (lane == f) x = a.v[f];
+            pa.f[(int64_t)lane * pa.cap + q] = x;
+        }
+        if (lane == 0) {
+            unsigned long long k0 = ch.key[perm ? (int64_t)perm[qlo] : qlo];
+            pa.key[q] = shift >= 64 ? 0ull : ((k0 >> shift) << shift);
+        }
+        for (int s = 0; s < C; s++) {
+            double acc = 0.0;
+            for (int64_t j = qlo + lane; j < qhi; j += 32) acc += ch.cnt[(int64_t)s * ch.ccap + (perm ? (int64_t)perm[j] : j)];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(CH_FULL, acc, o);
+            if (lane == 0) pa.cnt[(int64_t)s * pa.ccap + q] = acc;
+        }
+    }
+}
+
+// warp per parent (groups averaging several children: layer / phase / iteration / gpu roll-ups and
+// points): lanes take consecutive children (coalesced on field-major tables), every field and counter
+// in one pass, then a butterfly.
+__global__ void __launch_bounds__(256) k_sum_rows_warp(TabView ch, const uint32_t *__restrict__ perm,
+                                                       const int64_t *__restrict__ starts, int64_t ng, int shift,
+                                                       int C, TabView pa) {
+    const int lane = lane_id();
+    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (q >= ng) return;
+    const int64_t qlo = starts[q], qhi = starts[q + 1];
+    RowAcc a;
+    a.zero();
+    constexpr int CMAX = 32;
+    double acc[CMAX];
+#pragma unroll
+    for (int s = 0; s < CMAX; s++) acc[s] = 0.0;
+    for (int64_t j = qlo + lane; j < qhi; j += 32) {
+        const int64_t c = perm ? (int64_t)perm[j] : j;
+        a.add_child(ch, c);
+#pragma unroll
+        for (int s = 0; s < CMAX; s++)
+            if (s < C) acc[s] += ch.cnt[(int64_t)s * ch.ccap + c];
+    }
+    a.warp_all();
+    if (lane < RF_NFIELDS) {
+        int64_t x = a.v[0];
+#pragma unroll
+        for (int f = 1; f < RF_NFIELDS; f++) if (lane == f) x = a.v[f];
+        pa.f[(int64_t)lane * pa.cap + q] = x;
+    }
+    if (lane == 0) {
+        unsigned long long k0 = qhi > qlo ? ch.key[perm ? (int64_t)perm[qlo] : qlo] : 0ull;
+        pa.key[q] = shift >= 64 ? 0ull : ((k0 >> shift) << shift);
+    }
+#pragma unroll
+    for (int s = 0; s < CMAX; s++) {
+        if (s < C) {
+            double x = acc[s];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(CH_FULL, x, o);
+            if (lane == 0) pa.cnt[(int64_t)s * pa.ccap + q] = x;
+        }
     }
 }
 
@@ -229,6 +479,103 @@ __global__ void k_point_keys(const unsigned long long *__restrict__ key, int64_t
     }
     out[j] = o;
     v[j] = (uint32_t)j;
+}
+
+// points (gpu, iteration, op label) = instances of the iteration with that op label, summed over layers
+// in instance order.  One block per iteration group of the sorted instance table:
+// chunks of PT_CH instances are loaded coalesced into shared memory, then thread l folds the chunk's
+// instances with label l in order.  Results go to a dense [label][lg][rank] grid (compacted afterwards in
+// (label, lg, rank) order = point-key order).
+constexpr int PT_CH = 128;
+__global__ void __launch_bounds__(256) k_points_iter(TabView iv, const int64_t *__restrict__ its, int64_t n_it,
+                                                     KeyLayout Lk, const int64_t *__restrict__ list_beg,
+                                                     const int32_t *__restrict__ P_label, int nL, int n_lg, int R0,
+                                                     int C, int64_t *__restrict__ df, double *__restrict__ dc,
+                                                     int64_t *__restrict__ dvalid, unsigned int *__restrict__ ovf) {
+    extern __shared__ int64_t psm[];
+    const int NF = RF_NFIELDS + C;
+    int64_t *vals = psm;                                                      // [NF][PT_CH]
+    int32_t *lab = reinterpret_cast<int32_t *>(vals + (int64_t)NF * PT_CH);   // [PT_CH]
+    double *cacc = reinterpret_cast<double *>(lab + PT_CH);                   // [256][C] counter sums
+    const int64_t g = blockIdx.x;
+    if (g >= n_it) return;
+    const int64_t a = its[g], b = its[g + 1];
+    const unsigned long long k0 = iv.key[a];
+    const int lg = (int)(k0 >> Lk.sh_lg);
+    const int rank = (int)comp(k0, Lk.sh_it, Lk.kb[0]) - 1;
+    const int64_t opb = list_beg[lg * 4 + 3];
+    const int tid = threadIdx.x;
+    const int64_t cells = (int64_t)nL * n_lg * R0;
+    for (int lbase = 0; lbase < nL; lbase += blockDim.x) {     // labels beyond the block size: another sweep
+        const int my = lbase + tid;
+        RowAcc acc;
+        acc.zero();
+        int cnt_n = 0;
+        for (int s2 = 0; s2 < C; s2++) cacc[tid * C + s2] = 0.0;
+        for (int64_t j0 = a; j0 < b; j0 += PT_CH) {
+            const int m = (int)min((int64_t)PT_CH, b - j0);
+            for (int e = tid; e < NF * PT_CH; e += blockDim.x) {
+                const int f = e / PT_CH, t = e % PT_CH;
+                if (t < m) {
+                    const int64_t j = j0 + t;
+                    vals[e] = f < RF_NFIELDS ? iv.f[(int64_t)f * iv.cap + j]
+                                             : __double_as_longlong(iv.cnt[(int64_t)(f - RF_NFIELDS) * iv.ccap + j]);
+                }
+            }
+            for (int t = tid; t < PT_CH; t += blockDim.x) {
+                int l = -1;
+                if (t < m) {
+                    const int64_t rop = comp(iv.key[j0 + t], Lk.sh_op, Lk.kb[3]);
+                    l = rop > 0 ? P_label[opb + rop - 1] : -1;
+                    if (l >= nL) { atomicOr(ovf, 1u); l = -1; }
+                }
+                lab[t] = l;
+            }
+            __syncthreads();
+            if (my < nL) {
+                const int4 *l4 = reinterpret_cast<const int4 *>(lab);
+                for (int t4 = 0; t4 < (m + 3) / 4; t4++) {
+                    const int4 q = l4[t4];
+                    const int ls[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        if (ls[u] != my) continue;
+                        const int t = 4 * t4 + u;
+                        int64_t x[RF_NFIELDS];
+#pragma unroll
+                        for (int f = 0; f < RF_NFIELDS; f++) x[f] = vals[f * PT_CH + t];
+                        acc.merge(x);
+                        for (int s2 = 0; s2 < C; s2++)
+                            cacc[tid * C + s2] += __longlong_as_double(vals[(RF_NFIELDS + s2) * PT_CH + t]);
+                        cnt_n++;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (my < nL && cnt_n > 0) {
+            const int64_t cell = ((int64_t)my * n_lg + lg) * R0 + rank;
+#pragma unroll
+            for (int f = 0; f < RF_NFIELDS; f++) df[(int64_t)f * cells + cell] = acc.v[f];
+            for (int s2 = 0; s2 < C; s2++) dc[(int64_t)s2 * cells + cell] = cacc[tid * C + s2];
+            dvalid[cell] = 1;
+        }
+        __syncthreads();
+    }
+}
+
+// compaction of the dense point grid into the point table (cell order = point-key order)
+__global__ void k_points_compact(const int64_t *__restrict__ dvalid, const int64_t *__restrict__ ex, int64_t cells,
+                                 const int64_t *__restrict__ df, const double *__restrict__ dc, int C, int n_lg, int R0,
+                                 int kg, int kb0, TabView pt) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cells || !dvalid[c]) return;
+    const int64_t p = ex[c];
+    const int64_t label = c / ((int64_t)n_lg * R0), lg = (c / R0) % n_lg, rank = c % R0;
+    pt.key[p] = ((unsigned long long)label << (kg + kb0)) | ((unsigned long long)lg << kb0) | (unsigned long long)(rank + 1);
+#pragma unroll
+    for (int f = 0; f < RF_NFIELDS; f++) pt.f[(int64_t)f * pt.cap + p] = df[(int64_t)f * cells + c];
+    for (int s2 = 0; s2 < C; s2++) pt.cnt[(int64_t)s2 * pt.ccap + p] = dc[(int64_t)s2 * cells + c];
 }
 
 __global__ void k_decode_points(const unsigned long long *__restrict__ key, int64_t n, int kg, int kb0,
@@ -356,6 +703,20 @@ static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sor
 
 static TabView view(RowTable &t) { return TabView{t.key, t.f, t.cnt, t.cap, t.cap, 1}; }
 
+// parents from n children: warp per parent when groups average >= 4 children (and counters fit the
+// warp kernel's register array), else lane per parent with warp help for the few big groups
+static chopper_status sum_rows(chopper_ctx *ctx, const TabView &ch, const uint32_t *perm, const int64_t *starts,
+                               int64_t ng, int64_t n_children, int shift, int C, const TabView &pa) {
+    if (ng <= 0) return CHOPPER_OK;
+    if (n_children >= 4 * ng && C <= 32) {
+        k_sum_rows_warp<<<(unsigned)ceil_div(ng * 32, NT), NT, 0, ctx->st>>>(ch, perm, starts, ng, shift, C, pa);
+    } else {
+        k_sum_rows<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(ch, perm, starts, ng, shift, C, pa);
+    }
+    CH_LAUNCHED(ctx);
+    return CHOPPER_OK;
+}
+
 static chopper_status rollup(chopper_ctx *ctx, RowTable &child, RowTable &parent, int shift, int depth,
                              const KeyLayout &L, int32_t *lg_gpu_d) {
     int64_t *starts;
@@ -364,9 +725,7 @@ static chopper_status rollup(chopper_ctx *ctx, RowTable &child, RowTable &parent
     CH_TRY(alloc_table(ctx, parent, std::max<int64_t>(ng, 1), ctx->C, true));
     parent.n = ng;
     if (ng > 0) {
-        k_sum_rows<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(view(child), nullptr, starts, ng, shift, ctx->C,
-                                                                   view(parent));
-        CH_LAUNCHED(ctx);
+        CH_TRY(sum_rows(ctx, view(child), nullptr, starts, ng, child.n, shift, ctx->C, view(parent)));
         k_decode<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(parent.key, ng, L, depth, lg_gpu_d, ctx->d_list_beg,
                                                                  ctx->P_orig, ctx->P_label, parent.f, parent.cap,
                                                                  ctx->d_pred_end, parent.gpu, parent.it, parent.ph,
@@ -401,11 +760,47 @@ chopper_status ch_tables(chopper_ctx *ctx) {
     // sub-run fields were written with capacity N; re-point the table view at that layout
     TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, 1, std::max<int64_t>(R, 1), 16};   // AoS sub-run rows
     if (C > 0 && R > 0) {
-        for (int s0 = 0; s0 < C; s0 += CT_SG) {
-            k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, 0, ctx->st>>>(
-                ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, s0, ctx->N, subv.cnt,
-                subv.ccap);
-            CH_LAUNCHED(ctx);
+        const int n_lg = ctx->n_lg;
+        const int n_passes = (int)ctx->passes.size();
+        ctx->d_colbad = CH_ALLOC(ctx, unsigned int, (int64_t)n_lg * C);
+        CH_ALLOC_END(ctx);
+        for (int round = 0; round < 2; round++) {
+            CH_CUDA(ctx, cudaMemsetAsync(ctx->d_colbad, 0, 4 * (size_t)n_lg * C, ctx->st));
+            for (int s0 = 0; s0 < C; s0 += CT_SG) {
+                k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, 0, ctx->st>>>(
+                    ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, s0, ctx->N, subv.cnt,
+                    subv.ccap, ctx->d_colbad);
+                CH_LAUNCHED(ctx);
+            }
+            // finiteness of every name-matching pass (R8): columns feeding a slot were checked just now,
+            // the others by k_pass_finite in ch_align
+            std::vector<unsigned int> cb((size_t)n_lg * C), pb(std::max(n_passes, 1));
+            CH_CUDA(ctx, cudaMemcpyAsync(cb.data(), ctx->d_colbad, 4 * cb.size(), cudaMemcpyDeviceToHost, ctx->st));
+            if (n_passes > 0)
+                CH_CUDA(ctx, cudaMemcpyAsync(pb.data(), ctx->d_pass_bad, 4 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            bool changed = false;
+            for (int p = 0; p < n_passes; p++) {
+                if (ctx->pass_mismatch[p] >= 0 || ctx->pass_bad[p]) continue;
+                bool bad = pb[p] != 0;
+                for (size_t q = 0; q < cb.size(); q++)
+                    if (cb[q] && ctx->sel_pass[q] == p) bad = true;
+                if (bad) { ctx->pass_bad[p] = 1; changed = true; }
+            }
+            if (round == 0) {
+                for (int p = 0; p < n_passes; p++)
+                    if (ctx->pass_bad[p]) {
+                        ctx->rep.val_count[CV_COUNTER_NONFINITE]++;
+                        if (ctx->rep.val_first[CV_COUNTER_NONFINITE] < 0 || p < ctx->rep.val_first[CV_COUNTER_NONFINITE])
+                            ctx->rep.val_first[CV_COUNTER_NONFINITE] = p;
+                        ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
+                    }
+            }
+            if (!changed) break;
+            // a slot column was non-finite: the pass is skipped and the next valid pass provides the slot
+            // (every name-matching pass's finiteness is now known, so one redo settles it)
+            CH_TRY(ch_assign_slots(ctx));
+            CH_TRY(ch_counters_full(ctx));
         }
     }
     // instances: stable sort of sub-runs by key, then group equal keys
@@ -417,7 +812,46 @@ chopper_status ch_tables(chopper_ctx *ctx) {
         CH_LAUNCHED(ctx);
     }
     bool alt = false;
-    CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, R, 0, key_bits, &alt));
+    {
+        // segmented sort inside (gpu, iteration) prefixes; radix sort if the prefixes are not in order
+        bool done = false;
+        if (R > 1) {
+            size_t mk = ctx->used;
+            int64_t *hd = CH_ALLOC(ctx, int64_t, R), *ex = CH_ALLOC(ctx, int64_t, R), *st = CH_ALLOC(ctx, int64_t, R + 2);
+            int64_t *nseg_d = CH_ALLOC(ctx, int64_t, 1);
+            unsigned int *bad = CH_ALLOC(ctx, unsigned int, 1);
+            CH_ALLOC_END(ctx);
+            k_prefix_heads<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, R, L.sh_it, hd);
+            CH_LAUNCHED(ctx);
+            CH_TRY(ch_scan_excl_i64(ctx, hd, ex, R, nseg_d));
+            k_group_starts<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(hd, ex, R, st);
+            CH_LAUNCHED(ctx);
+            int64_t nseg = 0;
+            CH_CUDA(ctx, cudaMemcpyAsync(&nseg, nseg_d, 8, cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, cudaMemsetAsync(bad, 0, 4, ctx->st));
+            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            int64_t rr = R;
+            CH_CUDA(ctx, cudaMemcpyAsync(st + nseg, &rr, 8, cudaMemcpyHostToDevice, ctx->st));
+            k_prefix_check<<<(unsigned)ceil_div(nseg, NT), NT, 0, ctx->st>>>(k1, st, nseg, L.sh_it, bad);
+            CH_LAUNCHED(ctx);
+            unsigned int hbad = 0;
+            CH_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            if (!hbad) {
+                k_seg_sort<<<(unsigned)nseg, SS_NT, 0, ctx->st>>>(k1, v1, st, nseg);
+                CH_LAUNCHED(ctx);
+                k_valid_flags<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, R, hd);
+                CH_LAUNCHED(ctx);
+                CH_TRY(ch_scan_excl_i64(ctx, hd, ex, R, nseg_d));
+                k_partition<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, v1, R, ex, nseg_d, k2, v2);
+                CH_LAUNCHED(ctx);
+                alt = true;
+                done = true;
+            }
+            ctx->used = mk;
+        }
+        if (!done) CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, R, 0, key_bits, &alt));
+    }
     unsigned long long *ks = alt ? k2 : k1;
     uint32_t *so = alt ? v2 : v1;
     {
@@ -427,8 +861,7 @@ chopper_status ch_tables(chopper_ctx *ctx) {
         CH_TRY(alloc_table(ctx, ctx->inst, std::max<int64_t>(ng, 1), C, true));
         ctx->inst.n = ng;
         if (ng > 0) {
-            k_sum_rows<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(subv, so, starts, ng, 0, C, view(ctx->inst));
-            CH_LAUNCHED(ctx);
+            CH_TRY(sum_rows(ctx, subv, so, starts, ng, R, 0, C, view(ctx->inst)));
             k_decode<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(
                 ctx->inst.key, ng, L, 4, lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->P_label, ctx->inst.f,
                 ctx->inst.cap, ctx->d_pred_end, ctx->inst.gpu, ctx->inst.it, ctx->inst.ph, ctx->inst.ly, ctx->inst.op,
@@ -459,40 +892,50 @@ chopper_status ch_tables(chopper_ctx *ctx) {
             CH_LAUNCHED(ctx);
         }
     }
-    // points (label, gpu, iteration)
+    // points (label, gpu, iteration): per-iteration label folds into a dense grid, then compaction
     {
-        int64_t n = ctx->inst.n;
+        const int64_t n = ctx->inst.n;
+        const int nL = std::max(ctx->cfg.n_labels, 1), n_lg = std::max(ctx->n_lg, 1);
+        const int R0 = (int)std::max<int64_t>(ctx->max_it_list, 1);
+        const int64_t cells = (int64_t)nL * n_lg * R0;
         int lbits = bits_for((uint64_t)std::max(ctx->cfg.n_labels, 1));
         int pbits = lbits + ctx->kg + L.kb[0];
         if (pbits > 63) return ch_fail(ctx, CHOPPER_E_RANGE, "point key exceeds 63 bits");
-        unsigned long long *p1 = CH_ALLOC(ctx, unsigned long long, n + 1), *p2 = CH_ALLOC(ctx, unsigned long long, n + 1);
-        uint32_t *q1 = CH_ALLOC(ctx, uint32_t, n + 1), *q2 = CH_ALLOC(ctx, uint32_t, n + 1);
+        int64_t *its = nullptr, n_it = 0;
+        CH_TRY(group(ctx, ctx->inst.key, n, L.sh_it, &its, &n_it));
+        int64_t *df = CH_ALLOC(ctx, int64_t, (int64_t)RF_NFIELDS * cells);
+        double *dc = CH_ALLOC(ctx, double, (int64_t)std::max(C, 1) * cells);
+        int64_t *dvalid = CH_ALLOC(ctx, int64_t, cells), *dex = CH_ALLOC(ctx, int64_t, cells), *np_d = CH_ALLOC(ctx, int64_t, 1);
+        unsigned int *ovf = CH_ALLOC(ctx, unsigned int, 1);
         CH_ALLOC_END(ctx);
-        if (n > 0) {
-            k_point_keys<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->inst.key, n, L, ctx->d_list_beg,
-                                                                        ctx->P_label, ctx->kg, p1, q1);
+        CH_CUDA(ctx, cudaMemsetAsync(dvalid, 0, 8 * (size_t)cells, ctx->st));
+        CH_CUDA(ctx, cudaMemsetAsync(ovf, 0, 4, ctx->st));
+        if (n_it > 0) {
+            size_t shb = (size_t)(RF_NFIELDS + C) * PT_CH * 8 + 4 * PT_CH + (size_t)256 * std::max(C, 1) * 8;
+            static size_t attr_shb = 0;
+            if (shb > 48 * 1024 && shb > attr_shb) {
+                CH_CUDA(ctx, cudaFuncSetAttribute(k_points_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
+                attr_shb = shb;
+            }
+            k_points_iter<<<(unsigned)n_it, 256, shb, ctx->st>>>(view(ctx->inst), its, n_it, L, ctx->d_list_beg,
+                                                                 ctx->P_label, nL, n_lg, R0, C, df, dc, dvalid, ovf);
             CH_LAUNCHED(ctx);
         }
-        bool a2 = false;
-        CH_TRY(ch_radix_sort(ctx, p1, q1, p2, q2, n, 0, pbits, &a2));
-        unsigned long long *pk = a2 ? p2 : p1;
-        uint32_t *po = a2 ? q2 : q1;
-        int64_t *starts;
-        int64_t ng;
-        CH_TRY(group(ctx, pk, n, 0, &starts, &ng));
-        CH_TRY(alloc_table(ctx, ctx->point, std::max<int64_t>(ng, 1), C, true));
-        ctx->point.n = ng;
-        if (ng > 0) {
-            // sum instance rows into points, key = point key of the first instance
-            TabView iv = view(ctx->inst);
-            TabView pv = view(ctx->point);
-            k_sum_rows<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(iv, po, starts, ng, 64, C, pv);
+        CH_TRY(ch_scan_excl_i64(ctx, dvalid, dex, cells, np_d));
+        int64_t np = 0;
+        unsigned int hovf = 0;
+        CH_CUDA(ctx, cudaMemcpyAsync(&np, np_d, 8, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "op span label >= n_labels");
+        CH_TRY(alloc_table(ctx, ctx->point, std::max<int64_t>(np, 1), C, true));
+        ctx->point.n = np;
+        if (np > 0) {
+            k_points_compact<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(dvalid, dex, cells, df, dc, C, n_lg, R0,
+                                                                              ctx->kg, L.kb[0], view(ctx->point));
             CH_LAUNCHED(ctx);
-            // point keys: the sorted point keys at the group starts
-            k_gather_keys<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(pk, starts, ng, ctx->point.key);
-            CH_LAUNCHED(ctx);
-            k_decode_points<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(
-                ctx->point.key, ng, ctx->kg, L.kb[0], lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->point.f,
+            k_decode_points<<<(unsigned)ceil_div(np, NT), NT, 0, ctx->st>>>(
+                ctx->point.key, np, ctx->kg, L.kb[0], lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->point.f,
                 ctx->point.cap, ctx->d_pred_end, ctx->point.gpu, ctx->point.it, ctx->point.ph, ctx->point.ly,
                 ctx->point.op, ctx->point.label, ctx->point.rank, ctx->point.first_pred);
             CH_LAUNCHED(ctx);

@@ -221,6 +221,41 @@ def test_counter_alignment_mismatch_and_conflict():
         assert lib.chopper_pass_conflict(pipe.ctx, q) == ref["pass.conflict"][q]
 
 
+@pytest.mark.parametrize("where", ["comm", "compute", "unused_column"])
+def test_nonfinite_counter_pass_skipped(where):
+    """R8: a pass holding a non-finite value is skipped (CV_COUNTER_NONFINITE, E_VALIDATION) and the next
+    valid pass with the slot provides it.  The GPU checks the columns feeding a slot inside the counter
+    pass and redoes the slot assignment; a column feeding no slot is checked by k_pass_finite."""
+    tt = TinyTrace(n_counters=3).span(0, 0, 0, 10_000, 1).span(0, 3, 0, 10_000, 0)
+    names, kinds = [], []
+    for k in range(40):
+        kind = AG if k % 7 == 3 else COMPUTE
+        tt.ev(0, 100 * k, 100 * k + 1, 100 * k + 50, kind=kind, stream=1 if kind == AG else 0, name=k % 3)
+        names.append(k % 3)
+        kinds.append(kind)
+    rng = np.random.default_rng(7)
+    a = rng.integers(1, 100, size=(2, len(names))).astype(float)
+    b2 = rng.integers(1, 100, size=(2, len(names))).astype(float)
+    if where == "comm":
+        a[0, kinds.index(AG)] = np.nan          # pass 0 provides slots 0, 1
+    elif where == "compute":
+        a[1, 5] = np.inf
+    b2[0] = a[0] if where != "comm" else b2[0]  # pass 1: slot 0 again (agrees unless pass 0 is skipped) + slot 2
+    tt.counter_pass(0, names, [0, 1], a)
+    tt.counter_pass(0, names, [0, 2], b2)
+    if where == "unused_column":
+        bad = rng.integers(1, 100, size=(1, len(names))).astype(float)
+        bad[0, 3] = np.nan
+        tt.counter_pass(0, names, [1], bad)      # slot 1 already provided: column feeds no slot
+    b = tt.bundle()
+    p = params(b, slot_unum=-1, slot_uden=-1)
+    ref, got, res, pipe = run_both(b, p)
+    _check_status(ref, got)
+    np.testing.assert_array_equal(ref["val.count"], got["val.count"])
+    np.testing.assert_array_equal(ref["val.first"], got["val.first"])
+    assert_parity(ref, got)
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_random_traces(seed):
     """random multi-gpu traces with nested / crossing spans, skewed dispatch, comm on two streams, copies,

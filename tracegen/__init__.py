@@ -204,6 +204,25 @@ class Bundle:
             passes=[p for p in self.passes if p[0] in gset])
 
 
+    def prefix(self, n: int) -> "Bundle":
+        """The first n events of a single-gpu bundle (dispatch order) with the spans that start before the
+        last kept dispatch, the samples up to it and each counter pass cut to the kept non-MEMOP events:
+        a bounded sample of the same workload (the CPU baseline's sample)."""
+        n = min(int(n), self.n_events)
+        if n == self.n_events:
+            return self
+        t_cut = int(self.t_l[n - 1])
+        sm = self.span_start <= t_cut
+        pm = self.smp_ts <= t_cut
+        m = int(np.count_nonzero((self.meta[:n] & 0xFF) != MEMOP))
+        return dataclasses.replace(
+            self, t_l=self.t_l[:n], t_ks=self.t_ks[:n], t_ke=self.t_ke[:n], meta=self.meta[:n],
+            name_id=self.name_id[:n], span_gl=self.span_gl[sm], span_start=self.span_start[sm],
+            span_end=self.span_end[sm], span_label=self.span_label[sm], smp_gpu=self.smp_gpu[pm],
+            smp_ts=self.smp_ts[pm], smp_freq=self.smp_freq[pm], smp_power=self.smp_power[pm],
+            passes=[(g, nm[:m], sl, vals[:, :m]) for (g, nm, sl, vals) in self.passes])
+
+
 def _meta(gpu: int, stream: int, kind: int) -> np.uint32:
     return np.uint32((gpu << 24) | (stream << 8) | kind)
 
