@@ -388,8 +388,12 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), base, 8 * hb.size(), cudaMemcpyDeviceToHost, ctx->st));
         CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
         ctx->used = mark;
-        std::vector<int64_t> m_g(n_lg);
+        std::vector<int64_t> &m_g = ctx->h_mg;       // kept in ctx: the async copy below reads it
+        m_g.assign(n_lg, 0);
         for (int l = 0; l < n_lg; l++) m_g[l] = hb[l + 1] - hb[l];
+        ctx->d_mg = CH_ALLOC(ctx, int64_t, n_lg + 1);
+        CH_ALLOC_END(ctx);
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_mg, m_g.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
 
         if (n_passes > 0) {
             std::vector<int32_t> off(n_lg + 1, 0), idx;

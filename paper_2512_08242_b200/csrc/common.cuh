@@ -152,6 +152,8 @@ struct chopper_ctx {
     PassDesc *d_passes = nullptr;
     int32_t *d_slot_pass = nullptr;  // [n_lg][C] pass index providing the slot, -1 absent
     int32_t *d_nm_rank = nullptr;    // [N] rank among non-MEMOP events of its gpu
+    int64_t *d_mg = nullptr;         // [n_lg] non-MEMOP events per local gpu (counter column length)
+    std::vector<int64_t> h_mg;
     int64_t *d_delta = nullptr;      // [n_traced]
     int32_t *d_delta_flag = nullptr;
     std::vector<int64_t> delta;

@@ -14,73 +14,112 @@
 namespace {
 constexpr int NT = 256;
 
-// counter sums of each sub-run over its COMPUTE events, CT_SG slots per launch.  Lane = event: warp w of
-// a block walks events [base + 256w, base + 256w + 256) 32 at a time, so every load (meta, run id, pass
-// position, and the counter values at consecutive pass positions) is coalesced.  Sums within a warp come
-// from a segmented warp scan keyed by the sub-run id; a run still open at the end of a warp is finished
-// by thread 0 from the per-warp edge pieces (sub-runs never cross 2048-event tiles).  The pass also
-// checks every value it reads -- the slot's column at every non-MEMOP event, i.e. the whole column --
-// for finiteness (R8), so a counter pass is read once.
-constexpr int CT_NT = 256, CT_TILE = 2048, CT_SG = 8, CT_WARPS = CT_NT / 32, CT_WEV = CT_TILE / CT_WARPS;
-__global__ void __launch_bounds__(CT_NT) k_counters_tiled(const uint32_t *__restrict__ meta,
-                                                          const int32_t *__restrict__ run_id,
-                                                          const int32_t *__restrict__ nm_rank,
-                                                          const int32_t *__restrict__ gpu_lg,
-                                                          const double *const *__restrict__ col, int C, int s0,
-                                                          int64_t N, double *__restrict__ out, int64_t cap,
-                                                          unsigned int *__restrict__ colbad) {
-    __shared__ double s_lead[CT_WARPS][CT_SG], s_tail[CT_WARPS][CT_SG];
-    __shared__ int32_t s_tail_id[CT_WARPS], s_has[CT_WARPS];
+// counter sums of each sub-run over its COMPUTE events, CT_SG slots per launch.  A block stages its
+// 2048-event tile in shared memory with cp.async -- meta, sub-run ids, pass positions, and for each slot
+// the tile's contiguous range of the counter column (events of one gpu take consecutive pass positions,
+// D2) -- so every global read is a bulk asynchronous copy.  Lane = event: warp w walks events
+// [256w, 256w + 256) 32 at a time; sums within a warp come from a segmented warp scan keyed by the
+// sub-run id, and a run still open at the end of a warp is finished by thread 0 from the per-warp edge
+// pieces (sub-runs never cross tiles).  Every value read -- the slot's column at every non-MEMOP event,
+// i.e. the whole column -- is checked for finiteness (R8), so a counter pass is read once.
+constexpr int CT_NT = 256, CT_TILE = 2048, CT_SG = 4, CT_WARPS = CT_NT / 32, CT_WEV = CT_TILE / CT_WARPS;
+struct CtSmem {
+    uint32_t meta[CT_TILE];
+    int32_t rid[CT_TILE];
+    int32_t nm[CT_TILE];
+    double val[CT_SG][CT_TILE];
+    double lead[CT_WARPS][CT_SG], tail[CT_WARPS][CT_SG];
+    int32_t tail_id[CT_WARPS], has[CT_WARPS];
+};
+__device__ __forceinline__ void ct_cp16(void *smem, const void *g) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
+}
+__device__ __forceinline__ void ct_cp8(void *smem, const void *g) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g));
+}
+__global__ void __launch_bounds__(CT_NT, 2) k_counters_tiled(const uint32_t *__restrict__ meta,
+                                                             const int32_t *__restrict__ run_id,
+                                                             const int32_t *__restrict__ nm_rank,
+                                                             const int32_t *__restrict__ gpu_lg,
+                                                             const double *const *__restrict__ col, int C, int s0,
+                                                             int64_t N, double *__restrict__ out, int64_t cap,
+                                                             unsigned int *__restrict__ colbad,
+                                                             const int64_t *__restrict__ mg, int vec_ok) {
+    extern __shared__ __align__(16) unsigned char ct_dsm[];
+    CtSmem &S = *reinterpret_cast<CtSmem *>(ct_dsm);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * CT_TILE;
-    const int64_t w0 = base + (int64_t)w * CT_WEV;
+    const int nt = (int)min((int64_t)CT_TILE, N - base);
     const int ns = min(CT_SG, C - s0);
-    if (lane < CT_SG) s_lead[w][lane] = 0.0;
-    // the open run of this warp: running sum, id, and whether its head lies in this warp
+    // ---- stage the tile ----
+    if (vec_ok && nt == CT_TILE) {
+        for (int u = tid; u < CT_TILE / 4; u += CT_NT) {
+            ct_cp16(&S.meta[4 * u], meta + base + 4 * u);
+            ct_cp16(&S.rid[4 * u], run_id + base + 4 * u);
+            ct_cp16(&S.nm[4 * u], nm_rank + base + 4 * u);
+        }
+    } else {
+        for (int e = tid; e < CT_TILE; e += CT_NT) {
+            const bool ok = e < nt;
+            S.meta[e] = ok ? meta[base + e] : (uint32_t)CK_MEMOP;
+            S.rid[e] = ok ? run_id[base + e] : -2;
+            S.nm[e] = ok ? nm_rank[base + e] : 0;
+        }
+    }
+    // one gpu in the tile (events are grouped by gpu): its pass positions form one contiguous range
+    const int lg_a = gpu_lg[gpu_of(meta[base])], lg_b = gpu_lg[gpu_of(meta[base + nt - 1])];
+    const bool single = lg_a == lg_b;
+    int64_t nm_lo = 0;
+    int cnt = 0;
+    if (single) {
+        nm_lo = nm_rank[base];
+        cnt = (int)min((int64_t)CT_TILE, mg[lg_a] - nm_lo);
+        for (int q = 0; q < ns; q++) {
+            const double *c = col[lg_a * C + s0 + q];
+            if (!c) continue;
+            for (int k = tid; k < cnt; k += CT_NT) ct_cp8(&S.val[q][k], c + nm_lo + k);
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (lane < CT_SG) { S.lead[w][lane] = 0.0; }
+    __syncthreads();
+    // ---- per warp: 8 batches of 32 events ----
+    const int e0 = w * CT_WEV;
+    const int nv_w = max(0, min(CT_WEV, nt - e0));
     double carry[CT_SG];
 #pragma unroll
     for (int q = 0; q < CT_SG; q++) carry[q] = 0.0;
-    bool open = false, open_here = false, seen_head = false;
-    int32_t open_id = -1;
-    int32_t prev_last = (w0 > base && w0 < N) ? run_id[w0 - 1] : -1;   // -1: the tile start is a head
-    if (w0 > base && w0 < N) { open = true; open_id = prev_last; }      // continuing a run from the left
-    int lgc = -1;
-    const double *cp[CT_SG];
-#pragma unroll
-    for (int q = 0; q < CT_SG; q++) cp[q] = nullptr;
-    for (int it = 0; it < CT_WEV / 32; it++) {
-        const int64_t e = w0 + it * 32 + lane;
-        const bool valid = e < N;
-        const uint32_t m = valid ? meta[e] : (uint32_t)CK_MEMOP;
-        const int32_t rid = valid ? run_id[e] : -2;
-        const int32_t nm = valid ? nm_rank[e] : 0;
-        int32_t rprev = __shfl_up_sync(CH_FULL, rid, 1);
-        if (lane == 0) rprev = prev_last;
-        const bool head = valid && rid != rprev;
+    bool open = e0 > 0 && nv_w > 0, open_here = false, seen_head = false;
+    int32_t open_id = (e0 > 0 && nv_w > 0) ? S.rid[e0 - 1] : -1;
+    for (int b = 0; b < CT_WEV / 32; b++) {
+        const int e = e0 + b * 32 + lane;
+        const bool valid = b * 32 + lane < nv_w;
+        const unsigned vm = __ballot_sync(CH_FULL, valid);
+        if (vm == 0) break;
+        const uint32_t m = S.meta[e];
+        const int32_t rid = valid ? S.rid[e] : -2;
+        const int32_t nm = S.nm[e];
+        const bool head = valid && (e == 0 || rid != S.rid[e - 1]);
         const int kd = kind_of(m);
         const bool rd = valid && kd != CK_MEMOP;
-        const int lg = rd ? gpu_lg[gpu_of(m)] : -1;
-        const int lgw = __shfl_sync(CH_FULL, lg, 31);
-        if (lgw != lgc && lgw >= 0) {
-#pragma unroll
-            for (int q = 0; q < CT_SG; q++) cp[q] = q < ns ? col[lgw * C + s0 + q] : nullptr;
-            lgc = lgw;
-        }
         double v[CT_SG];
+        const int lg = rd ? gpu_lg[gpu_of(m)] : -1;
 #pragma unroll
         for (int q = 0; q < CT_SG; q++) {
             v[q] = 0.0;
             if (q < ns && rd) {
-                const double *c = lg == lgc ? cp[q] : col[lg * C + s0 + q];
+                const double *c = col[lg * C + s0 + q];
                 if (c) {
-                    const double x = __ldg(c + nm);
+                    const double x = (single && nm - nm_lo < cnt) ? S.val[q][nm - nm_lo] : __ldg(c + nm);
                     if (!isfinite(x)) atomicOr(&colbad[lg * C + s0 + q], 1u);
                     if (kd == CK_COMPUTE) v[q] = x;
                 }
             }
         }
-        const unsigned hm = __ballot_sync(CH_FULL, head), vm = __ballot_sync(CH_FULL, valid);
-        if (vm == 0) break;                                   // past the end of the events (warp-uniform)
+        const unsigned hm = __ballot_sync(CH_FULL, head);
         bool f = head;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -92,83 +131,70 @@ __global__ void __launch_bounds__(CT_NT) k_counters_tiled(const uint32_t *__rest
             }
             if (lane >= o) f = f || pf;
         }
-        const int last_valid = 31 - __clz(vm);               // valid lanes are a prefix
+        const int last_valid = 31 - __clz(vm);
         const int first_head = hm ? __ffs(hm) - 1 : 32;
-        // 1) the open run: continues through lanes [0, first_head) and ends before first_head / at the end
-        if (open) {
-            const int endl = min(first_head, last_valid + 1) - 1;   // its last lane in this batch (-1: none)
-            double tot[CT_SG];
+        if (lane < first_head) {
 #pragma unroll
-            for (int q = 0; q < CT_SG; q++) {
-                const double x = __shfl_sync(CH_FULL, v[q], endl < 0 ? 0 : endl);
-                tot[q] = carry[q] + (endl >= 0 ? x : 0.0);
-            }
-            const bool ends = first_head < 32 || last_valid < 31;
-            if (ends) {
-                if (lane == 0) {
-                    if (open_here) {
-                        for (int q = 0; q < ns; q++) out[(int64_t)(s0 + q) * cap + open_id] = tot[q];
-                    } else {
-                        for (int q = 0; q < ns; q++) s_lead[w][q] = tot[q];   // edge piece of a run from the left
-                    }
+            for (int q = 0; q < CT_SG; q++) v[q] = carry[q] + v[q];
+        }
+        // 1) the open run ends before first_head (or at the last valid event)
+        if (open && (first_head < 32 || last_valid < 31)) {
+            const int endl = min(first_head, last_valid + 1) - 1;
+            if (lane == (endl >= 0 ? endl : 0)) {
+                for (int q = 0; q < ns; q++) {
+                    const double t = endl >= 0 ? v[q] : carry[q];
+                    if (open_here) out[(int64_t)(s0 + q) * cap + open_id] = t;
+                    else S.lead[w][q] = t;
                 }
-                open = false;
-            } else {
-#pragma unroll
-                for (int q = 0; q < CT_SG; q++) carry[q] = tot[q];
             }
+            open = false;
         }
-        // 2) runs starting at heads of this batch: closed ones are written by their last lane
-        if (hm) {
-            const bool nxt_head = lane < 31 && ((hm >> (lane + 1)) & 1u);
-            const bool is_last = lane == last_valid;
-            if (f && head == false) {}                          // (f marks lanes at/after a head)
-            const bool closes = valid && f && (nxt_head || (is_last && last_valid < 31));
-            if (closes)
-                for (int q = 0; q < ns; q++) out[(int64_t)(s0 + q) * cap + rid] = v[q];
-            // the last head's run is open at lane 31
-            if (last_valid == 31) {
-                const int lh = 31 - __clz(hm);
-                (void)lh;
+        // 2) runs starting in this batch that end inside it
+        const bool nxt_head = lane < 31 && ((hm >> (lane + 1)) & 1u);
+        if (valid && lane >= first_head && (nxt_head || (lane == last_valid && last_valid < 31)))
+            for (int q = 0; q < ns; q++) out[(int64_t)(s0 + q) * cap + rid] = v[q];
+        // 3) the run open at lane 31
+        if (last_valid == 31) {
+            if (hm) { open_here = true; open_id = __shfl_sync(CH_FULL, rid, 31); }
 #pragma unroll
-                for (int q = 0; q < CT_SG; q++) carry[q] = __shfl_sync(CH_FULL, v[q], 31);
-                open = true;
-                open_here = true;
-                open_id = __shfl_sync(CH_FULL, rid, 31);
-            }
-            seen_head = true;
+            for (int q = 0; q < CT_SG; q++) carry[q] = __shfl_sync(CH_FULL, v[q], 31);
+            open = true;
         }
-        prev_last = __shfl_sync(CH_FULL, rid, 31);
+        seen_head = seen_head || hm != 0;
         if (last_valid < 31) break;
     }
     if (lane == 0) {
-        s_has[w] = seen_head;
-        s_tail_id[w] = open ? open_id : -1;
+        S.has[w] = seen_head;
+        S.tail_id[w] = open ? open_id : -1;
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++) s_tail[w][q] = open ? carry[q] : 0.0;
+        for (int q = 0; q < CT_SG; q++) S.tail[w][q] = open ? carry[q] : 0.0;
     }
     __syncthreads();
-    // a run open at the end of warp wa (head inside wa): + whole warps without a head + the lead of the next
     if (tid == 0) {
         for (int wa = 0; wa < CT_WARPS; wa++) {
-            if (s_tail_id[wa] < 0 || !s_has[wa]) continue;
-            const int32_t id = s_tail_id[wa];
+            if (S.tail_id[wa] < 0 || !S.has[wa]) continue;
+            const int32_t id = S.tail_id[wa];
             double acc[CT_SG];
-            for (int q = 0; q < ns; q++) acc[q] = s_tail[wa][q];
+            for (int q = 0; q < ns; q++) acc[q] = S.tail[wa][q];
             for (int wb = wa + 1; wb < CT_WARPS; wb++) {
-                if (s_has[wb]) {                                  // ends in wb's lead piece (maybe empty)
-                    for (int q = 0; q < ns; q++) acc[q] += s_lead[wb][q];
+                if (S.has[wb] || S.tail_id[wb] != id) {
+                    for (int q = 0; q < ns; q++) acc[q] += S.lead[wb][q];
                     break;
                 }
-                if (s_tail_id[wb] != id) {                        // wb had no events of this run: it ended
-                    for (int q = 0; q < ns; q++) acc[q] += s_lead[wb][q];
-                    break;
-                }
-                for (int q = 0; q < ns; q++) acc[q] += s_tail[wb][q];
+                for (int q = 0; q < ns; q++) acc[q] += S.tail[wb][q];
             }
             for (int q = 0; q < ns; q++) out[(int64_t)(s0 + q) * cap + id] = acc[q];
         }
     }
+}
+
+struct KeyLayout {
+    int sh_op, sh_ly, sh_ph, sh_it, sh_lg;
+    int kb[4];
+};
+
+__device__ __forceinline__ int64_t comp(unsigned long long key, int sh, int bits) {
+    return bits == 0 ? 0 : (int64_t)((key >> sh) & ((1ull << bits) - 1));
 }
 
 // ---- instance sort: sub-run keys are produced in dispatch order, so their (gpu, iteration) prefixes
@@ -198,10 +224,33 @@ __global__ void k_prefix_check(const unsigned long long *__restrict__ key, const
         break;
     }
 }
+// Inside an iteration the sub-run keys split into four classes by how many trailing levels are "none"
+// (op > 0; op = 0 < layer; layer = op = 0 < phase; phase = layer = op = 0).  In dispatch order each class
+// is normally already ascending (ops, and the pseudo-op gaps of a layer / phase / iteration, follow time),
+// so the segment is a 4-way merge: an element's position = its index in its class + the number of
+// smaller keys in each other class (binary searches in shared memory; keys of different classes differ).
+// Ties inside a class keep dispatch order (the order of a stable sort).  A segment with an unordered class
+// falls back to a bitonic sort by (key, sub-run index).
+struct SegSortSmem {
+    unsigned long long k[SS_MAX];
+    uint32_t v[SS_MAX];
+    unsigned long long ck[SS_MAX];      // class-partitioned keys
+    uint32_t cv[SS_MAX];
+    int cbeg[5];
+    int unsorted;
+    int64_t scan[33];
+};
+__device__ __forceinline__ int seg_class(unsigned long long k, const KeyLayout &L) {
+    if (k == CH_INVALID_KEY) return 3;
+    if (comp(k, L.sh_op, L.kb[3]) > 0) return 0;
+    if (comp(k, L.sh_ly, L.kb[2]) > 0) return 1;
+    if (comp(k, L.sh_ph, L.kb[1]) > 0) return 2;
+    return 3;
+}
 __global__ void __launch_bounds__(SS_NT) k_seg_sort(unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
-                                                    const int64_t *__restrict__ starts, int64_t nseg) {
-    __shared__ unsigned long long sk[SS_MAX];
-    __shared__ uint32_t sv[SS_MAX];
+                                                    const int64_t *__restrict__ starts, int64_t nseg, KeyLayout L) {
+    extern __shared__ __align__(16) unsigned char ss_dsm[];
+    SegSortSmem &S = *reinterpret_cast<SegSortSmem *>(ss_dsm);
     const int64_t lo = starts[blockIdx.x], hi = starts[blockIdx.x + 1];
     const int n = (int)(hi - lo);
     if (n <= 1 || n > SS_MAX) return;
@@ -209,11 +258,63 @@ __global__ void __launch_bounds__(SS_NT) k_seg_sort(unsigned long long *__restri
     for (int i = threadIdx.x + 1; i < n; i += blockDim.x)
         if (keys[lo + i] < keys[lo + i - 1]) sorted = false;
     if (__syncthreads_and(sorted)) return;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { S.k[i] = keys[lo + i]; S.v[i] = vals[lo + i]; }
+    if (threadIdx.x == 0) { S.unsorted = 0; S.cbeg[0] = 0; }
+    __syncthreads();
+    // stable partition by class: per-thread chunk counts, one packed block scan (4 x 16-bit counters)
+    const int per = (n + SS_NT - 1) / SS_NT;
+    const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
+    unsigned long long cnt = 0;
+    for (int i = i0; i < i1; i++) cnt += 1ull << (16 * seg_class(S.k[i], L));
+    int64_t tot;
+    unsigned long long ex = (unsigned long long)block_excl_sum<SS_NT>((int64_t)cnt, &tot, S.scan);
+    const unsigned long long t64 = (unsigned long long)tot;
+    int cb[4];
+    cb[0] = 0;
+    cb[1] = (int)(t64 & 0xFFFF);
+    cb[2] = cb[1] + (int)((t64 >> 16) & 0xFFFF);
+    cb[3] = cb[2] + (int)((t64 >> 32) & 0xFFFF);
+    if (threadIdx.x == 0) { S.cbeg[1] = cb[1]; S.cbeg[2] = cb[2]; S.cbeg[3] = cb[3]; S.cbeg[4] = n; }
+    int pos[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) pos[c] = cb[c] + (int)((ex >> (16 * c)) & 0xFFFF);
+    for (int i = i0; i < i1; i++) {
+        const int c = seg_class(S.k[i], L);
+        const int d = pos[c]++;
+        S.ck[d] = S.k[i];
+        S.cv[d] = S.v[i];
+    }
+    __syncthreads();
+    // every class ascending?
+    for (int c = 0; c < 4; c++)
+        for (int d = S.cbeg[c] + 1 + threadIdx.x; d < S.cbeg[c + 1]; d += blockDim.x)
+            if (S.ck[d] < S.ck[d - 1]) S.unsorted = 1;
+    __syncthreads();
+    if (!S.unsorted) {
+        for (int d = threadIdx.x; d < n; d += blockDim.x) {
+            int c = 0;
+            while (d >= S.cbeg[c + 1]) c++;
+            const unsigned long long x = S.ck[d];
+            int p = d - S.cbeg[c];
+            for (int o = 0; o < 4; o++) {
+                if (o == c) continue;
+                int l2 = S.cbeg[o], h2 = S.cbeg[o + 1];     // count of class-o keys < x
+                while (l2 < h2) {
+                    const int m = (l2 + h2) >> 1;
+                    if (S.ck[m] < x) l2 = m + 1; else h2 = m;
+                }
+                p += l2 - S.cbeg[o];
+            }
+            keys[lo + p] = x;
+            vals[lo + p] = S.cv[d];
+        }
+        return;
+    }
+    // fallback: bitonic sort by (key, sub-run index)
     int n2 = 1;
     while (n2 < n) n2 <<= 1;
     for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-        sk[i] = i < n ? keys[lo + i] : ~0ull;
-        sv[i] = i < n ? vals[lo + i] : 0xFFFFFFFFu;
+        if (i >= n) { S.k[i] = ~0ull; S.v[i] = 0xFFFFFFFFu; }
     }
     __syncthreads();
     for (int k = 2; k <= n2; k <<= 1) {
@@ -222,17 +323,18 @@ __global__ void __launch_bounds__(SS_NT) k_seg_sort(unsigned long long *__restri
                 const int x = i ^ j;
                 if (x > i) {
                     const bool up = (i & k) == 0;
-                    const unsigned long long a = sk[i], b = sk[x];
-                    const uint32_t va = sv[i], vb = sv[x];
-                    const bool gt = a > b || (a == b && va > vb);
-                    if (gt == up) { sk[i] = b; sk[x] = a; sv[i] = vb; sv[x] = va; }
+                    const unsigned long long a2 = S.k[i], b2 = S.k[x];
+                    const uint32_t va = S.v[i], vb = S.v[x];
+                    const bool gt = a2 > b2 || (a2 == b2 && va > vb);
+                    if (gt == up) { S.k[i] = b2; S.k[x] = a2; S.v[i] = vb; S.v[x] = va; }
                 }
             }
             __syncthreads();
         }
     }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) { keys[lo + i] = sk[i]; vals[lo + i] = sv[i]; }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { keys[lo + i] = S.k[i]; vals[lo + i] = S.v[i]; }
 }
+
 // stable partition: valid keys first (in order), invalid keys after
 __global__ void k_valid_flags(const unsigned long long *__restrict__ key, int64_t n, int64_t *__restrict__ f) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -425,13 +527,73 @@ __global__ void __launch_bounds__(256) k_sum_rows_warp(TabView ch, const uint32_
     }
 }
 
-struct KeyLayout {
-    int sh_op, sh_ly, sh_ph, sh_it, sh_lg;
-    int kb[4];
-};
-
-__device__ __forceinline__ int64_t comp(unsigned long long key, int sh, int bits) {
-    return bits == 0 ? 0 : (int64_t)((key >> sh) & ((1ull << bits) - 1));
+// block of RC_NT parents: their children (a contiguous range, or a perm range) are staged RC_CH at a time
+// in shared memory -- coalesced column loads for field-major tables, one 128 B row per child for the
+// AoS sub-run rows -- and each thread folds its own parent's children from shared memory in order.
+constexpr int RC_NT = 256, RC_CH = 256;
+__global__ void __launch_bounds__(RC_NT) k_sum_rows_chunked(TabView ch, const uint32_t *__restrict__ perm,
+                                                            const int64_t *__restrict__ starts, int64_t ng, int shift,
+                                                            int C, TabView pa) {
+    extern __shared__ int64_t rsm[];
+    const int NF = RF_NFIELDS + C;
+    int64_t *vals = rsm;                               // [NF][RC_CH]
+    const int tid = threadIdx.x;
+    const int64_t p0 = (int64_t)blockIdx.x * RC_NT;
+    const int64_t pend = min(p0 + RC_NT, ng);
+    const int64_t p = p0 + tid;
+    const int64_t c_lo = starts[p0], c_hi = starts[pend];
+    int64_t my_lo = 0, my_hi = 0;
+    if (p < ng) { my_lo = starts[p]; my_hi = starts[p + 1]; }
+    RowAcc a;
+    a.zero();
+    double cs[8];
+#pragma unroll
+    for (int s2 = 0; s2 < 8; s2++) cs[s2] = 0.0;
+    for (int64_t j0 = c_lo; j0 < c_hi; j0 += RC_CH) {
+        const int m = (int)min((int64_t)RC_CH, c_hi - j0);
+        if (ch.rs == 1 && !perm) {
+            for (int e = tid; e < NF * RC_CH; e += RC_NT) {
+                const int f = e / RC_CH, t = e % RC_CH;
+                if (t < m) {
+                    const int64_t c = j0 + t;
+                    vals[e] = f < RF_NFIELDS ? ch.f[(int64_t)f * ch.cap + c]
+                                             : __double_as_longlong(ch.cnt[(int64_t)(f - RF_NFIELDS) * ch.ccap + c]);
+                }
+            }
+        } else {
+            for (int t = tid; t < m; t += RC_NT) {
+                const int64_t c = perm ? (int64_t)perm[j0 + t] : j0 + t;
+                const int64_t *row = ch.f + c * ch.rs;
+#pragma unroll
+                for (int f = 0; f < RF_NFIELDS; f++) vals[f * RC_CH + t] = row[(int64_t)f * ch.cap];
+                for (int s2 = 0; s2 < C; s2++)
+                    vals[(RF_NFIELDS + s2) * RC_CH + t] = __double_as_longlong(ch.cnt[(int64_t)s2 * ch.ccap + c]);
+            }
+        }
+        __syncthreads();
+        const int64_t a0 = my_lo > j0 ? my_lo : j0, a1 = my_hi < j0 + m ? my_hi : j0 + m;
+        for (int64_t c = a0; c < a1; c++) {
+            const int t = (int)(c - j0);
+            int64_t x[RF_NFIELDS];
+#pragma unroll
+            for (int f = 0; f < RF_NFIELDS; f++) x[f] = vals[f * RC_CH + t];
+            a.merge(x);
+#pragma unroll
+            for (int s2 = 0; s2 < 8; s2++)
+                if (s2 < C) cs[s2] += __longlong_as_double(vals[(RF_NFIELDS + s2) * RC_CH + t]);
+            for (int s2 = 8; s2 < C; s2++)            // C > 8: accumulate in place
+                pa.cnt[(int64_t)s2 * pa.ccap + p] += __longlong_as_double(vals[(RF_NFIELDS + s2) * RC_CH + t]);
+        }
+        __syncthreads();
+    }
+    if (p >= ng) return;
+#pragma unroll
+    for (int f = 0; f < RF_NFIELDS; f++) pa.f[(int64_t)f * pa.cap + p] = a.v[f];
+#pragma unroll
+    for (int s2 = 0; s2 < 8; s2++)
+        if (s2 < C) pa.cnt[(int64_t)s2 * pa.ccap + p] = cs[s2];
+    const unsigned long long k0 = my_hi > my_lo ? ch.key[perm ? (int64_t)perm[my_lo] : my_lo] : 0ull;
+    pa.key[p] = shift >= 64 ? 0ull : ((k0 >> shift) << shift);
 }
 
 // identity columns of a row table: caller span indices, gpu, op label, iteration rank
@@ -486,17 +648,23 @@ __global__ void k_point_keys(const unsigned long long *__restrict__ key, int64_t
 // chunks of PT_CH instances are loaded coalesced into shared memory, then thread l folds the chunk's
 // instances with label l in order.  Results go to a dense [label][lg][rank] grid (compacted afterwards in
 // (label, lg, rank) order = point-key order).
-constexpr int PT_CH = 128;
+constexpr int PT_CH = 256;
 __global__ void __launch_bounds__(256) k_points_iter(TabView iv, const int64_t *__restrict__ its, int64_t n_it,
                                                      KeyLayout Lk, const int64_t *__restrict__ list_beg,
                                                      const int32_t *__restrict__ P_label, int nL, int n_lg, int R0,
                                                      int C, int64_t *__restrict__ df, double *__restrict__ dc,
                                                      int64_t *__restrict__ dvalid, unsigned int *__restrict__ ovf) {
+    // one instance per thread per chunk; a stable counting sort by label puts each label's instances of
+    // the chunk in a contiguous list (instance order), which thread `label` then folds
     extern __shared__ int64_t psm[];
     const int NF = RF_NFIELDS + C;
     int64_t *vals = psm;                                                      // [NF][PT_CH]
-    int32_t *lab = reinterpret_cast<int32_t *>(vals + (int64_t)NF * PT_CH);   // [PT_CH]
-    double *cacc = reinterpret_cast<double *>(lab + PT_CH);                   // [256][C] counter sums
+    double *cacc = reinterpret_cast<double *>(vals + (int64_t)NF * PT_CH);    // [nL][C]
+    int32_t *lab = reinterpret_cast<int32_t *>(cacc + (int64_t)nL * C);       // [PT_CH]
+    int32_t *order = lab + PT_CH;                                             // [PT_CH]
+    int32_t *wc = order + PT_CH;                                              // [8][nL] per-warp counts
+    int32_t *lstart = wc + 8 * nL;                                            // [nL]
+    __shared__ int64_t scan_sm[33];
     const int64_t g = blockIdx.x;
     if (g >= n_it) return;
     const int64_t a = its[g], b = its[g + 1];
@@ -504,63 +672,65 @@ __global__ void __launch_bounds__(256) k_points_iter(TabView iv, const int64_t *
     const int lg = (int)(k0 >> Lk.sh_lg);
     const int rank = (int)comp(k0, Lk.sh_it, Lk.kb[0]) - 1;
     const int64_t opb = list_beg[lg * 4 + 3];
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t cells = (int64_t)nL * n_lg * R0;
-    for (int lbase = 0; lbase < nL; lbase += blockDim.x) {     // labels beyond the block size: another sweep
-        const int my = lbase + tid;
-        RowAcc acc;
-        acc.zero();
-        int cnt_n = 0;
-        for (int s2 = 0; s2 < C; s2++) cacc[tid * C + s2] = 0.0;
-        for (int64_t j0 = a; j0 < b; j0 += PT_CH) {
-            const int m = (int)min((int64_t)PT_CH, b - j0);
-            for (int e = tid; e < NF * PT_CH; e += blockDim.x) {
-                const int f = e / PT_CH, t = e % PT_CH;
-                if (t < m) {
-                    const int64_t j = j0 + t;
-                    vals[e] = f < RF_NFIELDS ? iv.f[(int64_t)f * iv.cap + j]
-                                             : __double_as_longlong(iv.cnt[(int64_t)(f - RF_NFIELDS) * iv.ccap + j]);
-                }
+    RowAcc acc;
+    acc.zero();
+    int cnt_n = 0;
+    for (int q = tid; q < nL * C; q += blockDim.x) cacc[q] = 0.0;
+    for (int64_t j0 = a; j0 < b; j0 += PT_CH) {
+        const int m = (int)min((int64_t)PT_CH, b - j0);
+        for (int e = tid; e < NF * PT_CH; e += blockDim.x) {
+            const int f = e / PT_CH, t = e % PT_CH;
+            if (t < m) {
+                const int64_t j = j0 + t;
+                vals[e] = f < RF_NFIELDS ? iv.f[(int64_t)f * iv.cap + j]
+                                         : __double_as_longlong(iv.cnt[(int64_t)(f - RF_NFIELDS) * iv.ccap + j]);
             }
-            for (int t = tid; t < PT_CH; t += blockDim.x) {
-                int l = -1;
-                if (t < m) {
-                    const int64_t rop = comp(iv.key[j0 + t], Lk.sh_op, Lk.kb[3]);
-                    l = rop > 0 ? P_label[opb + rop - 1] : -1;
-                    if (l >= nL) { atomicOr(ovf, 1u); l = -1; }
-                }
-                lab[t] = l;
-            }
-            __syncthreads();
-            if (my < nL) {
-                const int4 *l4 = reinterpret_cast<const int4 *>(lab);
-                for (int t4 = 0; t4 < (m + 3) / 4; t4++) {
-                    const int4 q = l4[t4];
-                    const int ls[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        if (ls[u] != my) continue;
-                        const int t = 4 * t4 + u;
-                        int64_t x[RF_NFIELDS];
-#pragma unroll
-                        for (int f = 0; f < RF_NFIELDS; f++) x[f] = vals[f * PT_CH + t];
-                        acc.merge(x);
-                        for (int s2 = 0; s2 < C; s2++)
-                            cacc[tid * C + s2] += __longlong_as_double(vals[(RF_NFIELDS + s2) * PT_CH + t]);
-                        cnt_n++;
-                    }
-                }
-            }
-            __syncthreads();
         }
-        if (my < nL && cnt_n > 0) {
-            const int64_t cell = ((int64_t)my * n_lg + lg) * R0 + rank;
-#pragma unroll
-            for (int f = 0; f < RF_NFIELDS; f++) df[(int64_t)f * cells + cell] = acc.v[f];
-            for (int s2 = 0; s2 < C; s2++) dc[(int64_t)s2 * cells + cell] = cacc[tid * C + s2];
-            dvalid[cell] = 1;
+        for (int q = tid; q < 8 * nL; q += blockDim.x) wc[q] = 0;
+        int l = -1;
+        if (tid < m) {
+            const int64_t rop = comp(iv.key[j0 + tid], Lk.sh_op, Lk.kb[3]);
+            l = rop > 0 ? P_label[opb + rop - 1] : -1;
+            if (l >= nL) { atomicOr(ovf, 1u); l = -1; }
         }
         __syncthreads();
+        const unsigned mm = __match_any_sync(CH_FULL, l);
+        const int inrank = __popc(mm & lanemask_lt());
+        if (l >= 0 && inrank == 0) wc[w * nL + l] = __popc(mm);
+        __syncthreads();
+        // per label: counts over warps (exclusive per warp) and the label's start in the chunk order
+        int tot_l = 0;
+        if (tid < nL) {
+            for (int x = 0; x < 8; x++) { const int c = wc[x * nL + tid]; wc[x * nL + tid] = tot_l; tot_l += c; }
+        }
+        int64_t dummy;
+        const int st = (int)block_excl_sum<256>(tid < nL ? tot_l : 0, &dummy, scan_sm);
+        if (tid < nL) lstart[tid] = st;
+        __syncthreads();
+        if (l >= 0) order[lstart[l] + wc[w * nL + l] + inrank] = tid;
+        __syncthreads();
+        if (tid < nL) {
+            for (int k = st; k < st + tot_l; k++) {
+                const int t = order[k];
+                int64_t x[RF_NFIELDS];
+#pragma unroll
+                for (int f = 0; f < RF_NFIELDS; f++) x[f] = vals[f * PT_CH + t];
+                acc.merge(x);
+                for (int s2 = 0; s2 < C; s2++)
+                    cacc[tid * C + s2] += __longlong_as_double(vals[(RF_NFIELDS + s2) * PT_CH + t]);
+            }
+            cnt_n += tot_l;
+        }
+        __syncthreads();
+    }
+    if (tid < nL && cnt_n > 0) {
+        const int64_t cell = ((int64_t)tid * n_lg + lg) * R0 + rank;
+#pragma unroll
+        for (int f = 0; f < RF_NFIELDS; f++) df[(int64_t)f * cells + cell] = acc.v[f];
+        for (int s2 = 0; s2 < C; s2++) dc[(int64_t)s2 * cells + cell] = cacc[tid * C + s2];
+        dvalid[cell] = 1;
     }
 }
 
@@ -708,8 +878,19 @@ static TabView view(RowTable &t) { return TabView{t.key, t.f, t.cnt, t.cap, t.ca
 static chopper_status sum_rows(chopper_ctx *ctx, const TabView &ch, const uint32_t *perm, const int64_t *starts,
                                int64_t ng, int64_t n_children, int shift, int C, const TabView &pa) {
     if (ng <= 0) return CHOPPER_OK;
-    if (n_children >= 4 * ng && C <= 32) {
+    const size_t shb = (size_t)(RF_NFIELDS + C) * RC_CH * 8;
+    if (n_children >= 16 * ng && C <= 32) {
+        // parents with many children (layer -> phase, iteration -> gpu): a warp per parent
         k_sum_rows_warp<<<(unsigned)ceil_div(ng * 32, NT), NT, 0, ctx->st>>>(ch, perm, starts, ng, shift, C, pa);
+    } else if (ng >= (int64_t)RC_NT * 148 && shb <= 160 * 1024) {
+        // many parents with a few children each (instance -> layer): children staged per block
+        static size_t attr = 0;
+        if (shb > 48 * 1024 && shb > attr) {
+            CH_CUDA(ctx, cudaFuncSetAttribute(k_sum_rows_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
+            attr = shb;
+        }
+        if (C > 8) CH_CUDA(ctx, cudaMemsetAsync(pa.cnt, 0, 8 * (size_t)C * pa.ccap, ctx->st));
+        k_sum_rows_chunked<<<(unsigned)ceil_div(ng, RC_NT), RC_NT, shb, ctx->st>>>(ch, perm, starts, ng, shift, C, pa);
     } else {
         k_sum_rows<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(ch, perm, starts, ng, shift, C, pa);
     }
@@ -766,10 +947,17 @@ chopper_status ch_tables(chopper_ctx *ctx) {
         CH_ALLOC_END(ctx);
         for (int round = 0; round < 2; round++) {
             CH_CUDA(ctx, cudaMemsetAsync(ctx->d_colbad, 0, 4 * (size_t)n_lg * C, ctx->st));
+            static bool attr = false;
+            if (!attr) {
+                CH_CUDA(ctx, cudaFuncSetAttribute(k_counters_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)sizeof(CtSmem)));
+                attr = true;
+            }
+            const int vec_ok = (((uintptr_t)ctx->ev.meta | (uintptr_t)ctx->d_run_id | (uintptr_t)ctx->d_nm_rank) & 15u) == 0;
             for (int s0 = 0; s0 < C; s0 += CT_SG) {
-                k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, 0, ctx->st>>>(
+                k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->st>>>(
                     ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, s0, ctx->N, subv.cnt,
-                    subv.ccap, ctx->d_colbad);
+                    subv.ccap, ctx->d_colbad, ctx->d_mg, vec_ok);
                 CH_LAUNCHED(ctx);
             }
             // finiteness of every name-matching pass (R8): columns feeding a slot were checked just now,
@@ -838,7 +1026,13 @@ chopper_status ch_tables(chopper_ctx *ctx) {
             CH_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->st));
             CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
             if (!hbad) {
-                k_seg_sort<<<(unsigned)nseg, SS_NT, 0, ctx->st>>>(k1, v1, st, nseg);
+                static bool ss_attr = false;
+                if (!ss_attr) {
+                    CH_CUDA(ctx, cudaFuncSetAttribute(k_seg_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      (int)sizeof(SegSortSmem)));
+                    ss_attr = true;
+                }
+                k_seg_sort<<<(unsigned)nseg, SS_NT, sizeof(SegSortSmem), ctx->st>>>(k1, v1, st, nseg, L);
                 CH_LAUNCHED(ctx);
                 k_valid_flags<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, R, hd);
                 CH_LAUNCHED(ctx);
@@ -911,7 +1105,8 @@ chopper_status ch_tables(chopper_ctx *ctx) {
         CH_CUDA(ctx, cudaMemsetAsync(dvalid, 0, 8 * (size_t)cells, ctx->st));
         CH_CUDA(ctx, cudaMemsetAsync(ovf, 0, 4, ctx->st));
         if (n_it > 0) {
-            size_t shb = (size_t)(RF_NFIELDS + C) * PT_CH * 8 + 4 * PT_CH + (size_t)256 * std::max(C, 1) * 8;
+            if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels");
+            size_t shb = (size_t)(RF_NFIELDS + C) * PT_CH * 8 + (size_t)nL * C * 8 + 4 * (2 * PT_CH + 9 * (size_t)nL);
             static size_t attr_shb = 0;
             if (shb > 48 * 1024 && shb > attr_shb) {
                 CH_CUDA(ctx, cudaFuncSetAttribute(k_points_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
