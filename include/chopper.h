@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define CHOPPER_ABI_VERSION 1
+#define CHOPPER_ABI_VERSION 3
 
 typedef struct chopper_ctx chopper_ctx;
 typedef int32_t chopper_status;
@@ -142,13 +142,14 @@ typedef struct {
  * chopper_load_columns / chopper_destroy).  Columns are [n] unless noted. */
 typedef struct {
     int64_t n;
+    int64_t stride;                           /* column stride of counters / rates (>= n: the table capacity) */
     const int32_t *gpu, *it, *ph, *ly, *op;   /* caller span indices, -1 = none (unlabeled) */
     const int32_t *label;                     /* op label (points, instances), -1 otherwise */
     const int32_t *rank;                      /* iteration rank (iteration rows, points) else -1 */
     const int64_t *n_events, *n_compute, *busy, *first_ks, *first_idx, *first_pred, *last_ke;
     const int64_t *prep, *call, *ovl, *phi, *psi, *copy_ns, *ag_ns, *rs_ns;
-    const double *counters;                   /* [n_counters][n] */
-    const double *rates;                      /* [n_ratios][n] (points, iterations) or NULL */
+    const double *counters;                   /* [n_counters][stride] */
+    const double *rates;                      /* [n_ratios][stride] (points, iterations) or NULL */
     /* iteration rows only (else NULL) */
     const int64_t *wall, *comm_union, *aligned_first, *aligned_last;
     const int32_t *step;
@@ -175,6 +176,12 @@ typedef struct {
     int64_t delta[256];                       /* clock offsets per traced gpu (D13) */
     int32_t delta_flag[256];
     int64_t max_skew_ag, max_skew_rs;
+    /* report statistics per op label (O14): 16 doubles per label:
+     * 0 n_points, 1-5 duration q0, q25, q50, q75, q100 (ns), 6-10 overlap ratio q0..q100,
+     * 11 Pearson(overlap ratio, duration) (NaN if either is constant), 12 label, 13 mean duration (ns).
+     * Quantiles interpolate linearly at h = q (n - 1) (R9). */
+    int64_t n_report;
+    double report[256 * 16];
 } chopper_global;
 
 /* Device-side report read back by chopper_load_columns (host struct). */

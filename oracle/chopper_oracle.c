@@ -110,6 +110,16 @@ static double median_f64(const double *v, int64_t n) {
     return m;
 }
 
+/* quantile of sorted values at q in [0, 1]: linear interpolation between the order statistics at
+   h = q (n - 1) (R9; q = 0.5 is the D21 median up to the rounding of the interpolation) */
+static double quantile_sorted(const double *x, int64_t n, double q) {
+    double h = q * (double)(n - 1);
+    int64_t lo = (int64_t)floor(h);
+    if (lo >= n - 1) return x[n - 1];
+    double fr = h - (double)lo;
+    return x[lo] + fr * (x[lo + 1] - x[lo]);
+}
+
 /* ------------------------------------------------------------------ */
 /* O2: stable sort of events by (gpu, group, t_ks) (D1)                 */
 /* ------------------------------------------------------------------ */
@@ -275,6 +285,7 @@ typedef struct { int64_t busy, launch, ovl, phi; double cg, fp, un, ud; } point_
 enum { BD_FIT = 1, BD_NO_FLOPS = 2, BD_NO_UTIL = 4, BD_UTIL_RANGE = 8, BD_D0_ZERO = 16, BD_NO_CYCLES = 32,
        BD_NO_SAMPLES = 64, BD_INSUFFICIENT = 128 };
 #define N_BD 16
+#define N_RS 16
 /* out fields: 0 n_points,1 method,2 D_act_s,3 D0_s,4 D50_s,5 D_thr,6 Ovr_inst,7 Ovr_util,8 Ovr_overlap,
    9 D_peak,10 Ovr_freq,11 Ovr_launch,12 residual,13 Ovr_freq_samples,14 flags,15 label */
 static void breakdown_label(const or_input *in, int L, const point_t *p, int64_t n, int has_cyc, int has_fl,
@@ -798,6 +809,53 @@ or_result *or_run(const or_input *in) {
             w++;
         }
         free(pp);
+    }
+
+    /* ---------------- O14 report statistics per op label ----
+       Over the same points as O13 (sampled iterations, busy > 0, all op labels), in (gpu, iteration) order:
+       duration and overlap-ratio quantiles (min, q25, median, q75, max; R9) -- the fills of Fig. 6 -- and the
+       Pearson correlation of overlap ratio with duration (R10; NaN when either is constant, as the paper's
+       "low or nan values").  Row: 0 n, 1-5 duration q0..q100 (ns), 6-10 ratio q0..q100, 11 pearson,
+       12 label, 13 mean duration (ns), 14-15 NaN. */
+    {
+        double *rs = new_f64(r, "report.rows", (int64_t)in->n_labels * N_RS);
+        double *b = (double *)xcalloc(n_pt > 0 ? n_pt : 1, 8), *rr = (double *)xcalloc(n_pt > 0 ? n_pt : 1, 8);
+        double *sb = (double *)xcalloc(n_pt > 0 ? n_pt : 1, 8), *sr = (double *)xcalloc(n_pt > 0 ? n_pt : 1, 8);
+        for (int L = 0; L < in->n_labels; L++) {
+            double *o = &rs[(int64_t)L * N_RS];
+            for (int k = 0; k < N_RS; k++) o[k] = NAN;
+            int64_t n = 0;
+            for (int64_t x = 0; x < n_pt; x++) {
+                const row_t *pr = &pt[x];
+                if (pr->label != L || pr->r_it - 1 < in->warmup || pr->busy <= 0) continue;
+                if (!((in->bd_gpu_mask >> pr->gpu) & 1ull)) continue;
+                b[n] = (double)pr->busy;
+                rr[n] = (double)pr->ovl / (double)pr->busy;
+                n++;
+            }
+            o[0] = (double)n;
+            o[12] = (double)L;
+            if (n == 0) continue;
+            memcpy(sb, b, (size_t)n * 8);
+            memcpy(sr, rr, (size_t)n * 8);
+            qsort(sb, (size_t)n, 8, cmp_f64);
+            qsort(sr, (size_t)n, 8, cmp_f64);
+            const double qs[5] = {0.0, 0.25, 0.5, 0.75, 1.0};
+            for (int k = 0; k < 5; k++) { o[1 + k] = quantile_sorted(sb, n, qs[k]); o[6 + k] = quantile_sorted(sr, n, qs[k]); }
+            /* Pearson: two-pass means, sequential sums in (gpu, iteration) order */
+            double mb = 0.0, mr = 0.0;
+            for (int64_t i = 0; i < n; i++) { mb += b[i]; mr += rr[i]; }
+            mb /= (double)n;
+            mr /= (double)n;
+            double sxx = 0.0, syy = 0.0, sxy = 0.0;
+            for (int64_t i = 0; i < n; i++) {
+                double dx = rr[i] - mr, dy = b[i] - mb;
+                sxx += dx * dx; syy += dy * dy; sxy += dx * dy;
+            }
+            o[11] = (sxx > 0.0 && syy > 0.0) ? sxy / sqrt(sxx * syy) : NAN;
+            o[13] = mb;
+        }
+        free(b); free(rr); free(sb); free(sr);
     }
 
     /* per-event span indices are reported as caller indices (already) */

@@ -98,7 +98,7 @@ _ROW_I64 = ["n_events", "n_compute", "busy", "first_ks", "first_idx", "first_pre
 
 
 class chopper_rows(ctypes.Structure):
-    _fields_ = [("n", I64)] + [(k, P) for k in _ROW_I32] + [(k, P) for k in _ROW_I64] + \
+    _fields_ = [("n", I64), ("stride", I64)] + [(k, P) for k in _ROW_I32] + [(k, P) for k in _ROW_I64] + \
         [("counters", P), ("rates", P), ("wall", P), ("comm_union", P), ("aligned_first", P), ("aligned_last", P),
          ("step", P)]
 
@@ -112,7 +112,8 @@ class chopper_global(ctypes.Structure):
     _fields_ = [("n_iters", I64), ("step", I32 * 4096), ("complete", I32 * 4096), ("sampled", I32 * 4096),
                 ("T", I64 * 4096), ("aligned_first", I64 * 4096), ("aligned_last", I64 * 4096),
                 ("throughput", F64 * 4096), ("throughput_median", F64), ("n_bd", I64), ("bd", F64 * (256 * 16)),
-                ("delta", I64 * 256), ("delta_flag", I32 * 256), ("max_skew_ag", I64), ("max_skew_rs", I64)]
+                ("delta", I64 * 256), ("delta_flag", I32 * 256), ("max_skew_ag", I64), ("max_skew_rs", I64),
+                ("n_report", I64), ("report", F64 * (256 * 16))]
 
 
 class chopper_report(ctypes.Structure):
@@ -293,10 +294,11 @@ def rows_to_numpy(r: chopper_rows, n_counters: int, n_ratios: int = 0) -> Dict[s
         out[k] = dev_to_numpy(getattr(r, k), n, np.int32)
     for k in _ROW_I64:
         out[k] = dev_to_numpy(getattr(r, k), n, np.int64)
-    out["counters"] = np.stack([dev_to_numpy((r.counters or 0) + 8 * s * n if r.counters else None, n, np.float64)
+    st = int(r.stride) if r.stride else n
+    out["counters"] = np.stack([dev_to_numpy((r.counters or 0) + 8 * s * st if r.counters else None, n, np.float64)
                                 for s in range(n_counters)]) if n_counters else np.zeros((0, n))
     if r.rates and n_ratios:
-        out["rates"] = dev_to_numpy(r.rates, n_ratios * n, np.float64).reshape(n_ratios, n)
+        out["rates"] = np.stack([dev_to_numpy(r.rates + 8 * q * st, n, np.float64) for q in range(n_ratios)])
     for k in ("wall", "comm_union", "aligned_first", "aligned_last"):
         if getattr(r, k):
             out[k] = dev_to_numpy(getattr(r, k), n, np.int64)

@@ -101,6 +101,11 @@ __global__ void __launch_bounds__(MR_NT) k_meta_tiles(const uint32_t *__restrict
 }
 // base[c][lg] = global exclusive count of predicate c at the gpu's first event (lg = n_lg -> N);
 // also writes the exchange header (gpu, present, #AG, #RS) of every local gpu
+// non-MEMOP events per local gpu (the length of its counter columns)
+__global__ void k_mg(const int64_t *__restrict__ base, int n_lg, int64_t *__restrict__ mg) {
+    for (int l = threadIdx.x; l < n_lg; l += blockDim.x) mg[l] = base[l + 1] - base[l];
+}
+
 // one warp per (predicate, gpu boundary): tile prefix + the packed counts of the partial tile before it
 __global__ void k_gpu_bases(const uint32_t *__restrict__ meta, int64_t n, const int64_t *__restrict__ tex,
                             int64_t ntile, const int64_t *__restrict__ gbeg, int n_lg, int64_t *__restrict__ base,
@@ -367,6 +372,8 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         // AG / RS collective index (D13) written straight into the exchange block
         const int64_t K = ctx->xW / 4 - 1;
         int64_t ntile = ceil_div(N, MR_TILE);
+        ctx->d_mg = CH_ALLOC(ctx, int64_t, n_lg + 1);
+        CH_ALLOC_END(ctx);
         size_t mark = ctx->used;
         int64_t *tc = CH_ALLOC(ctx, int64_t, 3 * ntile), *tex = CH_ALLOC(ctx, int64_t, 3 * ntile);
         int64_t *base = CH_ALLOC(ctx, int64_t, 3 * (n_lg + 1));
@@ -384,16 +391,8 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
                                                              ctx->d_gpu_lg, tex, ntile, base, n_lg, ctx->d_nm_rank,
                                                              ctx->d_xsend, K, ctx->xW, ctx->d_xovf);
         CH_LAUNCHED(ctx);
-        std::vector<int64_t> hb(3 * (n_lg + 1));
-        CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), base, 8 * hb.size(), cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-        ctx->used = mark;
-        std::vector<int64_t> &m_g = ctx->h_mg;       // kept in ctx: the async copy below reads it
-        m_g.assign(n_lg, 0);
-        for (int l = 0; l < n_lg; l++) m_g[l] = hb[l + 1] - hb[l];
-        ctx->d_mg = CH_ALLOC(ctx, int64_t, n_lg + 1);
-        CH_ALLOC_END(ctx);
-        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_mg, m_g.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+        k_mg<<<1, 256, 0, ctx->st>>>(base, n_lg, ctx->d_mg);
+        CH_LAUNCHED(ctx);
 
         if (n_passes > 0) {
             std::vector<int32_t> off(n_lg + 1, 0), idx;
@@ -413,8 +412,12 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
             k_pass_check<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.name_id, N, ctx->d_gpu_lg,
                                                                         ctx->d_nm_rank, ctx->d_passes, doff, didx, mis);
             CH_LAUNCHED(ctx);
+            // one read-back: the name-sequence divergences and the per-gpu non-MEMOP counts
             std::vector<unsigned long long> hmis(n_passes);
+            std::vector<int64_t> &m_g = ctx->h_mg;
+            m_g.assign(n_lg, 0);
             CH_CUDA(ctx, cudaMemcpyAsync(hmis.data(), mis, 8 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, cudaMemcpyAsync(m_g.data(), ctx->d_mg, 8 * n_lg, cudaMemcpyDeviceToHost, ctx->st));
             CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
             ctx->pass_mismatch.assign(n_passes, -1);
             for (int p = 0; p < n_passes; p++) {
@@ -448,12 +451,10 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
             CH_CUDA(ctx, cudaMemcpyAsync(dpd, pd.data(), sizeof(PassDesc) * n_passes, cudaMemcpyHostToDevice, ctx->st));
             k_pass_finite<<<dim3(148 * 2, n_passes), NT, 0, ctx->st>>>(dpd, ctx->d_pass_bad);
             CH_LAUNCHED(ctx);
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));   // pd goes out of scope
         }
     }
     ctx->counters_out = (counters_out && C > 0 && N > 0) ? counters_out : nullptr;
     CH_TRY(ch_counters_full(ctx));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return CHOPPER_OK;
 }
 
@@ -527,7 +528,6 @@ chopper_status ch_assign_slots(chopper_ctx *ctx) {
         }
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->h_col_dev, hcol.data(), sizeof(double *) * nc, cudaMemcpyHostToDevice, ctx->st));
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_present, ctx->present.data(), 4 * nc, cudaMemcpyHostToDevice, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));   // hcol goes out of scope
     }
     ctx->d_col = ctx->h_col_dev;
     return CHOPPER_OK;

@@ -140,6 +140,7 @@ chopper_status chopper_overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_
 static void fill_rows(chopper_rows &r, const RowTable &t, bool iter, chopper_ctx *ctx) {
     memset(&r, 0, sizeof(r));
     r.n = t.n;
+    r.stride = t.cap;
     r.gpu = t.gpu; r.it = t.it; r.ph = t.ph; r.ly = t.ly; r.op = t.op; r.label = t.label; r.rank = t.rank;
     r.n_events = t.f + (int64_t)RF_NEV * t.cap;
     r.n_compute = t.f + (int64_t)RF_N * t.cap;
@@ -202,7 +203,6 @@ chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, c
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_ratio, r.data(), 4 * r.size(), cudaMemcpyHostToDevice, ctx->st));
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_ratio_scale, p->ratio_scale, 8 * p->n_ratios, cudaMemcpyHostToDevice,
                                      ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     }
     ch_tick(ctx, 5, 0);
     CH_TRY(ch_tables(ctx));

@@ -49,6 +49,7 @@ enum RowField {
 struct RowTable {
     int64_t cap = 0;
     int64_t n = 0;                  // host copy after count read-back
+    int64_t *n_dev = nullptr;       // device count (kernels read it: no host round trip between stages)
     unsigned long long *key = nullptr;
     int64_t *first_event = nullptr;  // for sub-runs; row: first child
     int64_t *f = nullptr;            // [RF_NFIELDS][cap]
@@ -125,6 +126,7 @@ struct chopper_ctx {
     int kb[4] = {0, 0, 0, 0};        // key bits per level
     int kg = 0;                      // key bits for lg
     int64_t max_it_list = 0;         // longest iteration-span list of a local gpu (iteration ranks < this)
+    int64_t n_layer_spans = 0;       // layer spans of the local gpus (fan-out hint for the roll-ups)
 
     // samples
     int64_t *d_smp_phi = nullptr, *d_smp_psi = nullptr;  // prefix integrals at sample k
@@ -154,6 +156,7 @@ struct chopper_ctx {
     int32_t *d_nm_rank = nullptr;    // [N] rank among non-MEMOP events of its gpu
     int64_t *d_mg = nullptr;         // [n_lg] non-MEMOP events per local gpu (counter column length)
     std::vector<int64_t> h_mg;
+    std::vector<int32_t> h_lg_gpu;    // host staging of lg -> gpu (async copies read it)
     int64_t *d_delta = nullptr;      // [n_traced]
     int32_t *d_delta_flag = nullptr;
     std::vector<int64_t> delta;
@@ -200,6 +203,7 @@ struct chopper_ctx {
     cudaEvent_t tev[8][2] = {};
     bool timed[8] = {};
     int64_t *d_dense = nullptr;      // local dense exchange blocks [dense_slots][W]
+    unsigned int *d_dense_ovf = nullptr;
     int dense_slots = 0;
     bool offsets_done = false;
 

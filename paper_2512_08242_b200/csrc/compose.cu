@@ -316,6 +316,100 @@ __global__ void k_bd_compose(BdArgs A, int nb) {
     out[15] = L;
 }
 
+// ---- report statistics per op label (O14) ----------------
+// One block per label over the same points as the breakdown (sampled iterations, busy > 0) in (gpu,
+// iteration) order: duration and overlap-ratio quantiles at q = 0, .25, .5, .75, 1 (linear interpolation at
+// h = q (n - 1), R9) from block bitonic sorts, and the Pearson correlation of ratio with duration (two
+// sequential passes in point order, R10).  Row layout as oracle report.rows.
+struct RepArgs {
+    const int64_t *blk;
+    int nslots;
+    Layout Ly;
+    const int32_t *slot_order;
+    int warmup;
+    int64_t maxp2;
+    double *wk;                  // [L][4][maxp2] global work (when shared memory is too small)
+    double *out;                 // [L][16]
+    int use_smem;
+};
+__device__ __forceinline__ double quantile_sorted_dev(const double *x, int n, double q) {
+    const double h = q * (double)(n - 1);
+    const int lo = (int)floor(h);
+    if (lo >= n - 1) return x[n - 1];
+    const double fr = h - (double)lo;
+    return x[lo] + fr * (x[lo + 1] - x[lo]);
+}
+__global__ void __launch_bounds__(512) k_report(RepArgs A) {
+    extern __shared__ int64_t rsh[];
+    const int L = blockIdx.x;
+    const Layout Ly = A.Ly;
+    double *w = A.use_smem ? reinterpret_cast<double *>(rsh) : A.wk + (int64_t)L * 4 * A.maxp2;
+    double *b = w, *r = w + A.maxp2, *sb = w + 2 * A.maxp2, *sr = w + 3 * A.maxp2;
+    double *out = A.out + (int64_t)L * 16;
+    __shared__ int64_t scan_sm[33];
+    __shared__ int s_count;
+    if (threadIdx.x == 0) s_count = 0;
+    __syncthreads();
+    int nq = 0;
+    while (nq < A.nslots && A.slot_order[nq] >= 0) nq++;
+    const int64_t r0 = A.warmup > 0 ? A.warmup : 0;
+    const int64_t nr = Ly.MI > r0 ? Ly.MI - r0 : 0;
+    const int64_t total = (int64_t)nq * nr;
+    for (int64_t c0 = 0; c0 < total; c0 += blockDim.x) {
+        const int64_t c = c0 + threadIdx.x;
+        bool ok = false;
+        const int64_t *p = nullptr;
+        if (c < total) {
+            const int64_t *bb = A.blk + (int64_t)A.slot_order[c / nr] * Ly.W;
+            p = bb + Ly.pt_off() + ((r0 + c % nr) * Ly.L + L) * PT_W;
+            ok = bb[1] != 0 && p[0] != 0 && p[1] > 0;
+        }
+        int64_t tot;
+        const int64_t pos = block_excl_sum<512>(ok ? 1 : 0, &tot, scan_sm) + s_count;
+        if (ok && pos < A.maxp2) {
+            b[pos] = (double)p[1];
+            r[pos] = (double)p[3] / (double)p[1];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_count += (int)tot;
+        __syncthreads();
+    }
+    const int n = s_count < A.maxp2 ? s_count : (int)A.maxp2;
+    if (threadIdx.x < 16) out[threadIdx.x] = NAN;
+    __syncthreads();
+    if (threadIdx.x == 0) { out[0] = n; out[12] = L; }
+    if (n == 0) return;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) { sb[i] = b[i]; sr[i] = r[i]; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mb = 0.0, mr = 0.0;
+        for (int i = 0; i < n; i++) { mb += b[i]; mr += r[i]; }
+        mb /= (double)n;
+        mr /= (double)n;
+        double sxx = 0.0, syy = 0.0, sxy = 0.0;
+        for (int i = 0; i < n; i++) {
+            const double dx = r[i] - mr, dy = b[i] - mb;
+            sxx += dx * dx;
+            syy += dy * dy;
+            sxy += dx * dy;
+        }
+        out[11] = (sxx > 0.0 && syy > 0.0) ? sxy / sqrt(sxx * syy) : NAN;
+        out[13] = mb;
+    }
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x)
+        if (i >= n) { sb[i] = INFINITY; sr[i] = INFINITY; }
+    __syncthreads();
+    block_bitonic<double>(sb, n2);
+    block_bitonic<double>(sr, n2);
+    if (threadIdx.x < 5) {
+        const double q = 0.25 * threadIdx.x;
+        out[1 + threadIdx.x] = quantile_sorted_dev(sb, n, q);
+        out[6 + threadIdx.x] = quantile_sorted_dev(sr, n, q);
+    }
+}
+
 // global iteration rows (a11): one thread per iteration rank of the reference gpu
 struct GlobArgs {
     const int64_t *blk;
@@ -491,10 +585,7 @@ static chopper_status densify(chopper_ctx *ctx, int64_t **blk_out, int *slots_ou
             ovf);
         CH_LAUNCHED(ctx);
     }
-    unsigned int hovf = 0;
-    CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-    if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "iteration rank >= max_iters or op label >= n_labels");
+    ctx->d_dense_ovf = ovf;     // checked at chopper_reduce_ranks' read-back (no round trip here)
     *blk_out = blk;
     *slots_out = slots;
     return CHOPPER_OK;
@@ -550,27 +641,34 @@ static chopper_status run_breakdown(chopper_ctx *ctx, const int64_t *blk, int ns
     CH_LAUNCHED(ctx);
     k_bd_compose<<<(unsigned)ceil_div(nb, 64), 64, 0, ctx->st>>>(A, nb);
     CH_LAUNCHED(ctx);
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return CHOPPER_OK;
 }
 
 // slot order by gpu id (host, from the exchange headers)
+// slot order by gpu id, on the device: slot b (present) goes to position #{present slots with a smaller
+// (gpu, slot)}; the rest of the order array is -1
+__global__ void k_slot_order(const int64_t *__restrict__ blk, int nslots, int64_t W, int32_t *__restrict__ order) {
+    for (int b = threadIdx.x; b <= nslots; b += blockDim.x) order[b] = -1;
+    __syncthreads();
+    for (int b = threadIdx.x; b < nslots; b += blockDim.x) {
+        const int64_t *x = blk + (int64_t)b * W;
+        if (!x[1]) continue;
+        const int64_t g = x[0];
+        int r = 0;
+        for (int c = 0; c < nslots; c++) {
+            const int64_t *y = blk + (int64_t)c * W;
+            if (y[1] && (y[0] < g || (y[0] == g && c < b))) r++;
+        }
+        order[r] = b;
+    }
+}
+
 static chopper_status slot_order(chopper_ctx *ctx, const int64_t *blk, int nslots, int64_t W, int32_t **out) {
-    // one strided copy of the (gpu, present) header words of every slot
-    std::vector<int64_t> hdr(2 * (size_t)nslots);
-    std::vector<std::pair<int64_t, int>> v;
-    CH_CUDA(ctx, cudaMemcpy2DAsync(hdr.data(), 16, blk, 8 * (size_t)W, 16, nslots, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-    for (int b = 0; b < nslots; b++)
-        if (hdr[2 * b + 1]) v.push_back({hdr[2 * b], b});
-    std::sort(v.begin(), v.end());
-    std::vector<int32_t> o(nslots + 1, -1);
-    for (size_t q = 0; q < v.size(); q++) o[q] = v[q].second;
     CH_ALLOC_BEGIN;
     int32_t *d = CH_ALLOC(ctx, int32_t, nslots + 1);
     CH_ALLOC_END(ctx);
-    CH_CUDA(ctx, cudaMemcpyAsync(d, o.data(), 4 * (nslots + 1), cudaMemcpyHostToDevice, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    k_slot_order<<<1, 256, 0, ctx->st>>>(blk, nslots, W, d);
+    CH_LAUNCHED(ctx);
     *out = d;
     return CHOPPER_OK;
 }
@@ -627,11 +725,35 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     double *bd;
     int64_t nbd;
     CH_TRY(run_breakdown(ctx, all, nslots, ord, &bd, &nbd));
+    // report statistics per op label (O14)
+    const int nL = ctx->cfg.n_labels;
+    double *rep = nullptr;
+    if (nL > 0) {
+        int64_t maxp = (int64_t)Ly.MI * ctx->cfg.n_traced_gpus, maxp2 = 1;
+        while (maxp2 < maxp) maxp2 <<= 1;
+        const size_t shb = (size_t)4 * 8 * maxp2;
+        const bool use_smem = shb <= 96 * 1024;
+        CH_ALLOC_BEGIN;
+        rep = CH_ALLOC(ctx, double, (int64_t)nL * 16);
+        double *wk = use_smem ? nullptr : CH_ALLOC(ctx, double, (int64_t)nL * 4 * maxp2);
+        CH_ALLOC_END(ctx);
+        static bool rattr = false;
+        if (!rattr) {
+            CH_CUDA(ctx, cudaFuncSetAttribute(k_report, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+            rattr = true;
+        }
+        RepArgs RA{all, nslots, Ly, ord, ctx->bd.warmup, maxp2, wk, rep, use_smem ? 1 : 0};
+        k_report<<<nL, 512, use_smem ? shb : 0, ctx->st>>>(RA);
+        CH_LAUNCHED(ctx);
+    }
     // host copies
     int64_t n = 0;
+    unsigned int hovf = 0;
+    if (ctx->d_dense_ovf) CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ctx->d_dense_ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(&n, nref, 8, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     if (n > 4096) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 4096 iterations in chopper_global");
+    if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "iteration rank >= max_iters or op label >= n_labels");
     out->n_iters = n;
     if (n > 0) {
         CH_CUDA(ctx, cudaMemcpyAsync(out->step, step, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
@@ -646,6 +768,9 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     if (nbd > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 breakdown rows");
     out->n_bd = nbd;
     if (nbd > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->bd, bd, 8 * 16 * nbd, cudaMemcpyDeviceToHost, ctx->st));
+    if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels in the report rows");
+    out->n_report = nL;
+    if (nL > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->report, rep, 8 * 16 * (size_t)nL, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     for (int g = 0; g < ctx->cfg.n_traced_gpus && g < 256; g++) {
         out->delta[g] = ctx->delta[g];

@@ -928,7 +928,6 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
         k_union_block<<<n_lg, 1024, 0, ctx->st>>>(ctx->d_vperm, vlo, vhi, ctx->ev.start_ns, ctx->ev.end_ns, ctx->V_s,
                                                   ctx->V_e, ctx->V_P, ctx->d_V_beg, ctx->d_V_cnt);
         CH_LAUNCHED(ctx);
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));   // host vectors a/b go out of scope
     }
     // sample prefix integrals (D10)
     ctx->smp_lo.assign(n_lg, 0);
@@ -965,7 +964,6 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
         std::vector<int32_t> hs(n_lg + 1, 0);
         for (int l = 0; l < n_lg; l++) hs[l] = ctx->smp_hi[l] > ctx->smp_lo[l] ? 1 : 0;
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_has_smp, hs.data(), 4 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     }
     return CHOPPER_OK;
 }
@@ -1036,7 +1034,6 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     // sentinel: sub-run R begins at N
     int64_t nv = N;
     CH_CUDA(ctx, cudaMemcpyAsync(ctx->sub.first_event + ctx->R, &nv, 8, cudaMemcpyHostToDevice, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     return CHOPPER_OK;
 }
 

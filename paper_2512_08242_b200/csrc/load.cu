@@ -367,7 +367,6 @@ chopper_status ch_load(chopper_ctx *ctx) {
         k_seg_scatter<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(alt ? v2 : v1, dlo, dpre, nseg, Mseg,
                                                                         ctx->d_perm);
         CH_LAUNCHED(ctx);
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));   // host vectors above go out of scope
         ctx->used = mk;
         ctx->full_sort = true;
         if (compute_resorted) {

@@ -317,8 +317,22 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         CH_CUDA(ctx, cudaMemsetAsync(big, 0, 4, ctx->st));
         k_fix_ties<<<g, NT, 0, ctx->st>>>(okeys, order, ctx->sp.end_ns, S, (unsigned long long)n_lists << rbits, big);
         CH_LAUNCHED(ctx);
+        // gather speculatively (long equal-start runs are rare); one read-back for the flag and the list begins
+        unsigned long long *lb2 = CH_ALLOC(ctx, unsigned long long, n_lists + 1);
+        CH_ALLOC_END(ctx);
+        auto gather = [&](const uint32_t *ord) -> chopper_status {
+            CH_TRY(ch_fill_u64(ctx, lb2, n_lists + 1, ~0ull));
+            k_span_gather<<<g, NT, 0, ctx->st>>>(ord, ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns,
+                                                 ctx->sp.label, S, ctx->d_gpu_lg, n_lg, ctx->P_start, ctx->P_end,
+                                                 ctx->P_orig, ctx->P_label, Plist, lb2);
+            CH_LAUNCHED(ctx);
+            return CHOPPER_OK;
+        };
+        CH_TRY(gather(order));
+        std::vector<unsigned long long> hb(n_lists + 1);
         unsigned int hbig = 0;
         CH_CUDA(ctx, cudaMemcpyAsync(&hbig, big, 4, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), lb2, 8 * (n_lists + 1), cudaMemcpyDeviceToHost, ctx->st));
         CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
         if (hbig) {
             // very long runs of equal starts: exact two-sort path (end desc, then (list, start) stable)
@@ -333,15 +347,10 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
             CH_LAUNCHED(ctx);
             CH_TRY(ch_radix_sort(ctx, ks, vs, ko, vo, S, 0, rbits + lbits, &alt));
             order = alt ? vo : vs;
+            CH_TRY(gather(order));
+            CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), lb2, 8 * (n_lists + 1), cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
         }
-        CH_TRY(ch_fill_u64(ctx, lb, n_lists + 1, ~0ull));
-        k_span_gather<<<g, NT, 0, ctx->st>>>(order, ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, ctx->sp.label,
-                                             S, ctx->d_gpu_lg, n_lg, ctx->P_start, ctx->P_end, ctx->P_orig,
-                                             ctx->P_label, Plist, lb);
-        CH_LAUNCHED(ctx);
-        std::vector<unsigned long long> hb(n_lists + 1);
-        CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), lb, 8 * (n_lists + 1), cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
         ctx->used = mark;
         ctx->list_beg[n_lists + 1] = S;
         for (int l = n_lists; l >= 0; l--) ctx->list_beg[l] = hb[l] == ~0ull ? ctx->list_beg[l + 1] : (int64_t)hb[l];
@@ -354,6 +363,9 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
     for (int l = 0; l < n_lists; l++) mx[l % 4] = std::max(mx[l % 4], ctx->list_beg[l + 1] - ctx->list_beg[l]);
     ctx->kg = bits_for((uint64_t)n_lg);
     ctx->max_it_list = mx[0];
+    ctx->n_layer_spans = 0;
+    for (int l = 0; l < n_lists; l++)
+        if (l % 4 == 2) ctx->n_layer_spans += ctx->list_beg[l + 1] - ctx->list_beg[l];
     int tot = ctx->kg;
     for (int lv = 0; lv < 4; lv++) { ctx->kb[lv] = bits_for((uint64_t)mx[lv] + 1); tot += ctx->kb[lv]; }
     if (tot > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "instance key exceeds 64 bits");

@@ -14,177 +14,163 @@
 namespace {
 constexpr int NT = 256;
 
-// counter sums of each sub-run over its COMPUTE events, CT_SG slots per launch.  A block stages its
-// 2048-event tile in shared memory with cp.async -- meta, sub-run ids, pass positions, and for each slot
-// the tile's contiguous range of the counter column (events of one gpu take consecutive pass positions,
-// D2) -- so every global read is a bulk asynchronous copy.  Lane = event: warp w walks events
-// [256w, 256w + 256) 32 at a time; sums within a warp come from a segmented warp scan keyed by the
-// sub-run id, and a run still open at the end of a warp is finished by thread 0 from the per-warp edge
-// pieces (sub-runs never cross tiles).  Every value read -- the slot's column at every non-MEMOP event,
-// i.e. the whole column -- is checked for finiteness (R8), so a counter pass is read once.
-constexpr int CT_NT = 256, CT_TILE = 2048, CT_SG = 4, CT_WARPS = CT_NT / 32, CT_WEV = CT_TILE / CT_WARPS;
-struct CtSmem {
-    uint32_t meta[CT_TILE];
-    int32_t rid[CT_TILE];
-    int32_t nm[CT_TILE];
-    double val[CT_SG][CT_TILE];
-    double lead[CT_WARPS][CT_SG], tail[CT_WARPS][CT_SG];
-    int32_t tail_id[CT_WARPS], has[CT_WARPS];
-};
-__device__ __forceinline__ void ct_cp16(void *smem, const void *g) {
-    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(g));
-}
-__device__ __forceinline__ void ct_cp8(void *smem, const void *g) {
-    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g));
-}
-__global__ void __launch_bounds__(CT_NT, 2) k_counters_tiled(const uint32_t *__restrict__ meta,
-                                                             const int32_t *__restrict__ run_id,
-                                                             const int32_t *__restrict__ nm_rank,
-                                                             const int32_t *__restrict__ gpu_lg,
-                                                             const double *const *__restrict__ col, int C, int s0,
-                                                             int64_t N, double *__restrict__ out, int64_t cap,
-                                                             unsigned int *__restrict__ colbad,
-                                                             const int64_t *__restrict__ mg, int vec_ok) {
-    extern __shared__ __align__(16) unsigned char ct_dsm[];
-    CtSmem &S = *reinterpret_cast<CtSmem *>(ct_dsm);
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int64_t base = (int64_t)blockIdx.x * CT_TILE;
-    const int nt = (int)min((int64_t)CT_TILE, N - base);
-    const int ns = min(CT_SG, C - s0);
-    // ---- stage the tile ----
-    if (vec_ok && nt == CT_TILE) {
-        for (int u = tid; u < CT_TILE / 4; u += CT_NT) {
-            ct_cp16(&S.meta[4 * u], meta + base + 4 * u);
-            ct_cp16(&S.rid[4 * u], run_id + base + 4 * u);
-            ct_cp16(&S.nm[4 * u], nm_rank + base + 4 * u);
+// counter sums of each sub-run over its COMPUTE events, tiled like the event pass (2048 events per
+// block, 8 consecutive per thread; sub-runs never cross tiles), CT_SG slots per launch.  Each thread
+// folds its 8 events sequentially (input order); runs that span threads are completed by a segmented
+// scan of (has-head, tail-or-whole) over the tile (warp shuffles + warp carries).  The pass also checks
+// every value it reads -- the slot's column at every non-MEMOP event of the gpu, i.e. the whole column
+// -- for finiteness (R8), so a counter pass is read once.
+constexpr int CT_NT = 256, CT_IPT = 8, CT_TILE = CT_NT * CT_IPT, CT_SG = 8, CT_WARPS = CT_NT / 32;
+__global__ void __launch_bounds__(CT_NT) k_counters_tiled(const uint32_t *__restrict__ meta,
+                                                          const int32_t *__restrict__ run_id,
+                                                          const int32_t *__restrict__ nm_rank,
+                                                          const int32_t *__restrict__ gpu_lg,
+                                                          const double *const *__restrict__ col, int C, int s0,
+                                                          int64_t N, double *__restrict__ out, int64_t cap,
+                                                          unsigned int *__restrict__ colbad, int vec_ok) {
+    __shared__ double s_agg[CT_WARPS][CT_SG], s_carry[CT_WARPS][CT_SG];
+    __shared__ int s_aflag[CT_WARPS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * CT_TILE, i0 = base + (int64_t)tid * CT_IPT;
+    const int nv = i0 >= N ? 0 : (int)min((int64_t)CT_IPT, N - i0);
+    uint32_t mt[CT_IPT];
+    int32_t rid[CT_IPT], nm[CT_IPT];
+    if (vec_ok && nv == CT_IPT) {
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            uint4 a = reinterpret_cast<const uint4 *>(meta + i0)[h];
+            int4 b = reinterpret_cast<const int4 *>(run_id + i0)[h];
+            int4 c = reinterpret_cast<const int4 *>(nm_rank + i0)[h];
+            mt[4 * h] = a.x; mt[4 * h + 1] = a.y; mt[4 * h + 2] = a.z; mt[4 * h + 3] = a.w;
+            rid[4 * h] = b.x; rid[4 * h + 1] = b.y; rid[4 * h + 2] = b.z; rid[4 * h + 3] = b.w;
+            nm[4 * h] = c.x; nm[4 * h + 1] = c.y; nm[4 * h + 2] = c.z; nm[4 * h + 3] = c.w;
         }
     } else {
-        for (int e = tid; e < CT_TILE; e += CT_NT) {
-            const bool ok = e < nt;
-            S.meta[e] = ok ? meta[base + e] : (uint32_t)CK_MEMOP;
-            S.rid[e] = ok ? run_id[base + e] : -2;
-            S.nm[e] = ok ? nm_rank[base + e] : 0;
+#pragma unroll
+        for (int k = 0; k < CT_IPT; k++) {
+            bool ok = k < nv;
+            mt[k] = ok ? meta[i0 + k] : (uint32_t)CK_MEMOP;
+            rid[k] = ok ? run_id[i0 + k] : -1;
+            nm[k] = ok ? nm_rank[i0 + k] : 0;
         }
     }
-    // one gpu in the tile (events are grouped by gpu): its pass positions form one contiguous range
-    const int lg_a = gpu_lg[gpu_of(meta[base])], lg_b = gpu_lg[gpu_of(meta[base + nt - 1])];
-    const bool single = lg_a == lg_b;
-    int64_t nm_lo = 0;
-    int cnt = 0;
-    if (single) {
-        nm_lo = nm_rank[base];
-        cnt = (int)min((int64_t)CT_TILE, mg[lg_a] - nm_lo);
-        for (int q = 0; q < ns; q++) {
-            const double *c = col[lg_a * C + s0 + q];
-            if (!c) continue;
-            for (int k = tid; k < cnt; k += CT_NT) ct_cp8(&S.val[q][k], c + nm_lo + k);
+    const int32_t prev = (tid > 0 && nv > 0) ? run_id[i0 - 1] : -1;
+    unsigned hmask = 0;
+#pragma unroll
+    for (int k = 0; k < CT_IPT; k++)
+        if (k < nv && (k == 0 ? (tid == 0 || rid[0] != prev) : rid[k] != rid[k - 1])) hmask |= 1u << k;
+    const bool has = hmask != 0;
+    // all counter values of the thread first (independent loads in flight), then the folds
+    double x[CT_SG][CT_IPT];
+    int lgp = -1;
+    const double *cp[CT_SG];
+#pragma unroll
+    for (int q = 0; q < CT_SG; q++) cp[q] = nullptr;
+#pragma unroll
+    for (int k = 0; k < CT_IPT; k++) {
+        const uint32_t m = mt[k];
+        const bool rd = k < nv && kind_of(m) != CK_MEMOP;
+        const int lg = rd ? gpu_lg[gpu_of(m)] : lgp;
+        if (rd && lg != lgp) {
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++) cp[q] = s0 + q < C ? col[lg * C + s0 + q] : nullptr;
+            lgp = lg;
         }
+#pragma unroll
+        for (int q = 0; q < CT_SG; q++) x[q][k] = (rd && cp[q]) ? __ldg(cp[q] + nm[k]) : 0.0;
     }
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    if (lane < CT_SG) { S.lead[w][lane] = 0.0; }
-    __syncthreads();
-    // ---- per warp: 8 batches of 32 events ----
-    const int e0 = w * CT_WEV;
-    const int nv_w = max(0, min(CT_WEV, nt - e0));
-    double carry[CT_SG];
+    double cur[CT_SG], p0[CT_SG];
 #pragma unroll
-    for (int q = 0; q < CT_SG; q++) carry[q] = 0.0;
-    bool open = e0 > 0 && nv_w > 0, open_here = false, seen_head = false;
-    int32_t open_id = (e0 > 0 && nv_w > 0) ? S.rid[e0 - 1] : -1;
-    for (int b = 0; b < CT_WEV / 32; b++) {
-        const int e = e0 + b * 32 + lane;
-        const bool valid = b * 32 + lane < nv_w;
-        const unsigned vm = __ballot_sync(CH_FULL, valid);
-        if (vm == 0) break;
-        const uint32_t m = S.meta[e];
-        const int32_t rid = valid ? S.rid[e] : -2;
-        const int32_t nm = S.nm[e];
-        const bool head = valid && (e == 0 || rid != S.rid[e - 1]);
-        const int kd = kind_of(m);
-        const bool rd = valid && kd != CK_MEMOP;
-        double v[CT_SG];
-        const int lg = rd ? gpu_lg[gpu_of(m)] : -1;
+    for (int q = 0; q < CT_SG; q++) {
+        cur[q] = 0.0;
+        p0[q] = 0.0;
+        const int s = s0 + q;
+        if (s >= C) continue;
+        double c = 0.0;
+        bool seen = false, bad = false;
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++) {
-            v[q] = 0.0;
-            if (q < ns && rd) {
-                const double *c = col[lg * C + s0 + q];
-                if (c) {
-                    const double x = (single && nm - nm_lo < cnt) ? S.val[q][nm - nm_lo] : __ldg(c + nm);
-                    if (!isfinite(x)) atomicOr(&colbad[lg * C + s0 + q], 1u);
-                    if (kd == CK_COMPUTE) v[q] = x;
-                }
+        for (int k = 0; k < CT_IPT; k++) {
+            if ((hmask >> k) & 1u) {          // (heads only at valid events)
+                if (!seen) { p0[q] = c; seen = true; }
+                else out[(int64_t)s * cap + rid[k > 0 ? k - 1 : 0]] = c;
+                c = 0.0;
+            }
+            const int kd = kind_of(mt[k]);    // (invalid events carry MEMOP)
+            if (kd != CK_MEMOP) {
+                bad |= !isfinite(x[q][k]);
+                if (kd == CK_COMPUTE) c += x[q][k];
             }
         }
-        const unsigned hm = __ballot_sync(CH_FULL, head);
-        bool f = head;
+        if (bad) {
+#pragma unroll
+            for (int k = 0; k < CT_IPT; k++)
+                if (kind_of(mt[k]) != CK_MEMOP && !isfinite(x[q][k])) atomicOr(&colbad[gpu_lg[gpu_of(mt[k])] * C + s], 1u);
+        }
+        cur[q] = c;
+    }
+    // segmented inclusive scan of (has, cur) inside the warp
+    bool f = has;
+    double v[CT_SG];
+#pragma unroll
+    for (int q = 0; q < CT_SG; q++) v[q] = cur[q];
+    if (!__all_sync(CH_FULL, has)) {
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const bool pf = __shfl_up_sync(CH_FULL, f, o);
+            bool pf = __shfl_up_sync(CH_FULL, f, o);
 #pragma unroll
             for (int q = 0; q < CT_SG; q++) {
-                const double pv = __shfl_up_sync(CH_FULL, v[q], o);
+                double pv = __shfl_up_sync(CH_FULL, v[q], o);
                 if (lane >= o && !f) v[q] = pv + v[q];
             }
             if (lane >= o) f = f || pf;
         }
-        const int last_valid = 31 - __clz(vm);
-        const int first_head = hm ? __ffs(hm) - 1 : 32;
-        if (lane < first_head) {
-#pragma unroll
-            for (int q = 0; q < CT_SG; q++) v[q] = carry[q] + v[q];
-        }
-        // 1) the open run ends before first_head (or at the last valid event)
-        if (open && (first_head < 32 || last_valid < 31)) {
-            const int endl = min(first_head, last_valid + 1) - 1;
-            if (lane == (endl >= 0 ? endl : 0)) {
-                for (int q = 0; q < ns; q++) {
-                    const double t = endl >= 0 ? v[q] : carry[q];
-                    if (open_here) out[(int64_t)(s0 + q) * cap + open_id] = t;
-                    else S.lead[w][q] = t;
-                }
-            }
-            open = false;
-        }
-        // 2) runs starting in this batch that end inside it
-        const bool nxt_head = lane < 31 && ((hm >> (lane + 1)) & 1u);
-        if (valid && lane >= first_head && (nxt_head || (lane == last_valid && last_valid < 31)))
-            for (int q = 0; q < ns; q++) out[(int64_t)(s0 + q) * cap + rid] = v[q];
-        // 3) the run open at lane 31
-        if (last_valid == 31) {
-            if (hm) { open_here = true; open_id = __shfl_sync(CH_FULL, rid, 31); }
-#pragma unroll
-            for (int q = 0; q < CT_SG; q++) carry[q] = __shfl_sync(CH_FULL, v[q], 31);
-            open = true;
-        }
-        seen_head = seen_head || hm != 0;
-        if (last_valid < 31) break;
     }
-    if (lane == 0) {
-        S.has[w] = seen_head;
-        S.tail_id[w] = open ? open_id : -1;
+    if (lane == 31) {
+        s_aflag[warp] = f;
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++) S.tail[w][q] = open ? carry[q] : 0.0;
+        for (int q = 0; q < CT_SG; q++) s_agg[warp][q] = v[q];
     }
     __syncthreads();
-    if (tid == 0) {
-        for (int wa = 0; wa < CT_WARPS; wa++) {
-            if (S.tail_id[wa] < 0 || !S.has[wa]) continue;
-            const int32_t id = S.tail_id[wa];
-            double acc[CT_SG];
-            for (int q = 0; q < ns; q++) acc[q] = S.tail[wa][q];
-            for (int wb = wa + 1; wb < CT_WARPS; wb++) {
-                if (S.has[wb] || S.tail_id[wb] != id) {
-                    for (int q = 0; q < ns; q++) acc[q] += S.lead[wb][q];
-                    break;
-                }
-                for (int q = 0; q < ns; q++) acc[q] += S.tail[wb][q];
-            }
-            for (int q = 0; q < ns; q++) out[(int64_t)(s0 + q) * cap + id] = acc[q];
+    if (tid < CT_WARPS) {
+        double c[CT_SG];
+        int cf = 0;
+#pragma unroll
+        for (int q = 0; q < CT_SG; q++) c[q] = 0.0;
+        for (int w = 0; w < tid; w++) {
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++) c[q] = s_aflag[w] ? s_agg[w][q] : c[q] + s_agg[w][q];
+            cf |= s_aflag[w];
         }
+#pragma unroll
+        for (int q = 0; q < CT_SG; q++) s_carry[tid][q] = c[q];
+    }
+    __syncthreads();
+    bool ef = __shfl_up_sync(CH_FULL, f, 1);
+    double e[CT_SG];
+#pragma unroll
+    for (int q = 0; q < CT_SG; q++) e[q] = __shfl_up_sync(CH_FULL, v[q], 1);
+    if (lane == 0) {
+        ef = false;
+#pragma unroll
+        for (int q = 0; q < CT_SG; q++) e[q] = 0.0;
+    }
+    if (!ef) {
+#pragma unroll
+        for (int q = 0; q < CT_SG; q++) e[q] = s_carry[warp][q] + e[q];
+    }
+    // the run ending in this thread's first piece (or at the end of the previous thread)
+    if (has && tid > 0) {
+#pragma unroll
+        for (int q = 0; q < CT_SG; q++)
+            if (s0 + q < C) out[(int64_t)(s0 + q) * cap + prev] = e[q] + p0[q];
+    }
+    // the run open at the end of the tile
+    if (tid == CT_NT - 1 && base < N) {
+        const int64_t last = base + CT_TILE - 1 < N ? base + CT_TILE - 1 : N - 1;
+        const int32_t id = run_id[last];
+#pragma unroll
+        for (int q = 0; q < CT_SG; q++)
+            if (s0 + q < C) out[(int64_t)(s0 + q) * cap + id] = f ? v[q] : s_carry[warp][q] + v[q];
     }
 }
 
@@ -209,10 +195,12 @@ __global__ void k_prefix_heads(const unsigned long long *__restrict__ key, int64
     head[j] = (j == 0 || (key[j] >> sh) != (key[j - 1] >> sh)) ? 1 : 0;
 }
 // valid segments must have strictly increasing prefixes; invalid keys (all ones) form their own segments
-__global__ void k_prefix_check(const unsigned long long *__restrict__ key, const int64_t *__restrict__ starts,
-                               int64_t nseg, int sh, unsigned int *__restrict__ bad) {
-    int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= nseg) return;
+__global__ void k_seg_starts_end(int64_t *__restrict__ starts, const int64_t *__restrict__ nseg, int64_t n) {
+    starts[*nseg] = n;
+}
+__device__ __forceinline__ void prefix_check_one(const unsigned long long *__restrict__ key,
+                                                 const int64_t *__restrict__ starts, int64_t s, int sh,
+                                                 unsigned int *__restrict__ bad) {
     const unsigned long long inv = CH_INVALID_KEY >> sh;
     const unsigned long long p = key[starts[s]] >> sh;
     if (starts[s + 1] - starts[s] > SS_MAX) atomicOr(bad, 2u);
@@ -223,6 +211,12 @@ __global__ void k_prefix_check(const unsigned long long *__restrict__ key, const
         if (q >= p) atomicOr(bad, 1u);
         break;
     }
+}
+__global__ void k_prefix_check(const unsigned long long *__restrict__ key, const int64_t *__restrict__ starts,
+                               const int64_t *__restrict__ nseg_d, int sh, unsigned int *__restrict__ bad) {
+    const int64_t nseg = *nseg_d;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < nseg; s += (int64_t)gridDim.x * blockDim.x)
+        prefix_check_one(key, starts, s, sh, bad);
 }
 // Inside an iteration the sub-run keys split into four classes by how many trailing levels are "none"
 // (op > 0; op = 0 < layer; layer = op = 0 < phase; phase = layer = op = 0).  In dispatch order each class
@@ -236,22 +230,30 @@ struct SegSortSmem {
     uint32_t v[SS_MAX];
     unsigned long long ck[SS_MAX];      // class-partitioned keys
     uint32_t cv[SS_MAX];
-    int cbeg[5];
+    int cbeg[9];
     int unsorted;
     int64_t scan[33];
 };
 __device__ __forceinline__ int seg_class(unsigned long long k, const KeyLayout &L) {
-    if (k == CH_INVALID_KEY) return 3;
-    if (comp(k, L.sh_op, L.kb[3]) > 0) return 0;
-    if (comp(k, L.sh_ly, L.kb[2]) > 0) return 1;
-    if (comp(k, L.sh_ph, L.kb[1]) > 0) return 2;
-    return 3;
+    if (k == CH_INVALID_KEY) return 7;
+    return (comp(k, L.sh_op, L.kb[3]) == 0 ? 1 : 0) | (comp(k, L.sh_ly, L.kb[2]) == 0 ? 2 : 0) |
+           (comp(k, L.sh_ph, L.kb[1]) == 0 ? 4 : 0);
 }
+__device__ void seg_sort_one(SegSortSmem &S, unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
+                             int64_t lo, int64_t hi, const KeyLayout &L);
 __global__ void __launch_bounds__(SS_NT) k_seg_sort(unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
-                                                    const int64_t *__restrict__ starts, int64_t nseg, KeyLayout L) {
+                                                    const int64_t *__restrict__ starts, const int64_t *__restrict__ nseg_d,
+                                                    KeyLayout L) {
     extern __shared__ __align__(16) unsigned char ss_dsm[];
     SegSortSmem &S = *reinterpret_cast<SegSortSmem *>(ss_dsm);
-    const int64_t lo = starts[blockIdx.x], hi = starts[blockIdx.x + 1];
+    const int64_t nseg = *nseg_d;
+    for (int64_t sg = blockIdx.x; sg < nseg; sg += gridDim.x) {
+        seg_sort_one(S, keys, vals, starts[sg], starts[sg + 1], L);
+        __syncthreads();
+    }
+}
+__device__ void seg_sort_one(SegSortSmem &S, unsigned long long *__restrict__ keys, uint32_t *__restrict__ vals,
+                             int64_t lo, int64_t hi, const KeyLayout &L) {
     const int n = (int)(hi - lo);
     if (n <= 1 || n > SS_MAX) return;
     bool sorted = true;   // fast exit for an already ordered segment
@@ -261,23 +263,30 @@ __global__ void __launch_bounds__(SS_NT) k_seg_sort(unsigned long long *__restri
     for (int i = threadIdx.x; i < n; i += blockDim.x) { S.k[i] = keys[lo + i]; S.v[i] = vals[lo + i]; }
     if (threadIdx.x == 0) { S.unsorted = 0; S.cbeg[0] = 0; }
     __syncthreads();
-    // stable partition by class: per-thread chunk counts, one packed block scan (4 x 16-bit counters)
+    // stable partition by class: per-thread chunk counts, two packed block scans (4 x 16-bit counters)
     const int per = (n + SS_NT - 1) / SS_NT;
     const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
-    unsigned long long cnt = 0;
-    for (int i = i0; i < i1; i++) cnt += 1ull << (16 * seg_class(S.k[i], L));
-    int64_t tot;
-    unsigned long long ex = (unsigned long long)block_excl_sum<SS_NT>((int64_t)cnt, &tot, S.scan);
-    const unsigned long long t64 = (unsigned long long)tot;
-    int cb[4];
-    cb[0] = 0;
-    cb[1] = (int)(t64 & 0xFFFF);
-    cb[2] = cb[1] + (int)((t64 >> 16) & 0xFFFF);
-    cb[3] = cb[2] + (int)((t64 >> 32) & 0xFFFF);
-    if (threadIdx.x == 0) { S.cbeg[1] = cb[1]; S.cbeg[2] = cb[2]; S.cbeg[3] = cb[3]; S.cbeg[4] = n; }
-    int pos[4];
-#pragma unroll
-    for (int c = 0; c < 4; c++) pos[c] = cb[c] + (int)((ex >> (16 * c)) & 0xFFFF);
+    unsigned long long cnt[2] = {0, 0};
+    for (int i = i0; i < i1; i++) {
+        const int c = seg_class(S.k[i], L);
+        cnt[c >> 2] += 1ull << (16 * (c & 3));
+    }
+    int cb[8], pos[8];
+    int run = 0;
+    for (int h = 0; h < 2; h++) {
+        int64_t tot;
+        const unsigned long long ex = (unsigned long long)block_excl_sum<SS_NT>((int64_t)cnt[h], &tot, S.scan);
+        const unsigned long long t64 = (unsigned long long)tot;
+        for (int c = 0; c < 4; c++) {
+            cb[4 * h + c] = run;
+            pos[4 * h + c] = run + (int)((ex >> (16 * c)) & 0xFFFF);
+            run += (int)((t64 >> (16 * c)) & 0xFFFF);
+        }
+    }
+    if (threadIdx.x == 0) {
+        for (int c = 0; c < 8; c++) S.cbeg[c] = cb[c];
+        S.cbeg[8] = n;
+    }
     for (int i = i0; i < i1; i++) {
         const int c = seg_class(S.k[i], L);
         const int d = pos[c]++;
@@ -286,7 +295,7 @@ __global__ void __launch_bounds__(SS_NT) k_seg_sort(unsigned long long *__restri
     }
     __syncthreads();
     // every class ascending?
-    for (int c = 0; c < 4; c++)
+    for (int c = 0; c < 8; c++)
         for (int d = S.cbeg[c] + 1 + threadIdx.x; d < S.cbeg[c + 1]; d += blockDim.x)
             if (S.ck[d] < S.ck[d - 1]) S.unsorted = 1;
     __syncthreads();
@@ -296,8 +305,8 @@ __global__ void __launch_bounds__(SS_NT) k_seg_sort(unsigned long long *__restri
             while (d >= S.cbeg[c + 1]) c++;
             const unsigned long long x = S.ck[d];
             int p = d - S.cbeg[c];
-            for (int o = 0; o < 4; o++) {
-                if (o == c) continue;
+            for (int o = 0; o < 8; o++) {
+                if (o == c || S.cbeg[o] == S.cbeg[o + 1]) continue;
                 int l2 = S.cbeg[o], h2 = S.cbeg[o + 1];     // count of class-o keys < x
                 while (l2 < h2) {
                     const int m = (l2 + h2) >> 1;
@@ -358,10 +367,25 @@ __global__ void k_copy_keys(const unsigned long long *__restrict__ k, int64_t n,
 }
 
 // heads of groups of equal (key >> shift) among valid keys; also the valid count
-__global__ void k_group_heads(const unsigned long long *__restrict__ key, int64_t n, int shift,
-                              int64_t *__restrict__ head, unsigned long long *__restrict__ nvalid) {
+// device-resident row counts: kernels are sized by a host upper bound and read the true count
+__device__ __forceinline__ int64_t dev_n(int64_t n, const int64_t *n_dev) {
+    if (!n_dev) return n;
+    const int64_t m = *n_dev;
+    return m < n ? m : n;
+}
+__global__ void k_group_init(unsigned long long *nvalid, int64_t n, const int64_t *__restrict__ n_dev) {
+    *nvalid = (unsigned long long)dev_n(n, n_dev);
+}
+// the end of the last group: the first invalid key (invalid keys sort last)
+__global__ void k_group_finish(int64_t *__restrict__ starts, const int64_t *__restrict__ ng,
+                               const unsigned long long *__restrict__ nvalid) {
+    starts[*ng] = (int64_t)*nvalid;
+}
+__global__ void k_group_heads(const unsigned long long *__restrict__ key, int64_t n, const int64_t *__restrict__ n_dev,
+                              int shift, int64_t *__restrict__ head, unsigned long long *__restrict__ nvalid) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
+    if (j >= dev_n(n, n_dev)) { head[j] = 0; return; }
     unsigned long long k = key[j];
     bool valid = k != CH_INVALID_KEY;
     if (!valid) { head[j] = 0; atomicMin(nvalid, (unsigned long long)j); return; }
@@ -428,11 +452,10 @@ struct RowAcc {
     }
 };
 
-__global__ void __launch_bounds__(256) k_sum_rows(TabView ch, const uint32_t *__restrict__ perm,
-                                                  const int64_t *__restrict__ starts, int64_t ng, int shift, int C,
-                                                  TabView pa) {
+__device__ __forceinline__ void sum_rows_thread_body(const TabView &ch, const uint32_t *__restrict__ perm,
+                                                     const int64_t *__restrict__ starts, int64_t ng, int shift, int C,
+                                                     const TabView &pa, int64_t p) {
     const int lane = lane_id();
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = p < ng;
     int64_t lo = 0, hi = 0;
     if (valid) { lo = starts[p]; hi = starts[p + 1]; }
@@ -482,15 +505,25 @@ __global__ void __launch_bounds__(256) k_sum_rows(TabView ch, const uint32_t *__
     }
 }
 
+__global__ void __launch_bounds__(256) k_sum_rows(TabView ch, const uint32_t *__restrict__ perm,
+                                                  const int64_t *__restrict__ starts, const int64_t *__restrict__ ng_dev,
+                                                  int shift, int C, TabView pa) {
+    const int64_t ng = *ng_dev;
+    for (int64_t pb = (int64_t)blockIdx.x * blockDim.x; pb < ng; pb += (int64_t)gridDim.x * blockDim.x)
+        sum_rows_thread_body(ch, perm, starts, ng, shift, C, pa, pb + threadIdx.x);
+}
+
 // warp per parent (groups averaging several children: layer / phase / iteration / gpu roll-ups and
 // points): lanes take consecutive children (coalesced on field-major tables), every field and counter
 // in one pass, then a butterfly.
 __global__ void __launch_bounds__(256) k_sum_rows_warp(TabView ch, const uint32_t *__restrict__ perm,
-                                                       const int64_t *__restrict__ starts, int64_t ng, int shift,
-                                                       int C, TabView pa) {
+                                                       const int64_t *__restrict__ starts,
+                                                       const int64_t *__restrict__ ng_dev, int shift, int C,
+                                                       TabView pa) {
     const int lane = lane_id();
-    const int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (q >= ng) return;
+    const int64_t ng = *ng_dev;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < ng; q += nw) {
     const int64_t qlo = starts[q], qhi = starts[q + 1];
     RowAcc a;
     a.zero();
@@ -525,6 +558,7 @@ __global__ void __launch_bounds__(256) k_sum_rows_warp(TabView ch, const uint32_
             if (lane == 0) pa.cnt[(int64_t)s * pa.ccap + q] = x;
         }
     }
+    }
 }
 
 // block of RC_NT parents: their children (a contiguous range, or a perm range) are staged RC_CH at a time
@@ -532,15 +566,18 @@ __global__ void __launch_bounds__(256) k_sum_rows_warp(TabView ch, const uint32_
 // AoS sub-run rows -- and each thread folds its own parent's children from shared memory in order.
 constexpr int RC_NT = 256, RC_CH = 256;
 __global__ void __launch_bounds__(RC_NT) k_sum_rows_chunked(TabView ch, const uint32_t *__restrict__ perm,
-                                                            const int64_t *__restrict__ starts, int64_t ng, int shift,
-                                                            int C, TabView pa) {
+                                                            const int64_t *__restrict__ starts,
+                                                            const int64_t *__restrict__ ng_dev, int shift, int C,
+                                                            TabView pa, int PB) {
+    // PB parents per block (<= RC_NT): about RC_CH children per block-iteration keeps the loads wide
     extern __shared__ int64_t rsm[];
     const int NF = RF_NFIELDS + C;
     int64_t *vals = rsm;                               // [NF][RC_CH]
     const int tid = threadIdx.x;
-    const int64_t p0 = (int64_t)blockIdx.x * RC_NT;
-    const int64_t pend = min(p0 + RC_NT, ng);
-    const int64_t p = p0 + tid;
+    const int64_t ng = *ng_dev;
+    for (int64_t p0 = (int64_t)blockIdx.x * PB; p0 < ng; p0 += (int64_t)gridDim.x * PB) {
+    const int64_t pend = min(p0 + PB, ng);
+    const int64_t p = tid < PB ? p0 + tid : ng;
     const int64_t c_lo = starts[p0], c_hi = starts[pend];
     int64_t my_lo = 0, my_hi = 0;
     if (p < ng) { my_lo = starts[p]; my_hi = starts[p + 1]; }
@@ -586,25 +623,28 @@ __global__ void __launch_bounds__(RC_NT) k_sum_rows_chunked(TabView ch, const ui
         }
         __syncthreads();
     }
-    if (p >= ng) return;
+    if (p < ng) {
 #pragma unroll
-    for (int f = 0; f < RF_NFIELDS; f++) pa.f[(int64_t)f * pa.cap + p] = a.v[f];
+        for (int f = 0; f < RF_NFIELDS; f++) pa.f[(int64_t)f * pa.cap + p] = a.v[f];
 #pragma unroll
-    for (int s2 = 0; s2 < 8; s2++)
-        if (s2 < C) pa.cnt[(int64_t)s2 * pa.ccap + p] = cs[s2];
-    const unsigned long long k0 = my_hi > my_lo ? ch.key[perm ? (int64_t)perm[my_lo] : my_lo] : 0ull;
-    pa.key[p] = shift >= 64 ? 0ull : ((k0 >> shift) << shift);
+        for (int s2 = 0; s2 < 8; s2++)
+            if (s2 < C) pa.cnt[(int64_t)s2 * pa.ccap + p] = cs[s2];
+        const unsigned long long k0 = my_hi > my_lo ? ch.key[perm ? (int64_t)perm[my_lo] : my_lo] : 0ull;
+        pa.key[p] = shift >= 64 ? 0ull : ((k0 >> shift) << shift);
+    }
+    }
 }
 
 // identity columns of a row table: caller span indices, gpu, op label, iteration rank
-__global__ void k_decode(const unsigned long long *__restrict__ key, int64_t n, KeyLayout L, int depth,
+__global__ void k_decode(const unsigned long long *__restrict__ key, const int64_t *__restrict__ n_dev, KeyLayout L,
+                         int depth,
                          const int32_t *__restrict__ lg_gpu, const int64_t *__restrict__ list_beg,
                          const int32_t *__restrict__ P_orig, const int32_t *__restrict__ P_label,
                          const int64_t *__restrict__ f, int64_t cap, const int64_t *__restrict__ pred_end,
                          int32_t *gpu, int32_t *it, int32_t *ph, int32_t *ly, int32_t *op, int32_t *label,
                          int32_t *rank, int64_t *first_pred) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    const int64_t n = *n_dev;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long k = key[j];
     int lg = (int)(k >> L.sh_lg);
     int64_t r[4] = {comp(k, L.sh_it, L.kb[0]), comp(k, L.sh_ph, L.kb[1]), comp(k, L.sh_ly, L.kb[2]),
@@ -622,26 +662,10 @@ __global__ void k_decode(const unsigned long long *__restrict__ key, int64_t n, 
     rank[j] = depth >= 1 && r[0] > 0 ? (int32_t)(r[0] - 1) : -1;
     int64_t fi = f[(int64_t)RF_FIRST_IDX * cap + j];
     first_pred[j] = (fi != INT64_MAX) ? pred_end[fi] : CH_NONE_TS;
+    }
 }
 
 // point key: (op label, gpu, iteration rank); instances without an op span are dropped
-__global__ void k_point_keys(const unsigned long long *__restrict__ key, int64_t n, KeyLayout L,
-                             const int64_t *__restrict__ list_beg, const int32_t *__restrict__ P_label, int kg,
-                             unsigned long long *__restrict__ out, uint32_t *__restrict__ v) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    unsigned long long k = key[j];
-    int lg = (int)(k >> L.sh_lg);
-    int64_t rop = comp(k, L.sh_op, L.kb[3]);
-    int64_t rit = comp(k, L.sh_it, L.kb[0]);
-    unsigned long long o = CH_INVALID_KEY;
-    if (rop > 0) {
-        unsigned long long lab = (unsigned long long)P_label[list_beg[lg * 4 + 3] + rop - 1];
-        o = (lab << (kg + L.kb[0])) | ((unsigned long long)lg << L.kb[0]) | (unsigned long long)rit;
-    }
-    out[j] = o;
-    v[j] = (uint32_t)j;
-}
 
 // points (gpu, iteration, op label) = instances of the iteration with that op label, summed over layers
 // in instance order.  One block per iteration group of the sorted instance table:
@@ -649,11 +673,27 @@ __global__ void k_point_keys(const unsigned long long *__restrict__ key, int64_t
 // instances with label l in order.  Results go to a dense [label][lg][rank] grid (compacted afterwards in
 // (label, lg, rank) order = point-key order).
 constexpr int PT_CH = 256;
-__global__ void __launch_bounds__(256) k_points_iter(TabView iv, const int64_t *__restrict__ its, int64_t n_it,
-                                                     KeyLayout Lk, const int64_t *__restrict__ list_beg,
+__device__ void points_iter_one(TabView iv, const int64_t *__restrict__ its, int64_t g, KeyLayout Lk,
+                                const int64_t *__restrict__ list_beg, const int32_t *__restrict__ P_label, int nL,
+                                int n_lg, int R0, int C, int64_t *__restrict__ df, double *__restrict__ dc,
+                                int64_t *__restrict__ dvalid, unsigned int *__restrict__ ovf);
+__global__ void __launch_bounds__(256) k_points_iter(TabView iv, const int64_t *__restrict__ its,
+                                                     const int64_t *__restrict__ n_it_d, KeyLayout Lk,
+                                                     const int64_t *__restrict__ list_beg,
                                                      const int32_t *__restrict__ P_label, int nL, int n_lg, int R0,
                                                      int C, int64_t *__restrict__ df, double *__restrict__ dc,
                                                      int64_t *__restrict__ dvalid, unsigned int *__restrict__ ovf) {
+    const int64_t n_it = *n_it_d;
+    for (int64_t g = blockIdx.x; g < n_it; g += gridDim.x) {
+        points_iter_one(iv, its, g, Lk, list_beg, P_label, nL, n_lg, R0, C, df, dc, dvalid, ovf);
+        __syncthreads();
+    }
+}
+__device__ void points_iter_one(TabView iv, const int64_t *__restrict__ its, int64_t g,
+                                KeyLayout Lk, const int64_t *__restrict__ list_beg,
+                                const int32_t *__restrict__ P_label, int nL, int n_lg, int R0,
+                                int C, int64_t *__restrict__ df, double *__restrict__ dc,
+                                int64_t *__restrict__ dvalid, unsigned int *__restrict__ ovf) {
     // one instance per thread per chunk; a stable counting sort by label puts each label's instances of
     // the chunk in a contiguous list (instance order), which thread `label` then folds
     extern __shared__ int64_t psm[];
@@ -665,8 +705,6 @@ __global__ void __launch_bounds__(256) k_points_iter(TabView iv, const int64_t *
     int32_t *wc = order + PT_CH;                                              // [8][nL] per-warp counts
     int32_t *lstart = wc + 8 * nL;                                            // [nL]
     __shared__ int64_t scan_sm[33];
-    const int64_t g = blockIdx.x;
-    if (g >= n_it) return;
     const int64_t a = its[g], b = its[g + 1];
     const unsigned long long k0 = iv.key[a];
     const int lg = (int)(k0 >> Lk.sh_lg);
@@ -748,13 +786,14 @@ __global__ void k_points_compact(const int64_t *__restrict__ dvalid, const int64
     for (int s2 = 0; s2 < C; s2++) pt.cnt[(int64_t)s2 * pt.ccap + p] = dc[(int64_t)s2 * cells + c];
 }
 
-__global__ void k_decode_points(const unsigned long long *__restrict__ key, int64_t n, int kg, int kb0,
+__global__ void k_decode_points(const unsigned long long *__restrict__ key, const int64_t *__restrict__ n_dev, int kg,
+                                int kb0,
                                 const int32_t *__restrict__ lg_gpu, const int64_t *__restrict__ list_beg,
                                 const int32_t *__restrict__ P_orig, const int64_t *__restrict__ f, int64_t cap,
                                 const int64_t *__restrict__ pred_end, int32_t *gpu, int32_t *it, int32_t *ph,
                                 int32_t *ly, int32_t *op, int32_t *label, int32_t *rank, int64_t *first_pred) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    const int64_t n = *n_dev;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     unsigned long long k = key[j];
     int64_t rit = (int64_t)(k & ((1ull << kb0) - 1));
     int lg = (int)((k >> kb0) & ((1ull << kg) - 1));
@@ -766,10 +805,12 @@ __global__ void k_decode_points(const unsigned long long *__restrict__ key, int6
     rank[j] = (int32_t)(rit - 1);
     int64_t fi = f[(int64_t)RF_FIRST_IDX * cap + j];
     first_pred[j] = (fi != INT64_MAX) ? pred_end[fi] : CH_NONE_TS;
+    }
 }
 
 // iteration extras: wall (telescoping chain span), comm union inside the iteration, aligned bounds, step
-__global__ void k_iter_extras(int64_t n, const int64_t *__restrict__ f, int64_t cap, const int32_t *__restrict__ gpu,
+__global__ void k_iter_extras(const int64_t *__restrict__ n_dev, const int64_t *__restrict__ f, int64_t cap,
+                              const int32_t *__restrict__ gpu,
                               const int32_t *__restrict__ it, const int64_t *__restrict__ first_pred,
                               const int32_t *__restrict__ gpu_lg, const int32_t *__restrict__ span_label,
                               const int64_t *__restrict__ Us, const int64_t *__restrict__ Ue,
@@ -777,8 +818,8 @@ __global__ void k_iter_extras(int64_t n, const int64_t *__restrict__ f, int64_t 
                               const int64_t *__restrict__ Ucnt, const int64_t *__restrict__ delta,
                               int64_t *__restrict__ wall, int64_t *__restrict__ cu, int64_t *__restrict__ af,
                               int64_t *__restrict__ al, int32_t *__restrict__ step) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    const int64_t n = *n_dev;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     int g = gpu[j];
     step[j] = span_label[it[j]];
     int64_t nn = f[(int64_t)RF_N * cap + j];
@@ -800,22 +841,21 @@ __global__ void k_iter_extras(int64_t n, const int64_t *__restrict__ f, int64_t 
     } else {
         wall[j] = 0; cu[j] = 0; af[j] = 0; al[j] = 0;
     }
-}
-
-__global__ void k_rates(int64_t n, const int64_t *__restrict__ f, const double *__restrict__ cnt, int64_t cap,
-                        int nr, const int32_t *__restrict__ rnum, const int32_t *__restrict__ rden,
-                        const double *__restrict__ rsc, double *__restrict__ out) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    for (int q = 0; q < nr; q++) {
-        double num = cnt[(int64_t)rnum[q] * cap + j];
-        double den = rden[q] < 0 ? (double)f[(int64_t)RF_BUSY * cap + j] * 1e-9 : cnt[(int64_t)rden[q] * cap + j];
-        out[(int64_t)q * n + j] = num / den * rsc[q];
     }
 }
-__global__ void k_gather_keys(const unsigned long long *k, const int64_t *starts, int64_t n, unsigned long long *out) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < n) out[j] = k[starts[j]];
+
+__global__ void k_rates(const int64_t *__restrict__ n_dev, const int64_t *__restrict__ f, const double *__restrict__ cnt,
+                        int64_t cap,
+                        int nr, const int32_t *__restrict__ rnum, const int32_t *__restrict__ rden,
+                        const double *__restrict__ rsc, double *__restrict__ out) {
+    const int64_t n = *n_dev;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        for (int q = 0; q < nr; q++) {
+            double num = cnt[(int64_t)rnum[q] * cap + j];
+            double den = rden[q] < 0 ? (double)f[(int64_t)RF_BUSY * cap + j] * 1e-9 : cnt[(int64_t)rden[q] * cap + j];
+            out[(int64_t)q * cap + j] = num / den * rsc[q];
+        }
+    }
 }
 }  // namespace
 
@@ -839,9 +879,16 @@ static chopper_status alloc_table(chopper_ctx *ctx, RowTable &t, int64_t cap, in
     return CHOPPER_OK;
 }
 
-// group the n sorted children (keys via perm) by key >> shift; returns group starts (device) and count
-static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sorted, int64_t n, int shift,
-                            int64_t **starts_out, int64_t *ng_out) {
+// grid for device-counted loops: enough blocks to fill the gpu, never more than the upper bound needs
+static unsigned grid_for(int64_t upper, int per_block) {
+    int64_t g = ceil_div(std::max<int64_t>(upper, 1), per_block);
+    return (unsigned)std::min<int64_t>(g, 148 * 16);
+}
+
+// group the sorted children (count *n_dev, upper bound n) by key >> shift: group starts and the group
+// count stay on the device (no host round trip); starts[ng] = end of the last group (first invalid key)
+static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sorted, int64_t n, const int64_t *n_dev,
+                            int shift, int64_t **starts_out, int64_t **ng_out) {
     CH_ALLOC_BEGIN;
     int64_t *head = CH_ALLOC(ctx, int64_t, n + 1);
     int64_t *ex = CH_ALLOC(ctx, int64_t, n + 1);
@@ -849,149 +896,109 @@ static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sor
     unsigned long long *nv = CH_ALLOC(ctx, unsigned long long, 1);
     int64_t *tot = CH_ALLOC(ctx, int64_t, 1);
     CH_ALLOC_END(ctx);
-    unsigned long long init = (unsigned long long)n;
-    CH_CUDA(ctx, cudaMemcpyAsync(nv, &init, 8, cudaMemcpyHostToDevice, ctx->st));
+    k_group_init<<<1, 1, 0, ctx->st>>>(nv, n, n_dev);
+    CH_LAUNCHED(ctx);
     if (n > 0) {
-        k_group_heads<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(keys_sorted, n, shift, head, nv);
+        k_group_heads<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(keys_sorted, n, n_dev, shift, head, nv);
         CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, head, ex, n, tot));
         k_group_starts<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(head, ex, n, starts);
         CH_LAUNCHED(ctx);
+    } else {
+        CH_CUDA(ctx, cudaMemsetAsync(tot, 0, 8, ctx->st));
     }
-    int64_t ng = 0;
-    unsigned long long hv = init;
-    if (n > 0) CH_CUDA(ctx, cudaMemcpyAsync(&ng, tot, 8, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(&hv, nv, 8, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-    int64_t nvalid = (int64_t)hv;
-    CH_CUDA(ctx, cudaMemcpyAsync(starts + ng, &nvalid, 8, cudaMemcpyHostToDevice, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    k_group_finish<<<1, 1, 0, ctx->st>>>(starts, tot, nv);
+    CH_LAUNCHED(ctx);
     *starts_out = starts;
-    *ng_out = ng;
+    *ng_out = tot;
     return CHOPPER_OK;
 }
 
 static TabView view(RowTable &t) { return TabView{t.key, t.f, t.cnt, t.cap, t.cap, 1}; }
 
-// parents from n children: warp per parent when groups average >= 4 children (and counters fit the
-// warp kernel's register array), else lane per parent with warp help for the few big groups
+// parents of the groups: mode 0 = children staged per block (many parents, few children each),
+// 1 = a warp per parent (few parents, many children), 2 = a lane per parent
 static chopper_status sum_rows(chopper_ctx *ctx, const TabView &ch, const uint32_t *perm, const int64_t *starts,
-                               int64_t ng, int64_t n_children, int shift, int C, const TabView &pa) {
-    if (ng <= 0) return CHOPPER_OK;
+                               const int64_t *ng_dev, int64_t ng_upper, int mode, int shift, int C, const TabView &pa,
+                               int fanout = 1) {
+    if (ng_upper <= 0) return CHOPPER_OK;
+    // parents per block for the staged kernel: ~RC_CH children per block from the expected fan-out
+    const int PB = fanout <= 1 ? RC_NT : std::max(8, std::min(RC_NT, RC_CH / fanout));
     const size_t shb = (size_t)(RF_NFIELDS + C) * RC_CH * 8;
-    if (n_children >= 16 * ng && C <= 32) {
-        // parents with many children (layer -> phase, iteration -> gpu): a warp per parent
-        k_sum_rows_warp<<<(unsigned)ceil_div(ng * 32, NT), NT, 0, ctx->st>>>(ch, perm, starts, ng, shift, C, pa);
-    } else if (ng >= (int64_t)RC_NT * 148 && shb <= 160 * 1024) {
-        // many parents with a few children each (instance -> layer): children staged per block
+    if (mode == 0 && shb > 160 * 1024) mode = 2;
+    if (mode == 1 && C > 32) mode = 2;
+    if (mode == 0) {
         static size_t attr = 0;
         if (shb > 48 * 1024 && shb > attr) {
             CH_CUDA(ctx, cudaFuncSetAttribute(k_sum_rows_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
             attr = shb;
         }
         if (C > 8) CH_CUDA(ctx, cudaMemsetAsync(pa.cnt, 0, 8 * (size_t)C * pa.ccap, ctx->st));
-        k_sum_rows_chunked<<<(unsigned)ceil_div(ng, RC_NT), RC_NT, shb, ctx->st>>>(ch, perm, starts, ng, shift, C, pa);
+        k_sum_rows_chunked<<<grid_for(ng_upper / std::max(fanout, 1), PB), RC_NT, shb, ctx->st>>>(ch, perm, starts, ng_dev,
+                                                                                                 shift, C, pa, PB);
+    } else if (mode == 1) {
+        k_sum_rows_warp<<<grid_for(ng_upper, NT / 32), NT, 0, ctx->st>>>(ch, perm, starts, ng_dev, shift, C, pa);
     } else {
-        k_sum_rows<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(ch, perm, starts, ng, shift, C, pa);
+        k_sum_rows<<<grid_for(ng_upper, NT), NT, 0, ctx->st>>>(ch, perm, starts, ng_dev, shift, C, pa);
     }
     CH_LAUNCHED(ctx);
     return CHOPPER_OK;
 }
 
-static chopper_status rollup(chopper_ctx *ctx, RowTable &child, RowTable &parent, int shift, int depth,
-                             const KeyLayout &L, int32_t *lg_gpu_d) {
-    int64_t *starts;
-    int64_t ng;
-    CH_TRY(group(ctx, child.key, child.n, shift, &starts, &ng));
-    CH_TRY(alloc_table(ctx, parent, std::max<int64_t>(ng, 1), ctx->C, true));
-    parent.n = ng;
-    if (ng > 0) {
-        CH_TRY(sum_rows(ctx, view(child), nullptr, starts, ng, child.n, shift, ctx->C, view(parent)));
-        k_decode<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(parent.key, ng, L, depth, lg_gpu_d, ctx->d_list_beg,
-                                                                 ctx->P_orig, ctx->P_label, parent.f, parent.cap,
-                                                                 ctx->d_pred_end, parent.gpu, parent.it, parent.ph,
-                                                                 parent.ly, parent.op, parent.label, parent.rank,
-                                                                 parent.first_pred);
-        CH_LAUNCHED(ctx);
-    }
+static chopper_status rollup(chopper_ctx *ctx, RowTable &child, RowTable &parent, int shift, int depth, int mode,
+                             const KeyLayout &L, int32_t *lg_gpu_d, int fanout = 1) {
+    int64_t *starts, *ng_dev;
+    CH_TRY(group(ctx, child.key, child.cap, child.n_dev, shift, &starts, &ng_dev));
+    CH_TRY(alloc_table(ctx, parent, std::max<int64_t>(child.cap, 1), ctx->C, true));
+    parent.n_dev = ng_dev;
+    CH_TRY(sum_rows(ctx, view(child), nullptr, starts, ng_dev, child.cap, mode, shift, ctx->C, view(parent), fanout));
+    k_decode<<<grid_for(child.cap, NT), NT, 0, ctx->st>>>(parent.key, ng_dev, L, depth, lg_gpu_d, ctx->d_list_beg,
+                                                          ctx->P_orig, ctx->P_label, parent.f, parent.cap,
+                                                          ctx->d_pred_end, parent.gpu, parent.it, parent.ph, parent.ly,
+                                                          parent.op, parent.label, parent.rank, parent.first_pred);
+    CH_LAUNCHED(ctx);
     return CHOPPER_OK;
 }
 
-chopper_status ch_tables(chopper_ctx *ctx) {
-    const int C = ctx->C;
-    const int64_t R = ctx->R;
-    KeyLayout L;
+static void key_layout(chopper_ctx *ctx, KeyLayout &L) {
     L.kb[0] = ctx->kb[0]; L.kb[1] = ctx->kb[1]; L.kb[2] = ctx->kb[2]; L.kb[3] = ctx->kb[3];
     L.sh_op = 0;
     L.sh_ly = L.kb[3];
     L.sh_ph = L.sh_ly + L.kb[2];
     L.sh_it = L.sh_ph + L.kb[1];
     L.sh_lg = L.sh_it + L.kb[0];
+}
+
+// all table stages, enqueued without host round trips except the rare radix-sort fallback check
+static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
+    const int C = ctx->C;
+    const int64_t R = ctx->R;
+    KeyLayout L;
+    key_layout(ctx, L);
     const int key_bits = L.sh_lg + ctx->kg;
     CH_ALLOC_BEGIN;
     int32_t *lg_gpu_d = CH_ALLOC(ctx, int32_t, ctx->n_lg + 1);
     ctx->sub.cnt = CH_ALLOC(ctx, double, (int64_t)(C > 0 ? C : 1) * std::max<int64_t>(R, 1));
     CH_ALLOC_END(ctx);
-    {
-        std::vector<int32_t> h(ctx->lg_gpu, ctx->lg_gpu + ctx->n_lg);
-        if (ctx->n_lg) CH_CUDA(ctx, cudaMemcpyAsync(lg_gpu_d, h.data(), 4 * ctx->n_lg, cudaMemcpyHostToDevice, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-    }
+    ctx->h_lg_gpu.assign(ctx->lg_gpu, ctx->lg_gpu + ctx->n_lg);
+    if (ctx->n_lg)
+        CH_CUDA(ctx, cudaMemcpyAsync(lg_gpu_d, ctx->h_lg_gpu.data(), 4 * ctx->n_lg, cudaMemcpyHostToDevice, ctx->st));
     ctx->sub.cap = std::max<int64_t>(R, 1);
-    // sub-run fields were written with capacity N; re-point the table view at that layout
     TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, 1, std::max<int64_t>(R, 1), 16};   // AoS sub-run rows
     if (C > 0 && R > 0) {
         const int n_lg = ctx->n_lg;
-        const int n_passes = (int)ctx->passes.size();
         ctx->d_colbad = CH_ALLOC(ctx, unsigned int, (int64_t)n_lg * C);
         CH_ALLOC_END(ctx);
-        for (int round = 0; round < 2; round++) {
-            CH_CUDA(ctx, cudaMemsetAsync(ctx->d_colbad, 0, 4 * (size_t)n_lg * C, ctx->st));
-            static bool attr = false;
-            if (!attr) {
-                CH_CUDA(ctx, cudaFuncSetAttribute(k_counters_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)sizeof(CtSmem)));
-                attr = true;
-            }
-            const int vec_ok = (((uintptr_t)ctx->ev.meta | (uintptr_t)ctx->d_run_id | (uintptr_t)ctx->d_nm_rank) & 15u) == 0;
-            for (int s0 = 0; s0 < C; s0 += CT_SG) {
-                k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->st>>>(
-                    ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, s0, ctx->N, subv.cnt,
-                    subv.ccap, ctx->d_colbad, ctx->d_mg, vec_ok);
-                CH_LAUNCHED(ctx);
-            }
-            // finiteness of every name-matching pass (R8): columns feeding a slot were checked just now,
-            // the others by k_pass_finite in ch_align
-            std::vector<unsigned int> cb((size_t)n_lg * C), pb(std::max(n_passes, 1));
-            CH_CUDA(ctx, cudaMemcpyAsync(cb.data(), ctx->d_colbad, 4 * cb.size(), cudaMemcpyDeviceToHost, ctx->st));
-            if (n_passes > 0)
-                CH_CUDA(ctx, cudaMemcpyAsync(pb.data(), ctx->d_pass_bad, 4 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-            bool changed = false;
-            for (int p = 0; p < n_passes; p++) {
-                if (ctx->pass_mismatch[p] >= 0 || ctx->pass_bad[p]) continue;
-                bool bad = pb[p] != 0;
-                for (size_t q = 0; q < cb.size(); q++)
-                    if (cb[q] && ctx->sel_pass[q] == p) bad = true;
-                if (bad) { ctx->pass_bad[p] = 1; changed = true; }
-            }
-            if (round == 0) {
-                for (int p = 0; p < n_passes; p++)
-                    if (ctx->pass_bad[p]) {
-                        ctx->rep.val_count[CV_COUNTER_NONFINITE]++;
-                        if (ctx->rep.val_first[CV_COUNTER_NONFINITE] < 0 || p < ctx->rep.val_first[CV_COUNTER_NONFINITE])
-                            ctx->rep.val_first[CV_COUNTER_NONFINITE] = p;
-                        ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
-                    }
-            }
-            if (!changed) break;
-            // a slot column was non-finite: the pass is skipped and the next valid pass provides the slot
-            // (every name-matching pass's finiteness is now known, so one redo settles it)
-            CH_TRY(ch_assign_slots(ctx));
-            CH_TRY(ch_counters_full(ctx));
+        CH_CUDA(ctx, cudaMemsetAsync(ctx->d_colbad, 0, 4 * (size_t)n_lg * C, ctx->st));
+        const int vec_ok = (((uintptr_t)ctx->ev.meta | (uintptr_t)ctx->d_run_id | (uintptr_t)ctx->d_nm_rank) & 15u) == 0;
+        for (int s0 = 0; s0 < C; s0 += CT_SG) {
+            k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, 0, ctx->st>>>(
+                ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, s0, ctx->N, subv.cnt,
+                subv.ccap, ctx->d_colbad, vec_ok);
+            CH_LAUNCHED(ctx);
         }
     }
-    // instances: stable sort of sub-runs by key, then group equal keys
+    // instances: sort of sub-runs by key, then groups of equal keys
     unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, R + 1), *k2 = CH_ALLOC(ctx, unsigned long long, R + 1);
     uint32_t *v1 = CH_ALLOC(ctx, uint32_t, R + 1), *v2 = CH_ALLOC(ctx, uint32_t, R + 1);
     CH_ALLOC_END(ctx);
@@ -1006,7 +1013,7 @@ chopper_status ch_tables(chopper_ctx *ctx) {
         if (R > 1) {
             size_t mk = ctx->used;
             int64_t *hd = CH_ALLOC(ctx, int64_t, R), *ex = CH_ALLOC(ctx, int64_t, R), *st = CH_ALLOC(ctx, int64_t, R + 2);
-            int64_t *nseg_d = CH_ALLOC(ctx, int64_t, 1);
+            int64_t *nseg_d = CH_ALLOC(ctx, int64_t, 1), *nv_d = CH_ALLOC(ctx, int64_t, 1);
             unsigned int *bad = CH_ALLOC(ctx, unsigned int, 1);
             CH_ALLOC_END(ctx);
             k_prefix_heads<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, R, L.sh_it, hd);
@@ -1014,13 +1021,10 @@ chopper_status ch_tables(chopper_ctx *ctx) {
             CH_TRY(ch_scan_excl_i64(ctx, hd, ex, R, nseg_d));
             k_group_starts<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(hd, ex, R, st);
             CH_LAUNCHED(ctx);
-            int64_t nseg = 0;
-            CH_CUDA(ctx, cudaMemcpyAsync(&nseg, nseg_d, 8, cudaMemcpyDeviceToHost, ctx->st));
             CH_CUDA(ctx, cudaMemsetAsync(bad, 0, 4, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-            int64_t rr = R;
-            CH_CUDA(ctx, cudaMemcpyAsync(st + nseg, &rr, 8, cudaMemcpyHostToDevice, ctx->st));
-            k_prefix_check<<<(unsigned)ceil_div(nseg, NT), NT, 0, ctx->st>>>(k1, st, nseg, L.sh_it, bad);
+            k_seg_starts_end<<<1, 1, 0, ctx->st>>>(st, nseg_d, R);
+            CH_LAUNCHED(ctx);
+            k_prefix_check<<<grid_for(R, NT), NT, 0, ctx->st>>>(k1, st, nseg_d, L.sh_it, bad);
             CH_LAUNCHED(ctx);
             unsigned int hbad = 0;
             CH_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->st));
@@ -1032,12 +1036,12 @@ chopper_status ch_tables(chopper_ctx *ctx) {
                                                       (int)sizeof(SegSortSmem)));
                     ss_attr = true;
                 }
-                k_seg_sort<<<(unsigned)nseg, SS_NT, sizeof(SegSortSmem), ctx->st>>>(k1, v1, st, nseg, L);
+                k_seg_sort<<<grid_for(R, 1), SS_NT, sizeof(SegSortSmem), ctx->st>>>(k1, v1, st, nseg_d, L);
                 CH_LAUNCHED(ctx);
                 k_valid_flags<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, R, hd);
                 CH_LAUNCHED(ctx);
-                CH_TRY(ch_scan_excl_i64(ctx, hd, ex, R, nseg_d));
-                k_partition<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, v1, R, ex, nseg_d, k2, v2);
+                CH_TRY(ch_scan_excl_i64(ctx, hd, ex, R, nv_d));
+                k_partition<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, v1, R, ex, nv_d, k2, v2);
                 CH_LAUNCHED(ctx);
                 alt = true;
                 done = true;
@@ -1049,107 +1053,144 @@ chopper_status ch_tables(chopper_ctx *ctx) {
     unsigned long long *ks = alt ? k2 : k1;
     uint32_t *so = alt ? v2 : v1;
     {
-        int64_t *starts;
-        int64_t ng;
-        CH_TRY(group(ctx, ks, R, 0, &starts, &ng));
-        CH_TRY(alloc_table(ctx, ctx->inst, std::max<int64_t>(ng, 1), C, true));
-        ctx->inst.n = ng;
-        if (ng > 0) {
-            CH_TRY(sum_rows(ctx, subv, so, starts, ng, R, 0, C, view(ctx->inst)));
-            k_decode<<<(unsigned)ceil_div(ng, NT), NT, 0, ctx->st>>>(
-                ctx->inst.key, ng, L, 4, lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->P_label, ctx->inst.f,
+        int64_t *starts, *ng_dev;
+        CH_TRY(group(ctx, ks, R, nullptr, 0, &starts, &ng_dev));
+        CH_TRY(alloc_table(ctx, ctx->inst, std::max<int64_t>(R, 1), C, true));
+        ctx->inst.n_dev = ng_dev;
+        if (R > 0) {
+            CH_TRY(sum_rows(ctx, subv, so, starts, ng_dev, R, 0, 0, C, view(ctx->inst)));
+            k_decode<<<grid_for(R, NT), NT, 0, ctx->st>>>(
+                ctx->inst.key, ng_dev, L, 4, lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->P_label, ctx->inst.f,
                 ctx->inst.cap, ctx->d_pred_end, ctx->inst.gpu, ctx->inst.it, ctx->inst.ph, ctx->inst.ly, ctx->inst.op,
                 ctx->inst.label, ctx->inst.rank, ctx->inst.first_pred);
             CH_LAUNCHED(ctx);
         }
     }
-    // roll-ups (D12)
-    CH_TRY(rollup(ctx, ctx->inst, ctx->layer, L.sh_ly, 3, L, lg_gpu_d));
-    CH_TRY(rollup(ctx, ctx->layer, ctx->phase, L.sh_ph, 2, L, lg_gpu_d));
-    CH_TRY(rollup(ctx, ctx->phase, ctx->iter, L.sh_it, 1, L, lg_gpu_d));
-    CH_TRY(rollup(ctx, ctx->iter, ctx->gpurow, L.sh_lg, 0, L, lg_gpu_d));
+    // roll-ups (D12): instance -> layer (staged), -> phase, -> iteration, -> gpu (warp per parent)
+    // instances per layer: ~ instances / layer spans of the local gpus (fan-out hint for the staging width)
+    const int64_t n_layers = std::max<int64_t>(ctx->n_layer_spans, 1);
+    const int fan_ly = (int)std::max<int64_t>(1, std::min<int64_t>(64, ctx->R / n_layers));
+    CH_TRY(rollup(ctx, ctx->inst, ctx->layer, L.sh_ly, 3, 0, L, lg_gpu_d, fan_ly));
+    CH_TRY(rollup(ctx, ctx->layer, ctx->phase, L.sh_ph, 2, 1, L, lg_gpu_d));
+    CH_TRY(rollup(ctx, ctx->phase, ctx->iter, L.sh_it, 1, 1, L, lg_gpu_d));
+    CH_TRY(rollup(ctx, ctx->iter, ctx->gpurow, L.sh_lg, 0, 1, L, lg_gpu_d));
     // iteration extras
     {
-        int64_t n = ctx->iter.n;
-        int64_t cap = std::max<int64_t>(n, 1);
+        const int64_t cap = std::max<int64_t>(ctx->iter.cap, 1);
         ctx->iter_wall = CH_ALLOC(ctx, int64_t, cap);
         ctx->iter_cu = CH_ALLOC(ctx, int64_t, cap);
         ctx->iter_af = CH_ALLOC(ctx, int64_t, cap);
         ctx->iter_al = CH_ALLOC(ctx, int64_t, cap);
         ctx->iter_step = CH_ALLOC(ctx, int32_t, cap);
         CH_ALLOC_END(ctx);
-        if (n > 0) {
-            k_iter_extras<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(
-                n, ctx->iter.f, ctx->iter.cap, ctx->iter.gpu, ctx->iter.it, ctx->iter.first_pred, ctx->d_gpu_lg,
-                ctx->sp.label, ctx->U_s, ctx->U_e, ctx->U_P, ctx->d_U_beg, ctx->d_U_cnt, ctx->d_delta, ctx->iter_wall,
-                ctx->iter_cu, ctx->iter_af, ctx->iter_al, ctx->iter_step);
-            CH_LAUNCHED(ctx);
-        }
+        k_iter_extras<<<grid_for(cap, NT), NT, 0, ctx->st>>>(
+            ctx->iter.n_dev, ctx->iter.f, ctx->iter.cap, ctx->iter.gpu, ctx->iter.it, ctx->iter.first_pred, ctx->d_gpu_lg,
+            ctx->sp.label, ctx->U_s, ctx->U_e, ctx->U_P, ctx->d_U_beg, ctx->d_U_cnt, ctx->d_delta, ctx->iter_wall,
+            ctx->iter_cu, ctx->iter_af, ctx->iter_al, ctx->iter_step);
+        CH_LAUNCHED(ctx);
     }
     // points (label, gpu, iteration): per-iteration label folds into a dense grid, then compaction
     {
-        const int64_t n = ctx->inst.n;
+        const int64_t n = ctx->inst.cap;
         const int nL = std::max(ctx->cfg.n_labels, 1), n_lg = std::max(ctx->n_lg, 1);
         const int R0 = (int)std::max<int64_t>(ctx->max_it_list, 1);
         const int64_t cells = (int64_t)nL * n_lg * R0;
         int lbits = bits_for((uint64_t)std::max(ctx->cfg.n_labels, 1));
         int pbits = lbits + ctx->kg + L.kb[0];
         if (pbits > 63) return ch_fail(ctx, CHOPPER_E_RANGE, "point key exceeds 63 bits");
-        int64_t *its = nullptr, n_it = 0;
-        CH_TRY(group(ctx, ctx->inst.key, n, L.sh_it, &its, &n_it));
+        if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels");
+        int64_t *its = nullptr, *n_it = nullptr;
+        CH_TRY(group(ctx, ctx->inst.key, n, ctx->inst.n_dev, L.sh_it, &its, &n_it));
         int64_t *df = CH_ALLOC(ctx, int64_t, (int64_t)RF_NFIELDS * cells);
         double *dc = CH_ALLOC(ctx, double, (int64_t)std::max(C, 1) * cells);
         int64_t *dvalid = CH_ALLOC(ctx, int64_t, cells), *dex = CH_ALLOC(ctx, int64_t, cells), *np_d = CH_ALLOC(ctx, int64_t, 1);
         unsigned int *ovf = CH_ALLOC(ctx, unsigned int, 1);
         CH_ALLOC_END(ctx);
+        *ovf_out = ovf;
         CH_CUDA(ctx, cudaMemsetAsync(dvalid, 0, 8 * (size_t)cells, ctx->st));
         CH_CUDA(ctx, cudaMemsetAsync(ovf, 0, 4, ctx->st));
-        if (n_it > 0) {
-            if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels");
-            size_t shb = (size_t)(RF_NFIELDS + C) * PT_CH * 8 + (size_t)nL * C * 8 + 4 * (2 * PT_CH + 9 * (size_t)nL);
-            static size_t attr_shb = 0;
-            if (shb > 48 * 1024 && shb > attr_shb) {
-                CH_CUDA(ctx, cudaFuncSetAttribute(k_points_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
-                attr_shb = shb;
-            }
-            k_points_iter<<<(unsigned)n_it, 256, shb, ctx->st>>>(view(ctx->inst), its, n_it, L, ctx->d_list_beg,
-                                                                 ctx->P_label, nL, n_lg, R0, C, df, dc, dvalid, ovf);
-            CH_LAUNCHED(ctx);
+        size_t shb = (size_t)(RF_NFIELDS + C) * PT_CH * 8 + (size_t)nL * C * 8 + 4 * (2 * PT_CH + 9 * (size_t)nL);
+        static size_t attr_shb = 0;
+        if (shb > 48 * 1024 && shb > attr_shb) {
+            CH_CUDA(ctx, cudaFuncSetAttribute(k_points_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
+            attr_shb = shb;
         }
+        k_points_iter<<<grid_for(std::min<int64_t>(n, (int64_t)n_lg * R0), 1), 256, shb, ctx->st>>>(
+            view(ctx->inst), its, n_it, L, ctx->d_list_beg, ctx->P_label, nL, n_lg, R0, C, df, dc, dvalid, ovf);
+        CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, dvalid, dex, cells, np_d));
-        int64_t np = 0;
-        unsigned int hovf = 0;
-        CH_CUDA(ctx, cudaMemcpyAsync(&np, np_d, 8, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-        if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "op span label >= n_labels");
-        CH_TRY(alloc_table(ctx, ctx->point, std::max<int64_t>(np, 1), C, true));
-        ctx->point.n = np;
-        if (np > 0) {
-            k_points_compact<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(dvalid, dex, cells, df, dc, C, n_lg, R0,
-                                                                              ctx->kg, L.kb[0], view(ctx->point));
-            CH_LAUNCHED(ctx);
-            k_decode_points<<<(unsigned)ceil_div(np, NT), NT, 0, ctx->st>>>(
-                ctx->point.key, np, ctx->kg, L.kb[0], lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->point.f,
-                ctx->point.cap, ctx->d_pred_end, ctx->point.gpu, ctx->point.it, ctx->point.ph, ctx->point.ly,
-                ctx->point.op, ctx->point.label, ctx->point.rank, ctx->point.first_pred);
-            CH_LAUNCHED(ctx);
-        }
+        CH_TRY(alloc_table(ctx, ctx->point, std::max<int64_t>(cells, 1), C, true));
+        ctx->point.n_dev = np_d;
+        k_points_compact<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(dvalid, dex, cells, df, dc, C, n_lg, R0,
+                                                                          ctx->kg, L.kb[0], view(ctx->point));
+        CH_LAUNCHED(ctx);
+        k_decode_points<<<grid_for(cells, NT), NT, 0, ctx->st>>>(
+            ctx->point.key, np_d, ctx->kg, L.kb[0], lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->point.f,
+            ctx->point.cap, ctx->d_pred_end, ctx->point.gpu, ctx->point.it, ctx->point.ph, ctx->point.ly,
+            ctx->point.op, ctx->point.label, ctx->point.rank, ctx->point.first_pred);
+        CH_LAUNCHED(ctx);
     }
     // derived ratio-of-sums rates
     if (ctx->n_ratios > 0) {
         RowTable *ts[2] = {&ctx->point, &ctx->iter};
         for (RowTable *t : ts) {
-            t->rates = CH_ALLOC(ctx, double, (int64_t)ctx->n_ratios * std::max<int64_t>(t->n, 1));
+            t->rates = CH_ALLOC(ctx, double, (int64_t)ctx->n_ratios * std::max<int64_t>(t->cap, 1));
             CH_ALLOC_END(ctx);
-            if (t->n > 0) {
-                k_rates<<<(unsigned)ceil_div(t->n, NT), NT, 0, ctx->st>>>(t->n, t->f, t->cnt, t->cap, ctx->n_ratios,
-                                                                          ctx->d_ratio, ctx->d_ratio + ctx->n_ratios,
-                                                                          ctx->d_ratio_scale, t->rates);
-                CH_LAUNCHED(ctx);
-            }
+            k_rates<<<grid_for(t->cap, NT), NT, 0, ctx->st>>>(t->n_dev, t->f, t->cnt, t->cap, ctx->n_ratios, ctx->d_ratio,
+                                                              ctx->d_ratio + ctx->n_ratios, ctx->d_ratio_scale, t->rates);
+            CH_LAUNCHED(ctx);
         }
     }
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    return CHOPPER_OK;
+}
+
+chopper_status ch_tables(chopper_ctx *ctx) {
+    const int C = ctx->C;
+    const int n_lg = ctx->n_lg;
+    const int n_passes = (int)ctx->passes.size();
+    const size_t mark = ctx->used;
+    for (int round = 0; round < 2; round++) {
+        ctx->used = mark;
+        unsigned int *ovf = nullptr;
+        CH_TRY(tables_body(ctx, &ovf));
+        // one read-back for every stage: row counts, the point-label overflow, and the finiteness of the
+        // counter columns that fed slots (R8; the others were checked by k_pass_finite in ch_align)
+        RowTable *tabs[6] = {&ctx->inst, &ctx->layer, &ctx->phase, &ctx->iter, &ctx->gpurow, &ctx->point};
+        int64_t hn[6] = {0, 0, 0, 0, 0, 0};
+        for (int q = 0; q < 6; q++)
+            if (tabs[q]->n_dev) CH_CUDA(ctx, cudaMemcpyAsync(&hn[q], tabs[q]->n_dev, 8, cudaMemcpyDeviceToHost, ctx->st));
+        unsigned int hovf = 0;
+        if (ovf) CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
+        std::vector<unsigned int> cb((size_t)std::max(n_lg * C, 1), 0), pb(std::max(n_passes, 1), 0);
+        if (C > 0 && ctx->R > 0)
+            CH_CUDA(ctx, cudaMemcpyAsync(cb.data(), ctx->d_colbad, 4 * (size_t)n_lg * C, cudaMemcpyDeviceToHost, ctx->st));
+        if (n_passes > 0)
+            CH_CUDA(ctx, cudaMemcpyAsync(pb.data(), ctx->d_pass_bad, 4 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        for (int q = 0; q < 6; q++) tabs[q]->n = hn[q];
+        if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "op span label >= n_labels");
+        bool changed = false;
+        for (int p = 0; p < n_passes; p++) {
+            if (ctx->pass_mismatch[p] >= 0 || ctx->pass_bad[p]) continue;
+            bool bad = pb[p] != 0;
+            for (size_t q = 0; q < (size_t)n_lg * C; q++)
+                if (cb[q] && ctx->sel_pass[q] == p) bad = true;
+            if (bad) { ctx->pass_bad[p] = 1; changed = true; }
+        }
+        if (round == 0) {
+            for (int p = 0; p < n_passes; p++)
+                if (ctx->pass_bad[p]) {
+                    ctx->rep.val_count[CV_COUNTER_NONFINITE]++;
+                    if (ctx->rep.val_first[CV_COUNTER_NONFINITE] < 0 || p < ctx->rep.val_first[CV_COUNTER_NONFINITE])
+                        ctx->rep.val_first[CV_COUNTER_NONFINITE] = p;
+                    ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
+                }
+        }
+        if (!changed) break;
+        // a slot column was non-finite: the pass is skipped and the next valid pass provides the slot
+        // (every name-matching pass's finiteness is now known, so one redo of the tables settles it)
+        CH_TRY(ch_assign_slots(ctx));
+        CH_TRY(ch_counters_full(ctx));
+    }
     return CHOPPER_OK;
 }

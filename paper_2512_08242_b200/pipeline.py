@@ -205,6 +205,7 @@ class Pipeline:
         o["glob.throughput"] = np.array(g.throughput[:n], np.float64)
         o["glob.throughput_median"] = np.array([g.throughput_median])
         o["bd.rows"] = np.array(g.bd[:int(g.n_bd) * 16], np.float64)
+        o["report.rows"] = np.array(g.report[:int(g.n_report) * 16], np.float64)
         G = self.cfg.n_traced_gpus
         o["gpu.delta"] = np.array(g.delta[:G], np.int64)
         o["gpu.delta_flag"] = np.array(g.delta_flag[:G], np.int32)

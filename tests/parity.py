@@ -86,4 +86,10 @@ def assert_parity(ref, got, per_event=True, tables=True, glob=True, bd=True):
         a, b = ref["bd.rows"], got["bd.rows"]
         if a.shape != b.shape or not np.allclose(a, b, rtol=FP_RTOL, atol=0, equal_nan=True):
             errs.append(f"bd.rows differ:\nref {a.reshape(-1, 16)[:3]}\ngot {b.reshape(-1, 16)[:3]}")
+        # report statistics (O14): quantiles and Pearson per label, fp64 within the same budget
+        a, b = ref["report.rows"], got.get("report.rows", np.zeros(0))
+        if a.shape != b.shape or not np.allclose(a, b, rtol=FP_RTOL, atol=1e-12, equal_nan=True):
+            bad = np.nonzero(~np.isclose(a, b, rtol=FP_RTOL, atol=1e-12, equal_nan=True))[0] if a.shape == b.shape else []
+            errs.append(f"report.rows differ at {bad[:8]}: ref {a[bad[:4]] if len(bad) else a.shape} "
+                        f"got {b[bad[:4]] if len(bad) else b.shape}")
     assert not errs, "\n".join(errs)

@@ -662,3 +662,69 @@ def test_validation_rules():
     assert len(o["ev.prep"]) == 2
     o = st(TinyTrace().ev(0, 0, 10, 15))
     assert o["status"][0] == 0 and (o["val.count"] == 0).all()
+
+
+# ---------------------------------------------------------------------------
+# O14 report statistics: quantile and Pearson rows per label
+# ---------------------------------------------------------------------------
+REP = dict(n=0, dur=slice(1, 6), ratio=slice(6, 11), pearson=11, label=12, mean=13)
+
+
+def report_rows(o):
+    return o["report.rows"].reshape(-1, 16)
+
+
+def test_report_aggregate_spec(golden):
+    g = golden("report.json")["aggregate"]
+    tt = _points_trace([(0, v) for v in g["values"]])
+    o = oracle.run(tt.bundle(), params(tt.bundle()))
+    assert report_rows(o)[0][REP["dur"]][2] == g["median"]
+
+
+def test_report_quantiles_worked(golden):
+    g = golden("report.json")["quantile"]
+    tt = _points_trace([(0, v) for v in g["values"]])
+    o = oracle.run(tt.bundle(), params(tt.bundle()))
+    row = report_rows(o)[0]
+    assert row[REP["n"]] == len(g["values"]) and row[REP["label"]] == 0
+    np.testing.assert_allclose(row[REP["dur"]], g["expected"], rtol=1e-15)
+    np.testing.assert_array_equal(row[REP["ratio"]], 0.0)
+
+
+@pytest.mark.parametrize("case", ["linear", "anti", "constant"])
+def test_report_pearson_worked(golden, case):
+    g = golden("report.json")["pearson"][case]
+    pts = [(int(round(r * d)), d) for r, d in zip(g["ratios"], g["durations"])]
+    tt = _points_trace(pts)
+    o = oracle.run(tt.bundle(), params(tt.bundle()))
+    rho = report_rows(o)[0][REP["pearson"]]
+    if g["rho"] is None:
+        assert np.isnan(rho)
+    else:
+        assert rho == pytest.approx(g["rho"], abs=1e-15)
+
+
+def test_report_matches_library_on_generated(gen_small):
+    """per label: quantiles == numpy.quantile(linear), Pearson == numpy.corrcoef, over the sampled points of
+    the oracle's (already pinned) point table; labels without points have n = 0 and NaN statistics."""
+    for b, o in gen_small:
+        p = oracle.default_params(b)
+        rows = report_rows(o)
+        lab, rank = o["point.label"], o["point.rank"]
+        busy, ovl = o["point.busy"], o["point.ovl"]
+        for L in range(len(b.labels)):
+            m = (lab == L) & (rank >= p["warmup"]) & (busy > 0)
+            row = rows[L]
+            assert row[REP["n"]] == m.sum() and row[REP["label"]] == L
+            if not m.any():
+                assert np.isnan(row[REP["dur"]]).all()
+                continue
+            d = busy[m].astype(float)
+            r = ovl[m] / busy[m]
+            np.testing.assert_allclose(row[REP["dur"]], np.quantile(d, [0, .25, .5, .75, 1]), rtol=1e-12)
+            np.testing.assert_allclose(row[REP["ratio"]], np.quantile(r, [0, .25, .5, .75, 1]), rtol=1e-12, atol=1e-15)
+            if np.ptp(r) == 0 or np.ptp(d) == 0:
+                assert np.isnan(row[REP["pearson"]])
+            else:
+                assert row[REP["pearson"]] == pytest.approx(np.corrcoef(r, d)[0, 1], rel=1e-9, abs=1e-12)
+            assert row[REP["mean"]] == pytest.approx(d.mean(), rel=1e-12)
