@@ -237,6 +237,14 @@ chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, c
  * (throughput, medians, global breakdown).  Synchronizes. */
 chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
 
+/* Per-GPU overlap CDFs of every op label (report statistics; Fig. 7;
+ * SPEC.md:494-497; R11), from the results of chopper_reduce_ranks (call it after that call).
+ * For each op label and traced gpu (ascending), the gpu's sampled points of the label (as in the breakdown)
+ * sorted by duration (ties: iteration rank); rows of 5 doubles: label, gpu, duration / the gpu's minimum
+ * duration, overlap ratio, empirical CDF (k + 1) / n.  out: host buffer of cap rows (may be NULL when cap is
+ * 0); *n_rows = number of rows (the first min(cap, *n_rows) are written).  Synchronizes the ctx stream. */
+chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows);
+
 /* report of the last chopper_load_columns (host copy) */
 chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out);
 /* synchronizes the ctx stream; returns the first latched error and fills the

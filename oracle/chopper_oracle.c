@@ -858,6 +858,55 @@ or_result *or_run(const or_input *in) {
         free(b); free(rr); free(sb); free(sr);
     }
 
+    /* ---------------- O15 per-GPU overlap CDF of every op label (Fig. 7) -----
+       For label L and traced gpu g: the sampled points of (g, L) (same selection as O13/O14) sorted by duration
+       (ties: iteration rank), duration normalized to the gpu's minimum (Fig. 7 caption), overlap ratio, and the
+       empirical CDF ordinate (k + 1) / n_g (R11).  Rows in (label, gpu, k) order: label, gpu, dur_norm, ratio,
+       cdf. */
+    {
+        int64_t ncdf = 0;
+        for (int64_t x = 0; x < n_pt; x++) {
+            const row_t *pr = &pt[x];
+            if (pr->r_it - 1 < in->warmup || pr->busy <= 0 || !((in->bd_gpu_mask >> pr->gpu) & 1ull)) continue;
+            ncdf++;
+        }
+        double *cd = new_f64(r, "cdf.rows", ncdf * 5);
+        int64_t w = 0;
+        int64_t *ord = (int64_t *)xcalloc(n_pt > 0 ? n_pt : 1, 8);
+        for (int L = 0; L < in->n_labels; L++) {
+            for (int g = 0; g < G; g++) {
+                int64_t n = 0;
+                for (int64_t x = 0; x < n_pt; x++) {
+                    const row_t *pr = &pt[x];
+                    if (pr->label != L || pr->gpu != g || pr->r_it - 1 < in->warmup || pr->busy <= 0) continue;
+                    if (!((in->bd_gpu_mask >> pr->gpu) & 1ull)) continue;
+                    ord[n++] = x;
+                }
+                /* insertion sort by (duration, iteration rank): points of one gpu and label are few */
+                for (int64_t a = 1; a < n; a++) {
+                    int64_t v = ord[a], b = a - 1;
+                    while (b >= 0 && (pt[ord[b]].busy > pt[v].busy ||
+                                      (pt[ord[b]].busy == pt[v].busy && pt[ord[b]].r_it > pt[v].r_it))) {
+                        ord[b + 1] = ord[b];
+                        b--;
+                    }
+                    ord[b + 1] = v;
+                }
+                for (int64_t k = 0; k < n; k++) {
+                    const row_t *pr = &pt[ord[k]];
+                    double *o = &cd[w * 5];
+                    o[0] = (double)L;
+                    o[1] = (double)g;
+                    o[2] = (double)pr->busy / (double)pt[ord[0]].busy;
+                    o[3] = (double)pr->ovl / (double)pr->busy;
+                    o[4] = (double)(k + 1) / (double)n;
+                    w++;
+                }
+            }
+        }
+        free(ord);
+    }
+
     /* per-event span indices are reported as caller indices (already) */
     for (int g = 0; g < G; g++) free(U[g]);
     free(U); free(nU); free(gbeg); free(gend); free(ord); free(rank1);

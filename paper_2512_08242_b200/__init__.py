@@ -127,7 +127,7 @@ EXPORTS = ["chopper_scratch_bytes", "chopper_create", "chopper_load_columns", "c
            "chopper_overlap", "chopper_breakdown", "chopper_reduce_ranks", "chopper_get_report",
            "chopper_status_sync", "chopper_last_error", "chopper_destroy", "chopper_kernel_launches",
            "chopper_abi_version", "chopper_pass_mismatch", "chopper_pass_conflict", "chopper_counter_present",
-           "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time"]
+           "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time", "chopper_report_cdf"]
 
 _lib = None
 
@@ -164,6 +164,7 @@ def load_library() -> ctypes.CDLL:
         "chopper_scratch_used": (I64, [P]),
         "chopper_set_timing": (None, [P, I32]),
         "chopper_phase_time": (I32, [P, I32, ctypes.POINTER(ctypes.c_float)]),
+        "chopper_report_cdf": (I32, [P, P, I64, ctypes.POINTER(I64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -231,6 +232,17 @@ def chopper_breakdown(ctx, p: chopper_bd_params, out: chopper_tables) -> int:
 
 def chopper_reduce_ranks(ctx, out: chopper_global) -> int:
     return load_library().chopper_reduce_ranks(ctx, ctypes.byref(out))
+
+
+def chopper_report_cdf(ctx) -> np.ndarray:
+    """per-GPU overlap CDF rows (label, gpu, duration / gpu minimum, overlap ratio, cdf) of every op label"""
+    lib = load_library()
+    n = I64()
+    _check(ctx, lib.chopper_report_cdf(ctx, None, 0, ctypes.byref(n)), "chopper_report_cdf")
+    out = np.zeros((max(n.value, 1), 5), np.float64)
+    if n.value > 0:
+        _check(ctx, lib.chopper_report_cdf(ctx, out.ctypes.data, n.value, ctypes.byref(n)), "chopper_report_cdf")
+    return out[:n.value]
 
 
 def chopper_get_report(ctx) -> chopper_report:

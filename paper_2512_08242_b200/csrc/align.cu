@@ -18,21 +18,43 @@ namespace {
 constexpr int NT = 256;
 
 
-// name-sequence check of every pass of the event's gpu
+// name-sequence check of every pass of the event's gpu: pass descriptors staged in shared memory, four
+// events per iteration with every load issued before the compares
+constexpr int PC_MAXP = 256;
 __global__ void k_pass_check(const uint32_t *__restrict__ meta, const int32_t *__restrict__ name_id, int64_t n,
                              const int32_t *__restrict__ gpu_lg, const int32_t *__restrict__ nm_rank,
                              const PassDesc *__restrict__ passes, const int32_t *__restrict__ pass_off,
-                             const int32_t *__restrict__ pass_idx, unsigned long long *__restrict__ mis) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    uint32_t m = meta[i];
-    if (kind_of(m) == CK_MEMOP) return;
-    int lg = gpu_lg[gpu_of(m)];
-    int64_t j = nm_rank[i];
-    int32_t nm = name_id[i];
-    for (int q = pass_off[lg]; q < pass_off[lg + 1]; q++) {
-        int p = pass_idx[q];
-        if (j < passes[p].n && passes[p].name_id[j] != nm) atomicMin(&mis[p], (unsigned long long)j);
+                             const int32_t *__restrict__ pass_idx, int n_lg, int n_passes,
+                             unsigned long long *__restrict__ mis) {
+    __shared__ PassDesc sp[PC_MAXP];
+    __shared__ int32_t soff[PC_MAXP + 1];
+    for (int q = threadIdx.x; q < n_passes && q < PC_MAXP; q += blockDim.x) sp[q] = passes[pass_idx[q]];
+    for (int q = threadIdx.x; q <= n_lg && q <= PC_MAXP; q += blockDim.x) soff[q] = pass_off[q];
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    constexpr int U = 4;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+        uint32_t mm[U];
+        int32_t jj[U], nn[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = i0 + u * stride;
+            const bool ok = i < n;
+            mm[u] = ok ? meta[i] : (uint32_t)CK_MEMOP;
+            jj[u] = ok ? nm_rank[i] : 0;
+            nn[u] = ok ? name_id[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t m = mm[u];
+            if (kind_of(m) == CK_MEMOP) continue;
+            const int lg = gpu_lg[gpu_of(m)];
+            const int64_t j = jj[u];
+            for (int q = soff[lg]; q < soff[lg + 1]; q++) {
+                const PassDesc &d = sp[q];
+                if (j < d.n && __ldg(d.name_id + j) != nn[u]) atomicMin(&mis[pass_idx[q]], (unsigned long long)j);
+            }
+        }
     }
 }
 
@@ -409,8 +431,10 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
             CH_CUDA(ctx, cudaMemcpyAsync(doff, off.data(), 4 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
             CH_CUDA(ctx, cudaMemcpyAsync(didx, idx.data(), 4 * n_passes, cudaMemcpyHostToDevice, ctx->st));
             CH_TRY(ch_fill_u64(ctx, mis, n_passes, ~0ull));
-            k_pass_check<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.name_id, N, ctx->d_gpu_lg,
-                                                                        ctx->d_nm_rank, ctx->d_passes, doff, didx, mis);
+            if (n_passes > PC_MAXP || n_lg > PC_MAXP) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 counter passes");
+            k_pass_check<<<(unsigned)std::min<int64_t>(ceil_div(N, NT * 4), 148 * 8), NT, 0, ctx->st>>>(
+                ctx->ev.meta, ctx->ev.name_id, N, ctx->d_gpu_lg, ctx->d_nm_rank, ctx->d_passes, doff, didx, n_lg, n_passes,
+                mis);
             CH_LAUNCHED(ctx);
             // one read-back: the name-sequence divergences and the per-gpu non-MEMOP counts
             std::vector<unsigned long long> hmis(n_passes);

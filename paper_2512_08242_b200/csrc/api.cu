@@ -234,6 +234,12 @@ chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     return CHOPPER_OK;
 }
 
+chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows) {
+    if (!ctx || !n_rows || cap < 0 || (cap > 0 && !out)) return CHOPPER_E_INVALID_ARG;
+    if (ctx->stage != 6) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_report_cdf before chopper_reduce_ranks");
+    return ch_report_cdf(ctx, out, cap, n_rows);
+}
+
 chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out) {
     if (!ctx || !out) return CHOPPER_E_INVALID_ARG;
     *out = ctx->rep;

@@ -204,6 +204,9 @@ struct chopper_ctx {
     bool timed[8] = {};
     int64_t *d_dense = nullptr;      // local dense exchange blocks [dense_slots][W]
     unsigned int *d_dense_ovf = nullptr;
+    int64_t *d_all = nullptr;        // all-gathered dense blocks (chopper_reduce_ranks), read by the report CDF
+    int32_t *d_all_order = nullptr;
+    int all_slots = 0;
     int dense_slots = 0;
     bool offsets_done = false;
 
@@ -371,6 +374,7 @@ chopper_status ch_tables(chopper_ctx *ctx);
 // compose.cu
 chopper_status ch_breakdown_local(chopper_ctx *ctx);
 chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
+chopper_status ch_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows);
 chopper_status ch_nccl_allgather(chopper_ctx *ctx, const void *send, void *recv, size_t bytes_per_rank);
 
 // lookup of an event's innermost span per level (spans.cu; used by events.cu)

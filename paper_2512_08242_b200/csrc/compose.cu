@@ -410,6 +410,83 @@ __global__ void __launch_bounds__(512) k_report(RepArgs A) {
     }
 }
 
+// ---- per-GPU overlap CDFs (O15; Fig. 7) ----------------------------
+// block (label, slot position): the gpu's sampled points of the label; count pass, then a write pass that
+// sorts them by (duration, iteration rank) -- one int64 key busy * 4096 + rank -- and emits
+// (label, gpu, duration / minimum, overlap ratio, (k + 1) / n) at the scanned offset.
+__device__ __forceinline__ bool cdf_point(const int64_t *blk, const Layout &Ly, int sl, int64_t r, int L,
+                                          const int64_t **pp) {
+    const int64_t *b = blk + (int64_t)sl * Ly.W;
+    const int64_t *p = b + Ly.pt_off() + (r * Ly.L + L) * PT_W;
+    *pp = p;
+    return b[1] != 0 && p[0] != 0 && p[1] > 0;
+}
+__global__ void k_cdf_count(const int64_t *__restrict__ blk, Layout Ly, const int32_t *__restrict__ order, int nslots,
+                            int warmup, int64_t *__restrict__ cnt) {
+    const int L = blockIdx.x, q = blockIdx.y;
+    const int sl = q < nslots ? order[q] : -1;
+    int c = 0;
+    if (sl >= 0)
+        for (int64_t r = (warmup > 0 ? warmup : 0) + threadIdx.x; r < Ly.MI; r += blockDim.x) {
+            const int64_t *p;
+            c += cdf_point(blk, Ly, sl, r, L, &p) ? 1 : 0;
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(CH_FULL, c, o);
+    __shared__ int sc[32];
+    if (lane_id() == 0) sc[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += sc[w];
+        cnt[(int64_t)L * gridDim.y + q] = t;
+    }
+}
+__global__ void __launch_bounds__(512) k_cdf_write(const int64_t *__restrict__ blk, Layout Ly,
+                                                   const int32_t *__restrict__ order, int nslots, int warmup,
+                                                   const int64_t *__restrict__ off, double *__restrict__ out) {
+    extern __shared__ int64_t ck[];                   // [pow2 >= MI] sort keys
+    const int L = blockIdx.x, q = blockIdx.y;
+    const int sl = q < nslots ? order[q] : -1;
+    if (sl < 0) return;
+    const int64_t *b = blk + (int64_t)sl * Ly.W;
+    const int64_t r0 = warmup > 0 ? warmup : 0;
+    __shared__ int64_t scan_sm[33];
+    __shared__ int s_n;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    for (int64_t c0 = r0; c0 < Ly.MI; c0 += blockDim.x) {          // ordered compaction by rank
+        const int64_t r = c0 + threadIdx.x;
+        const int64_t *p = nullptr;
+        const bool ok = r < Ly.MI && cdf_point(blk, Ly, sl, r, L, &p);
+        int64_t tot;
+        const int64_t pos = block_excl_sum<512>(ok ? 1 : 0, &tot, scan_sm) + s_n;
+        if (ok) ck[pos] = p[1] * 4096 + r;
+        __syncthreads();
+        if (threadIdx.x == 0) s_n += (int)tot;
+        __syncthreads();
+    }
+    const int n = s_n;
+    if (n == 0) return;
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int i = n + threadIdx.x; i < n2; i += blockDim.x) ck[i] = INT64_MAX;
+    __syncthreads();
+    block_bitonic<int64_t>(ck, n2);
+    const int64_t bmin = ck[0] >> 12;
+    const int64_t o0 = off[(int64_t)L * gridDim.y + q];
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const int64_t busy = ck[k] >> 12, r = ck[k] & 4095;
+        const int64_t *p = b + Ly.pt_off() + (r * Ly.L + L) * PT_W;
+        double *o = out + (o0 + k) * 5;
+        o[0] = L;
+        o[1] = (double)b[0];
+        o[2] = (double)busy / (double)bmin;
+        o[3] = (double)p[3] / (double)busy;
+        o[4] = (double)(k + 1) / (double)n;
+    }
+}
+
 // global iteration rows (a11): one thread per iteration rank of the reference gpu
 struct GlobArgs {
     const int64_t *blk;
@@ -699,6 +776,9 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     }
     int32_t *ord;
     CH_TRY(slot_order(ctx, all, nslots, Ly.W, &ord));
+    ctx->d_all = all;
+    ctx->d_all_order = ord;
+    ctx->all_slots = nslots;
     // global iterations + throughput
     int64_t MI = Ly.MI;
     int64_t mi2 = 1;
@@ -778,5 +858,40 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     }
     out->max_skew_ag = ctx->max_skew[0];
     out->max_skew_rs = ctx->max_skew[1];
+    return CHOPPER_OK;
+}
+
+chopper_status ch_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows) {
+    const Layout Ly = layout_of(ctx);
+    const int nL = ctx->cfg.n_labels, nslots = ctx->all_slots;
+    *n_rows = 0;
+    if (nL <= 0 || nslots <= 0 || !ctx->d_all) return CHOPPER_OK;
+    if (Ly.MI > 4096) return ch_fail(ctx, CHOPPER_E_RANGE, "max_iters > 4096 in chopper_report_cdf");
+    const int64_t cells = (int64_t)nL * nslots;
+    size_t mark = ctx->used;
+    CH_ALLOC_BEGIN;
+    int64_t *cnt = CH_ALLOC(ctx, int64_t, cells), *off = CH_ALLOC(ctx, int64_t, cells), *tot = CH_ALLOC(ctx, int64_t, 1);
+    double *rows = CH_ALLOC(ctx, double, (int64_t)nL * nslots * Ly.MI * 5);
+    CH_ALLOC_END(ctx);
+    k_cdf_count<<<dim3(nL, nslots), 256, 0, ctx->st>>>(ctx->d_all, Ly, ctx->d_all_order, nslots, ctx->bd.warmup, cnt);
+    CH_LAUNCHED(ctx);
+    CH_TRY(ch_scan_excl_i64(ctx, cnt, off, cells, tot));
+    int64_t mi2 = 1;
+    while (mi2 < Ly.MI) mi2 <<= 1;
+    static bool attr = false;
+    if (!attr) {
+        CH_CUDA(ctx, cudaFuncSetAttribute(k_cdf_write, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 1024));
+        attr = true;
+    }
+    k_cdf_write<<<dim3(nL, nslots), 512, 8 * mi2, ctx->st>>>(ctx->d_all, Ly, ctx->d_all_order, nslots, ctx->bd.warmup,
+                                                             off, rows);
+    CH_LAUNCHED(ctx);
+    int64_t n = 0;
+    CH_CUDA(ctx, cudaMemcpyAsync(&n, tot, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    const int64_t m = n < cap ? n : cap;
+    if (m > 0 && out) CH_CUDA(ctx, cudaMemcpy(out, rows, 8 * 5 * (size_t)m, cudaMemcpyDeviceToHost));
+    ctx->used = mark;
+    *n_rows = n;
     return CHOPPER_OK;
 }

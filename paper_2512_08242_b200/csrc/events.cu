@@ -508,6 +508,7 @@ __device__ __forceinline__ void smp_F(SmpCache &c, const EvParams &P, int64_t t,
 // 128-bit reads (unit j of 8 consecutive threads) then touch all 32 banks once.
 __device__ __forceinline__ int sw64(int t, int j) { return t * 4 + (j ^ ((t >> 1) & 3)); }
 __device__ __forceinline__ int sw32(int t, int j) { return t * 2 + (j ^ ((t >> 2) & 1)); }
+
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
@@ -528,6 +529,13 @@ struct EvSmem {
     int64_t tile, excl;
     int tot;
 };
+// element k of thread t in the swizzled layouts
+__device__ __forceinline__ int64_t ev_col(const EvSmem &S, int c, int t, int k) {
+    return reinterpret_cast<const int64_t *>(&S.col[c][sw64(t, k >> 1)])[k & 1];
+}
+__device__ __forceinline__ uint32_t ev_meta(const EvSmem &S, int t, int k) {
+    return reinterpret_cast<const uint32_t *>(&S.meta[sw32(t, k >> 2)])[k & 3];
+}
 
 __device__ __forceinline__ void stage_tile(EvSmem &S, const EvParams &P, int64_t base, bool vec) {
     const int tid = threadIdx.x;
@@ -629,40 +637,34 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
         int lgp = -1;
         unsigned long long prevk = CH_INVALID_KEY;
 #pragma unroll 1
-        for (int j = 0; j < EV_IPT / 2; j++) {
-            const longlong2 tv = S.col[0][sw64(tid, j)];
-            const uint2 mv = reinterpret_cast<const uint2 *>(&S.meta[sw32(tid, j >> 1)])[j & 1];
+        for (int k = 0; k < EV_IPT; k++) {           // one event per iteration: one inlined copy of the lookups
+            unsigned long long kk = CH_INVALID_KEY;
+            if (k < nv) {
+                const int64_t i = i0 + k;
+                const int64_t t = ev_col(S, 0, tid, k);
+                const int lg = P.gpu_lg[gpu_of(ev_meta(S, tid, k))];
+                if (lg != lgp) {
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const int k = 2 * j + h;
-                unsigned long long kk = CH_INVALID_KEY;
-                if (k < nv) {
-                    const int64_t i = i0 + k;
-                    const int64_t t = h ? tv.y : tv.x;
-                    const int lg = P.gpu_lg[gpu_of(h ? mv.y : mv.x)];
-                    if (lg != lgp) {
-#pragma unroll
-                        for (int lv = 0; lv < 4; lv++)
-                            lv_reset(lc[lv], P.sv, lg * 4 + lv, lgp < 0 && lg == seed_lg ? seed[lv] : -2);
-                        lgp = lg;
-                    }
-                    int32_t r[4];
-                    bool ok = true;
-#pragma unroll
-                    for (int lv = 0; lv < 4; lv++) {
-                        int32_t c = lv_lookup(lc[lv], P.sv, lv, t, i);
-                        ok &= c != -2;
-                        r[lv] = c >= 0 ? c - lc[lv].lb + 1 : 0;
-                    }
-                    if (ok && r[0] != 0)
-                        kk = ((unsigned long long)lg << P.sh_lg) | ((unsigned long long)r[0] << P.sh_it) |
-                             ((unsigned long long)r[1] << P.sh_ph) | ((unsigned long long)r[2] << P.sh_ly) |
-                             (unsigned long long)r[3];
-                    if (k > 0 && kk != prevk) hmask |= 1u << k;
+                    for (int lv = 0; lv < 4; lv++)
+                        lv_reset(lc[lv], P.sv, lg * 4 + lv, lgp < 0 && lg == seed_lg ? seed[lv] : -2);
+                    lgp = lg;
                 }
-                S.key[k][tid] = kk;
-                prevk = kk;
+                int32_t r[4];
+                bool ok = true;
+#pragma unroll
+                for (int lv = 0; lv < 4; lv++) {
+                    int32_t c = lv_lookup(lc[lv], P.sv, lv, t, i);
+                    ok &= c != -2;
+                    r[lv] = c >= 0 ? c - lc[lv].lb + 1 : 0;
+                }
+                if (ok && r[0] != 0)
+                    kk = ((unsigned long long)lg << P.sh_lg) | ((unsigned long long)r[0] << P.sh_it) |
+                         ((unsigned long long)r[1] << P.sh_ph) | ((unsigned long long)r[2] << P.sh_ly) |
+                         (unsigned long long)r[3];
+                if (k > 0 && kk != prevk) hmask |= 1u << k;
             }
+            S.key[k][tid] = kk;
+            prevk = kk;
         }
     }
     __syncthreads();
@@ -728,17 +730,11 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
     bool smp = false;
     int lgp = -1;
 #pragma unroll 1
-    for (int j = 0; j < EV_IPT / 2; j++) {
-        if (2 * j >= nv) break;
-        const longlong2 tlv = S.col[0][sw64(tid, j)], ksv = S.col[1][sw64(tid, j)], kev = S.col[2][sw64(tid, j)],
-                        pev = S.col[3][sw64(tid, j)];
-        const uint2 mv = reinterpret_cast<const uint2 *>(&S.meta[sw32(tid, j >> 1)])[j & 1];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int k = 2 * j + h;
+    for (int k = 0; k < EV_IPT; k++) {              // one event per iteration (one inlined copy of the caches)
+        {
             if (k >= nv) break;
             const int64_t i = i0 + k;
-            const uint32_t m = h ? mv.y : mv.x;
+            const uint32_t m = ev_meta(S, tid, k);
             const int lg = P.gpu_lg[gpu_of(m)];
             if (lg != lgp) {
                 cov_reset(cc, P.Ubeg[lg], P.Ucnt[lg]);
@@ -760,14 +756,14 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
                 P.sr_first[curid] = i;
             }
             const int kd = kind_of(m);
-            const int64_t ks = h ? ksv.y : ksv.x, ke = h ? kev.y : kev.x;
+            const int64_t ks = ev_col(S, 1, tid, k), ke = ev_col(S, 2, tid, k);
             const int64_t dur = ke - ks;
             int64_t ovl = 0, prep = 0, call = 0, phi = 0, psi = 0;
             cur.nev += 1;
             if (kd == CK_COMPUTE) {
-                const int64_t pe = h ? pev.y : pev.x;
+                const int64_t pe = ev_col(S, 3, tid, k);
                 if (pe != CH_NONE_TS) {
-                    const int64_t tl = h ? tlv.y : tlv.x;
+                    const int64_t tl = ev_col(S, 0, tid, k);
                     const int64_t t2 = tl < ks ? tl : ks;                  // D6: dispatch clamped to start
                     const int64_t a = t2 - pe;
                     prep = a > 0 ? a : 0;                                   // Eq. 1

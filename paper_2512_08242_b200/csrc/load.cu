@@ -25,23 +25,43 @@ __global__ void k_validate_events(const int64_t *__restrict__ tl, const int64_t 
     unsigned long long lo = ~0ull, hi = 0ull;
     int sg = -1;
     unsigned smx = 0;                      // max compute stream + 1 of gpu sg (flushed on change: few atomics)
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t m = meta[i];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    constexpr int U = 4;                   // events per iteration: all loads issued before the checks
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+        uint32_t mm[U], mpv[U], mnv[U];
+        int64_t av[U], bv[U], cv[U], apv[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = i0 + u * stride;
+            const bool ok = i < n;
+            mm[u] = ok ? meta[i] : 0u;
+            av[u] = ok ? tl[i] : 0;
+            bv[u] = ok ? ks[i] : 0;
+            cv[u] = ok ? ke[i] : 0;
+            mpv[u] = (ok && i > 0) ? meta[i - 1] : 0u;
+            apv[u] = (ok && i > 0) ? tl[i - 1] : 0;
+            mnv[u] = (ok && i + 1 < n) ? meta[i + 1] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+        const int64_t i = i0 + u * stride;
+        if (i >= n) break;
+        const uint32_t m = mm[u];
         int g = gpu_of(m), k = kind_of(m), s = stream_of(m);
-        int64_t a = tl[i], b = ks[i], c = ke[i];
+        int64_t a = av[u], b = bv[u], c = cv[u];
         if (b > c) viol(rep, CV_START_AFTER_END, i);
         if (i > 0) {
-            uint32_t mp = meta[i - 1];
+            uint32_t mp = mpv[u];
             int gp = gpu_of(mp);
             if (g < gp) viol(rep, CV_GPU_NOT_GROUPED, i);
-            if (g == gp && a < tl[i - 1]) viol(rep, CV_DISPATCH_DECREASING, i);
+            if (g == gp && a < apv[u]) viol(rep, CV_DISPATCH_DECREASING, i);
         }
         bool bad = k > CK_OTHER || g >= G || (k == CK_COMPUTE && s > 253);
         if (bad) {
             viol(rep, CV_BAD_META, i);
         } else {
-            if (i == 0 || gpu_of(meta[i - 1]) != g) atomicMin(&rep->gbeg[g], (unsigned long long)i);
-            if (i == n - 1 || gpu_of(meta[i + 1]) != g) atomicMax(&rep->gend[g], (unsigned long long)(i + 1));
+            if (i == 0 || gpu_of(mpv[u]) != g) atomicMin(&rep->gbeg[g], (unsigned long long)i);
+            if (i == n - 1 || gpu_of(mnv[u]) != g) atomicMax(&rep->gend[g], (unsigned long long)(i + 1));
             if (k == CK_COMPUTE) {
                 if (g != sg) {
                     if (sg >= 0 && smx) atomicMax(&smax[sg], smx);
@@ -57,6 +77,7 @@ __global__ void k_validate_events(const int64_t *__restrict__ tl, const int64_t 
         mx = mx > ec ? mx : ec;
         lo = lo < mn ? lo : mn;
         hi = hi > mx ? hi : mx;
+        }
     }
     if (sg >= 0 && smx) atomicMax(&smax[sg], smx);
 #pragma unroll
@@ -129,33 +150,52 @@ __global__ void k_make_keys(const uint32_t *__restrict__ meta, const int64_t *__
 }
 
 // chain predecessor + monotonicity + same-stream disjointness, in sorted order
+// 4 consecutive sorted positions per thread: the gathers of a position double as the predecessor's for
+// the next one, and all of them are issued before the checks
+constexpr int CHN = 4;
 __global__ void k_chain(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ meta,
                         const int64_t *__restrict__ ks, const int64_t *__restrict__ ke, int64_t n,
                         const int32_t *__restrict__ gpu_lg, int NG, int other, int64_t *__restrict__ pred_end,
                         DevReport *rep, unsigned int *__restrict__ bflag, unsigned long long *__restrict__ beg) {
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    uint32_t i = perm[j];
-    uint32_t m = meta[i];
-    int b = bucket_of(m, gpu_lg, NG, other);
-    int grp = b % NG;
-    bool same = false;
-    uint32_t ip = 0;
-    if (j > 0) {
-        ip = perm[j - 1];
-        same = bucket_of(meta[ip], gpu_lg, NG, other) == b;
+    const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * CHN;
+    if (j0 >= n) return;
+    uint32_t ii[CHN + 1], mm[CHN + 1];
+    int64_t sv[CHN + 1], ev[CHN + 1];
+#pragma unroll
+    for (int u = 0; u <= CHN; u++) {                  // u = 0: the predecessor of j0
+        const int64_t j = j0 + u - 1;
+        ii[u] = (j >= 0 && j < n) ? perm[j] : 0u;
     }
-    if (!same) beg[b] = (unsigned long long)j;     // first sorted position of the bucket
-    int64_t pe = CH_NONE_TS;
-    if (same && grp != other) {
-        int64_t a = ks[i];
-        if (a < ks[ip]) bflag[b] = 1u;                 // bucket not start-monotone: sort it
-        if (grp >= 1) {
-            pe = ke[ip];
-            if (a < pe) viol(rep, CV_STREAM_OVERLAP, i);
+#pragma unroll
+    for (int u = 0; u <= CHN; u++) {
+        const int64_t j = j0 + u - 1;
+        const bool ok = j >= 0 && j < n;
+        mm[u] = ok ? meta[ii[u]] : 0u;
+        sv[u] = ok ? ks[ii[u]] : 0;
+        ev[u] = ok ? ke[ii[u]] : 0;
+    }
+#pragma unroll
+    for (int u = 1; u <= CHN; u++) {
+        const int64_t j = j0 + u - 1;
+        if (j >= n) break;
+        const uint32_t i = ii[u], ip = ii[u - 1];
+        const uint32_t m = mm[u];
+        const int b = bucket_of(m, gpu_lg, NG, other);
+        const int grp = b % NG;
+        const bool same = j > 0 && bucket_of(mm[u - 1], gpu_lg, NG, other) == b;
+        if (!same) beg[b] = (unsigned long long)j;     // first sorted position of the bucket
+        int64_t pe = CH_NONE_TS;
+        if (same && grp != other) {
+            const int64_t a = sv[u];
+            if (a < sv[u - 1]) bflag[b] = 1u;              // bucket not start-monotone: sort it
+            if (grp >= 1) {
+                pe = ev[u - 1];
+                if (a < pe) viol(rep, CV_STREAM_OVERLAP, i);
+            }
         }
+        (void)ip;
+        if (kind_of(m) == CK_COMPUTE) pred_end[i] = pe;
     }
-    if (kind_of(m) == CK_COMPUTE) pred_end[i] = pe;
 }
 
 // keys of the events in the flagged bucket segments: (segment, t_ks - t0), value = input index
@@ -320,7 +360,7 @@ chopper_status ch_load(chopper_ctx *ctx) {
     // bucket begins (unchanged by the per-bucket timestamp sort below)
     unsigned long long *beg = reinterpret_cast<unsigned long long *>(ctx->d_bucket_beg);
     CH_TRY(ch_fill_u64(ctx, beg, nb + 1, ~0ull));
-    k_chain<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
+    k_chain<<<(unsigned)ceil_div(n, NT * CHN), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
                                                            ctx->ev.end_ns, n, ctx->d_gpu_lg, NG, other,
                                                            ctx->d_pred_end, ctx->d_rep, bflag, beg);
     CH_LAUNCHED(ctx);
@@ -376,7 +416,7 @@ chopper_status ch_load(chopper_ctx *ctx) {
                                          ctx->st));
             CH_CUDA(ctx, cudaMemcpyAsync(&ctx->d_rep->val_first[CV_STREAM_OVERLAP], &none, 8, cudaMemcpyHostToDevice,
                                          ctx->st));
-            k_chain<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
+            k_chain<<<(unsigned)ceil_div(n, NT * CHN), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, ctx->ev.start_ns,
                                                                    ctx->ev.end_ns, n, ctx->d_gpu_lg, NG, other,
                                                                    ctx->d_pred_end, ctx->d_rep, bflag, beg);
             CH_LAUNCHED(ctx);

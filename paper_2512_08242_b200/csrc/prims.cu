@@ -44,6 +44,66 @@ __global__ void k_tile_apply(const int64_t *__restrict__ in, int64_t n, const in
     if (total_dev && blockIdx.x == gridDim.x - 1 && threadIdx.x == SC_NT - 1) *total_dev = ex;
 }
 
+// single-pass exclusive scan (chained scan with decoupled look-back): tiles are taken in launch order
+// through a ticket, each publishes its aggregate, then its inclusive prefix once the predecessors' are
+// known; one launch per scan instead of tile-sums + recursive scan + apply.
+constexpr unsigned long long SP_A = 1ull << 62, SP_P = 2ull << 62, SP_MASK = (1ull << 62) - 1;
+__global__ void __launch_bounds__(SC_NT) k_scan_1pass(const int64_t *__restrict__ in, int64_t n,
+                                                      int64_t *__restrict__ out, int64_t *total_dev,
+                                                      unsigned long long *__restrict__ state,
+                                                      unsigned int *__restrict__ ticket) {
+    __shared__ int64_t sm[33];
+    __shared__ int64_t s_tile, s_excl;
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * SC_TILE + (int64_t)threadIdx.x * SC_IPT;
+    int64_t v[SC_IPT];
+    int64_t tsum = 0;
+#pragma unroll
+    for (int k = 0; k < SC_IPT; k++) {
+        v[k] = base + k < n ? in[base + k] : 0;
+        tsum += v[k];
+    }
+    int64_t tot;
+    int64_t ex = block_excl_sum<SC_NT>(tsum, &tot, sm);
+    const int lane = lane_id();
+    if (threadIdx.x < 32) {
+        int64_t excl = 0;
+        if (tile == 0) {
+            if (lane == 0) atomicExch(&state[0], SP_P | (unsigned long long)tot);
+        } else {
+            if (lane == 0) atomicExch(&state[tile], SP_A | (unsigned long long)tot);
+            int64_t p = tile - 1 - lane;
+            while (true) {
+                unsigned long long st = SP_P;
+                if (p >= 0) st = *((volatile unsigned long long *)&state[p]);
+                const unsigned fl = (unsigned)(st >> 62);
+                const unsigned pm = __ballot_sync(CH_FULL, fl == 2u), zm = __ballot_sync(CH_FULL, fl == 0u);
+                const int fp = pm ? __ffs(pm) - 1 : 32;
+                const unsigned need = fp >= 31 ? CH_FULL : ((2u << fp) - 1u);
+                if (zm & need) continue;
+                int64_t x = lane <= fp ? (int64_t)(st & SP_MASK) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(CH_FULL, x, o);
+                excl += x;
+                if (fp < 32) break;
+                p -= 32;
+            }
+            if (lane == 0) atomicExch(&state[tile], SP_P | (unsigned long long)(excl + tot));
+        }
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    ex += s_excl;
+#pragma unroll
+    for (int k = 0; k < SC_IPT; k++) {
+        if (base + k < n) out[base + k] = ex;
+        ex += v[k];
+    }
+    if (total_dev && tile == (int64_t)gridDim.x - 1 && threadIdx.x == SC_NT - 1) *total_dev = ex;
+}
+
 // ---- segmented scans: aggregate (head seen, value since last head) ------------------------------
 template <int OP>
 __device__ __forceinline__ int64_t op_comb(int64_t a, int64_t b) {
@@ -269,6 +329,19 @@ chopper_status ch_scan_excl_i64(chopper_ctx *ctx, const int64_t *in, int64_t *ou
         return CHOPPER_OK;
     }
     int64_t ntile = ceil_div(n, SC_TILE);
+    if (ntile > 1) {
+        // single pass: tile states + ticket, zeroed by one memset
+        size_t mark = ctx->used;
+        CH_ALLOC_BEGIN;
+        unsigned long long *state = CH_ALLOC(ctx, unsigned long long, ntile + 1);
+        CH_ALLOC_END(ctx);
+        CH_CUDA(ctx, cudaMemsetAsync(state, 0, 8 * (size_t)(ntile + 1), ctx->st));
+        k_scan_1pass<<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, n, out, total_dev, state,
+                                                             reinterpret_cast<unsigned int *>(state + ntile));
+        CH_LAUNCHED(ctx);
+        ctx->used = mark;
+        return CHOPPER_OK;
+    }
     size_t mark = ctx->used;
     CH_ALLOC_BEGIN;
     int64_t *offs = nullptr;

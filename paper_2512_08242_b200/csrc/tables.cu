@@ -589,21 +589,38 @@ __global__ void __launch_bounds__(RC_NT) k_sum_rows_chunked(TabView ch, const ui
     for (int64_t j0 = c_lo; j0 < c_hi; j0 += RC_CH) {
         const int m = (int)min((int64_t)RC_CH, c_hi - j0);
         if (ch.rs == 1 && !perm) {
-            for (int e = tid; e < NF * RC_CH; e += RC_NT) {
-                const int f = e / RC_CH, t = e % RC_CH;
-                if (t < m) {
-                    const int64_t c = j0 + t;
-                    vals[e] = f < RF_NFIELDS ? ch.f[(int64_t)f * ch.cap + c]
-                                             : __double_as_longlong(ch.cnt[(int64_t)(f - RF_NFIELDS) * ch.ccap + c]);
-                }
+            // all of a thread's column loads in flight before the shared-memory stores (RC_NT == RC_CH:
+            // thread t owns child j0 + t in every column)
+            if (tid < m) {
+                const int64_t c = j0 + tid;
+                int64_t x[RF_NFIELDS];
+#pragma unroll
+                for (int f = 0; f < RF_NFIELDS; f++) x[f] = __ldg(ch.f + (int64_t)f * ch.cap + c);
+                int64_t y[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) y[q] = q < C ? __double_as_longlong(__ldg(ch.cnt + (int64_t)q * ch.ccap + c)) : 0;
+#pragma unroll
+                for (int f = 0; f < RF_NFIELDS; f++) vals[f * RC_CH + tid] = x[f];
+#pragma unroll
+                for (int q = 0; q < 8; q++) if (q < C) vals[(RF_NFIELDS + q) * RC_CH + tid] = y[q];
+                for (int q = 8; q < C; q++)
+                    vals[(RF_NFIELDS + q) * RC_CH + tid] = __double_as_longlong(ch.cnt[(int64_t)q * ch.ccap + c]);
             }
         } else {
             for (int t = tid; t < m; t += RC_NT) {
                 const int64_t c = perm ? (int64_t)perm[j0 + t] : j0 + t;
                 const int64_t *row = ch.f + c * ch.rs;
+                int64_t x[RF_NFIELDS];
 #pragma unroll
-                for (int f = 0; f < RF_NFIELDS; f++) vals[f * RC_CH + t] = row[(int64_t)f * ch.cap];
-                for (int s2 = 0; s2 < C; s2++)
+                for (int f = 0; f < RF_NFIELDS; f++) x[f] = __ldg(row + (int64_t)f * ch.cap);
+                int64_t y[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) y[q] = q < C ? __double_as_longlong(__ldg(ch.cnt + (int64_t)q * ch.ccap + c)) : 0;
+#pragma unroll
+                for (int f = 0; f < RF_NFIELDS; f++) vals[f * RC_CH + t] = x[f];
+#pragma unroll
+                for (int q = 0; q < 8; q++) if (q < C) vals[(RF_NFIELDS + q) * RC_CH + t] = y[q];
+                for (int s2 = 8; s2 < C; s2++)
                     vals[(RF_NFIELDS + s2) * RC_CH + t] = __double_as_longlong(ch.cnt[(int64_t)s2 * ch.ccap + c]);
             }
         }
@@ -718,13 +735,20 @@ __device__ void points_iter_one(TabView iv, const int64_t *__restrict__ its, int
     for (int q = tid; q < nL * C; q += blockDim.x) cacc[q] = 0.0;
     for (int64_t j0 = a; j0 < b; j0 += PT_CH) {
         const int m = (int)min((int64_t)PT_CH, b - j0);
-        for (int e = tid; e < NF * PT_CH; e += blockDim.x) {
-            const int f = e / PT_CH, t = e % PT_CH;
-            if (t < m) {
-                const int64_t j = j0 + t;
-                vals[e] = f < RF_NFIELDS ? iv.f[(int64_t)f * iv.cap + j]
-                                         : __double_as_longlong(iv.cnt[(int64_t)(f - RF_NFIELDS) * iv.ccap + j]);
-            }
+        if (tid < m) {           // PT_CH == blockDim: thread t loads instance j0 + t, all loads in flight first
+            const int64_t j = j0 + tid;
+            int64_t x[RF_NFIELDS];
+#pragma unroll
+            for (int f = 0; f < RF_NFIELDS; f++) x[f] = __ldg(iv.f + (int64_t)f * iv.cap + j);
+            int64_t y[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) y[q] = q < C ? __double_as_longlong(__ldg(iv.cnt + (int64_t)q * iv.ccap + j)) : 0;
+#pragma unroll
+            for (int f = 0; f < RF_NFIELDS; f++) vals[f * PT_CH + tid] = x[f];
+#pragma unroll
+            for (int q = 0; q < 8; q++) if (q < C) vals[(RF_NFIELDS + q) * PT_CH + tid] = y[q];
+            for (int q = 8; q < C; q++)
+                vals[(RF_NFIELDS + q) * PT_CH + tid] = __double_as_longlong(iv.cnt[(int64_t)q * iv.ccap + j]);
         }
         for (int q = tid; q < 8 * nL; q += blockDim.x) wc[q] = 0;
         int l = -1;

@@ -13,7 +13,7 @@ from typing import Dict, Optional
 import numpy as np
 
 from . import (chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
-               chopper_create, chopper_destroy, chopper_events, chopper_get_report, chopper_global,
+               chopper_create, chopper_destroy, chopper_events, chopper_get_report, chopper_global, chopper_report_cdf,
                chopper_kernel_launches, chopper_load_columns, chopper_overlap, chopper_reduce_ranks,
                chopper_samples, chopper_scratch_bytes, chopper_spans, chopper_status_sync, chopper_tables,
                _check, bd_params, dev_to_numpy, load_library, rows_to_numpy)
@@ -165,9 +165,10 @@ class Pipeline:
         _check(self.ctx, chopper_breakdown(self.ctx, self._bd, tabs), "chopper_breakdown")
         glob = chopper_global()
         _check(self.ctx, chopper_reduce_ranks(self.ctx, glob), "chopper_reduce_ranks")
+        cdf = chopper_report_cdf(self.ctx) if full else None
         st, mask = chopper_status_sync(self.ctx)
         res.update(status=st, mask=mask, offsets=offs, tables=tabs, glob=glob, out=out,
-                   report=chopper_get_report(self.ctx))
+                   report=chopper_get_report(self.ctx), cdf=cdf)
         return res
 
     def to_numpy(self, res: dict, n_ratios: int = 0) -> Dict[str, np.ndarray]:
@@ -206,6 +207,8 @@ class Pipeline:
         o["glob.throughput_median"] = np.array([g.throughput_median])
         o["bd.rows"] = np.array(g.bd[:int(g.n_bd) * 16], np.float64)
         o["report.rows"] = np.array(g.report[:int(g.n_report) * 16], np.float64)
+        if res.get("cdf") is not None:
+            o["cdf.rows"] = res["cdf"].reshape(-1)
         G = self.cfg.n_traced_gpus
         o["gpu.delta"] = np.array(g.delta[:G], np.int64)
         o["gpu.delta_flag"] = np.array(g.delta_flag[:G], np.int32)

@@ -1,7 +1,8 @@
 #!/bin/bash
 # Profiling pass for one bench configuration (run under gpurun, 1 GPU).
-#   launches.csv : every kernel launch of warm-up + 1 timed step, device time (cold, serialized)
-#   prof_events  : ncu --set full of the fused event pass (k_events), one launch
+#   launches.csv    : every kernel launch of 3 warm-up + 1 timed step, device time (cold, serialised)
+#   prof_events     : ncu --set full of the fused event pass (k_events), one launch
+#   prof_tables     : ncu --set full of the counter pass and the staged roll-ups, one step's launches
 set -x
 OUT=${1:-gpurun_out}
 mkdir -p $OUT
@@ -9,4 +10,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/launches_bench.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_events -s 3 -c 1 -f -o $OUT/prof_events \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/prof_events.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_counters_tiled|k_sum_rows_chunked|k_points_iter" \
+    -s 12 -c 4 -f -o $OUT/prof_tables \
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/prof_tables.log 2>&1
 ls -la $OUT

@@ -92,4 +92,8 @@ def assert_parity(ref, got, per_event=True, tables=True, glob=True, bd=True):
             bad = np.nonzero(~np.isclose(a, b, rtol=FP_RTOL, atol=1e-12, equal_nan=True))[0] if a.shape == b.shape else []
             errs.append(f"report.rows differ at {bad[:8]}: ref {a[bad[:4]] if len(bad) else a.shape} "
                         f"got {b[bad[:4]] if len(bad) else b.shape}")
+        if "cdf.rows" in got:
+            a, b = ref["cdf.rows"], got["cdf.rows"]
+            if a.shape != b.shape or not np.allclose(a, b, rtol=FP_RTOL, atol=1e-12, equal_nan=True):
+                errs.append(f"cdf.rows differ: shapes {a.shape} {b.shape}")
     assert not errs, "\n".join(errs)

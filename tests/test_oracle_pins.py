@@ -728,3 +728,38 @@ def test_report_matches_library_on_generated(gen_small):
             else:
                 assert row[REP["pearson"]] == pytest.approx(np.corrcoef(r, d)[0, 1], rel=1e-9, abs=1e-12)
             assert row[REP["mean"]] == pytest.approx(d.mean(), rel=1e-12)
+
+
+def cdf_rows(o):
+    return o["cdf.rows"].reshape(-1, 5)
+
+
+@pytest.mark.parametrize("case", ["three", "single"])
+def test_cdf_spec(golden, case):
+    g = golden("report.json")["cdf"]
+    g = g if case == "three" else g["single"]
+    # shuffle the iteration order: the CDF sorts by duration
+    durs = list(reversed(g["durations"]))
+    tt = _points_trace([(0, d) for d in durs])
+    o = oracle.run(tt.bundle(), params(tt.bundle()))
+    rows = cdf_rows(o)
+    rows = rows[rows[:, 0] == 0]
+    np.testing.assert_allclose(rows[:, 2], g["normalized"], rtol=1e-15)
+    np.testing.assert_allclose(rows[:, 4], g["cdf"], rtol=1e-15)
+    np.testing.assert_array_equal(rows[:, 3], 0.0)
+
+
+def test_cdf_invariants_generated(gen_small):
+    """per (label, gpu): CDF ends at 1 and increases by 1/n, durations start at 1 and never decrease,
+    ratios in [0, 1]; the rows partition the O14 points of the label (same count)."""
+    for b, o in gen_small:
+        rows, rep = cdf_rows(o), report_rows(o)
+        for L in range(len(b.labels)):
+            sel = rows[rows[:, 0] == L]
+            assert len(sel) == rep[L][REP["n"]]
+            for g in np.unique(sel[:, 1]):
+                s = sel[sel[:, 1] == g]
+                n = len(s)
+                np.testing.assert_allclose(s[:, 4], np.arange(1, n + 1) / n, rtol=1e-15)
+                assert s[0, 2] == 1.0 and (np.diff(s[:, 2]) >= 0).all()
+                assert ((s[:, 3] >= 0) & (s[:, 3] <= 1)).all()
