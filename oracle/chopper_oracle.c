@@ -3,7 +3,8 @@
  *
  * A plain, slow, single-threaded reading of the Chopper analysis path
  * (arXiv 2512.08242).  Each block is labelled with the oracle step of
- * DESIGN.md ("O1".."O13") and the paper passage it restates.  Methods are
+ * DESIGN.md ("O1".."O15"; O14/O15 are the report statistics of SURVEY §8(f)
+ * row 1) and the paper passage it restates.  Methods are
  * deliberately the plain definitions: qsort + sequential loops, an
  * active-set sweep for span containment, explicit piecewise integration for
  * frequency / power, pairwise chain checks.  Nothing here is blocked, fused

@@ -26,31 +26,43 @@ constexpr unsigned long long FLAG_A = 1ull << 62, FLAG_P = 2ull << 62, VAL_MASK 
 
 // ---- comm / compute unions: one block per local gpu ----------------------------------------------
 // positions pos[lo..hi) index events sorted by t_ks; output merged intervals at out[lo + m].
-__global__ void __launch_bounds__(1024) k_union_block(const uint32_t *__restrict__ pos, const int64_t *__restrict__ seg_lo,
-                                                      const int64_t *__restrict__ seg_hi, const int64_t *__restrict__ ks,
-                                                      const int64_t *__restrict__ ke, int64_t *__restrict__ Us,
-                                                      int64_t *__restrict__ Ue, int64_t *__restrict__ UP,
-                                                      int64_t *__restrict__ Ubeg, int64_t *__restrict__ Ucnt) {
+// 4 consecutive sorted intervals per thread (all gathers in flight at once), 4096 per block iteration:
+// inclusive prefix max of the ends -> a head wherever a start exceeds the running max end -> merged
+// intervals, then prefix lengths.
+constexpr int UN_IPT = 4, UN_NT = 1024, UN_CH = UN_NT * UN_IPT;
+__global__ void __launch_bounds__(UN_NT) k_union_block(const uint32_t *__restrict__ pos, const int64_t *__restrict__ seg_lo,
+                                                       const int64_t *__restrict__ seg_hi, const int64_t *__restrict__ ks,
+                                                       const int64_t *__restrict__ ke, int64_t *__restrict__ Us,
+                                                       int64_t *__restrict__ Ue, int64_t *__restrict__ UP,
+                                                       int64_t *__restrict__ Ubeg, int64_t *__restrict__ Ucnt) {
     __shared__ int64_t sm[33];
     __shared__ int64_t smax[32];
-    __shared__ int64_t s_carry_max;
-    __shared__ int64_t s_m;
-    __shared__ unsigned char shead[1024 + 1];
-    int lg = blockIdx.x;
-    int64_t lo = seg_lo[lg], hi = seg_hi[lg];
-    int tid = threadIdx.x, w = tid >> 5, l = lane_id();
+    __shared__ int64_t s_carry_max, s_m, s_next_s;
+    const int lg = blockIdx.x;
+    const int64_t lo = seg_lo[lg], hi = seg_hi[lg];
+    const int tid = threadIdx.x, w = tid >> 5, l = lane_id();
     if (tid == 0) { s_carry_max = INT64_MIN; s_m = 0; }
     __syncthreads();
-    for (int64_t base = lo; base < hi; base += 1024) {
-        int64_t j = base + tid;
-        bool valid = j < hi;
-        int64_t s = 0, e = INT64_MIN;
-        if (valid) { uint32_t i = pos[j]; s = ks[i]; e = ke[i]; }
-        // inclusive prefix max of e across the block
-        int64_t v = e;
+    for (int64_t base = lo; base < hi; base += UN_CH) {
+        const int64_t j0 = base + (int64_t)tid * UN_IPT;
+        int64_t sv[UN_IPT], ev[UN_IPT];
+        uint32_t pi[UN_IPT];
+#pragma unroll
+        for (int u = 0; u < UN_IPT; u++) pi[u] = j0 + u < hi ? pos[j0 + u] : 0u;
+#pragma unroll
+        for (int u = 0; u < UN_IPT; u++) {
+            const bool ok = j0 + u < hi;
+            sv[u] = ok ? ks[pi[u]] : INT64_MAX;
+            ev[u] = ok ? ke[pi[u]] : INT64_MIN;
+        }
+        // thread max, then block inclusive prefix max of the thread maxima
+        int64_t tmax = INT64_MIN;
+#pragma unroll
+        for (int u = 0; u < UN_IPT; u++) tmax = ev[u] > tmax ? ev[u] : tmax;
+        int64_t v = tmax;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int64_t y = __shfl_up_sync(CH_FULL, v, o);
+            const int64_t y = __shfl_up_sync(CH_FULL, v, o);
             if (l >= o && y > v) v = y;
         }
         if (l == 31) smax[w] = v;
@@ -59,56 +71,68 @@ __global__ void __launch_bounds__(1024) k_union_block(const uint32_t *__restrict
             int64_t x = smax[l];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                int64_t y = __shfl_up_sync(CH_FULL, x, o);
+                const int64_t y = __shfl_up_sync(CH_FULL, x, o);
                 if (l >= o && y > x) x = y;
             }
-            smax[l] = x;   // inclusive over warps
+            smax[l] = x;
         }
         __syncthreads();
-        int64_t carry = s_carry_max;
-        int64_t wpre = w > 0 ? smax[w - 1] : INT64_MIN;
-        int64_t Mi = v;
-        if (wpre > Mi) Mi = wpre;
-        if (carry > Mi) Mi = carry;
-        // exclusive (previous element's inclusive max)
-        int64_t Mprev = __shfl_up_sync(CH_FULL, Mi, 1);
-        if (l == 0) {
-            Mprev = wpre > carry ? wpre : carry;
-            if (w > 0) {
-                // previous warp's last inclusive = max(carry, smax[w-1])
-            }
+        // running max before this thread's first interval
+        int64_t run = s_carry_max;
+        const int64_t wpre = w > 0 ? smax[w - 1] : INT64_MIN;
+        if (wpre > run) run = wpre;
+        const int64_t lpre = __shfl_up_sync(CH_FULL, v, 1);
+        if (l > 0 && lpre > run) run = lpre;
+        bool hd[UN_IPT];
+        int64_t mi[UN_IPT];
+        int nh = 0;
+#pragma unroll
+        for (int u = 0; u < UN_IPT; u++) {
+            hd[u] = j0 + u < hi && sv[u] > run;     // run = INT64_MIN for the very first interval
+            nh += hd[u];
+            if (ev[u] > run) run = ev[u];
+            mi[u] = run;                            // inclusive max through this interval
         }
-        bool head = valid && (s > Mprev);   // Mprev = INT64_MIN for the very first element
-        shead[tid] = head;
         int64_t tot;
-        int64_t ex = block_excl_sum<1024>(head ? 1 : 0, &tot, sm);
-        int64_t m0 = s_m;
-        if (head) Us[lo + m0 + ex] = s;
-        // last element of its run: next element is a head, or end of segment
-        bool nexthead;
-        if (tid < 1023) nexthead = (j + 1 < hi) ? (bool)shead[tid + 1] : true;
-        else {
-            if (j + 1 < hi) { uint32_t i2 = pos[j + 1]; nexthead = ks[i2] > Mi; }
-            else nexthead = true;
+        const int64_t ex = block_excl_sum<UN_NT>(nh, &tot, sm);
+        const int64_t m0 = s_m;
+        // the first start of the next thread decides whether this thread's last interval closes a run
+        int64_t k = m0 + ex;
+#pragma unroll
+        for (int u = 0; u < UN_IPT; u++) {
+            if (hd[u]) { Us[lo + k] = sv[u]; k++; }
+            bool close = false;
+            if (j0 + u < hi) {
+                if (u + 1 < UN_IPT) close = !(j0 + u + 1 < hi) || hd[u + 1];
+                else close = true;   // resolved below against the next thread's first start
+            }
+            if (close && u + 1 < UN_IPT) Ue[lo + k - 1] = mi[u];
         }
-        if (valid && nexthead) Ue[lo + m0 + ex + (head ? 0 : -1)] = Mi;
+        // last interval of the thread: closes a run if the next interval (next thread / next chunk) is a head
+        const int64_t jl = j0 + UN_IPT - 1;
+        if (jl < hi) {
+            bool nexthead = true;
+            if (jl + 1 < hi) nexthead = ks[pos[jl + 1]] > mi[UN_IPT - 1];
+            if (nexthead) Ue[lo + k - 1] = mi[UN_IPT - 1];
+        }
         __syncthreads();
-        if (tid == 1023) s_carry_max = Mi;
+        if (tid == UN_NT - 1) s_carry_max = run;
         if (tid == 0) s_m = m0 + tot;
         __syncthreads();
     }
-    int64_t mcount = s_m;
+    const int64_t mcount = s_m;
     // prefix lengths
-    int64_t run = 0;
-    for (int64_t base = 0; base < mcount; base += 1024) {
-        int64_t m = base + tid;
-        int64_t len = m < mcount ? Ue[lo + m] - Us[lo + m] : 0;
+    int64_t acc = 0;
+    for (int64_t b2 = 0; b2 < mcount; b2 += UN_NT) {
+        const int64_t m = b2 + tid;
+        const int64_t len = m < mcount ? Ue[lo + m] - Us[lo + m] : 0;
         int64_t tot;
-        int64_t ex = block_excl_sum<1024>(len, &tot, sm);
-        if (m < mcount) UP[lo + m] = run + ex;
-        run += tot;
+        const int64_t ex = block_excl_sum<UN_NT>(len, &tot, sm);
+        if (m < mcount) UP[lo + m] = acc + ex;
+        acc += tot;
     }
     if (tid == 0) { Ubeg[lg] = lo; Ucnt[lg] = mcount; }
+    (void)s_next_s;
 }
 
 // sample prefix inputs: f_k * (tau_{k+1} - tau_k) within a gpu, 0 at a gpu's last sample
@@ -885,7 +909,7 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
     CH_CUDA(ctx, cudaMemcpyAsync(seg_lo, lo.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(seg_hi, hi.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
     if (n_lg > 0) {
-        k_union_block<<<n_lg, 1024, 0, ctx->st>>>(ctx->d_perm, seg_lo, seg_hi, ctx->ev.start_ns, ctx->ev.end_ns, ctx->U_s,
+        k_union_block<<<n_lg, UN_NT, 0, ctx->st>>>(ctx->d_perm, seg_lo, seg_hi, ctx->ev.start_ns, ctx->ev.end_ns, ctx->U_s,
                                                   ctx->U_e, ctx->U_P, ctx->d_U_beg, ctx->d_U_cnt);
         CH_LAUNCHED(ctx);
     }
@@ -921,7 +945,7 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
         }
         CH_CUDA(ctx, cudaMemcpyAsync(vlo, a.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
         CH_CUDA(ctx, cudaMemcpyAsync(vhi, b.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
-        k_union_block<<<n_lg, 1024, 0, ctx->st>>>(ctx->d_vperm, vlo, vhi, ctx->ev.start_ns, ctx->ev.end_ns, ctx->V_s,
+        k_union_block<<<n_lg, UN_NT, 0, ctx->st>>>(ctx->d_vperm, vlo, vhi, ctx->ev.start_ns, ctx->ev.end_ns, ctx->V_s,
                                                   ctx->V_e, ctx->V_P, ctx->d_V_beg, ctx->d_V_cnt);
         CH_LAUNCHED(ctx);
     }

@@ -219,6 +219,71 @@ __global__ void k_seg_scatter(const uint32_t *__restrict__ sorted, const int64_t
     perm[lo[a] + (t - pre[a])] = sorted[t];
 }
 
+// ---- stream-merge fast path for the non-monotone buckets (D1) ------------------------------------
+// A bucket mixing several streams (all-gathers and reduce-scatters) is not start-monotone in dispatch
+// order, but each stream serializes its kernels, so each stream's events usually are.  Then the stable
+// timestamp sort of the bucket is a merge of its per-stream lists: an element's position is its index in
+// its stream's list plus, for every other stream of the bucket, the number of that stream's events with
+// a smaller (t_ks, input index) -- a binary search.  Lists come from a one-byte stable partition.
+constexpr int SS_STREAMS = 256;
+__device__ __forceinline__ int seg_of(const int64_t *__restrict__ pre, int nseg, int64_t t) {
+    int a = 0, b = nseg;
+    while (b - a > 1) { int m = (a + b) >> 1; if (pre[m] <= t) a = m; else b = m; }
+    return a;
+}
+__global__ void k_ss_keys(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ meta,
+                          const int64_t *__restrict__ lo, const int64_t *__restrict__ pre, int nseg, int64_t M,
+                          unsigned long long *__restrict__ key, uint32_t *__restrict__ val, unsigned int *__restrict__ cnt,
+                          unsigned int *__restrict__ fail) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M) return;
+    const int a = seg_of(pre, nseg, t);
+    const uint32_t i = perm[lo[a] + (t - pre[a])];
+    const int st = stream_of(meta[i]);
+    if (st >= SS_STREAMS) atomicOr(fail, 1u);
+    const int cell = a * SS_STREAMS + (st & (SS_STREAMS - 1));
+    key[t] = (unsigned long long)cell;
+    val[t] = i;
+    atomicAdd(&cnt[cell], 1u);
+}
+// each stream list start-monotone?
+__global__ void k_ss_check(const unsigned long long *__restrict__ key, const uint32_t *__restrict__ val, int64_t M,
+                           const int64_t *__restrict__ ks, unsigned int *__restrict__ fail) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0 || t >= M) return;
+    if (key[t] == key[t - 1] && ks[val[t]] < ks[val[t - 1]]) atomicOr(fail, 2u);
+}
+__global__ void k_ss_rank(const unsigned long long *__restrict__ key, const uint32_t *__restrict__ val, int64_t M,
+                          const int64_t *__restrict__ ks, const unsigned int *__restrict__ cnt,
+                          const int64_t *__restrict__ cstart, const int64_t *__restrict__ lo,
+                          uint32_t *__restrict__ perm) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= M) return;
+    const int cell = (int)key[t];
+    const int a = cell / SS_STREAMS;
+    const uint32_t x = val[t];
+    const int64_t kx = ks[x];
+    int64_t r = t - cstart[cell];
+    for (int c2 = a * SS_STREAMS; c2 < (a + 1) * SS_STREAMS; c2++) {
+        const unsigned int n2 = cnt[c2];
+        if (c2 == cell || n2 == 0) continue;
+        int64_t l = cstart[c2], h = l + n2;           // count of (ks, idx) < (kx, x) in list c2
+        const int64_t l0 = l;
+        while (l < h) {
+            const int64_t m = (l + h) >> 1;
+            const uint32_t y = val[m];
+            const int64_t ky = ks[y];
+            if (ky < kx || (ky == kx && y < x)) l = m + 1; else h = m;
+        }
+        r += l - l0;
+    }
+    perm[lo[a] + r] = x;
+}
+__global__ void k_u32_i64(const unsigned int *__restrict__ a, int64_t *__restrict__ b, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = a[i];
+}
+
 __global__ void k_init_report(DevReport *r) {
     int t = threadIdx.x;
     if (t < CV_NRULES) { r->val_count[t] = 0; r->val_first[t] = ~0ull; }
@@ -399,14 +464,47 @@ chopper_status ch_load(chopper_ctx *ctx) {
         seg_lo.push_back(n);
         CH_CUDA(ctx, cudaMemcpyAsync(dlo, seg_lo.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
         CH_CUDA(ctx, cudaMemcpyAsync(dpre, seg_pre.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
-        k_seg_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.start_ns, dlo, dpre, nseg, Mseg,
-                                                                     ctx->t0, tsbits, k1, v1);
-        CH_LAUNCHED(ctx);
-        bool alt;
-        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, tsbits + sb, &alt));
-        k_seg_scatter<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(alt ? v2 : v1, dlo, dpre, nseg, Mseg,
-                                                                        ctx->d_perm);
-        CH_LAUNCHED(ctx);
+        // stream-merge fast path (1-2 digit partition + binary-search ranks), else the full radix sort
+        bool merged = false;
+        {
+            const int64_t cells = (int64_t)nseg * SS_STREAMS;
+            unsigned int *cnt = CH_ALLOC(ctx, unsigned int, cells), *fail = CH_ALLOC(ctx, unsigned int, 1);
+            int64_t *c64 = CH_ALLOC(ctx, int64_t, cells), *cst = CH_ALLOC(ctx, int64_t, cells);
+            CH_ALLOC_END(ctx);
+            CH_CUDA(ctx, cudaMemsetAsync(cnt, 0, 4 * (size_t)cells, ctx->st));
+            CH_CUDA(ctx, cudaMemsetAsync(fail, 0, 4, ctx->st));
+            k_ss_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, dlo, dpre, nseg, Mseg,
+                                                                        k1, v1, cnt, fail);
+            CH_LAUNCHED(ctx);
+            bool alt2;
+            CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, sb + 8, &alt2));
+            unsigned long long *ksd = alt2 ? k2 : k1;
+            uint32_t *vsd = alt2 ? v2 : v1;
+            k_ss_check<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, fail);
+            CH_LAUNCHED(ctx);
+            k_u32_i64<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(cnt, c64, cells);
+            CH_LAUNCHED(ctx);
+            CH_TRY(ch_scan_excl_i64(ctx, c64, cst, cells, nullptr));
+            unsigned int hfail = 0;
+            CH_CUDA(ctx, cudaMemcpyAsync(&hfail, fail, 4, cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            if (!hfail) {
+                k_ss_rank<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, cnt, cst, dlo,
+                                                                            ctx->d_perm);
+                CH_LAUNCHED(ctx);
+                merged = true;
+            }
+        }
+        if (!merged) {
+            k_seg_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.start_ns, dlo, dpre, nseg,
+                                                                         Mseg, ctx->t0, tsbits, k1, v1);
+            CH_LAUNCHED(ctx);
+            bool alt;
+            CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, tsbits + sb, &alt));
+            k_seg_scatter<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(alt ? v2 : v1, dlo, dpre, nseg, Mseg,
+                                                                            ctx->d_perm);
+            CH_LAUNCHED(ctx);
+        }
         ctx->used = mk;
         ctx->full_sort = true;
         if (compute_resorted) {

@@ -20,8 +20,8 @@ constexpr int NT = 256;
 // scan of (has-head, tail-or-whole) over the tile (warp shuffles + warp carries).  The pass also checks
 // every value it reads -- the slot's column at every non-MEMOP event of the gpu, i.e. the whole column
 // -- for finiteness (R8), so a counter pass is read once.
-constexpr int CT_NT = 256, CT_IPT = 8, CT_TILE = CT_NT * CT_IPT, CT_SG = 8, CT_WARPS = CT_NT / 32;
-__global__ void __launch_bounds__(CT_NT) k_counters_tiled(const uint32_t *__restrict__ meta,
+constexpr int CT_NT = 256, CT_IPT = 8, CT_TILE = CT_NT * CT_IPT, CT_SG = 4, CT_WARPS = CT_NT / 32;
+__global__ void __launch_bounds__(CT_NT, 2) k_counters_tiled(const uint32_t *__restrict__ meta,
                                                           const int32_t *__restrict__ run_id,
                                                           const int32_t *__restrict__ nm_rank,
                                                           const int32_t *__restrict__ gpu_lg,
