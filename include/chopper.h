@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define CHOPPER_ABI_VERSION 3
+#define CHOPPER_ABI_VERSION 4
 
 typedef struct chopper_ctx chopper_ctx;
 typedef int32_t chopper_status;
@@ -182,6 +182,11 @@ typedef struct {
      * Quantiles interpolate linearly at h = q (n - 1) (R9). */
     int64_t n_report;
     double report[256 * 16];
+    /* end-to-end phase x op-type breakdown (O16, Fig. 4; R12): e2e[0] = number
+     * of (gpu, iteration) points; e2e[1 + 4 P + k], P = phase-span label 0..7, k = 0 vector / other,
+     * 1 gemm, 2 fa (summed instance durations, ns), 3 launch overhead (prep + call, ns): medians over the
+     * points (cells without instances count 0). */
+    double e2e[1 + 8 * 4];
 } chopper_global;
 
 /* Device-side report read back by chopper_load_columns (host struct). */

@@ -908,6 +908,46 @@ or_result *or_run(const or_input *in) {
         free(ord);
     }
 
+    /* ---------------- O16 end-to-end phase x op-type breakdown (Fig. 4) -----
+       Per traced gpu and sampled iteration (rank >= warmup, the iteration row exists): for each phase label
+       P in [0, 8) (the label of the phase span; instances of other labels are not counted) the summed
+       duration of its instances by op type T (0 vector / other incl. the unlabeled pseudo-ops, 1 gemm, 2 fa)
+       and the summed launch overhead (prep + call).  Row: 0 n_points, then for P = 0..7: median over the
+       points of [vec, gemm, fa, launch] (ns; cells without instances count 0) -- "median values across
+       iterations and GPUs" (Fig. 4 caption; R12). */
+    {
+        const int NP = 8;
+        int64_t npt = 0;
+        for (int64_t x = 0; x < n_itr; x++)
+            if (itr[x].r_it - 1 >= in->warmup && ((in->bd_gpu_mask >> itr[x].gpu) & 1ull)) npt++;
+        double *e2 = new_f64(r, "e2e.rows", 1 + NP * 4);
+        e2[0] = (double)npt;
+        int64_t *cell = (int64_t *)xcalloc((npt > 0 ? npt : 1) * NP * 4, 8);
+        int64_t w = 0;
+        for (int64_t x = 0; x < n_itr; x++) {
+            const row_t *it = &itr[x];
+            if (it->r_it - 1 < in->warmup || !((in->bd_gpu_mask >> it->gpu) & 1ull)) continue;
+            int64_t *c = &cell[w * NP * 4];
+            for (int64_t q = 0; q < n_inst; q++) {
+                const row_t *ins = &inst[q];
+                if (ins->gpu != it->gpu || ins->r_it != it->r_it || ins->ph < 0) continue;
+                const int P = in->span_label[ins->ph];
+                if (P < 0 || P >= NP) continue;
+                const int T = (ins->label >= 0 && in->op_type[ins->label] == 1) ? 1
+                            : (ins->label >= 0 && in->op_type[ins->label] == 2) ? 2 : 0;
+                c[P * 4 + T] += ins->busy;
+                c[P * 4 + 3] += ins->prep + ins->call;
+            }
+            w++;
+        }
+        int64_t *col = (int64_t *)xcalloc(npt > 0 ? npt : 1, 8);
+        for (int k = 0; k < NP * 4; k++) {
+            for (int64_t q = 0; q < npt; q++) col[q] = cell[q * NP * 4 + k];
+            e2[1 + k] = npt > 0 ? median_i64(col, npt) : NAN;
+        }
+        free(col); free(cell);
+    }
+
     /* per-event span indices are reported as caller indices (already) */
     for (int g = 0; g < G; g++) free(U[g]);
     free(U); free(nU); free(gbeg); free(gend); free(ord); free(rank1);

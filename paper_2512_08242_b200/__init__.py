@@ -113,7 +113,7 @@ class chopper_global(ctypes.Structure):
                 ("T", I64 * 4096), ("aligned_first", I64 * 4096), ("aligned_last", I64 * 4096),
                 ("throughput", F64 * 4096), ("throughput_median", F64), ("n_bd", I64), ("bd", F64 * (256 * 16)),
                 ("delta", I64 * 256), ("delta_flag", I32 * 256), ("max_skew_ag", I64), ("max_skew_rs", I64),
-                ("n_report", I64), ("report", F64 * (256 * 16))]
+                ("n_report", I64), ("report", F64 * (256 * 16)), ("e2e", F64 * 33)]
 
 
 class chopper_report(ctypes.Structure):

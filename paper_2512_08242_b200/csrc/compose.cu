@@ -19,11 +19,13 @@ namespace {
 constexpr int HDR = 4;          // gpu, present, has_samples, C
 constexpr int IT_W = 8;         // valid, step, busy, prep, call, n, first_ks, last_ke
 constexpr int PT_W = 9;         // valid, busy, launch, ovl, phi, cg, fp, un, ud
+constexpr int E2E_P = 8, E2E_W = E2E_P * 4;   // per iteration rank: [phase label][vec, gemm, fa, launch] (O16)
 
 struct Layout {
     int64_t MI, L, C, W;
     __host__ __device__ int64_t it_off() const { return HDR + C; }
     __host__ __device__ int64_t pt_off() const { return HDR + C + IT_W * MI; }
+    __host__ __device__ int64_t e2e_off() const { return HDR + C + IT_W * MI + PT_W * MI * L; }
 };
 
 __device__ __forceinline__ int64_t dbits(double d) { return __double_as_longlong(d); }
@@ -82,6 +84,29 @@ __global__ void k_dense_points(int64_t *blk, Layout Ly, int64_t n, const int32_t
     b[6] = dbits(s_fl >= 0 ? cnt[(int64_t)s_fl * cap + j] : 0.0);
     b[7] = dbits(s_un >= 0 ? cnt[(int64_t)s_un * cap + j] : 0.0);
     b[8] = dbits(s_ud >= 0 ? cnt[(int64_t)s_ud * cap + j] : 0.0);
+}
+
+// O16 cells: instance durations by (phase label, op type) and launch overhead by phase label, summed into
+// the gpu's iteration-rank row of the exchange block (integer atomics: exact in any order)
+__global__ void k_dense_e2e(int64_t *blk, Layout Ly, const int64_t *__restrict__ n_dev, const int32_t *__restrict__ gpu,
+                            const int32_t *__restrict__ rank, const int32_t *__restrict__ ph,
+                            const int32_t *__restrict__ label, const int64_t *__restrict__ f, int64_t cap,
+                            const int32_t *__restrict__ gpu_lg, const int32_t *__restrict__ span_label,
+                            const int32_t *__restrict__ op_type) {
+    const int64_t n = *n_dev;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = rank[j];
+        if (r < 0 || r >= Ly.MI || ph[j] < 0) continue;
+        const int P = span_label[ph[j]];
+        if (P < 0 || P >= E2E_P) continue;
+        const int lab = label[j];
+        const int T = lab >= 0 && op_type[lab] == 1 ? 1 : lab >= 0 && op_type[lab] == 2 ? 2 : 0;
+        int64_t *b = blk + (int64_t)gpu_lg[gpu[j]] * Ly.W + Ly.e2e_off() + r * E2E_W + P * 4;
+        const int64_t busy = f[(int64_t)RF_BUSY * cap + j];
+        const int64_t launch = f[(int64_t)RF_PREP * cap + j] + f[(int64_t)RF_CALL * cap + j];
+        if (busy) atomicAdd(reinterpret_cast<unsigned long long *>(b + T), (unsigned long long)busy);
+        if (launch) atomicAdd(reinterpret_cast<unsigned long long *>(b + 3), (unsigned long long)launch);
+    }
 }
 
 // ---- block-level helpers ----
@@ -487,6 +512,49 @@ __global__ void __launch_bounds__(512) k_cdf_write(const int64_t *__restrict__ b
     }
 }
 
+// O16 global: one block per cell; its values over the sampled (gpu, iteration) points of all gpus
+// (iteration rows present, rank >= warmup; cells without instances are 0), median by bitonic sort
+__global__ void __launch_bounds__(512) k_e2e(const int64_t *__restrict__ blk, Layout Ly, const int32_t *__restrict__ order,
+                                             int nslots, int warmup, int64_t maxp2, int64_t *__restrict__ wk,
+                                             double *__restrict__ out) {
+    extern __shared__ int64_t esh[];
+    const int k = blockIdx.x;                         // cell = P * 4 + {vec, gemm, fa, launch}
+    int64_t *w = wk ? wk + (int64_t)k * maxp2 : esh;
+    __shared__ int64_t scan_sm[33];
+    __shared__ int s_n;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    int nq = 0;
+    while (nq < nslots && order[nq] >= 0) nq++;
+    const int64_t r0 = warmup > 0 ? warmup : 0;
+    const int64_t nr = Ly.MI > r0 ? Ly.MI - r0 : 0;
+    const int64_t total = (int64_t)nq * nr;
+    for (int64_t c0 = 0; c0 < total; c0 += blockDim.x) {
+        const int64_t c = c0 + threadIdx.x;
+        bool ok = false;
+        int64_t v = 0;
+        if (c < total) {
+            const int64_t *b = blk + (int64_t)order[c / nr] * Ly.W;
+            const int64_t r = r0 + c % nr;
+            ok = b[1] != 0 && b[Ly.it_off() + r * IT_W] != 0;
+            v = b[Ly.e2e_off() + r * E2E_W + k];
+        }
+        int64_t tot;
+        const int64_t pos = block_excl_sum<512>(ok ? 1 : 0, &tot, scan_sm) + s_n;
+        if (ok && pos < maxp2) w[pos] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) s_n += (int)tot;
+        __syncthreads();
+    }
+    const int n = s_n < maxp2 ? s_n : (int)maxp2;
+    double m = NAN;
+    if (n > 0) m = med_i64(w, n, nullptr);
+    if (threadIdx.x == 0) {
+        out[1 + k] = m;
+        if (k == 0) out[0] = n;
+    }
+}
+
 // global iteration rows (a11): one thread per iteration rank of the reference gpu
 struct GlobArgs {
     const int64_t *blk;
@@ -622,7 +690,7 @@ static Layout layout_of(chopper_ctx *ctx) {
     Ly.MI = std::max(1, ctx->cfg.max_iters);
     Ly.L = std::max(1, ctx->cfg.n_labels);
     Ly.C = ctx->C;
-    Ly.W = HDR + Ly.C + IT_W * Ly.MI + PT_W * Ly.MI * Ly.L;
+    Ly.W = HDR + Ly.C + IT_W * Ly.MI + PT_W * Ly.MI * Ly.L + E2E_W * Ly.MI;
     return Ly;
 }
 
@@ -660,6 +728,12 @@ static chopper_status densify(chopper_ctx *ctx, int64_t **blk_out, int *slots_ou
             blk, Ly, ctx->point.n, ctx->point.gpu, ctx->point.rank, ctx->point.label, ctx->point.f, ctx->point.cnt,
             ctx->point.cap, ctx->d_gpu_lg, p.slot_gpu_cycles, p.slot_perf_flops, p.slot_util_num, p.slot_util_den,
             ovf);
+        CH_LAUNCHED(ctx);
+    }
+    if (ctx->inst.n > 0 && ctx->cfg.n_labels > 0) {
+        k_dense_e2e<<<(unsigned)std::min<int64_t>(ceil_div(ctx->inst.n, 256), 148 * 8), 256, 0, ctx->st>>>(
+            blk, Ly, ctx->inst.n_dev, ctx->inst.gpu, ctx->inst.rank, ctx->inst.ph, ctx->inst.label, ctx->inst.f,
+            ctx->inst.cap, ctx->d_gpu_lg, ctx->sp.label, ctx->d_op_type);
         CH_LAUNCHED(ctx);
     }
     ctx->d_dense_ovf = ovf;     // checked at chopper_reduce_ranks' read-back (no round trip here)
@@ -826,6 +900,19 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
         k_report<<<nL, 512, use_smem ? shb : 0, ctx->st>>>(RA);
         CH_LAUNCHED(ctx);
     }
+    // end-to-end phase x op-type medians (O16)
+    double *e2e = nullptr;
+    {
+        int64_t maxp = (int64_t)Ly.MI * ctx->cfg.n_traced_gpus, maxp2 = 1;
+        while (maxp2 < maxp) maxp2 <<= 1;
+        const bool sm_ok = 8 * maxp2 <= 48 * 1024;
+        CH_ALLOC_BEGIN;
+        e2e = CH_ALLOC(ctx, double, 1 + E2E_W);
+        int64_t *wk = sm_ok ? nullptr : CH_ALLOC(ctx, int64_t, (int64_t)E2E_W * maxp2);
+        CH_ALLOC_END(ctx);
+        k_e2e<<<E2E_W, 512, sm_ok ? 8 * maxp2 : 0, ctx->st>>>(all, Ly, ord, nslots, ctx->bd.warmup, maxp2, wk, e2e);
+        CH_LAUNCHED(ctx);
+    }
     // host copies
     int64_t n = 0;
     unsigned int hovf = 0;
@@ -850,6 +937,7 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     if (nbd > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->bd, bd, 8 * 16 * nbd, cudaMemcpyDeviceToHost, ctx->st));
     if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels in the report rows");
     out->n_report = nL;
+    CH_CUDA(ctx, cudaMemcpyAsync(out->e2e, e2e, 8 * (1 + E2E_W), cudaMemcpyDeviceToHost, ctx->st));
     if (nL > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->report, rep, 8 * 16 * (size_t)nL, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     for (int g = 0; g < ctx->cfg.n_traced_gpus && g < 256; g++) {

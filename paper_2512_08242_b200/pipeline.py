@@ -207,6 +207,7 @@ class Pipeline:
         o["glob.throughput_median"] = np.array([g.throughput_median])
         o["bd.rows"] = np.array(g.bd[:int(g.n_bd) * 16], np.float64)
         o["report.rows"] = np.array(g.report[:int(g.n_report) * 16], np.float64)
+        o["e2e.rows"] = np.array(g.e2e[:33], np.float64)
         if res.get("cdf") is not None:
             o["cdf.rows"] = res["cdf"].reshape(-1)
         G = self.cfg.n_traced_gpus

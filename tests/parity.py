@@ -92,6 +92,9 @@ def assert_parity(ref, got, per_event=True, tables=True, glob=True, bd=True):
             bad = np.nonzero(~np.isclose(a, b, rtol=FP_RTOL, atol=1e-12, equal_nan=True))[0] if a.shape == b.shape else []
             errs.append(f"report.rows differ at {bad[:8]}: ref {a[bad[:4]] if len(bad) else a.shape} "
                         f"got {b[bad[:4]] if len(bad) else b.shape}")
+        a, b = ref["e2e.rows"], got.get("e2e.rows", np.zeros(0))
+        if a.shape != b.shape or not np.allclose(a, b, rtol=0, atol=0, equal_nan=True):
+            errs.append(f"e2e.rows differ: ref {a[:9]} got {b[:9]}")
         if "cdf.rows" in got:
             a, b = ref["cdf.rows"], got["cdf.rows"]
             if a.shape != b.shape or not np.allclose(a, b, rtol=FP_RTOL, atol=1e-12, equal_nan=True):

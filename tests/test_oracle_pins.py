@@ -763,3 +763,39 @@ def test_cdf_invariants_generated(gen_small):
                 np.testing.assert_allclose(s[:, 4], np.arange(1, n + 1) / n, rtol=1e-15)
                 assert s[0, 2] == 1.0 and (np.diff(s[:, 2]) >= 0).all()
                 assert ((s[:, 3] >= 0) & (s[:, 3] <= 1)).all()
+
+
+def test_e2e_phase_optype_worked():
+    """O16 (Fig. 4 stacked bars): one gpu, one iteration, two phases; hand-summed cells.
+    P0: gemm op (kernels 100 + 50), fa op (70); P1: other op (30) + an unlabeled kernel (20, pseudo-op: vector).
+    Launch (Eqs. 1-3): gaps 0 (first kernel: none), 0, 50 in P0; 598730 and 10 in P1."""
+    tt = TinyTrace(labels=["g", "f", "v"])
+    tt.span(0, 0, 0, 10 ** 6, 0).span(0, 1, 0, 500_000, 0).span(0, 1, 500_000, 10 ** 6, 1)
+    tt.span(0, 3, 900, 1160, 0).span(0, 3, 1180, 1300, 1).span(0, 3, 599_000, 600_035, 2)
+    for ks, ke in ((1000, 1100), (1100, 1150), (1200, 1270), (600_000, 600_030), (600_040, 600_060)):
+        tt.ev(0, ks - 1, ks, ke)
+    b = tt.bundle()
+    o = oracle.run(b, params(b, op_type=np.array([1, 2, 0], np.int32), f_gemm=np.full(3, 1e9)))
+    e = o["e2e.rows"]
+    assert e[0] == 1
+    cells = e[1:].reshape(8, 4)      # [phase][vec, gemm, fa, launch]
+    np.testing.assert_array_equal(cells[0], [0, 150, 70, 50])
+    np.testing.assert_array_equal(cells[1], [50, 0, 0, 598_730 + 10])
+    np.testing.assert_array_equal(cells[2:], 0)
+
+
+def test_e2e_partitions_iteration_generated(gen_small):
+    """SPEC.md:491 invariant: the stacked segments partition the iteration (sum of vec / gemm / fa over phases
+    = iteration busy) -- checked on the single-point case of each gpu / iteration: with one sampled point
+    the medians are the point's own cells."""
+    for b, o in gen_small:
+        p = oracle.default_params(b)
+        # restrict to one gpu and the last iteration: warmup = last rank, gpu mask = gpu 0
+        last = int(o["iter.rank"][o["iter.gpu"] == 0].max())
+        o1 = oracle.run(b, dict(p, warmup=last), gpu_mask=1)
+        e = o1["e2e.rows"]
+        assert e[0] == 1
+        cells = e[1:].reshape(8, 4)
+        row = (o1["iter.gpu"] == 0) & (o1["iter.rank"] == last)
+        assert cells[:, :3].sum() == o1["iter.busy"][row][0]
+        assert cells[:, 3].sum() == o1["iter.prep"][row][0] + o1["iter.call"][row][0]
