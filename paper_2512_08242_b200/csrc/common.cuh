@@ -297,6 +297,19 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+// asynchronous global -> shared copies (cp.async, L2 -> SMEM without registers)
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
 
 // record a validation violation (count + smallest index)
 __device__ __forceinline__ void viol(DevReport *r, int rule, int64_t idx) {

@@ -533,14 +533,6 @@ __device__ __forceinline__ void smp_F(SmpCache &c, const EvParams &P, int64_t t,
 __device__ __forceinline__ int sw64(int t, int j) { return t * 4 + (j ^ ((t >> 1) & 3)); }
 __device__ __forceinline__ int sw32(int t, int j) { return t * 2 + (j ^ ((t >> 2) & 1)); }
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
 
 constexpr int EV_WARPS = EV_NT / 32;
 struct EvSmem {

@@ -15,21 +15,35 @@ namespace {
 constexpr int NT = 256;
 
 // counter sums of each sub-run over its COMPUTE events, tiled like the event pass (2048 events per
-// block, 8 consecutive per thread; sub-runs never cross tiles), CT_SG slots per launch.  Each thread
-// folds its 8 events sequentially (input order); runs that span threads are completed by a segmented
-// scan of (has-head, tail-or-whole) over the tile (warp shuffles + warp carries).  The pass also checks
-// every value it reads -- the slot's column at every non-MEMOP event of the gpu, i.e. the whole column
-// -- for finiteness (R8), so a counter pass is read once.
+// block, 8 consecutive per thread; sub-runs never cross tiles).  A counter pass enumerates the gpu's
+// non-MEMOP kernels in dispatch order (D2), so when a tile holds one gpu its counter values are one
+// contiguous rank range [nlo, nhi] of each column: it is staged into shared memory with coalesced
+// cp.async (no register round trip, all slots' copies in flight together) and each thread then reads
+// its own events' values from SMEM.  Tiles that straddle two gpus gather from global memory instead.
+// Each thread folds its 8 events sequentially (input order); runs that span threads are completed by
+// a segmented scan of (has-head, tail-or-whole) over the tile (warp shuffles + warp carries).  The
+// pass also checks every value it reads -- the slot's column at every non-MEMOP event of the gpu,
+// i.e. the whole column -- for finiteness (R8), so a counter pass is read once.  Slot groups of CT_SG
+// are processed in turn by the same block (the tile's event metadata is read once).
 constexpr int CT_NT = 256, CT_IPT = 8, CT_TILE = CT_NT * CT_IPT, CT_SG = 4, CT_WARPS = CT_NT / 32;
-__global__ void __launch_bounds__(CT_NT, 2) k_counters_tiled(const uint32_t *__restrict__ meta,
+// staged element j (tile-relative rank) lives at j ^ ((j >> 4) & 7): the 32 lanes of a warp read
+// elements 8 apart (one per thread-blocked event), which this spreads over all banks (2 wavefronts)
+__device__ __forceinline__ int ct_sw(int j) { return j ^ ((j >> 4) & 7); }
+struct CtSmem {
+    double x[CT_SG][CT_TILE];                 // 64 KB
+    double agg[CT_WARPS][CT_SG], carry[CT_WARPS][CT_SG];
+    int aflag[CT_WARPS];
+    int red[4][CT_WARPS];
+};
+__global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__restrict__ meta,
                                                           const int32_t *__restrict__ run_id,
                                                           const int32_t *__restrict__ nm_rank,
                                                           const int32_t *__restrict__ gpu_lg,
-                                                          const double *const *__restrict__ col, int C, int s0,
+                                                          const double *const *__restrict__ col, int C,
                                                           int64_t N, double *__restrict__ out, int64_t cap,
                                                           unsigned int *__restrict__ colbad, int vec_ok) {
-    __shared__ double s_agg[CT_WARPS][CT_SG], s_carry[CT_WARPS][CT_SG];
-    __shared__ int s_aflag[CT_WARPS];
+    extern __shared__ __align__(16) unsigned char ct_dsm[];
+    CtSmem &S = *reinterpret_cast<CtSmem *>(ct_dsm);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * CT_TILE, i0 = base + (int64_t)tid * CT_IPT;
     const int nv = i0 >= N ? 0 : (int)min((int64_t)CT_IPT, N - i0);
@@ -49,7 +63,7 @@ __global__ void __launch_bounds__(CT_NT, 2) k_counters_tiled(const uint32_t *__r
 #pragma unroll
         for (int k = 0; k < CT_IPT; k++) {
             bool ok = k < nv;
-            mt[k] = ok ? meta[i0 + k] : (uint32_t)CK_MEMOP;
+            mt[k] = ok ? meta[i0 + k] : (uint32_t)CK_MEMOP;     // (invalid events carry MEMOP)
             rid[k] = ok ? run_id[i0 + k] : -1;
             nm[k] = ok ? nm_rank[i0 + k] : 0;
         }
@@ -60,117 +74,164 @@ __global__ void __launch_bounds__(CT_NT, 2) k_counters_tiled(const uint32_t *__r
     for (int k = 0; k < CT_IPT; k++)
         if (k < nv && (k == 0 ? (tid == 0 || rid[0] != prev) : rid[k] != rid[k - 1])) hmask |= 1u << k;
     const bool has = hmask != 0;
-    // all counter values of the thread first (independent loads in flight), then the folds
-    double x[CT_SG][CT_IPT];
-    int lgp = -1;
-    const double *cp[CT_SG];
-#pragma unroll
-    for (int q = 0; q < CT_SG; q++) cp[q] = nullptr;
-#pragma unroll
-    for (int k = 0; k < CT_IPT; k++) {
-        const uint32_t m = mt[k];
-        const bool rd = k < nv && kind_of(m) != CK_MEMOP;
-        const int lg = rd ? gpu_lg[gpu_of(m)] : lgp;
-        if (rd && lg != lgp) {
-#pragma unroll
-            for (int q = 0; q < CT_SG; q++) cp[q] = s0 + q < C ? col[lg * C + s0 + q] : nullptr;
-            lgp = lg;
-        }
-#pragma unroll
-        for (int q = 0; q < CT_SG; q++) x[q][k] = (rd && cp[q]) ? __ldg(cp[q] + nm[k]) : 0.0;
-    }
-    double cur[CT_SG], p0[CT_SG];
-#pragma unroll
-    for (int q = 0; q < CT_SG; q++) {
-        cur[q] = 0.0;
-        p0[q] = 0.0;
-        const int s = s0 + q;
-        if (s >= C) continue;
-        double c = 0.0;
-        bool seen = false, bad = false;
+    // the tile's gpu range and counter-rank range over its non-MEMOP events
+    int lmin = INT_MAX, lmax = -1, nmin = INT_MAX, nmax = -1;
+    {
+        int gp = -1, lg = -1;
 #pragma unroll
         for (int k = 0; k < CT_IPT; k++) {
-            if ((hmask >> k) & 1u) {          // (heads only at valid events)
-                if (!seen) { p0[q] = c; seen = true; }
-                else out[(int64_t)s * cap + rid[k > 0 ? k - 1 : 0]] = c;
-                c = 0.0;
-            }
-            const int kd = kind_of(mt[k]);    // (invalid events carry MEMOP)
-            if (kd != CK_MEMOP) {
-                bad |= !isfinite(x[q][k]);
-                if (kd == CK_COMPUTE) c += x[q][k];
-            }
+            if (kind_of(mt[k]) == CK_MEMOP) continue;
+            const int g = gpu_of(mt[k]);
+            if (g != gp) { lg = gpu_lg[g]; gp = g; }
+            lmin = min(lmin, lg); lmax = max(lmax, lg);
+            nmin = min(nmin, nm[k]); nmax = max(nmax, nm[k]);
         }
-        if (bad) {
 #pragma unroll
-            for (int k = 0; k < CT_IPT; k++)
-                if (kind_of(mt[k]) != CK_MEMOP && !isfinite(x[q][k])) atomicOr(&colbad[gpu_lg[gpu_of(mt[k])] * C + s], 1u);
+        for (int o = 16; o > 0; o >>= 1) {
+            lmin = min(lmin, __shfl_xor_sync(CH_FULL, lmin, o));
+            lmax = max(lmax, __shfl_xor_sync(CH_FULL, lmax, o));
+            nmin = min(nmin, __shfl_xor_sync(CH_FULL, nmin, o));
+            nmax = max(nmax, __shfl_xor_sync(CH_FULL, nmax, o));
         }
-        cur[q] = c;
+        if (lane == 0) { S.red[0][warp] = lmin; S.red[1][warp] = lmax; S.red[2][warp] = nmin; S.red[3][warp] = nmax; }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < CT_WARPS; w++) {
+            lmin = min(lmin, S.red[0][w]); lmax = max(lmax, S.red[1][w]);
+            nmin = min(nmin, S.red[2][w]); nmax = max(nmax, S.red[3][w]);
+        }
     }
-    // segmented inclusive scan of (has, cur) inside the warp
-    bool f = has;
-    double v[CT_SG];
-#pragma unroll
-    for (int q = 0; q < CT_SG; q++) v[q] = cur[q];
-    if (!__all_sync(CH_FULL, has)) {
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            bool pf = __shfl_up_sync(CH_FULL, f, o);
+    const bool staged = lmax >= 0 && lmin == lmax;      // block-uniform
+    const int nlo = nmin, ncnt = nmax - nmin + 1;
+    for (int s0 = 0; s0 < C; s0 += CT_SG) {
+        unsigned cpm = 0;                     // slots with a staged column
+        if (staged) {
 #pragma unroll
             for (int q = 0; q < CT_SG; q++) {
-                double pv = __shfl_up_sync(CH_FULL, v[q], o);
-                if (lane >= o && !f) v[q] = pv + v[q];
+                const double *cp = s0 + q < C ? col[lmin * C + s0 + q] : nullptr;
+                if (cp) {
+                    cpm |= 1u << q;
+                    for (int j = tid; j < ncnt; j += CT_NT) cp_async8(&S.x[q][ct_sw(j)], cp + nlo + j);
+                }
             }
-            if (lane >= o) f = f || pf;
+            cp_async_wait_all();
+            __syncthreads();
         }
-    }
-    if (lane == 31) {
-        s_aflag[warp] = f;
+        double c[CT_SG], p0[CT_SG];
+        unsigned bad = 0;
+        bool seen = false;
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++) s_agg[warp][q] = v[q];
-    }
-    __syncthreads();
-    if (tid < CT_WARPS) {
-        double c[CT_SG];
-        int cf = 0;
+        for (int q = 0; q < CT_SG; q++) { c[q] = 0.0; p0[q] = 0.0; }
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++) c[q] = 0.0;
-        for (int w = 0; w < tid; w++) {
+        for (int k = 0; k < CT_IPT; k++) {
+            if ((hmask >> k) & 1u) {          // (heads only at valid events; k > 0 once seen)
+                if (!seen) {
 #pragma unroll
-            for (int q = 0; q < CT_SG; q++) c[q] = s_aflag[w] ? s_agg[w][q] : c[q] + s_agg[w][q];
-            cf |= s_aflag[w];
+                    for (int q = 0; q < CT_SG; q++) p0[q] = c[q];
+                    seen = true;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < CT_SG; q++)
+                        if (s0 + q < C) out[(int64_t)(s0 + q) * cap + rid[k > 0 ? k - 1 : 0]] = c[q];
+                }
+#pragma unroll
+                for (int q = 0; q < CT_SG; q++) c[q] = 0.0;
+            }
+            const int kd = kind_of(mt[k]);
+            const bool rd = kd != CK_MEMOP;
+            double v[CT_SG];
+            if (staged) {
+                const int j = ct_sw(nm[k] - nlo);
+#pragma unroll
+                for (int q = 0; q < CT_SG; q++) v[q] = rd && ((cpm >> q) & 1u) ? S.x[q][j] : 0.0;
+            } else {                          // tile straddles two gpus (rare): gather from the columns
+                const int lg = rd ? gpu_lg[gpu_of(mt[k])] : 0;
+#pragma unroll
+                for (int q = 0; q < CT_SG; q++) {
+                    const double *p = rd && s0 + q < C ? col[lg * C + s0 + q] : nullptr;
+                    v[q] = p ? __ldg(p + nm[k]) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++) {
+                if (!isfinite(v[q])) bad |= 1u << q;
+                if (kd == CK_COMPUTE) c[q] += v[q];
+            }
         }
+        if (bad) {                            // rare: flag the columns holding the non-finite values (R8)
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++) s_carry[tid][q] = c[q];
-    }
-    __syncthreads();
-    bool ef = __shfl_up_sync(CH_FULL, f, 1);
-    double e[CT_SG];
+            for (int k = 0; k < CT_IPT; k++) {
+                if (kind_of(mt[k]) == CK_MEMOP) continue;
+                const int lg = gpu_lg[gpu_of(mt[k])];
+                for (int q = 0; q < CT_SG; q++) {
+                    const double *p = s0 + q < C ? col[lg * C + s0 + q] : nullptr;
+                    if (((bad >> q) & 1u) && p && !isfinite(p[nm[k]])) atomicOr(&colbad[lg * C + s0 + q], 1u);
+                }
+            }
+        }
+        // segmented inclusive scan of (has, c) inside the warp
+        bool f = has;
+        double v[CT_SG];
 #pragma unroll
-    for (int q = 0; q < CT_SG; q++) e[q] = __shfl_up_sync(CH_FULL, v[q], 1);
-    if (lane == 0) {
-        ef = false;
+        for (int q = 0; q < CT_SG; q++) v[q] = c[q];
+        if (!__all_sync(CH_FULL, has)) {
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++) e[q] = 0.0;
-    }
-    if (!ef) {
+            for (int o = 1; o < 32; o <<= 1) {
+                bool pf = __shfl_up_sync(CH_FULL, f, o);
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++) e[q] = s_carry[warp][q] + e[q];
-    }
-    // the run ending in this thread's first piece (or at the end of the previous thread)
-    if (has && tid > 0) {
+                for (int q = 0; q < CT_SG; q++) {
+                    double pv = __shfl_up_sync(CH_FULL, v[q], o);
+                    if (lane >= o && !f) v[q] = pv + v[q];
+                }
+                if (lane >= o) f = f || pf;
+            }
+        }
+        if (lane == 31) {
+            S.aflag[warp] = f;
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++)
-            if (s0 + q < C) out[(int64_t)(s0 + q) * cap + prev] = e[q] + p0[q];
-    }
-    // the run open at the end of the tile
-    if (tid == CT_NT - 1 && base < N) {
-        const int64_t last = base + CT_TILE - 1 < N ? base + CT_TILE - 1 : N - 1;
-        const int32_t id = run_id[last];
+            for (int q = 0; q < CT_SG; q++) S.agg[warp][q] = v[q];
+        }
+        __syncthreads();
+        if (tid < CT_WARPS) {
+            double cc[CT_SG];
 #pragma unroll
-        for (int q = 0; q < CT_SG; q++)
-            if (s0 + q < C) out[(int64_t)(s0 + q) * cap + id] = f ? v[q] : s_carry[warp][q] + v[q];
+            for (int q = 0; q < CT_SG; q++) cc[q] = 0.0;
+            for (int w = 0; w < tid; w++) {
+#pragma unroll
+                for (int q = 0; q < CT_SG; q++) cc[q] = S.aflag[w] ? S.agg[w][q] : cc[q] + S.agg[w][q];
+            }
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++) S.carry[tid][q] = cc[q];
+        }
+        __syncthreads();
+        bool ef = __shfl_up_sync(CH_FULL, f, 1);
+        double e[CT_SG];
+#pragma unroll
+        for (int q = 0; q < CT_SG; q++) e[q] = __shfl_up_sync(CH_FULL, v[q], 1);
+        if (lane == 0) {
+            ef = false;
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++) e[q] = 0.0;
+        }
+        if (!ef) {
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++) e[q] = S.carry[warp][q] + e[q];
+        }
+        // the run ending in this thread's first piece (or at the end of the previous thread)
+        if (has && tid > 0) {
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++)
+                if (s0 + q < C) out[(int64_t)(s0 + q) * cap + prev] = e[q] + p0[q];
+        }
+        // the run open at the end of the tile
+        if (tid == CT_NT - 1 && base < N) {
+            const int64_t last = base + CT_TILE - 1 < N ? base + CT_TILE - 1 : N - 1;
+            const int32_t id = run_id[last];
+#pragma unroll
+            for (int q = 0; q < CT_SG; q++)
+                if (s0 + q < C) out[(int64_t)(s0 + q) * cap + id] = f ? v[q] : S.carry[warp][q] + v[q];
+        }
+        __syncthreads();                      // S.x / S.carry reused by the next slot group
     }
 }
 
@@ -1015,12 +1076,12 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         CH_ALLOC_END(ctx);
         CH_CUDA(ctx, cudaMemsetAsync(ctx->d_colbad, 0, 4 * (size_t)n_lg * C, ctx->st));
         const int vec_ok = (((uintptr_t)ctx->ev.meta | (uintptr_t)ctx->d_run_id | (uintptr_t)ctx->d_nm_rank) & 15u) == 0;
-        for (int s0 = 0; s0 < C; s0 += CT_SG) {
-            k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, 0, ctx->st>>>(
-                ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, s0, ctx->N, subv.cnt,
-                subv.ccap, ctx->d_colbad, vec_ok);
-            CH_LAUNCHED(ctx);
-        }
+        CH_CUDA(ctx, cudaFuncSetAttribute(k_counters_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(CtSmem)));
+        k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->st>>>(
+            ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, ctx->N, subv.cnt, subv.ccap,
+            ctx->d_colbad, vec_ok);
+        CH_LAUNCHED(ctx);
     }
     // instances: sort of sub-runs by key, then groups of equal keys
     unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, R + 1), *k2 = CH_ALLOC(ctx, unsigned long long, R + 1);
