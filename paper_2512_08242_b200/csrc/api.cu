@@ -22,7 +22,7 @@ size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_
     int64_t K = cfg->max_coll_per_class > 0 ? cfg->max_coll_per_class : 1;
     size_t b = 0;
     b += (size_t)N * (420 + 40 * C);         // sort buffers, chain, unions, sub-runs, instance tables
-    b += (size_t)S * 160;                    // push-order span arrays + sort buffers
+    b += (size_t)S * 192;                    // push-order span arrays + sort buffers + Euler tables
     b += (size_t)M * 64;                     // sample prefixes
     b += (size_t)G * (4 + 4 * K) * 8 * 2;    // clock-offset exchange
     b += (size_t)G * (8 + C + 8 * MI + 9 * MI * L) * 8 * 2;   // dense row exchange

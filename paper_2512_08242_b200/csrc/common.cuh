@@ -123,6 +123,25 @@ struct chopper_ctx {
     int32_t *d_list_flags = nullptr; // [n_lg*4] 1 = non-laminar
     std::vector<int32_t> list_flags;
     int32_t *d_attr_pre = nullptr;   // [4][N] precomputed (non-laminar lists)
+    // Euler boundary tables (all lists laminar): per list, the time-ordered span endpoints with the innermost
+    // owner after each one (rank + 1, 0 = none); list l occupies [2*list_beg[l] + l, 2*list_beg[l+1] + l + 1)
+    int64_t *ET_t = nullptr;
+    int32_t *ET_c = nullptr;
+    int64_t *d_et_beg = nullptr;     // [n_lg*4 + 1]
+    bool et_ok = false;
+    // combined key table (et_ok): per lg, the four levels' Euler entries merged by time, each with the full
+    // instance key after it; lg occupies [kt_beg[lg], kt_beg[lg+1]), entry 0 = (-inf, invalid)
+    int64_t *KT_t = nullptr;
+    unsigned long long *KT_k = nullptr;
+    int64_t *d_kt_beg = nullptr;     // [n_lg + 1]
+    // timeline (et_ok): per lg, comm-union boundaries and samples merged by time with the coverage and the
+    // frequency / power prefix integrals as affine functions of (t - t0) after each entry
+    int64_t *TL_t = nullptr;
+    int64_t *TL_v = nullptr;         // [3][cap]: coverage, frequency and power intercepts
+    int32_t *TL_s = nullptr;         // [3][cap]: in-union flag, f, p slopes
+    int64_t *d_tl_beg = nullptr;     // [n_lg + 1] capacity layout
+    int64_t *d_tl_len = nullptr;     // [n_lg] entries in use
+    int64_t tl_cap = 0;
     int kb[4] = {0, 0, 0, 0};        // key bits per level
     int kg = 0;                      // key bits for lg
     int64_t max_it_list = 0;         // longest iteration-span list of a local gpu (iteration ranks < this)
@@ -305,6 +324,10 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n" ::);

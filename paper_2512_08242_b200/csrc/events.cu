@@ -148,6 +148,85 @@ __global__ void k_smp_terms(const int32_t *__restrict__ g, const int64_t *__rest
     head[k] = (k == 0) || g[k - 1] != g[k];
 }
 
+
+// ---- timeline: comm-union boundaries and samples of a gpu merged by time (window-staged event pass) ----
+// Entry j of gpu lg holds, for every t from its time up to the next entry's: coverage cov(t) = V0 + S0*(t - t0),
+// frequency integral F(t) = V1 + S1*(t - t0) and power integral Pw(t) = V2 + S2*(t - t0) (MHz*ns, mW*ns; the
+// prefix integrals of the zero-order hold, D10).  Intercepts wrap modulo 2^64 like the prefix sums they come
+// from, so differences F(t_ke) - F(t_ks) are the exact int64 integrals.  Ties: union entries before samples.
+__global__ void k_timeline(const int64_t *__restrict__ tl_beg, const int64_t *__restrict__ ncomm, int n_lg,
+                           int64_t cap_total, const int64_t *__restrict__ Us, const int64_t *__restrict__ Ue,
+                           const int64_t *__restrict__ UP, const int64_t *__restrict__ Ubeg,
+                           const int64_t *__restrict__ Ucnt, const int64_t *__restrict__ ts,
+                           const int64_t *__restrict__ phi, const int64_t *__restrict__ psi,
+                           const int32_t *__restrict__ sf, const int32_t *__restrict__ sp,
+                           const int64_t *__restrict__ slo_a, const int64_t *__restrict__ shi_a, int64_t T0,
+                           int64_t cap, int64_t *__restrict__ Tt, int64_t *__restrict__ Tv, int32_t *__restrict__ Ts,
+                           int64_t *__restrict__ tl_len) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= cap_total) return;
+    int l = 0, h = n_lg;
+    while (h - l > 1) {
+        const int m = (l + h) >> 1;
+        if (tl_beg[m] <= j) l = m; else h = m;
+    }
+    const int lg = l;
+    const int64_t beg = tl_beg[lg], a = j - beg, nc = ncomm[lg];
+    const int64_t ub = Ubeg[lg], U = Ucnt[lg], slo = slo_a[lg], shi = shi_a[lg];
+    int64_t t, pos;
+    if (a == 0) {
+        t = INT64_MIN;
+        pos = beg;
+        tl_len[lg] = 1 + 2 * U + (shi - slo);
+    } else if (a - 1 < 2 * nc) {
+        const int64_t u = (a - 1) >> 1, e = (a - 1) & 1;
+        if (u >= U) return;
+        t = e ? Ue[ub + u] : Us[ub + u];
+        int64_t l2 = slo, h2 = shi;                  // samples strictly before t
+        while (l2 < h2) {
+            const int64_t m = (l2 + h2) >> 1;
+            if (ts[m] < t) l2 = m + 1; else h2 = m;
+        }
+        pos = beg + 1 + 2 * u + e + (l2 - slo);
+    } else {
+        const int64_t b = a - 1 - 2 * nc;
+        if (b >= shi - slo) return;
+        t = ts[slo + b];
+        const int64_t uu = last_le(Us, ub, ub + U, t);
+        const int64_t cu = uu < ub ? 0 : 2 * (uu - ub + 1) - (Ue[uu] > t ? 1 : 0);   // union entries at or before t
+        pos = beg + 1 + b + cu;
+    }
+    // state after the entry
+    unsigned long long c0 = 0, c1 = 0, c2 = 0;
+    int32_t inu = 0, f = 0, pw = 0;
+    const int64_t uu = last_le(Us, ub, ub + U, t);
+    if (uu >= ub) {
+        const int64_t s0 = Us[uu], e0 = Ue[uu];
+        if (t < e0) {
+            inu = 1;
+            c0 = (unsigned long long)UP[uu] - (unsigned long long)(s0 - T0);
+        } else {
+            c0 = (unsigned long long)UP[uu] + (unsigned long long)(e0 - s0);
+        }
+    }
+    if (shi > slo) {
+        int64_t q = last_le(ts, slo, shi, t);
+        if (q < slo) q = slo;                        // before the first sample: f_0 extended backwards (D10)
+        f = sf[q];
+        pw = sp[q];
+        const unsigned long long dq = (unsigned long long)(ts[q] - T0);
+        c1 = (unsigned long long)phi[q] - (unsigned long long)(int64_t)f * dq;
+        c2 = (unsigned long long)psi[q] - (unsigned long long)(int64_t)pw * dq;
+    }
+    Tt[pos] = t;
+    Tv[pos] = (int64_t)c0;
+    Tv[cap + pos] = (int64_t)c1;
+    Tv[2 * cap + pos] = (int64_t)c2;
+    Ts[pos] = inu;
+    Ts[cap + pos] = f;
+    Ts[2 * cap + pos] = pw;
+}
+
 // ---- compute-union keys for multi-stream gpus -----------------------------------------------------
 __global__ void k_vkeys(const uint32_t *__restrict__ meta, const int64_t *__restrict__ ks, int64_t n,
                         const int32_t *__restrict__ gpu_lg, int64_t t0, int tsbits, int lgbits,
@@ -190,6 +269,17 @@ struct EvParams {
     int64_t cap;
     unsigned long long *tile_state;
     unsigned int *ticket;
+    // window-staged pass: combined key table, timeline and per-tile seeds
+    const int64_t *KTt;
+    const unsigned long long *KTk;
+    const int64_t *kt_beg;
+    const int64_t *TLt, *TLv;
+    const int32_t *TLs;
+    const int64_t *tl_beg, *tl_len;
+    int64_t tl_cap, t0;
+    const int32_t *seeds;
+    int64_t ntile;
+    const int64_t *tile_base;     // [ntile + 1] first sub-run id of each tile
 };
 
 
@@ -588,6 +678,124 @@ __device__ __forceinline__ void stage_tile(EvSmem &S, const EvParams &P, int64_t
     __syncthreads();
 }
 
+
+// ---- sub-run heads: the tile start is always a head (sub-runs never cross tiles); block exclusive scan of
+// the per-thread head counts.  Keys of the tile are in S.key (written before the call).
+__device__ __forceinline__ int tile_head_scan(EvSmem &S, unsigned &hmask, int nv, int *tot_out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __syncthreads();
+    if (nv > 0 && (tid == 0 || S.key[0][tid] != S.key[EV_IPT - 1][tid - 1])) hmask |= 1u;
+    const int nh = __popc(hmask);
+    int wex = nh;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(CH_FULL, wex, o);
+        if (lane >= o) wex += y;
+    }
+    if (lane == 31) S.wheads[warp] = wex;
+    wex -= nh;
+    __syncthreads();
+    int wbase = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < EV_WARPS; w++) {
+        int c = S.wheads[w];
+        if (w < warp) wbase += c;
+        tot += c;
+    }
+    *tot_out = tot;
+    return wbase + wex;
+}
+
+// ---- decoupled look-back (warp 0, 32 predecessors per probe): global id of the tile's first head ----
+__device__ __forceinline__ void tile_lookback(EvSmem &S, const EvParams &P, int64_t tile, int tot) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        int64_t excl = 0;
+        if (tile == 0) {
+            if (lane == 0) atomicExch(&P.tile_state[0], FLAG_P | (unsigned long long)tot);
+        } else {
+            if (lane == 0) atomicExch(&P.tile_state[tile], FLAG_A | (unsigned long long)tot);
+            int64_t p = tile - 1 - lane;
+            while (true) {
+                unsigned long long s = (unsigned long long)FLAG_P;
+                if (p >= 0) s = *((volatile unsigned long long *)&P.tile_state[p]);
+                unsigned fl = (unsigned)(s >> 62);
+                unsigned pm = __ballot_sync(CH_FULL, fl == 2u), zm = __ballot_sync(CH_FULL, fl == 0u);
+                int fp = pm ? __ffs(pm) - 1 : 32;
+                unsigned need = fp >= 31 ? CH_FULL : ((2u << fp) - 1u);
+                if (zm & need) continue;                       // a predecessor has not published yet
+                int64_t v = lane <= fp ? (int64_t)(s & VAL_MASK) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CH_FULL, v, o);
+                excl += v;
+                if (fp < 32) break;
+                p -= 32;
+            }
+            if (lane == 0) atomicExch(&P.tile_state[tile], FLAG_P | (unsigned long long)(excl + tot));
+        }
+        if (lane == 0) { S.excl = excl; S.tot = tot; }
+    }
+    __syncthreads();
+}
+
+// ---- runs that span threads: segmented inclusive scan of (has, tail-or-whole) over the tile ----
+__device__ __forceinline__ void tile_finish(EvSmem &S, const EvParams &P, bool has, const Acc &cur, const Acc &p0,
+                                            int64_t run0, int64_t base) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t N = P.N;
+    bool f = has;
+    Acc v = cur;
+    if (!__all_sync(CH_FULL, has)) {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            Acc pv = v.shfl_up(o);
+            bool pf = __shfl_up_sync(CH_FULL, f, o);
+            if (lane >= o) {
+                if (!f) { pv.merge(v); v = pv; }
+                f = f || pf;
+            }
+        }
+    }
+    if (lane == 31) { S.wagg[warp] = v; S.wflag[warp] = f; }
+    __syncthreads();
+    if (tid < EV_WARPS) {                 // carry into warp tid: segmented combine of earlier warps
+        Acc c;
+        c.zero();
+        int cf = 0;
+        for (int w = 0; w < tid; w++) {
+            if (S.wflag[w]) { c = S.wagg[w]; cf = 1; }
+            else c.merge(S.wagg[w]);
+        }
+        S.wcarry[tid] = c;
+        S.wcflag[tid] = cf;
+    }
+    __syncthreads();
+    // exclusive value at this thread: warp-exclusive, completed with the warp carry if no head precedes
+    Acc e = v.shfl_up(1);
+    bool ef = __shfl_up_sync(CH_FULL, f, 1);
+    if (lane == 0) { e.zero(); ef = false; }
+    if (!ef) {
+        Acc c = S.wcarry[warp];
+        c.merge(e);
+        e = c;
+    }
+    // the run that ends in this thread's first piece (or at the end of the previous thread)
+    if (has && tid > 0) {
+        e.merge(p0);
+        write_subrun(P, run0 - 1, e, base);
+    }
+    // the run open at the end of the tile
+    if (tid == EV_NT - 1 && base < N) {
+        Acc last = v;
+        if (!f) {
+            Acc c = S.wcarry[warp];
+            c.merge(v);
+            last = c;
+        }
+        write_subrun(P, S.excl + S.tot - 1, last, base);
+    }
+}
+
 // the fused pass: one 2048-event tile per block, 8 consecutive events per thread
 __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
     extern __shared__ __align__(16) unsigned char ev_dsm[];
@@ -683,56 +891,9 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
             prevk = kk;
         }
     }
-    __syncthreads();
-    // the tile start is always a head (sub-runs never cross tiles)
-    if (nv > 0 && (tid == 0 || S.key[0][tid] != S.key[EV_IPT - 1][tid - 1])) hmask |= 1u;
-    const int nh = __popc(hmask);
-    // block exclusive scan of head counts (int32)
-    int wex = nh;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(CH_FULL, wex, o);
-        if (lane >= o) wex += y;
-    }
-    if (lane == 31) S.wheads[warp] = wex;
-    wex -= nh;
-    __syncthreads();
-    int wbase = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < EV_WARPS; w++) {
-        int c = S.wheads[w];
-        if (w < warp) wbase += c;
-        tot += c;
-    }
-    const int ex = wbase + wex;           // heads before this thread in the tile
-    // ---- decoupled look-back (warp 0, 32 predecessors per probe): global id of the tile's first head ----
-    if (warp == 0) {
-        int64_t excl = 0;
-        if (tile == 0) {
-            if (lane == 0) atomicExch(&P.tile_state[0], FLAG_P | (unsigned long long)tot);
-        } else {
-            if (lane == 0) atomicExch(&P.tile_state[tile], FLAG_A | (unsigned long long)tot);
-            int64_t p = tile - 1 - lane;
-            while (true) {
-                unsigned long long s = (unsigned long long)FLAG_P;
-                if (p >= 0) s = *((volatile unsigned long long *)&P.tile_state[p]);
-                unsigned fl = (unsigned)(s >> 62);
-                unsigned pm = __ballot_sync(CH_FULL, fl == 2u), zm = __ballot_sync(CH_FULL, fl == 0u);
-                int fp = pm ? __ffs(pm) - 1 : 32;
-                unsigned need = fp >= 31 ? CH_FULL : ((2u << fp) - 1u);
-                if (zm & need) continue;                       // a predecessor has not published yet
-                int64_t v = lane <= fp ? (int64_t)(s & VAL_MASK) : 0;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CH_FULL, v, o);
-                excl += v;
-                if (fp < 32) break;
-                p -= 32;
-            }
-            if (lane == 0) atomicExch(&P.tile_state[tile], FLAG_P | (unsigned long long)(excl + tot));
-        }
-        if (lane == 0) { S.excl = excl; S.tot = tot; }
-    }
-    __syncthreads();
+    int tot;
+    const int ex = tile_head_scan(S, hmask, nv, &tot);   // heads before this thread in the tile
+    tile_lookback(S, P, tile, tot);
     const int64_t run0 = S.excl + ex;     // global id of this thread's first head
 
     // ---- phase B: per-event values (a6-a8), outputs, thread-sequential folding (a9) ----
@@ -824,58 +985,417 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
         }
     }
 
-    // ---- runs that span threads: segmented inclusive scan of (has, tail-or-whole) over the tile ----
-    bool f = has;
-    Acc v = cur;
-    if (!__all_sync(CH_FULL, has)) {
+    tile_finish(S, P, has, cur, p0, run0, base);
+}
+
+// =================================================================================================
+// Window-staged event pass (every span list laminar).  The per-event lookups become forward walks over
+// shared-memory windows of six sorted tables: the Euler boundary tables of the four span levels (spans.cu:
+// the innermost owner is a direct read, no parent walk), the merged comm union and the sample stream.
+// k_tile_seeds finds, per tile, the entry each table's window starts at (last entry <= the tile's first
+// query); the window ends at the next tile's seed, which bounds every query of the tile when the gpu's
+// queries are monotone (dispatch times always; compute start/end times on one compute stream).  Queries
+// outside a window (several compute streams, a tile straddling two gpus, a window larger than the pool)
+// take a binary search over the whole table in global memory: same answer, slower.
+// =================================================================================================
+constexpr int NTAB = 2;                // 0 combined key table (by dispatch time), 1 timeline (by start / end time)
+constexpr int POOL = 22528;            // bytes of staged windows per tile
+constexpr int SEED_W = 4;              // per tile: 2 seeds, the tile's gpu (lg), pad
+constexpr int KT_B = 16, TL_B = 44;    // staged bytes per entry: time + key; time + 3 intercepts + 3 slopes
+
+struct TabWin {
+    int64_t lo;           // global index of window entry 0 (the gpu's table starts with a -inf sentinel)
+    int64_t next;         // time of the entry after the window (INT64_MAX at the table end)
+    int n, off;           // staged entries (0 = look up in global memory), byte offset in the pool
+};
+struct EvSmemW {
+    EvSmem e;
+    TabWin tw[NTAB];
+    int lgP;
+    __align__(16) unsigned char pool[POOL];
+};
+static_assert(sizeof(EvSmemW) <= 113 * 1024, "two event-pass blocks per SM");
+
+__device__ __forceinline__ void tab_bounds(const EvParams &P, int x, int lg, int64_t *gb, int64_t *ge) {
+    if (x == 0) { *gb = P.kt_beg[lg]; *ge = P.kt_beg[lg + 1]; }
+    else { *gb = P.tl_beg[lg]; *ge = *gb + P.tl_len[lg]; }
+}
+
+// per tile: the entry each window starts at -- last entry <= the tile's first dispatch (key table) and <= the
+// start of its first COMPUTE event among the first 32 (timeline)
+__global__ void k_tile_seeds(EvParams P, int32_t *__restrict__ seeds) {
+    const int lane = threadIdx.x & 31;
+    const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (tile >= P.ntile) return;
+    const int64_t base = tile * EV_TILE, i = base + lane;
+    const int lg = P.gpu_lg[gpu_of(P.meta[base])];
+    const uint32_t m = i < P.N ? P.meta[i] : 0u;
+    const bool cmp = i < P.N && kind_of(m) == CK_COMPUTE && P.gpu_lg[gpu_of(m)] == lg;
+    const unsigned cm = __ballot_sync(CH_FULL, cmp);
+    int64_t s = 0;
+    if (lane < NTAB) {
+        const int64_t t = lane == 0 ? P.tl[base] : (cm ? P.ks[base + __ffs(cm) - 1] : P.tl[base]);
+        int64_t gb, ge;
+        tab_bounds(P, lane, lg, &gb, &ge);
+        s = last_le(lane == 0 ? P.KTt : P.TLt, gb, ge, t);     // >= gb: entry 0 is -inf
+    } else if (lane == NTAB) {
+        s = lg;
+    }
+    if (lane < SEED_W) seeds[tile * SEED_W + lane] = (int32_t)s;
+}
+
+// Windows of the tile: bounds from this tile's and the next tile's seeds (threads 0, 1), pool placement (thread 0;
+// a window that does not fit is cut short), then cp.async copies by all threads (the caller waits).
+__device__ __forceinline__ void stage_windows(EvSmemW &W, const EvParams &P, int64_t tile) {
+    const int tid = threadIdx.x;
+    const int32_t *sd = P.seeds + tile * SEED_W;
+    const int lg = sd[NTAB];
+    __shared__ int64_t s_ge[NTAB];
+    if (tid < NTAB) {
+        const int x = tid;
+        int64_t gb, ge;
+        tab_bounds(P, x, lg, &gb, &ge);
+        int64_t lo = sd[x], hi = ge;
+        if (tile + 1 < P.ntile && sd[SEED_W + NTAB] == lg) {
+            hi = (int64_t)sd[SEED_W + x] + 1 + (x == 1 ? 4 : 0);    // timeline: a little slack
+            if (hi < lo + 1) hi = lo + 1;
+            if (hi > ge) hi = ge;
+        }
+        TabWin &w = W.tw[x];
+        w.lo = lo;
+        w.n = (int)(hi - lo);
+        s_ge[x] = ge;
+        if (x == 0) W.lgP = lg;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int off = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            Acc pv = v.shfl_up(o);
-            bool pf = __shfl_up_sync(CH_FULL, f, o);
-            if (lane >= o) {
-                if (!f) { pv.merge(v); v = pv; }
-                f = f || pf;
+        for (int x = NTAB - 1; x >= 0; x--) {       // timeline first (small), then the key table
+            TabWin &w = W.tw[x];
+            const int eb = x == 0 ? KT_B : TL_B;
+            int fit = (POOL - off) / eb;
+            if (fit < 0) fit = 0;
+            if (w.n > fit) w.n = fit & ~3;          // cut short: later queries go to global memory
+            w.off = off;
+            off += (w.n * eb + 15) & ~15;
+            const int64_t *T = x == 0 ? P.KTt : P.TLt;
+            w.next = w.lo + w.n < s_ge[x] ? __ldg(T + w.lo + w.n) : INT64_MAX;
+        }
+    }
+    __syncthreads();
+    {
+        const TabWin w = W.tw[0];
+        unsigned char *b = W.pool + w.off;
+        for (int j = tid; j < w.n; j += EV_NT) {
+            cp_async8(b + 8 * j, P.KTt + w.lo + j);
+            cp_async8(b + 8 * (w.n + j), P.KTk + w.lo + j);
+        }
+    }
+    {
+        const TabWin w = W.tw[1];
+        unsigned char *b = W.pool + w.off;
+        const int64_t cap = P.tl_cap;
+        for (int j = tid; j < w.n; j += EV_NT) {
+            const int64_t g = w.lo + j;
+            cp_async8(b + 8 * j, P.TLt + g);
+            cp_async8(b + 8 * (w.n + j), P.TLv + g);
+            cp_async8(b + 8 * (2 * w.n + j), P.TLv + cap + g);
+            cp_async8(b + 8 * (3 * w.n + j), P.TLv + 2 * cap + g);
+            cp_async4(b + 32 * w.n + 4 * j, P.TLs + g);
+            cp_async4(b + 36 * w.n + 4 * j, P.TLs + cap + g);
+            cp_async4(b + 40 * w.n + 4 * j, P.TLs + 2 * cap + g);
+        }
+    }
+}
+
+// register copy of one staged window
+struct WinR {
+    const int64_t *T;     // times in shared memory (payload follows)
+    int n;
+    int64_t next;
+};
+__device__ __forceinline__ WinR win_reg(const EvSmemW &W, int x) {
+    const TabWin &w = W.tw[x];
+    WinR r;
+    r.T = reinterpret_cast<const int64_t *>(W.pool + w.off);
+    r.n = w.n;
+    r.next = w.next;
+    return r;
+}
+
+// local index of the last window entry <= t, walking forward from the cursor c (-1: search the window);
+// -1 when t lies before the window, n - 1 with t >= next when it lies after it
+__device__ __forceinline__ int win_find(const int64_t *T, int n, int c, int64_t t) {
+    if (c < 0 || T[c] > t) {
+        int l = 0, h = n;
+        while (l < h) {
+            int m = (l + h) >> 1;
+            if (T[m] <= t) l = m + 1; else h = m;
+        }
+        return l - 1;
+    }
+    while (c + 1 < n && T[c + 1] <= t) c++;
+    return c;
+}
+__device__ __forceinline__ bool win_ok(const WinR &w, int c, int64_t t) {
+    return c >= 0 && (c < w.n - 1 || t < w.next);
+}
+
+// global-memory lookups (outside the staged windows)
+__device__ __noinline__ unsigned long long key_global(const int64_t *Kt, const unsigned long long *Kk, int64_t gb,
+                                                      int64_t ge, int64_t t) {
+    return __ldg(Kk + last_le(Kt, gb, ge, t));
+}
+struct TlVal {
+    unsigned long long cov, F, Pw;
+};
+__device__ __forceinline__ TlVal tl_eval(int64_t d, unsigned long long v0, unsigned long long v1, unsigned long long v2,
+                                         int32_t s0, int32_t s1, int32_t s2) {
+    TlVal r;
+    const unsigned long long ud = (unsigned long long)d;
+    r.cov = v0 + (s0 ? ud : 0ull);
+    r.F = v1 + (unsigned long long)(int64_t)s1 * ud;
+    r.Pw = v2 + (unsigned long long)(int64_t)s2 * ud;
+    return r;
+}
+__device__ __noinline__ TlVal tl_global(const int64_t *Tt, const int64_t *Tv, const int32_t *Ts, int64_t cap, int64_t gb,
+                                        int64_t ge, int64_t t, int64_t t0) {
+    const int64_t j = last_le(Tt, gb, ge, t);
+    return tl_eval(t - t0, (unsigned long long)__ldg(Tv + j), (unsigned long long)__ldg(Tv + cap + j),
+                   (unsigned long long)__ldg(Tv + 2 * cap + j), __ldg(Ts + j), __ldg(Ts + cap + j),
+                   __ldg(Ts + 2 * cap + j));
+}
+
+__device__ __forceinline__ unsigned long long key_w(const WinR &w, const EvParams &P, int64_t t, int &cur, bool prim,
+                                                    int lg) {
+    if (prim) {
+        const int c = win_find(w.T, w.n, cur, t);
+        if (win_ok(w, c, t)) {
+            cur = c;
+            return reinterpret_cast<const unsigned long long *>(w.T + w.n)[c];
+        }
+    }
+    return key_global(P.KTt, P.KTk, P.kt_beg[lg], P.kt_beg[lg + 1], t);
+}
+__device__ __forceinline__ TlVal tl_w(const WinR &w, const EvParams &P, int64_t t, int &cur, bool prim, int lg) {
+    if (prim) {
+        const int c = win_find(w.T, w.n, cur, t);
+        if (win_ok(w, c, t)) {
+            cur = c;
+            const int32_t *s32 = reinterpret_cast<const int32_t *>(w.T + 4 * w.n);
+            return tl_eval(t - P.t0, (unsigned long long)w.T[w.n + c], (unsigned long long)w.T[2 * w.n + c],
+                           (unsigned long long)w.T[3 * w.n + c], s32[c], s32[w.n + c], s32[2 * w.n + c]);
+        }
+    }
+    const int64_t gb = P.tl_beg[lg];
+    return tl_global(P.TLt, P.TLv, P.TLs, P.tl_cap, gb, gb + P.tl_len[lg], t, P.t0);
+}
+
+// ---- sub-run heads per tile (first pass): the same keys and head rule as k_events_w, counted, so that the main
+// pass knows every tile's first sub-run id up front (an exclusive scan of the counts) instead of waiting on a
+// look-back chain that any slow tile would stall for all later ones.  Columns are read straight from global
+// memory (8 consecutive events per thread, 16 B loads); only the key-table window is staged.
+constexpr int HD_POOL = 18432;
+__global__ void __launch_bounds__(EV_NT) k_tile_heads(EvParams P, int64_t *__restrict__ tile_cnt) {
+    __shared__ __align__(16) unsigned char pool[HD_POOL];
+    __shared__ int64_t s_lo, s_next;
+    __shared__ int s_n, s_lg;
+    __shared__ unsigned long long s_last[EV_WARPS];
+    __shared__ int s_cnt[EV_WARPS];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t tile = blockIdx.x, base = tile * EV_TILE, i0 = base + (int64_t)tid * EV_IPT, N = P.N;
+    if (tid == 0) {
+        const int32_t *sd = P.seeds + tile * SEED_W;
+        const int lg = sd[NTAB];
+        int64_t gb, ge;
+        tab_bounds(P, 0, lg, &gb, &ge);
+        int64_t lo = sd[0], hi = ge;
+        if (tile + 1 < P.ntile && sd[SEED_W + NTAB] == lg) hi = (int64_t)sd[SEED_W] + 1;
+        if (hi < lo + 1) hi = lo + 1;
+        if (hi > ge) hi = ge;
+        int n = (int)(hi - lo);
+        if (n > HD_POOL / KT_B) n = (HD_POOL / KT_B) & ~3;
+        s_lo = lo; s_n = n; s_lg = lg;
+        s_next = lo + n < ge ? __ldg(P.KTt + lo + n) : INT64_MAX;
+    }
+    __syncthreads();
+    {
+        const int64_t lo = s_lo;
+        const int n = s_n;
+        for (int j = tid; j < n; j += EV_NT) {
+            cp_async8(pool + 8 * j, P.KTt + lo + j);
+            cp_async8(pool + 8 * (n + j), P.KTk + lo + j);
+        }
+    }
+    int64_t tl[EV_IPT];
+    uint32_t mt[EV_IPT];
+    const int nv = i0 >= N ? 0 : (int)min((int64_t)EV_IPT, N - i0);
+    if (nv == EV_IPT && ((((uintptr_t)(P.tl + i0)) | ((uintptr_t)(P.meta + i0))) & 15u) == 0) {
+#pragma unroll
+        for (int u = 0; u < EV_IPT / 2; u++) {
+            const longlong2 v = __ldg(reinterpret_cast<const longlong2 *>(P.tl + i0) + u);
+            tl[2 * u] = v.x; tl[2 * u + 1] = v.y;
+        }
+#pragma unroll
+        for (int u = 0; u < EV_IPT / 4; u++) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(P.meta + i0) + u);
+            mt[4 * u] = v.x; mt[4 * u + 1] = v.y; mt[4 * u + 2] = v.z; mt[4 * u + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < EV_IPT; k++) {
+            tl[k] = k < nv ? P.tl[i0 + k] : 0;
+            mt[k] = k < nv ? P.meta[i0 + k] : 0u;
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    WinR wk;
+    wk.T = reinterpret_cast<const int64_t *>(pool);
+    wk.n = s_n;
+    wk.next = s_next;
+    const int lgP = s_lg;
+    int ck = -1;
+    unsigned long long prevk = CH_INVALID_KEY, first = CH_INVALID_KEY;
+    int nh = 0;
+#pragma unroll
+    for (int k = 0; k < EV_IPT; k++) {
+        unsigned long long kk = CH_INVALID_KEY;
+        if (k < nv) {
+            const int lg = P.gpu_lg[gpu_of(mt[k])];
+            kk = key_w(wk, P, tl[k], ck, lg == lgP, lg);
+            if (k > 0 && kk != prevk) nh++;
+        }
+        if (k == 0) first = kk;
+        prevk = kk;
+    }
+    // head at the thread's first event: tile start, or a key change from the previous thread's last event
+    unsigned long long pl = __shfl_up_sync(CH_FULL, prevk, 1);
+    if (lane == 31) s_last[warp] = prevk;
+    __syncthreads();
+    if (lane == 0) pl = warp > 0 ? s_last[warp - 1] : CH_INVALID_KEY;
+    if (nv > 0 && (tid == 0 || first != pl)) nh++;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nh += __shfl_xor_sync(CH_FULL, nh, o);
+    if (lane == 0) s_cnt[warp] = nh;
+    __syncthreads();
+    if (tid == 0) {
+        int64_t t = 0;
+        for (int w = 0; w < EV_WARPS; w++) t += s_cnt[w];
+        tile_cnt[tile] = t;
+    }
+}
+
+__global__ void __launch_bounds__(EV_NT, 2) k_events_w(EvParams P, int vec_ok) {
+    extern __shared__ __align__(16) unsigned char ev_dsm[];
+    EvSmemW &W = *reinterpret_cast<EvSmemW *>(ev_dsm);
+    EvSmem &S = W.e;
+    const int tid = threadIdx.x;
+    const int64_t tile = blockIdx.x;
+    if (tid == 0) { S.excl = P.tile_base[tile]; S.tot = (int)(P.tile_base[tile + 1] - P.tile_base[tile]); }
+    const int64_t base = tile * EV_TILE;
+    const int64_t i0 = base + (int64_t)tid * EV_IPT;
+    const int64_t N = P.N;
+    stage_windows(W, P, tile);
+    stage_tile(S, P, base, vec_ok && base + EV_TILE <= N);
+    cp_async_wait_all();
+    __syncthreads();
+    const int nv = i0 >= N ? 0 : (int)min((int64_t)EV_IPT, N - i0);
+    const int lgP = W.lgP;
+
+    // ---- phase A: instance key of every event (a5): the combined key table at the dispatch time ----
+    unsigned hmask = 0;
+    {
+        const WinR wk = win_reg(W, 0);
+        int ck = -1;
+        unsigned long long prevk = CH_INVALID_KEY;
+#pragma unroll 1
+        for (int k = 0; k < EV_IPT; k++) {
+            unsigned long long kk = CH_INVALID_KEY;
+            if (k < nv) {
+                const int64_t t = ev_col(S, 0, tid, k);
+                const int lg = P.gpu_lg[gpu_of(ev_meta(S, tid, k))];
+                kk = key_w(wk, P, t, ck, lg == lgP, lg);
+                if (k > 0 && kk != prevk) hmask |= 1u << k;
             }
+            S.key[k][tid] = kk;
+            prevk = kk;
         }
     }
-    if (lane == 31) { S.wagg[warp] = v; S.wflag[warp] = f; }
-    __syncthreads();
-    if (tid < EV_WARPS) {                 // carry into warp tid: segmented combine of earlier warps
-        Acc c;
-        c.zero();
-        int cf = 0;
-        for (int w = 0; w < tid; w++) {
-            if (S.wflag[w]) { c = S.wagg[w]; cf = 1; }
-            else c.merge(S.wagg[w]);
+    int tot;
+    const int ex = tile_head_scan(S, hmask, nv, &tot);   // tot == the first pass's count (same keys, same rule)
+    const int64_t run0 = S.excl + ex;
+
+    // ---- phase B: per-event values (a6-a8), outputs, thread-sequential folding (a9) ----
+    Acc cur, p0;
+    cur.zero();
+    p0.zero();
+    bool has = false;
+    int64_t curid = run0 - 1;
+    const WinR wt = win_reg(W, 1);
+    int ct = -1;
+#pragma unroll 1
+    for (int k = 0; k < EV_IPT; k++) {
+        if (k >= nv) break;
+        const int64_t i = i0 + k;
+        const uint32_t m = ev_meta(S, tid, k);
+        const int lg = P.gpu_lg[gpu_of(m)];
+        if ((hmask >> k) & 1u) {
+            if (!has) { p0 = cur; has = true; }
+            else write_subrun(P, curid, cur, base);
+            curid++;
+            cur.zero();
+            P.sr_key[curid] = S.key[k][tid];
+            P.sr_first[curid] = i;
         }
-        S.wcarry[tid] = c;
-        S.wcflag[tid] = cf;
-    }
-    __syncthreads();
-    // exclusive value at this thread: warp-exclusive, completed with the warp carry if no head precedes
-    Acc e = v.shfl_up(1);
-    bool ef = __shfl_up_sync(CH_FULL, f, 1);
-    if (lane == 0) { e.zero(); ef = false; }
-    if (!ef) {
-        Acc c = S.wcarry[warp];
-        c.merge(e);
-        e = c;
-    }
-    // the run that ends in this thread's first piece (or at the end of the previous thread)
-    if (has && tid > 0) {
-        e.merge(p0);
-        write_subrun(P, run0 - 1, e, base);
-    }
-    // the run open at the end of the tile
-    if (tid == EV_NT - 1 && base < N) {
-        Acc last = v;
-        if (!f) {
-            Acc c = S.wcarry[warp];
-            c.merge(v);
-            last = c;
+        const int kd = kind_of(m);
+        const int64_t ks = ev_col(S, 1, tid, k), ke = ev_col(S, 2, tid, k);
+        const int64_t dur = ke - ks;
+        int64_t ovl = 0, prep = 0, call = 0, phi = 0, psi = 0;
+        cur.nev += 1;
+        if (kd == CK_COMPUTE) {
+            const int64_t pe = ev_col(S, 3, tid, k);
+            if (pe != CH_NONE_TS) {
+                const int64_t tl = ev_col(S, 0, tid, k);
+                const int64_t t2 = tl < ks ? tl : ks;                  // D6: dispatch clamped to start
+                const int64_t a = t2 - pe;
+                prep = a > 0 ? a : 0;                                   // Eq. 1
+                const int64_t c1 = ks - t2, c2 = ks - pe;
+                const int64_t c = c1 < c2 ? c1 : c2;                    // Eq. 2
+                call = c > 0 ? c : 0;
+            }
+            const bool prim = lg == lgP;
+            const TlVal va = tl_w(wt, P, ks, ct, prim, lg);
+            const TlVal vb = tl_w(wt, P, ke, ct, prim, lg);
+            ovl = (int64_t)(vb.cov - va.cov);                           // |[t_ks, t_ke) ∩ U_g| (D9)
+            phi = (int64_t)(vb.F - va.F);                               // MHz*ns (D10)
+            psi = (int64_t)(vb.Pw - va.Pw);                             // mW*ns
+            cur.n += 1;
+            cur.busy += dur;
+            cur.prep += prep;
+            cur.call += call;
+            cur.ovl += ovl;
+            cur.phi += phi;
+            cur.psi += psi;
+            if (ks < cur.fks || (ks == cur.fks && tid * EV_IPT + k < cur.foff)) {
+                cur.fks = ks;
+                cur.foff = tid * EV_IPT + k;
+            }
+            if (ke > cur.lke) cur.lke = ke;
+        } else {
+            if (kd == CK_COPY || kd == CK_OTHER) cur.copy += dur;
+            else if (kd == CK_AG) cur.ag += dur;
+            else if (kd == CK_RS) cur.rs += dur;
         }
-        write_subrun(P, S.excl + S.tot - 1, last, base);
+        if (P.o_ovl && !is_comm(kd)) P.o_ovl[i] = ovl;
+        if (P.o_prep) P.o_prep[i] = prep;
+        if (P.o_call) P.o_call[i] = call;
+        if (P.o_phi) P.o_phi[i] = phi;
+        if (P.o_psi) P.o_psi[i] = psi;
+        if (P.o_run) P.o_run[i] = (int32_t)curid;
     }
+    tile_finish(S, P, has, cur, p0, run0, base);
 }
 }  // namespace
 
@@ -969,6 +1489,32 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
         CH_TRY(ch_seg_scan_i64(ctx, tp, hd, ctx->d_smp_psi, M, 0));
         ctx->used = mark;
     }
+    // timeline for the window-staged event pass
+    if (ctx->et_ok && n_lg > 0) {
+        std::vector<int64_t> tb(n_lg + 1), nc(n_lg);
+        int64_t off = 0;
+        for (int l = 0; l < n_lg; l++) {
+            nc[l] = ctx->bucket_beg[l * NG + 1] - ctx->bucket_beg[l * NG];
+            tb[l] = off;
+            off += 1 + 2 * nc[l] + (ctx->smp_hi[l] - ctx->smp_lo[l]);
+        }
+        tb[n_lg] = off;
+        ctx->tl_cap = off;
+        ctx->TL_t = CH_ALLOC(ctx, int64_t, off);
+        ctx->TL_v = CH_ALLOC(ctx, int64_t, 3 * off);
+        ctx->TL_s = CH_ALLOC(ctx, int32_t, 3 * off);
+        ctx->d_tl_beg = CH_ALLOC(ctx, int64_t, n_lg + 1);
+        ctx->d_tl_len = CH_ALLOC(ctx, int64_t, n_lg + 1);
+        int64_t *dnc = CH_ALLOC(ctx, int64_t, n_lg + 1);
+        CH_ALLOC_END(ctx);
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_tl_beg, tb.data(), 8 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(dnc, nc.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+        k_timeline<<<(unsigned)ceil_div(off, NT), NT, 0, ctx->st>>>(
+            ctx->d_tl_beg, dnc, n_lg, off, ctx->U_s, ctx->U_e, ctx->U_P, ctx->d_U_beg, ctx->d_U_cnt, ctx->smp.ts_ns,
+            ctx->d_smp_phi, ctx->d_smp_psi, ctx->smp.freq_mhz, ctx->smp.power_mw, ctx->d_smp_lo, ctx->d_smp_hi, ctx->t0,
+            off, ctx->TL_t, ctx->TL_v, ctx->TL_s, ctx->d_tl_len);
+        CH_LAUNCHED(ctx);
+    }
     // lg -> has samples (breakdown flag)
     ctx->d_has_smp = CH_ALLOC(ctx, int32_t, n_lg + 1);
     CH_ALLOC_END(ctx);
@@ -1022,19 +1568,50 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     P.o_run = ctx->d_run_id;
     P.sr_key = ctx->sub.key; P.sr_first = ctx->sub.first_event; P.sr_f = ctx->sub.f; P.cap = N;
     P.tile_state = ctx->d_tile_state; P.ticket = ctx->d_tile_ticket;
-    size_t dsm = sizeof(EvSmem);
-    static bool attr_set = false;
-    if (!attr_set) {
-        CH_CUDA(ctx, cudaFuncSetAttribute(k_events, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-        attr_set = true;
-    }
+    P.KTt = ctx->KT_t; P.KTk = ctx->KT_k; P.kt_beg = ctx->d_kt_beg;
+    P.TLt = ctx->TL_t; P.TLv = ctx->TL_v; P.TLs = ctx->TL_s; P.tl_beg = ctx->d_tl_beg; P.tl_len = ctx->d_tl_len;
+    P.tl_cap = ctx->tl_cap; P.t0 = ctx->t0; P.ntile = ntile;
     // 16 B cp.async staging needs 16 B aligned event columns (tile bases are multiples of 2048 events)
     auto al16 = [](const void *p) { return ((uintptr_t)p & 15u) == 0; };
     int vec_ok = al16(P.tl) && al16(P.ks) && al16(P.ke) && al16(P.pred_end) && al16(P.meta);
-    ch_tick(ctx, 4, 0);
-    k_events<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P, vec_ok);
-    CH_LAUNCHED(ctx);
-    ch_tick(ctx, 4, 1);
+    if (ctx->et_ok) {
+        // every span list laminar: Euler boundary tables, window-staged lookups
+        size_t mark = ctx->used;
+        int32_t *seeds = CH_ALLOC(ctx, int32_t, ntile * SEED_W);
+        int64_t *tcnt = CH_ALLOC(ctx, int64_t, ntile + 1), *tbase = CH_ALLOC(ctx, int64_t, ntile + 1);
+        CH_ALLOC_END(ctx);
+        P.seeds = seeds;
+        size_t dsm = sizeof(EvSmemW);
+        static bool attr_w = false;
+        if (!attr_w) {
+            CH_CUDA(ctx, cudaFuncSetAttribute(k_events_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+            attr_w = true;
+        }
+        ch_tick(ctx, 4, 0);
+        k_tile_seeds<<<(unsigned)ceil_div(ntile * 32, NT), NT, 0, ctx->st>>>(P, seeds);
+        CH_LAUNCHED(ctx);
+        k_tile_heads<<<(unsigned)ntile, EV_NT, 0, ctx->st>>>(P, tcnt);
+        CH_LAUNCHED(ctx);
+        CH_TRY(ch_scan_excl_i64(ctx, tcnt, tbase, ntile, tbase + ntile));
+        P.tile_base = tbase;
+        k_events_w<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P, vec_ok);
+        CH_LAUNCHED(ctx);
+        ch_tick(ctx, 4, 1);
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_tile_state + ntile - 1, tbase + ntile, 8, cudaMemcpyDeviceToDevice, ctx->st));
+        ctx->used = mark;
+    } else {
+        P.seeds = nullptr;
+        size_t dsm = sizeof(EvSmem);
+        static bool attr_set = false;
+        if (!attr_set) {
+            CH_CUDA(ctx, cudaFuncSetAttribute(k_events, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+            attr_set = true;
+        }
+        ch_tick(ctx, 4, 0);
+        k_events<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P, vec_ok);
+        CH_LAUNCHED(ctx);
+        ch_tick(ctx, 4, 1);
+    }
     if (ovl && ctx->n_lg > 0) {
         k_covl<<<dim3(64, ctx->n_lg), 128, 0, ctx->st>>>(P, ctx->n_lg);
         CH_LAUNCHED(ctx);

@@ -253,6 +253,102 @@ __global__ void k_attr_sweep(const int *__restrict__ lists, int n_sweep, const i
     }
 }
 
+// ---- Euler boundary tables (every list laminar) ----------------------------------------------------
+// In a laminar list the push order is a pre-order of the nesting forest, so the time-ordered sequence of
+// span endpoints is its Euler tour: before start(q) come the r starts of the earlier spans (r = rank of q in
+// the list) and the ends of those of them that are not ancestors of q (r - depth(q)); end(q) follows the
+// 2*size(q) - 1 endpoints of q's subtree.  Each entry records the innermost span after it: q after start(q),
+// parent(q) after end(q).  Equal times keep the tour order, so "last entry with time <= t" is the innermost
+// span containing t (half-open, D3; ties innermost = push-order last, D4) -- the owner the parent walk finds.
+__global__ void k_euler(const int64_t *__restrict__ Ps, const int64_t *__restrict__ Pe,
+                        const int32_t *__restrict__ parent, const int32_t *__restrict__ Plist, int64_t SL,
+                        const int64_t *__restrict__ list_beg, int64_t *__restrict__ Et, int32_t *__restrict__ Ec) {
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= SL) return;
+    const int list = Plist[q];
+    const int64_t lb = list_beg[list], le = list_beg[list + 1];
+    const int64_t r = q - lb;
+    int64_t d = 0;
+    for (int32_t p = parent[q]; p >= 0; p = parent[p]) d++;
+    const int64_t e = Pe[q];
+    // subtree = [q, first later span of the list starting at or after end(q))
+    int64_t l = q + 1, h = le;
+    while (l < h) {
+        int64_t m = (l + h) >> 1;
+        if (__ldg(Ps + m) < e) l = m + 1; else h = m;
+    }
+    const int64_t base = 2 * lb + list + 1;       // entry 0 of the list is the (-inf, none) sentinel
+    const int64_t ps = base + 2 * r - d, pe = ps + 2 * (l - q) - 1;
+    Et[ps] = Ps[q];
+    Ec[ps] = (int32_t)(r + 1);
+    Et[pe] = e;
+    const int32_t p = parent[q];
+    Ec[pe] = p >= 0 ? (int32_t)(p - lb + 1) : 0;
+}
+__global__ void k_euler_sentinels(const int64_t *__restrict__ list_beg, int n_lists, int64_t *__restrict__ Et,
+                                  int32_t *__restrict__ Ec, int64_t *__restrict__ et_beg) {
+    int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l > n_lists) return;
+    const int64_t b = 2 * list_beg[l] + l;
+    et_beg[l] = b;
+    if (l == n_lists) return;
+    Et[b] = INT64_MIN;
+    Ec[b] = 0;
+}
+// the tour must come out time-sorted; anything else sends the event pass down the parent-walk path
+__global__ void k_euler_check(const int64_t *__restrict__ Et, const int64_t *__restrict__ et_beg, int n_lists,
+                              int64_t n, unsigned int *bad) {
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j + 1 >= n) return;
+    if (Et[j + 1] < Et[j]) {
+        // a list boundary is allowed to decrease (next list's sentinel is INT64_MIN)
+        if (Et[j + 1] != INT64_MIN) atomicOr(bad, 1u);
+    }
+}
+
+// combined key table: every non-sentinel Euler entry of (lg, level) goes to its position in the time-merge of the
+// gpu's four lists (ties: lower level first, then list order) and records the instance key after it -- its own
+// level's code and, for the other levels, the code of their last entry at or before its time.  The last entry
+// at any time therefore carries the full key there; entry 0 of each gpu is (-inf, invalid).
+__global__ void k_keytab(const int64_t *__restrict__ Et, const int32_t *__restrict__ Ec,
+                         const int64_t *__restrict__ et_beg, const int64_t *__restrict__ list_beg, int n_lists,
+                         int64_t net, int sh_it, int sh_ph, int sh_ly, int sh_lg, int64_t *__restrict__ Kt,
+                         unsigned long long *__restrict__ Kk) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= net) return;
+    int l = 0, h = n_lists;                  // list of entry j: last l with et_beg[l] <= j
+    while (h - l > 1) {
+        const int m = (l + h) >> 1;
+        if (et_beg[m] <= j) l = m; else h = m;
+    }
+    const int lg = l >> 2, lv = l & 3;
+    const int64_t a = j - et_beg[l];
+    const int64_t kb = 2 * list_beg[lg * 4] + lg;
+    if (a == 0) {
+        if (lv == 0) { Kt[kb] = INT64_MIN; Kk[kb] = CH_INVALID_KEY; }
+        return;
+    }
+    const int64_t t = Et[j];
+    int64_t pos = kb + a;
+    uint32_t code[4];
+    code[lv] = (uint32_t)Ec[j];
+#pragma unroll
+    for (int o = 0; o < 4; o++) {
+        if (o == lv) continue;
+        const int64_t b = et_beg[lg * 4 + o], e = et_beg[lg * 4 + o + 1];
+        const int64_t le = last_le(Et, b, e, t);     // >= b: the sentinel is -inf
+        code[o] = (uint32_t)Ec[le];
+        int64_t c = le;
+        if (o > lv) while (c > b && Et[c] == t) c--;  // later levels: only entries strictly before t
+        pos += c - b;
+    }
+    Kt[pos] = t;
+    Kk[pos] = code[0] == 0 ? CH_INVALID_KEY
+                           : ((unsigned long long)lg << sh_lg) | ((unsigned long long)code[0] << sh_it) |
+                                 ((unsigned long long)code[1] << sh_ph) | ((unsigned long long)code[2] << sh_ly) |
+                                 (unsigned long long)code[3];
+}
+
 __global__ void k_attr_out(SpanView v, const int64_t *__restrict__ tl, const uint32_t *__restrict__ meta, int64_t N,
                            const int32_t *__restrict__ gpu_lg, const int32_t *__restrict__ Po,
                            int32_t *__restrict__ out) {
@@ -406,6 +502,50 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
     for (int l = 0; l < n_lists; l++) if (ctx->list_flags[l]) sweep.push_back(l);
     ctx->rep.non_laminar_lists = (int32_t)sweep.size();
     ctx->d_attr_pre = nullptr;
+    ctx->et_ok = false;
+    ctx->ET_t = nullptr;
+    ctx->ET_c = nullptr;
+    if (sweep.empty()) {
+        const int64_t net = 2 * SL + n_lists;
+        ctx->ET_t = CH_ALLOC(ctx, int64_t, net);
+        ctx->ET_c = CH_ALLOC(ctx, int32_t, net);
+        ctx->d_et_beg = CH_ALLOC(ctx, int64_t, n_lists + 1);
+        CH_ALLOC_END(ctx);
+        size_t mark = ctx->used;
+        unsigned int *bad = CH_ALLOC(ctx, unsigned int, 1);
+        CH_ALLOC_END(ctx);
+        k_euler_sentinels<<<(unsigned)ceil_div(n_lists + 1, NT), NT, 0, ctx->st>>>(ctx->d_list_beg, n_lists, ctx->ET_t,
+                                                                                  ctx->ET_c, ctx->d_et_beg);
+        CH_LAUNCHED(ctx);
+        CH_CUDA(ctx, cudaMemsetAsync(bad, 0, 4, ctx->st));
+        if (SL > 0) {
+            k_euler<<<(unsigned)ceil_div(SL, NT), NT, 0, ctx->st>>>(ctx->P_start, ctx->P_end, ctx->P_parent, Plist, SL,
+                                                                   ctx->d_list_beg, ctx->ET_t, ctx->ET_c);
+            CH_LAUNCHED(ctx);
+            k_euler_check<<<(unsigned)ceil_div(net, NT), NT, 0, ctx->st>>>(ctx->ET_t, ctx->d_et_beg, n_lists, net, bad);
+            CH_LAUNCHED(ctx);
+        }
+        unsigned int hbad = 0;
+        CH_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        ctx->used = mark;
+        ctx->et_ok = hbad == 0;
+    }
+    if (ctx->et_ok) {
+        const int64_t net = 2 * SL + n_lists, nkt = 2 * SL + n_lg;
+        ctx->KT_t = CH_ALLOC(ctx, int64_t, nkt);
+        ctx->KT_k = CH_ALLOC(ctx, unsigned long long, nkt);
+        ctx->d_kt_beg = CH_ALLOC(ctx, int64_t, n_lg + 1);
+        CH_ALLOC_END(ctx);
+        std::vector<int64_t> kb(n_lg + 1);
+        for (int l = 0; l <= n_lg; l++) kb[l] = 2 * ctx->list_beg[l * 4] + l;
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_kt_beg, kb.data(), 8 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
+        const int sh_ly = ctx->kb[3], sh_ph = sh_ly + ctx->kb[2], sh_it = sh_ph + ctx->kb[1], sh_lg = sh_it + ctx->kb[0];
+        k_keytab<<<(unsigned)ceil_div(net, NT), NT, 0, ctx->st>>>(ctx->ET_t, ctx->ET_c, ctx->d_et_beg, ctx->d_list_beg,
+                                                                 n_lists, net, sh_it, sh_ph, sh_ly, sh_lg, ctx->KT_t,
+                                                                 ctx->KT_k);
+        CH_LAUNCHED(ctx);
+    }
     if (!sweep.empty()) {
         ctx->d_attr_pre = CH_ALLOC(ctx, int32_t, 4 * ctx->N);
         int *dl = CH_ALLOC(ctx, int, (int64_t)sweep.size());
