@@ -636,14 +636,17 @@ struct EvSmem {
     int tot;
 };
 // element k of thread t in the swizzled layouts
-__device__ __forceinline__ int64_t ev_col(const EvSmem &S, int c, int t, int k) {
+template <class SM>
+__device__ __forceinline__ int64_t ev_col(const SM &S, int c, int t, int k) {
     return reinterpret_cast<const int64_t *>(&S.col[c][sw64(t, k >> 1)])[k & 1];
 }
-__device__ __forceinline__ uint32_t ev_meta(const EvSmem &S, int t, int k) {
+template <class SM>
+__device__ __forceinline__ uint32_t ev_meta(const SM &S, int t, int k) {
     return reinterpret_cast<const uint32_t *>(&S.meta[sw32(t, k >> 2)])[k & 3];
 }
 
-__device__ __forceinline__ void stage_tile(EvSmem &S, const EvParams &P, int64_t base, bool vec) {
+template <class SM>
+__device__ __forceinline__ void stage_tile(SM &S, const EvParams &P, int64_t base, bool vec) {
     const int tid = threadIdx.x;
     const int64_t *src[4] = {P.tl, P.ks, P.ke, P.pred_end};
     if (vec) {
@@ -706,6 +709,32 @@ __device__ __forceinline__ int tile_head_scan(EvSmem &S, unsigned &hmask, int nv
     return wbase + wex;
 }
 
+// the same scan when the caller has already decided whether the thread's first event is a head
+template <class SM>
+__device__ __forceinline__ int tile_head_scan_h(SM &S, unsigned &hmask, bool head0, int *tot_out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (head0) hmask |= 1u;
+    const int nh = __popc(hmask);
+    int wex = nh;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(CH_FULL, wex, o);
+        if (lane >= o) wex += y;
+    }
+    if (lane == 31) S.wheads[warp] = wex;
+    wex -= nh;
+    __syncthreads();
+    int wbase = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < EV_WARPS; w++) {
+        int c = S.wheads[w];
+        if (w < warp) wbase += c;
+        tot += c;
+    }
+    *tot_out = tot;
+    return wbase + wex;
+}
+
 // ---- decoupled look-back (warp 0, 32 predecessors per probe): global id of the tile's first head ----
 __device__ __forceinline__ void tile_lookback(EvSmem &S, const EvParams &P, int64_t tile, int tot) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -739,7 +768,8 @@ __device__ __forceinline__ void tile_lookback(EvSmem &S, const EvParams &P, int6
 }
 
 // ---- runs that span threads: segmented inclusive scan of (has, tail-or-whole) over the tile ----
-__device__ __forceinline__ void tile_finish(EvSmem &S, const EvParams &P, bool has, const Acc &cur, const Acc &p0,
+template <class SM>
+__device__ __forceinline__ void tile_finish(SM &S, const EvParams &P, bool has, const Acc &cur, const Acc &p0,
                                             int64_t run0, int64_t base) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t N = P.N;
@@ -999,7 +1029,7 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
 // take a binary search over the whole table in global memory: same answer, slower.
 // =================================================================================================
 constexpr int NTAB = 2;                // 0 combined key table (by dispatch time), 1 timeline (by start / end time)
-constexpr int POOL = 22528;            // bytes of staged windows per tile
+constexpr int POOL = 27648;            // bytes of staged windows per tile
 constexpr int SEED_W = 4;              // per tile: 2 seeds, the tile's gpu (lg), pad
 constexpr int KT_B = 16, TL_B = 44;    // staged bytes per entry: time + key; time + 3 intercepts + 3 slopes
 
@@ -1009,7 +1039,15 @@ struct TabWin {
     int n, off;           // staged entries (0 = look up in global memory), byte offset in the pool
 };
 struct EvSmemW {
-    EvSmem e;
+    longlong2 col[4][EV_TILE / 2];        // t_l, t_ks, t_ke, pred_end (64 KB)
+    uint4 meta[EV_TILE / 4];              // 8 KB
+    uint32_t kidx[EV_IPT][EV_NT];         // key of each event as a key-table index (8 KB), see key_at
+    unsigned long long lastk[EV_NT];      // key of each thread's last event slot
+    Acc wagg[EV_WARPS], wcarry[EV_WARPS];
+    int wflag[EV_WARPS], wcflag[EV_WARPS];
+    int wheads[EV_WARPS];
+    int64_t tile, excl;
+    int tot;
     TabWin tw[NTAB];
     int lgP;
     __align__(16) unsigned char pool[POOL];
@@ -1178,6 +1216,26 @@ __device__ __forceinline__ unsigned long long key_w(const WinR &w, const EvParam
     }
     return key_global(P.KTt, P.KTk, P.kt_beg[lg], P.kt_beg[lg + 1], t);
 }
+// key-table index of the innermost-key entry at t: the window-local index, or the global index with bit 31 set
+constexpr uint32_t KIDX_GLOBAL = 0x80000000u, KIDX_NONE = 0xFFFFFFFFu;
+__device__ __noinline__ uint32_t kidx_global(const int64_t *Kt, int64_t gb, int64_t ge, int64_t t) {
+    return (uint32_t)last_le(Kt, gb, ge, t) | KIDX_GLOBAL;
+}
+__device__ __forceinline__ uint32_t kidx_w(const WinR &w, const EvParams &P, int64_t t, int &cur, bool prim, int lg) {
+    if (prim) {
+        const int c = win_find(w.T, w.n, cur, t);
+        if (win_ok(w, c, t)) {
+            cur = c;
+            return (uint32_t)c;
+        }
+    }
+    return kidx_global(P.KTt, P.kt_beg[lg], P.kt_beg[lg + 1], t);
+}
+__device__ __forceinline__ unsigned long long key_at(const WinR &w, const EvParams &P, uint32_t v) {
+    if (v == KIDX_NONE) return CH_INVALID_KEY;
+    if (v & KIDX_GLOBAL) return __ldg(P.KTk + (v & ~KIDX_GLOBAL));
+    return reinterpret_cast<const unsigned long long *>(w.T + w.n)[v];
+}
 __device__ __forceinline__ TlVal tl_w(const WinR &w, const EvParams &P, int64_t t, int &cur, bool prim, int lg) {
     if (prim) {
         const int c = win_find(w.T, w.n, cur, t);
@@ -1289,42 +1347,47 @@ __global__ void __launch_bounds__(EV_NT) k_tile_heads(EvParams P, int64_t *__res
 
 __global__ void __launch_bounds__(EV_NT, 2) k_events_w(EvParams P, int vec_ok) {
     extern __shared__ __align__(16) unsigned char ev_dsm[];
-    EvSmemW &W = *reinterpret_cast<EvSmemW *>(ev_dsm);
-    EvSmem &S = W.e;
+    EvSmemW &S = *reinterpret_cast<EvSmemW *>(ev_dsm);
     const int tid = threadIdx.x;
     const int64_t tile = blockIdx.x;
     if (tid == 0) { S.excl = P.tile_base[tile]; S.tot = (int)(P.tile_base[tile + 1] - P.tile_base[tile]); }
     const int64_t base = tile * EV_TILE;
     const int64_t i0 = base + (int64_t)tid * EV_IPT;
     const int64_t N = P.N;
-    stage_windows(W, P, tile);
+    stage_windows(S, P, tile);
     stage_tile(S, P, base, vec_ok && base + EV_TILE <= N);
     cp_async_wait_all();
     __syncthreads();
     const int nv = i0 >= N ? 0 : (int)min((int64_t)EV_IPT, N - i0);
-    const int lgP = W.lgP;
+    const int lgP = S.lgP;
+    const WinR wk = win_reg(S, 0);
 
     // ---- phase A: instance key of every event (a5): the combined key table at the dispatch time ----
     unsigned hmask = 0;
+    unsigned long long firstk = CH_INVALID_KEY;
     {
-        const WinR wk = win_reg(W, 0);
         int ck = -1;
         unsigned long long prevk = CH_INVALID_KEY;
 #pragma unroll 1
         for (int k = 0; k < EV_IPT; k++) {
             unsigned long long kk = CH_INVALID_KEY;
+            uint32_t v = KIDX_NONE;
             if (k < nv) {
                 const int64_t t = ev_col(S, 0, tid, k);
                 const int lg = P.gpu_lg[gpu_of(ev_meta(S, tid, k))];
-                kk = key_w(wk, P, t, ck, lg == lgP, lg);
+                v = kidx_w(wk, P, t, ck, lg == lgP, lg);
+                kk = key_at(wk, P, v);
                 if (k > 0 && kk != prevk) hmask |= 1u << k;
             }
-            S.key[k][tid] = kk;
+            if (k == 0) firstk = kk;
+            S.kidx[k][tid] = v;
             prevk = kk;
         }
+        S.lastk[tid] = prevk;
     }
+    __syncthreads();
     int tot;
-    const int ex = tile_head_scan(S, hmask, nv, &tot);   // tot == the first pass's count (same keys, same rule)
+    const int ex = tile_head_scan_h(S, hmask, nv > 0 && (tid == 0 || firstk != S.lastk[tid - 1]), &tot);
     const int64_t run0 = S.excl + ex;
 
     // ---- phase B: per-event values (a6-a8), outputs, thread-sequential folding (a9) ----
@@ -1333,7 +1396,7 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events_w(EvParams P, int vec_ok) {
     p0.zero();
     bool has = false;
     int64_t curid = run0 - 1;
-    const WinR wt = win_reg(W, 1);
+    const WinR wt = win_reg(S, 1);
     int ct = -1;
 #pragma unroll 1
     for (int k = 0; k < EV_IPT; k++) {
@@ -1346,7 +1409,7 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events_w(EvParams P, int vec_ok) {
             else write_subrun(P, curid, cur, base);
             curid++;
             cur.zero();
-            P.sr_key[curid] = S.key[k][tid];
+            P.sr_key[curid] = key_at(wk, P, S.kidx[k][tid]);
             P.sr_first[curid] = i;
         }
         const int kd = kind_of(m);
