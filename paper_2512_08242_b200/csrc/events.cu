@@ -626,6 +626,7 @@ __device__ __forceinline__ int sw32(int t, int j) { return t * 2 + (j ^ ((t >> 2
 
 constexpr int EV_WARPS = EV_NT / 32;
 struct EvSmem {
+    static constexpr int NT = EV_NT, TILE = EV_TILE, WARPS = EV_WARPS;
     longlong2 col[4][EV_TILE / 2];        // t_l, t_ks, t_ke, pred_end (64 KB)
     uint4 meta[EV_TILE / 4];              // 8 KB
     unsigned long long key[EV_IPT][EV_NT];  // instance key per event, [k][thread] (16 KB)
@@ -654,19 +655,19 @@ __device__ __forceinline__ void stage_tile(SM &S, const EvParams &P, int64_t bas
         for (int c = 0; c < 4; c++) {
 #pragma unroll
             for (int r = 0; r < 4; r++) {
-                int u = tid + r * EV_NT;    // 16 B unit of the column: events 2u, 2u+1
+                int u = tid + r * SM::NT;    // 16 B unit of the column: events 2u, 2u+1
                 cp_async16(&S.col[c][sw64(u >> 2, u & 3)], src[c] + base + 2 * u);
             }
         }
 #pragma unroll
         for (int r = 0; r < 2; r++) {
-            int u = tid + r * EV_NT;        // events 4u .. 4u+3
+            int u = tid + r * SM::NT;        // events 4u .. 4u+3
             cp_async16(&S.meta[sw32(u >> 1, u & 1)], P.meta + base + 4 * u);
         }
         cp_async_wait_all();
     } else {
         // partial or unaligned tile: element-wise, same layout
-        for (int e = tid; e < EV_TILE; e += EV_NT) {
+        for (int e = tid; e < SM::TILE; e += SM::NT) {
             int64_t i = base + e;
             int t = e >> 3, k = e & 7;
             int64_t *dst;
@@ -726,7 +727,7 @@ __device__ __forceinline__ int tile_head_scan_h(SM &S, unsigned &hmask, bool hea
     __syncthreads();
     int wbase = 0, tot = 0;
 #pragma unroll
-    for (int w = 0; w < EV_WARPS; w++) {
+    for (int w = 0; w < SM::WARPS; w++) {
         int c = S.wheads[w];
         if (w < warp) wbase += c;
         tot += c;
@@ -788,7 +789,7 @@ __device__ __forceinline__ void tile_finish(SM &S, const EvParams &P, bool has, 
     }
     if (lane == 31) { S.wagg[warp] = v; S.wflag[warp] = f; }
     __syncthreads();
-    if (tid < EV_WARPS) {                 // carry into warp tid: segmented combine of earlier warps
+    if (tid < SM::WARPS) {                 // carry into warp tid: segmented combine of earlier warps
         Acc c;
         c.zero();
         int cf = 0;
@@ -815,7 +816,7 @@ __device__ __forceinline__ void tile_finish(SM &S, const EvParams &P, bool has, 
         write_subrun(P, run0 - 1, e, base);
     }
     // the run open at the end of the tile
-    if (tid == EV_NT - 1 && base < N) {
+    if (tid == SM::NT - 1 && base < N) {
         Acc last = v;
         if (!f) {
             Acc c = S.wcarry[warp];
@@ -1029,7 +1030,8 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
 // take a binary search over the whole table in global memory: same answer, slower.
 // =================================================================================================
 constexpr int NTAB = 2;                // 0 combined key table (by dispatch time), 1 timeline (by start / end time)
-constexpr int POOL = 27648;            // bytes of staged windows per tile
+constexpr int W_NT = 256, W_TILE = W_NT * EV_IPT, W_WARPS = W_NT / 32;   // 2048-event tiles, 2 blocks per SM
+constexpr int POOL = 28672;            // bytes of staged windows per tile
 constexpr int SEED_W = 4;              // per tile: 2 seeds, the tile's gpu (lg), pad
 constexpr int KT_B = 16, TL_B = 44;    // staged bytes per entry: time + key; time + 3 intercepts + 3 slopes
 
@@ -1039,13 +1041,14 @@ struct TabWin {
     int n, off;           // staged entries (0 = look up in global memory), byte offset in the pool
 };
 struct EvSmemW {
-    longlong2 col[4][EV_TILE / 2];        // t_l, t_ks, t_ke, pred_end (64 KB)
-    uint4 meta[EV_TILE / 4];              // 8 KB
-    uint32_t kidx[EV_IPT][EV_NT];         // key of each event as a key-table index (8 KB), see key_at
-    unsigned long long lastk[EV_NT];      // key of each thread's last event slot
-    Acc wagg[EV_WARPS], wcarry[EV_WARPS];
-    int wflag[EV_WARPS], wcflag[EV_WARPS];
-    int wheads[EV_WARPS];
+    static constexpr int NT = W_NT, TILE = W_TILE, WARPS = W_WARPS;
+    longlong2 col[4][W_TILE / 2];         // t_l, t_ks, t_ke, pred_end (32 KB)
+    uint4 meta[W_TILE / 4];               // 4 KB
+    uint32_t kidx[EV_IPT][W_NT];          // key of each event as a key-table index (4 KB), see key_at
+    unsigned long long lastk[W_NT];       // key of each thread's last event slot
+    Acc wagg[W_WARPS], wcarry[W_WARPS];
+    int wflag[W_WARPS], wcflag[W_WARPS];
+    int wheads[W_WARPS];
     int64_t tile, excl;
     int tot;
     TabWin tw[NTAB];
@@ -1065,7 +1068,7 @@ __global__ void k_tile_seeds(EvParams P, int32_t *__restrict__ seeds) {
     const int lane = threadIdx.x & 31;
     const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (tile >= P.ntile) return;
-    const int64_t base = tile * EV_TILE, i = base + lane;
+    const int64_t base = tile * W_TILE, i = base + lane;
     const int lg = P.gpu_lg[gpu_of(P.meta[base])];
     const uint32_t m = i < P.N ? P.meta[i] : 0u;
     const bool cmp = i < P.N && kind_of(m) == CK_COMPUTE && P.gpu_lg[gpu_of(m)] == lg;
@@ -1114,18 +1117,16 @@ __device__ __forceinline__ void stage_windows(EvSmemW &W, const EvParams &P, int
             const int eb = x == 0 ? KT_B : TL_B;
             int fit = (POOL - off) / eb;
             if (fit < 0) fit = 0;
-            if (w.n > fit) w.n = fit & ~3;          // cut short: later queries go to global memory
+            if (w.n > fit) w.n = fit & ~3;          // cut short: later queries read global memory
             w.off = off;
             off += (w.n * eb + 15) & ~15;
-            const int64_t *T = x == 0 ? P.KTt : P.TLt;
-            w.next = w.lo + w.n < s_ge[x] ? __ldg(T + w.lo + w.n) : INT64_MAX;
         }
     }
     __syncthreads();
     {
         const TabWin w = W.tw[0];
         unsigned char *b = W.pool + w.off;
-        for (int j = tid; j < w.n; j += EV_NT) {
+        for (int j = tid; j < w.n; j += W_NT) {
             cp_async8(b + 8 * j, P.KTt + w.lo + j);
             cp_async8(b + 8 * (w.n + j), P.KTk + w.lo + j);
         }
@@ -1134,7 +1135,7 @@ __device__ __forceinline__ void stage_windows(EvSmemW &W, const EvParams &P, int
         const TabWin w = W.tw[1];
         unsigned char *b = W.pool + w.off;
         const int64_t cap = P.tl_cap;
-        for (int j = tid; j < w.n; j += EV_NT) {
+        for (int j = tid; j < w.n; j += W_NT) {
             const int64_t g = w.lo + j;
             cp_async8(b + 8 * j, P.TLt + g);
             cp_async8(b + 8 * (w.n + j), P.TLv + g);
@@ -1148,121 +1149,121 @@ __device__ __forceinline__ void stage_windows(EvSmemW &W, const EvParams &P, int
 }
 
 // register copy of one staged window
+// A lookup table of one gpu, [gb, ge) in global memory (entry gb = -inf sentinel), with entries [lo, lo + n)
+// staged in shared memory.  Every read goes to the staged copy when the index is inside it, else to global memory
+// (L1/L2): a window that was cut short, or a query outside it, costs latency, never correctness.
 struct WinR {
-    const int64_t *T;     // times in shared memory (payload follows)
+    const int64_t *T;     // staged times (payload follows)
+    const int64_t *G;     // global time column
+    int64_t lo, gb, ge;
     int n;
-    int64_t next;
 };
-__device__ __forceinline__ WinR win_reg(const EvSmemW &W, int x) {
+__device__ __forceinline__ WinR win_reg(const EvSmemW &W, int x, const EvParams &P) {
     const TabWin &w = W.tw[x];
     WinR r;
     r.T = reinterpret_cast<const int64_t *>(W.pool + w.off);
+    r.G = x == 0 ? P.KTt : P.TLt;
+    r.lo = w.lo;
     r.n = w.n;
-    r.next = w.next;
+    tab_bounds(P, x, W.lgP, &r.gb, &r.ge);
     return r;
 }
-
-// local index of the last window entry <= t, walking forward from the cursor c (-1: search the window);
-// -1 when t lies before the window, n - 1 with t >= next when it lies after it
-__device__ __forceinline__ int win_find(const int64_t *T, int n, int c, int64_t t) {
-    if (c < 0 || T[c] > t) {
-        int l = 0, h = n;
+// a global-only view of table x of gpu lg (events of a second gpu in the tile); out of line, it is rare
+__device__ __noinline__ longlong2 tab_bounds_ool(const int64_t *beg, const int64_t *len, int lg) {
+    const int64_t b = beg[lg];
+    return make_longlong2(b, len ? b + len[lg] : beg[lg + 1]);
+}
+__device__ __forceinline__ WinR win_global(const EvParams &P, int x, int lg) {
+    WinR r;
+    r.T = nullptr;
+    r.G = x == 0 ? P.KTt : P.TLt;
+    r.lo = 0;
+    r.n = 0;
+    const longlong2 b = x == 0 ? tab_bounds_ool(P.kt_beg, nullptr, lg) : tab_bounds_ool(P.tl_beg, P.tl_len, lg);
+    r.gb = b.x;
+    r.ge = b.y;
+    return r;
+}
+__device__ __forceinline__ bool win_in(const WinR &w, int64_t j) { return (uint64_t)(j - w.lo) < (uint64_t)w.n; }
+__device__ __forceinline__ int64_t win_t(const WinR &w, int64_t j) {
+    return win_in(w, j) ? w.T[j - w.lo] : __ldg(w.G + j);
+}
+__device__ __noinline__ int64_t win_search_global(const int64_t *G, int64_t lo, int64_t hi, int64_t t) {
+    return last_le(G, lo, hi, t);
+}
+// cursor: entry j answers every t in [a, b)
+constexpr uint32_t KIDX_NONE = 0xFFFFFFFFu;   // event slot past the end of the events
+struct WCur {
+    int64_t j, a, b;
+};
+__device__ __forceinline__ void wcur_init(WCur &k) { k.j = -1; k.a = INT64_MAX; k.b = INT64_MIN; }
+__device__ __forceinline__ void wcur_seek(const WinR &w, WCur &k, int64_t t) {
+    if (t >= k.a && t < k.b) return;
+    int64_t j;
+    if (k.j >= 0 && t >= k.a) {
+        j = k.j;                                     // walk forward from the cursor (queries mostly increase)
+    } else if (w.n > 0 && w.T[0] <= t) {             // search the staged window: last staged entry <= t
+        int l = 1, h = w.n;
         while (l < h) {
-            int m = (l + h) >> 1;
-            if (T[m] <= t) l = m + 1; else h = m;
+            const int m = (l + h) >> 1;
+            if (w.T[m] <= t) l = m + 1; else h = m;
         }
-        return l - 1;
+        j = w.lo + l - 1;
+    } else {
+        j = win_search_global(w.G, w.gb, w.ge, t);
     }
-    while (c + 1 < n && T[c + 1] <= t) c++;
-    return c;
+    bool done = false;
+#pragma unroll 1
+    for (int s = 0; s < 8; s++) {
+        if (j + 1 >= w.ge || win_t(w, j + 1) > t) { done = true; break; }
+        j++;
+    }
+    if (!done) j = win_search_global(w.G, j, w.ge, t);
+    k.j = j;
+    k.a = win_t(w, j);
+    k.b = j + 1 < w.ge ? win_t(w, j + 1) : INT64_MAX;
 }
-__device__ __forceinline__ bool win_ok(const WinR &w, int c, int64_t t) {
-    return c >= 0 && (c < w.n - 1 || t < w.next);
-}
-
-// global-memory lookups (outside the staged windows)
-__device__ __noinline__ unsigned long long key_global(const int64_t *Kt, const unsigned long long *Kk, int64_t gb,
-                                                      int64_t ge, int64_t t) {
-    return __ldg(Kk + last_le(Kt, gb, ge, t));
+__device__ __forceinline__ unsigned long long key_at(const WinR &w, const EvParams &P, int64_t j) {
+    return win_in(w, j) ? reinterpret_cast<const unsigned long long *>(w.T + w.n)[j - w.lo] : __ldg(P.KTk + j);
 }
 struct TlVal {
     unsigned long long cov, F, Pw;
 };
-__device__ __forceinline__ TlVal tl_eval(int64_t d, unsigned long long v0, unsigned long long v1, unsigned long long v2,
-                                         int32_t s0, int32_t s1, int32_t s2) {
+// coverage, frequency and power integrals at t from timeline entry j (affine in t - t0, wrapping)
+__device__ __forceinline__ TlVal tl_at(const WinR &w, const EvParams &P, int64_t j, int64_t t) {
+    unsigned long long v0, v1, v2;
+    int32_t s0, s1, s2;
+    if (win_in(w, j)) {
+        const int c = (int)(j - w.lo);
+        const int32_t *s32 = reinterpret_cast<const int32_t *>(w.T + 4 * w.n);
+        v0 = w.T[w.n + c]; v1 = w.T[2 * w.n + c]; v2 = w.T[3 * w.n + c];
+        s0 = s32[c]; s1 = s32[w.n + c]; s2 = s32[2 * w.n + c];
+    } else {
+        const int64_t cap = P.tl_cap;
+        v0 = __ldg(P.TLv + j); v1 = __ldg(P.TLv + cap + j); v2 = __ldg(P.TLv + 2 * cap + j);
+        s0 = __ldg(P.TLs + j); s1 = __ldg(P.TLs + cap + j); s2 = __ldg(P.TLs + 2 * cap + j);
+    }
+    const unsigned long long ud = (unsigned long long)(t - P.t0);
     TlVal r;
-    const unsigned long long ud = (unsigned long long)d;
     r.cov = v0 + (s0 ? ud : 0ull);
     r.F = v1 + (unsigned long long)(int64_t)s1 * ud;
     r.Pw = v2 + (unsigned long long)(int64_t)s2 * ud;
     return r;
-}
-__device__ __noinline__ TlVal tl_global(const int64_t *Tt, const int64_t *Tv, const int32_t *Ts, int64_t cap, int64_t gb,
-                                        int64_t ge, int64_t t, int64_t t0) {
-    const int64_t j = last_le(Tt, gb, ge, t);
-    return tl_eval(t - t0, (unsigned long long)__ldg(Tv + j), (unsigned long long)__ldg(Tv + cap + j),
-                   (unsigned long long)__ldg(Tv + 2 * cap + j), __ldg(Ts + j), __ldg(Ts + cap + j),
-                   __ldg(Ts + 2 * cap + j));
-}
-
-__device__ __forceinline__ unsigned long long key_w(const WinR &w, const EvParams &P, int64_t t, int &cur, bool prim,
-                                                    int lg) {
-    if (prim) {
-        const int c = win_find(w.T, w.n, cur, t);
-        if (win_ok(w, c, t)) {
-            cur = c;
-            return reinterpret_cast<const unsigned long long *>(w.T + w.n)[c];
-        }
-    }
-    return key_global(P.KTt, P.KTk, P.kt_beg[lg], P.kt_beg[lg + 1], t);
-}
-// key-table index of the innermost-key entry at t: the window-local index, or the global index with bit 31 set
-constexpr uint32_t KIDX_GLOBAL = 0x80000000u, KIDX_NONE = 0xFFFFFFFFu;
-__device__ __noinline__ uint32_t kidx_global(const int64_t *Kt, int64_t gb, int64_t ge, int64_t t) {
-    return (uint32_t)last_le(Kt, gb, ge, t) | KIDX_GLOBAL;
-}
-__device__ __forceinline__ uint32_t kidx_w(const WinR &w, const EvParams &P, int64_t t, int &cur, bool prim, int lg) {
-    if (prim) {
-        const int c = win_find(w.T, w.n, cur, t);
-        if (win_ok(w, c, t)) {
-            cur = c;
-            return (uint32_t)c;
-        }
-    }
-    return kidx_global(P.KTt, P.kt_beg[lg], P.kt_beg[lg + 1], t);
-}
-__device__ __forceinline__ unsigned long long key_at(const WinR &w, const EvParams &P, uint32_t v) {
-    if (v == KIDX_NONE) return CH_INVALID_KEY;
-    if (v & KIDX_GLOBAL) return __ldg(P.KTk + (v & ~KIDX_GLOBAL));
-    return reinterpret_cast<const unsigned long long *>(w.T + w.n)[v];
-}
-__device__ __forceinline__ TlVal tl_w(const WinR &w, const EvParams &P, int64_t t, int &cur, bool prim, int lg) {
-    if (prim) {
-        const int c = win_find(w.T, w.n, cur, t);
-        if (win_ok(w, c, t)) {
-            cur = c;
-            const int32_t *s32 = reinterpret_cast<const int32_t *>(w.T + 4 * w.n);
-            return tl_eval(t - P.t0, (unsigned long long)w.T[w.n + c], (unsigned long long)w.T[2 * w.n + c],
-                           (unsigned long long)w.T[3 * w.n + c], s32[c], s32[w.n + c], s32[2 * w.n + c]);
-        }
-    }
-    const int64_t gb = P.tl_beg[lg];
-    return tl_global(P.TLt, P.TLv, P.TLs, P.tl_cap, gb, gb + P.tl_len[lg], t, P.t0);
 }
 
 // ---- sub-run heads per tile (first pass): the same keys and head rule as k_events_w, counted, so that the main
 // pass knows every tile's first sub-run id up front (an exclusive scan of the counts) instead of waiting on a
 // look-back chain that any slow tile would stall for all later ones.  Columns are read straight from global
 // memory (8 consecutive events per thread, 16 B loads); only the key-table window is staged.
-constexpr int HD_POOL = 18432;
-__global__ void __launch_bounds__(EV_NT) k_tile_heads(EvParams P, int64_t *__restrict__ tile_cnt) {
+constexpr int HD_POOL = 20480;
+__global__ void __launch_bounds__(W_NT) k_tile_heads(EvParams P, int64_t *__restrict__ tile_cnt) {
     __shared__ __align__(16) unsigned char pool[HD_POOL];
-    __shared__ int64_t s_lo, s_next;
+    __shared__ int64_t s_lo;
     __shared__ int s_n, s_lg;
-    __shared__ unsigned long long s_last[EV_WARPS];
-    __shared__ int s_cnt[EV_WARPS];
+    __shared__ unsigned long long s_last[W_WARPS];
+    __shared__ int s_cnt[W_WARPS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = blockIdx.x, base = tile * EV_TILE, i0 = base + (int64_t)tid * EV_IPT, N = P.N;
+    const int64_t tile = blockIdx.x, base = tile * W_TILE, i0 = base + (int64_t)tid * EV_IPT, N = P.N;
     if (tid == 0) {
         const int32_t *sd = P.seeds + tile * SEED_W;
         const int lg = sd[NTAB];
@@ -1275,13 +1276,12 @@ __global__ void __launch_bounds__(EV_NT) k_tile_heads(EvParams P, int64_t *__res
         int n = (int)(hi - lo);
         if (n > HD_POOL / KT_B) n = (HD_POOL / KT_B) & ~3;
         s_lo = lo; s_n = n; s_lg = lg;
-        s_next = lo + n < ge ? __ldg(P.KTt + lo + n) : INT64_MAX;
     }
     __syncthreads();
     {
         const int64_t lo = s_lo;
         const int n = s_n;
-        for (int j = tid; j < n; j += EV_NT) {
+        for (int j = tid; j < n; j += W_NT) {
             cp_async8(pool + 8 * j, P.KTt + lo + j);
             cp_async8(pool + 8 * (n + j), P.KTk + lo + j);
         }
@@ -1309,24 +1309,37 @@ __global__ void __launch_bounds__(EV_NT) k_tile_heads(EvParams P, int64_t *__res
     }
     cp_async_wait_all();
     __syncthreads();
+    const int lgP = s_lg;
     WinR wk;
     wk.T = reinterpret_cast<const int64_t *>(pool);
+    wk.G = P.KTt;
+    wk.lo = s_lo;
     wk.n = s_n;
-    wk.next = s_next;
-    const int lgP = s_lg;
-    int ck = -1;
+    wk.gb = P.kt_beg[lgP];
+    wk.ge = P.kt_beg[lgP + 1];
+    WCur ck;
+    wcur_init(ck);
+    int lgc = lgP;
     unsigned long long prevk = CH_INVALID_KEY, first = CH_INVALID_KEY;
+    int64_t prevj = -1;
     int nh = 0;
 #pragma unroll
     for (int k = 0; k < EV_IPT; k++) {
-        unsigned long long kk = CH_INVALID_KEY;
         if (k < nv) {
             const int lg = P.gpu_lg[gpu_of(mt[k])];
-            kk = key_w(wk, P, tl[k], ck, lg == lgP, lg);
-            if (k > 0 && kk != prevk) nh++;
+            if (lg != lgc) { wk = win_global(P, 0, lg); wcur_init(ck); lgc = lg; }
+            wcur_seek(wk, ck, tl[k]);
+            if (ck.j != prevj) {
+                const unsigned long long kk = key_at(wk, P, ck.j);
+                if (k > 0 && kk != prevk) nh++;
+                prevk = kk;
+                prevj = ck.j;
+            }
+        } else {
+            prevk = CH_INVALID_KEY;
+            prevj = -1;
         }
-        if (k == 0) first = kk;
-        prevk = kk;
+        if (k == 0) first = prevk;
     }
     // head at the thread's first event: tile start, or a key change from the previous thread's last event
     unsigned long long pl = __shfl_up_sync(CH_FULL, prevk, 1);
@@ -1340,48 +1353,59 @@ __global__ void __launch_bounds__(EV_NT) k_tile_heads(EvParams P, int64_t *__res
     __syncthreads();
     if (tid == 0) {
         int64_t t = 0;
-        for (int w = 0; w < EV_WARPS; w++) t += s_cnt[w];
+        for (int w = 0; w < W_WARPS; w++) t += s_cnt[w];
         tile_cnt[tile] = t;
     }
 }
 
-__global__ void __launch_bounds__(EV_NT, 2) k_events_w(EvParams P, int vec_ok) {
+__global__ void __launch_bounds__(W_NT, 2) k_events_w(EvParams P, int vec_ok) {
     extern __shared__ __align__(16) unsigned char ev_dsm[];
     EvSmemW &S = *reinterpret_cast<EvSmemW *>(ev_dsm);
     const int tid = threadIdx.x;
     const int64_t tile = blockIdx.x;
     if (tid == 0) { S.excl = P.tile_base[tile]; S.tot = (int)(P.tile_base[tile + 1] - P.tile_base[tile]); }
-    const int64_t base = tile * EV_TILE;
+    const int64_t base = tile * W_TILE;
     const int64_t i0 = base + (int64_t)tid * EV_IPT;
     const int64_t N = P.N;
     stage_windows(S, P, tile);
-    stage_tile(S, P, base, vec_ok && base + EV_TILE <= N);
+    stage_tile(S, P, base, vec_ok && base + W_TILE <= N);
     cp_async_wait_all();
     __syncthreads();
     const int nv = i0 >= N ? 0 : (int)min((int64_t)EV_IPT, N - i0);
     const int lgP = S.lgP;
-    const WinR wk = win_reg(S, 0);
+    const WinR wkP = win_reg(S, 0, P);
 
     // ---- phase A: instance key of every event (a5): the combined key table at the dispatch time ----
     unsigned hmask = 0;
     unsigned long long firstk = CH_INVALID_KEY;
     {
-        int ck = -1;
+        WinR wk = wkP;
+        int lgc = lgP;
+        WCur ck;
+        wcur_init(ck);
         unsigned long long prevk = CH_INVALID_KEY;
+        int64_t prevj = -1;
 #pragma unroll 1
         for (int k = 0; k < EV_IPT; k++) {
-            unsigned long long kk = CH_INVALID_KEY;
             uint32_t v = KIDX_NONE;
             if (k < nv) {
                 const int64_t t = ev_col(S, 0, tid, k);
                 const int lg = P.gpu_lg[gpu_of(ev_meta(S, tid, k))];
-                v = kidx_w(wk, P, t, ck, lg == lgP, lg);
-                kk = key_at(wk, P, v);
-                if (k > 0 && kk != prevk) hmask |= 1u << k;
+                if (lg != lgc) { wk = win_global(P, 0, lg); wcur_init(ck); lgc = lg; }
+                wcur_seek(wk, ck, t);
+                v = (uint32_t)ck.j;
+                if (ck.j != prevj) {                  // same entry => same key; else compare the keys
+                    const unsigned long long kk = key_at(wk, P, ck.j);
+                    if (k > 0 && kk != prevk) hmask |= 1u << k;
+                    prevk = kk;
+                    prevj = ck.j;
+                }
+            } else {
+                prevk = CH_INVALID_KEY;
+                prevj = -1;
             }
-            if (k == 0) firstk = kk;
+            if (k == 0) firstk = prevk;
             S.kidx[k][tid] = v;
-            prevk = kk;
         }
         S.lastk[tid] = prevk;
     }
@@ -1396,20 +1420,25 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events_w(EvParams P, int vec_ok) {
     p0.zero();
     bool has = false;
     int64_t curid = run0 - 1;
-    const WinR wt = win_reg(S, 1);
-    int ct = -1;
+    const WinR wtP = win_reg(S, 1, P);
+    WinR wt = wtP;
+    int lgc = lgP;
+    WCur ct;
+    wcur_init(ct);
 #pragma unroll 1
     for (int k = 0; k < EV_IPT; k++) {
         if (k >= nv) break;
         const int64_t i = i0 + k;
         const uint32_t m = ev_meta(S, tid, k);
         const int lg = P.gpu_lg[gpu_of(m)];
+        const bool prim = lg == lgP;
         if ((hmask >> k) & 1u) {
             if (!has) { p0 = cur; has = true; }
             else write_subrun(P, curid, cur, base);
             curid++;
             cur.zero();
-            P.sr_key[curid] = key_at(wk, P, S.kidx[k][tid]);
+            const uint32_t v = S.kidx[k][tid];
+            P.sr_key[curid] = key_at(prim ? wkP : win_global(P, 0, lg), P, (int64_t)v);
             P.sr_first[curid] = i;
         }
         const int kd = kind_of(m);
@@ -1428,9 +1457,11 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events_w(EvParams P, int vec_ok) {
                 const int64_t c = c1 < c2 ? c1 : c2;                    // Eq. 2
                 call = c > 0 ? c : 0;
             }
-            const bool prim = lg == lgP;
-            const TlVal va = tl_w(wt, P, ks, ct, prim, lg);
-            const TlVal vb = tl_w(wt, P, ke, ct, prim, lg);
+            if (lg != lgc) { wt = win_global(P, 1, lg); wcur_init(ct); lgc = lg; }
+            wcur_seek(wt, ct, ks);
+            const TlVal va = tl_at(wt, P, ct.j, ks);
+            wcur_seek(wt, ct, ke);
+            const TlVal vb = tl_at(wt, P, ct.j, ke);
             ovl = (int64_t)(vb.cov - va.cov);                           // |[t_ks, t_ke) ∩ U_g| (D9)
             phi = (int64_t)(vb.F - va.F);                               // MHz*ns (D10)
             psi = (int64_t)(vb.Pw - va.Pw);                             // mW*ns
@@ -1600,7 +1631,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     ctx->sub.first_event = CH_ALLOC(ctx, int64_t, N + 1);
     ctx->sub.f = CH_ALLOC(ctx, int64_t, (int64_t)SR_W * N);
     ctx->d_run_id = CH_ALLOC(ctx, int32_t, N);
-    ctx->d_tile_state = CH_ALLOC(ctx, unsigned long long, ntile);
+    ctx->d_tile_state = CH_ALLOC(ctx, unsigned long long, ceil_div(N, W_TILE));   // >= tiles of either pass
     ctx->d_tile_ticket = CH_ALLOC(ctx, unsigned int, 1);
     CH_ALLOC_END(ctx);
     CH_CUDA(ctx, cudaMemsetAsync(ctx->d_tile_state, 0, 8 * ntile, ctx->st));
@@ -1639,6 +1670,8 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     int vec_ok = al16(P.tl) && al16(P.ks) && al16(P.ke) && al16(P.pred_end) && al16(P.meta);
     if (ctx->et_ok) {
         // every span list laminar: Euler boundary tables, window-staged lookups
+        ntile = ceil_div(N, W_TILE);
+        P.ntile = ntile;
         size_t mark = ctx->used;
         int32_t *seeds = CH_ALLOC(ctx, int32_t, ntile * SEED_W);
         int64_t *tcnt = CH_ALLOC(ctx, int64_t, ntile + 1), *tbase = CH_ALLOC(ctx, int64_t, ntile + 1);
@@ -1653,11 +1686,11 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         ch_tick(ctx, 4, 0);
         k_tile_seeds<<<(unsigned)ceil_div(ntile * 32, NT), NT, 0, ctx->st>>>(P, seeds);
         CH_LAUNCHED(ctx);
-        k_tile_heads<<<(unsigned)ntile, EV_NT, 0, ctx->st>>>(P, tcnt);
+        k_tile_heads<<<(unsigned)ntile, W_NT, 0, ctx->st>>>(P, tcnt);
         CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, tcnt, tbase, ntile, tbase + ntile));
         P.tile_base = tbase;
-        k_events_w<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P, vec_ok);
+        k_events_w<<<(unsigned)ntile, W_NT, dsm, ctx->st>>>(P, vec_ok);
         CH_LAUNCHED(ctx);
         ch_tick(ctx, 4, 1);
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_tile_state + ntile - 1, tbase + ntile, 8, cudaMemcpyDeviceToDevice, ctx->st));
