@@ -442,6 +442,101 @@ __global__ void k_group_finish(int64_t *__restrict__ starts, const int64_t *__re
                                const unsigned long long *__restrict__ nvalid) {
     starts[*ng] = (int64_t)*nvalid;
 }
+// One pass per grouping: heads (first key of each run of equal key >> shift among the valid keys, which sort
+// first), their exclusive scan by a chained scan with decoupled look-back, and starts[g] = position of group g's
+// first key; the block holding the last valid key writes the group count and starts[count] = the number of
+// valid keys.  Blocks past the device-side count exit at once (nobody looks back past the last valid key).
+constexpr int GP_NT = 256, GP_IPT = 8, GP_TILE = GP_NT * GP_IPT;
+constexpr unsigned long long GP_A = 1ull << 62, GP_P = 2ull << 62, GP_MASK = (1ull << 62) - 1;
+__global__ void __launch_bounds__(GP_NT) k_group_1pass(const unsigned long long *__restrict__ key, int64_t n,
+                                                        const int64_t *__restrict__ n_dev, int shift,
+                                                        int64_t *__restrict__ starts, int64_t *__restrict__ ng,
+                                                        unsigned long long *__restrict__ state,
+                                                        unsigned int *__restrict__ ticket) {
+    __shared__ int s_w[GP_NT / 32];
+    __shared__ int64_t s_tile, s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ne = dev_n(n, n_dev);
+    if (tid == 0) s_tile = (int64_t)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t b0 = tile * GP_TILE;
+    if (b0 >= ne && !(ne == 0 && tile == 0)) return;
+    const int64_t j0 = b0 + (int64_t)tid * GP_IPT;
+    unsigned long long prev = j0 > 0 && j0 - 1 < ne ? key[j0 - 1] : CH_INVALID_KEY;
+    unsigned hm = 0;
+    int last_valid = -1;       // k of the last valid key of the tile, if its successor is invalid / past the end
+#pragma unroll
+    for (int k = 0; k < GP_IPT; k++) {
+        const int64_t j = j0 + k;
+        const unsigned long long x = j < ne ? key[j] : CH_INVALID_KEY;
+        if (x != CH_INVALID_KEY) {
+            const unsigned long long g = shift >= 64 ? 0ull : (x >> shift);
+            const unsigned long long gp = shift >= 64 ? 0ull : (prev >> shift);
+            if (j == 0 || prev == CH_INVALID_KEY || gp != g) hm |= 1u << k;
+            if (j + 1 >= ne || key[j + 1] == CH_INVALID_KEY) last_valid = k;
+        }
+        prev = x;
+    }
+    const int nh = __popc(hm);
+    int wex = nh;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(CH_FULL, wex, o);
+        if (lane >= o) wex += y;
+    }
+    if (lane == 31) s_w[warp] = wex;
+    wex -= nh;
+    __syncthreads();
+    int wb = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < GP_NT / 32; w++) {
+        const int c = s_w[w];
+        if (w < warp) wb += c;
+        tot += c;
+    }
+    if (warp == 0) {
+        int64_t excl = 0;
+        if (tile == 0) {
+            if (lane == 0) atomicExch(&state[0], GP_P | (unsigned long long)tot);
+        } else {
+            if (lane == 0) atomicExch(&state[tile], GP_A | (unsigned long long)tot);
+            int64_t p = tile - 1 - lane;
+            while (true) {
+                unsigned long long st = GP_P;
+                if (p >= 0) st = *((volatile unsigned long long *)&state[p]);
+                const unsigned fl = (unsigned)(st >> 62);
+                const unsigned pm = __ballot_sync(CH_FULL, fl == 2u), zm = __ballot_sync(CH_FULL, fl == 0u);
+                const int fp = pm ? __ffs(pm) - 1 : 32;
+                const unsigned need = fp >= 31 ? CH_FULL : ((2u << fp) - 1u);
+                if (zm & need) continue;
+                int64_t x = lane <= fp ? (int64_t)(st & GP_MASK) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(CH_FULL, x, o);
+                excl += x;
+                if (fp < 32) break;
+                p -= 32;
+            }
+            if (lane == 0) atomicExch(&state[tile], GP_P | (unsigned long long)(excl + tot));
+        }
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    int64_t o = s_excl + wb + wex;
+#pragma unroll
+    for (int k = 0; k < GP_IPT; k++)
+        if ((hm >> k) & 1u) starts[o++] = j0 + k;
+    if (last_valid >= 0) {
+        const int64_t cnt = s_excl + tot;
+        *ng = cnt;
+        starts[cnt] = j0 + last_valid + 1;
+    }
+    if (tile == 0 && tid == 0 && (ne == 0 || key[0] == CH_INVALID_KEY)) {
+        *ng = 0;
+        starts[0] = 0;
+    }
+}
+
 __global__ void k_group_heads(const unsigned long long *__restrict__ key, int64_t n, const int64_t *__restrict__ n_dev,
                               int shift, int64_t *__restrict__ head, unsigned long long *__restrict__ nvalid) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -975,25 +1070,18 @@ static unsigned grid_for(int64_t upper, int per_block) {
 static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sorted, int64_t n, const int64_t *n_dev,
                             int shift, int64_t **starts_out, int64_t **ng_out) {
     CH_ALLOC_BEGIN;
-    int64_t *head = CH_ALLOC(ctx, int64_t, n + 1);
-    int64_t *ex = CH_ALLOC(ctx, int64_t, n + 1);
     int64_t *starts = CH_ALLOC(ctx, int64_t, n + 2);
-    unsigned long long *nv = CH_ALLOC(ctx, unsigned long long, 1);
     int64_t *tot = CH_ALLOC(ctx, int64_t, 1);
     CH_ALLOC_END(ctx);
-    k_group_init<<<1, 1, 0, ctx->st>>>(nv, n, n_dev);
+    const int64_t ntile = std::max<int64_t>(ceil_div(n, GP_TILE), 1);
+    size_t mark = ctx->used;
+    unsigned long long *state = CH_ALLOC(ctx, unsigned long long, ntile + 1);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemsetAsync(state, 0, 8 * (size_t)(ntile + 1), ctx->st));
+    k_group_1pass<<<(unsigned)ntile, GP_NT, 0, ctx->st>>>(keys_sorted, n, n_dev, shift, starts, tot, state,
+                                                         reinterpret_cast<unsigned int *>(state + ntile));
     CH_LAUNCHED(ctx);
-    if (n > 0) {
-        k_group_heads<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(keys_sorted, n, n_dev, shift, head, nv);
-        CH_LAUNCHED(ctx);
-        CH_TRY(ch_scan_excl_i64(ctx, head, ex, n, tot));
-        k_group_starts<<<(unsigned)ceil_div(n, NT), NT, 0, ctx->st>>>(head, ex, n, starts);
-        CH_LAUNCHED(ctx);
-    } else {
-        CH_CUDA(ctx, cudaMemsetAsync(tot, 0, 8, ctx->st));
-    }
-    k_group_finish<<<1, 1, 0, ctx->st>>>(starts, tot, nv);
-    CH_LAUNCHED(ctx);
+    ctx->used = mark;
     *starts_out = starts;
     *ng_out = tot;
     return CHOPPER_OK;
