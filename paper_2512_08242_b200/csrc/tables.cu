@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
                 } else {
 #pragma unroll
                     for (int q = 0; q < CT_SG; q++)
-                        if (s0 + q < C) out[(int64_t)(s0 + q) * cap + rid[k > 0 ? k - 1 : 0]] = c[q];
+                        if (s0 + q < C) out[(int64_t)(s0 + q) + (int64_t)rid[k > 0 ? k - 1 : 0] * C] = c[q];
                 }
 #pragma unroll
                 for (int q = 0; q < CT_SG; q++) c[q] = 0.0;
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
         if (has && tid > 0) {
 #pragma unroll
             for (int q = 0; q < CT_SG; q++)
-                if (s0 + q < C) out[(int64_t)(s0 + q) * cap + prev] = e[q] + p0[q];
+                if (s0 + q < C) out[(int64_t)(s0 + q) + (int64_t)prev * C] = e[q] + p0[q];
         }
         // the run open at the end of the tile
         if (tid == CT_NT - 1 && base < N) {
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
             const int32_t id = run_id[last];
 #pragma unroll
             for (int q = 0; q < CT_SG; q++)
-                if (s0 + q < C) out[(int64_t)(s0 + q) * cap + id] = f ? v[q] : S.carry[warp][q] + v[q];
+                if (s0 + q < C) out[(int64_t)(s0 + q) + (int64_t)id * C] = f ? v[q] : S.carry[warp][q] + v[q];
         }
         __syncthreads();                      // S.x / S.carry reused by the next slot group
     }
@@ -449,7 +449,7 @@ __global__ void k_group_finish(int64_t *__restrict__ starts, const int64_t *__re
 constexpr int GP_NT = 256, GP_IPT = 8, GP_TILE = GP_NT * GP_IPT;
 constexpr unsigned long long GP_A = 1ull << 62, GP_P = 2ull << 62, GP_MASK = (1ull << 62) - 1;
 __global__ void __launch_bounds__(GP_NT) k_group_1pass(const unsigned long long *__restrict__ key, int64_t n,
-                                                        const int64_t *__restrict__ n_dev, int shift,
+                                                        const int64_t *__restrict__ n_dev, int shift, int all,
                                                         int64_t *__restrict__ starts, int64_t *__restrict__ ng,
                                                         unsigned long long *__restrict__ state,
                                                         unsigned int *__restrict__ ticket) {
@@ -470,11 +470,11 @@ __global__ void __launch_bounds__(GP_NT) k_group_1pass(const unsigned long long 
     for (int k = 0; k < GP_IPT; k++) {
         const int64_t j = j0 + k;
         const unsigned long long x = j < ne ? key[j] : CH_INVALID_KEY;
-        if (x != CH_INVALID_KEY) {
+        if (j < ne && (all || x != CH_INVALID_KEY)) {
             const unsigned long long g = shift >= 64 ? 0ull : (x >> shift);
             const unsigned long long gp = shift >= 64 ? 0ull : (prev >> shift);
-            if (j == 0 || prev == CH_INVALID_KEY || gp != g) hm |= 1u << k;
-            if (j + 1 >= ne || key[j + 1] == CH_INVALID_KEY) last_valid = k;
+            if (j == 0 || (!all && prev == CH_INVALID_KEY) || gp != g) hm |= 1u << k;
+            if (j + 1 >= ne || (!all && key[j + 1] == CH_INVALID_KEY)) last_valid = k;
         }
         prev = x;
     }
@@ -531,10 +531,89 @@ __global__ void __launch_bounds__(GP_NT) k_group_1pass(const unsigned long long 
         *ng = cnt;
         starts[cnt] = j0 + last_valid + 1;
     }
-    if (tile == 0 && tid == 0 && (ne == 0 || key[0] == CH_INVALID_KEY)) {
+    if (tile == 0 && tid == 0 && (ne == 0 || (!all && key[0] == CH_INVALID_KEY))) {
         *ng = 0;
         starts[0] = 0;
     }
+}
+
+// valid keys (with their values) to the front in order, invalid ones to the back (reversed: their order is
+// never used), one chained-scan pass; *nvalid = the number of valid keys (written by the last tile)
+__global__ void __launch_bounds__(GP_NT) k_compact_1pass(const unsigned long long *__restrict__ ki,
+                                                          const uint32_t *__restrict__ vi, int64_t n,
+                                                          unsigned long long *__restrict__ ko, uint32_t *__restrict__ vo,
+                                                          int64_t *__restrict__ nvalid,
+                                                          unsigned long long *__restrict__ state,
+                                                          unsigned int *__restrict__ ticket) {
+    __shared__ int s_w[GP_NT / 32];
+    __shared__ int64_t s_tile, s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = (int64_t)atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t j0 = tile * GP_TILE + (int64_t)tid * GP_IPT;
+    unsigned long long x[GP_IPT];
+    unsigned vm = 0;
+#pragma unroll
+    for (int k = 0; k < GP_IPT; k++) {
+        x[k] = j0 + k < n ? ki[j0 + k] : CH_INVALID_KEY;
+        if (j0 + k < n && x[k] != CH_INVALID_KEY) vm |= 1u << k;
+    }
+    const int nh = __popc(vm);
+    int wex = nh;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(CH_FULL, wex, o);
+        if (lane >= o) wex += y;
+    }
+    if (lane == 31) s_w[warp] = wex;
+    wex -= nh;
+    __syncthreads();
+    int wb = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < GP_NT / 32; w++) {
+        const int c = s_w[w];
+        if (w < warp) wb += c;
+        tot += c;
+    }
+    if (warp == 0) {
+        int64_t excl = 0;
+        if (tile == 0) {
+            if (lane == 0) atomicExch(&state[0], GP_P | (unsigned long long)tot);
+        } else {
+            if (lane == 0) atomicExch(&state[tile], GP_A | (unsigned long long)tot);
+            int64_t p = tile - 1 - lane;
+            while (true) {
+                unsigned long long st = GP_P;
+                if (p >= 0) st = *((volatile unsigned long long *)&state[p]);
+                const unsigned fl = (unsigned)(st >> 62);
+                const unsigned pm = __ballot_sync(CH_FULL, fl == 2u), zm = __ballot_sync(CH_FULL, fl == 0u);
+                const int fp = pm ? __ffs(pm) - 1 : 32;
+                const unsigned need = fp >= 31 ? CH_FULL : ((2u << fp) - 1u);
+                if (zm & need) continue;
+                int64_t y = lane <= fp ? (int64_t)(st & GP_MASK) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(CH_FULL, y, o);
+                excl += y;
+                if (fp < 32) break;
+                p -= 32;
+            }
+            if (lane == 0) atomicExch(&state[tile], GP_P | (unsigned long long)(excl + tot));
+        }
+        if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    int64_t e = s_excl + wb + wex;                  // valid keys before this thread's first
+#pragma unroll
+    for (int k = 0; k < GP_IPT; k++) {
+        const int64_t j = j0 + k;
+        if (j >= n) break;
+        const int64_t p = ((vm >> k) & 1u) ? e : n - 1 - (j - e);
+        ko[p] = x[k];
+        vo[p] = vi[j];
+        e += (vm >> k) & 1u;
+    }
+    if (j0 <= n - 1 && n - 1 < j0 + GP_IPT) *nvalid = e;
 }
 
 __global__ void k_group_heads(const unsigned long long *__restrict__ key, int64_t n, const int64_t *__restrict__ n_dev,
@@ -560,8 +639,9 @@ struct TabView {
     int64_t *f;
     double *cnt;
     int64_t cap;     // field stride (field-major tables: capacity; AoS sub-runs: 1)
-    int64_t ccap;    // counter-column capacity
+    int64_t ccap;    // counter-column stride (field-major tables: capacity; AoS sub-run counters: 1)
     int64_t rs;      // row stride (field-major: 1; AoS sub-runs: 16)
+    int64_t crs;     // counter row stride (field-major: 1; AoS sub-run counters: C)
 };
 
 // parent row p = sum of children [starts[p], starts[p+1]) (through perm if given).  Integer fields are
@@ -626,7 +706,7 @@ __device__ __forceinline__ void sum_rows_thread_body(const TabView &ch, const ui
         pa.key[p] = shift >= 64 ? 0ull : ((k0 >> shift) << shift);
         for (int s = 0; s < C; s++) {
             double acc = 0.0;
-            for (int64_t j = lo; j < hi; j++) acc += ch.cnt[(int64_t)s * ch.ccap + (perm ? (int64_t)perm[j] : j)];
+            for (int64_t j = lo; j < hi; j++) acc += ch.cnt[(int64_t)s * ch.ccap + (perm ? (int64_t)perm[j] : j) * ch.crs];
             pa.cnt[(int64_t)s * pa.ccap + p] = acc;
         }
     }
@@ -653,7 +733,7 @@ __device__ __forceinline__ void sum_rows_thread_body(const TabView &ch, const ui
         }
         for (int s = 0; s < C; s++) {
             double acc = 0.0;
-            for (int64_t j = qlo + lane; j < qhi; j += 32) acc += ch.cnt[(int64_t)s * ch.ccap + (perm ? (int64_t)perm[j] : j)];
+            for (int64_t j = qlo + lane; j < qhi; j += 32) acc += ch.cnt[(int64_t)s * ch.ccap + (perm ? (int64_t)perm[j] : j) * ch.crs];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(CH_FULL, acc, o);
             if (lane == 0) pa.cnt[(int64_t)s * pa.ccap + q] = acc;
@@ -692,7 +772,7 @@ __global__ void __launch_bounds__(256) k_sum_rows_warp(TabView ch, const uint32_
         a.add_child(ch, c);
 #pragma unroll
         for (int s = 0; s < CMAX; s++)
-            if (s < C) acc[s] += ch.cnt[(int64_t)s * ch.ccap + c];
+            if (s < C) acc[s] += ch.cnt[(int64_t)s * ch.ccap + (c) * ch.crs];
     }
     a.warp_all();
     if (lane < RF_NFIELDS) {
@@ -754,13 +834,13 @@ __global__ void __launch_bounds__(RC_NT) k_sum_rows_chunked(TabView ch, const ui
                 for (int f = 0; f < RF_NFIELDS; f++) x[f] = __ldg(ch.f + (int64_t)f * ch.cap + c);
                 int64_t y[8];
 #pragma unroll
-                for (int q = 0; q < 8; q++) y[q] = q < C ? __double_as_longlong(__ldg(ch.cnt + (int64_t)q * ch.ccap + c)) : 0;
+                for (int q = 0; q < 8; q++) y[q] = q < C ? __double_as_longlong(__ldg(ch.cnt + (int64_t)q * ch.ccap + c * ch.crs)) : 0;
 #pragma unroll
                 for (int f = 0; f < RF_NFIELDS; f++) vals[f * RC_CH + tid] = x[f];
 #pragma unroll
                 for (int q = 0; q < 8; q++) if (q < C) vals[(RF_NFIELDS + q) * RC_CH + tid] = y[q];
                 for (int q = 8; q < C; q++)
-                    vals[(RF_NFIELDS + q) * RC_CH + tid] = __double_as_longlong(ch.cnt[(int64_t)q * ch.ccap + c]);
+                    vals[(RF_NFIELDS + q) * RC_CH + tid] = __double_as_longlong(ch.cnt[(int64_t)q * ch.ccap + (c) * ch.crs]);
             }
         } else {
             for (int t = tid; t < m; t += RC_NT) {
@@ -771,13 +851,13 @@ __global__ void __launch_bounds__(RC_NT) k_sum_rows_chunked(TabView ch, const ui
                 for (int f = 0; f < RF_NFIELDS; f++) x[f] = __ldg(row + (int64_t)f * ch.cap);
                 int64_t y[8];
 #pragma unroll
-                for (int q = 0; q < 8; q++) y[q] = q < C ? __double_as_longlong(__ldg(ch.cnt + (int64_t)q * ch.ccap + c)) : 0;
+                for (int q = 0; q < 8; q++) y[q] = q < C ? __double_as_longlong(__ldg(ch.cnt + (int64_t)q * ch.ccap + c * ch.crs)) : 0;
 #pragma unroll
                 for (int f = 0; f < RF_NFIELDS; f++) vals[f * RC_CH + t] = x[f];
 #pragma unroll
                 for (int q = 0; q < 8; q++) if (q < C) vals[(RF_NFIELDS + q) * RC_CH + t] = y[q];
                 for (int s2 = 8; s2 < C; s2++)
-                    vals[(RF_NFIELDS + s2) * RC_CH + t] = __double_as_longlong(ch.cnt[(int64_t)s2 * ch.ccap + c]);
+                    vals[(RF_NFIELDS + s2) * RC_CH + t] = __double_as_longlong(ch.cnt[(int64_t)s2 * ch.ccap + (c) * ch.crs]);
             }
         }
         __syncthreads();
@@ -1068,7 +1148,7 @@ static unsigned grid_for(int64_t upper, int per_block) {
 // group the sorted children (count *n_dev, upper bound n) by key >> shift: group starts and the group
 // count stay on the device (no host round trip); starts[ng] = end of the last group (first invalid key)
 static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sorted, int64_t n, const int64_t *n_dev,
-                            int shift, int64_t **starts_out, int64_t **ng_out) {
+                            int shift, int64_t **starts_out, int64_t **ng_out, int all = 0) {
     CH_ALLOC_BEGIN;
     int64_t *starts = CH_ALLOC(ctx, int64_t, n + 2);
     int64_t *tot = CH_ALLOC(ctx, int64_t, 1);
@@ -1078,7 +1158,7 @@ static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sor
     unsigned long long *state = CH_ALLOC(ctx, unsigned long long, ntile + 1);
     CH_ALLOC_END(ctx);
     CH_CUDA(ctx, cudaMemsetAsync(state, 0, 8 * (size_t)(ntile + 1), ctx->st));
-    k_group_1pass<<<(unsigned)ntile, GP_NT, 0, ctx->st>>>(keys_sorted, n, n_dev, shift, starts, tot, state,
+    k_group_1pass<<<(unsigned)ntile, GP_NT, 0, ctx->st>>>(keys_sorted, n, n_dev, shift, all, starts, tot, state,
                                                          reinterpret_cast<unsigned int *>(state + ntile));
     CH_LAUNCHED(ctx);
     ctx->used = mark;
@@ -1087,7 +1167,7 @@ static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sor
     return CHOPPER_OK;
 }
 
-static TabView view(RowTable &t) { return TabView{t.key, t.f, t.cnt, t.cap, t.cap, 1}; }
+static TabView view(RowTable &t) { return TabView{t.key, t.f, t.cnt, t.cap, t.cap, 1, 1}; }
 
 // parents of the groups: mode 0 = children staged per block (many parents, few children each),
 // 1 = a warp per parent (few parents, many children), 2 = a lane per parent
@@ -1157,7 +1237,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
     if (ctx->n_lg)
         CH_CUDA(ctx, cudaMemcpyAsync(lg_gpu_d, ctx->h_lg_gpu.data(), 4 * ctx->n_lg, cudaMemcpyHostToDevice, ctx->st));
     ctx->sub.cap = std::max<int64_t>(R, 1);
-    TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, 1, std::max<int64_t>(R, 1), 16};   // AoS sub-run rows
+    TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, 1, 1, 16, std::max(C, 1)};   // AoS sub-run rows and counters
     if (C > 0 && R > 0) {
         const int n_lg = ctx->n_lg;
         ctx->d_colbad = CH_ALLOC(ctx, unsigned int, (int64_t)n_lg * C);
@@ -1185,18 +1265,12 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         bool done = false;
         if (R > 1) {
             size_t mk = ctx->used;
-            int64_t *hd = CH_ALLOC(ctx, int64_t, R), *ex = CH_ALLOC(ctx, int64_t, R), *st = CH_ALLOC(ctx, int64_t, R + 2);
-            int64_t *nseg_d = CH_ALLOC(ctx, int64_t, 1), *nv_d = CH_ALLOC(ctx, int64_t, 1);
+            int64_t *nv_d = CH_ALLOC(ctx, int64_t, 1);
             unsigned int *bad = CH_ALLOC(ctx, unsigned int, 1);
             CH_ALLOC_END(ctx);
-            k_prefix_heads<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, R, L.sh_it, hd);
-            CH_LAUNCHED(ctx);
-            CH_TRY(ch_scan_excl_i64(ctx, hd, ex, R, nseg_d));
-            k_group_starts<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(hd, ex, R, st);
-            CH_LAUNCHED(ctx);
+            int64_t *st = nullptr, *nseg_d = nullptr;
+            CH_TRY(group(ctx, k1, R, nullptr, L.sh_it, &st, &nseg_d, 1));   // segments: equal (gpu, iteration)
             CH_CUDA(ctx, cudaMemsetAsync(bad, 0, 4, ctx->st));
-            k_seg_starts_end<<<1, 1, 0, ctx->st>>>(st, nseg_d, R);
-            CH_LAUNCHED(ctx);
             k_prefix_check<<<grid_for(R, NT), NT, 0, ctx->st>>>(k1, st, nseg_d, L.sh_it, bad);
             CH_LAUNCHED(ctx);
             unsigned int hbad = 0;
@@ -1211,11 +1285,17 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
                 }
                 k_seg_sort<<<grid_for(R, 1), SS_NT, sizeof(SegSortSmem), ctx->st>>>(k1, v1, st, nseg_d, L);
                 CH_LAUNCHED(ctx);
-                k_valid_flags<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, R, hd);
-                CH_LAUNCHED(ctx);
-                CH_TRY(ch_scan_excl_i64(ctx, hd, ex, R, nv_d));
-                k_partition<<<(unsigned)ceil_div(R, NT), NT, 0, ctx->st>>>(k1, v1, R, ex, nv_d, k2, v2);
-                CH_LAUNCHED(ctx);
+                {
+                    const int64_t nt = ceil_div(R, GP_TILE);
+                    size_t m2 = ctx->used;
+                    unsigned long long *state = CH_ALLOC(ctx, unsigned long long, nt + 1);
+                    CH_ALLOC_END(ctx);
+                    CH_CUDA(ctx, cudaMemsetAsync(state, 0, 8 * (size_t)(nt + 1), ctx->st));
+                    k_compact_1pass<<<(unsigned)nt, GP_NT, 0, ctx->st>>>(k1, v1, R, k2, v2, nv_d, state,
+                                                                        reinterpret_cast<unsigned int *>(state + nt));
+                    CH_LAUNCHED(ctx);
+                    ctx->used = m2;
+                }
                 alt = true;
                 done = true;
             }
