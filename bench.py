@@ -293,7 +293,8 @@ def main():
         pass
     achieved = alg / (ev_avg * 1e-3) / 1e9 if ev_avg else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": (achieved / peak) if achieved else None, "traffic": traffic, "kernel": "k_events (fused a5-a9)",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "kernel": "event pass a5-a9 (k_tile_seeds + k_tile_heads + k_events_w; time = the whole phase)",
             "peak_source": peak_src, "alg_bytes_per_launch": alg, "avg_launch_ms": ev_avg,
             "phase_ms_last_step": phase_ms}
 
