@@ -244,6 +244,7 @@ __global__ void k_vkeys(const uint32_t *__restrict__ meta, const int64_t *__rest
 }
 
 // ---- fused event pass ---------------------------------------------------------------------------
+struct TileWin;
 struct EvParams {
     const int64_t *tl, *ks, *ke;
     const uint32_t *meta;
@@ -280,6 +281,7 @@ struct EvParams {
     const int32_t *seeds;
     int64_t ntile;
     const int64_t *tile_base;     // [ntile + 1] first sub-run id of each tile
+    const struct TileWin *twin;   // [ntile] placed windows
 };
 
 
@@ -1037,8 +1039,13 @@ constexpr int KT_B = 16, TL_B = 44;    // staged bytes per entry: time + key; ti
 
 struct TabWin {
     int64_t lo;           // global index of window entry 0 (the gpu's table starts with a -inf sentinel)
+    int64_t gb, ge;       // the gpu's table in global memory
     int64_t next;         // time of the entry after the window (INT64_MAX at the table end)
-    int n, off;           // staged entries (0 = look up in global memory), byte offset in the pool
+    int n, off;           // staged entries, byte offset in the pool
+};
+struct TileWin {          // per tile: both windows, placed (k_tile_windows), and the tile's gpu
+    TabWin tw[2];
+    int64_t lg;
 };
 struct EvSmemW {
     static constexpr int NT = W_NT, TILE = W_TILE, WARPS = W_WARPS;
@@ -1087,41 +1094,44 @@ __global__ void k_tile_seeds(EvParams P, int32_t *__restrict__ seeds) {
 
 // Windows of the tile: bounds from this tile's and the next tile's seeds (threads 0, 1), pool placement (thread 0;
 // a window that does not fit is cut short), then cp.async copies by all threads (the caller waits).
-__device__ __forceinline__ void stage_windows(EvSmemW &W, const EvParams &P, int64_t tile) {
-    const int tid = threadIdx.x;
+// Windows of every tile, one thread per tile: from this tile's seed to the next tile's (same gpu), placed in the
+// shared-memory pool (timeline first, then the key table; a window that does not fit is cut short and later
+// queries read global memory), with the time of the first entry after each window.
+__global__ void k_tile_windows(EvParams P, TileWin *__restrict__ out) {
+    const int64_t tile = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tile >= P.ntile) return;
     const int32_t *sd = P.seeds + tile * SEED_W;
     const int lg = sd[NTAB];
-    __shared__ int64_t s_ge[NTAB];
-    if (tid < NTAB) {
-        const int x = tid;
-        int64_t gb, ge;
-        tab_bounds(P, x, lg, &gb, &ge);
-        int64_t lo = sd[x], hi = ge;
+    TileWin r;
+    r.lg = lg;
+    int off = 0;
+#pragma unroll
+    for (int x = NTAB - 1; x >= 0; x--) {
+        TabWin &w = r.tw[x];
+        tab_bounds(P, x, lg, &w.gb, &w.ge);
+        int64_t lo = sd[x], hi = w.ge;
         if (tile + 1 < P.ntile && sd[SEED_W + NTAB] == lg) {
             hi = (int64_t)sd[SEED_W + x] + 1 + (x == 1 ? 4 : 0);    // timeline: a little slack
             if (hi < lo + 1) hi = lo + 1;
-            if (hi > ge) hi = ge;
+            if (hi > w.ge) hi = w.ge;
         }
-        TabWin &w = W.tw[x];
+        const int eb = x == 0 ? KT_B : TL_B;
+        int64_t n = hi - lo, fit = (POOL - off) / eb;
+        if (n > fit) n = fit & ~3;
         w.lo = lo;
-        w.n = (int)(hi - lo);
-        s_ge[x] = ge;
-        if (x == 0) W.lgP = lg;
+        w.n = (int)n;
+        w.off = off;
+        off += (int)((n * eb + 15) & ~15);
+        const int64_t *T = x == 0 ? P.KTt : P.TLt;
+        w.next = lo + n < w.ge ? T[lo + n] : INT64_MAX;
     }
-    __syncthreads();
-    if (tid == 0) {
-        int off = 0;
-#pragma unroll
-        for (int x = NTAB - 1; x >= 0; x--) {       // timeline first (small), then the key table
-            TabWin &w = W.tw[x];
-            const int eb = x == 0 ? KT_B : TL_B;
-            int fit = (POOL - off) / eb;
-            if (fit < 0) fit = 0;
-            if (w.n > fit) w.n = fit & ~3;          // cut short: later queries read global memory
-            w.off = off;
-            off += (w.n * eb + 15) & ~15;
-        }
-    }
+    out[tile] = r;
+}
+
+__device__ __forceinline__ void stage_windows(EvSmemW &W, const EvParams &P, int64_t tile) {
+    const int tid = threadIdx.x;
+    if (tid < NTAB) W.tw[tid] = P.twin[tile].tw[tid];
+    if (tid == 0) W.lgP = (int)P.twin[tile].lg;
     __syncthreads();
     {
         const TabWin w = W.tw[0];
@@ -1148,14 +1158,14 @@ __device__ __forceinline__ void stage_windows(EvSmemW &W, const EvParams &P, int
     }
 }
 
-// register copy of one staged window
 // A lookup table of one gpu, [gb, ge) in global memory (entry gb = -inf sentinel), with entries [lo, lo + n)
-// staged in shared memory.  Every read goes to the staged copy when the index is inside it, else to global memory
-// (L1/L2): a window that was cut short, or a query outside it, costs latency, never correctness.
+// staged in shared memory.  Lookups walk the staged copy; a query beyond it (a window cut short, a second
+// gpu's events in the tile, an earlier time on another compute stream) reads the same table in global memory:
+// latency, never a different answer.
 struct WinR {
     const int64_t *T;     // staged times (payload follows)
     const int64_t *G;     // global time column
-    int64_t lo, gb, ge;
+    int64_t lo, gb, ge, next;
     int n;
 };
 __device__ __forceinline__ WinR win_reg(const EvSmemW &W, int x, const EvParams &P) {
@@ -1165,7 +1175,9 @@ __device__ __forceinline__ WinR win_reg(const EvSmemW &W, int x, const EvParams 
     r.G = x == 0 ? P.KTt : P.TLt;
     r.lo = w.lo;
     r.n = w.n;
-    tab_bounds(P, x, W.lgP, &r.gb, &r.ge);
+    r.gb = w.gb;
+    r.ge = w.ge;
+    r.next = w.next;
     return r;
 }
 // a global-only view of table x of gpu lg (events of a second gpu in the tile); out of line, it is rare
@@ -1182,100 +1194,96 @@ __device__ __forceinline__ WinR win_global(const EvParams &P, int x, int lg) {
     const longlong2 b = x == 0 ? tab_bounds_ool(P.kt_beg, nullptr, lg) : tab_bounds_ool(P.tl_beg, P.tl_len, lg);
     r.gb = b.x;
     r.ge = b.y;
+    r.next = INT64_MAX;
     return r;
 }
 __device__ __forceinline__ bool win_in(const WinR &w, int64_t j) { return (uint64_t)(j - w.lo) < (uint64_t)w.n; }
 __device__ __forceinline__ int64_t win_t(const WinR &w, int64_t j) {
     return win_in(w, j) ? w.T[j - w.lo] : __ldg(w.G + j);
 }
-__device__ __noinline__ int64_t win_search_global(const int64_t *G, int64_t lo, int64_t hi, int64_t t) {
-    return last_le(G, lo, hi, t);
+// slow path: last entry <= t over [gb, ge) in global memory, starting from the cursor when it is behind t
+__device__ __noinline__ longlong2 seek_global(const int64_t *G, const int64_t *T, int64_t lo, int n, int64_t gb,
+                                              int64_t ge, int64_t j, int64_t t) {
+    const int64_t l = (j >= gb && j < ge && __ldg(G + j) <= t) ? j : gb;
+    const int64_t r = last_le(G, l, ge, t);
+    const int64_t b = r + 1 >= ge ? INT64_MAX : ((uint64_t)(r + 1 - lo) < (uint64_t)n ? T[r + 1 - lo] : __ldg(G + r + 1));
+    return make_longlong2(r, b);
 }
-// cursor: entry j answers every t in [a, b)
 constexpr uint32_t KIDX_NONE = 0xFFFFFFFFu;   // event slot past the end of the events
+// cursor: entry j answers every t in [a, b)
 struct WCur {
     int64_t j, a, b;
 };
 __device__ __forceinline__ void wcur_init(WCur &k) { k.j = -1; k.a = INT64_MAX; k.b = INT64_MIN; }
-__device__ __forceinline__ void wcur_seek(const WinR &w, WCur &k, int64_t t) {
-    if (t >= k.a && t < k.b) return;
-    int64_t j;
-    if (k.j >= 0 && t >= k.a) {
-        j = k.j;                                     // walk forward from the cursor (queries mostly increase)
-    } else if (w.n > 0 && w.T[0] <= t) {             // search the staged window: last staged entry <= t
-        int l = 1, h = w.n;
-        while (l < h) {
-            const int m = (l + h) >> 1;
-            if (w.T[m] <= t) l = m + 1; else h = m;
+// returns true when the cursor moved
+__device__ __forceinline__ bool wcur_seek(const WinR &w, WCur &k, int64_t t) {
+    if (t >= k.a && t < k.b) return false;
+    int c = (int)(k.j - w.lo);
+    if (!(win_in(w, k.j) && t >= k.a)) {
+        // fresh position: binary search of the staged window when t is inside it
+        c = -1;
+        if (w.n > 0 && w.T[0] <= t) {
+            int l = 1, h = w.n;
+            while (l < h) {
+                const int m = (l + h) >> 1;
+                if (w.T[m] <= t) l = m + 1; else h = m;
+            }
+            c = l - 1;
         }
-        j = w.lo + l - 1;
-    } else {
-        j = win_search_global(w.G, w.gb, w.ge, t);
     }
-    bool done = false;
-#pragma unroll 1
-    for (int s = 0; s < 8; s++) {
-        if (j + 1 >= w.ge || win_t(w, j + 1) > t) { done = true; break; }
-        j++;
+    if (c >= 0) {
+        while (c + 1 < w.n && w.T[c + 1] <= t) c++;            // forward walk in shared memory
+        if (c + 1 < w.n) { k.j = w.lo + c; k.a = w.T[c]; k.b = w.T[c + 1]; return true; }
+        if (t < w.next) { k.j = w.lo + c; k.a = w.T[c]; k.b = w.next; return true; }
     }
-    if (!done) j = win_search_global(w.G, j, w.ge, t);
-    k.j = j;
-    k.a = win_t(w, j);
-    k.b = j + 1 < w.ge ? win_t(w, j + 1) : INT64_MAX;
+    const longlong2 r = seek_global(w.G, w.T, w.lo, w.n, w.gb, w.ge, k.j, t);
+    k.j = r.x;
+    k.a = win_t(w, r.x);
+    k.b = r.y;
+    return true;
 }
 __device__ __forceinline__ unsigned long long key_at(const WinR &w, const EvParams &P, int64_t j) {
     return win_in(w, j) ? reinterpret_cast<const unsigned long long *>(w.T + w.n)[j - w.lo] : __ldg(P.KTk + j);
 }
-struct TlVal {
-    unsigned long long cov, F, Pw;
-};
-// coverage, frequency and power integrals at t from timeline entry j (affine in t - t0, wrapping)
-__device__ __forceinline__ TlVal tl_at(const WinR &w, const EvParams &P, int64_t j, int64_t t) {
+// timeline entry j: intercepts (cov, F, Pw) and slopes (in-union, f, p)
+struct TlEnt {
     unsigned long long v0, v1, v2;
     int32_t s0, s1, s2;
+};
+__device__ __forceinline__ TlEnt tl_ent(const WinR &w, const EvParams &P, int64_t j) {
+    TlEnt e;
     if (win_in(w, j)) {
         const int c = (int)(j - w.lo);
         const int32_t *s32 = reinterpret_cast<const int32_t *>(w.T + 4 * w.n);
-        v0 = w.T[w.n + c]; v1 = w.T[2 * w.n + c]; v2 = w.T[3 * w.n + c];
-        s0 = s32[c]; s1 = s32[w.n + c]; s2 = s32[2 * w.n + c];
+        e.v0 = w.T[w.n + c]; e.v1 = w.T[2 * w.n + c]; e.v2 = w.T[3 * w.n + c];
+        e.s0 = s32[c]; e.s1 = s32[w.n + c]; e.s2 = s32[2 * w.n + c];
     } else {
         const int64_t cap = P.tl_cap;
-        v0 = __ldg(P.TLv + j); v1 = __ldg(P.TLv + cap + j); v2 = __ldg(P.TLv + 2 * cap + j);
-        s0 = __ldg(P.TLs + j); s1 = __ldg(P.TLs + cap + j); s2 = __ldg(P.TLs + 2 * cap + j);
+        e.v0 = __ldg(P.TLv + j); e.v1 = __ldg(P.TLv + cap + j); e.v2 = __ldg(P.TLv + 2 * cap + j);
+        e.s0 = __ldg(P.TLs + j); e.s1 = __ldg(P.TLs + cap + j); e.s2 = __ldg(P.TLs + 2 * cap + j);
     }
-    const unsigned long long ud = (unsigned long long)(t - P.t0);
-    TlVal r;
-    r.cov = v0 + (s0 ? ud : 0ull);
-    r.F = v1 + (unsigned long long)(int64_t)s1 * ud;
-    r.Pw = v2 + (unsigned long long)(int64_t)s2 * ud;
-    return r;
+    return e;
 }
 
 // ---- sub-run heads per tile (first pass): the same keys and head rule as k_events_w, counted, so that the main
 // pass knows every tile's first sub-run id up front (an exclusive scan of the counts) instead of waiting on a
 // look-back chain that any slow tile would stall for all later ones.  Columns are read straight from global
 // memory (8 consecutive events per thread, 16 B loads); only the key-table window is staged.
-constexpr int HD_POOL = 20480;
+constexpr int HD_POOL = 28672;
 __global__ void __launch_bounds__(W_NT) k_tile_heads(EvParams P, int64_t *__restrict__ tile_cnt) {
     __shared__ __align__(16) unsigned char pool[HD_POOL];
-    __shared__ int64_t s_lo;
+    __shared__ int64_t s_lo, s_next;
     __shared__ int s_n, s_lg;
     __shared__ unsigned long long s_last[W_WARPS];
     __shared__ int s_cnt[W_WARPS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t tile = blockIdx.x, base = tile * W_TILE, i0 = base + (int64_t)tid * EV_IPT, N = P.N;
     if (tid == 0) {
-        const int32_t *sd = P.seeds + tile * SEED_W;
-        const int lg = sd[NTAB];
-        int64_t gb, ge;
-        tab_bounds(P, 0, lg, &gb, &ge);
-        int64_t lo = sd[0], hi = ge;
-        if (tile + 1 < P.ntile && sd[SEED_W + NTAB] == lg) hi = (int64_t)sd[SEED_W] + 1;
-        if (hi < lo + 1) hi = lo + 1;
-        if (hi > ge) hi = ge;
-        int n = (int)(hi - lo);
+        const TabWin w = P.twin[tile].tw[0];
+        int n = w.n;
         if (n > HD_POOL / KT_B) n = (HD_POOL / KT_B) & ~3;
-        s_lo = lo; s_n = n; s_lg = lg;
+        s_lo = w.lo; s_n = n; s_lg = (int)P.twin[tile].lg;
+        s_next = n == w.n ? w.next : __ldg(P.KTt + w.lo + n);
     }
     __syncthreads();
     {
@@ -1317,6 +1325,7 @@ __global__ void __launch_bounds__(W_NT) k_tile_heads(EvParams P, int64_t *__rest
     wk.n = s_n;
     wk.gb = P.kt_beg[lgP];
     wk.ge = P.kt_beg[lgP + 1];
+    wk.next = s_next;
     WCur ck;
     wcur_init(ck);
     int lgc = lgP;
@@ -1425,6 +1434,7 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_w(EvParams P, int vec_ok) {
     int lgc = lgP;
     WCur ct;
     wcur_init(ct);
+    TlEnt te{};
 #pragma unroll 1
     for (int k = 0; k < EV_IPT; k++) {
         if (k >= nv) break;
@@ -1458,13 +1468,24 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_w(EvParams P, int vec_ok) {
                 call = c > 0 ? c : 0;
             }
             if (lg != lgc) { wt = win_global(P, 1, lg); wcur_init(ct); lgc = lg; }
-            wcur_seek(wt, ct, ks);
-            const TlVal va = tl_at(wt, P, ct.j, ks);
-            wcur_seek(wt, ct, ke);
-            const TlVal vb = tl_at(wt, P, ct.j, ke);
-            ovl = (int64_t)(vb.cov - va.cov);                           // |[t_ks, t_ke) ∩ U_g| (D9)
-            phi = (int64_t)(vb.F - va.F);                               // MHz*ns (D10)
-            psi = (int64_t)(vb.Pw - va.Pw);                             // mW*ns
+            if (wcur_seek(wt, ct, ks)) te = tl_ent(wt, P, ct.j);
+            if (ke < ct.b) {
+                // one timeline entry covers [t_ks, t_ke): the integrals are its slopes times the duration
+                ovl = te.s0 ? dur : 0;                                  // |[t_ks, t_ke) ∩ U_g| (D9)
+                phi = (int64_t)te.s1 * dur;                             // MHz*ns (D10)
+                psi = (int64_t)te.s2 * dur;                             // mW*ns
+            } else {
+                const unsigned long long ua = (unsigned long long)(ks - P.t0);
+                const unsigned long long ca = te.v0 + (te.s0 ? ua : 0ull);
+                const unsigned long long fa = te.v1 + (unsigned long long)(int64_t)te.s1 * ua;
+                const unsigned long long pa = te.v2 + (unsigned long long)(int64_t)te.s2 * ua;
+                wcur_seek(wt, ct, ke);
+                te = tl_ent(wt, P, ct.j);
+                const unsigned long long ub = (unsigned long long)(ke - P.t0);
+                ovl = (int64_t)(te.v0 + (te.s0 ? ub : 0ull) - ca);
+                phi = (int64_t)(te.v1 + (unsigned long long)(int64_t)te.s1 * ub - fa);
+                psi = (int64_t)(te.v2 + (unsigned long long)(int64_t)te.s2 * ub - pa);
+            }
             cur.n += 1;
             cur.busy += dur;
             cur.prep += prep;
@@ -1675,6 +1696,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         size_t mark = ctx->used;
         int32_t *seeds = CH_ALLOC(ctx, int32_t, ntile * SEED_W);
         int64_t *tcnt = CH_ALLOC(ctx, int64_t, ntile + 1), *tbase = CH_ALLOC(ctx, int64_t, ntile + 1);
+        TileWin *twin = CH_ALLOC(ctx, TileWin, ntile);
         CH_ALLOC_END(ctx);
         P.seeds = seeds;
         size_t dsm = sizeof(EvSmemW);
@@ -1686,6 +1708,9 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         ch_tick(ctx, 4, 0);
         k_tile_seeds<<<(unsigned)ceil_div(ntile * 32, NT), NT, 0, ctx->st>>>(P, seeds);
         CH_LAUNCHED(ctx);
+        k_tile_windows<<<(unsigned)ceil_div(ntile, NT), NT, 0, ctx->st>>>(P, twin);
+        CH_LAUNCHED(ctx);
+        P.twin = twin;
         k_tile_heads<<<(unsigned)ntile, W_NT, 0, ctx->st>>>(P, tcnt);
         CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, tcnt, tbase, ntile, tbase + ntile));
