@@ -310,36 +310,95 @@ __global__ void k_euler_check(const int64_t *__restrict__ Et, const int64_t *__r
 // gpu's four lists (ties: lower level first, then list order) and records the instance key after it -- its own
 // level's code and, for the other levels, the code of their last entry at or before its time.  The last entry
 // at any time therefore carries the full key there; entry 0 of each gpu is (-inf, invalid).
-__global__ void k_keytab(const int64_t *__restrict__ Et, const int32_t *__restrict__ Ec,
-                         const int64_t *__restrict__ et_beg, const int64_t *__restrict__ list_beg, int n_lists,
-                         int64_t net, int sh_it, int sh_ph, int sh_ly, int sh_lg, int64_t *__restrict__ Kt,
-                         unsigned long long *__restrict__ Kk) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= net) return;
-    int l = 0, h = n_lists;                  // list of entry j: last l with et_beg[l] <= j
-    while (h - l > 1) {
-        const int m = (l + h) >> 1;
-        if (et_beg[m] <= j) l = m; else h = m;
+// Done in blocks of KT_CH consecutive entries of one list: the other three lists' entries between the
+// block's first and last time are staged in shared memory once per block (they are few: a block of op entries
+// spans a handful of layer / phase / iteration boundaries), so each entry's three rank searches run there.
+constexpr int KT_NT = 256, KT_CH = 2048, KT_WIN = 1024;
+__global__ void __launch_bounds__(KT_NT) k_keytab_blk(const int64_t *__restrict__ Et, const int32_t *__restrict__ Ec,
+                                                      const int64_t *__restrict__ et_beg,
+                                                      const int64_t *__restrict__ list_beg,
+                                                      const int64_t *__restrict__ chunk_beg, int n_lists, int sh_it,
+                                                      int sh_ph, int sh_ly, int sh_lg, int64_t *__restrict__ Kt,
+                                                      unsigned long long *__restrict__ Kk) {
+    __shared__ int64_t s_t[3][KT_WIN];
+    __shared__ int32_t s_c[3][KT_WIN];
+    __shared__ int64_t s_lo[3], s_n[3];
+    __shared__ int s_list;
+    __shared__ int64_t s_j0, s_j1;
+    const int tid = threadIdx.x;
+    const int64_t cb = blockIdx.x;
+    if (tid == 0) {
+        int l = 0, h = n_lists;                          // list of chunk cb: last l with chunk_beg[l] <= cb
+        while (h - l > 1) {
+            const int m = (l + h) >> 1;
+            if (chunk_beg[m] <= cb) l = m; else h = m;
+        }
+        s_list = l;
+        const int64_t b = et_beg[l], e = et_beg[l + 1];
+        s_j0 = b + (cb - chunk_beg[l]) * KT_CH;
+        s_j1 = s_j0 + KT_CH < e ? s_j0 + KT_CH : e;
     }
-    const int lg = l >> 2, lv = l & 3;
+    __syncthreads();
+    const int l = s_list, lg = l >> 2, lv = l & 3;
+    const int64_t j0 = s_j0, j1 = s_j1;
+    if (tid < 3) {
+        const int o = tid + (tid >= lv ? 1 : 0);
+        const int64_t b = et_beg[lg * 4 + o], e = et_beg[lg * 4 + o + 1];
+        const int64_t lo = last_le(Et, b, e, Et[j0]);       // >= b (sentinel)
+        const int64_t hi = last_le(Et, lo, e, Et[j1 - 1]) + 1;
+        s_lo[tid] = lo;
+        s_n[tid] = hi - lo <= KT_WIN ? hi - lo : -1;          // -1: search global memory
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        const int64_t n = s_n[q];
+        for (int i = tid; i < n; i += KT_NT) {
+            s_t[q][i] = Et[s_lo[q] + i];
+            s_c[q][i] = Ec[s_lo[q] + i];
+        }
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int64_t j = j0 + tid; j < j1; j += KT_NT) {
     const int64_t a = j - et_beg[l];
     const int64_t kb = 2 * list_beg[lg * 4] + lg;
     if (a == 0) {
         if (lv == 0) { Kt[kb] = INT64_MIN; Kk[kb] = CH_INVALID_KEY; }
-        return;
+        continue;
     }
     const int64_t t = Et[j];
     int64_t pos = kb + a;
     uint32_t code[4];
     code[lv] = (uint32_t)Ec[j];
 #pragma unroll
-    for (int o = 0; o < 4; o++) {
-        if (o == lv) continue;
-        const int64_t b = et_beg[lg * 4 + o], e = et_beg[lg * 4 + o + 1];
-        const int64_t le = last_le(Et, b, e, t);     // >= b: the sentinel is -inf
-        code[o] = (uint32_t)Ec[le];
-        int64_t c = le;
-        if (o > lv) while (c > b && Et[c] == t) c--;  // later levels: only entries strictly before t
+    for (int q = 0; q < 3; q++) {
+        const int o = q + (q >= lv ? 1 : 0);
+        const int64_t b = et_beg[lg * 4 + o];
+        int64_t le, c;
+        const int64_t n = s_n[q];
+        if (n > 0) {
+            int lo2 = 0, hi2 = (int)n;                      // last staged entry <= t (t >= the first)
+            while (lo2 < hi2) {
+                const int m = (lo2 + hi2) >> 1;
+                if (s_t[q][m] <= t) lo2 = m + 1; else hi2 = m;
+            }
+            int x = lo2 - 1;
+            code[o] = (uint32_t)s_c[q][x];
+            le = s_lo[q] + x;
+            if (o > lv) while (x > 0 && s_t[q][x] == t) x--;
+            c = s_lo[q] + x;
+            if (o > lv && x == 0 && s_t[q][0] == t) {         // ties reach the window start: finish in global memory
+                c = le;
+                while (c > b && Et[c] == t) c--;
+            }
+        } else {
+            const int64_t e = et_beg[lg * 4 + o + 1];
+            le = last_le(Et, b, e, t);
+            code[o] = (uint32_t)Ec[le];
+            c = le;
+            if (o > lv) while (c > b && Et[c] == t) c--;
+        }
         pos += c - b;
     }
     Kt[pos] = t;
@@ -347,6 +406,7 @@ __global__ void k_keytab(const int64_t *__restrict__ Et, const int32_t *__restri
                            : ((unsigned long long)lg << sh_lg) | ((unsigned long long)code[0] << sh_it) |
                                  ((unsigned long long)code[1] << sh_ph) | ((unsigned long long)code[2] << sh_ly) |
                                  (unsigned long long)code[3];
+    }
 }
 
 __global__ void k_attr_out(SpanView v, const int64_t *__restrict__ tl, const uint32_t *__restrict__ meta, int64_t N,
@@ -541,10 +601,24 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         for (int l = 0; l <= n_lg; l++) kb[l] = 2 * ctx->list_beg[l * 4] + l;
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_kt_beg, kb.data(), 8 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
         const int sh_ly = ctx->kb[3], sh_ph = sh_ly + ctx->kb[2], sh_it = sh_ph + ctx->kb[1], sh_lg = sh_it + ctx->kb[0];
-        k_keytab<<<(unsigned)ceil_div(net, NT), NT, 0, ctx->st>>>(ctx->ET_t, ctx->ET_c, ctx->d_et_beg, ctx->d_list_beg,
-                                                                 n_lists, net, sh_it, sh_ph, sh_ly, sh_lg, ctx->KT_t,
-                                                                 ctx->KT_k);
+        // chunks of KT_CH entries per Euler list (host-known list sizes)
+        std::vector<int64_t> cbeg(n_lists + 1);
+        int64_t nch = 0;
+        for (int l = 0; l < n_lists; l++) {
+            cbeg[l] = nch;
+            const int64_t len = 2 * (ctx->list_beg[l + 1] - ctx->list_beg[l]) + 1;
+            nch += ceil_div(len, KT_CH);
+        }
+        cbeg[n_lists] = nch;
+        size_t mk = ctx->used;
+        int64_t *dcb = CH_ALLOC(ctx, int64_t, n_lists + 1);
+        CH_ALLOC_END(ctx);
+        CH_CUDA(ctx, cudaMemcpyAsync(dcb, cbeg.data(), 8 * (n_lists + 1), cudaMemcpyHostToDevice, ctx->st));
+        k_keytab_blk<<<(unsigned)nch, KT_NT, 0, ctx->st>>>(ctx->ET_t, ctx->ET_c, ctx->d_et_beg, ctx->d_list_beg, dcb,
+                                                           n_lists, sh_it, sh_ph, sh_ly, sh_lg, ctx->KT_t, ctx->KT_k);
         CH_LAUNCHED(ctx);
+        ctx->used = mk;
+        (void)net;
     }
     if (!sweep.empty()) {
         ctx->d_attr_pre = CH_ALLOC(ctx, int32_t, 4 * ctx->N);
