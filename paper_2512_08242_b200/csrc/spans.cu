@@ -528,6 +528,17 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
 
     const int64_t SL = ctx->S_loc;
     ctx->list_flags.assign(n_lists, 0);
+    const int64_t net = 2 * SL + n_lists;
+    ctx->ET_t = CH_ALLOC(ctx, int64_t, net);
+    ctx->ET_c = CH_ALLOC(ctx, int32_t, net);
+    ctx->d_et_beg = CH_ALLOC(ctx, int64_t, n_lists + 1);
+    unsigned int *et_bad = CH_ALLOC(ctx, unsigned int, 1);
+    CH_ALLOC_END(ctx);
+    unsigned int h_et_bad = 0;
+    CH_CUDA(ctx, cudaMemsetAsync(et_bad, 0, 4, ctx->st));
+    k_euler_sentinels<<<(unsigned)ceil_div(n_lists + 1, NT), NT, 0, ctx->st>>>(ctx->d_list_beg, n_lists, ctx->ET_t,
+                                                                              ctx->ET_c, ctx->d_et_beg);
+    CH_LAUNCHED(ctx);
     if (SL > 0) {
         int64_t nch = ceil_div(SL, CHUNK);
         int levels = 1;
@@ -552,8 +563,17 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         k_laminar<<<g, NT, 0, ctx->st>>>(ctx->P_start, ctx->P_end, Plist, ctx->P_parent, SL, ctx->d_list_beg, n_lists,
                                          ctx->d_list_flags);
         CH_LAUNCHED(ctx);
+        // Euler boundary tables, built before the laminarity is known (used only if every list is laminar; in a
+        // non-laminar list the positions stay inside the list's range and are simply never read)
+        k_euler<<<(unsigned)ceil_div(SL, NT), NT, 0, ctx->st>>>(ctx->P_start, ctx->P_end, ctx->P_parent, Plist, SL,
+                                                               ctx->d_list_beg, ctx->ET_t, ctx->ET_c);
+        CH_LAUNCHED(ctx);
+        k_euler_check<<<(unsigned)ceil_div(net, NT), NT, 0, ctx->st>>>(ctx->ET_t, ctx->d_et_beg, n_lists, net, et_bad);
+        CH_LAUNCHED(ctx);
+        // one read-back: laminarity flags and the tour check
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->list_flags.data(), ctx->d_list_flags, 4 * n_lists, cudaMemcpyDeviceToHost,
                                      ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(&h_et_bad, et_bad, 4, cudaMemcpyDeviceToHost, ctx->st));
         CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
         ctx->used = mark;
     }
@@ -562,37 +582,9 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
     for (int l = 0; l < n_lists; l++) if (ctx->list_flags[l]) sweep.push_back(l);
     ctx->rep.non_laminar_lists = (int32_t)sweep.size();
     ctx->d_attr_pre = nullptr;
-    ctx->et_ok = false;
-    ctx->ET_t = nullptr;
-    ctx->ET_c = nullptr;
-    if (sweep.empty()) {
-        const int64_t net = 2 * SL + n_lists;
-        ctx->ET_t = CH_ALLOC(ctx, int64_t, net);
-        ctx->ET_c = CH_ALLOC(ctx, int32_t, net);
-        ctx->d_et_beg = CH_ALLOC(ctx, int64_t, n_lists + 1);
-        CH_ALLOC_END(ctx);
-        size_t mark = ctx->used;
-        unsigned int *bad = CH_ALLOC(ctx, unsigned int, 1);
-        CH_ALLOC_END(ctx);
-        k_euler_sentinels<<<(unsigned)ceil_div(n_lists + 1, NT), NT, 0, ctx->st>>>(ctx->d_list_beg, n_lists, ctx->ET_t,
-                                                                                  ctx->ET_c, ctx->d_et_beg);
-        CH_LAUNCHED(ctx);
-        CH_CUDA(ctx, cudaMemsetAsync(bad, 0, 4, ctx->st));
-        if (SL > 0) {
-            k_euler<<<(unsigned)ceil_div(SL, NT), NT, 0, ctx->st>>>(ctx->P_start, ctx->P_end, ctx->P_parent, Plist, SL,
-                                                                   ctx->d_list_beg, ctx->ET_t, ctx->ET_c);
-            CH_LAUNCHED(ctx);
-            k_euler_check<<<(unsigned)ceil_div(net, NT), NT, 0, ctx->st>>>(ctx->ET_t, ctx->d_et_beg, n_lists, net, bad);
-            CH_LAUNCHED(ctx);
-        }
-        unsigned int hbad = 0;
-        CH_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-        ctx->used = mark;
-        ctx->et_ok = hbad == 0;
-    }
+    ctx->et_ok = sweep.empty() && h_et_bad == 0;
     if (ctx->et_ok) {
-        const int64_t net = 2 * SL + n_lists, nkt = 2 * SL + n_lg;
+        const int64_t nkt = 2 * SL + n_lg;
         ctx->KT_t = CH_ALLOC(ctx, int64_t, nkt);
         ctx->KT_k = CH_ALLOC(ctx, unsigned long long, nkt);
         ctx->d_kt_beg = CH_ALLOC(ctx, int64_t, n_lg + 1);
