@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(256) k_sum_rows_warp(TabView ch, const uint32_
 // in shared memory -- coalesced column loads for field-major tables, one 128 B row per child for the
 // AoS sub-run rows -- and each thread folds its own parent's children from shared memory in order.
 constexpr int RC_NT = 256, RC_CH = 256;
-__global__ void __launch_bounds__(RC_NT) k_sum_rows_chunked(TabView ch, const uint32_t *__restrict__ perm,
+__global__ void __launch_bounds__(RC_NT, 3) k_sum_rows_chunked(TabView ch, const uint32_t *__restrict__ perm,
                                                             const int64_t *__restrict__ starts,
                                                             const int64_t *__restrict__ ng_dev, int shift, int C,
                                                             TabView pa, int PB) {
@@ -841,6 +841,24 @@ __global__ void __launch_bounds__(RC_NT) k_sum_rows_chunked(TabView ch, const ui
                 for (int q = 0; q < 8; q++) if (q < C) vals[(RF_NFIELDS + q) * RC_CH + tid] = y[q];
                 for (int q = 8; q < C; q++)
                     vals[(RF_NFIELDS + q) * RC_CH + tid] = __double_as_longlong(ch.cnt[(int64_t)q * ch.ccap + (c) * ch.crs]);
+            }
+        } else if (ch.cap == 1 && ch.rs == 16 && ch.ccap == 1 && ch.crs == C && C <= 8 && (C & 1) == 0) {
+            // AoS sub-runs: one 128 B row and C*8 B of counters per child, 16 B vector loads
+            for (int t = tid; t < m; t += RC_NT) {
+                const int64_t c = perm ? (int64_t)perm[j0 + t] : j0 + t;
+                const longlong2 *row = reinterpret_cast<const longlong2 *>(ch.f + c * 16);
+                longlong2 x[8];
+#pragma unroll
+                for (int f = 0; f < 8; f++) x[f] = __ldg(row + f);
+                longlong2 y[4];
+                const longlong2 *cr = reinterpret_cast<const longlong2 *>(ch.cnt + c * C);
+#pragma unroll
+                for (int q = 0; q < 4; q++) y[q] = 2 * q < C ? __ldg(cr + q) : make_longlong2(0, 0);
+#pragma unroll
+                for (int f = 0; f < RF_NFIELDS; f++) vals[f * RC_CH + t] = (f & 1) ? x[f >> 1].y : x[f >> 1].x;
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    if (q < C) vals[(RF_NFIELDS + q) * RC_CH + t] = (q & 1) ? y[q >> 1].y : y[q >> 1].x;
             }
         } else {
             for (int t = tid; t < m; t += RC_NT) {
