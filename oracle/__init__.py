@@ -188,3 +188,26 @@ def run(bundle, params: Optional[dict] = None, max_iters: int = 4096, gpu_mask: 
     finally:
         lib.or_free(h)
     return out
+
+
+def cpu_util(ts, core, util, topology) -> Dict[str, np.ndarray]:
+    """O17 CPU utilization: per-timestamp C_active / C_min and the summary row
+    [n_ts, median C_active, median C_min, max C_active, max C_min, physical occupancy, SMT co-activity,
+    #physical]; 'bad' = 1 when the samples are unsorted, out of range or the topology is invalid."""
+    lib = _load()
+    f = lib.or_cpu_util
+    f.restype = ctypes.c_int64
+    f.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p,
+                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32)]
+    ts = np.ascontiguousarray(ts, dtype=np.int64)
+    core = np.ascontiguousarray(core, dtype=np.int32)
+    util = np.ascontiguousarray(util, dtype=np.float64)
+    topo = np.ascontiguousarray(topology, dtype=np.int32)
+    n = int(ts.shape[0])
+    ca = np.zeros(max(n, 1), np.int64)
+    cm = np.zeros(max(n, 1), np.float64)
+    summ = np.full(8, np.nan)
+    bad = ctypes.c_int32(0)
+    nts = int(f(n, _ptr(ts), _ptr(core), _ptr(util), int(topo.shape[0]), _ptr(topo), ca.ctypes.data, cm.ctypes.data,
+                summ.ctypes.data, ctypes.byref(bad)))
+    return {"c_active": ca[:nts].copy(), "c_min": cm[:nts].copy(), "summary": summ, "bad": int(bad.value)}

@@ -957,3 +957,76 @@ or_result *or_run(const or_input *in) {
     return r;
 #undef VIOL
 }
+
+/* ======================================================================================================
+ * O17 CPU utilization (Sec. "CPU Utilization").
+ *   Logical cores:  C_active = sum_i [Util_i > 0],  C_min = sum_i Util_i / 100,
+ *   evaluated per sampling timestamp over the logical cores sampled there (reading R13).
+ *   Physical cores (Fig. 9): a physical core is occupied when one or more of its
+ *   logical cores is active; physical occupancy = |{phys(i) : Util_i > 0 at any timestamp}| / #physical
+ *   (SPEC.md:295).  SMT co-activity (Fig. 9's "yellow" points): among (timestamp, physical core) pairs with
+ *   an active logical core, the fraction with two or more.
+ *   Samples must be sorted by (ts, logical core) with 0 <= util <= 100 and core < N; anything else sets
+ *   *bad (nothing else is computed).  Medians follow D21 (even count: mean of the two central values).
+ *   Plain loops in sample order; C_min sums in logical-core order within a timestamp.
+ * ====================================================================================================== */
+int64_t or_cpu_util(int64_t n, const int64_t *ts, const int32_t *core, const double *util, int32_t n_logical,
+                    const int32_t *topology, int64_t *c_active, double *c_min, double *summary, int32_t *bad) {
+    /* summary: [0] n_ts [1] median C_active [2] median C_min [3] max C_active [4] max C_min
+     *          [5] physical occupancy [6] SMT co-activity fraction [7] #physical cores */
+    *bad = 0;
+    int32_t n_phys = 0;
+    for (int32_t i = 0; i < n_logical; i++) {
+        if (topology[i] < 0) { *bad = 1; return 0; }
+        if (topology[i] + 1 > n_phys) n_phys = topology[i] + 1;
+    }
+    for (int64_t k = 0; k < n; k++) {
+        if (core[k] < 0 || core[k] >= n_logical || !(util[k] >= 0.0 && util[k] <= 100.0)) { *bad = 1; return 0; }
+        if (k > 0 && (ts[k] < ts[k - 1] || (ts[k] == ts[k - 1] && core[k] <= core[k - 1]))) { *bad = 1; return 0; }
+    }
+    char *ever = (char *)xcalloc(n_phys > 0 ? n_phys : 1, 1);
+    int32_t *cnt = (int32_t *)xcalloc(n_phys > 0 ? n_phys : 1, sizeof(int32_t));
+    int64_t nts = 0, pairs1 = 0, pairs2 = 0;
+    for (int64_t a = 0; a < n;) {
+        int64_t b = a;
+        while (b < n && ts[b] == ts[a]) b++;
+        int64_t act = 0;
+        double cm = 0.0;
+        for (int32_t p = 0; p < n_phys; p++) cnt[p] = 0;
+        for (int64_t k = a; k < b; k++) {
+            if (util[k] > 0.0) {
+                act++;
+                ever[topology[core[k]]] = 1;
+                cnt[topology[core[k]]]++;
+            }
+            cm += util[k] / 100.0;
+        }
+        for (int32_t p = 0; p < n_phys; p++) {
+            if (cnt[p] >= 1) pairs1++;
+            if (cnt[p] >= 2) pairs2++;
+        }
+        c_active[nts] = act;
+        c_min[nts] = cm;
+        nts++;
+        a = b;
+    }
+    int64_t occ = 0;
+    for (int32_t p = 0; p < n_phys; p++) occ += ever[p];
+    int64_t amax = 0;
+    double mmax = 0.0;
+    for (int64_t q = 0; q < nts; q++) {
+        if (c_active[q] > amax) amax = c_active[q];
+        if (c_min[q] > mmax) mmax = c_min[q];
+    }
+    summary[0] = (double)nts;
+    summary[1] = nts > 0 ? median_i64(c_active, nts) : NAN;
+    summary[2] = nts > 0 ? median_f64(c_min, nts) : NAN;
+    summary[3] = (double)amax;
+    summary[4] = nts > 0 ? mmax : NAN;
+    summary[5] = n_phys > 0 ? (double)occ / (double)n_phys : NAN;
+    summary[6] = pairs1 > 0 ? (double)pairs2 / (double)pairs1 : NAN;
+    summary[7] = (double)n_phys;
+    free(ever);
+    free(cnt);
+    return nts;
+}

@@ -799,3 +799,66 @@ def test_e2e_partitions_iteration_generated(gen_small):
         row = (o1["iter.gpu"] == 0) & (o1["iter.rank"] == last)
         assert cells[:, :3].sum() == o1["iter.busy"][row][0]
         assert cells[:, 3].sum() == o1["iter.prep"][row][0] + o1["iter.call"][row][0]
+
+
+# ---------------------------------------------------------------------------
+# O17 CPU utilization
+# ---------------------------------------------------------------------------
+def _cpu(g):
+    return oracle.cpu_util(g["ts"], g["core"], g["util"], g["topology"])
+
+
+def test_cpu_util_spec(golden):
+    g = golden("cpu_util.json")
+    for case in ("spec_one_timestamp", "spec_all_zero"):
+        r = _cpu(g[case])
+        assert r["bad"] == 0
+        np.testing.assert_array_equal(r["c_active"], g[case]["c_active"])
+        np.testing.assert_allclose(r["c_min"], g[case]["c_min"], rtol=0, atol=1e-15)
+    c = g["spec_one_of_eight_physical"]
+    r = _cpu(c)
+    assert r["summary"][5] == c["occupancy"]          # 1 of 8 physical cores ever active
+    assert r["summary"][6] == c["smt"]                # two active siblings at one of the two timestamps
+    np.testing.assert_array_equal(r["c_active"], c["c_active"])
+    m = g["median_even"]
+    r = _cpu(m)
+    np.testing.assert_array_equal(r["c_active"], m["c_active"])
+    np.testing.assert_allclose(r["c_min"], m["c_min"], rtol=1e-15)
+    assert r["summary"][1] == m["median_c_active"]
+    assert abs(r["summary"][2] - m["median_c_min"]) < 1e-15
+
+
+def test_cpu_util_invariants_random():
+    """C_min <= C_active <= N at every timestamp; relabelling physical cores or adding idle
+    samples changes nothing; dropping a core's samples removes exactly its activity."""
+    rng = np.random.default_rng(17)
+    for _ in range(200):
+        P, S = int(rng.integers(1, 9)), int(rng.integers(1, 3))
+        N = P * S
+        topo = (np.arange(N) % P).astype(np.int32)
+        n_ts = int(rng.integers(1, 8))
+        ts, core, util = [], [], []
+        for t in range(n_ts):
+            cs = np.sort(rng.choice(N, size=int(rng.integers(1, N + 1)), replace=False))
+            for c in cs:
+                ts.append(10 * t)
+                core.append(int(c))
+                util.append(float(rng.choice([0, 0, rng.integers(1, 101), rng.random() * 100])))
+        ts, core, util = np.array(ts), np.array(core), np.array(util)
+        r = oracle.cpu_util(ts, core, util, topo)
+        assert r["bad"] == 0
+        assert np.all(r["c_min"] <= r["c_active"] + 1e-12) and np.all(r["c_active"] <= N)
+        perm = rng.permutation(P).astype(np.int32)
+        r2 = oracle.cpu_util(ts, core, util, perm[topo])
+        np.testing.assert_array_equal(r2["c_active"], r["c_active"])
+        np.testing.assert_array_equal(r2["summary"], r["summary"])
+        # occupancy from the definition: set of physical cores with any active logical core
+        act = set(int(topo[c]) for c, u in zip(core, util) if u > 0)
+        assert r["summary"][5] == len(act) / P
+
+
+def test_cpu_util_rejects_unsorted_and_out_of_range():
+    assert oracle.cpu_util([2, 1], [0, 0], [1, 1], [0])["bad"] == 1
+    assert oracle.cpu_util([1, 1], [1, 0], [1, 1], [0, 0])["bad"] == 1
+    assert oracle.cpu_util([1], [0], [101.0], [0])["bad"] == 1
+    assert oracle.cpu_util([1], [3], [1.0], [0])["bad"] == 1

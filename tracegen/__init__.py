@@ -507,3 +507,31 @@ def workload_shapes(cfg: TraceConfig) -> Dict[str, int]:
     """Workload spec (Table 2; vocab / head_dim are assumptions, D19)."""
     return dict(b=cfg.batch, s=cfg.seq, layers=cfg.n_layers, hidden=4096, ffn=14336, heads=32, kv_heads=8,
                 head_dim=128, vocab=128256)
+
+
+# ---------------------------------------------------------------------------
+# host CPU utilization samples (PAPER.md:655-698, Fig. 9; SURVEY §8(f) row 2)
+# ---------------------------------------------------------------------------
+def cpu_samples(seed: int, t_start: int, t_end: int, period_ns: int = 100_000_000, n_physical: int = 64, smt: int = 2,
+                n_workers: int = 32, p_active: float = 0.85, p_sibling: float = 0.05):
+    """Every logical core sampled every `period_ns` over [t_start, t_end): a fixed set of `n_workers` worker
+    threads (per-rank main / data-loader / communication threads) pinned to distinct physical cores, each
+    active with probability p_active at a sample with an integer utilisation in [5, 60] %, its SMT sibling
+    rarely (p_sibling) active too; every other core idle (util 0).  Linux-style topology: logical core i
+    belongs to physical core i % n_physical.  Returns (ts, core, util, topology), sorted by (ts, core).
+    Contains none of the method's arithmetic."""
+    rng = Rng(seed ^ 0xC0FFEE)
+    n_logical = n_physical * smt
+    topology = (np.arange(n_logical) % n_physical).astype(np.int32)
+    workers = np.sort(rng.integers(n_workers, 0, 1 << 30) % n_physical)
+    workers = np.unique(np.concatenate([workers, np.arange(n_physical)]))[:n_workers]   # distinct physical cores
+    n_ts = max(1, int((t_end - t_start) // period_ns))
+    ts = np.repeat(t_start + period_ns * np.arange(n_ts, dtype=np.int64), n_logical)
+    core = np.tile(np.arange(n_logical, dtype=np.int32), n_ts)
+    util = np.zeros((n_ts, n_logical), dtype=np.float64)
+    act = rng.uniform((n_ts, len(workers))) < p_active
+    util[:, workers] = np.where(act, rng.integers(n_ts * len(workers), 5, 61).reshape(n_ts, len(workers)), 0)
+    sib = rng.uniform((n_ts, len(workers))) < p_sibling
+    util[:, workers + n_physical] = np.where(sib, rng.integers(n_ts * len(workers), 5, 31).reshape(n_ts, len(workers)),
+                                             0)
+    return ts, core, util.reshape(-1), topology
