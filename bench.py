@@ -99,12 +99,11 @@ class ClockSampler:
 
 
 def workload(cid: int):
-    import oracle
     import tracegen
-    b = tracegen.generate(tracegen.config(cid))
-    p = oracle.default_params(b)   # breakdown parameter dict (hardware spec, slots, FLOP table inputs)
     import paper_2512_08242_b200 as ch
-    p["f_gemm"] = ch.flops_table(b.labels, tracegen.workload_shapes(b.cfg))   # product-side Eq. 4 table
+    b = tracegen.generate(tracegen.config(cid))
+    # product-side breakdown parameters (hardware spec, counter slots, Eq. 4 FLOP table); no oracle import here
+    p = ch.default_params(b, b.labels, tracegen.workload_shapes(b.cfg), tracegen.op_kind)
     return b, p
 
 
@@ -184,6 +183,12 @@ def main():
     stream = torch.cuda.Stream(dev)
     pipe = ch.Pipeline(G, len(b.labels), 256, 1 << 15, device=local, pg=pg, stream=stream)
     pipe.upload(shard, b.n_counters)
+    cpu = None
+    if rank == 0:
+        # host CPU utilisation samples over the trace: one host trace, processed by rank 0
+        import tracegen
+        cpu = tracegen.cpu_samples(b.cfg.seed, int(b.t_l.min()), int(b.t_ke.max()))
+        pipe.upload_cpu(*cpu)
     ch.chopper_set_timing(pipe.ctx, True)
     # warm-up (W >= 3)
     for _ in range(args.warmup):
@@ -236,11 +241,18 @@ def main():
                           torch.from_numpy(np.ascontiguousarray(vals)).pin_memory())
                          for (g, nm, sl, vals) in shard.passes]
         h2d = input_bytes(shard)
+        pinned_cpu = {}
+        if cpu is not None:
+            for k, v in zip(("ts", "core", "util", "topo"), cpu):
+                pinned_cpu[k] = torch.from_numpy(np.ascontiguousarray(v, pipe.cpu[k].cpu().numpy().dtype)).pin_memory()
+                h2d += pinned_cpu[k].numel() * pinned_cpu[k].element_size()
 
         def e2e_step():
             with torch.cuda.stream(stream):
                 for k, v in pinned.items():
                     pipe.d[k].copy_(v, non_blocking=True)
+                for k, v in pinned_cpu.items():
+                    pipe.cpu[k].copy_(v, non_blocking=True)
                 for q, (g, nm, sl, vals) in enumerate(pinned_passes):
                     pipe.passes_dev[q][1].copy_(nm, non_blocking=True)
                     pipe.passes_dev[q][3].copy_(vals, non_blocking=True)

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define CHOPPER_ABI_VERSION 4
+#define CHOPPER_ABI_VERSION 5
 
 typedef struct chopper_ctx chopper_ctx;
 typedef int32_t chopper_status;
@@ -249,6 +249,34 @@ chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
  * duration, overlap ratio, empirical CDF (k + 1) / n.  out: host buffer of cap rows (may be NULL when cap is
  * 0); *n_rows = number of rows (the first min(cap, *n_rows) are written).  Synchronizes the ctx stream. */
 chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows);
+
+/* CPU utilization (Sec. "CPU Utilization": C_active = sum_i [Util_i > 0],
+ * C_min = sum_i Util_i / 100, logical -> physical cores; R13).
+ * samples: n host-core utilisation samples, DEVICE pointers, sorted by (ts_ns, logical_core) with
+ *   0 <= util_pct <= 100 and 0 <= logical_core < n_logical.  topology: DEVICE [n_logical] logical -> physical
+ *   core id (>= 0).  Per distinct timestamp: C_active = #samples with util > 0, C_min = sum of util / 100 in
+ *   logical-core order.  c_active / c_min: DEVICE outputs of cap entries (nullable; the first min(cap, n_ts)
+ *   are written).  *out (host): timestamps, D21 medians and maxima of C_active and C_min, physical occupancy
+ *   (#physical cores with an active logical core at any timestamp / #physical cores) and SMT co-activity
+ *   (fraction of (timestamp, physical core) pairs with an active logical core that have two or more).
+ * Borrowed inputs, scratch from the ctx arena (released before returning).  Unsorted or out-of-range samples
+ * or a negative topology entry -> CHOPPER_E_VALIDATION (*out not written, per-timestamp outputs undefined).  Independent of the trace calls
+ * (valid at any stage after chopper_create).  Synchronizes the ctx stream. */
+typedef struct {
+    int64_t n;
+    const int64_t *ts_ns;
+    const int32_t *logical_core;
+    const double *util_pct;
+} chopper_cpu_samples;
+typedef struct {
+    int64_t n_ts;
+    int32_t n_logical, n_physical;
+    double c_active_median, c_min_median, c_active_max, c_min_max;
+    double physical_occupancy, smt_coactive;
+} chopper_cpu_summary;
+chopper_status chopper_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *samples, const int32_t *topology,
+                                int32_t n_logical, int64_t *c_active, double *c_min, int64_t cap,
+                                chopper_cpu_summary *out);
 
 /* report of the last chopper_load_columns (host copy) */
 chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out);

@@ -122,12 +122,23 @@ class chopper_report(ctypes.Structure):
                 ("non_laminar_lists", I32)]
 
 
+class chopper_cpu_samples(ctypes.Structure):
+    _fields_ = [("n", I64), ("ts_ns", P), ("logical_core", P), ("util_pct", P)]
+
+
+class chopper_cpu_summary(ctypes.Structure):
+    _fields_ = [("n_ts", I64), ("n_logical", I32), ("n_physical", I32), ("c_active_median", F64),
+                ("c_min_median", F64), ("c_active_max", F64), ("c_min_max", F64), ("physical_occupancy", F64),
+                ("smt_coactive", F64)]
+
+
 # every symbol include/chopper.h declares
 EXPORTS = ["chopper_scratch_bytes", "chopper_create", "chopper_load_columns", "chopper_align", "chopper_attribute",
            "chopper_overlap", "chopper_breakdown", "chopper_reduce_ranks", "chopper_get_report",
            "chopper_status_sync", "chopper_last_error", "chopper_destroy", "chopper_kernel_launches",
            "chopper_abi_version", "chopper_pass_mismatch", "chopper_pass_conflict", "chopper_counter_present",
-           "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time", "chopper_report_cdf"]
+           "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time", "chopper_report_cdf",
+           "chopper_cpu_util"]
 
 _lib = None
 
@@ -165,6 +176,8 @@ def load_library() -> ctypes.CDLL:
         "chopper_set_timing": (None, [P, I32]),
         "chopper_phase_time": (I32, [P, I32, ctypes.POINTER(ctypes.c_float)]),
         "chopper_report_cdf": (I32, [P, P, I64, ctypes.POINTER(I64)]),
+        "chopper_cpu_util": (I32, [P, ctypes.POINTER(chopper_cpu_samples), P, I32, P, P, I64,
+                                   ctypes.POINTER(chopper_cpu_summary)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -337,4 +350,17 @@ def bd_params(p: dict) -> chopper_bd_params:
     return q
 
 
-from .pipeline import Pipeline, flops_table  # noqa: E402,F401
+def chopper_cpu_util(ctx, ts, core, util, topology, c_active=None, c_min=None):
+    """CPU utilization (PAPER.md:655-698) over device tensors (int64 ts, int32 core, float64 util, int32 topology);
+    optional device outputs c_active (int64) / c_min (float64) per timestamp.  Returns the summary as a dict."""
+    lib = load_library()
+    s = chopper_cpu_samples(int(ts.numel()), _ptr(ts), _ptr(core), _ptr(util))
+    out = chopper_cpu_summary()
+    cap = 0 if c_active is None else int(c_active.numel())
+    _check(ctx, lib.chopper_cpu_util(ctx, ctypes.byref(s), _ptr(topology), int(topology.numel()), _ptr(c_active),
+                                     _ptr(c_min), cap, ctypes.byref(out)), "chopper_cpu_util")
+    return {k: getattr(out, k) for k, _ in chopper_cpu_summary._fields_}
+
+
+from .pipeline import Pipeline, default_params, flops_table  # noqa: E402,F401
+

@@ -240,6 +240,15 @@ chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, in
     return ch_report_cdf(ctx, out, cap, n_rows);
 }
 
+chopper_status chopper_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *samples, const int32_t *topology,
+                                int32_t n_logical, int64_t *c_active, double *c_min, int64_t cap,
+                                chopper_cpu_summary *out) {
+    if (!ctx || !samples || !out || samples->n < 0 || n_logical <= 0 || !topology || cap < 0 ||
+        (samples->n > 0 && (!samples->ts_ns || !samples->logical_core || !samples->util_pct)))
+        return CHOPPER_E_INVALID_ARG;
+    return ch_cpu_util(ctx, samples, topology, n_logical, c_active, c_min, cap, out);
+}
+
 chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out) {
     if (!ctx || !out) return CHOPPER_E_INVALID_ARG;
     *out = ctx->rep;

@@ -411,6 +411,8 @@ chopper_status ch_tables(chopper_ctx *ctx);
 chopper_status ch_breakdown_local(chopper_ctx *ctx);
 chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
 chopper_status ch_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows);
+chopper_status ch_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *s, const int32_t *topology, int32_t n_logical,
+                           int64_t *c_active, double *c_min, int64_t cap, chopper_cpu_summary *out);
 chopper_status ch_nccl_allgather(chopper_ctx *ctx, const void *send, void *recv, size_t bytes_per_rank);
 
 // lookup of an event's innermost span per level (spans.cu; used by events.cu)

@@ -683,6 +683,131 @@ __global__ void __launch_bounds__(256) k_global(GlobArgs A) {
     if (nst > 0) m = med_f64(A.work, nst, nullptr);
     if (threadIdx.x == 0) *A.med = m;
 }
+
+// ---- CPU utilization (R13) ------------------------------
+constexpr int CPU_PHYS_MAX = 4096, CPU_PW = CPU_PHYS_MAX / 32;
+struct CpuArgs {
+    int64_t n;
+    const int64_t *ts;
+    const int32_t *core;
+    const double *util;
+    const int32_t *topo;
+    int32_t n_logical;
+};
+// validation, timestamp heads (int64 flags for the scan) and the number of physical cores
+__global__ void k_cpu_check(CpuArgs A, int64_t *__restrict__ head, unsigned int *__restrict__ bad,
+                            int *__restrict__ n_phys) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < A.n_logical) {
+        const int p = A.topo[k];
+        if (p < 0 || p >= CPU_PHYS_MAX) atomicOr(bad, 1u);
+        else atomicMax(n_phys, p + 1);
+    }
+    if (k >= A.n) return;
+    const int64_t t = A.ts[k];
+    const int c = A.core[k];
+    const double u = A.util[k];
+    bool ok = c >= 0 && c < A.n_logical && u >= 0.0 && u <= 100.0;
+    if (k > 0) {
+        const int64_t tp = A.ts[k - 1];
+        if (t < tp || (t == tp && c <= A.core[k - 1])) ok = false;
+    }
+    if (!ok) atomicOr(bad, 1u);
+    head[k] = (k == 0 || t != A.ts[k - 1]) ? 1 : 0;
+}
+__global__ void k_cpu_starts(const int64_t *__restrict__ head, const int64_t *__restrict__ ex, int64_t n,
+                             int64_t *__restrict__ starts) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n && head[k]) starts[ex[k]] = k;
+    if (k == n - 1) starts[ex[k] + head[k]] = n;
+}
+// a warp per timestamp: C_active, C_min (lane 0, logical-core order), physical-core bitmaps
+__global__ void __launch_bounds__(256) k_cpu_ts(CpuArgs A, const int64_t *__restrict__ starts,
+                                                const int64_t *__restrict__ n_ts_d, const int *__restrict__ n_phys_d,
+                                                int64_t *__restrict__ ca, double *__restrict__ cm,
+                                                unsigned int *__restrict__ ever,
+                                                unsigned long long *__restrict__ pairs,
+                                                const unsigned int *__restrict__ bad) {
+    __shared__ unsigned int b1[8][CPU_PW], b2[8][CPU_PW];
+    if (*bad) return;                 // invalid samples: nothing is computed
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int nw = (*n_phys_d + 31) >> 5;
+    const int64_t n_ts = *n_ts_d;
+    for (int64_t q = (int64_t)blockIdx.x * 8 + w; q < n_ts; q += (int64_t)gridDim.x * 8) {
+        for (int x = l; x < nw; x += 32) { b1[w][x] = 0u; b2[w][x] = 0u; }
+        __syncwarp();
+        const int64_t a = starts[q], b = starts[q + 1];
+        int64_t act = 0;
+        for (int64_t k0 = a; k0 < b; k0 += 32) {
+            const int64_t k = k0 + l;
+            const bool on = k < b && A.util[k] > 0.0;
+            act += __popc(__ballot_sync(CH_FULL, on));
+            if (on) {
+                const int p = A.topo[A.core[k]];
+                const unsigned bit = 1u << (p & 31);
+                const unsigned old = atomicOr(&b1[w][p >> 5], bit);
+                if (old & bit) atomicOr(&b2[w][p >> 5], bit);
+            }
+        }
+        __syncwarp();
+        unsigned long long p1 = 0, p2 = 0;
+        for (int x = l; x < nw; x += 32) {
+            p1 += __popc(b1[w][x]);
+            p2 += __popc(b2[w][x]);
+            if (b1[w][x]) atomicOr(&ever[x], b1[w][x]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            p1 += __shfl_xor_sync(CH_FULL, p1, o);
+            p2 += __shfl_xor_sync(CH_FULL, p2, o);
+        }
+        if (l == 0) {
+            double s = 0.0;
+            for (int64_t k = a; k < b; k++) s += A.util[k] / 100.0;     // PAPER.md:676, logical-core order
+            ca[q] = act;
+            cm[q] = s;
+            if (p1) atomicAdd(&pairs[0], p1);
+            if (p2) atomicAdd(&pairs[1], p2);
+        }
+        __syncwarp();
+    }
+}
+// medians (D21, block bitonic over pow2-padded work arrays), maxima, occupancy, SMT co-activity
+__global__ void __launch_bounds__(512) k_cpu_summary(int64_t *__restrict__ ca, double *__restrict__ cm,
+                                                     const int64_t *__restrict__ n_ts_d, const int *__restrict__ n_phys_d,
+                                                     const unsigned int *__restrict__ ever,
+                                                     const unsigned long long *__restrict__ pairs,
+                                                     const unsigned int *__restrict__ bad, double *__restrict__ out) {
+    __shared__ int64_t s_amax;
+    __shared__ double s_mmax;
+    __shared__ int s_occ;
+    if (*bad) return;
+    const int n = (int)*n_ts_d;
+    const int n_phys = *n_phys_d;
+    if (threadIdx.x == 0) { s_amax = 0; s_mmax = 0.0; s_occ = 0; }
+    __syncthreads();
+    int64_t am = 0;
+    double mm = 0.0;
+    for (int q = threadIdx.x; q < n; q += blockDim.x) {
+        am = ca[q] > am ? ca[q] : am;
+        mm = cm[q] > mm ? cm[q] : mm;
+    }
+    atomicMax((unsigned long long *)&s_amax, (unsigned long long)am);
+    atomicMax((unsigned long long *)&s_mmax, (unsigned long long)__double_as_longlong(mm));   // non-negative doubles
+    for (int x = threadIdx.x; x < (n_phys + 31) / 32; x += blockDim.x) atomicAdd(&s_occ, __popc(ever[x]));
+    __syncthreads();
+    const double ma = n > 0 ? med_i64(ca, n, nullptr) : NAN;
+    const double mc = n > 0 ? med_f64(cm, n, nullptr) : NAN;
+    if (threadIdx.x == 0) {
+        out[0] = n;
+        out[1] = ma;
+        out[2] = mc;
+        out[3] = (double)s_amax;
+        out[4] = n > 0 ? s_mmax : NAN;
+        out[5] = n_phys > 0 ? (double)s_occ / (double)n_phys : NAN;
+        out[6] = pairs[0] > 0 ? (double)pairs[1] / (double)pairs[0] : NAN;
+    }
+}
 }  // namespace
 
 static Layout layout_of(chopper_ctx *ctx) {
@@ -981,5 +1106,64 @@ chopper_status ch_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t
     if (m > 0 && out) CH_CUDA(ctx, cudaMemcpy(out, rows, 8 * 5 * (size_t)m, cudaMemcpyDeviceToHost));
     ctx->used = mark;
     *n_rows = n;
+    return CHOPPER_OK;
+}
+
+chopper_status ch_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *S, const int32_t *topology, int32_t n_logical,
+                           int64_t *c_active, double *c_min, int64_t cap, chopper_cpu_summary *out) {
+    // sizes from the sample count (n_ts <= n): one host synchronization, at the end
+    const int64_t n = S->n;
+    int64_t p2 = 1;
+    while (p2 < std::max<int64_t>(n, 1)) p2 <<= 1;
+    if (p2 > (1ll << 30)) return ch_fail(ctx, CHOPPER_E_RANGE, "too many CPU samples");
+    const size_t mark = ctx->used;
+    CH_ALLOC_BEGIN;
+    int64_t *head = CH_ALLOC(ctx, int64_t, n + 1), *ex = CH_ALLOC(ctx, int64_t, n + 1);
+    int64_t *starts = CH_ALLOC(ctx, int64_t, n + 2), *n_ts_d = CH_ALLOC(ctx, int64_t, 1);
+    int64_t *ca = CH_ALLOC(ctx, int64_t, p2);
+    double *cm = CH_ALLOC(ctx, double, p2);
+    unsigned int *ever = CH_ALLOC(ctx, unsigned int, CPU_PW);
+    unsigned long long *pairs = CH_ALLOC(ctx, unsigned long long, 2);
+    double *dsum = CH_ALLOC(ctx, double, 8);
+    unsigned int *bad = CH_ALLOC(ctx, unsigned int, 2);      // [0] bad, [1] n_physical
+    CH_ALLOC_END(ctx);
+    CpuArgs A{n, S->ts_ns, S->logical_core, S->util_pct, topology, n_logical};
+    CH_CUDA(ctx, cudaMemsetAsync(bad, 0, 8, ctx->st));
+    CH_CUDA(ctx, cudaMemsetAsync(ever, 0, 4 * CPU_PW, ctx->st));
+    CH_CUDA(ctx, cudaMemsetAsync(pairs, 0, 16, ctx->st));
+    int *nph = reinterpret_cast<int *>(bad + 1);
+    const int64_t m = std::max<int64_t>(n, n_logical);
+    k_cpu_check<<<(unsigned)ceil_div(std::max<int64_t>(m, 1), 256), 256, 0, ctx->st>>>(A, head, bad, nph);
+    CH_LAUNCHED(ctx);
+    if (n > 0) {
+        CH_TRY(ch_scan_excl_i64(ctx, head, ex, n, n_ts_d));
+        k_cpu_starts<<<(unsigned)ceil_div(n, 256), 256, 0, ctx->st>>>(head, ex, n, starts);
+        CH_LAUNCHED(ctx);
+        k_cpu_ts<<<(unsigned)std::min<int64_t>(ceil_div(n, 8), 148 * 8), 256, 0, ctx->st>>>(A, starts, n_ts_d, nph, ca, cm,
+                                                                                           ever, pairs, bad);
+        CH_LAUNCHED(ctx);
+        if (c_active && cap > 0) CH_CUDA(ctx, cudaMemcpyAsync(c_active, ca, 8 * std::min(cap, n), cudaMemcpyDeviceToDevice, ctx->st));
+        if (c_min && cap > 0) CH_CUDA(ctx, cudaMemcpyAsync(c_min, cm, 8 * std::min(cap, n), cudaMemcpyDeviceToDevice, ctx->st));
+    } else {
+        CH_CUDA(ctx, cudaMemsetAsync(n_ts_d, 0, 8, ctx->st));
+    }
+    k_cpu_summary<<<1, 512, 0, ctx->st>>>(ca, cm, n_ts_d, nph, ever, pairs, bad, dsum);
+    CH_LAUNCHED(ctx);
+    double h[8];
+    unsigned int hb[2];
+    CH_CUDA(ctx, cudaMemcpyAsync(h, dsum, 8 * 7, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(hb, bad, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    ctx->used = mark;
+    if (hb[0]) return ch_fail(ctx, CHOPPER_E_VALIDATION, "CPU samples unsorted or out of range, or a bad topology entry");
+    out->n_ts = (int64_t)h[0];
+    out->n_logical = n_logical;
+    out->n_physical = (int32_t)hb[1];
+    out->c_active_median = h[1];
+    out->c_min_median = h[2];
+    out->c_active_max = h[3];
+    out->c_min_max = h[4];
+    out->physical_occupancy = h[5];
+    out->smt_coactive = h[6];
     return CHOPPER_OK;
 }

@@ -13,7 +13,7 @@ from typing import Dict, Optional
 import numpy as np
 
 from . import (chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
-               chopper_create, chopper_destroy, chopper_events, chopper_get_report, chopper_global, chopper_report_cdf,
+               chopper_cpu_util, chopper_create, chopper_destroy, chopper_events, chopper_get_report, chopper_global, chopper_report_cdf,
                chopper_kernel_launches, chopper_load_columns, chopper_overlap, chopper_reduce_ranks,
                chopper_samples, chopper_scratch_bytes, chopper_spans, chopper_status_sync, chopper_tables,
                _check, bd_params, dev_to_numpy, load_library, rows_to_numpy)
@@ -47,6 +47,25 @@ def flops_table(labels, shapes: Dict[str, int], bwd_gemm: float = 2.0, bwd_fa: f
     return out
 
 
+def default_params(cols, labels, shapes: Dict[str, int], op_kind) -> dict:
+    """Host-side breakdown parameters for a run (chopper_bd_params): the hardware spec (MI300X peak dense
+    throughput and clock), the workload (b, s, R, warm-up), the counter-slot layout of
+    the trace, the Eq. 4 FLOP table (flops_table) and op types.  Plumbing only."""
+    cfg = cols.cfg
+    C = cols.n_counters
+    p = dict(tpt_peak=1.3e15, freq_peak_hz=2.1e9, b=cfg.batch, s=cfg.seq, R=cfg.n_gpus, warmup=cfg.warmup,
+             slot_cycles=0 if C > 0 else -1, slot_flops=1 if C > 1 else -1,
+             slot_unum=2 if C > 3 else -1, slot_uden=3 if C > 3 else -1,
+             f_gemm=flops_table(labels, shapes), op_type=np.array([op_kind(l) for l in labels], dtype=np.int32))
+    if C >= 6:
+        # bandwidth = bytes / duration (PAPER.md:251), and a counter/counter ratio
+        p.update(ratio_num=np.array([4, 5, 1], dtype=np.int32), ratio_den=np.array([-1, -1, 0], dtype=np.int32),
+                 ratio_scale=np.array([1.0, 1.0, 1.0], dtype=np.float64))
+    else:
+        p.update(ratio_num=np.zeros(0, np.int32), ratio_den=np.zeros(0, np.int32), ratio_scale=np.zeros(0))
+    return p
+
+
 def _i64(a):
     return np.ascontiguousarray(a, dtype=np.int64)
 
@@ -78,6 +97,17 @@ class Pipeline:
         self.ctx = None
         self.scratch = None
         self.d = {}
+        self.cpu = None
+
+    def upload_cpu(self, ts, core, util, topology) -> None:
+        """Host CPU utilisation samples (sorted by (ts, logical core)) and the logical -> physical topology."""
+        torch = self.torch
+        dev = torch.device("cuda", self.device)
+        with torch.cuda.stream(self.stream):
+            self.cpu = {"ts": torch.from_numpy(_i64(ts)).to(dev),
+                        "core": torch.from_numpy(np.ascontiguousarray(core, np.int32)).to(dev),
+                        "util": torch.from_numpy(np.ascontiguousarray(util, np.float64)).to(dev),
+                        "topo": torch.from_numpy(np.ascontiguousarray(topology, np.int32)).to(dev)}
 
     # ---- inputs ----
     def upload(self, cols, n_counters: int, pinned_host: Optional[dict] = None) -> None:
@@ -166,6 +196,13 @@ class Pipeline:
         glob = chopper_global()
         _check(self.ctx, chopper_reduce_ranks(self.ctx, glob), "chopper_reduce_ranks")
         cdf = chopper_report_cdf(self.ctx) if full else None
+        if self.cpu is not None:
+            c = self.cpu
+            n = max(int(c["ts"].numel()), 1)
+            out["cpu_active"] = torch.empty(n, dtype=torch.int64, device=dev)
+            out["cpu_min"] = torch.empty(n, dtype=torch.float64, device=dev)
+            res["cpu"] = chopper_cpu_util(self.ctx, c["ts"], c["core"], c["util"], c["topo"], out["cpu_active"],
+                                          out["cpu_min"])
         st, mask = chopper_status_sync(self.ctx)
         res.update(status=st, mask=mask, offsets=offs, tables=tabs, glob=glob, out=out,
                    report=chopper_get_report(self.ctx), cdf=cdf)
@@ -210,6 +247,14 @@ class Pipeline:
         o["e2e.rows"] = np.array(g.e2e[:33], np.float64)
         if res.get("cdf") is not None:
             o["cdf.rows"] = res["cdf"].reshape(-1)
+        if res.get("cpu") is not None:
+            c = res["cpu"]
+            nts = int(c["n_ts"])
+            o["cpu.c_active"] = res["out"]["cpu_active"][:nts].cpu().numpy()
+            o["cpu.c_min"] = res["out"]["cpu_min"][:nts].cpu().numpy()
+            o["cpu.summary"] = np.array([nts, c["c_active_median"], c["c_min_median"], c["c_active_max"],
+                                         c["c_min_max"], c["physical_occupancy"], c["smt_coactive"],
+                                         c["n_physical"]], np.float64)
         G = self.cfg.n_traced_gpus
         o["gpu.delta"] = np.array(g.delta[:G], np.int64)
         o["gpu.delta_flag"] = np.array(g.delta_flag[:G], np.int32)

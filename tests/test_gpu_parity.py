@@ -349,3 +349,40 @@ def test_dense_spans_and_samples_overflow_windows():
     ref, got, res, _ = run_both(b, p)
     _check_status(ref, got)
     assert_parity(ref, got)
+
+
+def _cpu_both(ts, core, util, topo):
+    import torch
+    import paper_2512_08242_b200 as ch
+    ref = oracle.cpu_util(ts, core, util, topo)
+    b = TinyTrace().ev(0, 0, 10, 20).span(0, 0, 0, 100).bundle()
+    pipe = ch.Pipeline(1, 4, 4, 16, device=0)
+    pipe.upload(b, 0)
+    pipe.upload_cpu(ts, core, util, topo)
+    res = pipe.run(params(b), check=False)
+    got = pipe.to_numpy(res)
+    pipe.close()
+    return ref, got
+
+
+def test_cpu_util_golden_and_generated():
+    """CPU utilization through chopper_cpu_util vs O17: exact per timestamp (same
+    logical-core summation order), medians, maxima, occupancy and SMT co-activity."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cpu_util.json")))
+    cases = [g[k] for k in ("spec_one_timestamp", "spec_all_zero", "spec_one_of_eight_physical", "median_even")]
+    ts, core, util, topo = tracegen.cpu_samples(7, 1_700_000_000_000_000_000, 1_700_000_000_000_000_000 + 98 * 10 ** 9)
+    cases.append({"ts": ts, "core": core, "util": util, "topology": topo})
+    for c in cases:
+        ref, got = _cpu_both(np.asarray(c["ts"]), np.asarray(c["core"]), np.asarray(c["util"], np.float64),
+                             np.asarray(c["topology"]))
+        np.testing.assert_array_equal(ref["c_active"], got["cpu.c_active"])
+        np.testing.assert_array_equal(ref["c_min"], got["cpu.c_min"])
+        np.testing.assert_array_equal(ref["summary"], got["cpu.summary"])
+
+
+def test_cpu_util_rejects_unsorted():
+    import paper_2512_08242_b200 as ch
+    with pytest.raises(ch.ChopperError):
+        _cpu_both(np.array([2, 1]), np.array([0, 0]), np.array([1.0, 1.0]), np.array([0]))
