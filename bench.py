@@ -195,6 +195,7 @@ def main():
         res = pipe.run(p, full=False)
     launches0 = pipe.launches()
     ev_ms = []
+    ev_phase_ms = []
     clocks = ClockSampler(local)
     if rank == 0:
         clocks.start()
@@ -206,7 +207,8 @@ def main():
     t0.record(stream)
     for _ in range(args.steps):
         res = pipe.run(p, full=False)
-        ev_ms.append(ch.chopper_phase_time(pipe.ctx, 4))
+        ev_ms.append(ch.chopper_phase_time(pipe.ctx, 8))
+        ev_phase_ms.append(ch.chopper_phase_time(pipe.ctx, 4))
     t1.record(stream)
     torch.cuda.synchronize(dev)
     if pg is not None:
@@ -290,6 +292,8 @@ def main():
     R = pipe.ctx and int(ch.load_library().chopper_scratch_used(pipe.ctx))
     ev_ms = [x for x in ev_ms if x]
     ev_avg = sum(ev_ms) / len(ev_ms) if ev_ms else None
+    ev_phase_ms = [x for x in ev_phase_ms if x]
+    ev_phase_avg = sum(ev_phase_ms) / len(ev_phase_ms) if ev_phase_ms else None
     # algorithmic bytes per launch: event columns read by the pass
     # (t_l, t_ks, t_ke 24 B, meta 4 B, pred_end 8 B) + run id written (4 B, counters present)
     # + one 128 B sub-run row per instance run
@@ -306,8 +310,10 @@ def main():
     achieved = alg / (ev_avg * 1e-3) / 1e9 if ev_avg else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": "event pass a5-a9 (k_tile_seeds + k_tile_heads + k_events_w; time = the whole phase)",
+            "kernel": "k_events_w (main event-pass kernel, a5-a9; time = its own CUDA-event bracket)",
             "peak_source": peak_src, "alg_bytes_per_launch": alg, "avg_launch_ms": ev_avg,
+            "event_pass_phase_ms": ev_phase_avg,
+            "event_pass_phase_frac": (alg / (ev_phase_avg * 1e-3) / 1e9 / peak) if ev_phase_avg else None,
             "phase_ms_last_step": phase_ms}
 
     cpu = None

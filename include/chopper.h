@@ -300,8 +300,8 @@ int64_t chopper_scratch_used(const chopper_ctx *ctx);
 
 /* Device timing of pipeline phases with CUDA events recorded on the ctx
  * stream (off by default).  phase: 0 load, 1 align, 2 attribute,
- * 3 overlap prep, 4 fused event pass kernel, 5 tables, 6 breakdown,
- * 7 reduce_ranks.  chopper_phase_time returns 0 and *ms for the most recent
+ * 3 overlap prep, 4 event pass (its seed / window / head passes and the main kernel), 5 tables,
+ * 6 breakdown, 7 reduce_ranks, 8 the main event-pass kernel alone (k_events_w / k_events).  chopper_phase_time returns 0 and *ms for the most recent
  * run of that phase, CHOPPER_E_STATE if it was not timed. */
 void chopper_set_timing(chopper_ctx *ctx, int32_t on);
 chopper_status chopper_phase_time(chopper_ctx *ctx, int32_t phase, float *ms);

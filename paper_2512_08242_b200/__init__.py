@@ -286,7 +286,8 @@ def chopper_set_timing(ctx, on: bool) -> None:
     load_library().chopper_set_timing(ctx, 1 if on else 0)
 
 
-PHASES = ["load", "align", "attribute", "overlap_prep", "event_pass", "tables", "breakdown", "reduce_ranks"]
+PHASES = ["load", "align", "attribute", "overlap_prep", "event_pass", "tables", "breakdown", "reduce_ranks",
+          "event_kernel"]
 
 
 def chopper_phase_time(ctx, phase: int) -> Optional[float]:

@@ -304,7 +304,7 @@ void chopper_set_timing(chopper_ctx *ctx, int32_t on) {
 }
 
 chopper_status chopper_phase_time(chopper_ctx *ctx, int32_t phase, float *ms) {
-    if (!ctx || !ms || phase < 0 || phase >= 8) return CHOPPER_E_INVALID_ARG;
+    if (!ctx || !ms || phase < 0 || phase >= 9) return CHOPPER_E_INVALID_ARG;
     if (!ctx->timed[phase]) return CHOPPER_E_STATE;
     if (cudaEventSynchronize(ctx->tev[phase][1]) != cudaSuccess) return CHOPPER_E_CUDA;
     if (cudaEventElapsedTime(ms, ctx->tev[phase][0], ctx->tev[phase][1]) != cudaSuccess) return CHOPPER_E_CUDA;

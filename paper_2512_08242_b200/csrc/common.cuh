@@ -219,8 +219,8 @@ struct chopper_ctx {
     int32_t *d_has_smp = nullptr;    // [n_lg]
     // phase timing (chopper_set_timing)
     bool timing = false;
-    cudaEvent_t tev[8][2] = {};
-    bool timed[8] = {};
+    cudaEvent_t tev[9][2] = {};
+    bool timed[9] = {};
     int64_t *d_dense = nullptr;      // local dense exchange blocks [dense_slots][W]
     unsigned int *d_dense_ovf = nullptr;
     int64_t *d_all = nullptr;        // all-gathered dense blocks (chopper_reduce_ranks), read by the report CDF
@@ -329,6 +329,9 @@ __device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");

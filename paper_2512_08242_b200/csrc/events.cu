@@ -1715,8 +1715,10 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, tcnt, tbase, ntile, tbase + ntile));
         P.tile_base = tbase;
+        ch_tick(ctx, 8, 0);
         k_events_w<<<(unsigned)ntile, W_NT, dsm, ctx->st>>>(P, vec_ok);
         CH_LAUNCHED(ctx);
+        ch_tick(ctx, 8, 1);
         ch_tick(ctx, 4, 1);
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_tile_state + ntile - 1, tbase + ntile, 8, cudaMemcpyDeviceToDevice, ctx->st));
         ctx->used = mark;
@@ -1729,8 +1731,10 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
             attr_set = true;
         }
         ch_tick(ctx, 4, 0);
+        ch_tick(ctx, 8, 0);
         k_events<<<(unsigned)ntile, EV_NT, dsm, ctx->st>>>(P, vec_ok);
         CH_LAUNCHED(ctx);
+        ch_tick(ctx, 8, 1);
         ch_tick(ctx, 4, 1);
     }
     if (ovl && ctx->n_lg > 0) {
