@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define CHOPPER_ABI_VERSION 5
+#define CHOPPER_ABI_VERSION 6
 
 typedef struct chopper_ctx chopper_ctx;
 typedef int32_t chopper_status;
@@ -153,11 +153,13 @@ typedef struct {
     /* iteration rows only (else NULL) */
     const int64_t *wall, *comm_union, *aligned_first, *aligned_last;
     const int32_t *step;
+    const double *metrics;                    /* [n_metrics][stride] registry values (points, iterations) or NULL */
 } chopper_rows;
 
 typedef struct {
     chopper_rows inst, layer, phase, iter, gpu, point;
     int64_t n_bd;                             /* local breakdown rows */
+    int32_t n_metrics;                        /* derived-metric registry size (chopper_set_metrics) */
     const double *bd;                         /* device [n_bd][16], layout as chopper_global.bd */
 } chopper_tables;
 
@@ -249,6 +251,18 @@ chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
  * duration, overlap ratio, empirical CDF (k + 1) / n.  out: host buffer of cap rows (may be NULL when cap is
  * 0); *n_rows = number of rows (the first min(cap, *n_rows) are written).  Synchronizes the ctx stream. */
 chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows);
+
+/* Derived-metric registry ("calculating bandwidth from
+ * transferred bytes and kernel duration"; R14).  exprs: n infix expressions (host strings) over
+ * names[slot] (host strings: the counter slot names) and dur_s (the row's busy time, seconds): numbers,
+ * identifiers, + - * /, parentheses, unary minus; * and / bind tighter than + and -, binary operators are
+ * left-associative.  Compiled once on the host to postfix programs; every later chopper_breakdown evaluates
+ * them on the device for each point and iteration row over the row's summed counters (chopper_rows.metrics,
+ * [n][stride]).  A zero divisor gives NaN for that row.  Errors: an unknown name (MissingCounter) or a syntax
+ * error (ParseError) -> CHOPPER_E_INVALID_ARG, *bad_expr = the failing index (-1 on success), the registry is
+ * cleared; a name whose slot the trace lacks -> CHOPPER_E_INVALID_ARG at chopper_breakdown.  n = 0 clears. */
+chopper_status chopper_set_metrics(chopper_ctx *ctx, int32_t n, const char *const *exprs, int32_t n_names,
+                                   const char *const *names, int32_t *bad_expr);
 
 /* CPU utilization (Sec. "CPU Utilization": C_active = sum_i [Util_i > 0],
  * C_min = sum_i Util_i / 100, logical -> physical cores; R13).

@@ -211,3 +211,99 @@ def cpu_util(ts, core, util, topology) -> Dict[str, np.ndarray]:
     nts = int(f(n, _ptr(ts), _ptr(core), _ptr(util), int(topo.shape[0]), _ptr(topo), ca.ctypes.data, cm.ctypes.data,
                 summ.ctypes.data, ctypes.byref(bad)))
     return {"c_active": ca[:nts].copy(), "c_min": cm[:nts].copy(), "summary": summ, "bad": int(bad.value)}
+
+
+
+# ---------------------------------------------------------------------------
+# derived-metric registry: a recursive-descent evaluator
+#   expr := term (('+' | '-') term)* ; term := unary (('*' | '/') unary)* ; unary := '-' unary | primary
+#   primary := number | identifier | '(' expr ')'   (binary operators left-associative)
+# identifiers: counter names (the row's summed counter) and dur_s (the row's busy seconds); a zero divisor
+# gives NaN (reading R14).
+# ---------------------------------------------------------------------------
+class MetricError(ValueError):
+    pass
+
+
+def _metric_tokens(e: str):
+    import re
+    toks, i = [], 0
+    pat = re.compile(r"\s*(?:(\d+\.?\d*(?:[eE][+-]?\d+)?|\.\d+(?:[eE][+-]?\d+)?)|([A-Za-z_][A-Za-z0-9_.]*)|(.))")
+    while i < len(e):
+        m = pat.match(e, i)
+        if not m or m.end() == i:
+            break
+        i = m.end()
+        if m.group(1):
+            toks.append(("num", float(m.group(1))))
+        elif m.group(2):
+            toks.append(("id", m.group(2)))
+        elif m.group(3) and not m.group(3).isspace():
+            if m.group(3) not in "+-*/()":
+                raise MetricError(f"ParseError: unexpected character {m.group(3)!r}")
+            toks.append(("op", m.group(3)))
+    return toks
+
+
+def metric_eval(expr: str, names, counters, busy_ns):
+    """Evaluate one registry expression over rows: counters [C][n] (summed per row), busy_ns [n]."""
+    toks = _metric_tokens(expr)
+    counters = np.asarray(counters, dtype=np.float64)
+    dur = np.asarray(busy_ns, dtype=np.float64) * 1e-9
+    pos = [0]
+
+    def peek():
+        return toks[pos[0]] if pos[0] < len(toks) else (None, None)
+
+    def take():
+        t = peek()
+        pos[0] += 1
+        return t
+
+    def primary():
+        k, v = take()
+        if k == "num":
+            return np.full(dur.shape, v)
+        if k == "id":
+            if v == "dur_s":
+                return dur.copy()
+            if v not in names:
+                raise MetricError(f"MissingCounter({v})")
+            return counters[list(names).index(v)].copy()
+        if (k, v) == ("op", "("):
+            x = expr_()
+            if take() != ("op", ")"):
+                raise MetricError("ParseError: missing ')'")
+            return x
+        raise MetricError("ParseError")
+
+    def unary():
+        if peek() == ("op", "-"):
+            take()
+            return -unary()
+        return primary()
+
+    def term():
+        x = unary()
+        while peek() in (("op", "*"), ("op", "/")):
+            _, o = take()
+            y = unary()
+            if o == "*":
+                x = x * y
+            else:
+                with np.errstate(divide="ignore", invalid="ignore"):
+                    x = np.where(y == 0.0, np.nan, x / np.where(y == 0.0, 1.0, y))
+        return x
+
+    def expr_():
+        x = term()
+        while peek() in (("op", "+"), ("op", "-")):
+            _, o = take()
+            y = term()
+            x = x + y if o == "+" else x - y
+        return x
+
+    out = expr_()
+    if pos[0] != len(toks):
+        raise MetricError("ParseError: trailing tokens")
+    return out

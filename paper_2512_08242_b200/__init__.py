@@ -100,12 +100,12 @@ _ROW_I64 = ["n_events", "n_compute", "busy", "first_ks", "first_idx", "first_pre
 class chopper_rows(ctypes.Structure):
     _fields_ = [("n", I64), ("stride", I64)] + [(k, P) for k in _ROW_I32] + [(k, P) for k in _ROW_I64] + \
         [("counters", P), ("rates", P), ("wall", P), ("comm_union", P), ("aligned_first", P), ("aligned_last", P),
-         ("step", P)]
+         ("step", P), ("metrics", P)]
 
 
 class chopper_tables(ctypes.Structure):
     _fields_ = [(k, chopper_rows) for k in ("inst", "layer", "phase", "iter", "gpu", "point")] + \
-        [("n_bd", I64), ("bd", P)]
+        [("n_bd", I64), ("n_metrics", I32), ("bd", P)]
 
 
 class chopper_global(ctypes.Structure):
@@ -138,7 +138,7 @@ EXPORTS = ["chopper_scratch_bytes", "chopper_create", "chopper_load_columns", "c
            "chopper_status_sync", "chopper_last_error", "chopper_destroy", "chopper_kernel_launches",
            "chopper_abi_version", "chopper_pass_mismatch", "chopper_pass_conflict", "chopper_counter_present",
            "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time", "chopper_report_cdf",
-           "chopper_cpu_util"]
+           "chopper_cpu_util", "chopper_set_metrics"]
 
 _lib = None
 
@@ -176,6 +176,7 @@ def load_library() -> ctypes.CDLL:
         "chopper_set_timing": (None, [P, I32]),
         "chopper_phase_time": (I32, [P, I32, ctypes.POINTER(ctypes.c_float)]),
         "chopper_report_cdf": (I32, [P, P, I64, ctypes.POINTER(I64)]),
+        "chopper_set_metrics": (I32, [P, I32, P, I32, P, ctypes.POINTER(I32)]),
         "chopper_cpu_util": (I32, [P, ctypes.POINTER(chopper_cpu_samples), P, I32, P, P, I64,
                                    ctypes.POINTER(chopper_cpu_summary)]),
     }
@@ -313,7 +314,7 @@ def dev_to_numpy(ptr: Optional[int], n: int, dtype) -> np.ndarray:
     return t.cpu().numpy().copy()
 
 
-def rows_to_numpy(r: chopper_rows, n_counters: int, n_ratios: int = 0) -> Dict[str, np.ndarray]:
+def rows_to_numpy(r: chopper_rows, n_counters: int, n_ratios: int = 0, n_metrics: int = 0) -> Dict[str, np.ndarray]:
     n = int(r.n)
     out = {}
     for k in _ROW_I32:
@@ -325,6 +326,8 @@ def rows_to_numpy(r: chopper_rows, n_counters: int, n_ratios: int = 0) -> Dict[s
                                 for s in range(n_counters)]) if n_counters else np.zeros((0, n))
     if r.rates and n_ratios:
         out["rates"] = np.stack([dev_to_numpy(r.rates + 8 * q * st, n, np.float64) for q in range(n_ratios)])
+    if r.metrics and n_metrics:
+        out["metrics"] = np.stack([dev_to_numpy(r.metrics + 8 * q * st, n, np.float64) for q in range(n_metrics)])
     for k in ("wall", "comm_union", "aligned_first", "aligned_last"):
         if getattr(r, k):
             out[k] = dev_to_numpy(getattr(r, k), n, np.int64)
@@ -349,6 +352,17 @@ def bd_params(p: dict) -> chopper_bd_params:
                           ratio_scale=keep["rs"].ctypes.data if len(keep["rs"]) else None)
     q._keep = keep
     return q
+
+
+def chopper_set_metrics(ctx, exprs, names) -> None:
+    """Compile the derived-metric registry on the host side of the library; raises
+    ChopperError (MissingCounter / ParseError) naming the failing expression."""
+    lib = load_library()
+    ex = (ctypes.c_char_p * max(len(exprs), 1))(*[e.encode() for e in exprs])
+    nm = (ctypes.c_char_p * max(len(names), 1))(*[n.encode() for n in names])
+    bad = I32(-1)
+    _check(ctx, lib.chopper_set_metrics(ctx, len(exprs), ex, len(names), nm, ctypes.byref(bad)),
+           f"chopper_set_metrics (expression {bad.value})")
 
 
 def chopper_cpu_util(ctx, ts, core, util, topology, c_active=None, c_min=None):

@@ -159,6 +159,7 @@ static void fill_rows(chopper_rows &r, const RowTable &t, bool iter, chopper_ctx
     r.rs_ns = t.f + (int64_t)RF_RS * t.cap;
     r.counters = t.cnt;
     r.rates = t.rates;
+    r.metrics = t.metrics;
     if (iter) {
         r.wall = ctx->iter_wall;
         r.comm_union = ctx->iter_cu;
@@ -219,6 +220,7 @@ chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, c
     fill_rows(out->point, ctx->point, false, ctx);
     out->n_bd = ctx->n_bd;
     out->bd = ctx->d_bd;
+    out->n_metrics = ctx->n_metrics;
     ctx->stage = 5;
     return CHOPPER_OK;
 }
@@ -238,6 +240,12 @@ chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, in
     if (!ctx || !n_rows || cap < 0 || (cap > 0 && !out)) return CHOPPER_E_INVALID_ARG;
     if (ctx->stage != 6) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_report_cdf before chopper_reduce_ranks");
     return ch_report_cdf(ctx, out, cap, n_rows);
+}
+
+chopper_status chopper_set_metrics(chopper_ctx *ctx, int32_t n, const char *const *exprs, int32_t n_names,
+                                   const char *const *names, int32_t *bad_expr) {
+    if (!ctx || n < 0 || n_names < 0 || (n > 0 && !exprs) || (n_names > 0 && !names)) return CHOPPER_E_INVALID_ARG;
+    return ch_compile_metrics(ctx, n, exprs, n_names, names, bad_expr);
 }
 
 chopper_status chopper_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *samples, const int32_t *topology,

@@ -58,6 +58,7 @@ struct RowTable {
             *rank = nullptr;         // decoded identity columns (outputs)
     int64_t *first_ks = nullptr, *first_pred = nullptr;
     double *rates = nullptr;
+    double *metrics = nullptr;       // [n_metrics][cap] derived-metric registry values (points, iterations)
 };
 
 struct PassDesc {          // device copy of one counter pass
@@ -216,6 +217,10 @@ struct chopper_ctx {
     int32_t *d_ratio = nullptr;      // [2][n_ratios]
     double *d_ratio_scale = nullptr;
     int n_ratios = 0;
+    // derived-metric registry (metrics.cu): postfix programs, host copies
+    int n_metrics = 0;
+    std::vector<int32_t> met_ops, met_arg, met_beg;
+    std::vector<double> met_const;
     int32_t *d_has_smp = nullptr;    // [n_lg]
     // phase timing (chopper_set_timing)
     bool timing = false;
@@ -414,6 +419,9 @@ chopper_status ch_tables(chopper_ctx *ctx);
 chopper_status ch_breakdown_local(chopper_ctx *ctx);
 chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
 chopper_status ch_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows);
+chopper_status ch_compile_metrics(chopper_ctx *ctx, int32_t n, const char *const *exprs, int32_t n_names,
+                                  const char *const *names, int32_t *bad_expr);
+chopper_status ch_eval_metrics(chopper_ctx *ctx, RowTable &t);
 chopper_status ch_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *s, const int32_t *topology, int32_t n_logical,
                            int64_t *c_active, double *c_min, int64_t cap, chopper_cpu_summary *out);
 chopper_status ch_nccl_allgather(chopper_ctx *ctx, const void *send, void *recv, size_t bytes_per_rank);

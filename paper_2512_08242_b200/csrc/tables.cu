@@ -1412,6 +1412,9 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
             CH_LAUNCHED(ctx);
         }
     }
+    // derived-metric registry
+    CH_TRY(ch_eval_metrics(ctx, ctx->point));
+    CH_TRY(ch_eval_metrics(ctx, ctx->iter));
     return CHOPPER_OK;
 }
 

@@ -13,7 +13,7 @@ from typing import Dict, Optional
 import numpy as np
 
 from . import (chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
-               chopper_cpu_util, chopper_create, chopper_destroy, chopper_events, chopper_get_report, chopper_global, chopper_report_cdf,
+               chopper_cpu_util, chopper_create, chopper_set_metrics, chopper_destroy, chopper_events, chopper_get_report, chopper_global, chopper_report_cdf,
                chopper_kernel_launches, chopper_load_columns, chopper_overlap, chopper_reduce_ranks,
                chopper_samples, chopper_scratch_bytes, chopper_spans, chopper_status_sync, chopper_tables,
                _check, bd_params, dev_to_numpy, load_library, rows_to_numpy)
@@ -98,6 +98,10 @@ class Pipeline:
         self.scratch = None
         self.d = {}
         self.cpu = None
+
+    def set_metrics(self, exprs, names) -> None:
+        """Derived-metric registry: infix expressions over counter names and dur_s."""
+        chopper_set_metrics(self.ctx, list(exprs), list(names))
 
     def upload_cpu(self, ts, core, util, topology) -> None:
         """Host CPU utilisation samples (sorted by (ts, logical core)) and the logical -> physical topology."""
@@ -221,13 +225,15 @@ class Pipeline:
         tabs = res["tables"]
         for name, attr in (("inst", "inst"), ("layer", "layer"), ("phase", "phase"), ("iter", "iter"), ("gpu", "gpu"),
                            ("point", "point")):
-            r = rows_to_numpy(getattr(tabs, attr), C, n_ratios)
+            r = rows_to_numpy(getattr(tabs, attr), C, n_ratios, int(tabs.n_metrics))
             for k, v in r.items():
                 key = {"n_compute": "n", "step": "step"}.get(k, k)
                 if k == "counters":
                     o[f"{name}.counters"] = v.reshape(-1)
                 elif k == "rates":
                     o[f"{name}.rates"] = v.reshape(-1)
+                elif k == "metrics":
+                    o[f"{name}.metrics"] = v
                 else:
                     o[f"{name}.{key}"] = v
         nbd = int(tabs.n_bd)

@@ -386,3 +386,31 @@ def test_cpu_util_rejects_unsorted():
     import paper_2512_08242_b200 as ch
     with pytest.raises(ch.ChopperError):
         _cpu_both(np.array([2, 1]), np.array([0, 0]), np.array([1.0, 1.0]), np.array([0]))
+
+
+def test_metric_registry_parity():
+    """Derived-metric registry evaluated on the device over point and iteration rows vs the
+    oracle's recursive evaluator on the oracle's rows (row counter sums agree to 1e-9; NaN for zero divisors)."""
+    import paper_2512_08242_b200 as ch
+    b = tracegen.generate(tracegen.config(1))
+    C = b.n_counters
+    names = [f"c{k}" for k in range(C)]
+    exprs = ["c4 / dur_s", "(c1 + c2) * 0.5 - c3 / c0", "c5 / (c6 - c6)", "-c7 * 2 + dur_s", "1e-3 * c0"]
+    p = oracle.default_params(b)
+    ref = oracle.run(b, p, max_iters=8)
+    pipe = ch.Pipeline(b.cfg.n_gpus, len(b.labels), 8, 4096, device=0)
+    pipe.upload(b, C)
+    pipe.set_metrics(exprs, names)
+    res = pipe.run(p, full=False)
+    got = pipe.to_numpy(res, n_ratios=len(p["ratio_num"]))
+    for t in ("point", "iter"):
+        n = len(ref[f"{t}.busy"])
+        cnt = ref[f"{t}.counters"].reshape(C, n)
+        for m, e in enumerate(exprs):
+            want = oracle.metric_eval(e, names, cnt, ref[f"{t}.busy"])
+            np.testing.assert_allclose(got[f"{t}.metrics"][m], want, rtol=1e-9, atol=0, equal_nan=True)
+    with pytest.raises(ch.ChopperError, match="MissingCounter"):
+        pipe.set_metrics(["c0 / nope"], names)
+    with pytest.raises(ch.ChopperError, match="ParseError"):
+        pipe.set_metrics(["c0 / (c1"], names)
+    pipe.close()

@@ -862,3 +862,54 @@ def test_cpu_util_rejects_unsorted_and_out_of_range():
     assert oracle.cpu_util([1, 1], [1, 0], [1, 1], [0, 0])["bad"] == 1
     assert oracle.cpu_util([1], [0], [101.0], [0])["bad"] == 1
     assert oracle.cpu_util([1], [3], [1.0], [0])["bad"] == 1
+
+
+# ---------------------------------------------------------------------------
+# derived-metric registry
+# ---------------------------------------------------------------------------
+def test_metric_spec(golden):
+    g = golden("metrics.json")
+    for k, c in g.items():
+        if k.startswith("_"):
+            continue
+        if "error" in c:
+            with pytest.raises(oracle.MetricError, match=r"MissingCounter\(Z\)"):
+                oracle.metric_eval(c["expr"], c["names"], [[1.0]] * len(c["names"]), [1])
+            continue
+        v = oracle.metric_eval(c["expr"], c["names"], c["counters"], c["busy_ns"])
+        want = np.array([np.nan if x is None else x for x in c["value"]])
+        np.testing.assert_allclose(v, want, rtol=1e-15, equal_nan=True)
+
+
+def _rand_expr(rng, names, depth=0):
+    r = rng.random()
+    if depth > 3 or r < 0.3:
+        c = rng.integers(0, 3)
+        if c == 0:
+            return repr(float(rng.integers(1, 100)) / 8.0)
+        return str(rng.choice(names))
+    if r < 0.4:
+        return "-" + _rand_expr(rng, names, depth + 1)
+    if r < 0.5:
+        return "(" + _rand_expr(rng, names, depth + 1) + ")"
+    op = str(rng.choice(["+", "-", "*", "/"]))
+    return _rand_expr(rng, names, depth + 1) + " " + op + " " + _rand_expr(rng, names, depth + 1)
+
+
+def test_metric_random_vs_python_eval():
+    """1,000 random expressions vs Python's own evaluator of the same infix text (IEEE doubles, the same
+    precedence and left associativity)."""
+    rng = np.random.default_rng(2512)
+    names = ["A", "B", "C_x", "dur_s"]
+    vals = {"A": 3.5, "B": -1.25, "C_x": 1e9, "dur_s": 2e-3}
+    for _ in range(1000):
+        e = _rand_expr(rng, names)
+        got = oracle.metric_eval(e, ["A", "B", "C_x"], [[vals["A"]], [vals["B"]], [vals["C_x"]]], [2e6])[0]
+        try:
+            want = float(eval(e, {"__builtins__": {}}, dict(vals)))
+        except ZeroDivisionError:
+            want = float("nan")
+        if np.isnan(want):
+            assert np.isnan(got), e
+        else:
+            assert got == want or abs(got - want) <= 1e-12 * abs(want), (e, got, want)
