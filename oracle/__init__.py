@@ -307,3 +307,78 @@ def metric_eval(expr: str, names, counters, busy_ns):
     if pos[0] != len(toks):
         raise MetricError("ParseError: trailing tokens")
     return out
+
+
+# ---------------------------------------------------------------------------
+# Chrome-trace ingest (R15): Python's json with
+# exact decimals, plain loops.  Device events: ph X with cat "kernel" or "gpu_*" (pid = gpu, tid = stream,
+# args.correlation); host launches: flow-start events (ph "s", id = correlation, ts = dispatch); spans: ph X
+# with cat "user_annotation" (pid = gpu, args.level, args.label).  Times: decimal microseconds -> integer ns,
+# rounded half to even; end = start + duration, each rounded.  Kinds by the first matching rule
+# (R15).  name_id = order of first appearance of the name among device events.  Output grouped by gpu and
+# dispatch-ordered (stable: file order); kernels without a launch get dispatch = start and are counted.
+# ---------------------------------------------------------------------------
+def _kind_rule(cat: str, name: str) -> int:
+    n = name.lower()
+    if cat == "gpu_memset":
+        return 5          # MEMOP
+    if cat == "gpu_memcpy":
+        return 4          # COPY
+    if cat != "kernel":
+        return 6          # OTHER
+    if "allgather" in n or "all_gather" in n:
+        return 1          # AG
+    if "reducescatter" in n or "reduce_scatter" in n:
+        return 2          # RS
+    if "nccl" in n or "rccl" in n:
+        return 3          # COMM_OTHER
+    if "fsdp_copy" in n:
+        return 4          # COPY (D7: FSDP copy kernels are bubbles)
+    return 0              # COMPUTE
+
+
+def ingest_chrome(data: bytes) -> Dict[str, np.ndarray]:
+    import decimal
+    import json
+    D = decimal.Decimal
+
+    def ns(x) -> int:
+        return int((D(x) * 1000).quantize(D(1), rounding=decimal.ROUND_HALF_EVEN))
+
+    doc = json.loads(data, parse_float=D)
+    evs = doc["traceEvents"]
+    flows = {}
+    dev, spans = [], []
+    for e in evs:
+        ph, cat = e.get("ph"), e.get("cat", "")
+        if ph == "s" and "id" in e:
+            flows.setdefault(int(e["id"]), ns(e["ts"]))
+        elif ph == "X" and cat == "user_annotation":
+            a = e.get("args", {})
+            s = ns(e["ts"])
+            spans.append((int(e["pid"]), int(a["level"]), s, s + ns(e["dur"]), int(a["label"])))
+        elif ph == "X" and (cat == "kernel" or cat.startswith("gpu_")):
+            s = ns(e["ts"])
+            corr = e.get("args", {}).get("correlation")
+            dev.append((int(e["pid"]), int(e["tid"]), _kind_rule(cat, e["name"]), s, s + ns(e["dur"]), e["name"],
+                        None if corr is None else int(corr)))
+    names = {}
+    for d in dev:
+        names.setdefault(d[5], len(names))
+    missing = 0
+    rows = []
+    for q, d in enumerate(dev):
+        g, st, k, s, t, nm, c = d
+        if c is not None and c in flows:
+            tl = flows[c]
+        else:
+            tl = s
+            missing += 1
+        rows.append((g, tl, q, s, t, (g << 24) | (st << 8) | k, names[nm]))
+    rows.sort(key=lambda r: (r[0], r[1], r[2]))
+    a = np.array([(r[1], r[3], r[4], r[5], r[6]) for r in rows], dtype=np.int64).reshape(-1, 5)
+    sp = np.array(spans, dtype=np.int64).reshape(-1, 5)
+    return {"t_l": a[:, 0], "t_ks": a[:, 1], "t_ke": a[:, 2], "meta": a[:, 3].astype(np.uint32),
+            "name_id": a[:, 4].astype(np.int32), "span_gl": ((sp[:, 0] << 8) | sp[:, 1]).astype(np.uint32),
+            "span_start": sp[:, 2], "span_end": sp[:, 3], "span_label": sp[:, 4].astype(np.int32),
+            "n_missing": missing, "names": list(names)}

@@ -913,3 +913,41 @@ def test_metric_random_vs_python_eval():
             assert np.isnan(got), e
         else:
             assert got == want or abs(got - want) <= 1e-12 * abs(want), (e, got, want)
+
+
+# ---------------------------------------------------------------------------
+# Chrome-trace ingest
+# ---------------------------------------------------------------------------
+def test_chrome_ingest_spec(golden):
+    g = golden("chrome.json")
+    for k, c in g.items():
+        if k.startswith("_"):
+            continue
+        r = oracle.ingest_chrome(c["json"].encode())
+        assert r["n_missing"] == c["n_missing"], k
+        for f in ("t_l", "t_ks", "t_ke", "name_id", "span_gl", "span_start", "span_end", "span_label"):
+            if f in c:
+                np.testing.assert_array_equal(r[f], c[f], err_msg=f"{k}.{f}")
+        if "kind" in c:
+            np.testing.assert_array_equal(r["meta"] & 0xFF, c["kind"], err_msg=k)
+        if "stream" in c:
+            np.testing.assert_array_equal((r["meta"] >> 8) & 0xFFFF, c["stream"], err_msg=k)
+        if "gpu" in c:
+            np.testing.assert_array_equal(r["meta"] >> 24, c["gpu"], err_msg=k)
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_chrome_roundtrip(cid):
+    """bundle -> Chrome trace -> ingest gives the bundle's columns back (name ids up to the first-appearance
+    relabelling, spans as a multiset): the generator writes exact ns and sub-ns digits that round back."""
+    b = tracegen.generate(tracegen.config(cid))
+    r = oracle.ingest_chrome(tracegen.to_chrome(b, seed=cid))
+    for f in ("t_l", "t_ks", "t_ke", "meta"):
+        np.testing.assert_array_equal(r[f], getattr(b, f))
+    m = {}
+    assert all(m.setdefault(int(x), int(y)) == int(y) for x, y in zip(r["name_id"], b.name_id))
+    assert len(set(m.values())) == len(m)
+    key = lambda gl, s, e, lab: sorted(zip(gl.tolist(), s.tolist(), e.tolist(), lab.tolist()))
+    assert key(r["span_gl"], r["span_start"], r["span_end"], r["span_label"]) == \
+        key(b.span_gl, b.span_start, b.span_end, b.span_label)
+    assert r["n_missing"] == 0

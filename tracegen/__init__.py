@@ -535,3 +535,55 @@ def cpu_samples(seed: int, t_start: int, t_end: int, period_ns: int = 100_000_00
     util[:, workers + n_physical] = np.where(sib, rng.integers(n_ts * len(workers), 5, 31).reshape(n_ts, len(workers)),
                                              0)
     return ts, core, util.reshape(-1), topology
+
+
+# ---------------------------------------------------------------------------
+# Chrome-trace export of a bundle (input of the device ingest)
+# ---------------------------------------------------------------------------
+_CHROME_KIND = {COMPUTE: ("kernel", "k{}"), AG: ("kernel", "ncclDevKernel_AllGather_k{}"),
+                RS: ("kernel", "ncclDevKernel_ReduceScatter_k{}"), COMM_OTHER: ("kernel", "ncclDevKernel_AllReduce_k{}"),
+                COPY: ("kernel", "fsdp_copy_k{}"), MEMOP: ("gpu_memset", "Memset_k{}"), OTHER: ("gpu_user", "other_k{}")}
+
+
+def _us(ns: int, extra: str = "") -> str:
+    """integer ns as a decimal microsecond string with exactly three fractional digits (+ optional digits)"""
+    s = "-" if ns < 0 else ""
+    a = abs(int(ns))
+    return f"{s}{a // 1000}.{a % 1000:03d}{extra}"
+
+
+def to_chrome(b: "Bundle", seed: int = 1) -> bytes:
+    """The bundle's kernels (X events, cat / name by kind, pid = gpu, tid = stream, args.correlation), their
+    host launches as flow-start events (ph 's', id = correlation, ts = dispatch) and the spans as
+    user_annotation X events (args.level, args.label), flows and spans interleaved at random between the
+    kernels (kernels keep the bundle order).  Some timestamps carry extra sub-ns digits that round back to the
+    same ns (half-to-even never changes them).  Formatting only: none of the method's arithmetic."""
+    rng = Rng(seed ^ 0xC4120E)
+    n = b.n_events
+    kind = (b.meta & 0xFF).astype(np.int64)
+    gpu = (b.meta >> 24).astype(np.int64)
+    stream = ((b.meta >> 8) & 0xFFFF).astype(np.int64)
+    extra = rng.integers(n, 0, 4)
+    out = []
+    for i in range(n):
+        cat, nm = _CHROME_KIND[int(kind[i])]
+        ex = ["", "0", "4", "49"][int(extra[i])]
+        out.append((0, i, '{"ph": "X", "cat": "%s", "name": "%s", "pid": %d, "tid": %d, "ts": %s, "dur": %s, '
+                    '"args": {"correlation": %d, "device": %d, "stream": %d}}'
+                    % (cat, nm.format(int(b.name_id[i])), gpu[i], stream[i], _us(int(b.t_ks[i]), ex),
+                       _us(int(b.t_ke[i] - b.t_ks[i])), i + 1, gpu[i], stream[i])))
+    pos_f = rng.uniform(n)
+    for i in range(n):
+        out.append((1, i + pos_f[i], '{"ph": "s", "id": %d, "pid": %d, "tid": 1, "ts": %s, "cat": "ac2g", '
+                    '"name": "ac2g"}' % (i + 1, 1000 + gpu[i], _us(int(b.t_l[i])))))
+    S = len(b.span_start)
+    pos_s = rng.uniform(S) * n
+    for j in range(S):
+        g, lv = int(b.span_gl[j] >> 8), int(b.span_gl[j] & 0xFF)
+        out.append((1, pos_s[j], '{"ph": "X", "cat": "user_annotation", "name": "span\\"%d\\"", "pid": %d, '
+                    '"tid": "annotations", "ts": %s, "dur": %s, "args": {"level": %d, "label": %d}}'
+                    % (int(b.span_label[j]), g, _us(int(b.span_start[j])),
+                       _us(int(b.span_end[j] - b.span_start[j])), lv, int(b.span_label[j]))))
+    out.sort(key=lambda x: (x[1], x[0]))
+    return ('{"schemaVersion": 1, "traceEvents": [\n' + ",\n".join(x[2] for x in out) +
+            '\n], "displayTimeUnit": "ms"}\n').encode()
