@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define CHOPPER_ABI_VERSION 6
+#define CHOPPER_ABI_VERSION 7
 
 typedef struct chopper_ctx chopper_ctx;
 typedef int32_t chopper_status;
@@ -251,6 +251,40 @@ chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
  * duration, overlap ratio, empirical CDF (k + 1) / n.  out: host buffer of cap rows (may be NULL when cap is
  * 0); *n_rows = number of rows (the first min(cap, *n_rows) are written).  Synchronizes the ctx stream. */
 chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows);
+
+/* Chrome-trace ingest on the device (R15): the
+ * step before chopper_load_columns.  json: DEVICE bytes of a Chrome-trace document ({"traceEvents": [...]});
+ * device events = ph "X" with cat "kernel" or "gpu_*" (pid = gpu 0..255, tid = stream, args.correlation),
+ * host launches = flow-start events (ph "s", id = correlation, ts = dispatch), spans = ph "X" with cat
+ * "user_annotation" (pid = gpu, args.level 0..3, args.label); other events are ignored.  Times: decimal
+ * microseconds -> integer ns rounded half to even; end = start + duration.  Kinds by the first matching
+ * rule: cat gpu_memset -> MEMOP, gpu_memcpy -> COPY, other gpu_* -> OTHER; for cat kernel the lower-cased name
+ * containing allgather / all_gather -> AG, reducescatter / reduce_scatter -> RS, nccl / rccl -> COMM_OTHER,
+ * fsdp_copy -> COPY (D7), else COMPUTE.  name_id = order of first appearance of the (decoded) name among the
+ * device events.  A kernel whose correlation has no launch gets dispatch = start (counted in n_missing).
+ * Outputs (DEVICE, caller capacity ev_cap / span_cap): the chopper_events columns grouped by gpu and
+ * dispatch-ordered (ties: file order), spans in file order.  scratch: caller device buffer of
+ * chopper_ingest_scratch_bytes(n_bytes) (the ctx arena is not used; sized for event objects of >= 16 bytes,
+ * a denser document returns CHOPPER_E_RANGE).  Errors: unbalanced JSON, no traceEvents
+ * array or a malformed event object -> CHOPPER_E_VALIDATION (report.bad_offset = the object's byte offset);
+ * output capacity or time range -> CHOPPER_E_RANGE.  Synchronizes the ctx stream. */
+typedef struct {
+    int64_t *t_l, *t_ks, *t_ke;
+    uint32_t *meta;
+    int32_t *name_id;
+    int64_t ev_cap;
+    uint32_t *span_gl;
+    int64_t *span_start, *span_end;
+    int32_t *span_label;
+    int64_t span_cap;
+} chopper_ingest_out;
+typedef struct {
+    int64_t n_objects, n_kernels, n_flows, n_spans, n_missing, n_names;
+    int64_t bad_offset;            /* -1, or the byte offset of the first malformed event object */
+} chopper_ingest_report;
+size_t chopper_ingest_scratch_bytes(int64_t n_bytes);
+chopper_status chopper_ingest_chrome(chopper_ctx *ctx, const char *json, int64_t n_bytes, void *scratch,
+                                     size_t scratch_bytes, const chopper_ingest_out *out, chopper_ingest_report *rep);
 
 /* Derived-metric registry ("calculating bandwidth from
  * transferred bytes and kernel duration"; R14).  exprs: n infix expressions (host strings) over

@@ -122,6 +122,16 @@ class chopper_report(ctypes.Structure):
                 ("non_laminar_lists", I32)]
 
 
+class chopper_ingest_out(ctypes.Structure):
+    _fields_ = [("t_l", P), ("t_ks", P), ("t_ke", P), ("meta", P), ("name_id", P), ("ev_cap", I64), ("span_gl", P),
+                ("span_start", P), ("span_end", P), ("span_label", P), ("span_cap", I64)]
+
+
+class chopper_ingest_report(ctypes.Structure):
+    _fields_ = [("n_objects", I64), ("n_kernels", I64), ("n_flows", I64), ("n_spans", I64), ("n_missing", I64),
+                ("n_names", I64), ("bad_offset", I64)]
+
+
 class chopper_cpu_samples(ctypes.Structure):
     _fields_ = [("n", I64), ("ts_ns", P), ("logical_core", P), ("util_pct", P)]
 
@@ -138,7 +148,7 @@ EXPORTS = ["chopper_scratch_bytes", "chopper_create", "chopper_load_columns", "c
            "chopper_status_sync", "chopper_last_error", "chopper_destroy", "chopper_kernel_launches",
            "chopper_abi_version", "chopper_pass_mismatch", "chopper_pass_conflict", "chopper_counter_present",
            "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time", "chopper_report_cdf",
-           "chopper_cpu_util", "chopper_set_metrics"]
+           "chopper_cpu_util", "chopper_set_metrics", "chopper_ingest_scratch_bytes", "chopper_ingest_chrome"]
 
 _lib = None
 
@@ -177,6 +187,9 @@ def load_library() -> ctypes.CDLL:
         "chopper_phase_time": (I32, [P, I32, ctypes.POINTER(ctypes.c_float)]),
         "chopper_report_cdf": (I32, [P, P, I64, ctypes.POINTER(I64)]),
         "chopper_set_metrics": (I32, [P, I32, P, I32, P, ctypes.POINTER(I32)]),
+        "chopper_ingest_scratch_bytes": (ctypes.c_size_t, [I64]),
+        "chopper_ingest_chrome": (I32, [P, P, I64, P, ctypes.c_size_t, ctypes.POINTER(chopper_ingest_out),
+                                        ctypes.POINTER(chopper_ingest_report)]),
         "chopper_cpu_util": (I32, [P, ctypes.POINTER(chopper_cpu_samples), P, I32, P, P, I64,
                                    ctypes.POINTER(chopper_cpu_summary)]),
     }
@@ -352,6 +365,36 @@ def bd_params(p: dict) -> chopper_bd_params:
                           ratio_scale=keep["rs"].ctypes.data if len(keep["rs"]) else None)
     q._keep = keep
     return q
+
+
+def chopper_ingest_chrome(ctx, json_dev, ev_cap: int, span_cap: int, device=0):
+    """Chrome-trace JSON (a uint8 CUDA tensor) -> event and span columns (CUDA tensors, trimmed) + report dict."""
+    import torch
+    lib = load_library()
+    dev = json_dev.device
+    n = int(json_dev.numel())
+    scratch = torch.empty(int(lib.chopper_ingest_scratch_bytes(n)), dtype=torch.uint8, device=dev)
+    cols = {"t_l": torch.empty(max(ev_cap, 1), dtype=torch.int64, device=dev),
+            "t_ks": torch.empty(max(ev_cap, 1), dtype=torch.int64, device=dev),
+            "t_ke": torch.empty(max(ev_cap, 1), dtype=torch.int64, device=dev),
+            "meta": torch.empty(max(ev_cap, 1), dtype=torch.int32, device=dev),
+            "name_id": torch.empty(max(ev_cap, 1), dtype=torch.int32, device=dev),
+            "span_gl": torch.empty(max(span_cap, 1), dtype=torch.int32, device=dev),
+            "span_start": torch.empty(max(span_cap, 1), dtype=torch.int64, device=dev),
+            "span_end": torch.empty(max(span_cap, 1), dtype=torch.int64, device=dev),
+            "span_label": torch.empty(max(span_cap, 1), dtype=torch.int32, device=dev)}
+    o = chopper_ingest_out(*(_ptr(cols[k]) for k in ("t_l", "t_ks", "t_ke", "meta", "name_id")), ev_cap,
+                           *(_ptr(cols[k]) for k in ("span_gl", "span_start", "span_end", "span_label")), span_cap)
+    rep = chopper_ingest_report()
+    _check(ctx, lib.chopper_ingest_chrome(ctx, _ptr(json_dev), n, _ptr(scratch), scratch.numel(), ctypes.byref(o),
+                                          ctypes.byref(rep)), "chopper_ingest_chrome")
+    r = {k: getattr(rep, k) for k, _ in chopper_ingest_report._fields_}
+    nk, ns = int(rep.n_kernels), int(rep.n_spans)
+    for k in ("t_l", "t_ks", "t_ke", "meta", "name_id"):
+        cols[k] = cols[k][:nk]
+    for k in ("span_gl", "span_start", "span_end", "span_label"):
+        cols[k] = cols[k][:ns]
+    return cols, r
 
 
 def chopper_set_metrics(ctx, exprs, names) -> None:

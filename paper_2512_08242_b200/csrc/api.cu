@@ -242,6 +242,17 @@ chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, in
     return ch_report_cdf(ctx, out, cap, n_rows);
 }
 
+size_t chopper_ingest_scratch_bytes(int64_t n_bytes) { return n_bytes < 0 ? 0 : ch_ingest_scratch_bytes(n_bytes); }
+
+chopper_status chopper_ingest_chrome(chopper_ctx *ctx, const char *json, int64_t n_bytes, void *scratch,
+                                     size_t scratch_bytes, const chopper_ingest_out *out, chopper_ingest_report *rep) {
+    if (!ctx || n_bytes < 0 || (n_bytes > 0 && !json) || !scratch || !out || !rep || out->ev_cap < 0 ||
+        out->span_cap < 0 || (out->ev_cap > 0 && (!out->t_l || !out->t_ks || !out->t_ke || !out->meta || !out->name_id)) ||
+        (out->span_cap > 0 && (!out->span_gl || !out->span_start || !out->span_end || !out->span_label)))
+        return CHOPPER_E_INVALID_ARG;
+    return ch_ingest_chrome(ctx, json, n_bytes, scratch, scratch_bytes, out, rep);
+}
+
 chopper_status chopper_set_metrics(chopper_ctx *ctx, int32_t n, const char *const *exprs, int32_t n_names,
                                    const char *const *names, int32_t *bad_expr) {
     if (!ctx || n < 0 || n_names < 0 || (n > 0 && !exprs) || (n_names > 0 && !names)) return CHOPPER_E_INVALID_ARG;

@@ -392,6 +392,7 @@ __device__ __forceinline__ int64_t block_excl_sum(int64_t v, int64_t *total, int
 // cross-file host entry points
 // ---------------------------------------------------------------------------
 // prims.cu
+// exclusive scan of NON-NEGATIVE int64 values (< 2^62: the single-pass tile states keep two flag bits on top)
 chopper_status ch_scan_excl_i64(chopper_ctx *ctx, const int64_t *in, int64_t *out, int64_t n, int64_t *total_dev);
 chopper_status ch_seg_scan_i64(chopper_ctx *ctx, const int64_t *in, const uint8_t *head, int64_t *out, int64_t n,
                                int op /*0 sum excl, 1 max incl, 2 sum incl*/);
@@ -419,6 +420,9 @@ chopper_status ch_tables(chopper_ctx *ctx);
 chopper_status ch_breakdown_local(chopper_ctx *ctx);
 chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
 chopper_status ch_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows);
+size_t ch_ingest_scratch_bytes(int64_t n_bytes);
+chopper_status ch_ingest_chrome(chopper_ctx *ctx, const char *js, int64_t L, void *scratch, size_t scratch_bytes,
+                                const chopper_ingest_out *out, chopper_ingest_report *rep);
 chopper_status ch_compile_metrics(chopper_ctx *ctx, int32_t n, const char *const *exprs, int32_t n_names,
                                   const char *const *names, int32_t *bad_expr);
 chopper_status ch_eval_metrics(chopper_ctx *ctx, RowTable &t);

@@ -32,7 +32,7 @@ def test_exports_every_declared_symbol(lib):
 
 def test_abi_version_and_scratch(lib):
     import paper_2512_08242_b200 as ch
-    assert lib.chopper_abi_version() == 6
+    assert lib.chopper_abi_version() == 7
     cfg = ch.chopper_config(n_traced_gpus=8, n_labels=42, max_iters=256, max_coll_per_class=20000)
     small = ch.chopper_scratch_bytes(cfg, 1000, 100, 0, 0)
     big = ch.chopper_scratch_bytes(cfg, 20_000_000, 2_000_000, 1_000_000, 8)

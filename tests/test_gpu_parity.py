@@ -414,3 +414,58 @@ def test_metric_registry_parity():
     with pytest.raises(ch.ChopperError, match="ParseError"):
         pipe.set_metrics(["c0 / (c1"], names)
     pipe.close()
+
+
+def _ingest_gpu(data: bytes):
+    import torch
+    import paper_2512_08242_b200 as ch
+    b = TinyTrace().ev(0, 0, 10, 20).span(0, 0, 0, 100).bundle()
+    pipe = ch.Pipeline(1, 4, 4, 16, device=0)
+    pipe.upload(b, 0)
+    js = torch.frombuffer(bytearray(data), dtype=torch.uint8).to("cuda:0")
+    n = max(data.count(b'"ph"'), 1)
+    cols, rep = ch.chopper_ingest_chrome(pipe.ctx, js, n, n)
+    out = {k: v.cpu().numpy() for k, v in cols.items()}
+    out["meta"] = out["meta"].view(np.uint32)
+    out["span_gl"] = out["span_gl"].view(np.uint32)
+    pipe.close()
+    return out, rep
+
+
+def test_chrome_ingest_golden():
+    """device Chrome-trace ingest vs the oracle's on SPEC.md:104-106's examples, half-to-even rounding,
+    escapes and nested / ignored events"""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "chrome.json")))
+    for k, c in g.items():
+        if k.startswith("_"):
+            continue
+        ref = oracle.ingest_chrome(c["json"].encode())
+        got, rep = _ingest_gpu(c["json"].encode())
+        assert rep["n_missing"] == ref["n_missing"], k
+        for f in ("t_l", "t_ks", "t_ke", "meta", "name_id", "span_gl", "span_start", "span_end", "span_label"):
+            np.testing.assert_array_equal(got[f], ref[f], err_msg=f"{k}.{f}")
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+def test_chrome_ingest_generated(cid):
+    """bundle -> Chrome trace (shuffled flows and spans, sub-ns digits) -> device ingest == oracle ingest,
+    element by element (and == the bundle's columns)"""
+    b = tracegen.generate(tracegen.config(cid))
+    data = tracegen.to_chrome(b, seed=cid)
+    ref = oracle.ingest_chrome(data)
+    got, rep = _ingest_gpu(data)
+    assert rep["n_missing"] == ref["n_missing"] == 0
+    assert rep["n_names"] == len(ref["names"])
+    for f in ("t_l", "t_ks", "t_ke", "meta", "name_id", "span_gl", "span_start", "span_end", "span_label"):
+        np.testing.assert_array_equal(got[f], ref[f], err_msg=f)
+    np.testing.assert_array_equal(got["t_l"], b.t_l)
+
+
+def test_chrome_ingest_malformed():
+    import paper_2512_08242_b200 as ch
+    with pytest.raises(ch.ChopperError):
+        _ingest_gpu(b'{"traceEvents": [{"ph": "X", "cat": "kernel", "name": "k", "pid": 0, "tid": 0, "ts": 1, "dur": }]}')
+    with pytest.raises(ch.ChopperError):
+        _ingest_gpu(b'{"events": []}')
