@@ -1204,7 +1204,29 @@ __device__ __forceinline__ int64_t win_t(const WinR &w, int64_t j) {
 // slow path: last entry <= t over [gb, ge) in global memory, starting from the cursor when it is behind t
 __device__ __noinline__ longlong2 seek_global(const int64_t *G, const int64_t *T, int64_t lo, int n, int64_t gb,
                                               int64_t ge, int64_t j, int64_t t) {
-    const int64_t l = (j >= gb && j < ge && __ldg(G + j) <= t) ? j : gb;
+    int64_t l = gb;
+    if (j >= gb && j < ge && __ldg(G + j) <= t) {
+        // forward walk first (queries mostly increase; consecutive entries share L1 lines), then bisect
+        for (int s = 0; s < 16; s++) {
+            if (j + 1 >= ge || __ldg(G + j + 1) > t) {
+                const int64_t b = j + 1 >= ge ? INT64_MAX
+                                              : ((uint64_t)(j + 1 - lo) < (uint64_t)n ? T[j + 1 - lo] : __ldg(G + j + 1));
+                return make_longlong2(j, b);
+            }
+            j++;
+        }
+        // gallop: G[j] <= t; double the step until an entry past t (or the end) bounds the search
+        int64_t step = 32, hi = ge;
+        while (j + step < ge) {
+            if (__ldg(G + j + step) > t) { hi = j + step; break; }
+            j += step;
+            step <<= 1;
+        }
+        const int64_t r0 = last_le(G, j, hi, t);
+        const int64_t b0 = r0 + 1 >= ge ? INT64_MAX
+                                        : ((uint64_t)(r0 + 1 - lo) < (uint64_t)n ? T[r0 + 1 - lo] : __ldg(G + r0 + 1));
+        return make_longlong2(r0, b0);
+    }
     const int64_t r = last_le(G, l, ge, t);
     const int64_t b = r + 1 >= ge ? INT64_MAX : ((uint64_t)(r + 1 - lo) < (uint64_t)n ? T[r + 1 - lo] : __ldg(G + r + 1));
     return make_longlong2(r, b);
