@@ -50,6 +50,17 @@ chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int 
         delete c;
         return CHOPPER_E_CUDA;
     }
+    for (int q = 0; q < 3; q++) {
+        if (cudaStreamCreateWithFlags(&c->side[q], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->join_ev[q], cudaEventDisableTiming) != cudaSuccess) {
+            delete c;
+            return CHOPPER_E_CUDA;
+        }
+    }
+    if (cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) != cudaSuccess) {
+        delete c;
+        return CHOPPER_E_CUDA;
+    }
     *out = c;
     return CHOPPER_OK;
 }
@@ -299,6 +310,11 @@ void chopper_destroy(chopper_ctx *ctx) {
     for (auto &p : ctx->tev)
         for (auto &e : p)
             if (e) cudaEventDestroy(e);
+    for (int q = 0; q < 3; q++) {
+        if (ctx->side[q]) cudaStreamDestroy(ctx->side[q]);
+        if (ctx->join_ev[q]) cudaEventDestroy(ctx->join_ev[q]);
+    }
+    if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
     delete ctx;
 }
 

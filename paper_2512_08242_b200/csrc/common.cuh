@@ -76,6 +76,8 @@ struct chopper_ctx {
     chopper_config cfg{};
     int device = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t side[3] = {nullptr, nullptr, nullptr};   // fork / join of independent small kernels
+    cudaEvent_t fork_ev = nullptr, join_ev[3] = {nullptr, nullptr, nullptr};
     void *nccl = nullptr;
     int rank = 0, nranks = 1;
     char *scratch = nullptr;

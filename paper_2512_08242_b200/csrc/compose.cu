@@ -999,7 +999,11 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     G.warmup = ctx->bd.warmup;
     G.step = step; G.complete = comp; G.sampled = samp; G.T = T; G.af = af; G.al = al; G.tp = tp;
     G.n_out = nref; G.med = med; G.work = work;
-    k_global<<<1, 256, 0, ctx->st>>>(G);
+    // the global rows, the report statistics and the end-to-end medians are independent small kernels: they
+    // run on side streams, concurrently with the breakdown on the ctx stream (joined before the copies)
+    CH_CUDA(ctx, cudaEventRecord(ctx->fork_ev, ctx->st));
+    for (int q = 0; q < 3; q++) CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[q], ctx->fork_ev, 0));
+    k_global<<<1, 256, 0, ctx->side[0]>>>(G);
     CH_LAUNCHED(ctx);
     double *bd;
     int64_t nbd;
@@ -1022,7 +1026,7 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
             rattr = true;
         }
         RepArgs RA{all, nslots, Ly, ord, ctx->bd.warmup, maxp2, wk, rep, use_smem ? 1 : 0};
-        k_report<<<nL, 512, use_smem ? shb : 0, ctx->st>>>(RA);
+        k_report<<<nL, 512, use_smem ? shb : 0, ctx->side[1]>>>(RA);
         CH_LAUNCHED(ctx);
     }
     // end-to-end phase x op-type medians (O16)
@@ -1035,8 +1039,12 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
         e2e = CH_ALLOC(ctx, double, 1 + E2E_W);
         int64_t *wk = sm_ok ? nullptr : CH_ALLOC(ctx, int64_t, (int64_t)E2E_W * maxp2);
         CH_ALLOC_END(ctx);
-        k_e2e<<<E2E_W, 512, sm_ok ? 8 * maxp2 : 0, ctx->st>>>(all, Ly, ord, nslots, ctx->bd.warmup, maxp2, wk, e2e);
+        k_e2e<<<E2E_W, 512, sm_ok ? 8 * maxp2 : 0, ctx->side[2]>>>(all, Ly, ord, nslots, ctx->bd.warmup, maxp2, wk, e2e);
         CH_LAUNCHED(ctx);
+    }
+    for (int q = 0; q < 3; q++) {
+        CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[q], ctx->side[q]));
+        CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->join_ev[q], 0));
     }
     // host copies
     int64_t n = 0;
