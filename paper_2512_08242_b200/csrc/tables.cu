@@ -1256,6 +1256,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         CH_CUDA(ctx, cudaMemcpyAsync(lg_gpu_d, ctx->h_lg_gpu.data(), 4 * ctx->n_lg, cudaMemcpyHostToDevice, ctx->st));
     ctx->sub.cap = std::max<int64_t>(R, 1);
     TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, 1, 1, 16, std::max(C, 1)};   // AoS sub-run rows and counters
+    bool counters_forked = false;
     if (C > 0 && R > 0) {
         const int n_lg = ctx->n_lg;
         ctx->d_colbad = CH_ALLOC(ctx, unsigned int, (int64_t)n_lg * C);
@@ -1264,10 +1265,16 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         const int vec_ok = (((uintptr_t)ctx->ev.meta | (uintptr_t)ctx->d_run_id | (uintptr_t)ctx->d_nm_rank) & 15u) == 0;
         CH_CUDA(ctx, cudaFuncSetAttribute(k_counters_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)sizeof(CtSmem)));
-        k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->st>>>(
+        // the counter pass runs on a side stream, concurrently with the instance ordering below (which never
+        // touches the counter sums); it is joined before the sub-run -> instance sum
+        CH_CUDA(ctx, cudaEventRecord(ctx->fork_ev, ctx->st));
+        CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[0], ctx->fork_ev, 0));
+        k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->side[0]>>>(
             ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, ctx->N, subv.cnt, subv.ccap,
             ctx->d_colbad, vec_ok);
         CH_LAUNCHED(ctx);
+        CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[0], ctx->side[0]));
+        counters_forked = true;
     }
     // instances: sort of sub-runs by key, then groups of equal keys
     unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, R + 1), *k2 = CH_ALLOC(ctx, unsigned long long, R + 1);
@@ -1327,6 +1334,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         int64_t *starts, *ng_dev;
         CH_TRY(group(ctx, ks, R, nullptr, 0, &starts, &ng_dev));
         CH_TRY(alloc_table(ctx, ctx->inst, std::max<int64_t>(R, 1), C, true));
+        if (counters_forked) CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->join_ev[0], 0));
         ctx->inst.n_dev = ng_dev;
         if (R > 0) {
             CH_TRY(sum_rows(ctx, subv, so, starts, ng_dev, R, 0, 0, C, view(ctx->inst)));
