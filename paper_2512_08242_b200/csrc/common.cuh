@@ -82,6 +82,7 @@ struct chopper_ctx {
     int rank = 0, nranks = 1;
     char *scratch = nullptr;
     size_t scratch_bytes = 0, used = 0;
+    bool hold_scratch = false;       // inside a side-stream branch: temporaries are not released (see tables.cu)
     int64_t launches = 0;
     std::string err;
     int stage = 0;                 // 1 loaded, 2 aligned, 3 attributed, 4 overlapped, 5 breakdown

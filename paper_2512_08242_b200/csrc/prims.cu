@@ -339,7 +339,7 @@ chopper_status ch_scan_excl_i64(chopper_ctx *ctx, const int64_t *in, int64_t *ou
         k_scan_1pass<<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, n, out, total_dev, state,
                                                              reinterpret_cast<unsigned int *>(state + ntile));
         CH_LAUNCHED(ctx);
-        ctx->used = mark;
+        if (!ctx->hold_scratch) ctx->used = mark;
         return CHOPPER_OK;
     }
     size_t mark = ctx->used;
@@ -355,7 +355,7 @@ chopper_status ch_scan_excl_i64(chopper_ctx *ctx, const int64_t *in, int64_t *ou
     }
     k_tile_apply<<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, n, offs, out, total_dev);
     CH_LAUNCHED(ctx);
-    ctx->used = mark;
+    if (!ctx->hold_scratch) ctx->used = mark;
     return CHOPPER_OK;
 }
 

@@ -1179,7 +1179,7 @@ static chopper_status group(chopper_ctx *ctx, const unsigned long long *keys_sor
     k_group_1pass<<<(unsigned)ntile, GP_NT, 0, ctx->st>>>(keys_sorted, n, n_dev, shift, all, starts, tot, state,
                                                          reinterpret_cast<unsigned int *>(state + ntile));
     CH_LAUNCHED(ctx);
-    ctx->used = mark;
+    if (!ctx->hold_scratch) ctx->used = mark;
     *starts_out = starts;
     *ng_out = tot;
     return CHOPPER_OK;
@@ -1345,6 +1345,61 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
             CH_LAUNCHED(ctx);
         }
     }
+    // points (label, gpu, iteration): per-iteration label folds into a dense grid, then compaction.  Issued
+    // first, on a side stream (it only reads the instance table), so that it runs concurrently with the
+    // roll-ups below; scratch is not released inside the branch (the roll-ups allocate after it)
+    CH_CUDA(ctx, cudaEventRecord(ctx->fork_ev, ctx->st));
+    CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[1], ctx->fork_ev, 0));
+    cudaStream_t main_st = ctx->st;
+    ctx->st = ctx->side[1];
+    ctx->hold_scratch = true;
+    chopper_status pst = [&]() -> chopper_status {
+        {
+            const int64_t n = ctx->inst.cap;
+            const int nL = std::max(ctx->cfg.n_labels, 1), n_lg = std::max(ctx->n_lg, 1);
+            const int R0 = (int)std::max<int64_t>(ctx->max_it_list, 1);
+            const int64_t cells = (int64_t)nL * n_lg * R0;
+            int lbits = bits_for((uint64_t)std::max(ctx->cfg.n_labels, 1));
+            int pbits = lbits + ctx->kg + L.kb[0];
+            if (pbits > 63) return ch_fail(ctx, CHOPPER_E_RANGE, "point key exceeds 63 bits");
+            if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels");
+            int64_t *its = nullptr, *n_it = nullptr;
+            CH_TRY(group(ctx, ctx->inst.key, n, ctx->inst.n_dev, L.sh_it, &its, &n_it));
+            int64_t *df = CH_ALLOC(ctx, int64_t, (int64_t)RF_NFIELDS * cells);
+            double *dc = CH_ALLOC(ctx, double, (int64_t)std::max(C, 1) * cells);
+            int64_t *dvalid = CH_ALLOC(ctx, int64_t, cells), *dex = CH_ALLOC(ctx, int64_t, cells), *np_d = CH_ALLOC(ctx, int64_t, 1);
+            unsigned int *ovf = CH_ALLOC(ctx, unsigned int, 1);
+            CH_ALLOC_END(ctx);
+            *ovf_out = ovf;
+            CH_CUDA(ctx, cudaMemsetAsync(dvalid, 0, 8 * (size_t)cells, ctx->st));
+            CH_CUDA(ctx, cudaMemsetAsync(ovf, 0, 4, ctx->st));
+            size_t shb = (size_t)(RF_NFIELDS + C) * PT_CH * 8 + (size_t)nL * C * 8 + 4 * (2 * PT_CH + 9 * (size_t)nL);
+            static size_t attr_shb = 0;
+            if (shb > 48 * 1024 && shb > attr_shb) {
+                CH_CUDA(ctx, cudaFuncSetAttribute(k_points_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
+                attr_shb = shb;
+            }
+            k_points_iter<<<grid_for(std::min<int64_t>(n, (int64_t)n_lg * R0), 1), 256, shb, ctx->st>>>(
+                view(ctx->inst), its, n_it, L, ctx->d_list_beg, ctx->P_label, nL, n_lg, R0, C, df, dc, dvalid, ovf);
+            CH_LAUNCHED(ctx);
+            CH_TRY(ch_scan_excl_i64(ctx, dvalid, dex, cells, np_d));
+            CH_TRY(alloc_table(ctx, ctx->point, std::max<int64_t>(cells, 1), C, true));
+            ctx->point.n_dev = np_d;
+            k_points_compact<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(dvalid, dex, cells, df, dc, C, n_lg, R0,
+                                                                              ctx->kg, L.kb[0], view(ctx->point));
+            CH_LAUNCHED(ctx);
+            k_decode_points<<<grid_for(cells, NT), NT, 0, ctx->st>>>(
+                ctx->point.key, np_d, ctx->kg, L.kb[0], lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->point.f,
+                ctx->point.cap, ctx->d_pred_end, ctx->point.gpu, ctx->point.it, ctx->point.ph, ctx->point.ly,
+                ctx->point.op, ctx->point.label, ctx->point.rank, ctx->point.first_pred);
+            CH_LAUNCHED(ctx);
+        }
+        return CHOPPER_OK;
+    }();
+    ctx->hold_scratch = false;
+    CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[1], ctx->st));
+    ctx->st = main_st;
+    CH_TRY(pst);
     // roll-ups (D12): instance -> layer (staged), -> phase, -> iteration, -> gpu (warp per parent)
     // instances per layer: ~ instances / layer spans of the local gpus (fan-out hint for the staging width)
     const int64_t n_layers = std::max<int64_t>(ctx->n_layer_spans, 1);
@@ -1368,47 +1423,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
             ctx->iter_cu, ctx->iter_af, ctx->iter_al, ctx->iter_step);
         CH_LAUNCHED(ctx);
     }
-    // points (label, gpu, iteration): per-iteration label folds into a dense grid, then compaction
-    {
-        const int64_t n = ctx->inst.cap;
-        const int nL = std::max(ctx->cfg.n_labels, 1), n_lg = std::max(ctx->n_lg, 1);
-        const int R0 = (int)std::max<int64_t>(ctx->max_it_list, 1);
-        const int64_t cells = (int64_t)nL * n_lg * R0;
-        int lbits = bits_for((uint64_t)std::max(ctx->cfg.n_labels, 1));
-        int pbits = lbits + ctx->kg + L.kb[0];
-        if (pbits > 63) return ch_fail(ctx, CHOPPER_E_RANGE, "point key exceeds 63 bits");
-        if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels");
-        int64_t *its = nullptr, *n_it = nullptr;
-        CH_TRY(group(ctx, ctx->inst.key, n, ctx->inst.n_dev, L.sh_it, &its, &n_it));
-        int64_t *df = CH_ALLOC(ctx, int64_t, (int64_t)RF_NFIELDS * cells);
-        double *dc = CH_ALLOC(ctx, double, (int64_t)std::max(C, 1) * cells);
-        int64_t *dvalid = CH_ALLOC(ctx, int64_t, cells), *dex = CH_ALLOC(ctx, int64_t, cells), *np_d = CH_ALLOC(ctx, int64_t, 1);
-        unsigned int *ovf = CH_ALLOC(ctx, unsigned int, 1);
-        CH_ALLOC_END(ctx);
-        *ovf_out = ovf;
-        CH_CUDA(ctx, cudaMemsetAsync(dvalid, 0, 8 * (size_t)cells, ctx->st));
-        CH_CUDA(ctx, cudaMemsetAsync(ovf, 0, 4, ctx->st));
-        size_t shb = (size_t)(RF_NFIELDS + C) * PT_CH * 8 + (size_t)nL * C * 8 + 4 * (2 * PT_CH + 9 * (size_t)nL);
-        static size_t attr_shb = 0;
-        if (shb > 48 * 1024 && shb > attr_shb) {
-            CH_CUDA(ctx, cudaFuncSetAttribute(k_points_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
-            attr_shb = shb;
-        }
-        k_points_iter<<<grid_for(std::min<int64_t>(n, (int64_t)n_lg * R0), 1), 256, shb, ctx->st>>>(
-            view(ctx->inst), its, n_it, L, ctx->d_list_beg, ctx->P_label, nL, n_lg, R0, C, df, dc, dvalid, ovf);
-        CH_LAUNCHED(ctx);
-        CH_TRY(ch_scan_excl_i64(ctx, dvalid, dex, cells, np_d));
-        CH_TRY(alloc_table(ctx, ctx->point, std::max<int64_t>(cells, 1), C, true));
-        ctx->point.n_dev = np_d;
-        k_points_compact<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(dvalid, dex, cells, df, dc, C, n_lg, R0,
-                                                                          ctx->kg, L.kb[0], view(ctx->point));
-        CH_LAUNCHED(ctx);
-        k_decode_points<<<grid_for(cells, NT), NT, 0, ctx->st>>>(
-            ctx->point.key, np_d, ctx->kg, L.kb[0], lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->point.f,
-            ctx->point.cap, ctx->d_pred_end, ctx->point.gpu, ctx->point.it, ctx->point.ph, ctx->point.ly,
-            ctx->point.op, ctx->point.label, ctx->point.rank, ctx->point.first_pred);
-        CH_LAUNCHED(ctx);
-    }
+    CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->join_ev[1], 0));
     // derived ratio-of-sums rates
     if (ctx->n_ratios > 0) {
         RowTable *ts[2] = {&ctx->point, &ctx->iter};
