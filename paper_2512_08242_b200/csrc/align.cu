@@ -354,6 +354,7 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
     const int64_t N = ctx->N;
     const int n_lg = ctx->n_lg, C = n_counters;
     ctx->C = C;
+    ctx->off_pending = false;
     ctx->passes.clear();
     ctx->pass_slots.clear();
     std::vector<std::vector<int>> by_lg(n_lg);
@@ -415,6 +416,7 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         CH_LAUNCHED(ctx);
         k_mg<<<1, 256, 0, ctx->st>>>(base, n_lg, ctx->d_mg);
         CH_LAUNCHED(ctx);
+        CH_TRY(ch_offsets_launch(ctx));                 // the exchange block is complete: a4 shares the read-back
 
         if (n_passes > 0) {
             std::vector<int32_t> off(n_lg + 1, 0), idx;
@@ -557,11 +559,12 @@ chopper_status ch_assign_slots(chopper_ctx *ctx) {
     return CHOPPER_OK;
 }
 
-chopper_status ch_offsets(chopper_ctx *ctx) {
-    const int n_lg = ctx->n_lg, G = ctx->cfg.n_traced_gpus;
+// a4 in two halves: the launch half (exchange, lower medians, skew, asynchronous read-backs) is issued by
+// ch_align before its own read-back, so both share one host synchronization; the finish half reads them
+chopper_status ch_offsets_launch(chopper_ctx *ctx) {
+    const int G = ctx->cfg.n_traced_gpus;
     const int64_t W = ctx->xW, K = W / 4 - 1;
     const int slots = ctx->xslots;
-    (void)n_lg;
     CH_ALLOC_BEGIN;
     int64_t *all = CH_ALLOC(ctx, int64_t, (int64_t)slots * W * ctx->nranks);
     ctx->d_delta = CH_ALLOC(ctx, int64_t, G);
@@ -577,29 +580,41 @@ chopper_status ch_offsets(chopper_ctx *ctx) {
     } else {
         CH_CUDA(ctx, cudaMemcpyAsync(all, ctx->d_xsend, 8 * slots * W, cudaMemcpyDeviceToDevice, ctx->st));
     }
-    int nslots = slots * ctx->nranks;
+    const int nslots = slots * ctx->nranks;
     k_delta<<<nslots, DL_NT, 0, ctx->st>>>(all, nslots, W, K, ctx->d_delta, ctx->d_delta_flag);
     CH_LAUNCHED(ctx);
     k_skew<<<64, 256, 0, ctx->st>>>(all, nslots, W, K, ctx->d_delta, mskew);
     CH_LAUNCHED(ctx);
     ctx->delta.assign(G, 0);
     ctx->delta_flag.assign(G, 1);
-    unsigned long long hs[2] = {0, 0};
-    unsigned int hovf = 0;
-    std::vector<int64_t> hdr(2 * (size_t)nslots);
+    ctx->off_hs[0] = ctx->off_hs[1] = 0;
+    ctx->off_ovf = 0;
+    ctx->off_hdr.assign(2 * (size_t)nslots, 0);
     CH_CUDA(ctx, cudaMemcpyAsync(ctx->delta.data(), ctx->d_delta, 8 * G, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(ctx->delta_flag.data(), ctx->d_delta_flag, 4 * G, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(hs, mskew, 16, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ctx->d_xovf, 4, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpy2DAsync(hdr.data(), 16, all, 8 * (size_t)W, 16, nslots, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(ctx->off_hs, mskew, 16, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(&ctx->off_ovf, ctx->d_xovf, 4, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpy2DAsync(ctx->off_hdr.data(), 16, all, 8 * (size_t)W, 16, nslots, cudaMemcpyDeviceToHost,
+                                   ctx->st));
+    ctx->off_pending = true;
+    return CHOPPER_OK;
+}
+
+chopper_status ch_offsets_finish(chopper_ctx *ctx) {
+    const int G = ctx->cfg.n_traced_gpus;
+    if (!ctx->off_pending) CH_TRY(ch_offsets_launch(ctx));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));          // (already reached when ch_align synchronized)
+    ctx->off_pending = false;
+    const int nslots = (int)(ctx->off_hdr.size() / 2);
     // gpus absent from every rank keep flag 1 (no events)
     ctx->gpu_present.assign(G, 0);
     for (int b = 0; b < nslots; b++)
-        if (hdr[2 * (size_t)b + 1]) ctx->gpu_present[hdr[2 * (size_t)b]] = 1;
+        if (ctx->off_hdr[2 * (size_t)b + 1]) ctx->gpu_present[ctx->off_hdr[2 * (size_t)b]] = 1;
     for (int g = 0; g < G; g++) if (!ctx->gpu_present[g]) { ctx->delta_flag[g] = 1; ctx->delta[g] = 0; }
-    ctx->max_skew[0] = (int64_t)hs[0];
-    ctx->max_skew[1] = (int64_t)hs[1];
-    if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "more collectives per class than max_coll_per_class");
+    ctx->max_skew[0] = (int64_t)ctx->off_hs[0];
+    ctx->max_skew[1] = (int64_t)ctx->off_hs[1];
+    if (ctx->off_ovf) return ch_fail(ctx, CHOPPER_E_RANGE, "more collectives per class than max_coll_per_class");
     return CHOPPER_OK;
 }
+
+chopper_status ch_offsets(chopper_ctx *ctx) { return ch_offsets_finish(ctx); }

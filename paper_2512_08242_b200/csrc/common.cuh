@@ -185,6 +185,10 @@ struct chopper_ctx {
     std::vector<int64_t> delta;
     std::vector<int32_t> delta_flag;
     int64_t max_skew[2] = {0, 0};
+    unsigned long long off_hs[2] = {0, 0};      // a4 read-back staging (ch_offsets_launch / _finish)
+    unsigned int off_ovf = 0;
+    std::vector<int64_t> off_hdr;
+    bool off_pending = false;
     std::vector<int32_t> present;    // [n_lg][C]
     int32_t *d_present = nullptr;    // [n_lg][C]
     const double **d_col = nullptr;  // [n_lg][C] value column of the pass providing the slot
@@ -417,6 +421,7 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
 chopper_status ch_assign_slots(chopper_ctx *ctx);          // slot -> column from the passes' known state
 chopper_status ch_counters_full(chopper_ctx *ctx);         // full-mode [C][N] counter matrix
 chopper_status ch_offsets(chopper_ctx *ctx);
+chopper_status ch_offsets_launch(chopper_ctx *ctx);
 // tables.cu
 chopper_status ch_tables(chopper_ctx *ctx);
 // compose.cu
