@@ -469,3 +469,39 @@ def test_chrome_ingest_malformed():
         _ingest_gpu(b'{"traceEvents": [{"ph": "X", "cat": "kernel", "name": "k", "pid": 0, "tid": 0, "ts": 1, "dur": }]}')
     with pytest.raises(ch.ChopperError):
         _ingest_gpu(b'{"events": []}')
+
+
+def test_multi_stream_many_tiles():
+    """two compute streams per gpu over many tiles: timeline queries go backwards between streams (the event
+    pass seeks out of its windows), the compute union is built explicitly, chains per (gpu, stream)"""
+    rng = np.random.default_rng(91)
+    G = 2
+    tt = TinyTrace(n_gpus=G, n_counters=2, labels=["l%d" % i for i in range(4)])
+    for g in range(G):
+        tt.span(g, 0, 0, 10 ** 9, 5).span(g, 1, 0, 10 ** 9, 0)
+        t_host = 0
+        t_dev = [1000, 1000]
+        names = []
+        for k in range(6000):
+            st = int(rng.integers(0, 2))
+            d = int(rng.integers(20, 300))
+            ks = t_dev[st] + int(rng.integers(0, 40))
+            t_dev[st] = ks + d
+            t_host += int(rng.integers(1, 60))
+            tl = min(t_host, ks)
+            tt.ev(g, tl, ks, ks + d, stream=st, name=k % 5)
+            names.append(k % 5)
+            if k % 25 == 0:
+                tt.span(g, 3, tl, tl + 2000, k % 4)
+            if k % 9 == 0:
+                a = ks + int(rng.integers(0, 200))
+                tt.ev(g, tl, a, a + int(rng.integers(50, 900)), kind=AG if k % 2 else RS, stream=2 + (k % 2), name=5)
+                names.append(5)
+            if k % 7 == 0:
+                tt.sample(g, ks, int(rng.integers(1300, 2100)), int(rng.integers(500, 900)))
+        tt.counter_pass(g, names, [0, 1], rng.integers(0, 1000, size=(2, len(names))).astype(float))
+    b = tt.bundle()
+    p = params(b, f_gemm=np.full(4, 1e9), op_type=np.array([1, 2, 0, 1], np.int32))
+    ref, got, res, _ = run_both(b, p)
+    _check_status(ref, got)
+    assert_parity(ref, got)
