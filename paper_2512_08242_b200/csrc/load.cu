@@ -198,6 +198,195 @@ __global__ void k_chain(const uint32_t *__restrict__ perm, const uint32_t *__res
     }
 }
 
+// ---- lean a2 (every gpu has at most one compute stream): no full partition.  The compute group of a gpu in
+// dispatch order IS its (g, stream, t_ks) order when it is start-monotone (checked here; otherwise the full
+// path runs), so the chain predecessor is the previous COMPUTE event of the gpu in input order.  Only the
+// communication and compute buckets of the permutation are written (the union and the full-mode compute
+// overlap read them); the other bucket is never read.
+constexpr int LN_NT = 256, LN_IPT = 8, LN_TILE = LN_NT * LN_IPT;
+// per tile: communication / compute counts, the last compute index; per bucket counts (global atomics)
+__global__ void __launch_bounds__(LN_NT) k_lean_tiles(const uint32_t *__restrict__ meta, int64_t n,
+                                                      const int32_t *__restrict__ gpu_lg, int NG, int other,
+                                                      int64_t *__restrict__ t_comm, int64_t *__restrict__ t_comp,
+                                                      int64_t *__restrict__ t_last, unsigned long long *__restrict__ bcnt,
+                                                      int nb) {
+    extern __shared__ unsigned int ln_h[];               // [nb]
+    __shared__ int64_t sm[33];
+    for (int b = threadIdx.x; b < nb; b += LN_NT) ln_h[b] = 0;
+    __syncthreads();
+    const int64_t i0 = (int64_t)blockIdx.x * LN_TILE + (int64_t)threadIdx.x * LN_IPT;
+    int64_t cc = 0, cp = 0, last = -1;
+    for (int k = 0; k < LN_IPT; k++) {
+        const int64_t i = i0 + k;
+        if (i >= n) break;
+        const uint32_t m = meta[i];
+        const int kd = kind_of(m);
+        if (is_comm(kd)) cc++;
+        else if (kd == CK_COMPUTE) { cp++; last = i; }
+        atomicAdd(&ln_h[bucket_of(m, gpu_lg, NG, other)], 1u);
+    }
+    int64_t tc, tp;
+    block_excl_sum<LN_NT>(cc, &tc, sm);
+    block_excl_sum<LN_NT>(cp, &tp, sm);
+    // block max of last
+    int64_t x = last;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) { const int64_t y = __shfl_xor_sync(CH_FULL, x, o); x = y > x ? y : x; }
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t mx = -1;
+        for (int w = 0; w < LN_NT / 32; w++) mx = sm[w] > mx ? sm[w] : mx;
+        t_comm[blockIdx.x] = tc;
+        t_comp[blockIdx.x] = tp;
+        t_last[blockIdx.x] = mx;
+    }
+    for (int b = threadIdx.x; b < nb; b += LN_NT)
+        if (ln_h[b]) atomicAdd(&bcnt[b], (unsigned long long)ln_h[b]);
+}
+// one block: exclusive max-scan of the tiles' last compute index (carry into every tile), bucket begins
+// (exclusive scan of the bucket counts), and per-lg communication / compute ranks at the gpu's start
+__global__ void k_lean_small(const int64_t *__restrict__ t_last, int64_t ntile, int64_t *__restrict__ carry,
+                             const unsigned long long *__restrict__ bcnt, int nb, int NG,
+                             int64_t *__restrict__ bbeg, int64_t *__restrict__ lg_comm0, int64_t *__restrict__ lg_comp0,
+                             int n_lg) {
+    __shared__ int64_t s_run;
+    if (threadIdx.x == 0) {
+        s_run = -1;
+        int64_t acc = 0, c0 = 0, p0 = 0;
+        for (int b = 0; b < nb; b++) {
+            bbeg[b] = acc;
+            acc += (int64_t)bcnt[b];
+        }
+        bbeg[nb] = acc;
+        for (int l = 0; l < n_lg; l++) {
+            lg_comm0[l] = c0;
+            lg_comp0[l] = p0;
+            c0 += (int64_t)bcnt[l * NG + 0];
+            p0 += (int64_t)bcnt[l * NG + 1];
+        }
+    }
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < ntile; b0 += blockDim.x) {
+        const int64_t t = b0 + threadIdx.x;
+        int64_t v = t < ntile ? t_last[t] : -1;
+        // inclusive max-scan in the block (warp shuffles + a warp of partials)
+        __shared__ int64_t wm[32];
+        int64_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const int64_t y = __shfl_up_sync(CH_FULL, x, o); if ((threadIdx.x & 31) >= o && y > x) x = y; }
+        if ((threadIdx.x & 31) == 31) wm[threadIdx.x >> 5] = x;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            int64_t z = threadIdx.x < blockDim.x / 32 ? wm[threadIdx.x] : -1;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) { const int64_t y = __shfl_up_sync(CH_FULL, z, o); if ((int)threadIdx.x >= o && y > z) z = y; }
+            wm[threadIdx.x] = z;
+        }
+        __syncthreads();
+        int64_t inc = x;
+        if ((threadIdx.x >> 5) > 0 && wm[(threadIdx.x >> 5) - 1] > inc) inc = wm[(threadIdx.x >> 5) - 1];
+        if (s_run > inc) inc = s_run;
+        // exclusive: the inclusive value of the previous tile
+        int64_t ex = __shfl_up_sync(CH_FULL, inc, 1);
+        if ((threadIdx.x & 31) == 0) ex = (threadIdx.x >> 5) > 0 ? (wm[(threadIdx.x >> 5) - 1] > s_run ? wm[(threadIdx.x >> 5) - 1] : s_run) : s_run;
+        if (t < ntile) carry[t] = ex;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_run = inc;
+        __syncthreads();
+    }
+}
+// the chain and the two buckets, per tile of 2048 events (8 consecutive per thread)
+__global__ void __launch_bounds__(LN_NT) k_lean_chain(const uint32_t *__restrict__ meta,
+                                                      const int64_t *__restrict__ ks, const int64_t *__restrict__ ke,
+                                                      int64_t n, const int32_t *__restrict__ gpu_lg, int NG,
+                                                      const int64_t *__restrict__ g_beg,
+                                                      const int64_t *__restrict__ t_comm_ex,
+                                                      const int64_t *__restrict__ t_comp_ex,
+                                                      const int64_t *__restrict__ carry,
+                                                      const int64_t *__restrict__ bbeg,
+                                                      const int64_t *__restrict__ lg_comm0,
+                                                      const int64_t *__restrict__ lg_comp0,
+                                                      uint32_t *__restrict__ perm, int64_t *__restrict__ pred_end,
+                                                      DevReport *rep, unsigned int *__restrict__ nonmono) {
+    __shared__ int64_t sm[33];
+    __shared__ int64_t wl[LN_NT / 32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * LN_TILE + (int64_t)tid * LN_IPT;
+    const int nv = i0 >= n ? 0 : (int)min((int64_t)LN_IPT, n - i0);
+    uint32_t mt[LN_IPT];
+    int64_t vs[LN_IPT], ve[LN_IPT];
+    if (nv == LN_IPT && ((((uintptr_t)(meta + i0)) | ((uintptr_t)(ks + i0)) | ((uintptr_t)(ke + i0))) & 15u) == 0) {
+#pragma unroll
+        for (int h = 0; h < LN_IPT / 4; h++) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4 *>(meta + i0) + h);
+            mt[4 * h] = x.x; mt[4 * h + 1] = x.y; mt[4 * h + 2] = x.z; mt[4 * h + 3] = x.w;
+        }
+#pragma unroll
+        for (int h = 0; h < LN_IPT / 2; h++) {
+            const longlong2 x = __ldg(reinterpret_cast<const longlong2 *>(ks + i0) + h);
+            const longlong2 y = __ldg(reinterpret_cast<const longlong2 *>(ke + i0) + h);
+            vs[2 * h] = x.x; vs[2 * h + 1] = x.y;
+            ve[2 * h] = y.x; ve[2 * h + 1] = y.y;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < LN_IPT; k++) {
+            const bool ok = k < nv;
+            mt[k] = ok ? meta[i0 + k] : (uint32_t)CK_MEMOP;
+            vs[k] = ok ? ks[i0 + k] : 0;
+            ve[k] = ok ? ke[i0 + k] : 0;
+        }
+    }
+    int64_t cc = 0, cp = 0, last = -1;
+#pragma unroll
+    for (int k = 0; k < LN_IPT; k++) {
+        const int kd = kind_of(mt[k]);
+        if (k < nv && is_comm(kd)) cc++;
+        else if (k < nv && kd == CK_COMPUTE) { cp++; last = i0 + k; }
+    }
+    int64_t ex_c = block_excl_sum<LN_NT>(cc, nullptr, sm) + t_comm_ex[blockIdx.x];
+    int64_t ex_p = block_excl_sum<LN_NT>(cp, nullptr, sm) + t_comp_ex[blockIdx.x];
+    // the last compute index before this thread
+    int64_t x = last;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { const int64_t y = __shfl_up_sync(CH_FULL, x, o); if (lane >= o && y > x) x = y; }
+    if (lane == 31) wl[w] = x;
+    __syncthreads();
+    int64_t before = carry[blockIdx.x];
+    for (int q = 0; q < w; q++) before = wl[q] > before ? wl[q] : before;
+    const int64_t xp = __shfl_up_sync(CH_FULL, x, 1);
+    if (lane > 0 && xp > before) before = xp;
+    // the predecessor's start / end: from global memory for the thread's first compute event, then registers
+    int64_t p_ks = 0, p_ke = 0;
+    if (before >= 0 && cp > 0) { p_ks = ks[before]; p_ke = ke[before]; }
+#pragma unroll
+    for (int k = 0; k < LN_IPT; k++) {
+        if (k >= nv) break;
+        const int64_t i = i0 + k;
+        const uint32_t m = mt[k];
+        const int kd = kind_of(m);
+        const int lg = gpu_lg[gpu_of(m)];
+        if (is_comm(kd)) {
+            perm[bbeg[lg * NG + 0] + (ex_c - lg_comm0[lg])] = (uint32_t)i;
+            ex_c++;
+        } else if (kd == CK_COMPUTE) {
+            perm[bbeg[lg * NG + 1] + (ex_p - lg_comp0[lg])] = (uint32_t)i;
+            ex_p++;
+            int64_t pe = CH_NONE_TS;
+            if (before >= g_beg[lg]) {
+                pe = p_ke;
+                if (vs[k] < p_ks) atomicOr(nonmono, 1u);          // not start-monotone: the full path sorts it
+                if (vs[k] < pe) viol(rep, CV_STREAM_OVERLAP, i);
+            }
+            pred_end[i] = pe;
+            before = i;
+            p_ks = vs[k];
+            p_ke = ve[k];
+        }
+    }
+}
+
 // keys of the events in the flagged bucket segments: (segment, t_ks - t0), value = input index
 __global__ void k_seg_keys(const uint32_t *__restrict__ perm, const int64_t *__restrict__ ks,
                            const int64_t *__restrict__ lo, const int64_t *__restrict__ pre, int nseg, int64_t M,
@@ -329,6 +518,83 @@ static void fill_public_report(chopper_ctx *ctx) {
     r.full_sort_used = ctx->full_sort ? 1 : 0;
 }
 
+static chopper_status finish_load(chopper_ctx *ctx) {
+    // same-stream overlaps are data (SPEC.md:59-60): reported, processing continues
+    fill_public_report(ctx);
+    if (ctx->h_rep.val_count[CV_STREAM_OVERLAP]) ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
+    ctx->loaded_ok = true;
+    ctx->mark_after_load = ctx->used;
+    return CHOPPER_OK;
+}
+
+// the lean a2 (see k_lean_chain); *fell_back = true when a compute group is not start-monotone (the caller then
+// runs the full partition + chain, which resets the overlap report it recomputes)
+// stable timestamp sort of the permutation segments [seg_lo[s], seg_lo[s] + size) (D1): a stream-merge fast
+// path (partition by stream + binary-search ranks), else a radix sort on (segment, t_ks - t0)
+static chopper_status sort_segments(chopper_ctx *ctx, std::vector<int64_t> seg_lo, std::vector<int64_t> seg_pre,
+                                    int64_t Mseg) {
+    const int64_t n = ctx->N;
+    CH_ALLOC_BEGIN;
+    const int nseg = (int)seg_lo.size();
+    seg_pre.push_back(Mseg);
+    int tsbits = bits_for((uint64_t)(ctx->t_max - ctx->t0));
+    int sb = bits_for((uint64_t)nseg);
+    if (tsbits + sb > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "sort key exceeds 64 bits");
+    size_t mk = ctx->used;
+    unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, Mseg), *k2 = CH_ALLOC(ctx, unsigned long long, Mseg);
+    uint32_t *v1 = CH_ALLOC(ctx, uint32_t, Mseg), *v2 = CH_ALLOC(ctx, uint32_t, Mseg);
+    int64_t *dlo = CH_ALLOC(ctx, int64_t, nseg + 1), *dpre = CH_ALLOC(ctx, int64_t, nseg + 1);
+    CH_ALLOC_END(ctx);
+    seg_lo.push_back(n);
+    CH_CUDA(ctx, cudaMemcpyAsync(dlo, seg_lo.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(dpre, seg_pre.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
+    // stream-merge fast path (1-2 digit partition + binary-search ranks), else the full radix sort
+    bool merged = false;
+    {
+        const int64_t cells = (int64_t)nseg * SS_STREAMS;
+        unsigned int *cnt = CH_ALLOC(ctx, unsigned int, cells), *fail = CH_ALLOC(ctx, unsigned int, 1);
+        int64_t *c64 = CH_ALLOC(ctx, int64_t, cells), *cst = CH_ALLOC(ctx, int64_t, cells);
+        CH_ALLOC_END(ctx);
+        CH_CUDA(ctx, cudaMemsetAsync(cnt, 0, 4 * (size_t)cells, ctx->st));
+        CH_CUDA(ctx, cudaMemsetAsync(fail, 0, 4, ctx->st));
+        k_ss_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, dlo, dpre, nseg, Mseg,
+                                                                    k1, v1, cnt, fail);
+        CH_LAUNCHED(ctx);
+        bool alt2;
+        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, sb + 8, &alt2));
+        unsigned long long *ksd = alt2 ? k2 : k1;
+        uint32_t *vsd = alt2 ? v2 : v1;
+        k_ss_check<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, fail);
+        CH_LAUNCHED(ctx);
+        k_u32_i64<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(cnt, c64, cells);
+        CH_LAUNCHED(ctx);
+        CH_TRY(ch_scan_excl_i64(ctx, c64, cst, cells, nullptr));
+        unsigned int hfail = 0;
+        CH_CUDA(ctx, cudaMemcpyAsync(&hfail, fail, 4, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        if (!hfail) {
+            k_ss_rank<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, cnt, cst, dlo,
+                                                                        ctx->d_perm);
+            CH_LAUNCHED(ctx);
+            merged = true;
+        }
+    }
+    if (!merged) {
+        k_seg_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.start_ns, dlo, dpre, nseg,
+                                                                     Mseg, ctx->t0, tsbits, k1, v1);
+        CH_LAUNCHED(ctx);
+        bool alt;
+        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, tsbits + sb, &alt));
+        k_seg_scatter<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(alt ? v2 : v1, dlo, dpre, nseg, Mseg,
+                                                                        ctx->d_perm);
+        CH_LAUNCHED(ctx);
+    }
+    ctx->used = mk;
+    return CHOPPER_OK;
+}
+
+static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back);
+
 chopper_status ch_load(chopper_ctx *ctx) {
     const int G = ctx->cfg.n_traced_gpus;
     const int64_t n = ctx->N;
@@ -402,6 +668,11 @@ chopper_status ch_load(chopper_ctx *ctx) {
     ctx->d_bucket_beg = CH_ALLOC(ctx, int64_t, ctx->n_buckets + 1);
     CH_ALLOC_END(ctx);
     const int NG = ctx->NG, other = NG - 1;
+    if (!ctx->multi_stream && ctx->n_buckets <= 1024) {
+        bool fell_back = false;
+        CH_TRY(lean_a2(ctx, &fell_back));
+        if (!fell_back) return finish_load(ctx);
+    }
     size_t mark = ctx->used;
     if (ctx->n_buckets <= 256) {
         CH_TRY(ch_radix_partition_meta(ctx, ctx->ev.meta, ctx->d_gpu_lg, NG, other, ctx->d_perm, n));
@@ -451,61 +722,7 @@ chopper_status ch_load(chopper_ctx *ctx) {
             if (b % NG >= 1 && b % NG != other) compute_resorted = true;
         }
     if (Mseg > 0) {
-        const int nseg = (int)seg_lo.size();
-        seg_pre.push_back(Mseg);
-        int tsbits = bits_for((uint64_t)(ctx->t_max - ctx->t0));
-        int sb = bits_for((uint64_t)nseg);
-        if (tsbits + sb > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "sort key exceeds 64 bits");
-        size_t mk = ctx->used;
-        unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, Mseg), *k2 = CH_ALLOC(ctx, unsigned long long, Mseg);
-        uint32_t *v1 = CH_ALLOC(ctx, uint32_t, Mseg), *v2 = CH_ALLOC(ctx, uint32_t, Mseg);
-        int64_t *dlo = CH_ALLOC(ctx, int64_t, nseg + 1), *dpre = CH_ALLOC(ctx, int64_t, nseg + 1);
-        CH_ALLOC_END(ctx);
-        seg_lo.push_back(n);
-        CH_CUDA(ctx, cudaMemcpyAsync(dlo, seg_lo.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(dpre, seg_pre.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
-        // stream-merge fast path (1-2 digit partition + binary-search ranks), else the full radix sort
-        bool merged = false;
-        {
-            const int64_t cells = (int64_t)nseg * SS_STREAMS;
-            unsigned int *cnt = CH_ALLOC(ctx, unsigned int, cells), *fail = CH_ALLOC(ctx, unsigned int, 1);
-            int64_t *c64 = CH_ALLOC(ctx, int64_t, cells), *cst = CH_ALLOC(ctx, int64_t, cells);
-            CH_ALLOC_END(ctx);
-            CH_CUDA(ctx, cudaMemsetAsync(cnt, 0, 4 * (size_t)cells, ctx->st));
-            CH_CUDA(ctx, cudaMemsetAsync(fail, 0, 4, ctx->st));
-            k_ss_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, dlo, dpre, nseg, Mseg,
-                                                                        k1, v1, cnt, fail);
-            CH_LAUNCHED(ctx);
-            bool alt2;
-            CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, sb + 8, &alt2));
-            unsigned long long *ksd = alt2 ? k2 : k1;
-            uint32_t *vsd = alt2 ? v2 : v1;
-            k_ss_check<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, fail);
-            CH_LAUNCHED(ctx);
-            k_u32_i64<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(cnt, c64, cells);
-            CH_LAUNCHED(ctx);
-            CH_TRY(ch_scan_excl_i64(ctx, c64, cst, cells, nullptr));
-            unsigned int hfail = 0;
-            CH_CUDA(ctx, cudaMemcpyAsync(&hfail, fail, 4, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
-            if (!hfail) {
-                k_ss_rank<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, cnt, cst, dlo,
-                                                                            ctx->d_perm);
-                CH_LAUNCHED(ctx);
-                merged = true;
-            }
-        }
-        if (!merged) {
-            k_seg_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.start_ns, dlo, dpre, nseg,
-                                                                         Mseg, ctx->t0, tsbits, k1, v1);
-            CH_LAUNCHED(ctx);
-            bool alt;
-            CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, tsbits + sb, &alt));
-            k_seg_scatter<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(alt ? v2 : v1, dlo, dpre, nseg, Mseg,
-                                                                            ctx->d_perm);
-            CH_LAUNCHED(ctx);
-        }
-        ctx->used = mk;
+        CH_TRY(sort_segments(ctx, seg_lo, seg_pre, Mseg));
         ctx->full_sort = true;
         if (compute_resorted) {
             // chain predecessors and the disjointness check depend on the corrected order
@@ -521,10 +738,68 @@ chopper_status ch_load(chopper_ctx *ctx) {
             CH_TRY(read_report(ctx));
         }
     }
-    // same-stream overlaps are data (SPEC.md:59-60): reported, processing continues
-    fill_public_report(ctx);
-    if (ctx->h_rep.val_count[CV_STREAM_OVERLAP]) ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
-    ctx->loaded_ok = true;
-    ctx->mark_after_load = ctx->used;
+    return finish_load(ctx);
+}
+
+static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back) {
+    const int64_t n = ctx->N;
+    const int NG = ctx->NG, other = NG - 1, nb = ctx->n_buckets, n_lg = ctx->n_lg;
+    *fell_back = false;
+    const int64_t ntile = ceil_div(n, LN_TILE);
+    CH_ALLOC_BEGIN;
+    const size_t keep = ctx->used;
+    int64_t *tcm = CH_ALLOC(ctx, int64_t, ntile + 1), *tcp = CH_ALLOC(ctx, int64_t, ntile + 1);
+    int64_t *tla = CH_ALLOC(ctx, int64_t, ntile + 1), *tcme = CH_ALLOC(ctx, int64_t, ntile + 1);
+    int64_t *tcpe = CH_ALLOC(ctx, int64_t, ntile + 1), *carry = CH_ALLOC(ctx, int64_t, ntile + 1);
+    unsigned long long *bcnt = CH_ALLOC(ctx, unsigned long long, nb + 1);
+    int64_t *lc0 = CH_ALLOC(ctx, int64_t, n_lg + 1), *lp0 = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    int64_t *gb = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    unsigned int *nonmono = CH_ALLOC(ctx, unsigned int, 1);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemsetAsync(bcnt, 0, 8 * (size_t)(nb + 1), ctx->st));
+    CH_CUDA(ctx, cudaMemsetAsync(nonmono, 0, 4, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(gb, ctx->g_beg, 8 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
+    k_lean_tiles<<<(unsigned)ntile, LN_NT, 4 * nb, ctx->st>>>(ctx->ev.meta, n, ctx->d_gpu_lg, NG, other, tcm, tcp, tla,
+                                                              bcnt, nb);
+    CH_LAUNCHED(ctx);
+    CH_TRY(ch_scan_excl_i64(ctx, tcm, tcme, ntile, nullptr));
+    CH_TRY(ch_scan_excl_i64(ctx, tcp, tcpe, ntile, nullptr));
+    k_lean_small<<<1, 1024, 0, ctx->st>>>(tla, ntile, carry, bcnt, nb, NG, ctx->d_bucket_beg, lc0, lp0, n_lg);
+    CH_LAUNCHED(ctx);
+    k_lean_chain<<<(unsigned)ntile, LN_NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, ctx->ev.end_ns, n, ctx->d_gpu_lg,
+                                                         NG, gb, tcme, tcpe, carry, ctx->d_bucket_beg, lc0, lp0,
+                                                         ctx->d_perm, ctx->d_pred_end, ctx->d_rep, nonmono);
+    CH_LAUNCHED(ctx);
+    ctx->bucket_beg.assign(nb + 1, 0);
+    unsigned int hnm = 0;
+    CH_CUDA(ctx, cudaMemcpyAsync(ctx->bucket_beg.data(), ctx->d_bucket_beg, 8 * (nb + 1), cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(&hnm, nonmono, 4, cudaMemcpyDeviceToHost, ctx->st));
+    CH_TRY(read_report(ctx));
+    ctx->used = keep;
+    if (hnm) {
+        // a compute group out of start order: the full path (it resets and recomputes the overlap report)
+        unsigned long long zero = 0, none = ~0ull;
+        CH_CUDA(ctx, cudaMemcpyAsync(&ctx->d_rep->val_count[CV_STREAM_OVERLAP], &zero, 8, cudaMemcpyHostToDevice, ctx->st));
+        CH_CUDA(ctx, cudaMemcpyAsync(&ctx->d_rep->val_first[CV_STREAM_OVERLAP], &none, 8, cudaMemcpyHostToDevice, ctx->st));
+        *fell_back = true;
+        return CHOPPER_OK;
+    }
+    ctx->full_sort = false;
+    // communication buckets: a stable timestamp sort of each (streams interleave); one segment per gpu
+    std::vector<int64_t> seg_lo, seg_pre;
+    int64_t Mseg = 0;
+    for (int l = 0; l < n_lg; l++) {
+        const int b = l * NG;
+        const int64_t c = ctx->bucket_beg[b + 1] - ctx->bucket_beg[b];
+        if (c >= 2) {
+            seg_lo.push_back(ctx->bucket_beg[b]);
+            seg_pre.push_back(Mseg);
+            Mseg += c;
+        }
+    }
+    if (Mseg > 0) {
+        CH_TRY(sort_segments(ctx, seg_lo, seg_pre, Mseg));
+        ctx->full_sort = true;
+    }
     return CHOPPER_OK;
 }
