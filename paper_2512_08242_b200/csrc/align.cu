@@ -101,6 +101,16 @@ __global__ void k_counters_out(const uint32_t *__restrict__ meta, int64_t n, con
 // ---- per-gpu ranks from meta: non-MEMOP (counter-pass position), AG and RS (collective index) -------
 // tile = 2048 events; counts of the three predicates packed 21 bits apart
 constexpr int MR_NT = 256, MR_IPT = 8, MR_TILE = MR_NT * MR_IPT;
+// a thread's 8 consecutive metas (two 16 B loads when whole and aligned; MEMOP past the end)
+__device__ __forceinline__ void load_meta8(const uint32_t *__restrict__ meta, int64_t i0, int64_t n, uint32_t (&mm)[8]) {
+    if (i0 + 8 <= n && (((uintptr_t)(meta + i0)) & 15u) == 0) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(meta + i0)), b = __ldg(reinterpret_cast<const uint4 *>(meta + i0) + 1);
+        mm[0] = a.x; mm[1] = a.y; mm[2] = a.z; mm[3] = a.w; mm[4] = b.x; mm[5] = b.y; mm[6] = b.z; mm[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; k++) mm[k] = i0 + k < n ? meta[i0 + k] : (uint32_t)CK_MEMOP;
+    }
+}
 __device__ __forceinline__ unsigned long long pred3(uint32_t m) {
     int k = kind_of(m);
     return (k != CK_MEMOP ? 1ull : 0ull) | (k == CK_AG ? 1ull << 21 : 0ull) | (k == CK_RS ? 1ull << 42 : 0ull);
@@ -110,8 +120,11 @@ __global__ void __launch_bounds__(MR_NT) k_meta_tiles(const uint32_t *__restrict
     __shared__ int64_t sm[33];
     int64_t i0 = (int64_t)blockIdx.x * MR_TILE + (int64_t)threadIdx.x * MR_IPT;
     unsigned long long c = 0;
+    uint32_t mm[MR_IPT];
+    load_meta8(meta, i0, n, mm);
+#pragma unroll
     for (int k = 0; k < MR_IPT; k++)
-        if (i0 + k < n) c += pred3(meta[i0 + k]);
+        if (i0 + k < n) c += pred3(mm[k]);
     int64_t tot;
     block_excl_sum<MR_NT>((int64_t)c, &tot, sm);
     if (threadIdx.x == 0) {
@@ -166,16 +179,16 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
     int64_t i0 = (int64_t)blockIdx.x * MR_TILE + (int64_t)threadIdx.x * MR_IPT;
     uint32_t mm[MR_IPT];
     unsigned long long c = 0;
+    load_meta8(meta, i0, n, mm);
 #pragma unroll
-    for (int k = 0; k < MR_IPT; k++) {
-        mm[k] = i0 + k < n ? meta[i0 + k] : (uint32_t)CK_MEMOP;
+    for (int k = 0; k < MR_IPT; k++)
         if (i0 + k < n) c += pred3(mm[k]);
-    }
     int64_t tot;
     unsigned long long ex = (unsigned long long)block_excl_sum<MR_NT>((int64_t)c, &tot, sm);
     int64_t r0 = tex[blockIdx.x] + (int64_t)(ex & 0x1FFFFF);
     int64_t r1 = tex[ntile + blockIdx.x] + (int64_t)((ex >> 21) & 0x1FFFFF);
     int64_t r2 = tex[2 * ntile + blockIdx.x] + (int64_t)(ex >> 42);
+    int32_t nr[MR_IPT];
 #pragma unroll
     for (int k = 0; k < MR_IPT; k++) {
         int64_t i = i0 + k;
@@ -183,7 +196,7 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
         uint32_t m = mm[k];
         int lg = gpu_lg[gpu_of(m)];
         int kd = kind_of(m);
-        nm_rank[i] = (int32_t)(r0 - base[lg]);
+        nr[k] = (int32_t)(r0 - base[lg]);
         if (kd == CK_AG || kd == CK_RS) {
             int64_t j = kd == CK_AG ? r1 - base[(n_lg + 1) + lg] : r2 - base[2 * (n_lg + 1) + lg];
             if (j >= K) atomicOr(ovf, 1u);
@@ -196,6 +209,14 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
         if (kd != CK_MEMOP) r0++;
         if (kd == CK_AG) r1++;
         if (kd == CK_RS) r2++;
+    }
+    if (i0 + MR_IPT <= n && (((uintptr_t)(nm_rank + i0)) & 15u) == 0) {
+        reinterpret_cast<int4 *>(nm_rank + i0)[0] = make_int4(nr[0], nr[1], nr[2], nr[3]);
+        reinterpret_cast<int4 *>(nm_rank + i0)[1] = make_int4(nr[4], nr[5], nr[6], nr[7]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < MR_IPT; k++)
+            if (i0 + k < n) nm_rank[i0 + k] = nr[k];
     }
 }
 
