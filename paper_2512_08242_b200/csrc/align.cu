@@ -18,45 +18,7 @@ namespace {
 constexpr int NT = 256;
 
 
-// name-sequence check of every pass of the event's gpu: pass descriptors staged in shared memory, four
-// events per iteration with every load issued before the compares
-constexpr int PC_MAXP = 256;
-__global__ void k_pass_check(const uint32_t *__restrict__ meta, const int32_t *__restrict__ name_id, int64_t n,
-                             const int32_t *__restrict__ gpu_lg, const int32_t *__restrict__ nm_rank,
-                             const PassDesc *__restrict__ passes, const int32_t *__restrict__ pass_off,
-                             const int32_t *__restrict__ pass_idx, int n_lg, int n_passes,
-                             unsigned long long *__restrict__ mis) {
-    __shared__ PassDesc sp[PC_MAXP];
-    __shared__ int32_t soff[PC_MAXP + 1];
-    for (int q = threadIdx.x; q < n_passes && q < PC_MAXP; q += blockDim.x) sp[q] = passes[pass_idx[q]];
-    for (int q = threadIdx.x; q <= n_lg && q <= PC_MAXP; q += blockDim.x) soff[q] = pass_off[q];
-    __syncthreads();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    constexpr int U = 4;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
-        uint32_t mm[U];
-        int32_t jj[U], nn[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int64_t i = i0 + u * stride;
-            const bool ok = i < n;
-            mm[u] = ok ? meta[i] : (uint32_t)CK_MEMOP;
-            jj[u] = ok ? nm_rank[i] : 0;
-            nn[u] = ok ? name_id[i] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const uint32_t m = mm[u];
-            if (kind_of(m) == CK_MEMOP) continue;
-            const int lg = gpu_lg[gpu_of(m)];
-            const int64_t j = jj[u];
-            for (int q = soff[lg]; q < soff[lg + 1]; q++) {
-                const PassDesc &d = sp[q];
-                if (j < d.n && __ldg(d.name_id + j) != nn[u]) atomicMin(&mis[pass_idx[q]], (unsigned long long)j);
-            }
-        }
-    }
-}
+constexpr int PC_MAXP = 256;           // counter passes per rank (staged in shared memory by the rank pass)
 
 // non-finite values in any pass (blockIdx.y = pass): streaming read, 4 doubles per thread step
 __global__ void k_pass_finite(const PassDesc *__restrict__ passes, unsigned int *__restrict__ bad) {
@@ -174,11 +136,22 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
                                                       const int32_t *__restrict__ gpu_lg, const int64_t *__restrict__ tex,
                                                       int64_t ntile, const int64_t *__restrict__ base, int n_lg,
                                                       int32_t *__restrict__ nm_rank, int64_t *__restrict__ xsend,
-                                                      int64_t K, int64_t W, unsigned int *__restrict__ ovf) {
+                                                      int64_t K, int64_t W, unsigned int *__restrict__ ovf,
+                                                      const int32_t *__restrict__ name_id,
+                                                      const PassDesc *__restrict__ passes,
+                                                      const int32_t *__restrict__ pass_off,
+                                                      const int32_t *__restrict__ pass_idx, int n_passes,
+                                                      unsigned long long *__restrict__ mis) {
     __shared__ int64_t sm[33];
+    __shared__ PassDesc sp[PC_MAXP];
+    __shared__ int32_t soff[PC_MAXP + 1];
     int64_t i0 = (int64_t)blockIdx.x * MR_TILE + (int64_t)threadIdx.x * MR_IPT;
     uint32_t mm[MR_IPT];
     unsigned long long c = 0;
+    if (n_passes > 0) {                  // (visible after block_excl_sum's barriers)
+        for (int q = threadIdx.x; q < n_passes; q += MR_NT) sp[q] = passes[pass_idx[q]];
+        for (int q = threadIdx.x; q <= n_lg; q += MR_NT) soff[q] = pass_off[q];
+    }
     load_meta8(meta, i0, n, mm);
 #pragma unroll
     for (int k = 0; k < MR_IPT; k++)
@@ -209,6 +182,46 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
         if (kd != CK_MEMOP) r0++;
         if (kd == CK_AG) r1++;
         if (kd == CK_RS) r2++;
+    }
+    if (n_passes > 0) {
+        // a3 name-sequence check (D2): the pass entry at this event's rank must carry its name id
+        int32_t nn[MR_IPT];
+        if (i0 + MR_IPT <= n && (((uintptr_t)(name_id + i0)) & 15u) == 0) {
+            const int4 a = reinterpret_cast<const int4 *>(name_id + i0)[0], b = reinterpret_cast<const int4 *>(name_id + i0)[1];
+            nn[0] = a.x; nn[1] = a.y; nn[2] = a.z; nn[3] = a.w; nn[4] = b.x; nn[5] = b.y; nn[6] = b.z; nn[7] = b.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < MR_IPT; k++) nn[k] = i0 + k < n ? name_id[i0 + k] : 0;
+        }
+        bool one_gpu = i0 + MR_IPT <= n;
+#pragma unroll
+        for (int k = 1; k < MR_IPT; k++) one_gpu &= gpu_of(mm[k]) == gpu_of(mm[0]);
+        if (one_gpu) {                   // usual case: pass-outer, the thread's 8 name loads in flight together
+            const int lg = gpu_lg[gpu_of(mm[0])];
+            for (int q = soff[lg]; q < soff[lg + 1]; q++) {
+                const PassDesc d = sp[q];
+                int32_t got[MR_IPT];
+#pragma unroll
+                for (int k = 0; k < MR_IPT; k++)
+                    got[k] = kind_of(mm[k]) != CK_MEMOP && nr[k] < d.n ? __ldg(d.name_id + nr[k]) : nn[k];
+                int64_t bad = INT64_MAX;
+#pragma unroll
+                for (int k = MR_IPT - 1; k >= 0; k--)
+                    if (got[k] != nn[k]) bad = nr[k];
+                if (bad != INT64_MAX) atomicMin(&mis[pass_idx[q]], (unsigned long long)bad);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < MR_IPT; k++) {
+                if (i0 + k >= n || kind_of(mm[k]) == CK_MEMOP) continue;
+                const int lg = gpu_lg[gpu_of(mm[k])];
+                const int64_t j = nr[k];
+                for (int q = soff[lg]; q < soff[lg + 1]; q++) {
+                    const PassDesc &d = sp[q];
+                    if (j < d.n && __ldg(d.name_id + j) != nn[k]) atomicMin(&mis[pass_idx[q]], (unsigned long long)j);
+                }
+            }
+        }
     }
     if (i0 + MR_IPT <= n && (((uintptr_t)(nm_rank + i0)) & 15u) == 0) {
         reinterpret_cast<int4 *>(nm_rank + i0)[0] = make_int4(nr[0], nr[1], nr[2], nr[3]);
@@ -431,34 +444,39 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         k_gpu_bases<<<1, 1024, 0, ctx->st>>>(
             ctx->ev.meta, N, tex, ntile, dgbeg, n_lg, base, dlg, ctx->d_xsend, ctx->xW);
         CH_LAUNCHED(ctx);
-        k_meta_apply<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, ctx->ev.end_ns, N,
-                                                             ctx->d_gpu_lg, tex, ntile, base, n_lg, ctx->d_nm_rank,
-                                                             ctx->d_xsend, K, ctx->xW, ctx->d_xovf);
-        CH_LAUNCHED(ctx);
-        k_mg<<<1, 256, 0, ctx->st>>>(base, n_lg, ctx->d_mg);
-        CH_LAUNCHED(ctx);
-        CH_TRY(ch_offsets_launch(ctx));                 // the exchange block is complete: a4 shares the read-back
-
+        // pass descriptors grouped by local gpu: the a3 name-sequence check runs inside the rank pass
+        int32_t *doff = nullptr, *didx = nullptr;
+        unsigned long long *mis = nullptr;
         if (n_passes > 0) {
-            std::vector<int32_t> off(n_lg + 1, 0), idx;
+            if (n_passes > PC_MAXP || n_lg > PC_MAXP) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 counter passes");
+            std::vector<int32_t> &off = ctx->h_pass_off, &idx = ctx->h_pass_idx;
+            off.assign(n_lg + 1, 0);
+            idx.clear();
             for (int l = 0; l < n_lg; l++) {
                 off[l] = (int32_t)idx.size();
                 for (int p : by_lg[l]) idx.push_back(p);
             }
             off[n_lg] = (int32_t)idx.size();
-            int32_t *doff = CH_ALLOC(ctx, int32_t, n_lg + 1), *didx = CH_ALLOC(ctx, int32_t, n_passes);
-            unsigned long long *mis = CH_ALLOC(ctx, unsigned long long, n_passes);
+            doff = CH_ALLOC(ctx, int32_t, n_lg + 1);
+            didx = CH_ALLOC(ctx, int32_t, n_passes);
+            mis = CH_ALLOC(ctx, unsigned long long, n_passes);
             CH_ALLOC_END(ctx);
             CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_passes, ctx->passes.data(), sizeof(PassDesc) * n_passes,
                                          cudaMemcpyHostToDevice, ctx->st));
             CH_CUDA(ctx, cudaMemcpyAsync(doff, off.data(), 4 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
             CH_CUDA(ctx, cudaMemcpyAsync(didx, idx.data(), 4 * n_passes, cudaMemcpyHostToDevice, ctx->st));
             CH_TRY(ch_fill_u64(ctx, mis, n_passes, ~0ull));
-            if (n_passes > PC_MAXP || n_lg > PC_MAXP) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 counter passes");
-            k_pass_check<<<(unsigned)std::min<int64_t>(ceil_div(N, NT * 4), 148 * 8), NT, 0, ctx->st>>>(
-                ctx->ev.meta, ctx->ev.name_id, N, ctx->d_gpu_lg, ctx->d_nm_rank, ctx->d_passes, doff, didx, n_lg, n_passes,
-                mis);
-            CH_LAUNCHED(ctx);
+        }
+        k_meta_apply<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, ctx->ev.end_ns, N,
+                                                             ctx->d_gpu_lg, tex, ntile, base, n_lg, ctx->d_nm_rank,
+                                                             ctx->d_xsend, K, ctx->xW, ctx->d_xovf, ctx->ev.name_id,
+                                                             ctx->d_passes, doff, didx, n_passes, mis);
+        CH_LAUNCHED(ctx);
+        k_mg<<<1, 256, 0, ctx->st>>>(base, n_lg, ctx->d_mg);
+        CH_LAUNCHED(ctx);
+        CH_TRY(ch_offsets_launch(ctx));                 // the exchange block is complete: a4 shares the read-back
+
+        if (n_passes > 0) {
             // one read-back: the name-sequence divergences and the per-gpu non-MEMOP counts
             std::vector<unsigned long long> hmis(n_passes);
             std::vector<int64_t> &m_g = ctx->h_mg;

@@ -179,6 +179,7 @@ struct chopper_ctx {
     int32_t *d_nm_rank = nullptr;    // [N] rank among non-MEMOP events of its gpu
     int64_t *d_mg = nullptr;         // [n_lg] non-MEMOP events per local gpu (counter column length)
     std::vector<int64_t> h_mg;
+    std::vector<int32_t> h_pass_off, h_pass_idx;   // a3: passes grouped by local gpu (upload staging)
     std::vector<int32_t> h_lg_gpu;    // host staging of lg -> gpu (async copies read it)
     int64_t *d_delta = nullptr;      // [n_traced]
     int32_t *d_delta_flag = nullptr;

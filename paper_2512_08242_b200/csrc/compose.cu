@@ -110,21 +110,52 @@ __global__ void k_dense_e2e(int64_t *blk, Layout Ly, const int64_t *__restrict__
 }
 
 // ---- block-level helpers ----
+// Bitonic sort of a[0..n2) (n2 a power of two) by the whole block.  Each warp owns a contiguous segment of
+// n2 / warps elements, so every stage with partner distance j below the segment length stays inside one warp
+// and needs only __syncwarp; block barriers remain for the log2(warps) widest distances of each merge.
 template <class T>
 __device__ void block_bitonic(T *a, int n2) {
+    const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int seg = n2 / nw;
+    const bool local_ok = seg >= 32 && seg * nw == n2;
     for (int k = 2; k <= n2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
+            if (local_ok && j < seg) {
+                for (int i = w * seg + l; i < (w + 1) * seg; i += 32) {
+                    const int x = i ^ j;
+                    if (x > i) {
+                        const bool up = (i & k) == 0;
+                        const T p = a[i], q = a[x];
+                        if ((p > q) == up) { a[i] = q; a[x] = p; }
+                    }
+                }
+                __syncwarp();
+                continue;
+            }
+            __syncthreads();
             for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-                int x = i ^ j;
+                const int x = i ^ j;
                 if (x > i) {
-                    bool up = (i & k) == 0;
-                    T p = a[i], q = a[x];
+                    const bool up = (i & k) == 0;
+                    const T p = a[i], q = a[x];
                     if ((p > q) == up) { a[i] = q; a[x] = p; }
                 }
             }
             __syncthreads();
         }
     }
+    __syncthreads();
+}
+// block sum of doubles (all threads get the total); sh holds >= 32 doubles
+__device__ __forceinline__ double block_sum_f64(double v, double *sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CH_FULL, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) t += sh[i];
+    return t;
 }
 __device__ __forceinline__ int pow2ceil(int n) {
     int p = 1;
@@ -345,7 +376,7 @@ __global__ void k_bd_compose(BdArgs A, int nb) {
 // One block per label over the same points as the breakdown (sampled iterations, busy > 0) in (gpu,
 // iteration) order: duration and overlap-ratio quantiles at q = 0, .25, .5, .75, 1 (linear interpolation at
 // h = q (n - 1), R9) from block bitonic sorts, and the Pearson correlation of ratio with duration (two
-// sequential passes in point order, R10).  Row layout as oracle report.rows.
+// passes, means then centred sums, each a block reduction; R10).  Row layout as oracle report.rows.
 struct RepArgs {
     const int64_t *blk;
     int nslots;
@@ -406,20 +437,24 @@ __global__ void __launch_bounds__(512) k_report(RepArgs A) {
     if (n == 0) return;
     for (int i = threadIdx.x; i < n; i += blockDim.x) { sb[i] = b[i]; sr[i] = r[i]; }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double mb = 0.0, mr = 0.0;
-        for (int i = 0; i < n; i++) { mb += b[i]; mr += r[i]; }
-        mb /= (double)n;
-        mr /= (double)n;
-        double sxx = 0.0, syy = 0.0, sxy = 0.0;
-        for (int i = 0; i < n; i++) {
+    {
+        __shared__ double red[32];
+        double pb = 0.0, pr = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) { pb += b[i]; pr += r[i]; }
+        const double mb = block_sum_f64(pb, red) / (double)n;
+        const double mr = block_sum_f64(pr, red) / (double)n;
+        double pxx = 0.0, pyy = 0.0, pxy = 0.0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
             const double dx = r[i] - mr, dy = b[i] - mb;
-            sxx += dx * dx;
-            syy += dy * dy;
-            sxy += dx * dy;
+            pxx += dx * dx;
+            pyy += dy * dy;
+            pxy += dx * dy;
         }
-        out[11] = (sxx > 0.0 && syy > 0.0) ? sxy / sqrt(sxx * syy) : NAN;
-        out[13] = mb;
+        const double sxx = block_sum_f64(pxx, red), syy = block_sum_f64(pyy, red), sxy = block_sum_f64(pxy, red);
+        if (threadIdx.x == 0) {
+            out[11] = (sxx > 0.0 && syy > 0.0) ? sxy / sqrt(sxx * syy) : NAN;
+            out[13] = mb;
+        }
     }
     int n2 = 1;
     while (n2 < n) n2 <<= 1;

@@ -906,6 +906,89 @@ __global__ void __launch_bounds__(RC_NT, 3) k_sum_rows_chunked(TabView ch, const
     }
 }
 
+// Field-major children with several children per parent (instance -> layer): staged like
+// k_sum_rows_chunked, but the fold is split by (column, parent) so that all threads work -- thread task
+// (f, i) folds column f of parent i over its children in order (counter sums keep the sequential child
+// order); running values live in shared memory across chunks.  C <= 8.
+__global__ void __launch_bounds__(RC_NT, 3) k_sum_rows_cols(TabView ch, const int64_t *__restrict__ starts,
+                                                         const int64_t *__restrict__ ng_dev, int shift, int C,
+                                                         TabView pa, int PB) {
+    extern __shared__ int64_t rsm[];
+    const int NF = RF_NFIELDS + C;
+    int64_t *vals = rsm;                               // [NF][RC_CH]
+    int64_t *acc = rsm + NF * RC_CH;                   // [NF][PB]
+    __shared__ int64_t s_lo[RC_NT + 1];
+    const int tid = threadIdx.x;
+    const int64_t ng = *ng_dev;
+    for (int64_t p0 = (int64_t)blockIdx.x * PB; p0 < ng; p0 += (int64_t)gridDim.x * PB) {
+        const int np = (int)min((int64_t)PB, ng - p0);
+        __syncthreads();
+        for (int i = tid; i <= np; i += RC_NT) s_lo[i] = starts[p0 + i];
+        for (int t = tid; t < NF * np; t += RC_NT) {
+            const int f = t / np;
+            acc[f * PB + t % np] = f == RF_FIRST_IDX || f == RF_FIRST_KS ? INT64_MAX : f == RF_LAST_KE ? INT64_MIN : 0;
+        }
+        __syncthreads();
+        const int64_t c_lo = s_lo[0], c_hi = s_lo[np];
+        for (int64_t j0 = c_lo; j0 < c_hi; j0 += RC_CH) {
+            const int m = (int)min((int64_t)RC_CH, c_hi - j0);
+            if (tid < m) {
+                const int64_t c = j0 + tid;
+                int64_t x[RF_NFIELDS];
+#pragma unroll
+                for (int f = 0; f < RF_NFIELDS; f++) x[f] = __ldg(ch.f + (int64_t)f * ch.cap + c);
+                int64_t y[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) y[q] = q < C ? __double_as_longlong(__ldg(ch.cnt + (int64_t)q * ch.ccap + c * ch.crs)) : 0;
+#pragma unroll
+                for (int f = 0; f < RF_NFIELDS; f++) vals[f * RC_CH + tid] = x[f];
+#pragma unroll
+                for (int q = 0; q < 8; q++) if (q < C) vals[(RF_NFIELDS + q) * RC_CH + tid] = y[q];
+            }
+            __syncthreads();
+            for (int t = tid; t < NF * np; t += RC_NT) {
+                const int f = t / np, i = t - f * np;
+                if (f == RF_FIRST_IDX) continue;                  // folded with RF_FIRST_KS
+                const int64_t lo = max(s_lo[i], j0), hi = min(s_lo[i + 1], j0 + m);
+                if (lo >= hi) continue;
+                const int64_t *v = vals + f * RC_CH - j0;
+                int64_t &a = acc[f * PB + i];
+                if (f >= RF_NFIELDS) {
+                    double x = __longlong_as_double(a);
+                    for (int64_t c = lo; c < hi; c++) x += __longlong_as_double(v[c]);
+                    a = __double_as_longlong(x);
+                } else if (f == RF_LAST_KE) {
+                    int64_t x = a;
+                    for (int64_t c = lo; c < hi; c++) x = max(x, v[c]);
+                    a = x;
+                } else if (f == RF_FIRST_KS) {
+                    const int64_t *vi = vals + RF_FIRST_IDX * RC_CH - j0;
+                    int64_t ks = a, ix = acc[RF_FIRST_IDX * PB + i];
+                    for (int64_t c = lo; c < hi; c++)
+                        if (v[c] < ks || (v[c] == ks && vi[c] < ix)) { ks = v[c]; ix = vi[c]; }
+                    a = ks;
+                    acc[RF_FIRST_IDX * PB + i] = ix;
+                } else {
+                    int64_t x = a;
+                    for (int64_t c = lo; c < hi; c++) x += v[c];
+                    a = x;
+                }
+            }
+            __syncthreads();
+        }
+        for (int t = tid; t < NF * np; t += RC_NT) {
+            const int f = t / np, i = t - f * np;
+            const int64_t x = acc[f * PB + i];
+            if (f < RF_NFIELDS) pa.f[(int64_t)f * pa.cap + p0 + i] = x;
+            else pa.cnt[(int64_t)(f - RF_NFIELDS) * pa.ccap + p0 + i] = __longlong_as_double(x);
+        }
+        for (int i = tid; i < np; i += RC_NT) {
+            const unsigned long long k0 = s_lo[i + 1] > s_lo[i] ? ch.key[s_lo[i]] : 0ull;
+            pa.key[p0 + i] = shift >= 64 ? 0ull : ((k0 >> shift) << shift);
+        }
+    }
+}
+
 // identity columns of a row table: caller span indices, gpu, op label, iteration rank
 __global__ void k_decode(const unsigned long long *__restrict__ key, const int64_t *__restrict__ n_dev, KeyLayout L,
                          int depth,
@@ -1198,7 +1281,15 @@ static chopper_status sum_rows(chopper_ctx *ctx, const TabView &ch, const uint32
     const size_t shb = (size_t)(RF_NFIELDS + C) * RC_CH * 8;
     if (mode == 0 && shb > 160 * 1024) mode = 2;
     if (mode == 1 && C > 32) mode = 2;
-    if (mode == 0) {
+    if (mode == 0 && !perm && ch.rs == 1 && C <= 8 && fanout >= 2) {
+        const size_t shc = (size_t)(RF_NFIELDS + C) * (RC_CH + PB) * 8;
+        static size_t attr_c = 0;
+        if (shc > attr_c) {                   // (static + dynamic must fit the limit: always set it)
+            CH_CUDA(ctx, cudaFuncSetAttribute(k_sum_rows_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shc));
+            attr_c = shc;
+        }
+        k_sum_rows_cols<<<grid_for(ng_upper / fanout, PB), RC_NT, shc, ctx->st>>>(ch, starts, ng_dev, shift, C, pa, PB);
+    } else if (mode == 0) {
         static size_t attr = 0;
         if (shb > 48 * 1024 && shb > attr) {
             CH_CUDA(ctx, cudaFuncSetAttribute(k_sum_rows_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));

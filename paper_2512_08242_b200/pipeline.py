@@ -155,6 +155,45 @@ class Pipeline:
             self.ctx = chopper_create(self.cfg, self.device, self.stream.cuda_stream, self.comm, self.rank,
                                       self.nranks, self.scratch)
 
+    # ---- double-buffered streaming inputs ----
+    def input_set(self) -> dict:
+        """The device input buffers now in use, as a set `use_inputs` / `stage_inputs` accept."""
+        return {"d": self.d, "passes": self.passes_dev, "cpu": self.cpu}
+
+    def new_input_set(self) -> dict:
+        """A second device copy of the input buffers (same shapes), for streaming trace after trace: the next
+        trace's host->device copy runs on a copy stream while `run` computes on the other set."""
+        torch = self.torch
+        return {"d": {k: torch.empty_like(v) for k, v in self.d.items()},
+                "passes": [(g, torch.empty_like(nm), sl, torch.empty_like(v)) for (g, nm, sl, v) in self.passes_dev],
+                "cpu": None if self.cpu is None else {k: torch.empty_like(v) for k, v in self.cpu.items()}}
+
+    def stage_inputs(self, s: dict, pinned: dict, pinned_passes, pinned_cpu: Optional[dict], copy_stream):
+        """Enqueue the pinned-host -> device copies of one trace into set `s` on `copy_stream`; returns the
+        CUDA event that completes with them (pass it to `use_inputs`).  The caller guarantees that no
+        queued `run` still reads `s` (run returns after its status read-back, so the set used by the
+        previous, returned call is free)."""
+        torch = self.torch
+        with torch.cuda.stream(copy_stream):
+            for k, v in pinned.items():
+                s["d"][k].copy_(v, non_blocking=True)
+            for q, (nm, vals) in enumerate(pinned_passes):
+                s["passes"][q][1].copy_(nm, non_blocking=True)
+                s["passes"][q][3].copy_(vals, non_blocking=True)
+            if pinned_cpu:
+                for k, v in pinned_cpu.items():
+                    s["cpu"][k].copy_(v, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+        return ev
+
+    def use_inputs(self, s: dict, ready=None) -> None:
+        """Make `s` the input set of the next `run`; its compute stream waits for `ready` (a stage_inputs
+        event) on the device, the host does not block."""
+        if ready is not None:
+            self.stream.wait_event(ready)
+        self.d, self.passes_dev, self.cpu = s["d"], s["passes"], s["cpu"]
+
     # ---- run ----
     def run(self, params: dict, full: bool = False, check: bool = True) -> dict:
         """All six ABI calls.  full=True also writes the per-event outputs (parity mode)."""

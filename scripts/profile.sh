@@ -12,7 +12,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 python scripts/launches.py $OUT/launches.csv 4 40 > $OUT/launches.txt 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_events -s 3 -c 1 -f -o $OUT/prof_events \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/prof_events.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_counters_tiled|k_sum_rows_chunked" \
+ncu --set full --clock-control none --import-source on -k regex:"k_counters_tiled|k_sum_rows_chunked|k_sum_rows_cols" \
     -s 9 -c 3 -f -o $OUT/prof_tables \
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/prof_tables.log 2>&1
 ls -la $OUT

@@ -87,6 +87,47 @@ def test_tables_only_mode_matches_full():
         np.testing.assert_array_equal(np.nan_to_num(full[k]), np.nan_to_num(lean[k]), err_msg=k)
 
 
+@pytest.mark.parametrize("how", ["shuffled", "reversed_level"])
+def test_span_input_order(how):
+    """spans in any input order (fully shuffled, or each (gpu, level) list in start order but the lists
+    interleaved differently) give the oracle's span table and outputs."""
+    b = tracegen.generate(tracegen.config(1))
+    rng = np.random.default_rng(7)
+    if how == "shuffled":
+        perm = rng.permutation(len(b.span_gl))
+    else:                                   # lists interleaved in a new order, each still in start order
+        lv = (b.span_gl & 0xFF).astype(np.int64)
+        perm = np.lexsort((np.arange(len(lv)), -lv))
+    b2 = tracegen.dataclasses.replace(b, span_gl=b.span_gl[perm], span_start=b.span_start[perm],
+                                      span_end=b.span_end[perm], span_label=b.span_label[perm])
+    ref, got, res, pipe = run_both(b2)
+    _check_status(ref, got)
+    assert_parity(ref, got)
+
+
+def test_double_buffered_inputs():
+    """stage_inputs / use_inputs (the streaming e2e path): a run on the second input set, filled from pinned
+    host memory on a copy stream while the first set is clobbered, gives the same tables."""
+    import torch
+    import paper_2512_08242_b200 as ch
+    b = tracegen.generate(tracegen.config(1))
+    p = oracle.default_params(b)
+    pipe = ch.Pipeline(b.cfg.n_gpus, len(b.labels), 16, 4096)
+    pipe.upload(b, b.n_counters)
+    want = pipe.to_numpy(pipe.run(p, full=False), len(p["ratio_num"]))
+    a, s2 = pipe.input_set(), pipe.new_input_set()
+    pinned = {k: v.cpu().pin_memory() for k, v in a["d"].items()}
+    pp = [(nm.cpu().pin_memory(), vals.cpu().pin_memory()) for (_, nm, _, vals) in a["passes"]]
+    cs = torch.cuda.Stream()
+    ready = pipe.stage_inputs(s2, pinned, pp, None, cs)
+    for v in a["d"].values():
+        v.zero_()
+    pipe.use_inputs(s2, ready)
+    got = pipe.to_numpy(pipe.run(p, full=False), len(p["ratio_num"]))
+    for k in want:
+        np.testing.assert_array_equal(np.nan_to_num(want[k]), np.nan_to_num(got[k]), err_msg=k)
+
+
 # ---------------------------------------------------------------------------
 # edge cases
 # ---------------------------------------------------------------------------
