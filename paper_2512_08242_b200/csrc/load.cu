@@ -360,8 +360,10 @@ __global__ void __launch_bounds__(LN_NT) k_lean_chain(const uint32_t *__restrict
     // the predecessor's start / end: from global memory for the thread's first compute event, then registers
     int64_t p_ks = 0, p_ke = 0;
     if (before >= 0 && cp > 0) { p_ks = ks[before]; p_ke = ke[before]; }
+    int64_t pes[LN_IPT];                  // chain ends (CH_NONE_TS at non-compute events: never read there)
 #pragma unroll
     for (int k = 0; k < LN_IPT; k++) {
+        pes[k] = CH_NONE_TS;
         if (k >= nv) break;
         const int64_t i = i0 + k;
         const uint32_t m = mt[k];
@@ -379,11 +381,20 @@ __global__ void __launch_bounds__(LN_NT) k_lean_chain(const uint32_t *__restrict
                 if (vs[k] < p_ks) atomicOr(nonmono, 1u);          // not start-monotone: the full path sorts it
                 if (vs[k] < pe) viol(rep, CV_STREAM_OVERLAP, i);
             }
-            pred_end[i] = pe;
+            pes[k] = pe;
             before = i;
             p_ks = vs[k];
             p_ke = ve[k];
         }
+    }
+    if (nv == LN_IPT && (((uintptr_t)(pred_end + i0)) & 15u) == 0) {
+#pragma unroll
+        for (int h = 0; h < LN_IPT / 2; h++)
+            reinterpret_cast<longlong2 *>(pred_end + i0)[h] = make_longlong2(pes[2 * h], pes[2 * h + 1]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < LN_IPT; k++)
+            if (k < nv && kind_of(mt[k]) == CK_COMPUTE) pred_end[i0 + k] = pes[k];
     }
 }
 
