@@ -235,7 +235,7 @@ struct KeyMeta {  // partition digit: bucket = lg * NG + dense group (a2 fast pa
 };
 
 template <class KS>
-__global__ void __launch_bounds__(RX_NT) k_rx_upsweep(KS ks, int64_t n, unsigned int *__restrict__ counts,
+__global__ void __launch_bounds__(RX_NT) k_rx_upsweep(KS ks, int64_t n, int64_t *__restrict__ counts,
                                                       int64_t ntile) {
     __shared__ unsigned int h[256];
     h[threadIdx.x] = 0;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(RX_NT) k_rx_upsweep(KS ks, int64_t n, unsigned
         if (i < n) atomicAdd(&h[ks.digit(i)], 1u);
     }
     __syncthreads();
-    counts[(int64_t)threadIdx.x * ntile + blockIdx.x] = h[threadIdx.x];
+    counts[(int64_t)threadIdx.x * ntile + blockIdx.x] = (int64_t)h[threadIdx.x];   // (int64: scanned directly)
 }
 
 template <class KS, bool HAS_KEYS, bool HAS_VALS>
@@ -316,10 +316,6 @@ __global__ void __launch_bounds__(RX_NT) k_rx_downsweep(KS ks, const unsigned lo
         if (HAS_KEYS) keys_out[pos] = sk[j];
         vals_out[pos] = sv[j];
     }
-}
-__global__ void k_u32_to_i64(const unsigned int *a, int64_t *b, int64_t n) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) b[i] = a[i];
 }
 }  // namespace
 
@@ -398,7 +394,6 @@ chopper_status ch_radix_sort(chopper_ctx *ctx, unsigned long long *keys, uint32_
     int64_t ntile = ceil_div(n, RX_TILE);
     size_t mark = ctx->used;
     CH_ALLOC_BEGIN;
-    unsigned int *counts = CH_ALLOC(ctx, unsigned int, 256 * ntile);
     int64_t *cnt64 = CH_ALLOC(ctx, int64_t, 256 * ntile);
     int64_t *offs = CH_ALLOC(ctx, int64_t, 256 * ntile);
     CH_ALLOC_END(ctx);
@@ -407,9 +402,7 @@ chopper_status ch_radix_sort(chopper_ctx *ctx, unsigned long long *keys, uint32_
     bool alt = false;
     for (int b = bit_lo; b < bit_hi; b += 8) {
         KeyArr ks{ki, b};
-        k_rx_upsweep<KeyArr><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, n, counts, ntile);
-        CH_LAUNCHED(ctx);
-        k_u32_to_i64<<<(unsigned)ceil_div(256 * ntile, 256), 256, 0, ctx->st>>>(counts, cnt64, 256 * ntile);
+        k_rx_upsweep<KeyArr><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, n, cnt64, ntile);
         CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, cnt64, offs, 256 * ntile, nullptr));
         k_rx_downsweep<KeyArr, true, true><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, ki, vi, n, offs, ntile, ko, vo);
@@ -430,14 +423,11 @@ chopper_status ch_radix_partition_meta(chopper_ctx *ctx, const uint32_t *meta, c
     int64_t ntile = ceil_div(n, RX_TILE);
     size_t mark = ctx->used;
     CH_ALLOC_BEGIN;
-    unsigned int *counts = CH_ALLOC(ctx, unsigned int, 256 * ntile);
     int64_t *cnt64 = CH_ALLOC(ctx, int64_t, 256 * ntile);
     int64_t *offs = CH_ALLOC(ctx, int64_t, 256 * ntile);
     CH_ALLOC_END(ctx);
     KeyMeta ks{meta, gpu_lg, NG, other_group};
-    k_rx_upsweep<KeyMeta><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, n, counts, ntile);
-    CH_LAUNCHED(ctx);
-    k_u32_to_i64<<<(unsigned)ceil_div(256 * ntile, 256), 256, 0, ctx->st>>>(counts, cnt64, 256 * ntile);
+    k_rx_upsweep<KeyMeta><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, n, cnt64, ntile);
     CH_LAUNCHED(ctx);
     CH_TRY(ch_scan_excl_i64(ctx, cnt64, offs, 256 * ntile, nullptr));
     k_rx_downsweep<KeyMeta, false, false><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, nullptr, nullptr, n, offs, ntile,
