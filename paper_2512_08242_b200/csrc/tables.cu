@@ -25,7 +25,7 @@ constexpr int NT = 256;
 // pass also checks every value it reads -- the slot's column at every non-MEMOP event of the gpu,
 // i.e. the whole column -- for finiteness (R8), so a counter pass is read once.  Slot groups of CT_SG
 // are processed in turn by the same block (the tile's event metadata is read once).
-constexpr int CT_NT = 256, CT_IPT = 8, CT_TILE = CT_NT * CT_IPT, CT_SG = 4, CT_WARPS = CT_NT / 32;
+constexpr int CT_NT = 256, CT_IPT = 8, CT_TILE = CT_NT * CT_IPT, CT_SG = 4, CT_WARPS = CT_NT / 32, CT_CP = 128;
 // staged element j (tile-relative rank) lives at j ^ ((j >> 4) & 7): the 32 lanes of a warp read
 // elements 8 apart (one per thread-blocked event), which this spreads over all banks (2 wavefronts)
 __device__ __forceinline__ int ct_sw(int j) { return j ^ ((j >> 4) & 7); }
@@ -34,6 +34,7 @@ struct CtSmem {
     double agg[CT_WARPS][CT_SG], carry[CT_WARPS][CT_SG];
     int aflag[CT_WARPS];
     int red[4][CT_WARPS];
+    const double *cp[CT_CP];                  // column pointers [lg][slot], loaded beside the metadata
 };
 __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__restrict__ meta,
                                                           const int32_t *__restrict__ run_id,
@@ -41,10 +42,13 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
                                                           const int32_t *__restrict__ gpu_lg,
                                                           const double *const *__restrict__ col, int C,
                                                           int64_t N, double *__restrict__ out, int64_t cap,
-                                                          unsigned int *__restrict__ colbad, int vec_ok) {
+                                                          unsigned int *__restrict__ colbad, int vec_ok,
+                                                          int n_lg) {
     extern __shared__ __align__(16) unsigned char ct_dsm[];
     CtSmem &S = *reinterpret_cast<CtSmem *>(ct_dsm);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool cp_sm = n_lg * C <= CT_CP;     // (visible after the range reduction's barrier)
+    if (cp_sm && tid < n_lg * C) S.cp[tid] = col[tid];
     const int64_t base = (int64_t)blockIdx.x * CT_TILE, i0 = base + (int64_t)tid * CT_IPT;
     const int nv = i0 >= N ? 0 : (int)min((int64_t)CT_IPT, N - i0);
     uint32_t mt[CT_IPT];
@@ -108,7 +112,7 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
         if (staged) {
 #pragma unroll
             for (int q = 0; q < CT_SG; q++) {
-                const double *cp = s0 + q < C ? col[lmin * C + s0 + q] : nullptr;
+                const double *cp = s0 + q < C ? (cp_sm ? S.cp[lmin * C + s0 + q] : col[lmin * C + s0 + q]) : nullptr;
                 if (cp) {
                     cpm |= 1u << q;
                     for (int j = tid; j < ncnt; j += CT_NT) cp_async8(&S.x[q][ct_sw(j)], cp + nlo + j);
@@ -1049,15 +1053,18 @@ __device__ void points_iter_one(TabView iv, const int64_t *__restrict__ its, int
                                 int C, int64_t *__restrict__ df, double *__restrict__ dc,
                                 int64_t *__restrict__ dvalid, unsigned int *__restrict__ ovf) {
     // one instance per thread per chunk; a stable counting sort by label puts each label's instances of
-    // the chunk in a contiguous list (instance order), which thread `label` then folds
+    // the chunk in a contiguous list (instance order), which the block then folds split by (column, label):
+    // task (f, l) folds column f of label l's list in order (running values in shared memory)
     extern __shared__ int64_t psm[];
     const int NF = RF_NFIELDS + C;
     int64_t *vals = psm;                                                      // [NF][PT_CH]
-    double *cacc = reinterpret_cast<double *>(vals + (int64_t)NF * PT_CH);    // [nL][C]
-    int32_t *lab = reinterpret_cast<int32_t *>(cacc + (int64_t)nL * C);       // [PT_CH]
+    int64_t *pacc = vals + (int64_t)NF * PT_CH;                               // [NF][nL] running values
+    int32_t *lab = reinterpret_cast<int32_t *>(pacc + (int64_t)NF * nL);      // [PT_CH]
     int32_t *order = lab + PT_CH;                                             // [PT_CH]
     int32_t *wc = order + PT_CH;                                              // [8][nL] per-warp counts
     int32_t *lstart = wc + 8 * nL;                                            // [nL]
+    int32_t *ltot = lstart + nL;                                              // [nL] chunk list length
+    int32_t *lcnt = ltot + nL;                                                // [nL] instances folded
     __shared__ int64_t scan_sm[33];
     const int64_t a = its[g], b = its[g + 1];
     const unsigned long long k0 = iv.key[a];
@@ -1066,10 +1073,11 @@ __device__ void points_iter_one(TabView iv, const int64_t *__restrict__ its, int
     const int64_t opb = list_beg[lg * 4 + 3];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const int64_t cells = (int64_t)nL * n_lg * R0;
-    RowAcc acc;
-    acc.zero();
-    int cnt_n = 0;
-    for (int q = tid; q < nL * C; q += blockDim.x) cacc[q] = 0.0;
+    for (int t = tid; t < NF * nL; t += blockDim.x) {
+        const int f = t / nL;
+        pacc[t] = f == RF_FIRST_IDX || f == RF_FIRST_KS ? INT64_MAX : f == RF_LAST_KE ? INT64_MIN : 0;
+    }
+    for (int q = tid; q < nL; q += blockDim.x) lcnt[q] = 0;
     for (int64_t j0 = a; j0 < b; j0 += PT_CH) {
         const int m = (int)min((int64_t)PT_CH, b - j0);
         if (tid < m) {           // PT_CH == blockDim: thread t loads instance j0 + t, all loads in flight first
@@ -1106,30 +1114,47 @@ __device__ void points_iter_one(TabView iv, const int64_t *__restrict__ its, int
         }
         int64_t dummy;
         const int st = (int)block_excl_sum<256>(tid < nL ? tot_l : 0, &dummy, scan_sm);
-        if (tid < nL) lstart[tid] = st;
+        if (tid < nL) { lstart[tid] = st; ltot[tid] = tot_l; lcnt[tid] += tot_l; }
         __syncthreads();
         if (l >= 0) order[lstart[l] + wc[w * nL + l] + inrank] = tid;
         __syncthreads();
-        if (tid < nL) {
-            for (int k = st; k < st + tot_l; k++) {
-                const int t = order[k];
-                int64_t x[RF_NFIELDS];
-#pragma unroll
-                for (int f = 0; f < RF_NFIELDS; f++) x[f] = vals[f * PT_CH + t];
-                acc.merge(x);
-                for (int s2 = 0; s2 < C; s2++)
-                    cacc[tid * C + s2] += __longlong_as_double(vals[(RF_NFIELDS + s2) * PT_CH + t]);
+        for (int t = tid; t < NF * nL; t += blockDim.x) {
+            const int f = t / nL, lb = t - f * nL;
+            const int c0 = lstart[lb], c1 = c0 + ltot[lb];
+            if (f == RF_FIRST_IDX || c0 == c1) continue;              // (FIRST_IDX folds with FIRST_KS)
+            const int64_t *v = vals + f * PT_CH;
+            if (f >= RF_NFIELDS) {
+                double x = __longlong_as_double(pacc[t]);
+                for (int k = c0; k < c1; k++) x += __longlong_as_double(v[order[k]]);
+                pacc[t] = __double_as_longlong(x);
+            } else if (f == RF_LAST_KE) {
+                int64_t x = pacc[t];
+                for (int k = c0; k < c1; k++) x = max(x, v[order[k]]);
+                pacc[t] = x;
+            } else if (f == RF_FIRST_KS) {
+                const int64_t *vi = vals + RF_FIRST_IDX * PT_CH;
+                int64_t ks = pacc[t], ix = pacc[RF_FIRST_IDX * nL + lb];
+                for (int k = c0; k < c1; k++) {
+                    const int o = order[k];
+                    if (v[o] < ks || (v[o] == ks && vi[o] < ix)) { ks = v[o]; ix = vi[o]; }
+                }
+                pacc[t] = ks;
+                pacc[RF_FIRST_IDX * nL + lb] = ix;
+            } else {
+                int64_t x = pacc[t];
+                for (int k = c0; k < c1; k++) x += v[order[k]];
+                pacc[t] = x;
             }
-            cnt_n += tot_l;
         }
         __syncthreads();
     }
-    if (tid < nL && cnt_n > 0) {
-        const int64_t cell = ((int64_t)tid * n_lg + lg) * R0 + rank;
-#pragma unroll
-        for (int f = 0; f < RF_NFIELDS; f++) df[(int64_t)f * cells + cell] = acc.v[f];
-        for (int s2 = 0; s2 < C; s2++) dc[(int64_t)s2 * cells + cell] = cacc[tid * C + s2];
-        dvalid[cell] = 1;
+    for (int t = tid; t < NF * nL; t += blockDim.x) {
+        const int f = t / nL, lb = t - f * nL;
+        if (lcnt[lb] == 0) continue;
+        const int64_t cell = ((int64_t)lb * n_lg + lg) * R0 + rank;
+        if (f < RF_NFIELDS) df[(int64_t)f * cells + cell] = pacc[t];
+        else dc[(int64_t)(f - RF_NFIELDS) * cells + cell] = __longlong_as_double(pacc[t]);
+        if (f == 0) dvalid[cell] = 1;
     }
 }
 
@@ -1362,7 +1387,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[0], ctx->fork_ev, 0));
         k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->side[0]>>>(
             ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, ctx->N, subv.cnt, subv.ccap,
-            ctx->d_colbad, vec_ok);
+            ctx->d_colbad, vec_ok, n_lg);
         CH_LAUNCHED(ctx);
         CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[0], ctx->side[0]));
         counters_forked = true;
@@ -1464,7 +1489,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
             *ovf_out = ovf;
             CH_CUDA(ctx, cudaMemsetAsync(dvalid, 0, 8 * (size_t)cells, ctx->st));
             CH_CUDA(ctx, cudaMemsetAsync(ovf, 0, 4, ctx->st));
-            size_t shb = (size_t)(RF_NFIELDS + C) * PT_CH * 8 + (size_t)nL * C * 8 + 4 * (2 * PT_CH + 9 * (size_t)nL);
+            size_t shb = (size_t)(RF_NFIELDS + C) * (PT_CH + nL) * 8 + 4 * (2 * PT_CH + 11 * (size_t)nL);
             static size_t attr_shb = 0;
             if (shb > 48 * 1024 && shb > attr_shb) {
                 CH_CUDA(ctx, cudaFuncSetAttribute(k_points_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
