@@ -163,12 +163,22 @@ __global__ void k_chunk_stack(const int64_t *__restrict__ Pe, const int32_t *__r
     cmax[c] = sp > 0 ? se[0] : INT64_MIN;   // bottom of the final stack = max end of the last list
 }
 
-__global__ void k_sparse_level(const int64_t *__restrict__ prev, int64_t *__restrict__ next, int64_t nch, int64_t w) {
+// up to 3 sparse-table levels per launch: level k-1+g (g = 1..ng) at c is the max of level k-1 at
+// c - m w, m < 2^g (w = 2^(k-1)), so one launch reads 2^ng entries of level k-1 and writes ng levels
+__global__ void k_sparse_levels(const int64_t *__restrict__ prev, int64_t *__restrict__ next, int64_t nch, int64_t w,
+                                int ng) {
     int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nch) return;
-    int64_t a = prev[c];
-    int64_t b = c - w >= 0 ? prev[c - w] : INT64_MIN;
-    next[c] = a > b ? a : b;
+    int64_t v[8];
+#pragma unroll
+    for (int m = 0; m < 8; m++) v[m] = (m < (1 << ng) && c - m * w >= 0) ? prev[c - m * w] : INT64_MIN;
+    int64_t mx = v[0];
+#pragma unroll
+    for (int g = 1; g <= 3; g++) {
+        if (g > ng) break;
+        for (int m = 1 << (g - 1); m < (1 << g); m++) mx = v[m] > mx ? v[m] : mx;
+        next[(int64_t)(g - 1) * nch + c] = mx;
+    }
 }
 
 __global__ void k_resolve(const int64_t *__restrict__ Pe, const int32_t *__restrict__ Plist, int64_t S,
@@ -551,9 +561,11 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         k_chunk_stack<<<(unsigned)ceil_div(nch, 64), 64, 0, ctx->st>>>(ctx->P_end, Plist, SL, ctx->P_parent, cstack, csp,
                                                                       sparse, ctx->d_list_beg);
         CH_LAUNCHED(ctx);
-        for (int k = 1; k < levels; k++) {
-            k_sparse_level<<<(unsigned)ceil_div(nch, NT), NT, 0, ctx->st>>>(sparse + (int64_t)(k - 1) * nch,
-                                                                            sparse + (int64_t)k * nch, nch, 1ll << (k - 1));
+        for (int k = 1; k < levels; k += 3) {
+            const int ng = std::min(3, levels - k);
+            k_sparse_levels<<<(unsigned)ceil_div(nch, NT), NT, 0, ctx->st>>>(sparse + (int64_t)(k - 1) * nch,
+                                                                             sparse + (int64_t)k * nch, nch,
+                                                                             1ll << (k - 1), ng);
             CH_LAUNCHED(ctx);
         }
         unsigned g = (unsigned)ceil_div(SL, NT);
