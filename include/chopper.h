@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define CHOPPER_ABI_VERSION 7
+#define CHOPPER_ABI_VERSION 8
 
 typedef struct chopper_ctx chopper_ctx;
 typedef int32_t chopper_status;
@@ -206,7 +206,8 @@ typedef struct {
 size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_t n_spans, int64_t n_samples,
                              int32_t n_counters);
 
-/* nccl_comm: ncclComm_t of the process group (borrowed), NULL when nranks == 1.
+/* nccl_comm: ncclComm_t of the process group (borrowed), NULL when nranks == 1 (or when a transport is
+ * installed with chopper_set_allgather before chopper_align).
  * cuda_stream: cudaStream_t (borrowed), NULL = legacy default stream. */
 chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int device, void *cuda_stream,
                               void *nccl_comm, int rank, int nranks, void *scratch, size_t scratch_bytes);
@@ -236,12 +237,20 @@ chopper_status chopper_attribute(chopper_ctx *ctx, int32_t *span_idx);
 chopper_status chopper_overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_ns, int64_t *call_ns,
                                int64_t *phi, int64_t *psi);
 
-/* a9 segmented reductions + roll-ups, a10 gap decomposition over this
- * rank's points.  Fills *out with device table pointers.  Synchronizes. */
+/* a9 segmented reductions + roll-ups (instance -> layer -> phase -> iteration -> GPU, points summed across
+ * layers) and a10 gap decomposition (Eqs. 4-8 plus the launch term,
+ * PAPER.md:727-791; D14-D20) over this rank's points.  p: host parameters (read during the call).
+ * Fills *out with device table pointers into the ctx scratch (valid until the next chopper_load_columns).
+ * Errors: slot / ratio indices out of range -> CHOPPER_E_INVALID_ARG; iteration rank >= max_iters or op label
+ * >= n_labels -> CHOPPER_E_RANGE (latched, reported by chopper_reduce_ranks).  Synchronizes. */
 chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, chopper_tables *out);
 
-/* a11: NCCL all-gather #2 of per-gpu rows, then global composition
- * (throughput, medians, global breakdown).  Synchronizes. */
+/* a11: all-gather #2 of the dense per-gpu rows (NCCL or the chopper_set_allgather transport), then the global
+ * composition every rank computes in the same fixed order: per-iteration T = max over GPUs of busy + launch,
+ * throughput b*s*R / T and its median over sampled iterations, the
+ * breakdown over all GPUs' points, clock offsets and collective skew (D13), report
+ * statistics.  out: host struct, overwritten.  Errors: more than 4096 iterations / 256 breakdown rows or
+ * labels -> CHOPPER_E_RANGE; a peer rank failed earlier in the step -> CHOPPER_E_STATE.  Synchronizes. */
 chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out);
 
 /* Per-GPU overlap CDFs of every op label (report statistics; Fig. 7;
@@ -325,6 +334,35 @@ typedef struct {
 chopper_status chopper_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *samples, const int32_t *topology,
                                 int32_t n_logical, int64_t *c_active, double *c_min, int64_t cap,
                                 chopper_cpu_summary *out);
+
+/* Cross-rank exchange transport.  By default the two exchange steps -- all-gather #1 of the
+ * collective-end vectors inside chopper_align (clock offsets, D13) and all-gather #2 of the dense per-GPU row
+ * blocks inside chopper_reduce_ranks (throughput takes the max over GPUs, the breakdown
+ * medians pool all GPUs) -- are one ncclAllGather each on the ctx stream over the borrowed nccl_comm.
+ * chopper_set_allgather replaces that call for this ctx: fn(user, send, recv, bytes_per_rank, rank, nranks,
+ * cuda_stream) must leave in DEVICE recv[r * bytes_per_rank ...] the send block of rank r for every r, ordered
+ * after the work already enqueued on cuda_stream, and return 0 (non-zero -> CHOPPER_E_NCCL).  fn = NULL restores
+ * NCCL.  With a transport set, chopper_create's nccl_comm may be NULL for nranks > 1.
+ *
+ * Failure protocol (nranks > 1): every rank makes all six trace calls of a step in order, even after one of
+ * them failed.  A call made after this rank's failure does no work and returns CHOPPER_E_STATE, but
+ * chopper_align and chopper_reduce_ranks still take part in their all-gather with a block marked failed, so
+ * no rank waits forever; a rank that receives such a block returns CHOPPER_E_STATE from that call ("a peer
+ * rank failed"), and so do its later calls of the step.  chopper_load_columns starts a new step. */
+typedef int32_t (*chopper_allgather_fn)(void *user, const void *send, void *recv, size_t bytes_per_rank,
+                                        int32_t rank, int32_t nranks, void *cuda_stream);
+chopper_status chopper_set_allgather(chopper_ctx *ctx, chopper_allgather_fn fn, void *user);
+
+/* In-process loopback transport: nranks contexts on one device, each driven by its own host thread (tests
+ * run P = 1/2/4/8 ranks on one GPU this way and require identical chopper_global results).  Pass
+ * chopper_loopback_allgather and the group as chopper_set_allgather's fn / user.  The all-gather synchronizes
+ * the caller's stream, waits until all nranks threads arrived (60 s limit -> returns non-zero), copies every
+ * rank's send block device-to-device into recv, synchronizes again and waits for all ranks to finish copying.
+ * create returns NULL for nranks outside 1..256; destroy frees the group (no thread may be inside it). */
+void *chopper_loopback_create(int32_t nranks);
+void chopper_loopback_destroy(void *group);
+int32_t chopper_loopback_allgather(void *group, const void *send, void *recv, size_t bytes_per_rank, int32_t rank,
+                                   int32_t nranks, void *cuda_stream);
 
 /* report of the last chopper_load_columns (host copy) */
 chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out);

@@ -148,7 +148,9 @@ EXPORTS = ["chopper_scratch_bytes", "chopper_create", "chopper_load_columns", "c
            "chopper_status_sync", "chopper_last_error", "chopper_destroy", "chopper_kernel_launches",
            "chopper_abi_version", "chopper_pass_mismatch", "chopper_pass_conflict", "chopper_counter_present",
            "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time", "chopper_report_cdf",
-           "chopper_cpu_util", "chopper_set_metrics", "chopper_ingest_scratch_bytes", "chopper_ingest_chrome"]
+           "chopper_cpu_util", "chopper_set_metrics", "chopper_ingest_scratch_bytes", "chopper_ingest_chrome",
+           "chopper_set_allgather", "chopper_loopback_create", "chopper_loopback_destroy",
+           "chopper_loopback_allgather"]
 
 _lib = None
 
@@ -192,6 +194,10 @@ def load_library() -> ctypes.CDLL:
                                         ctypes.POINTER(chopper_ingest_report)]),
         "chopper_cpu_util": (I32, [P, ctypes.POINTER(chopper_cpu_samples), P, I32, P, P, I64,
                                    ctypes.POINTER(chopper_cpu_summary)]),
+        "chopper_set_allgather": (I32, [P, P, P]),
+        "chopper_loopback_create": (P, [I32]),
+        "chopper_loopback_destroy": (None, [P]),
+        "chopper_loopback_allgather": (I32, [P, P, P, ctypes.c_size_t, I32, I32, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -270,6 +276,28 @@ def chopper_report_cdf(ctx) -> np.ndarray:
     if n.value > 0:
         _check(ctx, lib.chopper_report_cdf(ctx, out.ctypes.data, n.value, ctypes.byref(n)), "chopper_report_cdf")
     return out[:n.value]
+
+
+class LoopbackGroup:
+    """In-process all-gather transport for `nranks` contexts on one device (chopper_loopback_*): each rank's
+    Pipeline runs in its own host thread; used to run P = 1/2/4/8 ranks on one GPU."""
+
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        self.handle = load_library().chopper_loopback_create(nranks)
+        if not self.handle:
+            raise ValueError(f"bad loopback group size {nranks}")
+
+    def close(self):
+        if self.handle:
+            load_library().chopper_loopback_destroy(self.handle)
+            self.handle = None
+
+
+def chopper_set_allgather_loopback(ctx, group: LoopbackGroup) -> None:
+    lib = load_library()
+    fn = ctypes.cast(lib.chopper_loopback_allgather, P)
+    _check(ctx, lib.chopper_set_allgather(ctx, fn, group.handle), "chopper_set_allgather")
 
 
 def chopper_get_report(ctx) -> chopper_report:

@@ -368,6 +368,12 @@ __global__ void k_skew(const int64_t *__restrict__ all, int nslots, int64_t W, i
 }  // namespace
 
 chopper_status ch_nccl_allgather(chopper_ctx *ctx, const void *send, void *recv, size_t bytes_per_rank) {
+    if (ctx->ag_fn) {
+        int32_t r = ctx->ag_fn(ctx->ag_user, send, recv, bytes_per_rank, ctx->rank, ctx->nranks, (void *)ctx->st);
+        if (r != 0) return ch_fail(ctx, CHOPPER_E_NCCL, "all-gather transport failed: " + std::to_string(r));
+        return CHOPPER_OK;
+    }
+    if (!ctx->nccl) return ch_fail(ctx, CHOPPER_E_NCCL, "nranks > 1 without an NCCL communicator or a transport");
     typedef int (*fn_t)(const void *, void *, size_t, int, void *, cudaStream_t);
     static fn_t fn = nullptr;
     if (!fn) {
@@ -615,6 +621,7 @@ chopper_status ch_offsets_launch(chopper_ctx *ctx) {
     CH_CUDA(ctx, cudaMemsetAsync(mskew, 0, 16, ctx->st));
     // NCCL all-gather #1: every rank's collective-end vectors (D13)
     if (ctx->nranks > 1) {
+        ctx->x_exchanged = true;       // this rank took part (even if the transport reports an error)
         CH_TRY(ch_nccl_allgather(ctx, ctx->d_xsend, all, sizeof(int64_t) * slots * W));
     } else {
         CH_CUDA(ctx, cudaMemcpyAsync(all, ctx->d_xsend, 8 * slots * W, cudaMemcpyDeviceToDevice, ctx->st));
@@ -650,6 +657,10 @@ chopper_status ch_offsets_finish(chopper_ctx *ctx) {
     for (int b = 0; b < nslots; b++)
         if (ctx->off_hdr[2 * (size_t)b + 1]) ctx->gpu_present[ctx->off_hdr[2 * (size_t)b]] = 1;
     for (int g = 0; g < G; g++) if (!ctx->gpu_present[g]) { ctx->delta_flag[g] = 1; ctx->delta[g] = 0; }
+    // a slot whose gpu field is -1 is a failed rank's block (ch_exchange_poison): the step is dead everywhere
+    for (int b = 0; b < nslots; b++)
+        if (ctx->off_hdr[2 * (size_t)b] == -1)
+            return ch_fail(ctx, CHOPPER_E_STATE, "a peer rank failed earlier in this step (all-gather #1)");
     ctx->max_skew[0] = (int64_t)ctx->off_hs[0];
     ctx->max_skew[1] = (int64_t)ctx->off_hs[1];
     if (ctx->off_ovf) return ch_fail(ctx, CHOPPER_E_RANGE, "more collectives per class than max_coll_per_class");
@@ -657,3 +668,25 @@ chopper_status ch_offsets_finish(chopper_ctx *ctx) {
 }
 
 chopper_status ch_offsets(chopper_ctx *ctx) { return ch_offsets_finish(ctx); }
+
+// failure protocol (chopper.h): a rank that failed still makes this step's missing all-gather, with a block of
+// the shape every healthy rank sends (derived from chopper_config, nranks and n_counters only) whose first slot
+// header carries gpu = -1.  The step's scratch content is dead, so the blocks reuse the arena from mark_base.
+chopper_status ch_exchange_poison(chopper_ctx *ctx, int which) {
+    if (ctx->nranks <= 1) return CHOPPER_OK;
+    if (which == 1 ? ctx->x_exchanged : ctx->d_exchanged) return CHOPPER_OK;
+    const int slots = (int)ceil_div(ctx->cfg.n_traced_gpus, ctx->nranks);
+    const int64_t W = which == 1 ? 4 + 4 * (int64_t)std::max(1, ctx->cfg.max_coll_per_class) : ch_dense_width(ctx);
+    ctx->used = ctx->mark_base;
+    CH_ALLOC_BEGIN;
+    int64_t *send = CH_ALLOC(ctx, int64_t, (int64_t)slots * W);
+    int64_t *recv = CH_ALLOC(ctx, int64_t, (int64_t)slots * W * ctx->nranks);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemsetAsync(send, 0, 8 * (size_t)slots * W, ctx->st));
+    static const int64_t failed = -1;
+    CH_CUDA(ctx, cudaMemcpyAsync(send, &failed, 8, cudaMemcpyHostToDevice, ctx->st));
+    if (which == 1) ctx->x_exchanged = true; else ctx->d_exchanged = true;
+    CH_TRY(ch_nccl_allgather(ctx, send, recv, sizeof(int64_t) * (size_t)slots * W));
+    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    return CHOPPER_OK;
+}

@@ -2,11 +2,50 @@
 // status latching.  Every compute step runs in the kernels of this directory.
 #include "common.cuh"
 
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+
 chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &msg) {
     ctx->err = msg;
     ctx->latched_host |= 1u << s;
     return s;
 }
+
+// failure protocol (chopper.h): remember this rank's first failure of the step (several ranks only)
+static chopper_status step(chopper_ctx *ctx, chopper_status s) {
+    if (s != CHOPPER_OK && ctx->nranks > 1 && ctx->poison == CHOPPER_OK) ctx->poison = s;
+    return s;
+}
+// a call made after this rank's failure: no work, E_STATE (keeps the first error's message)
+static chopper_status dead_call(chopper_ctx *ctx) {
+    ctx->latched_host |= 1u << CHOPPER_E_STATE;
+    if (ctx->err.empty()) ctx->err = "call after a failed call of this step";
+    return CHOPPER_E_STATE;
+}
+
+// in-process loopback transport (chopper_loopback_*): a generation barrier over the group's threads
+namespace {
+struct LoopGroup {
+    int n = 0;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    int64_t gen = 0;
+    std::vector<const void *> send;
+};
+bool loop_barrier(LoopGroup *g) {
+    std::unique_lock<std::mutex> lk(g->m);
+    const int64_t my = g->gen;
+    if (++g->arrived == g->n) {
+        g->arrived = 0;
+        g->gen++;
+        g->cv.notify_all();
+        return true;
+    }
+    return g->cv.wait_for(lk, std::chrono::seconds(60), [&] { return g->gen != my; });
+}
+}  // namespace
 
 extern "C" {
 
@@ -35,7 +74,7 @@ chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int 
                               void *nccl_comm, int rank, int nranks, void *scratch, size_t scratch_bytes) {
     if (!out || !cfg || !scratch) return CHOPPER_E_INVALID_ARG;
     if (cfg->n_traced_gpus <= 0 || cfg->n_traced_gpus > CH_MAX_GPUS || cfg->n_labels < 0 || cfg->max_iters <= 0 ||
-        cfg->max_coll_per_class < 0 || nranks <= 0 || rank < 0 || rank >= nranks || (nranks > 1 && !nccl_comm))
+        cfg->max_coll_per_class < 0 || nranks <= 0 || rank < 0 || rank >= nranks)
         return CHOPPER_E_INVALID_ARG;
     chopper_ctx *c = new chopper_ctx();
     c->cfg = *cfg;
@@ -65,9 +104,20 @@ chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int 
     return CHOPPER_OK;
 }
 
+static chopper_status load_columns(chopper_ctx *ctx, const chopper_events *ev, const chopper_spans *sp,
+                                   const chopper_samples *smp);
 chopper_status chopper_load_columns(chopper_ctx *ctx, const chopper_events *ev, const chopper_spans *sp,
                                     const chopper_samples *smp) {
-    if (!ctx || !ev || !sp) return CHOPPER_E_INVALID_ARG;
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    ctx->poison = CHOPPER_OK;             // a new step
+    ctx->x_exchanged = ctx->d_exchanged = false;
+    ctx->stage = 0;
+    return step(ctx, load_columns(ctx, ev, sp, smp));
+}
+
+static chopper_status load_columns(chopper_ctx *ctx, const chopper_events *ev, const chopper_spans *sp,
+                                   const chopper_samples *smp) {
+    if (!ev || !sp) return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "NULL events / spans");
     if (ev->n < 0 || ev->n > 0x7fffffffll || sp->n < 0 || sp->n > 0x7fffffffll)
         return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "event / span count out of range");
     if (ev->n > 0 && (!ev->dispatch_ns || !ev->start_ns || !ev->end_ns || !ev->meta || !ev->name_id))
@@ -101,9 +151,8 @@ chopper_status chopper_load_columns(chopper_ctx *ctx, const chopper_events *ev, 
     return CHOPPER_OK;
 }
 
-chopper_status chopper_align(chopper_ctx *ctx, const chopper_counter_pass *passes, int32_t n_passes,
-                             int32_t n_counters, double *counters_out, int64_t *offsets_ns) {
-    if (!ctx) return CHOPPER_E_INVALID_ARG;
+static chopper_status align(chopper_ctx *ctx, const chopper_counter_pass *passes, int32_t n_passes,
+                            int32_t n_counters, double *counters_out, int64_t *offsets_ns) {
     if (ctx->stage != 1 || !ctx->loaded_ok) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_align before load");
     if (n_passes < 0 || n_counters < 0 || (n_passes > 0 && !passes))
         return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "bad counter passes");
@@ -118,8 +167,20 @@ chopper_status chopper_align(chopper_ctx *ctx, const chopper_counter_pass *passe
     return CHOPPER_OK;
 }
 
-chopper_status chopper_attribute(chopper_ctx *ctx, int32_t *span_idx) {
+chopper_status chopper_align(chopper_ctx *ctx, const chopper_counter_pass *passes, int32_t n_passes,
+                             int32_t n_counters, double *counters_out, int64_t *offsets_ns) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    ctx->C = n_counters > 0 ? n_counters : 0;     // fixes the shape of exchange #2 even if this call fails
+    if (ctx->poison != CHOPPER_OK) {
+        chopper_status s = ch_exchange_poison(ctx, 1);
+        return s != CHOPPER_OK ? s : dead_call(ctx);
+    }
+    chopper_status s = step(ctx, align(ctx, passes, n_passes, n_counters, counters_out, offsets_ns));
+    if (s != CHOPPER_OK) ch_exchange_poison(ctx, 1);     // no-op if this rank's all-gather #1 already ran
+    return s;
+}
+
+static chopper_status attribute(chopper_ctx *ctx, int32_t *span_idx) {
     if (ctx->stage == 1 && ctx->nranks == 1) {
         // align may be skipped on one rank without counters
         CH_TRY(ch_align(ctx, nullptr, 0, 0, nullptr));
@@ -136,9 +197,14 @@ chopper_status chopper_attribute(chopper_ctx *ctx, int32_t *span_idx) {
     return CHOPPER_OK;
 }
 
-chopper_status chopper_overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_ns, int64_t *call_ns, int64_t *phi,
-                               int64_t *psi) {
+chopper_status chopper_attribute(chopper_ctx *ctx, int32_t *span_idx) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    if (ctx->poison != CHOPPER_OK) return dead_call(ctx);
+    return step(ctx, attribute(ctx, span_idx));
+}
+
+static chopper_status overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_ns, int64_t *call_ns, int64_t *phi,
+                              int64_t *psi) {
     if (ctx->stage != 3) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_overlap out of order");
     ch_tick(ctx, 3, 0);
     CH_TRY(ch_overlap_prep(ctx));
@@ -146,6 +212,13 @@ chopper_status chopper_overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_
     CH_TRY(ch_event_pass(ctx, ovl_ns, prep_ns, call_ns, phi, psi));
     ctx->stage = 4;
     return CHOPPER_OK;
+}
+
+chopper_status chopper_overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_ns, int64_t *call_ns, int64_t *phi,
+                               int64_t *psi) {
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    if (ctx->poison != CHOPPER_OK) return dead_call(ctx);
+    return step(ctx, overlap(ctx, ovl_ns, prep_ns, call_ns, phi, psi));
 }
 
 static void fill_rows(chopper_rows &r, const RowTable &t, bool iter, chopper_ctx *ctx) {
@@ -180,8 +253,7 @@ static void fill_rows(chopper_rows &r, const RowTable &t, bool iter, chopper_ctx
     }
 }
 
-chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, chopper_tables *out) {
-    if (!ctx) return CHOPPER_E_INVALID_ARG;
+static chopper_status breakdown(chopper_ctx *ctx, const chopper_bd_params *p, chopper_tables *out) {
     if (ctx->stage != 4) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_breakdown out of order");
     if (!p || !out || (ctx->cfg.n_labels > 0 && (!p->f_gemm || !p->op_type)) || p->n_ratios < 0 ||
         (p->n_ratios > 0 && (!p->ratio_num || !p->ratio_den || !p->ratio_scale)))
@@ -236,8 +308,14 @@ chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, c
     return CHOPPER_OK;
 }
 
-chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
-    if (!ctx || !out) return CHOPPER_E_INVALID_ARG;
+chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, chopper_tables *out) {
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    if (ctx->poison != CHOPPER_OK) return dead_call(ctx);
+    return step(ctx, breakdown(ctx, p, out));
+}
+
+static chopper_status reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
+    if (!out) return ch_fail(ctx, CHOPPER_E_INVALID_ARG, "NULL chopper_global");
     if (ctx->stage != 5) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_reduce_ranks out of order");
     memset(out, 0, sizeof(*out));
     ch_tick(ctx, 7, 0);
@@ -245,6 +323,17 @@ chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     ch_tick(ctx, 7, 1);
     ctx->stage = 6;
     return CHOPPER_OK;
+}
+
+chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    if (ctx->poison != CHOPPER_OK) {
+        chopper_status s = ch_exchange_poison(ctx, 2);
+        return s != CHOPPER_OK ? s : dead_call(ctx);
+    }
+    chopper_status s = step(ctx, reduce_ranks(ctx, out));
+    if (s != CHOPPER_OK) ch_exchange_poison(ctx, 2);     // no-op if this rank's all-gather #2 already ran
+    return s;
 }
 
 chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows) {
@@ -277,6 +366,43 @@ chopper_status chopper_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *sam
         (samples->n > 0 && (!samples->ts_ns || !samples->logical_core || !samples->util_pct)))
         return CHOPPER_E_INVALID_ARG;
     return ch_cpu_util(ctx, samples, topology, n_logical, c_active, c_min, cap, out);
+}
+
+chopper_status chopper_set_allgather(chopper_ctx *ctx, chopper_allgather_fn fn, void *user) {
+    if (!ctx) return CHOPPER_E_INVALID_ARG;
+    ctx->ag_fn = fn;
+    ctx->ag_user = fn ? user : nullptr;
+    return CHOPPER_OK;
+}
+
+void *chopper_loopback_create(int32_t nranks) {
+    if (nranks < 1 || nranks > CH_MAX_GPUS) return nullptr;
+    LoopGroup *g = new LoopGroup();
+    g->n = nranks;
+    g->send.assign(nranks, nullptr);
+    return g;
+}
+
+void chopper_loopback_destroy(void *group) { delete static_cast<LoopGroup *>(group); }
+
+int32_t chopper_loopback_allgather(void *group, const void *send, void *recv, size_t bytes_per_rank, int32_t rank,
+                                   int32_t nranks, void *cuda_stream) {
+    LoopGroup *g = static_cast<LoopGroup *>(group);
+    if (!g || nranks != g->n || rank < 0 || rank >= nranks) return 1;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return 2;       // this rank's send block is complete
+    {
+        std::lock_guard<std::mutex> lk(g->m);
+        g->send[rank] = send;
+    }
+    if (!loop_barrier(g)) return 3;                                 // every send block is complete
+    for (int r = 0; r < nranks; r++)
+        if (cudaMemcpyAsync((char *)recv + (size_t)r * bytes_per_rank, g->send[r], bytes_per_rank,
+                            cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+            return 4;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return 5;
+    if (!loop_barrier(g)) return 6;                                 // nobody reuses a send block early
+    return 0;
 }
 
 chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out) {

@@ -80,6 +80,14 @@ struct chopper_ctx {
     cudaEvent_t fork_ev = nullptr, join_ev[3] = {nullptr, nullptr, nullptr};
     void *nccl = nullptr;
     int rank = 0, nranks = 1;
+    chopper_allgather_fn ag_fn = nullptr;    // exchange transport (chopper_set_allgather), else NCCL
+    void *ag_user = nullptr;
+    // failure protocol (nranks > 1, chopper.h): first failure of this rank in the current step, 0 = none;
+    // whether this step's all-gather #1 / #2 already happened (a failing call makes the missing one)
+    chopper_status poison = CHOPPER_OK;
+    bool x_exchanged = false, d_exchanged = false;
+    int v_blocks = 0;                // k_validate_events grid: one wave of resident blocks on ctx->device
+    size_t mark_base = 0;            // scratch offset after the report (poison exchanges allocate from here)
     char *scratch = nullptr;
     size_t scratch_bytes = 0, used = 0;
     bool hold_scratch = false;       // inside a side-stream branch: temporaries are not released (see tables.cu)
@@ -438,6 +446,9 @@ chopper_status ch_eval_metrics(chopper_ctx *ctx, RowTable &t);
 chopper_status ch_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *s, const int32_t *topology, int32_t n_logical,
                            int64_t *c_active, double *c_min, int64_t cap, chopper_cpu_summary *out);
 chopper_status ch_nccl_allgather(chopper_ctx *ctx, const void *send, void *recv, size_t bytes_per_rank);
+// failure protocol: this rank's side of exchange #which (1 offsets, 2 dense rows) as a block marked failed
+chopper_status ch_exchange_poison(chopper_ctx *ctx, int which);
+int64_t ch_dense_width(chopper_ctx *ctx);        // int64 words per dense slot (compose.cu)
 
 // lookup of an event's innermost span per level (spans.cu; used by events.cu)
 struct SpanView {

@@ -958,11 +958,14 @@ static chopper_status run_breakdown(chopper_ctx *ctx, const int64_t *blk, int ns
 // slot order by gpu id (host, from the exchange headers)
 // slot order by gpu id, on the device: slot b (present) goes to position #{present slots with a smaller
 // (gpu, slot)}; the rest of the order array is -1
-__global__ void k_slot_order(const int64_t *__restrict__ blk, int nslots, int64_t W, int32_t *__restrict__ order) {
+// (a slot whose gpu field is -1 is a failed rank's block, ch_exchange_poison: *poison is set)
+__global__ void k_slot_order(const int64_t *__restrict__ blk, int nslots, int64_t W, int32_t *__restrict__ order,
+                             unsigned int *__restrict__ poison) {
     for (int b = threadIdx.x; b <= nslots; b += blockDim.x) order[b] = -1;
     __syncthreads();
     for (int b = threadIdx.x; b < nslots; b += blockDim.x) {
         const int64_t *x = blk + (int64_t)b * W;
+        if (poison && x[0] == -1) *poison = 1u;
         if (!x[1]) continue;
         const int64_t g = x[0];
         int r = 0;
@@ -974,15 +977,18 @@ __global__ void k_slot_order(const int64_t *__restrict__ blk, int nslots, int64_
     }
 }
 
-static chopper_status slot_order(chopper_ctx *ctx, const int64_t *blk, int nslots, int64_t W, int32_t **out) {
+static chopper_status slot_order(chopper_ctx *ctx, const int64_t *blk, int nslots, int64_t W, int32_t **out,
+                                 unsigned int *poison = nullptr) {
     CH_ALLOC_BEGIN;
     int32_t *d = CH_ALLOC(ctx, int32_t, nslots + 1);
     CH_ALLOC_END(ctx);
-    k_slot_order<<<1, 256, 0, ctx->st>>>(blk, nslots, W, d);
+    k_slot_order<<<1, 256, 0, ctx->st>>>(blk, nslots, W, d, poison);
     CH_LAUNCHED(ctx);
     *out = d;
     return CHOPPER_OK;
 }
+
+int64_t ch_dense_width(chopper_ctx *ctx) { return layout_of(ctx).W; }
 
 chopper_status ch_breakdown_local(chopper_ctx *ctx) {
     int64_t *blk;
@@ -1002,14 +1008,17 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     const int nslots = slots * ctx->nranks;
     CH_ALLOC_BEGIN;
     int64_t *all = CH_ALLOC(ctx, int64_t, (int64_t)nslots * Ly.W);
+    unsigned int *poison = CH_ALLOC(ctx, unsigned int, 1);
     CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemsetAsync(poison, 0, 4, ctx->st));
     if (ctx->nranks > 1) {
+        ctx->d_exchanged = true;
         CH_TRY(ch_nccl_allgather(ctx, ctx->d_dense, all, sizeof(int64_t) * (size_t)slots * Ly.W));
     } else {
         CH_CUDA(ctx, cudaMemcpyAsync(all, ctx->d_dense, 8 * (size_t)slots * Ly.W, cudaMemcpyDeviceToDevice, ctx->st));
     }
     int32_t *ord;
-    CH_TRY(slot_order(ctx, all, nslots, Ly.W, &ord));
+    CH_TRY(slot_order(ctx, all, nslots, Ly.W, &ord, poison));
     ctx->d_all = all;
     ctx->d_all_order = ord;
     ctx->all_slots = nslots;
@@ -1083,10 +1092,12 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     }
     // host copies
     int64_t n = 0;
-    unsigned int hovf = 0;
+    unsigned int hovf = 0, hpoison = 0;
     if (ctx->d_dense_ovf) CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ctx->d_dense_ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(&n, nref, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(&hpoison, poison, 4, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    if (hpoison) return ch_fail(ctx, CHOPPER_E_STATE, "a peer rank failed earlier in this step (all-gather #2)");
     if (n > 4096) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 4096 iterations in chopper_global");
     if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "iteration rank >= max_iters or op label >= n_labels");
     out->n_iters = n;

@@ -614,19 +614,18 @@ chopper_status ch_load(chopper_ctx *ctx) {
     ctx->d_rep = CH_ALLOC(ctx, DevReport, 1);
     ctx->d_gpu_lg = CH_ALLOC(ctx, int32_t, CH_MAX_GPUS);
     CH_ALLOC_END(ctx);
+    ctx->mark_base = ctx->used;
     k_init_report<<<1, 256, 0, ctx->st>>>(ctx->d_rep);
     CH_LAUNCHED(ctx);
-    // one full wave of resident blocks (grid-stride): no partial last wave
-    static int v_blocks = 0;
-    if (!v_blocks) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // one full wave of resident blocks (grid-stride): no partial last wave; sized once per ctx for its device
+    if (!ctx->v_blocks) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
         int per = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_validate_events, NT, 0);
-        v_blocks = std::max(per, 1) * sms;
+        ctx->v_blocks = std::max(per, 1) * sms;
     }
-    unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, NT), 1), v_blocks);
+    unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, NT), 1), ctx->v_blocks);
     if (n > 0) {
         k_validate_events<<<grid, NT, 0, ctx->st>>>(ctx->ev.dispatch_ns, ctx->ev.start_ns, ctx->ev.end_ns, ctx->ev.meta,
                                                     n, G, ctx->d_rep);

@@ -458,6 +458,11 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
     CH_CUDA(ctx, cudaMemsetAsync(ctx->d_list_flags, 0, sizeof(int32_t) * (n_lists + 1), ctx->st));
     ctx->list_beg.assign(n_lists + 2, 0);
     ctx->S_loc = 0;
+    if (n_lg == 0) {                 // a rank without events (its traced GPUs are empty): no span lists
+        CH_CUDA(ctx, cudaMemsetAsync(ctx->d_list_beg, 0, sizeof(int64_t) * (n_lists + 2), ctx->st));
+        ctx->et_ok = false;
+        return CHOPPER_OK;
+    }
     if (S > 0) {
         int64_t smin = dec_i64(ctx->h_rep.s_min_enc), emax = dec_i64(ctx->h_rep.s_max_enc);
         if (ctx->h_rep.s_min_enc == ~0ull) { smin = 0; emax = 0; }

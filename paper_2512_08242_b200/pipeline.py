@@ -12,11 +12,11 @@ from typing import Dict, Optional
 
 import numpy as np
 
-from . import (chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
+from . import (chopper_set_allgather_loopback, chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
                chopper_cpu_util, chopper_create, chopper_set_metrics, chopper_destroy, chopper_events, chopper_get_report, chopper_global, chopper_report_cdf,
                chopper_kernel_launches, chopper_load_columns, chopper_overlap, chopper_reduce_ranks,
                chopper_samples, chopper_scratch_bytes, chopper_spans, chopper_status_sync, chopper_tables,
-               _check, bd_params, dev_to_numpy, load_library, rows_to_numpy)
+               ChopperError, _check, bd_params, chopper_last_error, dev_to_numpy, load_library, rows_to_numpy)
 
 _GEMM = {"qkv_ip", "attn_op", "mlp_gp", "mlp_up", "mlp_dp", "lp"}
 
@@ -75,7 +75,7 @@ class Pipeline:
     (t_l, t_ks, t_ke, meta, name_id, span_*, smp_*, passes)."""
 
     def __init__(self, n_traced_gpus: int, n_labels: int, max_iters: int, max_coll_per_class: int,
-                 device: int = 0, pg=None, stream=None):
+                 device: int = 0, pg=None, stream=None, loopback=None, rank: int = 0):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("paper_2512_08242_b200 needs a CUDA device (no CPU fallback)")
@@ -94,6 +94,10 @@ class Pipeline:
             if self.nranks > 1:
                 be = pg._get_backend(torch.device("cuda", device))
                 self.comm = int(be._comm_ptr())
+        self.loopback = loopback
+        if loopback is not None:
+            # in-process ranks on one device (chopper_loopback_*): rank r of loopback.nranks
+            self.rank, self.nranks = rank, loopback.nranks
         self.ctx = None
         self.scratch = None
         self.d = {}
@@ -154,6 +158,8 @@ class Pipeline:
         if self.ctx is None:
             self.ctx = chopper_create(self.cfg, self.device, self.stream.cuda_stream, self.comm, self.rank,
                                       self.nranks, self.scratch)
+            if self.loopback is not None:
+                chopper_set_allgather_loopback(self.ctx, self.loopback)
 
     # ---- double-buffered streaming inputs ----
     def input_set(self) -> dict:
@@ -211,6 +217,9 @@ class Pipeline:
         s = chopper_load_columns(self.ctx, ev, sp, smp)
         res["load_status"] = s
         res["report"] = chopper_get_report(self.ctx)
+        if s != 0 and self.nranks > 1:
+            # failure protocol (chopper.h): the remaining calls still run so every rank's all-gathers match
+            self._finish_failed_step()
         if s != 0:
             _check(self.ctx, s, "chopper_load_columns", allow=allow)
             return res
@@ -229,15 +238,26 @@ class Pipeline:
             for k in ("ovl", "prep", "call", "phi", "psi"):
                 out[k] = torch.empty(max(N, 1), dtype=torch.int64, device=dev)
         offs = np.zeros(self.cfg.n_traced_gpus, dtype=np.int64)
-        _check(self.ctx, chopper_align(self.ctx, passes, C, out.get("counters") if C else None, offs), "chopper_align")
-        _check(self.ctx, chopper_attribute(self.ctx, out.get("span_idx")), "chopper_attribute")
-        _check(self.ctx, chopper_overlap(self.ctx, out.get("ovl"), out.get("prep"), out.get("call"), out.get("phi"),
-                                         out.get("psi")), "chopper_overlap")
         self._bd = bd_params(params)
         tabs = chopper_tables()
-        _check(self.ctx, chopper_breakdown(self.ctx, self._bd, tabs), "chopper_breakdown")
         glob = chopper_global()
-        _check(self.ctx, chopper_reduce_ranks(self.ctx, glob), "chopper_reduce_ranks")
+        calls = [("chopper_align", lambda: chopper_align(self.ctx, passes, C, out.get("counters") if C else None, offs)),
+                 ("chopper_attribute", lambda: chopper_attribute(self.ctx, out.get("span_idx"))),
+                 ("chopper_overlap", lambda: chopper_overlap(self.ctx, out.get("ovl"), out.get("prep"), out.get("call"),
+                                                             out.get("phi"), out.get("psi"))),
+                 ("chopper_breakdown", lambda: chopper_breakdown(self.ctx, self._bd, tabs)),
+                 ("chopper_reduce_ranks", lambda: chopper_reduce_ranks(self.ctx, glob))]
+        first = None
+        for name, call in calls:
+            st = call()
+            if st != 0 and first is None:
+                first = (name, st, chopper_last_error(self.ctx))
+                if self.nranks == 1:
+                    break
+            # several ranks: keep calling after a failure (chopper.h failure protocol) so no peer hangs
+        if first is not None:
+            name, st, msg = first
+            raise ChopperError(st, f"{name}: {msg}")
         cdf = chopper_report_cdf(self.ctx) if full else None
         if self.cpu is not None:
             c = self.cpu
@@ -250,6 +270,22 @@ class Pipeline:
         res.update(status=st, mask=mask, offsets=offs, tables=tabs, glob=glob, out=out,
                    report=chopper_get_report(self.ctx), cdf=cdf)
         return res
+
+    def _finish_failed_step(self) -> None:
+        """After a failed chopper_load_columns on one of several ranks: make the step's remaining calls (each
+        returns CHOPPER_E_STATE; align and reduce_ranks join their all-gathers with a failed block)."""
+        dummy = chopper_global()
+        chopper_align(self.ctx, [], self.n_counters, None, None)
+        chopper_attribute(self.ctx, None)
+        chopper_overlap(self.ctx)
+        chopper_breakdown(self.ctx, bd_params(self._dummy_params()), chopper_tables())
+        chopper_reduce_ranks(self.ctx, dummy)
+
+    def _dummy_params(self) -> dict:
+        L = self.cfg.n_labels
+        return dict(tpt_peak=1.0, freq_peak_hz=1.0, b=1, s=1, R=1, warmup=0, slot_cycles=-1, slot_flops=-1,
+                    slot_unum=-1, slot_uden=-1, f_gemm=np.zeros(max(L, 1)), op_type=np.zeros(max(L, 1), np.int32),
+                    ratio_num=np.zeros(0, np.int32), ratio_den=np.zeros(0, np.int32), ratio_scale=np.zeros(0))
 
     def to_numpy(self, res: dict, n_ratios: int = 0) -> Dict[str, np.ndarray]:
         """Results in the oracle's naming (tests compare these element by element)."""

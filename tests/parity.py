@@ -79,9 +79,10 @@ def assert_parity(ref, got, per_event=True, tables=True, glob=True, bd=True):
             errs.append("glob.throughput differs")
         if not np.allclose(ref["glob.throughput_median"], got["glob.throughput_median"], rtol=1e-12, equal_nan=True):
             errs.append("glob.throughput_median differs")
-        sk = ref.get("skew.ag", np.zeros(0))
-        if sk.size and int(sk.max()) != int(got["skew.max_ag"][0]):
-            errs.append("max AG skew differs")
+        for cls, key in (("skew.ag", "skew.max_ag"), ("skew.rs", "skew.max_rs")):
+            sk = ref.get(cls, np.zeros(0))
+            if sk.size and int(sk.max()) != int(got[key][0]):
+                errs.append(f"{key} differs: ref {int(sk.max())} got {int(got[key][0])}")
     if bd:
         a, b = ref["bd.rows"], got["bd.rows"]
         if a.shape != b.shape or not np.allclose(a, b, rtol=FP_RTOL, atol=0, equal_nan=True):

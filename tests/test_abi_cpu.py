@@ -32,7 +32,7 @@ def test_exports_every_declared_symbol(lib):
 
 def test_abi_version_and_scratch(lib):
     import paper_2512_08242_b200 as ch
-    assert lib.chopper_abi_version() == 7
+    assert lib.chopper_abi_version() == 8
     cfg = ch.chopper_config(n_traced_gpus=8, n_labels=42, max_iters=256, max_coll_per_class=20000)
     small = ch.chopper_scratch_bytes(cfg, 1000, 100, 0, 0)
     big = ch.chopper_scratch_bytes(cfg, 20_000_000, 2_000_000, 1_000_000, 8)
@@ -49,9 +49,20 @@ def test_create_rejects_bad_args(lib):
     assert lib.chopper_create(ctypes.byref(ctx), ctypes.byref(cfg), 0, None, None, 0, 1,
                               ctypes.cast(buf, ctypes.c_void_p), 16) == 2
     cfg.n_traced_gpus = 2
-    # several ranks need a communicator
-    assert lib.chopper_create(ctypes.byref(ctx), ctypes.byref(cfg), 0, None, None, 0, 2,
+    # rank outside 0..nranks-1
+    assert lib.chopper_create(ctypes.byref(ctx), ctypes.byref(cfg), 0, None, None, 2, 2,
                               ctypes.cast(buf, ctypes.c_void_p), 16) == 2
+
+
+def test_loopback_group_sizes(lib):
+    """the in-process transport's group accepts 1..256 ranks (host logic; the copy itself needs a GPU)"""
+    assert not lib.chopper_loopback_create(0) and not lib.chopper_loopback_create(257)
+    g = lib.chopper_loopback_create(4)
+    assert g
+    # a rank outside the group is refused before touching the device
+    assert lib.chopper_loopback_allgather(g, None, None, 8, 4, 4, None) != 0
+    assert lib.chopper_loopback_allgather(g, None, None, 8, 0, 3, None) != 0
+    lib.chopper_loopback_destroy(g)
 
 
 def test_no_cpu_fallback():

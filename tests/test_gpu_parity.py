@@ -546,3 +546,85 @@ def test_multi_stream_many_tiles():
     ref, got, res, _ = run_both(b, p)
     _check_status(ref, got)
     assert_parity(ref, got)
+
+
+@pytest.mark.slow
+def test_config4_tables_only_bench_path():
+    """The exact bench path: BASELINE configs[3] at full size in tables-only mode (per-event outputs NULL),
+    every table, global row and breakdown against the oracle."""
+    b = tracegen.generate(tracegen.config(4))
+    ref, got, res, pipe = run_both(b, max_iters=256, full=False)
+    _check_status(ref, got)
+    assert_parity(ref, got, per_event=False)
+
+
+def test_hand_worked_skew_and_iteration_bounds(golden):
+    """tests/golden/skew.json through the CUDA path: clock offsets, max AG / RS arrival skew, iteration
+    comm_union and aligned bounds (the oracle pins of test_oracle_pins_extra)."""
+    import test_oracle_pins_extra as pins
+    g = golden("skew.json")
+    b = pins._skew_trace(g).bundle()
+    ref, got, res, pipe = run_both(b, params(b))
+    assert_parity(ref, got)
+    assert int(got["skew.max_ag"][0]) == max(g["ag"]["skew"]) and int(got["skew.max_rs"][0]) == max(g["rs"]["skew"])
+    gi = g["iteration"]
+    tt = TinyTrace(n_gpus=2)
+    for gpu, key in ((0, "gpu0"), (1, "gpu1_true")):
+        d = gi["delta"][gpu]
+        evs = [(s + d, e + d, COMPUTE, 0) for s, e in gi[key]["compute"]]
+        evs += [(s + d, e + d, AG, 1) for s, e in gi[key]["ag"]] + [(s + d, e + d, RS, 2) for s, e in gi[key]["rs"]]
+        for s, e, k, st in sorted(evs):
+            tt.ev(gpu, s - 5, s, e, kind=k, stream=st)
+        tt.span(gpu, 0, 0, 100_000, 7)
+    b = tt.bundle()
+    ref, got, res, pipe = run_both(b, params(b))
+    assert_parity(ref, got)
+    np.testing.assert_array_equal(got["iter.comm_union"], [gi["gpu0"]["comm_union"], gi["gpu1_true"]["comm_union"]])
+    np.testing.assert_array_equal(got["glob.aligned_last"], [gi["glob_aligned_last"]])
+
+
+def test_rates_spec_examples(golden):
+    """SPEC.md:305-308 rate examples (bandwidth, counter ratio, ratio of sums) through the CUDA path."""
+    import test_oracle_pins_extra as pins
+    g = golden("rates.json")
+    rs = g["ratio_of_sums"]
+    tt = pins._rate_trace(rs["X"], rs["Y"], [500, 700])
+    b = tt.bundle()
+    p = params(b, ratio_num=np.array([0, 1], np.int32), ratio_den=np.array([1, -1], np.int32),
+               ratio_scale=np.array([1.0, 1e-9]), op_type=np.zeros(1, np.int32))
+    ref, got, res, pipe = run_both(b, p)
+    assert_parity(ref, got)
+    assert got["iter.rates"][0] == pytest.approx(rs["expect"], rel=1e-15)
+    assert got["point.rates"][0] == pytest.approx(rs["expect"], rel=1e-15)
+
+
+def test_two_compute_streams_chain():
+    """D8 chain per (gpu, stream), three compute streams per GPU (the general a2 path)."""
+    rng = np.random.default_rng(11)
+    tt = TinyTrace(n_gpus=2)
+    evs = []
+    for g in range(2):
+        tt.span(g, 0, 0, 10 ** 7, 3)
+        for st in range(3):
+            t = 1000 + 37 * st
+            for k in range(300):
+                d = int(rng.integers(5, 200))
+                evs.append((g, t - int(rng.integers(0, 400)), t, t + d, st))
+                t += d + int(rng.integers(0, 50))
+    for (g, tl, ks, ke, st) in sorted(evs, key=lambda e: (e[0], e[1])):
+        tt.ev(g, tl, ks, ke, stream=st)
+    b = tt.bundle()
+    ref, got, res, pipe = run_both(b, params(b))
+    _check_status(ref, got)
+    assert_parity(ref, got)
+
+
+def test_zero_events():
+    """a context with no events at all (a rank whose traced GPUs are empty): every call succeeds with empty
+    tables, like the oracle."""
+    tt = TinyTrace(n_gpus=2)
+    tt.span(0, 0, 0, 100, 1)
+    b = tt.bundle()
+    ref, got, res, pipe = run_both(b, params(b))
+    assert len(got["inst.gpu"]) == 0 and len(ref["inst.gpu"]) == 0
+    assert_parity(ref, got)
