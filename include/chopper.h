@@ -301,7 +301,7 @@ chopper_status chopper_ingest_chrome(chopper_ctx *ctx, const char *json, int64_t
  * identifiers, + - * /, parentheses, unary minus; * and / bind tighter than + and -, binary operators are
  * left-associative.  Compiled once on the host to postfix programs; every later chopper_breakdown evaluates
  * them on the device for each point and iteration row over the row's summed counters (chopper_rows.metrics,
- * [n][stride]).  A zero divisor gives NaN for that row.  Errors: an unknown name (MissingCounter) or a syntax
+ * [n][stride]).  A zero divisor, or a quotient that is not finite, gives NaN for that row (DivisionByZero).  Errors: an unknown name (MissingCounter) or a syntax
  * error (ParseError) -> CHOPPER_E_INVALID_ARG, *bad_expr = the failing index (-1 on success), the registry is
  * cleared; a name whose slot the trace lacks -> CHOPPER_E_INVALID_ARG at chopper_breakdown.  n = 0 clears. */
 chopper_status chopper_set_metrics(chopper_ctx *ctx, int32_t n, const char *const *exprs, int32_t n_names,

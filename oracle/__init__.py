@@ -218,8 +218,8 @@ def cpu_util(ts, core, util, topology) -> Dict[str, np.ndarray]:
 # derived-metric registry: a recursive-descent evaluator
 #   expr := term (('+' | '-') term)* ; term := unary (('*' | '/') unary)* ; unary := '-' unary | primary
 #   primary := number | identifier | '(' expr ')'   (binary operators left-associative)
-# identifiers: counter names (the row's summed counter) and dur_s (the row's busy seconds); a zero divisor
-# gives NaN (reading R14).
+# identifiers: counter names (the row's summed counter) and dur_s (the row's busy seconds); a zero divisor or
+# an infinite quotient gives NaN (reading R14).
 # ---------------------------------------------------------------------------
 class MetricError(ValueError):
     pass
@@ -291,8 +291,9 @@ def metric_eval(expr: str, names, counters, busy_ns):
             if o == "*":
                 x = x * y
             else:
-                with np.errstate(divide="ignore", invalid="ignore"):
-                    x = np.where(y == 0.0, np.nan, x / np.where(y == 0.0, 1.0, y))
+                with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+                    q = np.where(y == 0.0, np.nan, x / np.where(y == 0.0, 1.0, y))
+                    x = np.where(np.isinf(q), np.nan, q)     # "error, not infinity" (R14)
         return x
 
     def expr_():

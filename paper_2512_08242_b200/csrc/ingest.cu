@@ -214,7 +214,11 @@ __device__ bool read_int(Cursor &c, int64_t *out) {
     if (c.peek() == '-') { neg = true; c.p++; }
     if (!(c.peek() >= '0' && c.peek() <= '9')) return false;
     unsigned long long v = 0;
-    while (c.p < c.e && c.js[c.p] >= '0' && c.js[c.p] <= '9') v = v * 10 + (unsigned long long)(c.js[c.p++] - '0');
+    while (c.p < c.e && c.js[c.p] >= '0' && c.js[c.p] <= '9') {
+        if (v > (unsigned long long)(INT64_MAX / 10)) return false;     // more than 19 digits: out of range
+        v = v * 10 + (unsigned long long)(c.js[c.p++] - '0');
+    }
+    if (v > (unsigned long long)INT64_MAX) return false;
     *out = neg ? -(int64_t)v : (int64_t)v;
     return true;
 }
@@ -257,7 +261,11 @@ __device__ bool read_us_ns(Cursor &c, int64_t *out) {
     if (x >= 0) {
         if (x > 38) return false;
         r = D;
-        for (int q = 0; q < x; q++) r *= 10;
+        if (r > (unsigned __int128)INT64_MAX) return false;
+        for (int q = 0; q < x; q++) {                    // out of range as soon as it passes INT64_MAX (no wrap)
+            if (r > (unsigned __int128)(INT64_MAX / 10)) return false;
+            r *= 10;
+        }
     } else {
         const int k = -x;
         if (k > 38) { r = 0; sticky |= D != 0; D = 0; }

@@ -38,7 +38,12 @@ __global__ void k_metrics(const int64_t *__restrict__ n_dev, const int64_t *__re
                     if (o == MO_ADD) r = a + b;
                     else if (o == MO_SUB) r = a - b;
                     else if (o == MO_MUL) r = a * b;
-                    else r = b == 0.0 ? NAN : a / b;
+                    else {
+                        // SPEC.md:304 "division by zero yields error, not infinity" (R14): a zero divisor, or a
+                        // quotient that is not finite (a subnormal divisor), makes the row's value NaN
+                        r = b == 0.0 ? NAN : a / b;
+                        if (isinf(r)) r = NAN;
+                    }
                     st[sp - 1] = r;
                 }
             }

@@ -436,7 +436,8 @@ def test_metric_registry_parity():
     b = tracegen.generate(tracegen.config(1))
     C = b.n_counters
     names = [f"c{k}" for k in range(C)]
-    exprs = ["c4 / dur_s", "(c1 + c2) * 0.5 - c3 / c0", "c5 / (c6 - c6)", "-c7 * 2 + dur_s", "1e-3 * c0"]
+    exprs = ["c4 / dur_s", "(c1 + c2) * 0.5 - c3 / c0", "c5 / (c6 - c6)", "-c7 * 2 + dur_s", "1e-3 * c0",
+             "c0 / 1e-320"]
     p = oracle.default_params(b)
     ref = oracle.run(b, p, max_iters=8)
     pipe = ch.Pipeline(b.cfg.n_gpus, len(b.labels), 8, 4096, device=0)

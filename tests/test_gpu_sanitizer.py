@@ -32,6 +32,6 @@ def test_compute_sanitizer(tool):
     cmd += [sys.executable, os.path.join(HERE, "sanitize_run.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=3000)
     out = p.stdout + p.stderr
-    summ = re.findall(r"ERROR SUMMARY: (\d+) error", out)
+    summ = re.findall(r"ERROR SUMMARY: (\d+) error", out) + re.findall(r"RACECHECK SUMMARY: \d+ hazards? displayed \((\d+) error", out)
     assert p.returncode == 0 and "sanitize workload ok" in out, out[-4000:]
     assert summ and all(int(x) == 0 for x in summ), out[-4000:]

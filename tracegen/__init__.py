@@ -146,6 +146,8 @@ def config(cid: int, scale: float = 1.0) -> TraceConfig:
     elif cid == 4:  # long run, 8 GPUs x 200 iterations (~20M events)
         c = TraceConfig(config_id=4, seed=0x5EED0004, n_gpus=8, n_iters=200, n_layers=32, warmup=10,
                         n_counters=8, with_samples=True)
+    elif cid == 5:  # synthetic stress: 1B events over 8 GPUs, deep op / layer nesting (tracegen/stress.py)
+        c = TraceConfig(config_id=5, seed=0x5EED0005, n_gpus=8, n_iters=117, n_layers=32, warmup=2)
     else:
         raise ValueError(f"unknown config {cid}")
     if scale != 1.0:
@@ -275,6 +277,9 @@ def _program(cfg: TraceConfig, labels: List[str]):
 # generator
 # ---------------------------------------------------------------------------
 def generate(cfg: TraceConfig) -> Bundle:
+    if cfg.config_id == 5:
+        from . import stress
+        return stress.generate(cfg)
     labels = label_vocabulary()
     segs = _program(cfg, labels)
     G = cfg.n_gpus
