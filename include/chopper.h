@@ -202,7 +202,48 @@ typedef struct {
     int32_t non_laminar_lists;                /* (gpu, level) span lists needing the exact sweep path */
 } chopper_report;
 
-/* Worst-case scratch bytes for a ctx (all ranks may pass their own sizes). */
+/* Scratch plan (SURVEY §7 hard part 5: 1B events on one B200).  The library never allocates device memory:
+ * every intermediate lives in the caller's scratch arena, so the arena's size is planned from the trace's
+ * shape.  Each item is an upper bound on the bytes the ctx keeps for it; total = persistent items + the
+ * largest transient sort buffer + fixed slack.  The bounds that keep it near the real use are structural:
+ * inside a gpu the events are dispatch-ordered and an event's instance key is a step function of its dispatch
+ * time with steps only at that gpu's span endpoints, so instance runs (and instance rows) number at most
+ * min(N, 2 S + N / 2048 + G + 1), and rows of a level above the operation at most 2 * (spans of the levels
+ * above it) + G.  chopper_scratch_used reports the measured high-water mark to compare with.
+ *   n_spans[4]: spans per level (iteration, phase, layer, operation) on this rank;
+ *   n_comm: communication events (AG / RS / COMM_OTHER), -1 = unknown (n_events);
+ *   n_local_gpus: traced GPUs with events on this rank, <= 0 = n_traced_gpus;
+ *   max_compute_streams: per gpu, <= 0 = unknown (254): above 1 the general sort path and the explicit
+ *     compute union are planned;
+ *   laminar: 1 = no two same-level spans of a gpu cross (FSDP annotations), else the exact sweep's per-event
+ *     table is planned.
+ * items may be NULL.  Returns items->total. */
+typedef struct {
+    int64_t n_events;
+    int64_t n_spans[4];
+    int64_t n_samples;
+    int64_t n_comm;
+    int32_t n_counters;
+    int32_t n_local_gpus;
+    int32_t max_compute_streams;
+    int32_t laminar;
+} chopper_shape;
+typedef struct {
+    size_t events;       /* per-event columns the ctx keeps: permutation, chain ends, counter positions, ... */
+    size_t spans;        /* push-ordered span table, Euler boundary tables, merged key table */
+    size_t unions;       /* communication / compute unions, frequency-power timeline, sample prefixes */
+    size_t subruns;      /* event-pass rows (one per instance run) and their counter sums */
+    size_t instances;    /* instance table */
+    size_t rollups;      /* layer, phase, iteration, gpu tables */
+    size_t points;       /* (gpu, iteration, label) points */
+    size_t exchange;     /* clock-offset and dense-row exchange blocks, breakdown / report work arrays */
+    size_t transient;    /* the largest sort buffer (released after its stage) */
+    size_t total;
+} chopper_scratch_items;
+size_t chopper_scratch_plan(const chopper_config *cfg, const chopper_shape *shape, chopper_scratch_items *items);
+
+/* Worst-case scratch bytes knowing only the sizes: chopper_scratch_plan with every span counted at the
+ * iteration level, n_comm = n_events, unknown stream count and laminarity. */
 size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_t n_spans, int64_t n_samples,
                              int32_t n_counters);
 
@@ -381,7 +422,7 @@ int32_t chopper_abi_version(void);
 int64_t chopper_pass_mismatch(const chopper_ctx *ctx, int32_t p);
 int64_t chopper_pass_conflict(const chopper_ctx *ctx, int32_t p);
 int32_t chopper_counter_present(const chopper_ctx *ctx, int32_t gpu, int32_t slot);
-/* scratch bytes in use (high-water of the bump arena) */
+/* high-water mark of the ctx's scratch arena since chopper_create (bytes) */
 int64_t chopper_scratch_used(const chopper_ctx *ctx);
 
 /* Device timing of pipeline phases with CUDA events recorded on the ctx

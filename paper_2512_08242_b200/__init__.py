@@ -77,6 +77,16 @@ class chopper_samples(ctypes.Structure):
     _fields_ = [("n", I64), ("gpu", P), ("ts_ns", P), ("freq_mhz", P), ("power_mw", P)]
 
 
+class chopper_shape(ctypes.Structure):
+    _fields_ = [("n_events", I64), ("n_spans", I64 * 4), ("n_samples", I64), ("n_comm", I64), ("n_counters", I32),
+                ("n_local_gpus", I32), ("max_compute_streams", I32), ("laminar", I32)]
+
+
+class chopper_scratch_items(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_size_t) for k in ("events", "spans", "unions", "subruns", "instances", "rollups",
+                                               "points", "exchange", "transient", "total")]
+
+
 class chopper_counter_pass(ctypes.Structure):
     _fields_ = [("gpu", I32), ("n", I64), ("name_id", P), ("k", I32), ("slot", P), ("values", P)]
 
@@ -149,7 +159,7 @@ EXPORTS = ["chopper_scratch_bytes", "chopper_create", "chopper_load_columns", "c
            "chopper_abi_version", "chopper_pass_mismatch", "chopper_pass_conflict", "chopper_counter_present",
            "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time", "chopper_report_cdf",
            "chopper_cpu_util", "chopper_set_metrics", "chopper_ingest_scratch_bytes", "chopper_ingest_chrome",
-           "chopper_set_allgather", "chopper_loopback_create", "chopper_loopback_destroy",
+           "chopper_set_allgather", "chopper_loopback_create", "chopper_scratch_plan", "chopper_loopback_destroy",
            "chopper_loopback_allgather"]
 
 _lib = None
@@ -195,6 +205,8 @@ def load_library() -> ctypes.CDLL:
         "chopper_cpu_util": (I32, [P, ctypes.POINTER(chopper_cpu_samples), P, I32, P, P, I64,
                                    ctypes.POINTER(chopper_cpu_summary)]),
         "chopper_set_allgather": (I32, [P, P, P]),
+        "chopper_scratch_plan": (ctypes.c_size_t, [ctypes.POINTER(chopper_config), ctypes.POINTER(chopper_shape),
+                                                   ctypes.POINTER(chopper_scratch_items)]),
         "chopper_loopback_create": (P, [I32]),
         "chopper_loopback_destroy": (None, [P]),
         "chopper_loopback_allgather": (I32, [P, P, P, ctypes.c_size_t, I32, I32, P]),
@@ -229,6 +241,13 @@ def _check(ctx, s: int, what: str, allow=()):
 
 def chopper_scratch_bytes(cfg: chopper_config, n_events: int, n_spans: int, n_samples: int, n_counters: int) -> int:
     return int(load_library().chopper_scratch_bytes(ctypes.byref(cfg), n_events, n_spans, n_samples, n_counters))
+
+
+def chopper_scratch_plan(cfg: chopper_config, shape: chopper_shape) -> Dict[str, int]:
+    """itemized scratch plan (bytes) for a trace of the given shape (include/chopper.h)"""
+    it = chopper_scratch_items()
+    load_library().chopper_scratch_plan(ctypes.byref(cfg), ctypes.byref(shape), ctypes.byref(it))
+    return {k: int(getattr(it, k)) for k, _ in chopper_scratch_items._fields_}
 
 
 def chopper_create(cfg: chopper_config, device: int, stream_ptr: int, nccl_comm: int, rank: int, nranks: int,
@@ -448,5 +467,5 @@ def chopper_cpu_util(ctx, ts, core, util, topology, c_active=None, c_min=None):
     return {k: getattr(out, k) for k, _ in chopper_cpu_summary._fields_}
 
 
-from .pipeline import Pipeline, default_params, flops_table  # noqa: E402,F401
+from .pipeline import Pipeline, default_params, flops_table, scratch_plan, trace_shape  # noqa: E402,F401
 

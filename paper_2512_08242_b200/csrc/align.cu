@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
             }
         }
     }
+    if (!nm_rank) return;                // no counters: the counter-pass positions are not needed
     if (i0 + MR_IPT <= n && (((uintptr_t)(nm_rank + i0)) & 15u) == 0) {
         reinterpret_cast<int4 *>(nm_rank + i0)[0] = make_int4(nr[0], nr[1], nr[2], nr[3]);
         reinterpret_cast<int4 *>(nm_rank + i0)[1] = make_int4(nr[4], nr[5], nr[6], nr[7]);
@@ -409,7 +410,7 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         by_lg[lg].push_back(p);
     }
     CH_ALLOC_BEGIN;
-    ctx->d_nm_rank = CH_ALLOC(ctx, int32_t, N);
+    ctx->d_nm_rank = C > 0 ? CH_ALLOC(ctx, int32_t, N) : nullptr;     // counter-pass position (D2), counters only
     ctx->d_passes = CH_ALLOC(ctx, PassDesc, n_passes + 1);
     int64_t *dgbeg = CH_ALLOC(ctx, int64_t, n_lg + 1);
     CH_ALLOC_END(ctx);

@@ -51,23 +51,68 @@ extern "C" {
 
 int32_t chopper_abi_version(void) { return CHOPPER_ABI_VERSION; }
 
+size_t chopper_scratch_plan(const chopper_config *cfg, const chopper_shape *sh, chopper_scratch_items *items) {
+    chopper_scratch_items it{};
+    if (!cfg || !sh) {
+        if (items) *items = it;
+        return 0;
+    }
+    auto pos = [](int64_t v) { return (size_t)(v > 0 ? v : 0); };
+    const size_t N = pos(sh->n_events), M = pos(sh->n_samples);
+    const size_t S0 = pos(sh->n_spans[0]), S1 = pos(sh->n_spans[1]), S2 = pos(sh->n_spans[2]), S3 = pos(sh->n_spans[3]);
+    const size_t S = S0 + S1 + S2 + S3;
+    const size_t C = pos(sh->n_counters);
+    const size_t Gt = pos(cfg->n_traced_gpus) > 0 ? pos(cfg->n_traced_gpus) : 1;
+    const size_t G = sh->n_local_gpus > 0 ? pos(sh->n_local_gpus) : Gt;
+    const size_t NC = sh->n_comm >= 0 ? std::min(pos(sh->n_comm), N) : N;
+    const bool multi = sh->max_compute_streams != 1;
+    const bool laminar = sh->laminar == 1;
+    const size_t MI = pos(cfg->max_iters) > 0 ? pos(cfg->max_iters) : 1, L = pos(cfg->n_labels) > 0 ? pos(cfg->n_labels) : 1;
+    const size_t K = pos(cfg->max_coll_per_class) > 0 ? pos(cfg->max_coll_per_class) : 1;
+    const size_t tiles = (N + 2047) / 2048 + 1;
+    const size_t Rb = std::min(N, 2 * S + tiles + G + 1) + 1;          // instance runs / instance rows
+    const size_t row = 8 + 8 * RF_NFIELDS + 8 * std::max<size_t>(C, 1) + 7 * 4 + 8;   // RowTable with identity
+    // events: permutation + chain predecessor end; counter-pass position + run id (counters); the exact
+    // sweep's [4][N] span table (non-laminar); the explicit compute union + its permutation (several streams)
+    it.events = N * 12 + (C ? N * 8 : 0) + (laminar ? 0 : N * 16) + (multi ? N * 28 : 0);
+    // push-order span arrays (32 B), Euler tables (12 B per endpoint), merged key table (16 B per endpoint),
+    // chunk stacks and sparse tables (~8 B)
+    it.spans = S * 32 + (2 * S + 4 * G + 2) * 28 + S * 8 + 4096 * (G + 1);
+    it.unions = NC * 24 + (NC + M + 2 * G) * 44 + M * 40;
+    it.subruns = Rb * 144 + Rb * 8 * C + tiles * (8 * 3 + 16 + 64);
+    it.instances = Rb * (row + 16);                                       // + group starts
+    size_t roll = 0;
+    const size_t above[4] = {G, 2 * S0 + G, 2 * (S0 + S1) + G, 2 * (S0 + S1 + S2) + G};
+    for (int d = 0; d < 4; d++) roll += (std::min(Rb, above[d]) + 2) * (row + 16);
+    it.rollups = roll + (std::min(Rb, above[1]) + 2) * 44;              // iteration extras
+    const size_t its = std::min(MI, S0 + 1);
+    const size_t cells = L * G * its;
+    it.points = cells * (row + 8 * RF_NFIELDS + 8 * std::max<size_t>(C, 1) + 16) + Rb * 16;
+    const size_t W1 = 4 + 4 * K;
+    const size_t W2 = 4 + C + 8 * MI + 9 * MI * L + 32 * MI;
+    it.exchange = (Gt + 8) * (W1 + W2) * 8 * 2 + L * 16 * 8 * MI * Gt * 2 + L * 4 * 8 * MI * Gt + 32 * 8 * MI * Gt;
+    // sort buffers: events (general path: keys, values, alternates), spans, instance runs
+    it.transient = std::max({(multi ? N : NC) * 24, S * 24, Rb * 24, N * (multi ? 20 : 0)});
+    it.total = it.events + it.spans + it.unions + it.subruns + it.instances + it.rollups + it.points + it.exchange +
+               it.transient;
+    it.total += it.total / 16 + ((size_t)64 << 20);                     // alignment + small buffers
+    if (items) *items = it;
+    return it.total;
+}
+
 size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_t n_spans, int64_t n_samples,
                              int32_t n_counters) {
     if (!cfg) return 0;
-    int64_t N = n_events > 0 ? n_events : 1, S = n_spans > 0 ? n_spans : 1, M = n_samples > 0 ? n_samples : 1;
-    int64_t C = n_counters > 0 ? n_counters : 0;
-    int64_t G = cfg->n_traced_gpus > 0 ? cfg->n_traced_gpus : 1;
-    int64_t MI = cfg->max_iters > 0 ? cfg->max_iters : 1, L = cfg->n_labels > 0 ? cfg->n_labels : 1;
-    int64_t K = cfg->max_coll_per_class > 0 ? cfg->max_coll_per_class : 1;
-    size_t b = 0;
-    b += (size_t)N * (420 + 40 * C);         // sort buffers, chain, unions, sub-runs, instance tables
-    b += (size_t)S * 192;                    // push-order span arrays + sort buffers + Euler tables
-    b += (size_t)M * 64;                     // sample prefixes
-    b += (size_t)G * (4 + 4 * K) * 8 * 2;    // clock-offset exchange
-    b += (size_t)G * (8 + C + 8 * MI + 9 * MI * L) * 8 * 2;   // dense row exchange
-    b += (size_t)L * 10 * 8 * MI * G * 2;    // breakdown scratch
-    b += (size_t)256 << 20;
-    return b;
+    chopper_shape sh{};
+    sh.n_events = n_events;
+    sh.n_spans[0] = n_spans;
+    sh.n_samples = n_samples;
+    sh.n_comm = -1;
+    sh.n_counters = n_counters;
+    sh.n_local_gpus = 0;
+    sh.max_compute_streams = 0;
+    sh.laminar = 0;
+    return chopper_scratch_plan(cfg, &sh, nullptr);
 }
 
 chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int device, void *cuda_stream,
@@ -458,7 +503,7 @@ int32_t chopper_counter_present(const chopper_ctx *ctx, int32_t gpu, int32_t slo
     int lg = ctx->gpu_lg_h[gpu];
     return lg >= 0 && (size_t)lg * ctx->C + slot < ctx->present.size() ? ctx->present[(size_t)lg * ctx->C + slot] : 0;
 }
-int64_t chopper_scratch_used(const chopper_ctx *ctx) { return ctx ? (int64_t)ctx->used : 0; }
+int64_t chopper_scratch_used(const chopper_ctx *ctx) { return ctx ? (int64_t)ctx->high : 0; }
 
 void chopper_set_timing(chopper_ctx *ctx, int32_t on) {
     if (ctx) ctx->timing = on != 0;

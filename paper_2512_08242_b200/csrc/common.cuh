@@ -89,7 +89,7 @@ struct chopper_ctx {
     int v_blocks = 0;                // k_validate_events grid: one wave of resident blocks on ctx->device
     size_t mark_base = 0;            // scratch offset after the report (poison exchanges allocate from here)
     char *scratch = nullptr;
-    size_t scratch_bytes = 0, used = 0;
+    size_t scratch_bytes = 0, used = 0, high = 0;   // bump arena: bytes in use, high-water mark
     bool hold_scratch = false;       // inside a side-stream branch: temporaries are not released (see tables.cu)
     int64_t launches = 0;
     std::string err;
@@ -308,6 +308,7 @@ inline T *ch_alloc(chopper_ctx *ctx, int64_t n, chopper_status *st) {
         return nullptr;
     }
     ctx->used = off + bytes;
+    if (ctx->used > ctx->high) ctx->high = ctx->used;
     return reinterpret_cast<T *>(ctx->scratch + off);
 }
 #define CH_ALLOC(ctx, T, n) ch_alloc<T>((ctx), (n), &st_)

@@ -34,12 +34,14 @@ __global__ void __launch_bounds__(UN_NT) k_union_block(const uint32_t *__restric
                                                        const int64_t *__restrict__ seg_hi, const int64_t *__restrict__ ks,
                                                        const int64_t *__restrict__ ke, int64_t *__restrict__ Us,
                                                        int64_t *__restrict__ Ue, int64_t *__restrict__ UP,
-                                                       int64_t *__restrict__ Ubeg, int64_t *__restrict__ Ucnt) {
+                                                       int64_t *__restrict__ Ubeg, int64_t *__restrict__ Ucnt,
+                                                       const int64_t *__restrict__ obase) {
     __shared__ int64_t sm[33];
     __shared__ int64_t smax[32];
     __shared__ int64_t s_carry_max, s_m, s_next_s;
     const int lg = blockIdx.x;
     const int64_t lo = seg_lo[lg], hi = seg_hi[lg];
+    const int64_t ob = obase ? obase[lg] : lo;     // output offset of this gpu's merged intervals
     const int tid = threadIdx.x, w = tid >> 5, l = lane_id();
     if (tid == 0) { s_carry_max = INT64_MIN; s_m = 0; }
     __syncthreads();
@@ -100,20 +102,20 @@ __global__ void __launch_bounds__(UN_NT) k_union_block(const uint32_t *__restric
         int64_t k = m0 + ex;
 #pragma unroll
         for (int u = 0; u < UN_IPT; u++) {
-            if (hd[u]) { Us[lo + k] = sv[u]; k++; }
+            if (hd[u]) { Us[ob + k] = sv[u]; k++; }
             bool close = false;
             if (j0 + u < hi) {
                 if (u + 1 < UN_IPT) close = !(j0 + u + 1 < hi) || hd[u + 1];
                 else close = true;   // resolved below against the next thread's first start
             }
-            if (close && u + 1 < UN_IPT) Ue[lo + k - 1] = mi[u];
+            if (close && u + 1 < UN_IPT) Ue[ob + k - 1] = mi[u];
         }
         // last interval of the thread: closes a run if the next interval (next thread / next chunk) is a head
         const int64_t jl = j0 + UN_IPT - 1;
         if (jl < hi) {
             bool nexthead = true;
             if (jl + 1 < hi) nexthead = ks[pos[jl + 1]] > mi[UN_IPT - 1];
-            if (nexthead) Ue[lo + k - 1] = mi[UN_IPT - 1];
+            if (nexthead) Ue[ob + k - 1] = mi[UN_IPT - 1];
         }
         __syncthreads();
         if (tid == UN_NT - 1) s_carry_max = run;
@@ -125,13 +127,13 @@ __global__ void __launch_bounds__(UN_NT) k_union_block(const uint32_t *__restric
     int64_t acc = 0;
     for (int64_t b2 = 0; b2 < mcount; b2 += UN_NT) {
         const int64_t m = b2 + tid;
-        const int64_t len = m < mcount ? Ue[lo + m] - Us[lo + m] : 0;
+        const int64_t len = m < mcount ? Ue[ob + m] - Us[ob + m] : 0;
         int64_t tot;
         const int64_t ex = block_excl_sum<UN_NT>(len, &tot, sm);
-        if (m < mcount) UP[lo + m] = acc + ex;
+        if (m < mcount) UP[ob + m] = acc + ex;
         acc += tot;
     }
-    if (tid == 0) { Ubeg[lg] = lo; Ucnt[lg] = mcount; }
+    if (tid == 0) { Ubeg[lg] = ob; Ucnt[lg] = mcount; }
     (void)s_next_s;
 }
 
@@ -387,6 +389,7 @@ struct Acc {
 // sub-run rows are AoS: 16 int64 (14 fields in RowField order + pad) = one 128 B line per row
 constexpr int SR_W = 16;
 __device__ __forceinline__ void write_subrun(const EvParams &P, int64_t id, const Acc &a, int64_t base) {
+    if (id >= P.cap) return;      // beyond the structural bound (host reports CHOPPER_E_RANGE)
     longlong2 *dst = reinterpret_cast<longlong2 *>(P.sr_f + id * SR_W);
     const int64_t fidx = a.foff == INT32_MAX ? INT64_MAX : base + a.foff;
     // RowField: NEV N BUSY FIRST_IDX LAST_KE PREP CALL OVL PHI PSI COPY AG RS FIRST_KS
@@ -962,8 +965,10 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
                 else write_subrun(P, curid, cur, base);
                 curid++;
                 cur.zero();
-                P.sr_key[curid] = S.key[k][tid];
-                P.sr_first[curid] = i;
+                if (curid < P.cap) {
+                    P.sr_key[curid] = S.key[k][tid];
+                    P.sr_first[curid] = i;
+                }
             }
             const int kd = kind_of(m);
             const int64_t ks = ev_col(S, 1, tid, k), ke = ev_col(S, 2, tid, k);
@@ -1470,8 +1475,10 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_w(EvParams P, int vec_ok) {
             curid++;
             cur.zero();
             const uint32_t v = S.kidx[k][tid];
-            P.sr_key[curid] = key_at(prim ? wkP : win_global(P, 0, lg), P, (int64_t)v);
-            P.sr_first[curid] = i;
+            if (curid < P.cap) {
+                P.sr_key[curid] = key_at(prim ? wkP : win_global(P, 0, lg), P, (int64_t)v);
+                P.sr_first[curid] = i;
+            }
         }
         const int kd = kind_of(m);
         const int64_t ks = ev_col(S, 1, tid, k), ke = ev_col(S, 2, tid, k);
@@ -1544,22 +1551,30 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
     ctx->d_U_cnt = CH_ALLOC(ctx, int64_t, n_lg + 1);
     ctx->d_V_beg = CH_ALLOC(ctx, int64_t, n_lg + 1);
     ctx->d_V_cnt = CH_ALLOC(ctx, int64_t, n_lg + 1);
-    ctx->U_s = CH_ALLOC(ctx, int64_t, N);
-    ctx->U_e = CH_ALLOC(ctx, int64_t, N);
-    ctx->U_P = CH_ALLOC(ctx, int64_t, N);
+    // comm union U_g over the communication bucket of each gpu (all comm streams, D9): at most one merged
+    // interval per communication event, stored compactly (gpu after gpu)
+    std::vector<int64_t> lo(n_lg + 1), hi(n_lg + 1), ob(n_lg + 1, 0);
+    for (int l = 0; l < n_lg; l++) {
+        lo[l] = ctx->bucket_beg[l * NG];
+        hi[l] = ctx->bucket_beg[l * NG + 1];
+        ob[l + 1] = ob[l] + (hi[l] - lo[l]);
+    }
+    const int64_t n_comm = ob[n_lg];
+    ctx->U_s = CH_ALLOC(ctx, int64_t, n_comm);
+    ctx->U_e = CH_ALLOC(ctx, int64_t, n_comm);
+    ctx->U_P = CH_ALLOC(ctx, int64_t, n_comm);
     ctx->d_smp_lo = CH_ALLOC(ctx, int64_t, n_lg + 1);
     ctx->d_smp_hi = CH_ALLOC(ctx, int64_t, n_lg + 1);
     int64_t *seg_lo = CH_ALLOC(ctx, int64_t, n_lg + 1);
     int64_t *seg_hi = CH_ALLOC(ctx, int64_t, n_lg + 1);
+    int64_t *seg_ob = CH_ALLOC(ctx, int64_t, n_lg + 1);
     CH_ALLOC_END(ctx);
-    // comm union U_g over the communication bucket of each gpu (all comm streams, D9)
-    std::vector<int64_t> lo(n_lg), hi(n_lg);
-    for (int l = 0; l < n_lg; l++) { lo[l] = ctx->bucket_beg[l * NG]; hi[l] = ctx->bucket_beg[l * NG + 1]; }
     CH_CUDA(ctx, cudaMemcpyAsync(seg_lo, lo.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(seg_hi, hi.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(seg_ob, ob.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
     if (n_lg > 0) {
         k_union_block<<<n_lg, UN_NT, 0, ctx->st>>>(ctx->d_perm, seg_lo, seg_hi, ctx->ev.start_ns, ctx->ev.end_ns, ctx->U_s,
-                                                  ctx->U_e, ctx->U_P, ctx->d_U_beg, ctx->d_U_cnt);
+                                                  ctx->U_e, ctx->U_P, ctx->d_U_beg, ctx->d_U_cnt, seg_ob);
         CH_LAUNCHED(ctx);
     }
     // compute union V_g: explicit only with several compute streams or same-stream overlaps
@@ -1595,7 +1610,7 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
         CH_CUDA(ctx, cudaMemcpyAsync(vlo, a.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
         CH_CUDA(ctx, cudaMemcpyAsync(vhi, b.data(), 8 * n_lg, cudaMemcpyHostToDevice, ctx->st));
         k_union_block<<<n_lg, UN_NT, 0, ctx->st>>>(ctx->d_vperm, vlo, vhi, ctx->ev.start_ns, ctx->ev.end_ns, ctx->V_s,
-                                                  ctx->V_e, ctx->V_P, ctx->d_V_beg, ctx->d_V_cnt);
+                                                  ctx->V_e, ctx->V_P, ctx->d_V_beg, ctx->d_V_cnt, nullptr);
         CH_LAUNCHED(ctx);
     }
     // sample prefix integrals (D10)
@@ -1669,11 +1684,15 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     if (N == 0) return CHOPPER_OK;
     int64_t ntile = ceil_div(N, EV_TILE);
     CH_ALLOC_BEGIN;
-    ctx->sub.cap = N;
-    ctx->sub.key = CH_ALLOC(ctx, unsigned long long, N + 1);
-    ctx->sub.first_event = CH_ALLOC(ctx, int64_t, N + 1);
-    ctx->sub.f = CH_ALLOC(ctx, int64_t, (int64_t)SR_W * N);
-    ctx->d_run_id = CH_ALLOC(ctx, int32_t, N);
+    // sub-run capacity: inside one gpu the events are dispatch-ordered and an event's instance key is a step
+    // function of its dispatch time with steps only at the gpu's span endpoints, so the key changes at most
+    // 2 * (spans of the gpu) times; runs also break at tile and gpu boundaries
+    const int64_t cap = std::min<int64_t>(N, 2 * ctx->S_loc + ceil_div(N, std::min(EV_TILE, W_TILE)) + ctx->n_lg + 1);
+    ctx->sub.cap = cap;
+    ctx->sub.key = CH_ALLOC(ctx, unsigned long long, cap + 1);
+    ctx->sub.first_event = CH_ALLOC(ctx, int64_t, cap + 1);
+    ctx->sub.f = CH_ALLOC(ctx, int64_t, (int64_t)SR_W * cap);
+    ctx->d_run_id = ctx->C > 0 ? CH_ALLOC(ctx, int32_t, N) : nullptr;     // read only by the counter pass
     ctx->d_tile_state = CH_ALLOC(ctx, unsigned long long, ceil_div(N, W_TILE));   // >= tiles of either pass
     ctx->d_tile_ticket = CH_ALLOC(ctx, unsigned int, 1);
     CH_ALLOC_END(ctx);
@@ -1703,7 +1722,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     P.phi_pre = ctx->d_smp_phi; P.psi_pre = ctx->d_smp_psi; P.smp_lo = ctx->d_smp_lo; P.smp_hi = ctx->d_smp_hi;
     P.o_ovl = ovl; P.o_prep = prep; P.o_call = call; P.o_phi = phi; P.o_psi = psi;
     P.o_run = ctx->d_run_id;
-    P.sr_key = ctx->sub.key; P.sr_first = ctx->sub.first_event; P.sr_f = ctx->sub.f; P.cap = N;
+    P.sr_key = ctx->sub.key; P.sr_first = ctx->sub.first_event; P.sr_f = ctx->sub.f; P.cap = cap;
     P.tile_state = ctx->d_tile_state; P.ticket = ctx->d_tile_ticket;
     P.KTt = ctx->KT_t; P.KTk = ctx->KT_k; P.kt_beg = ctx->d_kt_beg;
     P.TLt = ctx->TL_t; P.TLv = ctx->TL_v; P.TLs = ctx->TL_s; P.tl_beg = ctx->d_tl_beg; P.tl_len = ctx->d_tl_len;
@@ -1767,6 +1786,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     CH_CUDA(ctx, cudaMemcpyAsync(&last, ctx->d_tile_state + ntile - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
     ctx->R = (int64_t)(last & VAL_MASK);
+    if (ctx->R > cap) return ch_fail(ctx, CHOPPER_E_RANGE, "sub-runs exceed their structural bound");
     // sentinel: sub-run R begins at N
     int64_t nv = N;
     CH_CUDA(ctx, cudaMemcpyAsync(ctx->sub.first_event + ctx->R, &nv, 8, cudaMemcpyHostToDevice, ctx->st));

@@ -1332,11 +1332,31 @@ static chopper_status sum_rows(chopper_ctx *ctx, const TabView &ch, const uint32
     return CHOPPER_OK;
 }
 
+// parent rows beyond the table's capacity (a violated structural bound): clamp and latch CHOPPER_E_RANGE
+__global__ void k_clamp_rows(int64_t *__restrict__ n_dev, int64_t cap, DevReport *__restrict__ rep) {
+    if (threadIdx.x == 0 && *n_dev > cap) {
+        *n_dev = cap;
+        latch(rep, CHOPPER_E_RANGE);
+    }
+}
+
+// rows of the parent level (depth 3 layer, 2 phase, 1 iteration, 0 gpu): an instance key's (it, ph, ly) prefix
+// is a step function of the dispatch time with steps only at the gpu's iteration / phase / layer span
+// endpoints, so a gpu has at most 1 + 2 * (its spans of the levels above) distinct prefixes
+static int64_t parent_bound(chopper_ctx *ctx, int depth) {
+    int64_t s = 0;
+    for (int l = 0; l < ctx->n_lg * 4; l++)
+        if (l % 4 < depth) s += ctx->list_beg[l + 1] - ctx->list_beg[l];
+    return 2 * s + ctx->n_lg;
+}
+
 static chopper_status rollup(chopper_ctx *ctx, RowTable &child, RowTable &parent, int shift, int depth, int mode,
                              const KeyLayout &L, int32_t *lg_gpu_d, int fanout = 1) {
     int64_t *starts, *ng_dev;
     CH_TRY(group(ctx, child.key, child.cap, child.n_dev, shift, &starts, &ng_dev));
-    CH_TRY(alloc_table(ctx, parent, std::max<int64_t>(child.cap, 1), ctx->C, true));
+    CH_TRY(alloc_table(ctx, parent, std::max<int64_t>(std::min(child.cap, parent_bound(ctx, depth)), 1), ctx->C, true));
+    k_clamp_rows<<<1, 32, 0, ctx->st>>>(ng_dev, parent.cap, ctx->d_rep);
+    CH_LAUNCHED(ctx);
     parent.n_dev = ng_dev;
     CH_TRY(sum_rows(ctx, view(child), nullptr, starts, ng_dev, child.cap, mode, shift, ctx->C, view(parent), fanout));
     k_decode<<<grid_for(child.cap, NT), NT, 0, ctx->st>>>(parent.key, ng_dev, L, depth, lg_gpu_d, ctx->d_list_beg,

@@ -12,7 +12,7 @@ from typing import Dict, Optional
 
 import numpy as np
 
-from . import (chopper_set_allgather_loopback, chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
+from . import (chopper_set_allgather_loopback, chopper_scratch_plan, chopper_shape, chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
                chopper_cpu_util, chopper_create, chopper_set_metrics, chopper_destroy, chopper_events, chopper_get_report, chopper_global, chopper_report_cdf,
                chopper_kernel_launches, chopper_load_columns, chopper_overlap, chopper_reduce_ranks,
                chopper_samples, chopper_scratch_bytes, chopper_spans, chopper_status_sync, chopper_tables,
@@ -64,6 +64,30 @@ def default_params(cols, labels, shapes: Dict[str, int], op_kind) -> dict:
     else:
         p.update(ratio_num=np.zeros(0, np.int32), ratio_den=np.zeros(0, np.int32), ratio_scale=np.zeros(0))
     return p
+
+
+def trace_shape(cols, n_counters: int, laminar: bool = True) -> "chopper_shape":
+    """chopper_shape of a trace's columns (counts only: spans per level, communication events, local gpus,
+    compute streams) for chopper_scratch_plan.  `laminar` is the caller's statement that no same-level spans
+    cross (true for FSDP annotations; False plans the exact sweep's per-event table)."""
+    meta = np.asarray(cols.meta, np.uint32)
+    kind = meta & 0xFF
+    lv = np.asarray(cols.span_gl, np.uint32) & 0xFF
+    comp = kind == 0
+    streams = int(((meta[comp] >> 8) & 0xFFFF).max()) + 1 if comp.any() else 1
+    sh = chopper_shape(n_events=len(meta), n_samples=len(cols.smp_gpu), n_comm=int(np.isin(kind, (1, 2, 3)).sum()),
+                       n_counters=n_counters, n_local_gpus=len(np.unique(meta >> 24)),
+                       max_compute_streams=streams, laminar=1 if laminar else 0)
+    for k in range(4):
+        sh.n_spans[k] = int((lv == k).sum())
+    return sh
+
+
+def scratch_plan(n_traced_gpus: int, n_labels: int, max_iters: int, max_coll_per_class: int, cols, n_counters: int,
+                 laminar: bool = True) -> Dict[str, int]:
+    cfg = chopper_config(n_traced_gpus=n_traced_gpus, n_labels=n_labels, max_iters=max_iters,
+                         max_coll_per_class=max_coll_per_class)
+    return chopper_scratch_plan(cfg, trace_shape(cols, n_counters, laminar))
 
 
 def _i64(a):
@@ -118,8 +142,10 @@ class Pipeline:
                         "topo": torch.from_numpy(np.ascontiguousarray(topology, np.int32)).to(dev)}
 
     # ---- inputs ----
-    def upload(self, cols, n_counters: int, pinned_host: Optional[dict] = None) -> None:
-        """Copy input columns to the device (from pinned host tensors if given)."""
+    def upload(self, cols, n_counters: int, pinned_host: Optional[dict] = None, plan_laminar: Optional[bool] = None) -> None:
+        """Copy input columns to the device (from pinned host tensors if given).  The scratch arena is sized by
+        chopper_scratch_bytes (worst case), or by chopper_scratch_plan of the trace's shape when plan_laminar
+        is given (the caller states whether same-level spans may cross)."""
         torch = self.torch
         dev = torch.device("cuda", self.device)
         src = {
@@ -148,7 +174,10 @@ class Pipeline:
         self.d = d
         self.n_counters = n_counters
         self.N, self.S, self.M = len(src["t_l"]), len(src["span_gl"]), len(src["smp_gpu"])
-        need = chopper_scratch_bytes(self.cfg, self.N, self.S, self.M, n_counters)
+        if plan_laminar is None:
+            need = chopper_scratch_bytes(self.cfg, self.N, self.S, self.M, n_counters)
+        else:
+            need = chopper_scratch_plan(self.cfg, trace_shape(cols, n_counters, plan_laminar))["total"]
         if self.scratch is None or self.scratch.numel() < need:
             self.scratch = None
             if self.ctx:

@@ -629,3 +629,22 @@ def test_zero_events():
     ref, got, res, pipe = run_both(b, params(b))
     assert len(got["inst.gpu"]) == 0 and len(ref["inst.gpu"]) == 0
     assert_parity(ref, got)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_scratch_plan_bounds_high_water(cid):
+    """chopper_scratch_plan of the trace's shape (the arena the library is given) bounds the measured
+    high-water mark, and the step succeeds in exactly that arena."""
+    import paper_2512_08242_b200 as ch
+    b = tracegen.generate(tracegen.config(cid))
+    p = oracle.default_params(b)
+    mi, kc = b.cfg.n_iters + 3, 1 << 15
+    pipe = ch.Pipeline(b.cfg.n_gpus, len(b.labels), mi, kc)
+    pipe.upload(b, b.n_counters, plan_laminar=True)
+    plan = ch.scratch_plan(b.cfg.n_gpus, len(b.labels), mi, kc, b, b.n_counters)
+    assert pipe.scratch.numel() == plan["total"]
+    for full in (False, True):
+        pipe.run(p, full=full)
+    used = ch.load_library().chopper_scratch_used(pipe.ctx)
+    assert 0 < used <= plan["total"]
+    pipe.close()
