@@ -1,27 +1,34 @@
 """bench.py -- events/s of the B200 Chopper hot path (BASELINE.json metric).
 
-python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 4]
+python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config 4|5]
 
 A step = one pass of the whole hot path (chopper_load_columns -> align ->
 attribute -> overlap -> breakdown -> reduce_ranks)
-over the resident synthetic trace of BASELINE.json configs[3] (Llama 3 8B FSDP
-long run: 8 traced GPUs x 200 iterations, ~17.6M kernel events, 8 counters,
-1 ms frequency / power samples).  With N ranks (torchrun, NCCL), rank r owns
-traced GPUs {g : g mod N == r} of that same trace (strong scaling).
+over a resident synthetic trace.  Default: BASELINE.json configs[3] (Llama 3
+8B FSDP long run: 8 traced GPUs x 200 iterations, ~17.6M kernel events, 8
+counters, 1 ms frequency / power samples) -- the config the metric is quoted on
+that fits one GPU.  --config 5: configs[4], the 1B-event stress trace (8 shards
+x 124.6M events, op nesting depth 7; tracegen/stress.py).  With N ranks
+(torchrun, NCCL), rank r owns traced GPUs {g : g mod N == r} of the same trace
+(each rank generates only its own shard).
 
 value  = events processed by all ranks / device time of K steps (max over ranks)
 e2e    = same metric with the H2D copy of every input column from pinned host
-         memory and the D2H of the results inside the timed region; inputs are
-         double-buffered (trace i+1 copies on a copy stream while trace i
-         computes), so e2e approaches max(H2D, compute) per step.
-roofline: the fused event pass kernel (dominant), algorithmic bytes / its
-         CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
+         memory and the D2H of the results inside the timed region (config 4:
+         double-buffered, trace i+1 copies while trace i computes; config 5:
+         serial, the device cannot hold two copies of a 1B-event trace).
+roofline: the dominant kernel (the fused event pass k_events_w), SURVEY 8(d)
+         algorithmic bytes (28 B/event of event columns + one 96 B time row per
+         instance) / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs;
+         the same for the counter pass (68 B/event at C = 8) and for the whole
+         pipeline (all input columns + instance rows / step time).
 --impl reference times the CPU oracle (oracle/, single-threaded C) as it
 stands on a bounded sample of the same workload.
 """
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -39,20 +46,30 @@ WORKLOADS = {
     2: "configs[1]: Llama 3 8B FSDP-shaped trace, 8 GPUs x 10 iterations (~0.9M events)",
     3: "configs[2]: Llama 3 8B FSDP trace + 20 counters/kernel + 1 ms freq/power samples",
     4: "configs[3]: Llama 3 8B FSDP long run, 8 GPUs x 200 iterations (~17.6M events), 8 counters, samples",
+    5: "configs[4]: synthetic stress, 8 GPUs x 117 iterations x 1.065M events (997M events), op nesting depth 7",
 }
-
-
-# cpu_baseline: the whole workload once (~15 s of single-threaded oracle work on the dev host);
-# --impl reference: traced GPU 0's shard per step (~1.5 s), so K + W steps finish within a minute or two
+NOMINAL_HBM_GBS = 8000.0     # north_star's "~8 TB/s" B200 HBM3e
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "measured copy (MEASURED_PEAKS.json)"
+        return float(p["hbm_gbs"]), "measured copy (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_info():
+    model = platform.processor() or "unknown"
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
 class ClockSampler:
@@ -100,11 +117,19 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def workload(cid: int):
+def workload(cid: int, gpus=None, n_iters=None):
+    """the synthetic trace of BASELINE configs[cid-1] (only the traced GPUs `gpus` for config 5) and the
+    product-side breakdown parameters (hardware spec, counter slots, Eq. 4 FLOP table; no oracle import)"""
     import tracegen
     import paper_2512_08242_b200 as ch
-    b = tracegen.generate(tracegen.config(cid))
-    # product-side breakdown parameters (hardware spec, counter slots, Eq. 4 FLOP table); no oracle import here
+    cfg = tracegen.config(cid)
+    if cid == 5:
+        from tracegen import stress
+        b = stress.generate(cfg, gpus=gpus, n_iters=n_iters, threads=min(32, os.cpu_count() or 8))
+    else:
+        b = tracegen.generate(cfg)
+        if gpus is not None:
+            b = b.gpu_slice(gpus)
     p = ch.default_params(b, b.labels, tracegen.workload_shapes(b.cfg), tracegen.op_kind)
     return b, p
 
@@ -118,33 +143,61 @@ def input_bytes(b) -> int:
     return int(n)
 
 
-def run_reference(args):
-    """The oracle as it stands, single-threaded, on a bounded sample (traced GPU 0's shard) of the workload."""
+def oracle_sample(cid: int):
+    """the bounded CPU sample (about 10-30 s of single-threaded oracle work): config 4 -> the whole workload;
+    config 5 -> the first 16 iterations of traced GPU 0's shard (17M events); smaller configs -> the whole
+    trace"""
+    if cid == 5:
+        b, p = workload(5, gpus=[0], n_iters=16)
+        return b, p, f"traced GPU 0's shard, first 16 of 117 iterations ({b.n_events} events, {len(b.span_gl)} spans)"
+    b, p = workload(cid)
+    return b, p, f"the whole workload ({b.n_events} events, all {b.cfg.n_gpus} traced GPUs, spans, samples, passes)"
+
+
+def time_oracle(b, p, max_iters):
+    """the oracle (O1-O16 of chopper_oracle.c) pinned to one host core; seconds"""
     import oracle
+    oracle.build()
+    old = os.sched_getaffinity(0)
+    core = min(old)
+    os.sched_setaffinity(0, {core})
+    try:
+        t = time.perf_counter()
+        oracle.run(b, p, max_iters=max_iters)
+        return time.perf_counter() - t, core
+    finally:
+        os.sched_setaffinity(0, old)
+
+
+def run_reference(args):
+    """The oracle as it stands, single-threaded on one pinned core, on a bounded sample of the workload per
+    step: traced GPU 0's shard (config 4) / its first 4 iterations (config 5)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    b, p = workload(args.config)
-    sample = b.gpu_slice([0])
-    oracle.build()
+    if args.config == 5:
+        b, p = workload(5, gpus=[0], n_iters=4)
+        what = f"first 4 iterations of traced GPU 0's shard ({b.n_events} events)"
+    else:
+        full, p = workload(args.config)
+        b = full.gpu_slice([0])
+        what = f"traced GPU 0 shard ({b.n_events} events, its spans, samples and counter passes)"
+    mi = b.cfg.n_iters + 8
     for _ in range(args.warmup):
-        oracle.run(sample, p, max_iters=256)
+        time_oracle(b, p, mi)
     t = []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        oracle.run(sample, p, max_iters=256)
-        t.append(time.perf_counter() - t0)
-    ev = sample.n_events
+        dt, core = time_oracle(b, p, mi)
+        t.append(dt)
+    ev = b.n_events
     value = ev * args.steps / sum(t)
     line = {"metric": METRIC, "value": value, "unit": "events/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(t) / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": WORKLOADS[args.config], "sample": f"traced GPU 0 shard ({ev} events)",
-                       "n_events": ev},
+            "config": {"workload": WORKLOADS[args.config], "sample": what, "n_events": ev},
             "cpu_baseline": {"value": value, "unit": "events/s", "cores": 1, "kind": "oracle",
-                             "sample": f"traced GPU 0 shard of {WORKLOADS[args.config]} ({ev} events, its "
-                                       f"spans, samples and counter passes) per step"},
+                             "sample": f"{what} per step, oracle O1-O16 pinned to core {core}", **host_info()},
             "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -158,6 +211,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full", action="store_true", help="skip the full-mode (per-event outputs) timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -177,27 +231,36 @@ def main():
         pg = dist.group.WORLD
         dist.barrier()
     ch.build()
-    b, p = workload(args.config)
-    G = b.cfg.n_gpus
+    import tracegen
+    G = tracegen.config(args.config).n_gpus
     mine = [g for g in range(G) if g % world == rank]
-    shard = b.gpu_slice(mine) if world > 1 else b
+    tg = time.time()
+    if args.config == 5:
+        shard, p = workload(5, gpus=mine)            # each rank draws only its own traced GPUs
+    else:
+        full_trace, p = workload(args.config)
+        shard = full_trace.gpu_slice(mine) if world > 1 else full_trace
+    t_gen = time.time() - tg
+    b = shard
     n_ev_local = shard.n_events
+    C = shard.n_counters
     stream = torch.cuda.Stream(dev)
-    pipe = ch.Pipeline(G, len(b.labels), 256, 1 << 15, device=local, pg=pg, stream=stream)
-    pipe.upload(shard, b.n_counters)
+    mi = b.cfg.n_iters + 8
+    kcoll = 1 << 15
+    pipe = ch.Pipeline(G, len(b.labels), mi, kcoll, device=local, pg=pg, stream=stream)
+    # the scratch arena from chopper_scratch_plan of the shard's shape (FSDP annotations nest: laminar)
+    pipe.upload(shard, C, plan_laminar=True)
+    plan = ch.scratch_plan(G, len(b.labels), mi, kcoll, shard, C)
     cpu = None
-    if rank == 0:
+    if rank == 0 and args.config != 5:
         # host CPU utilisation samples over the trace: one host trace, processed by rank 0
-        import tracegen
         cpu = tracegen.cpu_samples(b.cfg.seed, int(b.t_l.min()), int(b.t_ke.max()))
         pipe.upload_cpu(*cpu)
     ch.chopper_set_timing(pipe.ctx, True)
-    # warm-up (W >= 3)
     for _ in range(args.warmup):
         res = pipe.run(p, full=False)
-    launches0 = pipe.launches()
-    ev_ms = []
-    ev_phase_ms = []
+    launches0, syncs0 = pipe.launches(), pipe.host_syncs()
+    ev_ms, ev_phase_ms, cnt_ms = [], [], []
     clocks = ClockSampler(local)
     if rank == 0:
         clocks.start()
@@ -211,24 +274,49 @@ def main():
         res = pipe.run(p, full=False)
         ev_ms.append(ch.chopper_phase_time(pipe.ctx, 8))
         ev_phase_ms.append(ch.chopper_phase_time(pipe.ctx, 4))
+        cnt_ms.append(ch.chopper_phase_time(pipe.ctx, 9) if C else None)
     t1.record(stream)
     torch.cuda.synchronize(dev)
     if pg is not None:
         dist.barrier()
     clocks.stop()
     launches = pipe.launches() - launches0
+    syncs = pipe.host_syncs() - syncs0
     ms = t0.elapsed_time(t1)
     phase_ms = {name: ch.chopper_phase_time(pipe.ctx, i) for i, name in enumerate(ch.PHASES)}
-    if pg is not None:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        ntot = torch.tensor([n_ev_local], device=dev, dtype=torch.int64)
-        dist.all_reduce(ntot)
-        n_events = int(ntot.item())
-    else:
-        n_events = n_ev_local
+    n_inst_local = int(res["tables"].inst.n)
+
+    def allreduce(v, op="max", dtype=None):
+        if pg is None:
+            return v
+        t = torch.tensor([v], device=dev, dtype=dtype or torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        return t.item()
+    ms = float(allreduce(ms))
+    n_events = int(allreduce(n_ev_local, "sum", torch.int64))
+    n_inst = int(allreduce(n_inst_local, "sum", torch.int64))
     value = n_events * args.steps / (ms * 1e-3)
+
+    # ---- full mode: the per-event outputs (span indices, ovl, prep, call, phi, psi) written too ----
+    full_mode = None
+    if not args.no_full and args.config != 5:
+        for _ in range(2):
+            pipe.run(p, full=True)
+        if pg is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0.record(stream)
+        for _ in range(args.steps):
+            pipe.run(p, full=True)
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        fms = float(allreduce(t0.elapsed_time(t1)))
+        full_mode = {"value": n_events * args.steps / (fms * 1e-3), "unit": "events/s", "ms_per_step": fms / args.steps,
+                     "per_event_out_bytes": 4 * 4 + 5 * 8 + 8 * C}
+    elif args.config == 5:
+        full_mode = {"value": None, "note": "not run at 1B events on one GPU: the per-event outputs (28 GB) do not "
+                                            "fit beside the inputs and the scratch plan; full-mode parity runs on "
+                                            "shard 0 in tests/test_gpu_config5.py"}
 
     # ---- e2e: pinned host columns copied in, results read back, every step ----
     e2e = None
@@ -250,13 +338,10 @@ def main():
             for k, v in zip(("ts", "core", "util", "topo"), cpu):
                 pinned_cpu[k] = torch.from_numpy(np.ascontiguousarray(v, pipe.cpu[k].cpu().numpy().dtype)).pin_memory()
                 h2d += pinned_cpu[k].numel() * pinned_cpu[k].element_size()
-
-        # double-buffered streaming: trace i+1's host->device copy runs on a copy stream while trace i
-        # computes on the other device input set (every step still copies its whole input and reads its
-        # result back; the first copy is not overlapped)
         copy_stream = torch.cuda.Stream(dev)
-        sets = [pipe.input_set(), pipe.new_input_set()]
         pp = [(nm, vals) for (_, nm, _, vals) in pinned_passes]
+        double = args.config != 5
+        sets = [pipe.input_set(), pipe.new_input_set()] if double else [pipe.input_set()]
 
         def e2e_run(k):
             """k steps; returns the d2h bytes of the last step's result"""
@@ -264,12 +349,15 @@ def main():
             ready = pipe.stage_inputs(sets[0], pinned, pp, pinned_cpu, copy_stream)
             d2h = 0
             for i in range(k):
-                pipe.use_inputs(sets[i % 2], ready)
-                if i + 1 < k:
+                pipe.use_inputs(sets[i % len(sets)], ready)
+                if double and i + 1 < k:
                     ready = pipe.stage_inputs(sets[(i + 1) % 2], pinned, pp, pinned_cpu, copy_stream)
                 r = pipe.run(p, full=False)
                 g = r["glob"]
                 d2h = int(g.n_iters) * 44 + int(g.n_bd) * 128 + 8
+                if not double and i + 1 < k:
+                    copy_stream.wait_stream(stream)
+                    ready = pipe.stage_inputs(sets[0], pinned, pp, pinned_cpu, copy_stream)
             stream.wait_stream(copy_stream)
             return d2h
 
@@ -282,13 +370,9 @@ def main():
         t1.record(stream)
         torch.cuda.synchronize(dev)
         pipe.use_inputs(sets[0])
-        ems = t0.elapsed_time(t1)
-        if pg is not None:
-            t = torch.tensor([ems], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+        ems = float(allreduce(t0.elapsed_time(t1)))
         e2e = {"value": n_events * args.steps / (ems * 1e-3), "unit": "events/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h}
+               "d2h_bytes_per_step": d2h, "inputs": "double-buffered" if double else "serial copy then compute"}
 
     if rank != 0:
         if pg is not None:
@@ -296,54 +380,64 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel: fused event pass ----
+    # ---- roofline (SURVEY 8(d) algorithmic bytes) ----
     peak, peak_src = peaks()
-    R = pipe.ctx and int(ch.load_library().chopper_scratch_used(pipe.ctx))
-    ev_ms = [x for x in ev_ms if x]
-    ev_avg = sum(ev_ms) / len(ev_ms) if ev_ms else None
-    ev_phase_ms = [x for x in ev_phase_ms if x]
-    ev_phase_avg = sum(ev_phase_ms) / len(ev_phase_ms) if ev_phase_ms else None
-    # algorithmic bytes per launch: event columns read by the pass
-    # (t_l, t_ks, t_ke 24 B, meta 4 B, pred_end 8 B) + run id written (4 B, counters present)
-    # + one 128 B sub-run row per instance run
-    n_runs = int(res["tables"].inst.n)   # lower bound on sub-runs; DESIGN.md counts sub-runs ~ instances
-    alg = n_ev_local * (24 + 4 + 8 + (4 if b.n_counters else 0)) + 128 * n_runs
-    traffic = None
+    avg = (lambda xs: (sum(x for x in xs if x) / len([x for x in xs if x])) if any(xs) else None)
+    ev_avg, ev_phase_avg, cnt_avg = avg(ev_ms), avg(ev_phase_ms), avg(cnt_ms)
+    # event pass: t_l, t_ks, t_ke (24 B) + meta (4 B) per event, one 96 B time row (12 x int64) per instance
+    alg = n_ev_local * 28 + 96 * n_inst_local
+    achieved = alg / (ev_avg * 1e-3) / 1e9 if ev_avg else None
+    traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "event_pass_traffic.json")) as f:
             tj = json.load(f)
-            if tj.get("config") == args.config:
-                traffic = tj.get("dram_bytes_per_launch")
+        if tj.get("config") == args.config:
+            traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
     except Exception:
         pass
-    achieved = alg / (ev_avg * 1e-3) / 1e9 if ev_avg else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-            "kernel": "k_events_w (main event-pass kernel, a5-a9; time = its own CUDA-event bracket)",
-            "peak_source": peak_src, "alg_bytes_per_launch": alg, "avg_launch_ms": ev_avg,
-            "event_pass_phase_ms": ev_phase_avg,
-            "event_pass_phase_frac": (alg / (ev_phase_avg * 1e-3) / 1e9 / peak) if ev_phase_avg else None,
-            "phase_ms_last_step": phase_ms}
+            "traffic_source": traffic_src or "no committed ncu capture for this config",
+            "kernel": "k_events_w (fused event pass, a5-a9 time part; time = its own CUDA-event bracket)",
+            "peak_source": peak_src, "frac_of_nominal_8TBs": (achieved / NOMINAL_HBM_GBS) if achieved else None,
+            "alg_bytes_per_launch": alg, "alg_formula": "28 B/event (t_l, t_ks, t_ke, meta) + 96 B/instance row",
+            "avg_launch_ms": ev_avg, "event_pass_phase_ms": ev_phase_avg, "phase_ms_last_step": phase_ms}
+    if C and cnt_avg:
+        calg = n_ev_local * (4 + 8 * C)
+        roof["counter_pass"] = {"kernel": "k_counters_tiled", "alg_bytes_per_launch": calg,
+                                "alg_formula": f"meta 4 B + {C} counters x 8 B per event", "avg_launch_ms": cnt_avg,
+                                "achieved": calg / (cnt_avg * 1e-3) / 1e9,
+                                "frac": calg / (cnt_avg * 1e-3) / 1e9 / peak}
+    # the whole pipeline: every input column once + the instance rows
+    S_loc, M_loc = len(shard.span_gl), len(shard.smp_gpu)
+    pipe_alg = n_ev_local * (32 + 8 * C) + S_loc * 24 + M_loc * 20 + n_inst_local * (96 + 8 * C)
+    pipe_gbs = pipe_alg * world / (ms / args.steps * 1e-3) / 1e9
+    roof["pipeline"] = {"alg_bytes_per_step": pipe_alg * world, "achieved_gbs": pipe_gbs, "frac": pipe_gbs / peak,
+                        "frac_of_nominal_8TBs": pipe_gbs / NOMINAL_HBM_GBS,
+                        "alg_formula": f"events x (32 + 8C) B + spans x 24 B + samples x 20 B + instances x (96 + 8C) B"}
 
-    cpu = None
+    cpu_b = None
     if not args.no_cpu_baseline and world == 1:
-        import oracle
-        oracle.build()
-        t = time.perf_counter()
-        oracle.run(b, p, max_iters=256)
-        dt = time.perf_counter() - t
-        cpu = {"value": b.n_events / dt, "unit": "events/s", "cores": 1, "kind": "oracle",
-               "sample": f"the whole workload ({b.n_events} events, all 8 traced GPUs) once, single-threaded C "
-                         f"oracle O1-O13, {dt:.1f} s"}
+        sb, sp, what = oracle_sample(args.config)
+        dt, core = time_oracle(sb, sp, sb.cfg.n_iters + 8)
+        cpu_b = {"value": sb.n_events / dt, "unit": "events/s", "cores": 1, "kind": "oracle",
+                 "sample": f"{what}, once; single-threaded C oracle O1-O16 pinned to core {core}, {dt:.1f} s",
+                 **host_info()}
 
     line = {"metric": METRIC, "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "int64/f64", "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "n_events": n_events, "n_counters": b.n_counters,
-                       "n_spans": int(len(b.span_gl)), "n_samples": int(len(b.smp_gpu)), "mode": "tables-only",
-                       "l2": f"inputs {input_bytes(b) / 1e9:.2f} GB > 126 MB L2 (no flush needed)",
-                       "parallelism": f"trace shards: rank r owns traced GPUs g mod {world} == r"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64/f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "n_events": n_events, "n_counters": C,
+                       "n_spans_rank0": S_loc, "n_samples_rank0": M_loc, "instances": n_inst, "mode": "tables-only",
+                       "l2": f"inputs {input_bytes(shard) / 1e9:.2f} GB per rank > 126 MB L2 (no flush needed)",
+                       "parallelism": f"trace shards: rank r owns traced GPUs g mod {world} == r",
+                       "generation_s": round(t_gen, 1)},
+            "roofline": roof, "cpu_baseline": cpu_b, "e2e": e2e, "full_mode": full_mode,
+            "gpu_launches": launches, "launches_per_step": launches / args.steps,
+            "host_syncs_per_step": syncs / args.steps,
+            "scratch": {"plan_bytes": plan["total"], "high_water_bytes": int(ch.load_library().chopper_scratch_used(pipe.ctx)),
+                        "plan_items": plan},
             "clocks": clocks.summary()}
     print(json.dumps(line))
     pipe.close()

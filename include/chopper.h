@@ -415,6 +415,8 @@ void chopper_destroy(chopper_ctx *ctx);
 
 /* number of device kernels this ctx launched since creation (bench evidence) */
 int64_t chopper_kernel_launches(const chopper_ctx *ctx);
+/* number of host synchronizations with the ctx stream since creation (each waits for the queued work) */
+int64_t chopper_host_syncs(const chopper_ctx *ctx);
 int32_t chopper_abi_version(void);
 
 /* introspection after chopper_align: first name-sequence divergence / first
@@ -428,7 +430,8 @@ int64_t chopper_scratch_used(const chopper_ctx *ctx);
 /* Device timing of pipeline phases with CUDA events recorded on the ctx
  * stream (off by default).  phase: 0 load, 1 align, 2 attribute,
  * 3 overlap prep, 4 event pass (its seed / window / head passes and the main kernel), 5 tables,
- * 6 breakdown, 7 reduce_ranks, 8 the main event-pass kernel alone (k_events_w / k_events).  chopper_phase_time returns 0 and *ms for the most recent
+ * 6 breakdown, 7 reduce_ranks, 8 the main event-pass kernel alone (k_events_w / k_events), 9 the counter-pass kernel
+ * alone (k_counters_tiled, on its side stream; counters only).  chopper_phase_time returns 0 and *ms for the most recent
  * run of that phase, CHOPPER_E_STATE if it was not timed. */
 void chopper_set_timing(chopper_ctx *ctx, int32_t on);
 chopper_status chopper_phase_time(chopper_ctx *ctx, int32_t phase, float *ms);

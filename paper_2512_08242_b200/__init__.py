@@ -159,7 +159,7 @@ EXPORTS = ["chopper_scratch_bytes", "chopper_create", "chopper_load_columns", "c
            "chopper_abi_version", "chopper_pass_mismatch", "chopper_pass_conflict", "chopper_counter_present",
            "chopper_scratch_used", "chopper_set_timing", "chopper_phase_time", "chopper_report_cdf",
            "chopper_cpu_util", "chopper_set_metrics", "chopper_ingest_scratch_bytes", "chopper_ingest_chrome",
-           "chopper_set_allgather", "chopper_loopback_create", "chopper_scratch_plan", "chopper_loopback_destroy",
+           "chopper_set_allgather", "chopper_loopback_create", "chopper_scratch_plan", "chopper_host_syncs", "chopper_loopback_destroy",
            "chopper_loopback_allgather"]
 
 _lib = None
@@ -190,6 +190,7 @@ def load_library() -> ctypes.CDLL:
         "chopper_last_error": (ctypes.c_char_p, [P]),
         "chopper_destroy": (None, [P]),
         "chopper_kernel_launches": (I64, [P]),
+        "chopper_host_syncs": (I64, [P]),
         "chopper_abi_version": (I32, []),
         "chopper_pass_mismatch": (I64, [P, I32]),
         "chopper_pass_conflict": (I64, [P, I32]),
@@ -348,7 +349,7 @@ def chopper_set_timing(ctx, on: bool) -> None:
 
 
 PHASES = ["load", "align", "attribute", "overlap_prep", "event_pass", "tables", "breakdown", "reduce_ranks",
-          "event_kernel"]
+          "event_kernel", "counter_kernel"]
 
 
 def chopper_phase_time(ctx, phase: int) -> Optional[float]:

@@ -490,7 +490,7 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
             m_g.assign(n_lg, 0);
             CH_CUDA(ctx, cudaMemcpyAsync(hmis.data(), mis, 8 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
             CH_CUDA(ctx, cudaMemcpyAsync(m_g.data(), ctx->d_mg, 8 * n_lg, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            CH_CUDA(ctx, ch_sync(ctx));
             ctx->pass_mismatch.assign(n_passes, -1);
             for (int p = 0; p < n_passes; p++) {
                 const PassDesc &d = ctx->passes[p];
@@ -583,7 +583,7 @@ chopper_status ch_assign_slots(chopper_ctx *ctx) {
     if (conflicts) {
         std::vector<unsigned long long> hconf(n_passes);
         CH_CUDA(ctx, cudaMemcpyAsync(hconf.data(), ctx->d_conf, 8 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        CH_CUDA(ctx, ch_sync(ctx));
         for (int p = 0; p < n_passes; p++)
             if (hconf[p] != ~0ull) ctx->pass_conflict[p] = (int64_t)hconf[p];
     }
@@ -650,7 +650,7 @@ chopper_status ch_offsets_launch(chopper_ctx *ctx) {
 chopper_status ch_offsets_finish(chopper_ctx *ctx) {
     const int G = ctx->cfg.n_traced_gpus;
     if (!ctx->off_pending) CH_TRY(ch_offsets_launch(ctx));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));          // (already reached when ch_align synchronized)
+    CH_CUDA(ctx, ch_sync(ctx));          // (already reached when ch_align synchronized)
     ctx->off_pending = false;
     const int nslots = (int)(ctx->off_hdr.size() / 2);
     // gpus absent from every rank keep flag 1 (no events)
@@ -688,6 +688,6 @@ chopper_status ch_exchange_poison(chopper_ctx *ctx, int which) {
     CH_CUDA(ctx, cudaMemcpyAsync(send, &failed, 8, cudaMemcpyHostToDevice, ctx->st));
     if (which == 1) ctx->x_exchanged = true; else ctx->d_exchanged = true;
     CH_TRY(ch_nccl_allgather(ctx, send, recv, sizeof(int64_t) * (size_t)slots * W));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    CH_CUDA(ctx, ch_sync(ctx));
     return CHOPPER_OK;
 }

@@ -459,7 +459,7 @@ chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out) {
 chopper_status chopper_status_sync(chopper_ctx *ctx, uint32_t *mask) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
     uint32_t m = ctx->latched_host;
-    if (cudaStreamSynchronize(ctx->st) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;
+    if (ch_sync(ctx) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;
     if (ctx->d_rep) {
         unsigned int dl = 0;
         if (cudaMemcpy(&dl, &ctx->d_rep->latched, 4, cudaMemcpyDeviceToHost) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;
@@ -490,6 +490,7 @@ void chopper_destroy(chopper_ctx *ctx) {
 }
 
 int64_t chopper_kernel_launches(const chopper_ctx *ctx) { return ctx ? ctx->launches : 0; }
+int64_t chopper_host_syncs(const chopper_ctx *ctx) { return ctx ? ctx->syncs : 0; }
 
 /* extra introspection used by the Python binding / tests */
 int64_t chopper_pass_mismatch(const chopper_ctx *ctx, int32_t p) {
@@ -510,7 +511,7 @@ void chopper_set_timing(chopper_ctx *ctx, int32_t on) {
 }
 
 chopper_status chopper_phase_time(chopper_ctx *ctx, int32_t phase, float *ms) {
-    if (!ctx || !ms || phase < 0 || phase >= 9) return CHOPPER_E_INVALID_ARG;
+    if (!ctx || !ms || phase < 0 || phase >= 10) return CHOPPER_E_INVALID_ARG;
     if (!ctx->timed[phase]) return CHOPPER_E_STATE;
     if (cudaEventSynchronize(ctx->tev[phase][1]) != cudaSuccess) return CHOPPER_E_CUDA;
     if (cudaEventElapsedTime(ms, ctx->tev[phase][0], ctx->tev[phase][1]) != cudaSuccess) return CHOPPER_E_CUDA;

@@ -92,6 +92,7 @@ struct chopper_ctx {
     size_t scratch_bytes = 0, used = 0, high = 0;   // bump arena: bytes in use, high-water mark
     bool hold_scratch = false;       // inside a side-stream branch: temporaries are not released (see tables.cu)
     int64_t launches = 0;
+    int64_t syncs = 0;               // host synchronizations with the ctx stream
     std::string err;
     int stage = 0;                 // 1 loaded, 2 aligned, 3 attributed, 4 overlapped, 5 breakdown
     bool loaded_ok = false;
@@ -125,6 +126,7 @@ struct chopper_ctx {
     std::vector<int64_t> bucket_beg;
     int64_t *d_pred_end = nullptr;   // [N] end of chain predecessor or NONE
     bool full_sort = false;
+    bool lean = false;               // one compute stream per gpu, start-monotone in dispatch order (lean a2)
 
     // spans (push order)
     int64_t S_loc = 0;               // spans of local gpus with positive length
@@ -240,8 +242,8 @@ struct chopper_ctx {
     int32_t *d_has_smp = nullptr;    // [n_lg]
     // phase timing (chopper_set_timing)
     bool timing = false;
-    cudaEvent_t tev[9][2] = {};
-    bool timed[9] = {};
+    cudaEvent_t tev[10][2] = {};
+    bool timed[10] = {};
     int64_t *d_dense = nullptr;      // local dense exchange blocks [dense_slots][W]
     unsigned int *d_dense_ovf = nullptr;
     int64_t *d_all = nullptr;        // all-gathered dense blocks (chopper_reduce_ranks), read by the report CDF
@@ -284,12 +286,18 @@ struct chopper_ctx {
     } while (0)
 
 chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &msg);
-inline void ch_tick(chopper_ctx *ctx, int phase, int end) {
+// host synchronization with the ctx stream (counted: chopper_host_syncs)
+inline cudaError_t ch_sync(chopper_ctx *ctx) {
+    ctx->syncs++;
+    return cudaStreamSynchronize(ctx->st);
+}
+inline void ch_tick_on(chopper_ctx *ctx, int phase, int end, cudaStream_t st) {
     if (!ctx->timing) return;
     if (!ctx->tev[phase][end]) cudaEventCreate(&ctx->tev[phase][end]);
-    cudaEventRecord(ctx->tev[phase][end], ctx->st);
+    cudaEventRecord(ctx->tev[phase][end], st);
     if (end) ctx->timed[phase] = true;
 }
+inline void ch_tick(chopper_ctx *ctx, int phase, int end) { ch_tick_on(ctx, phase, end, ctx->st); }
 chopper_status ch_fill_u64(chopper_ctx *ctx, unsigned long long *p, int64_t n, unsigned long long v);
 
 // ---------------------------------------------------------------------------

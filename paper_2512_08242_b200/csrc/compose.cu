@@ -1096,7 +1096,7 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     if (ctx->d_dense_ovf) CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ctx->d_dense_ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(&n, nref, 8, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(&hpoison, poison, 4, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    CH_CUDA(ctx, ch_sync(ctx));
     if (hpoison) return ch_fail(ctx, CHOPPER_E_STATE, "a peer rank failed earlier in this step (all-gather #2)");
     if (n > 4096) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 4096 iterations in chopper_global");
     if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "iteration rank >= max_iters or op label >= n_labels");
@@ -1118,7 +1118,7 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     out->n_report = nL;
     CH_CUDA(ctx, cudaMemcpyAsync(out->e2e, e2e, 8 * (1 + E2E_W), cudaMemcpyDeviceToHost, ctx->st));
     if (nL > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->report, rep, 8 * 16 * (size_t)nL, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    CH_CUDA(ctx, ch_sync(ctx));
     for (int g = 0; g < ctx->cfg.n_traced_gpus && g < 256; g++) {
         out->delta[g] = ctx->delta[g];
         out->delta_flag[g] = ctx->delta_flag[g];
@@ -1155,7 +1155,7 @@ chopper_status ch_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t
     CH_LAUNCHED(ctx);
     int64_t n = 0;
     CH_CUDA(ctx, cudaMemcpyAsync(&n, tot, 8, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    CH_CUDA(ctx, ch_sync(ctx));
     const int64_t m = n < cap ? n : cap;
     if (m > 0 && out) CH_CUDA(ctx, cudaMemcpy(out, rows, 8 * 5 * (size_t)m, cudaMemcpyDeviceToHost));
     ctx->used = mark;
@@ -1207,7 +1207,7 @@ chopper_status ch_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *S, const
     unsigned int hb[2];
     CH_CUDA(ctx, cudaMemcpyAsync(h, dsum, 8 * 7, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(hb, bad, 8, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    CH_CUDA(ctx, ch_sync(ctx));
     ctx->used = mark;
     if (hb[0]) return ch_fail(ctx, CHOPPER_E_VALIDATION, "CPU samples unsorted or out of range, or a bad topology entry");
     out->n_ts = (int64_t)h[0];

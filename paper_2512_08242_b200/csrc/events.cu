@@ -17,6 +17,8 @@
 // sub-runs with equal keys are merged into instances in tables.cu.
 #include "common.cuh"
 
+#include <cuda.h>
+
 SpanView ch_span_view(chopper_ctx *ctx);
 
 namespace {
@@ -284,6 +286,7 @@ struct EvParams {
     int64_t ntile;
     const int64_t *tile_base;     // [ntile + 1] first sub-run id of each tile
     const struct TileWin *twin;   // [ntile] placed windows
+    const struct TileWinL *twinl; // [ntile] placed windows of the lean pass
 };
 
 
@@ -670,6 +673,7 @@ __device__ __forceinline__ void stage_tile(SM &S, const EvParams &P, int64_t bas
             cp_async16(&S.meta[sw32(u >> 1, u & 1)], P.meta + base + 4 * u);
         }
         cp_async_wait_all();
+        __syncthreads();
     } else {
         // partial or unaligned tile: element-wise, same layout
         for (int e = tid; e < SM::TILE; e += SM::NT) {
@@ -1541,6 +1545,486 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_w(EvParams P, int vec_ok) {
     }
     tile_finish(S, P, has, cur, p0, run0, base);
 }
+
+// =================================================================================================
+// Lean event pass (the FSDP case: every span list laminar, one compute stream per gpu whose kernels are
+// start-monotone in dispatch order -- the lean a2 of load.cu).  Same tiles, head rule, sub-run rows and
+// results as k_events_w, built for the B200 memory system:
+//   * the tile's event columns arrive by TMA: one elected thread issues 2-D tensor loads (t_l, t_ks, t_ke as
+//     [rows of 8 int64], meta as [rows of 8 uint32]) whose hardware 64 B / 32 B swizzle is the thread-blocked
+//     layout ev_col / ev_meta read (thread t owns row t: conflict-free 16 B shared loads), and 1-D bulk copies
+//     (cp.async.bulk) of the key-table and timeline windows; one mbarrier with the transaction byte count;
+//   * the launch chain (a7) needs no predecessor column: on one start-monotone compute stream the predecessor
+//     of a COMPUTE kernel is the previous COMPUTE kernel of its gpu in dispatch order, so each thread carries
+//     the last one's end through its 8 events, takes the value before its first event from a block scan of
+//     (position, end), and the tile's carry-in comes from k_tile_seeds_l (a backward search before the tile);
+//   * per-event outputs are compiled in only for full mode (OUT).
+// =================================================================================================
+constexpr int L_POOL = 28672;          // bytes of staged windows per tile (larger windows: global fallback)
+
+struct TabWinL {
+    int64_t lo, gb, ge, next;  // logical window [lo, lo + n) of the gpu's table [gb, ge); time after it
+    int n, shift, a_n, off;    // copied: a_n entries from lo - shift (16 B-aligned), at byte off of the pool
+};
+struct TileWinL {
+    TabWinL tw[2];
+    int64_t lg;                // local gpu of the tile's first event
+    int64_t pe;                // chain carry: end of the last COMPUTE event of that gpu before the tile, or NONE
+};
+struct EvSmemL {
+    static constexpr int NT = W_NT, TILE = W_TILE, WARPS = W_WARPS;
+    longlong2 col[3][W_TILE / 2];         // t_l, t_ks, t_ke (48 KB), 64 B-swizzled rows (TMA)
+    uint4 meta[W_TILE / 4];               // 8 KB, 32 B-swizzled rows (TMA)
+    uint32_t kidx[EV_IPT][W_NT];          // key of each event as a key-table index (8 KB)
+    unsigned long long lastk[W_NT];
+    Acc wagg[W_WARPS], wcarry[W_WARPS];
+    int wflag[W_WARPS], wcflag[W_WARPS];
+    int wheads[W_WARPS];
+    int32_t wpos[W_WARPS];                // chain scan: last COMPUTE position / end per warp
+    int64_t wend[W_WARPS];
+    int64_t tile, excl;
+    int tot;
+    unsigned long long bar[2];
+    __align__(16) unsigned char pool[L_POOL];
+};
+static_assert(sizeof(EvSmemL) <= 113 * 1024, "two lean event-pass blocks per SM");
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *map, int c0, int c1, unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// per tile (a warp each): the windows' seeds as k_tile_seeds, and the chain carry -- the end of the last COMPUTE
+// event of the tile's first gpu before the tile (NONE when the gpu starts in this tile or has none before)
+__global__ void k_tile_seeds_l(EvParams P, int32_t *__restrict__ seeds, int64_t *__restrict__ tile_pe) {
+    const int lane = threadIdx.x & 31;
+    const int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (tile >= P.ntile) return;
+    const int64_t base = tile * W_TILE, i = base + lane;
+    const uint32_t m0 = P.meta[base];
+    const int lg = P.gpu_lg[gpu_of(m0)];
+    const uint32_t m = i < P.N ? P.meta[i] : 0u;
+    const bool cmp = i < P.N && kind_of(m) == CK_COMPUTE && P.gpu_lg[gpu_of(m)] == lg;
+    const unsigned cm = __ballot_sync(CH_FULL, cmp);
+    int64_t s = 0;
+    if (lane < NTAB) {
+        const int64_t t = lane == 0 ? P.tl[base] : (cm ? P.ks[base + __ffs(cm) - 1] : P.tl[base]);
+        int64_t gb, ge;
+        tab_bounds(P, lane, lg, &gb, &ge);
+        s = last_le(lane == 0 ? P.KTt : P.TLt, gb, ge, t);
+    } else if (lane == NTAB) {
+        s = lg;
+    }
+    if (lane < SEED_W) seeds[tile * SEED_W + lane] = (int32_t)s;
+    // backward search for the chain carry, 32 events per probe
+    int64_t pe = CH_NONE_TS;
+    for (int64_t p = base - 1; p >= 0; p -= 32) {
+        const int64_t q = p - lane;
+        const uint32_t mq = q >= 0 ? P.meta[q] : 0u;
+        const bool other = q < 0 || gpu_of(mq) != gpu_of(m0);
+        const bool hit = !other && kind_of(mq) == CK_COMPUTE;
+        const unsigned hm = __ballot_sync(CH_FULL, hit), om = __ballot_sync(CH_FULL, other);
+        if (hm | om) {
+            const int f = __ffs(hm | om) - 1;
+            if ((hm >> f) & 1u) pe = P.ke[p - f];
+            break;
+        }
+    }
+    if (lane == 0) tile_pe[tile] = pe;
+}
+
+// window placement with 16 B-aligned copies: the key table (times, keys: 2 entries per 16 B) and the timeline
+// (times, 3 intercepts, 3 int32 slopes: 4 entries per 16 B) are copied from an aligned start, the logical
+// window begins `shift` entries in
+__global__ void k_tile_windows_l(EvParams P, const int64_t *__restrict__ tile_pe, TileWinL *__restrict__ out) {
+    const int64_t tile = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tile >= P.ntile) return;
+    const int32_t *sd = P.seeds + tile * SEED_W;
+    const int lg = sd[NTAB];
+    TileWinL r;
+    r.lg = lg;
+    r.pe = tile_pe[tile];
+    int off = 0;
+#pragma unroll
+    for (int x = NTAB - 1; x >= 0; x--) {
+        TabWinL &w = r.tw[x];
+        tab_bounds(P, x, lg, &w.gb, &w.ge);
+        int64_t lo = sd[x], hi = w.ge;
+        if (tile + 1 < P.ntile && sd[SEED_W + NTAB] == lg) {
+            hi = (int64_t)sd[SEED_W + x] + 1 + (x == 1 ? 4 : 0);
+            if (hi < lo + 1) hi = lo + 1;
+            if (hi > w.ge) hi = w.ge;
+        }
+        const int A = x == 0 ? 2 : 4, eb = x == 0 ? KT_B : TL_B;
+        const int shift = (int)(lo & (A - 1));
+        int64_t n = hi - lo;
+        const int64_t fit = ((L_POOL - off) / eb) & ~(int64_t)(A - 1);
+        if (shift + n > fit) n = fit - shift > 0 ? fit - shift : 0;
+        const int a_n = n > 0 ? (int)((shift + n + A - 1) & ~(int64_t)(A - 1)) : 0;
+        w.lo = lo;
+        w.n = (int)n;
+        w.shift = shift;
+        w.a_n = a_n;
+        w.off = off;
+        off += a_n * eb;
+        const int64_t *T = x == 0 ? P.KTt : P.TLt;
+        w.next = lo + n < w.ge ? T[lo + n] : INT64_MAX;
+    }
+    out[tile] = r;
+}
+
+struct WinL {              // a staged window (logical entries [lo, lo + n)) of one table, or global only (n = 0)
+    const int64_t *T;      // logical times
+    const int64_t *G;      // global times
+    int64_t lo, gb, ge, next;
+    int n, stride, shift;  // payload column stride (entries) in the pool; logical start - aligned copy start
+};
+__device__ __forceinline__ WinL winl_reg(const TabWinL &w, const EvSmemL &S, int x, const EvParams &P) {
+    WinL r;
+    r.T = reinterpret_cast<const int64_t *>(S.pool + w.off) + w.shift;
+    r.G = x == 0 ? P.KTt : P.TLt;
+    r.lo = w.lo;
+    r.n = w.n;
+    r.stride = w.a_n;
+    r.shift = w.shift;
+    r.gb = w.gb;
+    r.ge = w.ge;
+    r.next = w.next;
+    return r;
+}
+__device__ __forceinline__ WinL winl_global(const EvParams &P, int x, int lg) {
+    WinL r;
+    r.T = nullptr;
+    r.G = x == 0 ? P.KTt : P.TLt;
+    r.lo = 0;
+    r.n = 0;
+    r.stride = 0;
+    r.shift = 0;
+    const longlong2 b = x == 0 ? tab_bounds_ool(P.kt_beg, nullptr, lg) : tab_bounds_ool(P.tl_beg, P.tl_len, lg);
+    r.gb = b.x;
+    r.ge = b.y;
+    r.next = INT64_MAX;
+    return r;
+}
+__device__ __forceinline__ bool winl_in(const WinL &w, int64_t j) { return (uint64_t)(j - w.lo) < (uint64_t)w.n; }
+__device__ __forceinline__ bool winl_seek(const WinL &w, WCur &k, int64_t t) {
+    if (t >= k.a && t < k.b) return false;
+    int c = (int)(k.j - w.lo);
+    if (!(winl_in(w, k.j) && t >= k.a)) {
+        c = -1;
+        if (w.n > 0 && w.T[0] <= t) {
+            int l = 1, h = w.n;
+            while (l < h) {
+                const int mm = (l + h) >> 1;
+                if (w.T[mm] <= t) l = mm + 1; else h = mm;
+            }
+            c = l - 1;
+        }
+    }
+    if (c >= 0) {
+        while (c + 1 < w.n && w.T[c + 1] <= t) c++;
+        if (c + 1 < w.n) { k.j = w.lo + c; k.a = w.T[c]; k.b = w.T[c + 1]; return true; }
+        if (t < w.next) { k.j = w.lo + c; k.a = w.T[c]; k.b = w.next; return true; }
+    }
+    const longlong2 r = seek_global(w.G, w.T, w.lo, w.n, w.gb, w.ge, k.j, t);
+    k.j = r.x;
+    k.a = winl_in(w, r.x) ? w.T[r.x - w.lo] : __ldg(w.G + r.x);
+    k.b = r.y;
+    return true;
+}
+__device__ __forceinline__ unsigned long long keyl_at(const WinL &w, const EvParams &P, int64_t j) {
+    return winl_in(w, j) ? reinterpret_cast<const unsigned long long *>(w.T + w.stride)[j - w.lo] : __ldg(P.KTk + j);
+}
+__device__ __forceinline__ TlEnt tll_ent(const WinL &w, const EvParams &P, int64_t j) {
+    TlEnt e;
+    if (winl_in(w, j)) {
+        // copy layout (from the aligned start): times, 3 intercept columns (int64), 3 slope columns (int32), each
+        // column `stride` entries; T is the logical start, so every column is offset by the same shift
+        const int c = (int)(j - w.lo), st = w.stride;
+        const int64_t *v = w.T + st;
+        e.v0 = v[c]; e.v1 = v[st + c]; e.v2 = v[2 * st + c];
+        const int32_t *s0 = reinterpret_cast<const int32_t *>(w.T - w.shift + 4 * st) + w.shift;
+        e.s0 = s0[c]; e.s1 = s0[st + c]; e.s2 = s0[2 * st + c];
+    } else {
+        const int64_t cap = P.tl_cap;
+        e.v0 = __ldg(P.TLv + j); e.v1 = __ldg(P.TLv + cap + j); e.v2 = __ldg(P.TLv + 2 * cap + j);
+        e.s0 = __ldg(P.TLs + j); e.s1 = __ldg(P.TLs + cap + j); e.s2 = __ldg(P.TLs + 2 * cap + j);
+    }
+    return e;
+}
+
+// element k of thread t in the TMA-swizzled rows (k is a constant after unrolling: one LOP for the swizzle)
+__device__ __forceinline__ int64_t rcol(const EvSmemL &S, int c, int t, int x64, int k) {
+    return reinterpret_cast<const int64_t *>(&S.col[c][t * 4 + ((k >> 1) ^ x64)])[k & 1];
+}
+__device__ __forceinline__ uint32_t rmeta(const EvSmemL &S, int t, int x32, int k) {
+    return reinterpret_cast<const uint32_t *>(&S.meta[t * 2 + ((k >> 2) ^ x32)])[k & 3];
+}
+// the window of table x for gpu g: the staged one for the tile's gpu, else the gpu's table in global memory
+// (inline: a non-inlined callee taking EvParams by reference would force a stack copy of the whole struct)
+__device__ __forceinline__ WinL winl_for(const EvParams &P, int x, int g, int lgP, const WinL &staged) {
+    const int lg = P.gpu_lg[g];
+    return lg == lgP ? staged : winl_global(P, x, lg);
+}
+
+template <bool OUT>
+__global__ void __launch_bounds__(W_NT, 2) k_events_l(EvParams P, const __grid_constant__ CUtensorMap tm_tl,
+                                                      const __grid_constant__ CUtensorMap tm_ks,
+                                                      const __grid_constant__ CUtensorMap tm_ke,
+                                                      const __grid_constant__ CUtensorMap tm_meta) {
+    extern __shared__ __align__(1024) unsigned char evl_dsm[];
+    EvSmemL &S = *reinterpret_cast<EvSmemL *>(evl_dsm);       // the TMA swizzle needs a 1024 B-aligned base
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t tile = blockIdx.x;
+    const int64_t base = tile * W_TILE;
+    const int64_t i0 = base + (int64_t)tid * EV_IPT;
+    const int64_t N = P.N;
+    // ---- staging: the columns by TMA (warp 0) and the key-table / timeline windows by bulk copies (warps 1, 2)
+    // on two mbarriers; every thread reads the tile's scalars and window descriptors itself (broadcast loads),
+    // so nobody waits at a barrier for another thread's global loads ----
+    if (tid == 0) {
+        if (smem_u32(evl_dsm) & 1023u) __trap();
+        mbar_init(&S.bar[0], 1);
+        mbar_init(&S.bar[1], 2);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const TileWinL *twp = P.twinl + tile;
+    if (tid == 0) {
+        mbar_arrive_tx(&S.bar[0], 3u * 16384u + 8192u);
+        const int row = (int)(base >> 3);
+        tma_2d(&S.col[0][0], &tm_tl, 0, row, &S.bar[0]);
+        tma_2d(&S.col[1][0], &tm_ks, 0, row, &S.bar[0]);
+        tma_2d(&S.col[2][0], &tm_ke, 0, row, &S.bar[0]);
+        tma_2d(&S.meta[0], &tm_meta, 0, row, &S.bar[0]);
+        S.excl = P.tile_base[tile];
+        S.tot = (int)(P.tile_base[tile + 1] - P.tile_base[tile]);
+    } else if (tid == 32) {
+        const TabWinL k = twp->tw[0];
+        mbar_arrive_tx(&S.bar[1], (unsigned)k.a_n * KT_B);
+        if (k.a_n > 0) {
+            unsigned char *b = S.pool + k.off;
+            const int64_t a0 = k.lo - k.shift;
+            bulk_g2s(b, P.KTt + a0, 8u * k.a_n, &S.bar[1]);
+            bulk_g2s(b + 8 * k.a_n, P.KTk + a0, 8u * k.a_n, &S.bar[1]);
+        }
+    } else if (tid == 64) {
+        const TabWinL t = twp->tw[1];
+        mbar_arrive_tx(&S.bar[1], (unsigned)t.a_n * TL_B);
+        if (t.a_n > 0) {
+            unsigned char *b = S.pool + t.off;
+            const int64_t a0 = t.lo - t.shift, cap = P.tl_cap;
+            const unsigned n8 = 8u * t.a_n, n4 = 4u * t.a_n;
+            bulk_g2s(b, P.TLt + a0, n8, &S.bar[1]);
+            bulk_g2s(b + n8, P.TLv + a0, n8, &S.bar[1]);
+            bulk_g2s(b + 2 * n8, P.TLv + cap + a0, n8, &S.bar[1]);
+            bulk_g2s(b + 3 * n8, P.TLv + 2 * cap + a0, n8, &S.bar[1]);
+            bulk_g2s(b + 4 * n8, P.TLs + a0, n4, &S.bar[1]);
+            bulk_g2s(b + 4 * n8 + n4, P.TLs + cap + a0, n4, &S.bar[1]);
+            bulk_g2s(b + 4 * n8 + 2 * n4, P.TLs + 2 * cap + a0, n4, &S.bar[1]);
+        }
+    }
+    const int lgP = (int)twp->lg;
+    const int gP = gpu_of(__ldg(P.meta + base));
+    mbar_wait(&S.bar[0], 0);
+    mbar_wait(&S.bar[1], 0);
+    const int nv = i0 >= N ? 0 : (int)min((int64_t)EV_IPT, N - i0);
+    const int x64 = (tid >> 1) & 3, x32 = (tid >> 2) & 1;
+    if (nv > 0 && nv < EV_IPT) {
+        // the last partial row (N % 8 events) lies outside the tensor maps: this thread fills it in
+        for (int k = 0; k < nv; k++) {
+            const int64_t i = i0 + k;
+            reinterpret_cast<int64_t *>(&S.col[0][tid * 4 + ((k >> 1) ^ x64)])[k & 1] = P.tl[i];
+            reinterpret_cast<int64_t *>(&S.col[1][tid * 4 + ((k >> 1) ^ x64)])[k & 1] = P.ks[i];
+            reinterpret_cast<int64_t *>(&S.col[2][tid * 4 + ((k >> 1) ^ x64)])[k & 1] = P.ke[i];
+            reinterpret_cast<uint32_t *>(&S.meta[tid * 2 + ((k >> 2) ^ x32)])[k & 3] = P.meta[i];
+        }
+    }
+    const WinL wkP = winl_reg(twp->tw[0], S, 0, P);
+
+    // ---- phase A: instance key per event (a5) and the thread's last COMPUTE kernel (a7 chain) ----
+    unsigned hmask = 0;
+    unsigned long long firstk = CH_INVALID_KEY;
+    int32_t lpos = -1;                         // tile offset of the thread's last COMPUTE event
+    int64_t lend = 0;
+    {
+        WinL wk = wkP;
+        int gc = gP;
+        WCur ck;
+        wcur_init(ck);
+        unsigned long long prevk = CH_INVALID_KEY;
+        int64_t prevj = -1;
+#pragma unroll 1
+        for (int k = 0; k < EV_IPT; k++) {
+            uint32_t v = KIDX_NONE;
+            if (k < nv) {
+                const int64_t t = rcol(S, 0, tid, x64, k);
+                const uint32_t m = rmeta(S, tid, x32, k);
+                const int g = gpu_of(m);
+                if (g != gc) { wk = winl_for(P, 0, g, lgP, wkP); wcur_init(ck); gc = g; }
+                if (!(t < ck.b && t >= ck.a)) winl_seek(wk, ck, t);
+                v = (uint32_t)ck.j;
+                if (ck.j != prevj) {                  // same entry => same key; else compare the keys
+                    const unsigned long long kk = keyl_at(wk, P, ck.j);
+                    if (k > 0 && kk != prevk) hmask |= 1u << k;
+                    prevk = kk;
+                    prevj = ck.j;
+                }
+                if (kind_of(m) == CK_COMPUTE) { lpos = tid * EV_IPT + k; lend = rcol(S, 2, tid, x64, k); }
+            } else {
+                prevk = CH_INVALID_KEY;
+                prevj = -1;
+            }
+            if (k == 0) firstk = prevk;
+            S.kidx[k][tid] = v;
+        }
+        S.lastk[tid] = prevk;
+    }
+    // chain scan: the last COMPUTE event before this thread (position, end); the later position wins
+    int32_t xpos = lpos;
+    int64_t xend = lend;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t yp = __shfl_up_sync(CH_FULL, xpos, o);
+        const int64_t ye = __shfl_up_sync(CH_FULL, xend, o);
+        if (lane >= o && yp > xpos) { xpos = yp; xend = ye; }
+    }
+    if (lane == 31) { S.wpos[warp] = xpos; S.wend[warp] = xend; }
+    __syncthreads();
+    int tot;
+    const int ex = tile_head_scan_h(S, hmask, nv > 0 && (tid == 0 || firstk != S.lastk[tid - 1]), &tot);
+    const int64_t run0 = S.excl + ex;
+    int32_t ppos = __shfl_up_sync(CH_FULL, xpos, 1);
+    int64_t pend = __shfl_up_sync(CH_FULL, xend, 1);
+    if (lane == 0) { ppos = -1; pend = 0; }
+    for (int w = warp - 1; w >= 0 && ppos < 0; w--)
+        if (S.wpos[w] >= 0) { ppos = S.wpos[w]; pend = S.wend[w]; }
+    // the predecessor of the thread's first COMPUTE event: an earlier one in the tile (its gpu), else the tile
+    // carry, which belongs to the tile's first gpu
+    int pgpu;
+    if (ppos >= 0) {
+        const int pt = ppos >> 3, pk = ppos & 7;
+        pgpu = gpu_of(reinterpret_cast<const uint32_t *>(&S.meta[pt * 2 + ((pk >> 2) ^ ((pt >> 2) & 1))])[pk & 3]);
+    } else {
+        pend = twp->pe;
+        pgpu = pend == CH_NONE_TS ? -1 : gP;
+    }
+
+    // ---- phase B: per-event values (a6-a8), thread-sequential folding (a9) ----
+    Acc cur, p0;
+    cur.zero();
+    p0.zero();
+    bool has = false;
+    int64_t curid = run0 - 1;
+    const WinL wtP = winl_reg(twp->tw[1], S, 1, P);
+    WinL wt = wtP;
+    int gc = gP;
+    WCur ct;
+    wcur_init(ct);
+    TlEnt te{};
+    int32_t *const o_run = P.o_run;
+    const int64_t t0 = P.t0, cap = P.cap;
+#pragma unroll 1
+    for (int k = 0; k < EV_IPT; k++) {
+        if (k < nv) {
+            const int64_t i = i0 + k;
+            const uint32_t m = rmeta(S, tid, x32, k);
+            const int g = gpu_of(m);
+            if ((hmask >> k) & 1u) {
+                if (!has) { p0 = cur; has = true; }
+                else write_subrun(P, curid, cur, base);
+                curid++;
+                cur.zero();
+                const uint32_t v = S.kidx[k][tid];
+                if (curid < cap) {
+                    P.sr_key[curid] = keyl_at(g == gP ? wkP : winl_for(P, 0, g, lgP, wkP), P, (int64_t)v);
+                    P.sr_first[curid] = i;
+                }
+            }
+            const int kd = kind_of(m);
+            const int64_t ks = rcol(S, 1, tid, x64, k), ke = rcol(S, 2, tid, x64, k);
+            const int64_t dur = ke - ks;
+            int64_t ovl = 0, prep = 0, call = 0, phi = 0, psi = 0;
+            cur.nev += 1;
+            if (kd == CK_COMPUTE) {
+                if (pgpu == g) {
+                    const int64_t tl = rcol(S, 0, tid, x64, k);
+                    const int64_t t2 = tl < ks ? tl : ks;              // D6: dispatch clamped to start
+                    const int64_t a = t2 - pend;
+                    prep = a > 0 ? a : 0;                               // Eq. 1
+                    const int64_t c1 = ks - t2, c2 = ks - pend;
+                    const int64_t c = c1 < c2 ? c1 : c2;                // Eq. 2
+                    call = c > 0 ? c : 0;
+                }
+                pgpu = g;
+                pend = ke;
+                if (g != gc) { wt = winl_for(P, 1, g, lgP, wtP); wcur_init(ct); gc = g; }
+                if (!(ks < ct.b && ks >= ct.a) && winl_seek(wt, ct, ks)) te = tll_ent(wt, P, ct.j);
+                if (ke < ct.b) {
+                    ovl = te.s0 ? dur : 0;                              // |[t_ks, t_ke) ∩ U_g| (D9)
+                    phi = (int64_t)te.s1 * dur;                         // MHz*ns (D10)
+                    psi = (int64_t)te.s2 * dur;                         // mW*ns
+                } else {
+                    const unsigned long long ua = (unsigned long long)(ks - t0);
+                    const unsigned long long ca = te.v0 + (te.s0 ? ua : 0ull);
+                    const unsigned long long fa = te.v1 + (unsigned long long)(int64_t)te.s1 * ua;
+                    const unsigned long long pa = te.v2 + (unsigned long long)(int64_t)te.s2 * ua;
+                    winl_seek(wt, ct, ke);
+                    te = tll_ent(wt, P, ct.j);
+                    const unsigned long long ub = (unsigned long long)(ke - t0);
+                    ovl = (int64_t)(te.v0 + (te.s0 ? ub : 0ull) - ca);
+                    phi = (int64_t)(te.v1 + (unsigned long long)(int64_t)te.s1 * ub - fa);
+                    psi = (int64_t)(te.v2 + (unsigned long long)(int64_t)te.s2 * ub - pa);
+                }
+                cur.n += 1;
+                cur.busy += dur;
+                cur.prep += prep;
+                cur.call += call;
+                cur.ovl += ovl;
+                cur.phi += phi;
+                cur.psi += psi;
+                if (ks < cur.fks) {                  // one start-monotone stream: the first COMPUTE event wins
+                    cur.fks = ks;
+                    cur.foff = tid * EV_IPT + k;
+                }
+                if (ke > cur.lke) cur.lke = ke;
+            } else {
+                if (kd == CK_COPY || kd == CK_OTHER) cur.copy += dur;
+                else if (kd == CK_AG) cur.ag += dur;
+                else if (kd == CK_RS) cur.rs += dur;
+            }
+            if (OUT) {
+                if (P.o_ovl && !is_comm(kd)) P.o_ovl[i] = ovl;
+                if (P.o_prep) P.o_prep[i] = prep;
+                if (P.o_call) P.o_call[i] = call;
+                if (P.o_phi) P.o_phi[i] = phi;
+                if (P.o_psi) P.o_psi[i] = psi;
+            }
+            if (o_run) o_run[i] = (int32_t)curid;
+        }
+    }
+    tile_finish(S, P, has, cur, p0, run0, base);
+}
 }  // namespace
 
 chopper_status ch_overlap_prep(chopper_ctx *ctx) {
@@ -1651,10 +2135,13 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
             off += 1 + 2 * nc[l] + (ctx->smp_hi[l] - ctx->smp_lo[l]);
         }
         tb[n_lg] = off;
-        ctx->tl_cap = off;
-        ctx->TL_t = CH_ALLOC(ctx, int64_t, off);
-        ctx->TL_v = CH_ALLOC(ctx, int64_t, 3 * off);
-        ctx->TL_s = CH_ALLOC(ctx, int32_t, 3 * off);
+        // column stride a multiple of 4 entries: every column starts 16 B-aligned (bulk window copies); + 8
+        // entries of padding so an aligned copy may read past a gpu's last entry
+        const int64_t cap = (off + 3) & ~(int64_t)3;
+        ctx->tl_cap = cap;
+        ctx->TL_t = CH_ALLOC(ctx, int64_t, cap + 8);
+        ctx->TL_v = CH_ALLOC(ctx, int64_t, 3 * cap + 8);
+        ctx->TL_s = CH_ALLOC(ctx, int32_t, 3 * cap + 8);
         ctx->d_tl_beg = CH_ALLOC(ctx, int64_t, n_lg + 1);
         ctx->d_tl_len = CH_ALLOC(ctx, int64_t, n_lg + 1);
         int64_t *dnc = CH_ALLOC(ctx, int64_t, n_lg + 1);
@@ -1664,7 +2151,7 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
         k_timeline<<<(unsigned)ceil_div(off, NT), NT, 0, ctx->st>>>(
             ctx->d_tl_beg, dnc, n_lg, off, ctx->U_s, ctx->U_e, ctx->U_P, ctx->d_U_beg, ctx->d_U_cnt, ctx->smp.ts_ns,
             ctx->d_smp_phi, ctx->d_smp_psi, ctx->smp.freq_mhz, ctx->smp.power_mw, ctx->d_smp_lo, ctx->d_smp_hi, ctx->t0,
-            off, ctx->TL_t, ctx->TL_v, ctx->TL_s, ctx->d_tl_len);
+            cap, ctx->TL_t, ctx->TL_v, ctx->TL_s, ctx->d_tl_len);
         CH_LAUNCHED(ctx);
     }
     // lg -> has samples (breakdown flag)
@@ -1676,6 +2163,37 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_has_smp, hs.data(), 4 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
     }
     return CHOPPER_OK;
+}
+
+// 2-D tensor map of an event column as [N / 8 rows][8 elements] (one row per thread of the lean pass), box of
+// 256 rows, with the 64 B (int64) / 32 B (uint32) swizzle that matches ev_col / ev_meta
+typedef CUresult (*encode_tiled_fn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                    const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static encode_tiled_fn tensor_map_encoder() {
+    static encode_tiled_fn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (encode_tiled_fn)p;
+    }
+    return fn;
+}
+static bool column_map(CUtensorMap *m, const void *col, int64_t n, int elem) {
+    encode_tiled_fn enc = tensor_map_encoder();
+    if (!enc || ((uintptr_t)col & 15u) || n < 8) return false;
+    const cuuint64_t dims[2] = {8, (cuuint64_t)(n / 8)};
+    const cuuint64_t strides[1] = {(cuuint64_t)8 * elem};
+    const cuuint32_t box[2] = {8, W_NT};
+    const cuuint32_t es[2] = {1, 1};
+    return enc(m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void *>(col),
+               dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               elem == 8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int64_t *call, int64_t *phi, int64_t *psi) {
@@ -1730,7 +2248,54 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     // 16 B cp.async staging needs 16 B aligned event columns (tile bases are multiples of 2048 events)
     auto al16 = [](const void *p) { return ((uintptr_t)p & 15u) == 0; };
     int vec_ok = al16(P.tl) && al16(P.ks) && al16(P.ke) && al16(P.pred_end) && al16(P.meta);
-    if (ctx->et_ok) {
+    CUtensorMap tm[4];
+    // CHOPPER_EVENT_PASS=general forces the window-staged general pass (k_events_w) on lean traces (A/B runs)
+    static const bool force_general = getenv("CHOPPER_EVENT_PASS") && !strcmp(getenv("CHOPPER_EVENT_PASS"), "general");
+    const bool lean_pass = ctx->et_ok && ctx->lean && !force_general &&
+                           column_map(&tm[0], P.tl, N, 8) && column_map(&tm[1], P.ks, N, 8) &&
+                           column_map(&tm[2], P.ke, N, 8) && column_map(&tm[3], P.meta, N, 4);
+    if (lean_pass) {
+        // the lean pass: TMA staging, launch chain from the tile (no predecessor column)
+        ntile = ceil_div(N, W_TILE);
+        P.ntile = ntile;
+        size_t mark = ctx->used;
+        int32_t *seeds = CH_ALLOC(ctx, int32_t, ntile * SEED_W);
+        int64_t *tpe = CH_ALLOC(ctx, int64_t, ntile + 1);
+        int64_t *tcnt = CH_ALLOC(ctx, int64_t, ntile + 1), *tbase = CH_ALLOC(ctx, int64_t, ntile + 1);
+        TileWin *twin = CH_ALLOC(ctx, TileWin, ntile);
+        TileWinL *twinl = CH_ALLOC(ctx, TileWinL, ntile);
+        CH_ALLOC_END(ctx);
+        P.seeds = seeds;
+        const size_t dsm = sizeof(EvSmemL);
+        static bool attr_l = false;
+        if (!attr_l) {
+            CH_CUDA(ctx, cudaFuncSetAttribute(k_events_l<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+            CH_CUDA(ctx, cudaFuncSetAttribute(k_events_l<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+            attr_l = true;
+        }
+        ch_tick(ctx, 4, 0);
+        k_tile_seeds_l<<<(unsigned)ceil_div(ntile * 32, NT), NT, 0, ctx->st>>>(P, seeds, tpe);
+        CH_LAUNCHED(ctx);
+        k_tile_windows<<<(unsigned)ceil_div(ntile, NT), NT, 0, ctx->st>>>(P, twin);
+        CH_LAUNCHED(ctx);
+        k_tile_windows_l<<<(unsigned)ceil_div(ntile, NT), NT, 0, ctx->st>>>(P, tpe, twinl);
+        CH_LAUNCHED(ctx);
+        P.twin = twin;
+        P.twinl = twinl;
+        k_tile_heads<<<(unsigned)ntile, W_NT, 0, ctx->st>>>(P, tcnt);
+        CH_LAUNCHED(ctx);
+        CH_TRY(ch_scan_excl_i64(ctx, tcnt, tbase, ntile, tbase + ntile));
+        P.tile_base = tbase;
+        const bool out = ovl || prep || call || phi || psi;
+        ch_tick(ctx, 8, 0);
+        if (out) k_events_l<true><<<(unsigned)ntile, W_NT, dsm, ctx->st>>>(P, tm[0], tm[1], tm[2], tm[3]);
+        else k_events_l<false><<<(unsigned)ntile, W_NT, dsm, ctx->st>>>(P, tm[0], tm[1], tm[2], tm[3]);
+        CH_LAUNCHED(ctx);
+        ch_tick(ctx, 8, 1);
+        ch_tick(ctx, 4, 1);
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_tile_state + ntile - 1, tbase + ntile, 8, cudaMemcpyDeviceToDevice, ctx->st));
+        ctx->used = mark;
+    } else if (ctx->et_ok) {
         // every span list laminar: Euler boundary tables, window-staged lookups
         ntile = ceil_div(N, W_TILE);
         P.ntile = ntile;
@@ -1784,7 +2349,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     }
     unsigned long long last = 0;
     CH_CUDA(ctx, cudaMemcpyAsync(&last, ctx->d_tile_state + ntile - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    CH_CUDA(ctx, ch_sync(ctx));
     ctx->R = (int64_t)(last & VAL_MASK);
     if (ctx->R > cap) return ch_fail(ctx, CHOPPER_E_RANGE, "sub-runs exceed their structural bound");
     // sentinel: sub-run R begins at N

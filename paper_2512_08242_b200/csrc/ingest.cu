@@ -626,7 +626,7 @@ chopper_status ch_ingest_chrome(chopper_ctx *ctx, const char *js, int64_t L, voi
         }
         int64_t h3[3];
         CH_CUDA(ctx, cudaMemcpyAsync(h3, tot, 24, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        CH_CUDA(ctx, ch_sync(ctx));
         h3[1] -= (int64_t)JC * nch;
         if ((h3[0] & 1) || h3[1] != 0)
             return ch_fail(ctx, CHOPPER_E_VALIDATION, "JSON: unbalanced strings or brackets (quotes " +
@@ -681,7 +681,7 @@ chopper_status ch_ingest_chrome(chopper_ctx *ctx, const char *js, int64_t L, voi
         CH_CUDA(ctx, cudaMemcpyAsync(h7, tot, 56, cudaMemcpyDeviceToHost, ctx->st));
         CH_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->st));
         CH_CUDA(ctx, cudaMemcpyAsync(hk, key, 32, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        CH_CUDA(ctx, ch_sync(ctx));
         const int64_t nk = h7[4], nf = h7[5], ns = h7[6];
         rep->n_objects = h7[3];
         rep->n_kernels = nk;
@@ -734,7 +734,7 @@ chopper_status ch_ingest_chrome(chopper_ctx *ctx, const char *js, int64_t L, voi
             k_hash_uniq<<<gk, NT, 0, ctx->st>>>(hs, hv, nk, hf, hex, uh, ufirst, uidx);
             CH_LAUNCHED(ctx);
             CH_CUDA(ctx, cudaMemcpyAsync(&nu, tot + 6, 8, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            CH_CUDA(ctx, ch_sync(ctx));
             bool alt2 = false;
             CH_TRY(ch_radix_sort(ctx, ufirst, uidx, uf2, ui2, nu, 0, bits_for((uint64_t)std::max<int64_t>(nk, 1)), &alt2));
             k_hash_rank<<<(unsigned)ceil_div(std::max<int64_t>(nu, 1), NT), NT, 0, ctx->st>>>(alt2 ? ui2 : uidx, nu, uid);
@@ -744,7 +744,7 @@ chopper_status ch_ingest_chrome(chopper_ctx *ctx, const char *js, int64_t L, voi
             CH_LAUNCHED(ctx);
             unsigned long long hm[3];
             CH_CUDA(ctx, cudaMemcpyAsync(hm, key + 4, 24, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            CH_CUDA(ctx, ch_sync(ctx));
             rep->n_missing = (int64_t)hm[0];
             const int64_t tmin = dec_i64(hm[1]), tmax = dec_i64(hm[2]);
             const int tsbits = bits_for((uint64_t)(tmax - tmin));
@@ -763,7 +763,7 @@ chopper_status ch_ingest_chrome(chopper_ctx *ctx, const char *js, int64_t L, voi
             CH_LAUNCHED(ctx);
         }
         CH_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        CH_CUDA(ctx, ch_sync(ctx));
         if (hbad) return ch_fail(ctx, CHOPPER_E_VALIDATION, "ingest: span gpu or level out of range");
         return CHOPPER_OK;
     }();

@@ -511,7 +511,7 @@ chopper_status ch_fill_u64(chopper_ctx *ctx, unsigned long long *p, int64_t n, u
 
 static chopper_status read_report(chopper_ctx *ctx) {
     CH_CUDA(ctx, cudaMemcpyAsync(&ctx->h_rep, ctx->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+    CH_CUDA(ctx, ch_sync(ctx));
     return CHOPPER_OK;
 }
 
@@ -582,7 +582,7 @@ static chopper_status sort_segments(chopper_ctx *ctx, std::vector<int64_t> seg_l
         CH_TRY(ch_scan_excl_i64(ctx, c64, cst, cells, nullptr));
         unsigned int hfail = 0;
         CH_CUDA(ctx, cudaMemcpyAsync(&hfail, fail, 4, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        CH_CUDA(ctx, ch_sync(ctx));
         if (!hfail) {
             k_ss_rank<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, cnt, cst, dlo,
                                                                         ctx->d_perm);
@@ -688,10 +688,14 @@ chopper_status ch_load(chopper_ctx *ctx) {
     ctx->d_bucket_beg = CH_ALLOC(ctx, int64_t, ctx->n_buckets + 1);
     CH_ALLOC_END(ctx);
     const int NG = ctx->NG, other = NG - 1;
+    ctx->lean = false;
     if (!ctx->multi_stream && ctx->n_buckets <= 1024) {
         bool fell_back = false;
         CH_TRY(lean_a2(ctx, &fell_back));
-        if (!fell_back) return finish_load(ctx);
+        if (!fell_back) {
+            ctx->lean = true;          // compute kernels of every gpu are start-monotone in dispatch order
+            return finish_load(ctx);
+        }
     }
     size_t mark = ctx->used;
     if (ctx->n_buckets <= 256) {

@@ -504,7 +504,7 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         unsigned int hbig = 0;
         CH_CUDA(ctx, cudaMemcpyAsync(&hbig, big, 4, cudaMemcpyDeviceToHost, ctx->st));
         CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), lb2, 8 * (n_lists + 1), cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        CH_CUDA(ctx, ch_sync(ctx));
         if (hbig) {
             // very long runs of equal starts: exact two-sort path (end desc, then (list, start) stable)
             k_span_key1<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, S, emax, k1, v1);
@@ -520,7 +520,7 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
             order = alt ? vo : vs;
             CH_TRY(gather(order));
             CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), lb2, 8 * (n_lists + 1), cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            CH_CUDA(ctx, ch_sync(ctx));
         }
         ctx->used = mark;
         ctx->list_beg[n_lists + 1] = S;
@@ -591,7 +591,7 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->list_flags.data(), ctx->d_list_flags, 4 * n_lists, cudaMemcpyDeviceToHost,
                                      ctx->st));
         CH_CUDA(ctx, cudaMemcpyAsync(&h_et_bad, et_bad, 4, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        CH_CUDA(ctx, ch_sync(ctx));
         ctx->used = mark;
     }
     // exact sweep for non-laminar lists
@@ -602,8 +602,8 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
     ctx->et_ok = sweep.empty() && h_et_bad == 0;
     if (ctx->et_ok) {
         const int64_t nkt = 2 * SL + n_lg;
-        ctx->KT_t = CH_ALLOC(ctx, int64_t, nkt);
-        ctx->KT_k = CH_ALLOC(ctx, unsigned long long, nkt);
+        ctx->KT_t = CH_ALLOC(ctx, int64_t, nkt + 8);              // + 8: 16 B-aligned bulk copies of windows
+        ctx->KT_k = CH_ALLOC(ctx, unsigned long long, nkt + 8);
         ctx->d_kt_beg = CH_ALLOC(ctx, int64_t, n_lg + 1);
         CH_ALLOC_END(ctx);
         std::vector<int64_t> kb(n_lg + 1);

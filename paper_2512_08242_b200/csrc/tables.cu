@@ -1405,10 +1405,12 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         // touches the counter sums); it is joined before the sub-run -> instance sum
         CH_CUDA(ctx, cudaEventRecord(ctx->fork_ev, ctx->st));
         CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[0], ctx->fork_ev, 0));
+        ch_tick_on(ctx, 9, 0, ctx->side[0]);
         k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->side[0]>>>(
             ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, ctx->N, subv.cnt, subv.ccap,
             ctx->d_colbad, vec_ok, n_lg);
         CH_LAUNCHED(ctx);
+        ch_tick_on(ctx, 9, 1, ctx->side[0]);
         CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[0], ctx->side[0]));
         counters_forked = true;
     }
@@ -1436,7 +1438,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
             CH_LAUNCHED(ctx);
             unsigned int hbad = 0;
             CH_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+            CH_CUDA(ctx, ch_sync(ctx));
             if (!hbad) {
                 static bool ss_attr = false;
                 if (!ss_attr) {
@@ -1599,7 +1601,7 @@ chopper_status ch_tables(chopper_ctx *ctx) {
             CH_CUDA(ctx, cudaMemcpyAsync(cb.data(), ctx->d_colbad, 4 * (size_t)n_lg * C, cudaMemcpyDeviceToHost, ctx->st));
         if (n_passes > 0)
             CH_CUDA(ctx, cudaMemcpyAsync(pb.data(), ctx->d_pass_bad, 4 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaStreamSynchronize(ctx->st));
+        CH_CUDA(ctx, ch_sync(ctx));
         for (int q = 0; q < 6; q++) tabs[q]->n = hn[q];
         if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "op span label >= n_labels");
         bool changed = false;

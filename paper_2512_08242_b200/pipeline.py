@@ -379,6 +379,9 @@ class Pipeline:
     def launches(self) -> int:
         return chopper_kernel_launches(self.ctx) if self.ctx else 0
 
+    def host_syncs(self) -> int:
+        return int(load_library().chopper_host_syncs(self.ctx)) if self.ctx else 0
+
     def close(self):
         if self.ctx:
             chopper_destroy(self.ctx)
