@@ -317,6 +317,128 @@ __global__ void __launch_bounds__(RX_NT) k_rx_downsweep(KS ks, const unsigned lo
         vals_out[pos] = sv[j];
     }
 }
+
+// ---- onesweep radix sort (one launch per digit pass) ---------------------------------------------------
+// All digit histograms come from one read of the keys (k_rx_hist); each pass is one kernel: tiles are taken in
+// ticket order, rank their keys locally (warp match, as the downsweep above), publish their per-digit counts and
+// find, per digit, the count of that digit in all earlier tiles by a decoupled look-back (thread d walks back
+// over digit d's tile states until an inclusive prefix); the tile is then staged in shared memory in (digit,
+// input) order and written bucket by bucket.  Stable.  Tile states carry the pass number, so one zeroing per sort
+// serves every pass.
+constexpr unsigned long long OS_A = 1ull << 62, OS_P = 2ull << 62, OS_VAL = (1ull << 48) - 1;
+constexpr int OS_MAXP = 8;
+__global__ void __launch_bounds__(256) k_rx_hist(const unsigned long long *__restrict__ keys, int64_t n, int bit_lo,
+                                                 int npass, unsigned int *__restrict__ hist) {
+    __shared__ unsigned int h[OS_MAXP][256];
+    for (int q = threadIdx.x; q < OS_MAXP * 256; q += 256) (&h[0][0])[q] = 0;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < n; i += (int64_t)gridDim.x * 256) {
+        const unsigned long long k = keys[i] >> bit_lo;
+        for (int p = 0; p < npass; p++) atomicAdd(&h[p][(k >> (8 * p)) & 0xFFu], 1u);
+    }
+    __syncthreads();
+    for (int p = 0; p < npass; p++)
+        if (h[p][threadIdx.x]) atomicAdd(&hist[p * 256 + threadIdx.x], h[p][threadIdx.x]);
+}
+// exclusive scan of each pass's 256 digit counts (one block)
+__global__ void k_rx_hist_scan(unsigned int *__restrict__ hist, int npass, int64_t *__restrict__ excl) {
+    __shared__ int64_t sm[33];
+    for (int p = 0; p < npass; p++) {
+        int64_t tot;
+        excl[p * 256 + threadIdx.x] = block_excl_sum<256>((int64_t)hist[p * 256 + threadIdx.x], &tot, sm);
+    }
+}
+template <bool HAS_KEYS, bool HAS_VALS>
+__global__ void __launch_bounds__(RX_NT) k_rx_onesweep(const unsigned long long *__restrict__ keys_in,
+                                                       const uint32_t *__restrict__ vals_in, int64_t n, int shift,
+                                                       int pass, const int64_t *__restrict__ hexcl,
+                                                       unsigned long long *__restrict__ state,
+                                                       unsigned int *__restrict__ ticket,
+                                                       unsigned long long *__restrict__ keys_out,
+                                                       uint32_t *__restrict__ vals_out) {
+    __shared__ unsigned int wh[RX_WARPS][256];
+    __shared__ int64_t goff[256];
+    __shared__ int64_t s_tile;
+    __shared__ int64_t sc[33];
+    __shared__ int tstart[256];
+    __shared__ unsigned long long sk[HAS_KEYS ? RX_TILE : 1];
+    __shared__ uint32_t sv[RX_TILE];
+    __shared__ uint8_t sd[RX_TILE];
+    const int w = threadIdx.x >> 5, l = lane_id();
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(ticket + pass, 1u);
+    for (int d = threadIdx.x; d < 256 * RX_WARPS; d += RX_NT) (&wh[0][0])[d] = 0;
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t base = tile * RX_TILE + (int64_t)w * (32 * RX_ROUNDS);
+    int dg[RX_ROUNDS];
+    unsigned int rk[RX_ROUNDS];
+    unsigned long long kv[RX_ROUNDS];
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int r = 0; r < RX_ROUNDS; r++) {
+        const int64_t i = base + r * 32 + l;
+        const bool valid = i < n;
+        kv[r] = valid ? keys_in[i] : 0ull;
+        const int d = valid ? (int)((kv[r] >> shift) & 0xFFu) : 256 + l;
+        const unsigned mm = __match_any_sync(CH_FULL, d);
+        const unsigned int before = valid ? wh[w][d] : 0;
+        __syncwarp();
+        if (valid && (mm & lt) == 0) wh[w][d] = before + __popc(mm);
+        __syncwarp();
+        dg[r] = d;
+        rk[r] = before + __popc(mm & lt);
+    }
+    __syncthreads();
+    unsigned int run = 0;
+    for (int q = 0; q < RX_WARPS; q++) {
+        const unsigned int c = wh[q][threadIdx.x];
+        wh[q][threadIdx.x] = run;
+        run += c;
+    }
+    // publish this tile's count of digit d, then look back over earlier tiles for digit d
+    {
+        const int d = threadIdx.x;
+        const unsigned long long tag = (unsigned long long)(pass + 1) << 48;
+        volatile unsigned long long *st = state + tile * 256 + d;
+        int64_t excl = 0;
+        if (tile == 0) {
+            *st = OS_P | tag | (unsigned long long)run;
+        } else {
+            *st = OS_A | tag | (unsigned long long)run;
+            for (int64_t p = tile - 1; p >= 0;) {
+                const unsigned long long x = *(const volatile unsigned long long *)(state + p * 256 + d);
+                if (((x >> 48) & 0x3FFFull) != (unsigned long long)(pass + 1) || (x >> 62) == 0) continue;
+                excl += (int64_t)(x & OS_VAL);
+                if ((x >> 62) == 2) break;
+                p--;
+            }
+            *st = OS_P | tag | (unsigned long long)(excl + run);
+        }
+        goff[d] = hexcl[pass * 256 + d] + excl;
+    }
+    int64_t ttot;
+    tstart[threadIdx.x] = (int)block_excl_sum<RX_NT>((int64_t)run, &ttot, sc);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RX_ROUNDS; r++) {
+        const int64_t i = base + r * 32 + l;
+        if (i < n) {
+            const int d = dg[r];
+            const int loc = tstart[d] + (int)wh[w][d] + (int)rk[r];
+            if (HAS_KEYS) sk[loc] = kv[r];
+            sv[loc] = HAS_VALS ? vals_in[i] : (uint32_t)i;
+            sd[loc] = (uint8_t)d;
+        }
+    }
+    __syncthreads();
+    const int tn = (int)ttot;
+    for (int j = threadIdx.x; j < tn; j += RX_NT) {
+        const int d = sd[j];
+        const int64_t pos = goff[d] + (j - tstart[d]);
+        if (HAS_KEYS) keys_out[pos] = sk[j];
+        vals_out[pos] = sv[j];
+    }
+}
 }  // namespace
 
 chopper_status ch_scan_excl_i64(chopper_ctx *ctx, const int64_t *in, int64_t *out, int64_t n, int64_t *total_dev) {
@@ -391,21 +513,29 @@ chopper_status ch_radix_sort(chopper_ctx *ctx, unsigned long long *keys, uint32_
                              uint32_t *vals_alt, int64_t n, int bit_lo, int bit_hi, bool *result_in_alt) {
     *result_in_alt = false;
     if (n <= 0 || bit_hi <= bit_lo) return CHOPPER_OK;
-    int64_t ntile = ceil_div(n, RX_TILE);
+    const int64_t ntile = ceil_div(n, RX_TILE);
+    const int npass = (bit_hi - bit_lo + 7) / 8;
+    if (npass > OS_MAXP) return ch_fail(ctx, CHOPPER_E_RANGE, "radix key wider than 64 bits");
     size_t mark = ctx->used;
     CH_ALLOC_BEGIN;
-    int64_t *cnt64 = CH_ALLOC(ctx, int64_t, 256 * ntile);
-    int64_t *offs = CH_ALLOC(ctx, int64_t, 256 * ntile);
+    // one zeroed block: tile states [ntile][256], digit histograms [npass][256], tickets [npass]
+    unsigned long long *state = CH_ALLOC(ctx, unsigned long long, ntile * 256 + 256 * OS_MAXP / 2 + OS_MAXP);
+    int64_t *hexcl = CH_ALLOC(ctx, int64_t, 256 * OS_MAXP);
     CH_ALLOC_END(ctx);
+    unsigned int *hist = reinterpret_cast<unsigned int *>(state + ntile * 256);
+    unsigned int *ticket = hist + 256 * OS_MAXP;
+    CH_CUDA(ctx, cudaMemsetAsync(state, 0, 8 * (size_t)(ntile * 256 + 256 * OS_MAXP / 2 + OS_MAXP), ctx->st));
+    k_rx_hist<<<(unsigned)std::min<int64_t>(ceil_div(n, 256 * 16), 148 * 8), 256, 0, ctx->st>>>(keys, n, bit_lo, npass,
+                                                                                              hist);
+    CH_LAUNCHED(ctx);
+    k_rx_hist_scan<<<1, 256, 0, ctx->st>>>(hist, npass, hexcl);
+    CH_LAUNCHED(ctx);
     unsigned long long *ki = keys, *ko = keys_alt;
     uint32_t *vi = vals, *vo = vals_alt;
     bool alt = false;
-    for (int b = bit_lo; b < bit_hi; b += 8) {
-        KeyArr ks{ki, b};
-        k_rx_upsweep<KeyArr><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, n, cnt64, ntile);
-        CH_LAUNCHED(ctx);
-        CH_TRY(ch_scan_excl_i64(ctx, cnt64, offs, 256 * ntile, nullptr));
-        k_rx_downsweep<KeyArr, true, true><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ks, ki, vi, n, offs, ntile, ko, vo);
+    for (int p = 0; p < npass; p++) {
+        k_rx_onesweep<true, true><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ki, vi, n, bit_lo + 8 * p, p, hexcl, state,
+                                                                          ticket, ko, vo);
         CH_LAUNCHED(ctx);
         std::swap(ki, ko);
         std::swap(vi, vo);
