@@ -390,9 +390,9 @@ def main():
     traffic, traffic_src = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "event_pass_traffic.json")) as f:
-            tj = json.load(f)
-        if tj.get("config") == args.config:
-            traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
+            tj = json.load(f).get("configs", {}).get(str(args.config))
+        if tj:
+            traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source") + " (committed capture, not this run)"
     except Exception:
         pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
