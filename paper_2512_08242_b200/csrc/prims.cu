@@ -348,45 +348,51 @@ __global__ void k_rx_hist_scan(unsigned int *__restrict__ hist, int npass, int64
         excl[p * 256 + threadIdx.x] = block_excl_sum<256>((int64_t)hist[p * 256 + threadIdx.x], &tot, sm);
     }
 }
-template <bool HAS_KEYS, bool HAS_VALS>
-__global__ void __launch_bounds__(RX_NT) k_rx_onesweep(const unsigned long long *__restrict__ keys_in,
-                                                       const uint32_t *__restrict__ vals_in, int64_t n, int shift,
-                                                       int pass, const int64_t *__restrict__ hexcl,
-                                                       unsigned long long *__restrict__ state,
-                                                       unsigned int *__restrict__ ticket,
-                                                       unsigned long long *__restrict__ keys_out,
-                                                       uint32_t *__restrict__ vals_out) {
+constexpr int OS_ROUNDS = 16, OS_TILE = RX_NT * OS_ROUNDS;     // 4096 keys per tile
+struct OsSmem {
+    unsigned long long sk[OS_TILE];
+    uint32_t sv[OS_TILE];
+    uint8_t sd[OS_TILE];
+};
+__global__ void __launch_bounds__(RX_NT, 2) k_rx_onesweep(const unsigned long long *__restrict__ keys_in,
+                                                          const uint32_t *__restrict__ vals_in, int64_t n, int shift,
+                                                          int pass, const int64_t *__restrict__ hexcl,
+                                                          unsigned long long *__restrict__ state,
+                                                          unsigned int *__restrict__ ticket,
+                                                          unsigned long long *__restrict__ keys_out,
+                                                          uint32_t *__restrict__ vals_out) {
+    extern __shared__ __align__(16) unsigned char os_dsm[];
+    OsSmem &T = *reinterpret_cast<OsSmem *>(os_dsm);
     __shared__ unsigned int wh[RX_WARPS][256];
     __shared__ int64_t goff[256];
     __shared__ int64_t s_tile;
     __shared__ int64_t sc[33];
     __shared__ int tstart[256];
-    __shared__ unsigned long long sk[HAS_KEYS ? RX_TILE : 1];
-    __shared__ uint32_t sv[RX_TILE];
-    __shared__ uint8_t sd[RX_TILE];
     const int w = threadIdx.x >> 5, l = lane_id();
     if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(ticket + pass, 1u);
     for (int d = threadIdx.x; d < 256 * RX_WARPS; d += RX_NT) (&wh[0][0])[d] = 0;
     __syncthreads();
     const int64_t tile = s_tile;
-    const int64_t base = tile * RX_TILE + (int64_t)w * (32 * RX_ROUNDS);
-    int dg[RX_ROUNDS];
-    unsigned int rk[RX_ROUNDS];
-    unsigned long long kv[RX_ROUNDS];
+    const int64_t base = tile * OS_TILE + (int64_t)w * (32 * OS_ROUNDS);
+    unsigned long long kv[OS_ROUNDS];
+#pragma unroll
+    for (int r = 0; r < OS_ROUNDS; r++) {      // all loads in flight before the ranking
+        const int64_t i = base + r * 32 + l;
+        kv[r] = i < n ? keys_in[i] : 0ull;
+    }
+    uint32_t dr[OS_ROUNDS];                    // digit (8 bits) | rank in the warp's digit sequence << 8
     const unsigned lt = lanemask_lt();
 #pragma unroll
-    for (int r = 0; r < RX_ROUNDS; r++) {
+    for (int r = 0; r < OS_ROUNDS; r++) {
         const int64_t i = base + r * 32 + l;
         const bool valid = i < n;
-        kv[r] = valid ? keys_in[i] : 0ull;
         const int d = valid ? (int)((kv[r] >> shift) & 0xFFu) : 256 + l;
         const unsigned mm = __match_any_sync(CH_FULL, d);
         const unsigned int before = valid ? wh[w][d] : 0;
         __syncwarp();
         if (valid && (mm & lt) == 0) wh[w][d] = before + __popc(mm);
         __syncwarp();
-        dg[r] = d;
-        rk[r] = before + __popc(mm & lt);
+        dr[r] = (uint32_t)(d & 0xFF) | ((before + __popc(mm & lt)) << 8);
     }
     __syncthreads();
     unsigned int run = 0;
@@ -420,23 +426,23 @@ __global__ void __launch_bounds__(RX_NT) k_rx_onesweep(const unsigned long long 
     tstart[threadIdx.x] = (int)block_excl_sum<RX_NT>((int64_t)run, &ttot, sc);
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < RX_ROUNDS; r++) {
+    for (int r = 0; r < OS_ROUNDS; r++) {
         const int64_t i = base + r * 32 + l;
         if (i < n) {
-            const int d = dg[r];
-            const int loc = tstart[d] + (int)wh[w][d] + (int)rk[r];
-            if (HAS_KEYS) sk[loc] = kv[r];
-            sv[loc] = HAS_VALS ? vals_in[i] : (uint32_t)i;
-            sd[loc] = (uint8_t)d;
+            const int d = (int)(dr[r] & 0xFFu);
+            const int loc = tstart[d] + (int)wh[w][d] + (int)(dr[r] >> 8);
+            T.sk[loc] = kv[r];
+            T.sv[loc] = vals_in[i];
+            T.sd[loc] = (uint8_t)d;
         }
     }
     __syncthreads();
     const int tn = (int)ttot;
     for (int j = threadIdx.x; j < tn; j += RX_NT) {
-        const int d = sd[j];
+        const int d = T.sd[j];
         const int64_t pos = goff[d] + (j - tstart[d]);
-        if (HAS_KEYS) keys_out[pos] = sk[j];
-        vals_out[pos] = sv[j];
+        keys_out[pos] = T.sk[j];
+        vals_out[pos] = T.sv[j];
     }
 }
 }  // namespace
@@ -513,7 +519,7 @@ chopper_status ch_radix_sort(chopper_ctx *ctx, unsigned long long *keys, uint32_
                              uint32_t *vals_alt, int64_t n, int bit_lo, int bit_hi, bool *result_in_alt) {
     *result_in_alt = false;
     if (n <= 0 || bit_hi <= bit_lo) return CHOPPER_OK;
-    const int64_t ntile = ceil_div(n, RX_TILE);
+    const int64_t ntile = ceil_div(n, OS_TILE);
     const int npass = (bit_hi - bit_lo + 7) / 8;
     if (npass > OS_MAXP) return ch_fail(ctx, CHOPPER_E_RANGE, "radix key wider than 64 bits");
     size_t mark = ctx->used;
@@ -533,9 +539,14 @@ chopper_status ch_radix_sort(chopper_ctx *ctx, unsigned long long *keys, uint32_
     unsigned long long *ki = keys, *ko = keys_alt;
     uint32_t *vi = vals, *vo = vals_alt;
     bool alt = false;
+    static bool os_attr = false;
+    if (!os_attr) {
+        CH_CUDA(ctx, cudaFuncSetAttribute(k_rx_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OsSmem)));
+        os_attr = true;
+    }
     for (int p = 0; p < npass; p++) {
-        k_rx_onesweep<true, true><<<(unsigned)ntile, RX_NT, 0, ctx->st>>>(ki, vi, n, bit_lo + 8 * p, p, hexcl, state,
-                                                                          ticket, ko, vo);
+        k_rx_onesweep<<<(unsigned)ntile, RX_NT, sizeof(OsSmem), ctx->st>>>(ki, vi, n, bit_lo + 8 * p, p, hexcl, state,
+                                                                           ticket, ko, vo);
         CH_LAUNCHED(ctx);
         std::swap(ki, ko);
         std::swap(vi, vo);

@@ -1541,8 +1541,10 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
     // roll-ups (D12): instance -> layer (staged), -> phase, -> iteration, -> gpu (warp per parent)
     // instances per layer: ~ instances / layer spans of the local gpus (fan-out hint for the staging width)
     const int64_t n_layers = std::max<int64_t>(ctx->n_layer_spans, 1);
-    const int fan_ly = (int)std::max<int64_t>(1, std::min<int64_t>(64, ctx->R / n_layers));
-    CH_TRY(rollup(ctx, ctx->inst, ctx->layer, L.sh_ly, 3, 0, L, lg_gpu_d, fan_ly));
+    const int64_t fan = ctx->R / n_layers;
+    const int fan_ly = (int)std::max<int64_t>(1, std::min<int64_t>(64, fan));
+    // thousands of instances per layer (deep op trees, config 5): a warp per layer; else the staged fold
+    CH_TRY(rollup(ctx, ctx->inst, ctx->layer, L.sh_ly, 3, fan > 256 ? 1 : 0, L, lg_gpu_d, fan_ly));
     CH_TRY(rollup(ctx, ctx->layer, ctx->phase, L.sh_ph, 2, 1, L, lg_gpu_d));
     CH_TRY(rollup(ctx, ctx->phase, ctx->iter, L.sh_it, 1, 1, L, lg_gpu_d));
     CH_TRY(rollup(ctx, ctx->iter, ctx->gpurow, L.sh_lg, 0, 1, L, lg_gpu_d));
