@@ -367,6 +367,25 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+// chain predecessor end (a7, D7/D8) of COMPUTE event i: the materialized column when the general a2 path built
+// one, else -- the lean a2 path, one start-monotone compute stream per gpu -- the end of the previous COMPUTE event
+// of the same gpu in dispatch order, found by walking back over the non-COMPUTE events in between
+struct PredView {
+    const int64_t *pred_end;     // [N] or NULL (lean)
+    const uint32_t *meta;
+    const int64_t *ke;
+};
+__device__ __forceinline__ int64_t pred_of(const PredView &v, int64_t i) {
+    if (v.pred_end) return v.pred_end[i];
+    const int g = (int)(__ldg(v.meta + i) >> 24);
+    for (int64_t q = i - 1; q >= 0; q--) {
+        const uint32_t m = __ldg(v.meta + q);
+        if ((int)(m >> 24) != g) break;
+        if ((m & 0xFFu) == CK_COMPUTE) return __ldg(v.ke + q);
+    }
+    return CH_NONE_TS;
+}
+
 // record a validation violation (count + smallest index)
 __device__ __forceinline__ void viol(DevReport *r, int rule, int64_t idx) {
     atomicAdd(&r->val_count[rule], 1ull);

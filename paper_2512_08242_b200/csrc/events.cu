@@ -836,6 +836,12 @@ __device__ __forceinline__ void tile_finish(SM &S, const EvParams &P, bool has, 
     }
 }
 
+// the chain predecessor column of a lean-loaded trace (general event passes read it)
+__global__ void k_pred_lean(PredView pv, int64_t n, int64_t *__restrict__ pred_end) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) pred_end[i] = kind_of(pv.meta[i]) == CK_COMPUTE ? pred_of(pv, i) : CH_NONE_TS;
+}
+
 // the fused pass: one 2048-event tile per block, 8 consecutive events per thread
 __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
     extern __shared__ __align__(16) unsigned char ev_dsm[];
@@ -2254,6 +2260,16 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     const bool lean_pass = ctx->et_ok && ctx->lean && !force_general &&
                            column_map(&tm[0], P.tl, N, 8) && column_map(&tm[1], P.ks, N, 8) &&
                            column_map(&tm[2], P.ke, N, 8) && column_map(&tm[3], P.meta, N, 4);
+    if (!lean_pass && !ctx->d_pred_end) {
+        // a lean-loaded trace on a general event pass: materialize the chain predecessor column it reads
+        CH_ALLOC_BEGIN;
+        ctx->d_pred_end = CH_ALLOC(ctx, int64_t, N);
+        CH_ALLOC_END(ctx);
+        k_pred_lean<<<(unsigned)ceil_div(N, NT), NT, 0, ctx->st>>>(PredView{nullptr, ctx->ev.meta, ctx->ev.end_ns}, N,
+                                                                  ctx->d_pred_end);
+        CH_LAUNCHED(ctx);
+        P.pred_end = ctx->d_pred_end;
+    }
     if (lean_pass) {
         // the lean pass: TMA staging, launch chain from the tile (no predecessor column)
         ntile = ceil_div(N, W_TILE);

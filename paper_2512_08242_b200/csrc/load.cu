@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(LN_NT) k_lean_chain(const uint32_t *__restrict
             p_ke = ve[k];
         }
     }
+    if (!pred_end) return;                // lean a2: the event pass and the tables derive the chain themselves
     if (nv == LN_IPT && (((uintptr_t)(pred_end + i0)) & 15u) == 0) {
 #pragma unroll
         for (int h = 0; h < LN_IPT / 2; h++)
@@ -684,7 +685,7 @@ chopper_status ch_load(chopper_ctx *ctx) {
                                  ctx->st));
     // a2: partition by (lg, dense group); full radix sort only if a group is not start-monotone
     ctx->d_perm = CH_ALLOC(ctx, uint32_t, n);
-    ctx->d_pred_end = CH_ALLOC(ctx, int64_t, n);
+    ctx->d_pred_end = nullptr;       // materialized by the general path only (k_chain); lean: derived (PredView)
     ctx->d_bucket_beg = CH_ALLOC(ctx, int64_t, ctx->n_buckets + 1);
     CH_ALLOC_END(ctx);
     const int NG = ctx->NG, other = NG - 1;
@@ -697,6 +698,8 @@ chopper_status ch_load(chopper_ctx *ctx) {
             return finish_load(ctx);
         }
     }
+    ctx->d_pred_end = CH_ALLOC(ctx, int64_t, n);
+    CH_ALLOC_END(ctx);
     size_t mark = ctx->used;
     if (ctx->n_buckets <= 256) {
         CH_TRY(ch_radix_partition_meta(ctx, ctx->ev.meta, ctx->d_gpu_lg, NG, other, ctx->d_perm, n));
@@ -792,7 +795,7 @@ static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back) {
     CH_LAUNCHED(ctx);
     k_lean_chain<<<(unsigned)ntile, LN_NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, ctx->ev.end_ns, n, ctx->d_gpu_lg,
                                                          NG, gb, tcme, tcpe, carry, ctx->d_bucket_beg, lc0, lp0,
-                                                         ctx->d_perm, ctx->d_pred_end, ctx->d_rep, nonmono);
+                                                         ctx->d_perm, nullptr, ctx->d_rep, nonmono);
     CH_LAUNCHED(ctx);
     ctx->bucket_beg.assign(nb + 1, 0);
     unsigned int hnm = 0;

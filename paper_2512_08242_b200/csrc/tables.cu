@@ -998,7 +998,7 @@ __global__ void k_decode(const unsigned long long *__restrict__ key, const int64
                          int depth,
                          const int32_t *__restrict__ lg_gpu, const int64_t *__restrict__ list_beg,
                          const int32_t *__restrict__ P_orig, const int32_t *__restrict__ P_label,
-                         const int64_t *__restrict__ f, int64_t cap, const int64_t *__restrict__ pred_end,
+                         const int64_t *__restrict__ f, int64_t cap, PredView pv,
                          int32_t *gpu, int32_t *it, int32_t *ph, int32_t *ly, int32_t *op, int32_t *label,
                          int32_t *rank, int64_t *first_pred) {
     const int64_t n = *n_dev;
@@ -1019,7 +1019,7 @@ __global__ void k_decode(const unsigned long long *__restrict__ key, const int64
     label[j] = (depth >= 4 && r[3] > 0) ? P_label[list_beg[lg * 4 + 3] + r[3] - 1] : -1;
     rank[j] = depth >= 1 && r[0] > 0 ? (int32_t)(r[0] - 1) : -1;
     int64_t fi = f[(int64_t)RF_FIRST_IDX * cap + j];
-    first_pred[j] = (fi != INT64_MAX) ? pred_end[fi] : CH_NONE_TS;
+    first_pred[j] = (fi != INT64_MAX) ? pred_of(pv, fi) : CH_NONE_TS;
     }
 }
 
@@ -1176,7 +1176,7 @@ __global__ void k_decode_points(const unsigned long long *__restrict__ key, cons
                                 int kb0,
                                 const int32_t *__restrict__ lg_gpu, const int64_t *__restrict__ list_beg,
                                 const int32_t *__restrict__ P_orig, const int64_t *__restrict__ f, int64_t cap,
-                                const int64_t *__restrict__ pred_end, int32_t *gpu, int32_t *it, int32_t *ph,
+                                PredView pv, int32_t *gpu, int32_t *it, int32_t *ph,
                                 int32_t *ly, int32_t *op, int32_t *label, int32_t *rank, int64_t *first_pred) {
     const int64_t n = *n_dev;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
@@ -1190,7 +1190,7 @@ __global__ void k_decode_points(const unsigned long long *__restrict__ key, cons
     label[j] = lab;
     rank[j] = (int32_t)(rit - 1);
     int64_t fi = f[(int64_t)RF_FIRST_IDX * cap + j];
-    first_pred[j] = (fi != INT64_MAX) ? pred_end[fi] : CH_NONE_TS;
+    first_pred[j] = (fi != INT64_MAX) ? pred_of(pv, fi) : CH_NONE_TS;
     }
 }
 
@@ -1361,7 +1361,7 @@ static chopper_status rollup(chopper_ctx *ctx, RowTable &child, RowTable &parent
     CH_TRY(sum_rows(ctx, view(child), nullptr, starts, ng_dev, child.cap, mode, shift, ctx->C, view(parent), fanout));
     k_decode<<<grid_for(child.cap, NT), NT, 0, ctx->st>>>(parent.key, ng_dev, L, depth, lg_gpu_d, ctx->d_list_beg,
                                                           ctx->P_orig, ctx->P_label, parent.f, parent.cap,
-                                                          ctx->d_pred_end, parent.gpu, parent.it, parent.ph, parent.ly,
+                                                          PredView{ctx->d_pred_end, ctx->ev.meta, ctx->ev.end_ns}, parent.gpu, parent.it, parent.ph, parent.ly,
                                                           parent.op, parent.label, parent.rank, parent.first_pred);
     CH_LAUNCHED(ctx);
     return CHOPPER_OK;
@@ -1478,7 +1478,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
             CH_TRY(sum_rows(ctx, subv, so, starts, ng_dev, R, 0, 0, C, view(ctx->inst)));
             k_decode<<<grid_for(R, NT), NT, 0, ctx->st>>>(
                 ctx->inst.key, ng_dev, L, 4, lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->P_label, ctx->inst.f,
-                ctx->inst.cap, ctx->d_pred_end, ctx->inst.gpu, ctx->inst.it, ctx->inst.ph, ctx->inst.ly, ctx->inst.op,
+                ctx->inst.cap, PredView{ctx->d_pred_end, ctx->ev.meta, ctx->ev.end_ns}, ctx->inst.gpu, ctx->inst.it, ctx->inst.ph, ctx->inst.ly, ctx->inst.op,
                 ctx->inst.label, ctx->inst.rank, ctx->inst.first_pred);
             CH_LAUNCHED(ctx);
         }
@@ -1528,7 +1528,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
             CH_LAUNCHED(ctx);
             k_decode_points<<<grid_for(cells, NT), NT, 0, ctx->st>>>(
                 ctx->point.key, np_d, ctx->kg, L.kb[0], lg_gpu_d, ctx->d_list_beg, ctx->P_orig, ctx->point.f,
-                ctx->point.cap, ctx->d_pred_end, ctx->point.gpu, ctx->point.it, ctx->point.ph, ctx->point.ly,
+                ctx->point.cap, PredView{ctx->d_pred_end, ctx->ev.meta, ctx->ev.end_ns}, ctx->point.gpu, ctx->point.it, ctx->point.ph, ctx->point.ly,
                 ctx->point.op, ctx->point.label, ctx->point.rank, ctx->point.first_pred);
             CH_LAUNCHED(ctx);
         }
