@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
                                                       const PassDesc *__restrict__ passes,
                                                       const int32_t *__restrict__ pass_off,
                                                       const int32_t *__restrict__ pass_idx, int n_passes,
-                                                      unsigned long long *__restrict__ mis) {
+                                                      unsigned long long *__restrict__ mis,
+                                                      int32_t *__restrict__ t_nm) {
     __shared__ int64_t sm[33];
     __shared__ PassDesc sp[PC_MAXP];
     __shared__ int32_t soff[PC_MAXP + 1];
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
     int64_t tot;
     unsigned long long ex = (unsigned long long)block_excl_sum<MR_NT>((int64_t)c, &tot, sm);
     int64_t r0 = tex[blockIdx.x] + (int64_t)(ex & 0x1FFFFF);
+    if (t_nm) t_nm[(int64_t)blockIdx.x * MR_NT + threadIdx.x] = (int32_t)r0;   // the counter pass's positions
     int64_t r1 = tex[ntile + blockIdx.x] + (int64_t)((ex >> 21) & 0x1FFFFF);
     int64_t r2 = tex[2 * ntile + blockIdx.x] + (int64_t)(ex >> 42);
     int32_t nr[MR_IPT];
@@ -410,7 +412,11 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         by_lg[lg].push_back(p);
     }
     CH_ALLOC_BEGIN;
-    ctx->d_nm_rank = C > 0 ? CH_ALLOC(ctx, int32_t, N) : nullptr;     // counter-pass position (D2), counters only
+    // counter-pass positions (D2): per event only for the full-mode [C][N] output; the counter pass derives them
+    // from the rank before each thread's first event (t_nm) and each gpu's first rank (nm_base)
+    ctx->d_nm_rank = (C > 0 && counters_out) ? CH_ALLOC(ctx, int32_t, N) : nullptr;
+    ctx->d_t_nm = C > 0 ? CH_ALLOC(ctx, int32_t, ceil_div(std::max<int64_t>(N, 1), MR_TILE) * MR_NT) : nullptr;
+    ctx->d_nm_base = nullptr;
     ctx->d_passes = CH_ALLOC(ctx, PassDesc, n_passes + 1);
     int64_t *dgbeg = CH_ALLOC(ctx, int64_t, n_lg + 1);
     CH_ALLOC_END(ctx);
@@ -438,9 +444,9 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         int64_t ntile = ceil_div(N, MR_TILE);
         ctx->d_mg = CH_ALLOC(ctx, int64_t, n_lg + 1);
         CH_ALLOC_END(ctx);
-        size_t mark = ctx->used;
         int64_t *tc = CH_ALLOC(ctx, int64_t, 3 * ntile), *tex = CH_ALLOC(ctx, int64_t, 3 * ntile);
         int64_t *base = CH_ALLOC(ctx, int64_t, 3 * (n_lg + 1));
+        ctx->d_nm_base = base;           // component 0: non-MEMOP rank of each local gpu's first event
         int32_t *dlg = CH_ALLOC(ctx, int32_t, n_lg + 1);
         CH_ALLOC_END(ctx);
         std::vector<int32_t> hlg(ctx->lg_gpu, ctx->lg_gpu + n_lg);
@@ -477,7 +483,7 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         k_meta_apply<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, ctx->ev.end_ns, N,
                                                              ctx->d_gpu_lg, tex, ntile, base, n_lg, ctx->d_nm_rank,
                                                              ctx->d_xsend, K, ctx->xW, ctx->d_xovf, ctx->ev.name_id,
-                                                             ctx->d_passes, doff, didx, n_passes, mis);
+                                                             ctx->d_passes, doff, didx, n_passes, mis, ctx->d_t_nm);
         CH_LAUNCHED(ctx);
         k_mg<<<1, 256, 0, ctx->st>>>(base, n_lg, ctx->d_mg);
         CH_LAUNCHED(ctx);

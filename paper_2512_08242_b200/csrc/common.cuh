@@ -177,7 +177,11 @@ struct chopper_ctx {
     // sub-runs (a9 time part), produced by the fused event pass
     int64_t R = 0;
     RowTable sub;
-    int32_t *d_run_id = nullptr;     // [N] sub-run of each event
+    int64_t *d_tile_sub = nullptr;   // [ntile + 1] first sub-run id of each 2048-event tile (event pass)
+    int32_t *d_t_run = nullptr;      // [ntile * 256] run id before each event-pass thread's first event
+    uint8_t *d_t_hm = nullptr;       // [ntile * 256] that thread's head mask (the counter pass derives run ids)
+    int32_t *d_t_nm = nullptr;       // [ntile * 256] non-MEMOP rank before each thread's first event (a3 positions)
+    int64_t *d_nm_base = nullptr;    // [n_lg + 1] non-MEMOP rank of each local gpu's first event
     unsigned long long *d_tile_state = nullptr;
     unsigned int *d_tile_ticket = nullptr;
 
@@ -186,7 +190,7 @@ struct chopper_ctx {
     std::vector<PassDesc> passes;
     PassDesc *d_passes = nullptr;
     int32_t *d_slot_pass = nullptr;  // [n_lg][C] pass index providing the slot, -1 absent
-    int32_t *d_nm_rank = nullptr;    // [N] rank among non-MEMOP events of its gpu
+    int32_t *d_nm_rank = nullptr;    // [N] rank among non-MEMOP events of its gpu (full-mode counter output only)
     int64_t *d_mg = nullptr;         // [n_lg] non-MEMOP events per local gpu (counter column length)
     std::vector<int64_t> h_mg;
     std::vector<int32_t> h_pass_off, h_pass_idx;   // a3: passes grouped by local gpu (upload staging)

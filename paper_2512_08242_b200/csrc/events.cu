@@ -267,7 +267,9 @@ struct EvParams {
     const int32_t *smp_f, *smp_p;
     const int64_t *phi_pre, *psi_pre, *smp_lo, *smp_hi;
     int64_t *o_ovl, *o_prep, *o_call, *o_phi, *o_psi;
-    int32_t *o_run;
+    int32_t *o_run;               // (unused: the counter pass reads the per-thread values below)
+    int32_t *t_run;               // [ntile][256] run id before each thread's first event (counters only)
+    uint8_t *t_hm;                // [ntile][256] head mask of each thread's 8 events
     unsigned long long *sr_key;
     int64_t *sr_first;
     int64_t *sr_f;
@@ -836,6 +838,14 @@ __device__ __forceinline__ void tile_finish(SM &S, const EvParams &P, bool has, 
     }
 }
 
+// first sub-run id of every tile from the look-back states (inclusive prefixes) of k_events
+__global__ void k_tile_sub_state(const unsigned long long *__restrict__ state, int64_t ntile,
+                                 int64_t *__restrict__ tile_sub) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t == 0) tile_sub[0] = 0;
+    if (t < ntile) tile_sub[t + 1] = (int64_t)(state[t] & VAL_MASK);
+}
+
 // the chain predecessor column of a lean-loaded trace (general event passes read it)
 __global__ void k_pred_lean(PredView pv, int64_t n, int64_t *__restrict__ pred_end) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -941,6 +951,10 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
     const int ex = tile_head_scan(S, hmask, nv, &tot);   // heads before this thread in the tile
     tile_lookback(S, P, tile, tot);
     const int64_t run0 = S.excl + ex;     // global id of this thread's first head
+    if (P.t_run) {                        // the counter pass's view of the runs: 5 B per thread
+        P.t_run[tile * (int64_t)blockDim.x + threadIdx.x] = (int32_t)(run0 - 1);    // (k_events: ticketed tiles)
+        P.t_hm[tile * (int64_t)blockDim.x + threadIdx.x] = (uint8_t)hmask;
+    }
 
     // ---- phase B: per-event values (a6-a8), outputs, thread-sequential folding (a9) ----
     Acc cur, p0;
@@ -1029,7 +1043,6 @@ __global__ void __launch_bounds__(EV_NT, 2) k_events(EvParams P, int vec_ok) {
             if (P.o_call) P.o_call[i] = call;
             if (P.o_phi) P.o_phi[i] = phi;
             if (P.o_psi) P.o_psi[i] = psi;
-            if (P.o_run) P.o_run[i] = (int32_t)curid;
         }
     }
 
@@ -1459,6 +1472,10 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_w(EvParams P, int vec_ok) {
     int tot;
     const int ex = tile_head_scan_h(S, hmask, nv > 0 && (tid == 0 || firstk != S.lastk[tid - 1]), &tot);
     const int64_t run0 = S.excl + ex;
+    if (P.t_run) {                        // the counter pass's view of the runs: 5 B per thread
+        P.t_run[tile * (int64_t)blockDim.x + threadIdx.x] = (int32_t)(run0 - 1);    // (k_events: ticketed tiles)
+        P.t_hm[tile * (int64_t)blockDim.x + threadIdx.x] = (uint8_t)hmask;
+    }
 
     // ---- phase B: per-event values (a6-a8), outputs, thread-sequential folding (a9) ----
     Acc cur, p0;
@@ -1547,7 +1564,6 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_w(EvParams P, int vec_ok) {
         if (P.o_call) P.o_call[i] = call;
         if (P.o_phi) P.o_phi[i] = phi;
         if (P.o_psi) P.o_psi[i] = psi;
-        if (P.o_run) P.o_run[i] = (int32_t)curid;
     }
     tile_finish(S, P, has, cur, p0, run0, base);
 }
@@ -1920,6 +1936,10 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_l(EvParams P, const __grid_c
     int tot;
     const int ex = tile_head_scan_h(S, hmask, nv > 0 && (tid == 0 || firstk != S.lastk[tid - 1]), &tot);
     const int64_t run0 = S.excl + ex;
+    if (P.t_run) {                        // the counter pass's view of the runs: 5 B per thread
+        P.t_run[tile * (int64_t)blockDim.x + threadIdx.x] = (int32_t)(run0 - 1);    // (k_events: ticketed tiles)
+        P.t_hm[tile * (int64_t)blockDim.x + threadIdx.x] = (uint8_t)hmask;
+    }
     int32_t ppos = __shfl_up_sync(CH_FULL, xpos, 1);
     int64_t pend = __shfl_up_sync(CH_FULL, xend, 1);
     if (lane == 0) { ppos = -1; pend = 0; }
@@ -1948,7 +1968,6 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_l(EvParams P, const __grid_c
     WCur ct;
     wcur_init(ct);
     TlEnt te{};
-    int32_t *const o_run = P.o_run;
     const int64_t t0 = P.t0, cap = P.cap;
 #pragma unroll 1
     for (int k = 0; k < EV_IPT; k++) {
@@ -2026,7 +2045,6 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_l(EvParams P, const __grid_c
                 if (P.o_phi) P.o_phi[i] = phi;
                 if (P.o_psi) P.o_psi[i] = psi;
             }
-            if (o_run) o_run[i] = (int32_t)curid;
         }
     }
     tile_finish(S, P, has, cur, p0, run0, base);
@@ -2216,7 +2234,11 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     ctx->sub.key = CH_ALLOC(ctx, unsigned long long, cap + 1);
     ctx->sub.first_event = CH_ALLOC(ctx, int64_t, cap + 1);
     ctx->sub.f = CH_ALLOC(ctx, int64_t, (int64_t)SR_W * cap);
-    ctx->d_run_id = ctx->C > 0 ? CH_ALLOC(ctx, int32_t, N) : nullptr;     // read only by the counter pass
+    ctx->d_tile_sub = CH_ALLOC(ctx, int64_t, ceil_div(N, W_TILE) + 1);      // kept: the counter pass's run ids
+    // per-thread run ids and head masks (2048-event tiles of 256 threads) for the counter pass (counters only)
+    const int64_t nthr = ceil_div(N, W_TILE) * W_NT;
+    ctx->d_t_run = ctx->C > 0 ? CH_ALLOC(ctx, int32_t, nthr) : nullptr;
+    ctx->d_t_hm = ctx->C > 0 ? CH_ALLOC(ctx, uint8_t, nthr) : nullptr;
     ctx->d_tile_state = CH_ALLOC(ctx, unsigned long long, ceil_div(N, W_TILE));   // >= tiles of either pass
     ctx->d_tile_ticket = CH_ALLOC(ctx, unsigned int, 1);
     CH_ALLOC_END(ctx);
@@ -2245,7 +2267,9 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     P.smp_ts = ctx->smp.ts_ns; P.smp_f = ctx->smp.freq_mhz; P.smp_p = ctx->smp.power_mw;
     P.phi_pre = ctx->d_smp_phi; P.psi_pre = ctx->d_smp_psi; P.smp_lo = ctx->d_smp_lo; P.smp_hi = ctx->d_smp_hi;
     P.o_ovl = ovl; P.o_prep = prep; P.o_call = call; P.o_phi = phi; P.o_psi = psi;
-    P.o_run = ctx->d_run_id;
+    P.o_run = nullptr;
+    P.t_run = ctx->d_t_run;
+    P.t_hm = ctx->d_t_hm;
     P.sr_key = ctx->sub.key; P.sr_first = ctx->sub.first_event; P.sr_f = ctx->sub.f; P.cap = cap;
     P.tile_state = ctx->d_tile_state; P.ticket = ctx->d_tile_ticket;
     P.KTt = ctx->KT_t; P.KTk = ctx->KT_k; P.kt_beg = ctx->d_kt_beg;
@@ -2277,7 +2301,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         size_t mark = ctx->used;
         int32_t *seeds = CH_ALLOC(ctx, int32_t, ntile * SEED_W);
         int64_t *tpe = CH_ALLOC(ctx, int64_t, ntile + 1);
-        int64_t *tcnt = CH_ALLOC(ctx, int64_t, ntile + 1), *tbase = CH_ALLOC(ctx, int64_t, ntile + 1);
+        int64_t *tcnt = CH_ALLOC(ctx, int64_t, ntile + 1), *tbase = ctx->d_tile_sub;
         TileWin *twin = CH_ALLOC(ctx, TileWin, ntile);
         TileWinL *twinl = CH_ALLOC(ctx, TileWinL, ntile);
         CH_ALLOC_END(ctx);
@@ -2317,7 +2341,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         P.ntile = ntile;
         size_t mark = ctx->used;
         int32_t *seeds = CH_ALLOC(ctx, int32_t, ntile * SEED_W);
-        int64_t *tcnt = CH_ALLOC(ctx, int64_t, ntile + 1), *tbase = CH_ALLOC(ctx, int64_t, ntile + 1);
+        int64_t *tcnt = CH_ALLOC(ctx, int64_t, ntile + 1), *tbase = ctx->d_tile_sub;
         TileWin *twin = CH_ALLOC(ctx, TileWin, ntile);
         CH_ALLOC_END(ctx);
         P.seeds = seeds;
@@ -2358,6 +2382,8 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         CH_LAUNCHED(ctx);
         ch_tick(ctx, 8, 1);
         ch_tick(ctx, 4, 1);
+        k_tile_sub_state<<<(unsigned)ceil_div(ntile + 1, NT), NT, 0, ctx->st>>>(ctx->d_tile_state, ntile, ctx->d_tile_sub);
+        CH_LAUNCHED(ctx);
     }
     if (ovl && ctx->n_lg > 0) {
         k_covl<<<dim3(64, ctx->n_lg), 128, 0, ctx->st>>>(P, ctx->n_lg);

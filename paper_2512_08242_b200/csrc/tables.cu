@@ -37,8 +37,11 @@ struct CtSmem {
     const double *cp[CT_CP];                  // column pointers [lg][slot], loaded beside the metadata
 };
 __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__restrict__ meta,
-                                                          const int32_t *__restrict__ run_id,
-                                                          const int32_t *__restrict__ nm_rank,
+                                                          const int32_t *__restrict__ t_run,
+                                                          const uint8_t *__restrict__ t_hm,
+                                                          const int32_t *__restrict__ t_nm,
+                                                          const int64_t *__restrict__ nm_base,
+                                                          const int64_t *__restrict__ tile_sub,
                                                           const int32_t *__restrict__ gpu_lg,
                                                           const double *const *__restrict__ col, int C,
                                                           int64_t N, double *__restrict__ out, int64_t cap,
@@ -51,32 +54,40 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
     if (cp_sm && tid < n_lg * C) S.cp[tid] = col[tid];
     const int64_t base = (int64_t)blockIdx.x * CT_TILE, i0 = base + (int64_t)tid * CT_IPT;
     const int nv = i0 >= N ? 0 : (int)min((int64_t)CT_IPT, N - i0);
+    // the event pass and the a3 rank pass use the same 2048-event tiles of 256 threads x 8 events: each thread's
+    // run id before its first event + head mask, and its non-MEMOP rank before its first event, give every run id
+    // and counter position here (5 + 4 B per 8 events instead of 8 B per event)
+    const int64_t th = (int64_t)blockIdx.x * CT_NT + tid;
+    const int32_t rrun = nv > 0 ? t_run[th] : 0;
+    const unsigned hmask = nv > 0 ? (unsigned)t_hm[th] : 0u;
+    const int32_t rnm = nv > 0 ? t_nm[th] : 0;
     uint32_t mt[CT_IPT];
-    int32_t rid[CT_IPT], nm[CT_IPT];
     if (vec_ok && nv == CT_IPT) {
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             uint4 a = reinterpret_cast<const uint4 *>(meta + i0)[h];
-            int4 b = reinterpret_cast<const int4 *>(run_id + i0)[h];
-            int4 c = reinterpret_cast<const int4 *>(nm_rank + i0)[h];
             mt[4 * h] = a.x; mt[4 * h + 1] = a.y; mt[4 * h + 2] = a.z; mt[4 * h + 3] = a.w;
-            rid[4 * h] = b.x; rid[4 * h + 1] = b.y; rid[4 * h + 2] = b.z; rid[4 * h + 3] = b.w;
-            nm[4 * h] = c.x; nm[4 * h + 1] = c.y; nm[4 * h + 2] = c.z; nm[4 * h + 3] = c.w;
         }
     } else {
 #pragma unroll
+        for (int k = 0; k < CT_IPT; k++) mt[k] = k < nv ? meta[i0 + k] : (uint32_t)CK_MEMOP;   // invalid: MEMOP
+    }
+    int32_t rid[CT_IPT], nm[CT_IPT];
+    {
+        int r = rrun, q = rnm, gp = -1;
+        int64_t gb = 0;
+#pragma unroll
         for (int k = 0; k < CT_IPT; k++) {
-            bool ok = k < nv;
-            mt[k] = ok ? meta[i0 + k] : (uint32_t)CK_MEMOP;     // (invalid events carry MEMOP)
-            rid[k] = ok ? run_id[i0 + k] : -1;
-            nm[k] = ok ? nm_rank[i0 + k] : 0;
+            r += (hmask >> k) & 1u;
+            rid[k] = r;
+            const bool rd = kind_of(mt[k]) != CK_MEMOP;
+            const int g = gpu_of(mt[k]);
+            if (rd && g != gp) { gb = nm_base[gpu_lg[g]]; gp = g; }
+            nm[k] = (int32_t)(q - gb);
+            q += rd ? 1 : 0;
         }
     }
-    const int32_t prev = (tid > 0 && nv > 0) ? run_id[i0 - 1] : -1;
-    unsigned hmask = 0;
-#pragma unroll
-    for (int k = 0; k < CT_IPT; k++)
-        if (k < nv && (k == 0 ? (tid == 0 || rid[0] != prev) : rid[k] != rid[k - 1])) hmask |= 1u << k;
+    const int32_t prev = rrun;
     const bool has = hmask != 0;
     // the tile's gpu range and counter-rank range over its non-MEMOP events
     int lmin = INT_MAX, lmax = -1, nmin = INT_MAX, nmax = -1;
@@ -229,8 +240,7 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
         }
         // the run open at the end of the tile
         if (tid == CT_NT - 1 && base < N) {
-            const int64_t last = base + CT_TILE - 1 < N ? base + CT_TILE - 1 : N - 1;
-            const int32_t id = run_id[last];
+            const int32_t id = (int32_t)(tile_sub[blockIdx.x + 1] - 1);      // the tile's last run
 #pragma unroll
             for (int q = 0; q < CT_SG; q++)
                 if (s0 + q < C) out[(int64_t)(s0 + q) + (int64_t)id * C] = f ? v[q] : S.carry[warp][q] + v[q];
@@ -1398,7 +1408,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         ctx->d_colbad = CH_ALLOC(ctx, unsigned int, (int64_t)n_lg * C);
         CH_ALLOC_END(ctx);
         CH_CUDA(ctx, cudaMemsetAsync(ctx->d_colbad, 0, 4 * (size_t)n_lg * C, ctx->st));
-        const int vec_ok = (((uintptr_t)ctx->ev.meta | (uintptr_t)ctx->d_run_id | (uintptr_t)ctx->d_nm_rank) & 15u) == 0;
+        const int vec_ok = (((uintptr_t)ctx->ev.meta) & 15u) == 0;
         CH_CUDA(ctx, cudaFuncSetAttribute(k_counters_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)sizeof(CtSmem)));
         // the counter pass runs on a side stream, concurrently with the instance ordering below (which never
@@ -1407,8 +1417,8 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[0], ctx->fork_ev, 0));
         ch_tick_on(ctx, 9, 0, ctx->side[0]);
         k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->side[0]>>>(
-            ctx->ev.meta, ctx->d_run_id, ctx->d_nm_rank, ctx->d_gpu_lg, ctx->d_col, C, ctx->N, subv.cnt, subv.ccap,
-            ctx->d_colbad, vec_ok, n_lg);
+            ctx->ev.meta, ctx->d_t_run, ctx->d_t_hm, ctx->d_t_nm, ctx->d_nm_base, ctx->d_tile_sub, ctx->d_gpu_lg,
+            ctx->d_col, C, ctx->N, subv.cnt, subv.ccap, ctx->d_colbad, vec_ok, n_lg);
         CH_LAUNCHED(ctx);
         ch_tick_on(ctx, 9, 1, ctx->side[0]);
         CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[0], ctx->side[0]));
