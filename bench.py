@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-full", action="store_true", help="skip the full-mode (per-event outputs) timing")
+    ap.add_argument("--traced", default=None,
+                    help="comma-separated traced GPUs to process on this one GPU (a rank's shard: scaling proxy)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -234,12 +236,14 @@ def main():
     import tracegen
     G = tracegen.config(args.config).n_gpus
     mine = [g for g in range(G) if g % world == rank]
+    if args.traced is not None:
+        mine = [int(x) for x in args.traced.split(",")]
     tg = time.time()
     if args.config == 5:
         shard, p = workload(5, gpus=mine)            # each rank draws only its own traced GPUs
     else:
         full_trace, p = workload(args.config)
-        shard = full_trace.gpu_slice(mine) if world > 1 else full_trace
+        shard = full_trace.gpu_slice(mine) if (world > 1 or args.traced is not None) else full_trace
     t_gen = time.time() - tg
     b = shard
     n_ev_local = shard.n_events

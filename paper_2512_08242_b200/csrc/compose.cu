@@ -1094,31 +1094,30 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     int64_t n = 0;
     unsigned int hovf = 0, hpoison = 0;
     if (ctx->d_dense_ovf) CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ctx->d_dense_ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
+    // one read-back: every array at its capacity (max_iters entries, at most 4096), the counts with it
+    if (nbd > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 breakdown rows");
+    if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels in the report rows");
+    const int64_t mc = std::min<int64_t>(MI, 4096);
     CH_CUDA(ctx, cudaMemcpyAsync(&n, nref, 8, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(&hpoison, poison, 4, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, ch_sync(ctx));
-    if (hpoison) return ch_fail(ctx, CHOPPER_E_STATE, "a peer rank failed earlier in this step (all-gather #2)");
-    if (n > 4096) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 4096 iterations in chopper_global");
-    if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "iteration rank >= max_iters or op label >= n_labels");
-    out->n_iters = n;
-    if (n > 0) {
-        CH_CUDA(ctx, cudaMemcpyAsync(out->step, step, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(out->complete, comp, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(out->sampled, samp, 4 * n, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(out->T, T, 8 * n, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(out->aligned_first, af, 8 * n, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(out->aligned_last, al, 8 * n, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(out->throughput, tp, 8 * n, cudaMemcpyDeviceToHost, ctx->st));
-    }
+    CH_CUDA(ctx, cudaMemcpyAsync(out->step, step, 4 * mc, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(out->complete, comp, 4 * mc, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(out->sampled, samp, 4 * mc, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(out->T, T, 8 * mc, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(out->aligned_first, af, 8 * mc, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(out->aligned_last, al, 8 * mc, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(out->throughput, tp, 8 * mc, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(&out->throughput_median, med, 8, cudaMemcpyDeviceToHost, ctx->st));
-    if (nbd > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 breakdown rows");
-    out->n_bd = nbd;
     if (nbd > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->bd, bd, 8 * 16 * nbd, cudaMemcpyDeviceToHost, ctx->st));
-    if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels in the report rows");
-    out->n_report = nL;
     CH_CUDA(ctx, cudaMemcpyAsync(out->e2e, e2e, 8 * (1 + E2E_W), cudaMemcpyDeviceToHost, ctx->st));
     if (nL > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->report, rep, 8 * 16 * (size_t)nL, cudaMemcpyDeviceToHost, ctx->st));
     CH_CUDA(ctx, ch_sync(ctx));
+    if (hpoison) return ch_fail(ctx, CHOPPER_E_STATE, "a peer rank failed earlier in this step (all-gather #2)");
+    if (n > mc) return ch_fail(ctx, CHOPPER_E_RANGE, "more iterations than max_iters (or 4096) in chopper_global");
+    if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "iteration rank >= max_iters or op label >= n_labels");
+    out->n_iters = n;
+    out->n_bd = nbd;
+    out->n_report = nL;
     for (int g = 0; g < ctx->cfg.n_traced_gpus && g < 256; g++) {
         out->delta[g] = ctx->delta[g];
         out->delta_flag[g] = ctx->delta_flag[g];
