@@ -494,8 +494,8 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
             std::vector<unsigned long long> hmis(n_passes);
             std::vector<int64_t> &m_g = ctx->h_mg;
             m_g.assign(n_lg, 0);
-            CH_CUDA(ctx, cudaMemcpyAsync(hmis.data(), mis, 8 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
-            CH_CUDA(ctx, cudaMemcpyAsync(m_g.data(), ctx->d_mg, 8 * n_lg, cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, ch_d2h(ctx, hmis.data(), mis, 8 * n_passes));
+            CH_CUDA(ctx, ch_d2h(ctx, m_g.data(), ctx->d_mg, 8 * n_lg));
             CH_CUDA(ctx, ch_sync(ctx));
             ctx->pass_mismatch.assign(n_passes, -1);
             for (int p = 0; p < n_passes; p++) {
@@ -588,7 +588,7 @@ chopper_status ch_assign_slots(chopper_ctx *ctx) {
     }
     if (conflicts) {
         std::vector<unsigned long long> hconf(n_passes);
-        CH_CUDA(ctx, cudaMemcpyAsync(hconf.data(), ctx->d_conf, 8 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, ch_d2h(ctx, hconf.data(), ctx->d_conf, 8 * n_passes));
         CH_CUDA(ctx, ch_sync(ctx));
         for (int p = 0; p < n_passes; p++)
             if (hconf[p] != ~0ull) ctx->pass_conflict[p] = (int64_t)hconf[p];
@@ -643,12 +643,11 @@ chopper_status ch_offsets_launch(chopper_ctx *ctx) {
     ctx->off_hs[0] = ctx->off_hs[1] = 0;
     ctx->off_ovf = 0;
     ctx->off_hdr.assign(2 * (size_t)nslots, 0);
-    CH_CUDA(ctx, cudaMemcpyAsync(ctx->delta.data(), ctx->d_delta, 8 * G, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(ctx->delta_flag.data(), ctx->d_delta_flag, 4 * G, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(ctx->off_hs, mskew, 16, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(&ctx->off_ovf, ctx->d_xovf, 4, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpy2DAsync(ctx->off_hdr.data(), 16, all, 8 * (size_t)W, 16, nslots, cudaMemcpyDeviceToHost,
-                                   ctx->st));
+    CH_CUDA(ctx, ch_d2h(ctx, ctx->delta.data(), ctx->d_delta, 8 * G));
+    CH_CUDA(ctx, ch_d2h(ctx, ctx->delta_flag.data(), ctx->d_delta_flag, 4 * G));
+    CH_CUDA(ctx, ch_d2h(ctx, ctx->off_hs, mskew, 16));
+    CH_CUDA(ctx, ch_d2h(ctx, &ctx->off_ovf, ctx->d_xovf, 4));
+    CH_CUDA(ctx, ch_d2h_2d(ctx, ctx->off_hdr.data(), 16, all, 8 * (size_t)W, 16, nslots));
     ctx->off_pending = true;
     return CHOPPER_OK;
 }

@@ -7,6 +7,7 @@
 #include <mutex>
 
 chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &msg) {
+    ctx->pin_pending.clear();            // read-backs of the failed stage are dropped (stack destinations)
     ctx->err = msg;
     ctx->latched_host |= 1u << s;
     return s;
@@ -14,6 +15,7 @@ chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &ms
 
 // failure protocol (chopper.h): remember this rank's first failure of the step (several ranks only)
 static chopper_status step(chopper_ctx *ctx, chopper_status s) {
+    if (s != CHOPPER_OK) ctx->pin_pending.clear();
     if (s != CHOPPER_OK && ctx->nranks > 1 && ctx->poison == CHOPPER_OK) ctx->poison = s;
     return s;
 }
@@ -144,6 +146,13 @@ chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int 
     if (cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
         return CHOPPER_E_CUDA;
+    }
+    // pinned host ring for the stage read-backs (host memory; device memory is never allocated)
+    c->pin_cap = 4u << 20;
+    if (cudaHostAlloc(&c->h_pin, c->pin_cap, cudaHostAllocDefault) != cudaSuccess) {
+        c->h_pin = nullptr;              // pageable read-backs (correct, slower)
+        c->pin_cap = 0;
+        cudaGetLastError();
     }
     *out = c;
     return CHOPPER_OK;
@@ -459,12 +468,10 @@ chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out) {
 chopper_status chopper_status_sync(chopper_ctx *ctx, uint32_t *mask) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
     uint32_t m = ctx->latched_host;
-    if (ch_sync(ctx) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;
-    if (ctx->d_rep) {
-        unsigned int dl = 0;
-        if (cudaMemcpy(&dl, &ctx->d_rep->latched, 4, cudaMemcpyDeviceToHost) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;
-        m |= dl;
-    }
+    unsigned int dl = 0;
+    if (ctx->d_rep && ch_d2h(ctx, &dl, &ctx->d_rep->latched, 4) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;
+    if (ch_sync(ctx) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;     // (one synchronization, the flag with it)
+    m |= dl;
     if (mask) *mask = m;
     const chopper_status order[] = {CHOPPER_E_CUDA, CHOPPER_E_NCCL, CHOPPER_E_VALIDATION, CHOPPER_E_ALIGNMENT,
                                     CHOPPER_E_AMBIGUOUS_SPANS, CHOPPER_E_RANGE, CHOPPER_E_INSUFFICIENT_DATA,
@@ -486,6 +493,7 @@ void chopper_destroy(chopper_ctx *ctx) {
         if (ctx->join_ev[q]) cudaEventDestroy(ctx->join_ev[q]);
     }
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
     delete ctx;
 }
 

@@ -93,6 +93,12 @@ struct chopper_ctx {
     bool hold_scratch = false;       // inside a side-stream branch: temporaries are not released (see tables.cu)
     int64_t launches = 0;
     int64_t syncs = 0;               // host synchronizations with the ctx stream
+    // pinned read-back ring: device->host copies of a stage land here asynchronously and are copied to
+    // their destinations at the stage's ch_sync (a pageable destination would block the host per copy)
+    unsigned char *h_pin = nullptr;
+    size_t pin_cap = 0, pin_used = 0;
+    struct PinCopy { void *dst; const void *src; size_t n; };
+    std::vector<PinCopy> pin_pending;
     std::string err;
     int stage = 0;                 // 1 loaded, 2 aligned, 3 attributed, 4 overlapped, 5 breakdown
     bool loaded_ok = false;
@@ -268,6 +274,7 @@ struct chopper_ctx {
         cudaError_t e_ = (call);                                                           \
         if (e_ != cudaSuccess) {                                                           \
             (ctx)->err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #call;     \
+            (ctx)->pin_pending.clear();                                                    \
             return CHOPPER_E_CUDA;                                                         \
         }                                                                                  \
     } while (0)
@@ -283,6 +290,7 @@ struct chopper_ctx {
         (ctx)->launches++;                                                                 \
         cudaError_t e_ = cudaGetLastError();                                               \
         if (e_ != cudaSuccess) {                                                           \
+            (ctx)->pin_pending.clear();                                                    \
             (ctx)->err = std::string("CUDA launch: ") + cudaGetErrorString(e_) + " @" +      \
                          std::to_string(__LINE__) + " " + __FILE__;                        \
             return CHOPPER_E_CUDA;                                                         \
@@ -293,7 +301,38 @@ chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &ms
 // host synchronization with the ctx stream (counted: chopper_host_syncs)
 inline cudaError_t ch_sync(chopper_ctx *ctx) {
     ctx->syncs++;
-    return cudaStreamSynchronize(ctx->st);
+    const cudaError_t e = cudaStreamSynchronize(ctx->st);
+    if (e == cudaSuccess)
+        for (const auto &p : ctx->pin_pending) memcpy(p.dst, p.src, p.n);
+    ctx->pin_pending.clear();
+    ctx->pin_used = 0;
+    return e;
+}
+// a pinned ring slot of n bytes (16 B aligned), or nullptr when the ring is full / absent
+inline unsigned char *ch_pin_slot(chopper_ctx *ctx, size_t n) {
+    const size_t a = (ctx->pin_used + 15) & ~(size_t)15;
+    if (!ctx->h_pin || a + n > ctx->pin_cap) return nullptr;
+    ctx->pin_used = a + n;
+    return ctx->h_pin + a;
+}
+// device -> host copy on the ctx stream whose destination is valid after the next ch_sync (the caller
+// reads it only after synchronizing, in the same scope for stack destinations)
+inline cudaError_t ch_d2h(chopper_ctx *ctx, void *dst, const void *src, size_t n) {
+    if (n == 0) return cudaSuccess;
+    unsigned char *slot = ch_pin_slot(ctx, n);
+    if (!slot) return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, ctx->st);   // pageable: blocking
+    const cudaError_t e = cudaMemcpyAsync(slot, src, n, cudaMemcpyDeviceToHost, ctx->st);
+    if (e == cudaSuccess) ctx->pin_pending.push_back({dst, slot, n});
+    return e;
+}
+inline cudaError_t ch_d2h_2d(chopper_ctx *ctx, void *dst, size_t dpitch, const void *src, size_t spitch,
+                             size_t width, size_t height) {
+    if (width == 0 || height == 0) return cudaSuccess;
+    unsigned char *slot = dpitch == width ? ch_pin_slot(ctx, width * height) : nullptr;
+    if (!slot) return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, cudaMemcpyDeviceToHost, ctx->st);
+    const cudaError_t e = cudaMemcpy2DAsync(slot, width, src, spitch, width, height, cudaMemcpyDeviceToHost, ctx->st);
+    if (e == cudaSuccess) ctx->pin_pending.push_back({dst, slot, width * height});
+    return e;
 }
 inline void ch_tick_on(chopper_ctx *ctx, int phase, int end, cudaStream_t st) {
     if (!ctx->timing) return;

@@ -1093,24 +1093,24 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     // host copies
     int64_t n = 0;
     unsigned int hovf = 0, hpoison = 0;
-    if (ctx->d_dense_ovf) CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ctx->d_dense_ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
+    if (ctx->d_dense_ovf) CH_CUDA(ctx, ch_d2h(ctx, &hovf, ctx->d_dense_ovf, 4));
     // one read-back: every array at its capacity (max_iters entries, at most 4096), the counts with it
     if (nbd > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 breakdown rows");
     if (nL > 256) return ch_fail(ctx, CHOPPER_E_RANGE, "more than 256 op labels in the report rows");
     const int64_t mc = std::min<int64_t>(MI, 4096);
-    CH_CUDA(ctx, cudaMemcpyAsync(&n, nref, 8, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(&hpoison, poison, 4, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(out->step, step, 4 * mc, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(out->complete, comp, 4 * mc, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(out->sampled, samp, 4 * mc, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(out->T, T, 8 * mc, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(out->aligned_first, af, 8 * mc, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(out->aligned_last, al, 8 * mc, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(out->throughput, tp, 8 * mc, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(&out->throughput_median, med, 8, cudaMemcpyDeviceToHost, ctx->st));
-    if (nbd > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->bd, bd, 8 * 16 * nbd, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(out->e2e, e2e, 8 * (1 + E2E_W), cudaMemcpyDeviceToHost, ctx->st));
-    if (nL > 0) CH_CUDA(ctx, cudaMemcpyAsync(out->report, rep, 8 * 16 * (size_t)nL, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, ch_d2h(ctx, &n, nref, 8));
+    CH_CUDA(ctx, ch_d2h(ctx, &hpoison, poison, 4));
+    CH_CUDA(ctx, ch_d2h(ctx, out->step, step, 4 * mc));
+    CH_CUDA(ctx, ch_d2h(ctx, out->complete, comp, 4 * mc));
+    CH_CUDA(ctx, ch_d2h(ctx, out->sampled, samp, 4 * mc));
+    CH_CUDA(ctx, ch_d2h(ctx, out->T, T, 8 * mc));
+    CH_CUDA(ctx, ch_d2h(ctx, out->aligned_first, af, 8 * mc));
+    CH_CUDA(ctx, ch_d2h(ctx, out->aligned_last, al, 8 * mc));
+    CH_CUDA(ctx, ch_d2h(ctx, out->throughput, tp, 8 * mc));
+    CH_CUDA(ctx, ch_d2h(ctx, &out->throughput_median, med, 8));
+    if (nbd > 0) CH_CUDA(ctx, ch_d2h(ctx, out->bd, bd, 8 * 16 * nbd));
+    CH_CUDA(ctx, ch_d2h(ctx, out->e2e, e2e, 8 * (1 + E2E_W)));
+    if (nL > 0) CH_CUDA(ctx, ch_d2h(ctx, out->report, rep, 8 * 16 * (size_t)nL));
     CH_CUDA(ctx, ch_sync(ctx));
     if (hpoison) return ch_fail(ctx, CHOPPER_E_STATE, "a peer rank failed earlier in this step (all-gather #2)");
     if (n > mc) return ch_fail(ctx, CHOPPER_E_RANGE, "more iterations than max_iters (or 4096) in chopper_global");
@@ -1153,7 +1153,7 @@ chopper_status ch_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t
                                                              off, rows);
     CH_LAUNCHED(ctx);
     int64_t n = 0;
-    CH_CUDA(ctx, cudaMemcpyAsync(&n, tot, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, ch_d2h(ctx, &n, tot, 8));
     CH_CUDA(ctx, ch_sync(ctx));
     const int64_t m = n < cap ? n : cap;
     if (m > 0 && out) CH_CUDA(ctx, cudaMemcpy(out, rows, 8 * 5 * (size_t)m, cudaMemcpyDeviceToHost));
@@ -1204,8 +1204,8 @@ chopper_status ch_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *S, const
     CH_LAUNCHED(ctx);
     double h[8];
     unsigned int hb[2];
-    CH_CUDA(ctx, cudaMemcpyAsync(h, dsum, 8 * 7, cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(hb, bad, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, ch_d2h(ctx, h, dsum, 8 * 7));
+    CH_CUDA(ctx, ch_d2h(ctx, hb, bad, 8));
     CH_CUDA(ctx, ch_sync(ctx));
     ctx->used = mark;
     if (hb[0]) return ch_fail(ctx, CHOPPER_E_VALIDATION, "CPU samples unsorted or out of range, or a bad topology entry");

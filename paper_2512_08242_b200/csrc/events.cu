@@ -804,9 +804,12 @@ __device__ __forceinline__ void tile_finish(SM &S, const EvParams &P, bool has, 
         Acc c;
         c.zero();
         int cf = 0;
-        for (int w = 0; w < tid; w++) {
-            if (S.wflag[w]) { c = S.wagg[w]; cf = 1; }
-            else c.merge(S.wagg[w]);
+#pragma unroll
+        for (int w = 0; w < SM::WARPS - 1; w++) {   // unrolled, predicated: the shared loads issue together
+            if (w < tid) {
+                if (S.wflag[w]) { c = S.wagg[w]; cf = 1; }
+                else c.merge(S.wagg[w]);
+            }
         }
         S.wcarry[tid] = c;
         S.wcflag[tid] = cf;
@@ -2390,7 +2393,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         CH_LAUNCHED(ctx);
     }
     unsigned long long last = 0;
-    CH_CUDA(ctx, cudaMemcpyAsync(&last, ctx->d_tile_state + ntile - 1, 8, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, ch_d2h(ctx, &last, ctx->d_tile_state + ntile - 1, 8));
     CH_CUDA(ctx, ch_sync(ctx));
     ctx->R = (int64_t)(last & VAL_MASK);
     if (ctx->R > cap) return ch_fail(ctx, CHOPPER_E_RANGE, "sub-runs exceed their structural bound");

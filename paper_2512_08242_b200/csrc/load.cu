@@ -511,7 +511,7 @@ chopper_status ch_fill_u64(chopper_ctx *ctx, unsigned long long *p, int64_t n, u
 }
 
 static chopper_status read_report(chopper_ctx *ctx) {
-    CH_CUDA(ctx, cudaMemcpyAsync(&ctx->h_rep, ctx->d_rep, sizeof(DevReport), cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, ch_d2h(ctx, &ctx->h_rep, ctx->d_rep, sizeof(DevReport)));
     CH_CUDA(ctx, ch_sync(ctx));
     return CHOPPER_OK;
 }
@@ -582,7 +582,7 @@ static chopper_status sort_segments(chopper_ctx *ctx, std::vector<int64_t> seg_l
         CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, c64, cst, cells, nullptr));
         unsigned int hfail = 0;
-        CH_CUDA(ctx, cudaMemcpyAsync(&hfail, fail, 4, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, ch_d2h(ctx, &hfail, fail, 4));
         CH_CUDA(ctx, ch_sync(ctx));
         if (!hfail) {
             k_ss_rank<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, cnt, cst, dlo,
@@ -729,8 +729,8 @@ chopper_status ch_load(chopper_ctx *ctx) {
     CH_LAUNCHED(ctx);
     ctx->bucket_beg.assign(nb + 1, 0);
     std::vector<unsigned int> hflag(nb + 1, 0);
-    CH_CUDA(ctx, cudaMemcpyAsync(ctx->bucket_beg.data(), beg, 8 * (nb + 1), cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(hflag.data(), bflag, 4 * (nb + 1), cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, ch_d2h(ctx, ctx->bucket_beg.data(), beg, 8 * (nb + 1)));
+    CH_CUDA(ctx, ch_d2h(ctx, hflag.data(), bflag, 4 * (nb + 1)));
     CH_TRY(read_report(ctx));
     ctx->bucket_beg[nb] = n;
     for (int b = nb - 1; b >= 0; b--)
@@ -799,8 +799,8 @@ static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back) {
     CH_LAUNCHED(ctx);
     ctx->bucket_beg.assign(nb + 1, 0);
     unsigned int hnm = 0;
-    CH_CUDA(ctx, cudaMemcpyAsync(ctx->bucket_beg.data(), ctx->d_bucket_beg, 8 * (nb + 1), cudaMemcpyDeviceToHost, ctx->st));
-    CH_CUDA(ctx, cudaMemcpyAsync(&hnm, nonmono, 4, cudaMemcpyDeviceToHost, ctx->st));
+    CH_CUDA(ctx, ch_d2h(ctx, ctx->bucket_beg.data(), ctx->d_bucket_beg, 8 * (nb + 1)));
+    CH_CUDA(ctx, ch_d2h(ctx, &hnm, nonmono, 4));
     CH_TRY(read_report(ctx));
     ctx->used = keep;
     if (hnm) {

@@ -502,8 +502,8 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         CH_TRY(gather(order));
         std::vector<unsigned long long> hb(n_lists + 1);
         unsigned int hbig = 0;
-        CH_CUDA(ctx, cudaMemcpyAsync(&hbig, big, 4, cudaMemcpyDeviceToHost, ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), lb2, 8 * (n_lists + 1), cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, ch_d2h(ctx, &hbig, big, 4));
+        CH_CUDA(ctx, ch_d2h(ctx, hb.data(), lb2, 8 * (n_lists + 1)));
         CH_CUDA(ctx, ch_sync(ctx));
         if (hbig) {
             // very long runs of equal starts: exact two-sort path (end desc, then (list, start) stable)
@@ -519,7 +519,7 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
             CH_TRY(ch_radix_sort(ctx, ks, vs, ko, vo, S, 0, rbits + lbits, &alt));
             order = alt ? vo : vs;
             CH_TRY(gather(order));
-            CH_CUDA(ctx, cudaMemcpyAsync(hb.data(), lb2, 8 * (n_lists + 1), cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, ch_d2h(ctx, hb.data(), lb2, 8 * (n_lists + 1)));
             CH_CUDA(ctx, ch_sync(ctx));
         }
         ctx->used = mark;
@@ -588,9 +588,8 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         k_euler_check<<<(unsigned)ceil_div(net, NT), NT, 0, ctx->st>>>(ctx->ET_t, ctx->d_et_beg, n_lists, net, et_bad);
         CH_LAUNCHED(ctx);
         // one read-back: laminarity flags and the tour check
-        CH_CUDA(ctx, cudaMemcpyAsync(ctx->list_flags.data(), ctx->d_list_flags, 4 * n_lists, cudaMemcpyDeviceToHost,
-                                     ctx->st));
-        CH_CUDA(ctx, cudaMemcpyAsync(&h_et_bad, et_bad, 4, cudaMemcpyDeviceToHost, ctx->st));
+        CH_CUDA(ctx, ch_d2h(ctx, ctx->list_flags.data(), ctx->d_list_flags, 4 * n_lists));
+        CH_CUDA(ctx, ch_d2h(ctx, &h_et_bad, et_bad, 4));
         CH_CUDA(ctx, ch_sync(ctx));
         ctx->used = mark;
     }

@@ -211,9 +211,12 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
             double cc[CT_SG];
 #pragma unroll
             for (int q = 0; q < CT_SG; q++) cc[q] = 0.0;
-            for (int w = 0; w < tid; w++) {
 #pragma unroll
-                for (int q = 0; q < CT_SG; q++) cc[q] = S.aflag[w] ? S.agg[w][q] : cc[q] + S.agg[w][q];
+            for (int w = 0; w < CT_WARPS - 1; w++) {
+                if (w < tid) {
+#pragma unroll
+                    for (int q = 0; q < CT_SG; q++) cc[q] = S.aflag[w] ? S.agg[w][q] : cc[q] + S.agg[w][q];
+                }
             }
 #pragma unroll
             for (int q = 0; q < CT_SG; q++) S.carry[tid][q] = cc[q];
@@ -1387,12 +1390,41 @@ static void key_layout(chopper_ctx *ctx, KeyLayout &L) {
 }
 
 // all table stages, enqueued without host round trips except the rare radix-sort fallback check
+
+// development aid (CHOPPER_DBG_TICKS=1): device timestamps of the tables stages, printed after the stage's sync
+namespace {
+struct DbgTicks {
+    bool on = getenv("CHOPPER_DBG_TICKS") != nullptr;
+    cudaEvent_t ev[32] = {};
+    const char *lab[32] = {};
+    int n = 0;
+    void mark(cudaStream_t st, const char *l) {
+        if (!on || n >= 32) return;
+        if (!ev[n]) cudaEventCreate(&ev[n]);
+        cudaEventRecord(ev[n], st);
+        lab[n++] = l;
+    }
+    void dump() {
+        if (!on || n < 2) { n = 0; return; }
+        fprintf(stderr, "[tables]");
+        for (int i = 1; i < n; i++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, " %s %.3f", lab[i], ms);
+        }
+        fprintf(stderr, "\n");
+        n = 0;
+    }
+};
+DbgTicks g_dbg;
+}
 static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
     const int C = ctx->C;
     const int64_t R = ctx->R;
     KeyLayout L;
     key_layout(ctx, L);
     const int key_bits = L.sh_lg + ctx->kg;
+    g_dbg.mark(ctx->st, "begin");
     CH_ALLOC_BEGIN;
     int32_t *lg_gpu_d = CH_ALLOC(ctx, int32_t, ctx->n_lg + 1);
     ctx->sub.cnt = CH_ALLOC(ctx, double, (int64_t)(C > 0 ? C : 1) * std::max<int64_t>(R, 1));
@@ -1424,6 +1456,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[0], ctx->side[0]));
         counters_forked = true;
     }
+    g_dbg.mark(ctx->st, "fork");
     // instances: sort of sub-runs by key, then groups of equal keys
     unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, R + 1), *k2 = CH_ALLOC(ctx, unsigned long long, R + 1);
     uint32_t *v1 = CH_ALLOC(ctx, uint32_t, R + 1), *v2 = CH_ALLOC(ctx, uint32_t, R + 1);
@@ -1447,9 +1480,10 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
             k_prefix_check<<<grid_for(R, NT), NT, 0, ctx->st>>>(k1, st, nseg_d, L.sh_it, bad);
             CH_LAUNCHED(ctx);
             unsigned int hbad = 0;
-            CH_CUDA(ctx, cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, ch_d2h(ctx, &hbad, bad, 4));
             CH_CUDA(ctx, ch_sync(ctx));
             if (!hbad) {
+    g_dbg.mark(ctx->st, "prefsync");
                 static bool ss_attr = false;
                 if (!ss_attr) {
                     CH_CUDA(ctx, cudaFuncSetAttribute(k_seg_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1476,6 +1510,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         }
         if (!done) CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, R, 0, key_bits, &alt));
     }
+    g_dbg.mark(ctx->st, "ordered");
     unsigned long long *ks = alt ? k2 : k1;
     uint32_t *so = alt ? v2 : v1;
     {
@@ -1483,6 +1518,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         CH_TRY(group(ctx, ks, R, nullptr, 0, &starts, &ng_dev));
         CH_TRY(alloc_table(ctx, ctx->inst, std::max<int64_t>(R, 1), C, true));
         if (counters_forked) CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->join_ev[0], 0));
+    g_dbg.mark(ctx->st, "join");
         ctx->inst.n_dev = ng_dev;
         if (R > 0) {
             CH_TRY(sum_rows(ctx, subv, so, starts, ng_dev, R, 0, 0, C, view(ctx->inst)));
@@ -1548,6 +1584,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
     CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[1], ctx->st));
     ctx->st = main_st;
     CH_TRY(pst);
+    g_dbg.mark(ctx->st, "instdone");
     // roll-ups (D12): instance -> layer (staged), -> phase, -> iteration, -> gpu (warp per parent)
     // instances per layer: ~ instances / layer spans of the local gpus (fan-out hint for the staging width)
     const int64_t n_layers = std::max<int64_t>(ctx->n_layer_spans, 1);
@@ -1555,9 +1592,11 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
     const int fan_ly = (int)std::max<int64_t>(1, std::min<int64_t>(64, fan));
     // thousands of instances per layer (deep op trees, config 5): a warp per layer; else the staged fold
     CH_TRY(rollup(ctx, ctx->inst, ctx->layer, L.sh_ly, 3, fan > 256 ? 1 : 0, L, lg_gpu_d, fan_ly));
+    g_dbg.mark(ctx->st, "layer");
     CH_TRY(rollup(ctx, ctx->layer, ctx->phase, L.sh_ph, 2, 1, L, lg_gpu_d));
     CH_TRY(rollup(ctx, ctx->phase, ctx->iter, L.sh_it, 1, 1, L, lg_gpu_d));
     CH_TRY(rollup(ctx, ctx->iter, ctx->gpurow, L.sh_lg, 0, 1, L, lg_gpu_d));
+    g_dbg.mark(ctx->st, "rollups");
     // iteration extras
     {
         const int64_t cap = std::max<int64_t>(ctx->iter.cap, 1);
@@ -1574,6 +1613,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
         CH_LAUNCHED(ctx);
     }
     CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->join_ev[1], 0));
+    g_dbg.mark(ctx->st, "pointsjoin");
     // derived ratio-of-sums rates
     if (ctx->n_ratios > 0) {
         RowTable *ts[2] = {&ctx->point, &ctx->iter};
@@ -1588,6 +1628,7 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
     // derived-metric registry
     CH_TRY(ch_eval_metrics(ctx, ctx->point));
     CH_TRY(ch_eval_metrics(ctx, ctx->iter));
+    g_dbg.mark(ctx->st, "metrics");
     return CHOPPER_OK;
 }
 
@@ -1605,15 +1646,17 @@ chopper_status ch_tables(chopper_ctx *ctx) {
         RowTable *tabs[6] = {&ctx->inst, &ctx->layer, &ctx->phase, &ctx->iter, &ctx->gpurow, &ctx->point};
         int64_t hn[6] = {0, 0, 0, 0, 0, 0};
         for (int q = 0; q < 6; q++)
-            if (tabs[q]->n_dev) CH_CUDA(ctx, cudaMemcpyAsync(&hn[q], tabs[q]->n_dev, 8, cudaMemcpyDeviceToHost, ctx->st));
+            if (tabs[q]->n_dev) CH_CUDA(ctx, ch_d2h(ctx, &hn[q], tabs[q]->n_dev, 8));
         unsigned int hovf = 0;
-        if (ovf) CH_CUDA(ctx, cudaMemcpyAsync(&hovf, ovf, 4, cudaMemcpyDeviceToHost, ctx->st));
+        if (ovf) CH_CUDA(ctx, ch_d2h(ctx, &hovf, ovf, 4));
         std::vector<unsigned int> cb((size_t)std::max(n_lg * C, 1), 0), pb(std::max(n_passes, 1), 0);
         if (C > 0 && ctx->R > 0)
-            CH_CUDA(ctx, cudaMemcpyAsync(cb.data(), ctx->d_colbad, 4 * (size_t)n_lg * C, cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, ch_d2h(ctx, cb.data(), ctx->d_colbad, 4 * (size_t)n_lg * C));
         if (n_passes > 0)
-            CH_CUDA(ctx, cudaMemcpyAsync(pb.data(), ctx->d_pass_bad, 4 * n_passes, cudaMemcpyDeviceToHost, ctx->st));
+            CH_CUDA(ctx, ch_d2h(ctx, pb.data(), ctx->d_pass_bad, 4 * n_passes));
+        g_dbg.mark(ctx->st, "readback");
         CH_CUDA(ctx, ch_sync(ctx));
+        g_dbg.dump();
         for (int q = 0; q < 6; q++) tabs[q]->n = hn[q];
         if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "op span label >= n_labels");
         bool changed = false;
