@@ -164,14 +164,20 @@ __global__ void __launch_bounds__(MR_NT) k_meta_apply(const uint32_t *__restrict
     int64_t r1 = tex[ntile + blockIdx.x] + (int64_t)((ex >> 21) & 0x1FFFFF);
     int64_t r2 = tex[2 * ntile + blockIdx.x] + (int64_t)(ex >> 42);
     int32_t nr[MR_IPT];
+    int gcur = -1, lg = 0;                // the gpu's local index and rank base, reloaded when the gpu changes
+    int64_t b0 = 0;
 #pragma unroll
     for (int k = 0; k < MR_IPT; k++) {
         int64_t i = i0 + k;
         if (i >= n) break;
         uint32_t m = mm[k];
-        int lg = gpu_lg[gpu_of(m)];
+        if (gpu_of(m) != gcur) {
+            gcur = gpu_of(m);
+            lg = gpu_lg[gcur];
+            b0 = base[lg];
+        }
         int kd = kind_of(m);
-        nr[k] = (int32_t)(r0 - base[lg]);
+        nr[k] = (int32_t)(r0 - b0);
         if (kd == CK_AG || kd == CK_RS) {
             int64_t j = kd == CK_AG ? r1 - base[(n_lg + 1) + lg] : r2 - base[2 * (n_lg + 1) + lg];
             if (j >= K) atomicOr(ovf, 1u);

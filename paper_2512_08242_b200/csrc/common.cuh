@@ -133,6 +133,8 @@ struct chopper_ctx {
     int64_t *d_pred_end = nullptr;   // [N] end of chain predecessor or NONE
     bool full_sort = false;
     bool lean = false;               // one compute stream per gpu, start-monotone in dispatch order (lean a2)
+    bool tables_radix = false;       // sticky: a trace of this ctx needed the radix instance sort (tables.cu)
+    unsigned int *d_prefix_bad = nullptr;   // deferred instance-order check, read with the tables' row counts
 
     // spans (push order)
     int64_t S_loc = 0;               // spans of local gpus with positive length

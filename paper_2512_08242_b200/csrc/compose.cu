@@ -187,6 +187,20 @@ __device__ double med_f64(double *a, int n, double *sh) {
     return m;
 }
 
+// medians of up to MED_SM values sorted in a static shared-memory buffer (16 KB) instead of in place in global
+// memory (each bitonic stage would otherwise be a global-memory round trip)
+constexpr int MED_SM = 2048;
+__device__ __forceinline__ int64_t *med_buf() {
+    __shared__ __align__(16) int64_t b[MED_SM];
+    return b;
+}
+__device__ __forceinline__ double med_i64_s(int64_t *a, int n) {
+    return med_i64(a, n, pow2ceil(n) <= MED_SM ? med_buf() : nullptr);
+}
+__device__ __forceinline__ double med_f64_s(double *a, int n) {
+    return med_f64(a, n, pow2ceil(n) <= MED_SM ? reinterpret_cast<double *>(med_buf()) : nullptr);
+}
+
 enum { BD_FIT = 1, BD_NO_FLOPS = 2, BD_NO_UTIL = 4, BD_UTIL_RANGE = 8, BD_D0_ZERO = 16, BD_NO_CYCLES = 32,
        BD_NO_SAMPLES = 64, BD_INSUFFICIENT = 128 };
 
@@ -583,7 +597,7 @@ __global__ void __launch_bounds__(512) k_e2e(const int64_t *__restrict__ blk, La
     }
     const int n = s_n < maxp2 ? s_n : (int)maxp2;
     double m = NAN;
-    if (n > 0) m = med_i64(w, n, nullptr);
+    if (n > 0) m = med_i64_s(w, n);
     if (threadIdx.x == 0) {
         out[1 + k] = m;
         if (k == 0) out[0] = n;
@@ -715,7 +729,7 @@ __global__ void __launch_bounds__(256) k_global(GlobArgs A) {
     __syncthreads();
     int nst = s_nst;
     double m = NAN;
-    if (nst > 0) m = med_f64(A.work, nst, nullptr);
+    if (nst > 0) m = med_f64_s(A.work, nst);
     if (threadIdx.x == 0) *A.med = m;
 }
 
@@ -773,10 +787,17 @@ __global__ void __launch_bounds__(256) k_cpu_ts(CpuArgs A, const int64_t *__rest
         __syncwarp();
         const int64_t a = starts[q], b = starts[q + 1];
         int64_t act = 0;
+        double s = 0.0;
         for (int64_t k0 = a; k0 < b; k0 += 32) {
             const int64_t k = k0 + l;
-            const bool on = k < b && A.util[k] > 0.0;
+            const double u = k < b ? A.util[k] : 0.0;
+            const bool on = k < b && u > 0.0;
             act += __popc(__ballot_sync(CH_FULL, on));
+            // C_min = sum of Util_i / 100: the divisions in parallel, the sum in logical-core
+            // order (every lane adds the same terms in the same order, so lane 0 holds the sequential sum)
+            const double qd = u / 100.0;
+            const int m = (int)min((int64_t)32, b - k0);
+            for (int j = 0; j < m; j++) s += __shfl_sync(CH_FULL, qd, j);
             if (on) {
                 const int p = A.topo[A.core[k]];
                 const unsigned bit = 1u << (p & 31);
@@ -797,8 +818,6 @@ __global__ void __launch_bounds__(256) k_cpu_ts(CpuArgs A, const int64_t *__rest
             p2 += __shfl_xor_sync(CH_FULL, p2, o);
         }
         if (l == 0) {
-            double s = 0.0;
-            for (int64_t k = a; k < b; k++) s += A.util[k] / 100.0;     // PAPER.md:676, logical-core order
             ca[q] = act;
             cm[q] = s;
             if (p1) atomicAdd(&pairs[0], p1);
@@ -831,8 +850,8 @@ __global__ void __launch_bounds__(512) k_cpu_summary(int64_t *__restrict__ ca, d
     atomicMax((unsigned long long *)&s_mmax, (unsigned long long)__double_as_longlong(mm));   // non-negative doubles
     for (int x = threadIdx.x; x < (n_phys + 31) / 32; x += blockDim.x) atomicAdd(&s_occ, __popc(ever[x]));
     __syncthreads();
-    const double ma = n > 0 ? med_i64(ca, n, nullptr) : NAN;
-    const double mc = n > 0 ? med_f64(cm, n, nullptr) : NAN;
+    const double ma = n > 0 ? med_i64_s(ca, n) : NAN;
+    const double mc = n > 0 ? med_f64_s(cm, n) : NAN;
     if (threadIdx.x == 0) {
         out[0] = n;
         out[1] = ma;

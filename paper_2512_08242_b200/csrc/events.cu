@@ -125,14 +125,23 @@ __global__ void __launch_bounds__(UN_NT) k_union_block(const uint32_t *__restric
         __syncthreads();
     }
     const int64_t mcount = s_m;
-    // prefix lengths
+    // prefix lengths (UN_IPT consecutive merged intervals per thread)
     int64_t acc = 0;
-    for (int64_t b2 = 0; b2 < mcount; b2 += UN_NT) {
-        const int64_t m = b2 + tid;
-        const int64_t len = m < mcount ? Ue[ob + m] - Us[ob + m] : 0;
+    for (int64_t b2 = 0; b2 < mcount; b2 += UN_CH) {
+        const int64_t m0 = b2 + (int64_t)tid * UN_IPT;
+        int64_t len[UN_IPT], s = 0;
+#pragma unroll
+        for (int u = 0; u < UN_IPT; u++) {
+            len[u] = m0 + u < mcount ? Ue[ob + m0 + u] - Us[ob + m0 + u] : 0;
+            s += len[u];
+        }
         int64_t tot;
-        const int64_t ex = block_excl_sum<UN_NT>(len, &tot, sm);
-        if (m < mcount) UP[ob + m] = acc + ex;
+        int64_t ex = block_excl_sum<UN_NT>(s, &tot, sm);
+#pragma unroll
+        for (int u = 0; u < UN_IPT; u++) {
+            if (m0 + u < mcount) UP[ob + m0 + u] = acc + ex;
+            ex += len[u];
+        }
         acc += tot;
     }
     if (tid == 0) { Ubeg[lg] = ob; Ucnt[lg] = mcount; }

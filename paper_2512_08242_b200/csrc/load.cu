@@ -361,6 +361,9 @@ __global__ void __launch_bounds__(LN_NT) k_lean_chain(const uint32_t *__restrict
     int64_t p_ks = 0, p_ke = 0;
     if (before >= 0 && cp > 0) { p_ks = ks[before]; p_ke = ke[before]; }
     int64_t pes[LN_IPT];                  // chain ends (CH_NONE_TS at non-compute events: never read there)
+    // per-gpu bases, reloaded only when the gpu changes (a thread's 8 events are nearly always one gpu's)
+    int gcur = -1;
+    int64_t cbase = 0, pbase = 0, gb0 = 0;
 #pragma unroll
     for (int k = 0; k < LN_IPT; k++) {
         pes[k] = CH_NONE_TS;
@@ -368,15 +371,21 @@ __global__ void __launch_bounds__(LN_NT) k_lean_chain(const uint32_t *__restrict
         const int64_t i = i0 + k;
         const uint32_t m = mt[k];
         const int kd = kind_of(m);
-        const int lg = gpu_lg[gpu_of(m)];
+        if (gpu_of(m) != gcur && (is_comm(kd) || kd == CK_COMPUTE)) {
+            gcur = gpu_of(m);
+            const int lg = gpu_lg[gcur];
+            cbase = bbeg[lg * NG + 0] - lg_comm0[lg];
+            pbase = bbeg[lg * NG + 1] - lg_comp0[lg];
+            gb0 = g_beg[lg];
+        }
         if (is_comm(kd)) {
-            perm[bbeg[lg * NG + 0] + (ex_c - lg_comm0[lg])] = (uint32_t)i;
+            perm[cbase + ex_c] = (uint32_t)i;
             ex_c++;
         } else if (kd == CK_COMPUTE) {
-            perm[bbeg[lg * NG + 1] + (ex_p - lg_comp0[lg])] = (uint32_t)i;
+            perm[pbase + ex_p] = (uint32_t)i;
             ex_p++;
             int64_t pe = CH_NONE_TS;
-            if (before >= g_beg[lg]) {
+            if (before >= gb0) {
                 pe = p_ke;
                 if (vs[k] < p_ks) atomicOr(nonmono, 1u);          // not start-monotone: the full path sorts it
                 if (vs[k] < pe) viol(rep, CV_STREAM_OVERLAP, i);

@@ -1468,21 +1468,24 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
     bool alt = false;
     {
         // segmented sort inside (gpu, iteration) prefixes; radix sort if the prefixes are not in order
+        // The check that the (gpu, iteration) prefixes come in order (and that no segment exceeds SS_MAX) is not
+        // waited for: its flag is read with the row counts at the end of the stage, and a failed check redoes the
+        // tables with the radix sort (ch_tables), which this ctx then uses from the start (tables_radix)
         bool done = false;
-        if (R > 1) {
+        ctx->d_prefix_bad = nullptr;
+        if (R > 1 && !ctx->tables_radix) {
+            unsigned int *bad = CH_ALLOC(ctx, unsigned int, 1);
+            CH_ALLOC_END(ctx);
+            ctx->d_prefix_bad = bad;
             size_t mk = ctx->used;
             int64_t *nv_d = CH_ALLOC(ctx, int64_t, 1);
-            unsigned int *bad = CH_ALLOC(ctx, unsigned int, 1);
             CH_ALLOC_END(ctx);
             int64_t *st = nullptr, *nseg_d = nullptr;
             CH_TRY(group(ctx, k1, R, nullptr, L.sh_it, &st, &nseg_d, 1));   // segments: equal (gpu, iteration)
             CH_CUDA(ctx, cudaMemsetAsync(bad, 0, 4, ctx->st));
             k_prefix_check<<<grid_for(R, NT), NT, 0, ctx->st>>>(k1, st, nseg_d, L.sh_it, bad);
             CH_LAUNCHED(ctx);
-            unsigned int hbad = 0;
-            CH_CUDA(ctx, ch_d2h(ctx, &hbad, bad, 4));
-            CH_CUDA(ctx, ch_sync(ctx));
-            if (!hbad) {
+            {
     g_dbg.mark(ctx->st, "prefsync");
                 static bool ss_attr = false;
                 if (!ss_attr) {
@@ -1647,8 +1650,9 @@ chopper_status ch_tables(chopper_ctx *ctx) {
         int64_t hn[6] = {0, 0, 0, 0, 0, 0};
         for (int q = 0; q < 6; q++)
             if (tabs[q]->n_dev) CH_CUDA(ctx, ch_d2h(ctx, &hn[q], tabs[q]->n_dev, 8));
-        unsigned int hovf = 0;
+        unsigned int hovf = 0, hbad = 0;
         if (ovf) CH_CUDA(ctx, ch_d2h(ctx, &hovf, ovf, 4));
+        if (ctx->d_prefix_bad) CH_CUDA(ctx, ch_d2h(ctx, &hbad, ctx->d_prefix_bad, 4));   // deferred order check
         std::vector<unsigned int> cb((size_t)std::max(n_lg * C, 1), 0), pb(std::max(n_passes, 1), 0);
         if (C > 0 && ctx->R > 0)
             CH_CUDA(ctx, ch_d2h(ctx, cb.data(), ctx->d_colbad, 4 * (size_t)n_lg * C));
@@ -1658,6 +1662,13 @@ chopper_status ch_tables(chopper_ctx *ctx) {
         CH_CUDA(ctx, ch_sync(ctx));
         g_dbg.dump();
         for (int q = 0; q < 6; q++) tabs[q]->n = hn[q];
+        if (hbad) {
+            // instance prefixes out of order (or a segment over SS_MAX): the segmented order was not valid; redo
+            // the stage with the radix sort (this ctx keeps it)
+            ctx->tables_radix = true;
+            round--;
+            continue;
+        }
         if (hovf) return ch_fail(ctx, CHOPPER_E_RANGE, "op span label >= n_labels");
         bool changed = false;
         for (int p = 0; p < n_passes; p++) {

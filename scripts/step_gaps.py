@@ -9,6 +9,8 @@ from paper_2512_08242_b200 import pipeline as pl
 
 b = tracegen.generate(tracegen.config(int(sys.argv[1]) if len(sys.argv) > 1 else 4))
 p = ch.default_params(b, b.labels, tracegen.workload_shapes(b.cfg), tracegen.op_kind)
+if len(sys.argv) > 2 and sys.argv[2] == "shard":      # traced GPU 0's shard (one rank of eight)
+    b = b.gpu_slice([0])
 stream = torch.cuda.Stream()
 pipe = ch.Pipeline(b.cfg.n_gpus, len(b.labels), 256, 1 << 15, device=0, stream=stream)
 pipe.upload(b, b.n_counters)
