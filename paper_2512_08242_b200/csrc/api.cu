@@ -80,7 +80,13 @@ size_t chopper_scratch_plan(const chopper_config *cfg, const chopper_shape *sh, 
     // push-order span arrays (32 B), Euler tables (12 B per endpoint), merged key table (16 B per endpoint),
     // chunk stacks and sparse tables (~8 B)
     it.spans = S * 32 + (2 * S + 4 * G + 2) * 28 + S * 8 + 4096 * (G + 1);
+    // the push-order sort's key / value buffers, held from chopper_load_columns to chopper_attribute (the sort
+    // runs beside chopper_align)
+    it.spans += S * 24 + 16 * (4 * G + 2);
     it.unions = NC * 24 + (NC + M + 2 * G) * 44 + M * 40;
+    // the preparation runs beside chopper_attribute and keeps its transients for the step: the compute-union sort
+    // keys (several streams) and the sample terms
+    it.unions += (multi ? N * 20 : 0) + M * 17;
     it.subruns = Rb * 144 + Rb * 8 * C + tiles * (8 * 3 + 16 + 64);
     it.instances = Rb * (row + 16);                                       // + group starts
     size_t roll = 0;
@@ -142,6 +148,12 @@ chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int 
             delete c;
             return CHOPPER_E_CUDA;
         }
+    }
+    if (cudaEventCreateWithFlags(&c->prep_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->span_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->span_join, cudaEventDisableTiming) != cudaSuccess) {
+        delete c;
+        return CHOPPER_E_CUDA;
     }
     if (cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming) != cudaSuccess) {
         delete c;
@@ -244,6 +256,22 @@ static chopper_status attribute(chopper_ctx *ctx, int32_t *span_idx) {
     }
     if (ctx->stage != 2) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_attribute out of order");
     ch_tick(ctx, 2, 0);
+    // chopper_overlap's preparation (comm union, sample integrals, timeline) needs nothing from the span tables:
+    // it runs on side[1] beside the span build, whose kernels are small and whose host synchronizations would
+    // leave the gpu idle; chopper_overlap joins it
+    {
+        CH_CUDA(ctx, cudaEventRecord(ctx->fork_ev, ctx->st));
+        CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[1], ctx->fork_ev, 0));
+        cudaStream_t main_st = ctx->st;
+        ctx->st = ctx->side[1];
+        ctx->hold_scratch = true;
+        const chopper_status ps = ch_overlap_prep(ctx);
+        ctx->hold_scratch = false;
+        CH_CUDA(ctx, cudaEventRecord(ctx->prep_join, ctx->st));
+        ctx->st = main_st;
+        CH_TRY(ps);
+        ctx->prep_done = ctx->prep_pending = true;
+    }
     CH_TRY(ch_build_spans(ctx));
     CH_TRY(ch_attr_pass(ctx, span_idx));
     ch_tick(ctx, 2, 1);
@@ -261,7 +289,12 @@ static chopper_status overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_n
                               int64_t *psi) {
     if (ctx->stage != 3) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_overlap out of order");
     ch_tick(ctx, 3, 0);
-    CH_TRY(ch_overlap_prep(ctx));
+    if (ctx->prep_pending) {                    // enqueued beside chopper_attribute
+        CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->prep_join, 0));
+        ctx->prep_pending = false;
+    }
+    if (!ctx->prep_done) CH_TRY(ch_overlap_prep(ctx));
+    ctx->prep_done = false;
     ch_tick(ctx, 3, 1);
     CH_TRY(ch_event_pass(ctx, ovl_ns, prep_ns, call_ns, phi, psi));
     ctx->stage = 4;
@@ -493,6 +526,9 @@ void chopper_destroy(chopper_ctx *ctx) {
         if (ctx->join_ev[q]) cudaEventDestroy(ctx->join_ev[q]);
     }
     if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+    if (ctx->span_fork) cudaEventDestroy(ctx->span_fork);
+    if (ctx->prep_join) cudaEventDestroy(ctx->prep_join);
+    if (ctx->span_join) cudaEventDestroy(ctx->span_join);
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
     delete ctx;
 }

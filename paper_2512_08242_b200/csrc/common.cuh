@@ -78,6 +78,23 @@ struct chopper_ctx {
     cudaStream_t st = nullptr;
     cudaStream_t side[3] = {nullptr, nullptr, nullptr};   // fork / join of independent small kernels
     cudaEvent_t fork_ev = nullptr, join_ev[3] = {nullptr, nullptr, nullptr};
+    // span push-order sort enqueued on side[2] at the end of chopper_load_columns (spans.cu), so that it runs
+    // beside chopper_align; chopper_attribute joins it.  Its buffers stay allocated for the step.
+    cudaEvent_t span_fork = nullptr, span_join = nullptr;
+    bool span_pending = false;       // the sort's kernels were enqueued on side[2] and are not joined yet
+    bool span_launched = false;      // ch_span_sort_launch ran for this step (its buffers are allocated)
+    // the union / sample / timeline preparation of chopper_overlap, enqueued on side[1] by chopper_attribute
+    cudaEvent_t prep_join = nullptr;
+    bool prep_done = false, prep_pending = false;
+    struct SpanSort {
+        unsigned long long *k1, *k2, *lb, *lb2;
+        uint32_t *v1, *v2, *order;
+        unsigned long long *okeys;
+        unsigned int *big;
+        int32_t *Plist;
+        int rbits, lbits;
+        int64_t smin, emax;
+    } ss{};
     void *nccl = nullptr;
     int rank = 0, nranks = 1;
     chopper_allgather_fn ag_fn = nullptr;    // exchange transport (chopper_set_allgather), else NCCL
@@ -493,6 +510,7 @@ chopper_status ch_radix_partition_meta(chopper_ctx *ctx, const uint32_t *meta, c
 chopper_status ch_load(chopper_ctx *ctx);
 // spans.cu
 chopper_status ch_build_spans(chopper_ctx *ctx);
+chopper_status ch_span_sort_launch(chopper_ctx *ctx);
 chopper_status ch_attr_pass(chopper_ctx *ctx, int32_t *span_idx);
 // events.cu
 chopper_status ch_overlap_prep(chopper_ctx *ctx);

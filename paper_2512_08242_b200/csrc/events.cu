@@ -2119,7 +2119,7 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
         bool alt;
         CH_TRY(ch_radix_sort(ctx, k1, ctx->d_vperm, k2, v2, N, 0, tsbits + lgbits, &alt));
         if (alt) CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_vperm, v2, 4 * N, cudaMemcpyDeviceToDevice, ctx->st));
-        ctx->used = mark;
+        if (!ctx->hold_scratch) ctx->used = mark;
         // compute events of lg are contiguous in vperm: counts per gpu from the buckets
         std::vector<int64_t> a(n_lg), b(n_lg);
         int64_t off = 0;
@@ -2159,10 +2159,11 @@ chopper_status ch_overlap_prep(chopper_ctx *ctx) {
         CH_LAUNCHED(ctx);
         CH_TRY(ch_seg_scan_i64(ctx, tf, hd, ctx->d_smp_phi, M, 0));
         CH_TRY(ch_seg_scan_i64(ctx, tp, hd, ctx->d_smp_psi, M, 0));
-        ctx->used = mark;
+        if (!ctx->hold_scratch) ctx->used = mark;
     }
-    // timeline for the window-staged event pass
-    if (ctx->et_ok && n_lg > 0) {
+    // timeline for the window-staged event passes (built before the span lists' laminarity is known when this
+    // runs beside chopper_attribute; unused for a non-laminar trace)
+    if (n_lg > 0) {
         std::vector<int64_t> tb(n_lg + 1), nc(n_lg);
         int64_t off = 0;
         for (int l = 0; l < n_lg; l++) {

@@ -544,6 +544,8 @@ static chopper_status finish_load(chopper_ctx *ctx) {
     fill_public_report(ctx);
     if (ctx->h_rep.val_count[CV_STREAM_OVERLAP]) ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
     ctx->loaded_ok = true;
+    // the spans are validated: their push-order sort starts now, beside chopper_align (spans.cu)
+    CH_TRY(ch_span_sort_launch(ctx));
     ctx->mark_after_load = ctx->used;
     return CHOPPER_OK;
 }
@@ -619,6 +621,18 @@ static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back);
 chopper_status ch_load(chopper_ctx *ctx) {
     const int G = ctx->cfg.n_traced_gpus;
     const int64_t n = ctx->N;
+    // a span sort of an earlier step that was never joined (the step failed) must finish before its scratch is
+    // reused
+    if (ctx->span_pending) {
+        CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->span_join, 0));
+        ctx->span_pending = false;
+    }
+    ctx->span_launched = false;
+    if (ctx->prep_pending) {                    // likewise chopper_overlap's preparation
+        CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->prep_join, 0));
+        ctx->prep_pending = false;
+    }
+    ctx->prep_done = false;
     ctx->used = 0;
     CH_ALLOC_BEGIN;
     ctx->d_rep = CH_ALLOC(ctx, DevReport, 1);

@@ -508,7 +508,7 @@ chopper_status ch_seg_scan_i64(chopper_ctx *ctx, const int64_t *in, const uint8_
     else if (op == 0) k_seg_apply<0, true><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
     else k_seg_apply<0, false><<<(unsigned)ntile, SC_NT, 0, ctx->st>>>(in, head, n, carry, out);
     CH_LAUNCHED(ctx);
-    ctx->used = mark;
+    if (!ctx->hold_scratch) ctx->used = mark;
     return CHOPPER_OK;
 }
 
@@ -553,7 +553,7 @@ chopper_status ch_radix_sort(chopper_ctx *ctx, unsigned long long *keys, uint32_
         alt = !alt;
     }
     *result_in_alt = alt;
-    ctx->used = mark;
+    if (!ctx->hold_scratch) ctx->used = mark;
     return CHOPPER_OK;
 }
 

@@ -441,7 +441,14 @@ __global__ void k_attr_out(SpanView v, const int64_t *__restrict__ tl, const uin
 }
 }  // namespace
 
-chopper_status ch_build_spans(chopper_ctx *ctx) {
+// The push-order sort (a5, first half): one stable (list, start) radix sort with input order as tie-break, equal-
+// start runs reordered by (end desc, index desc) in place, then the gather into push order with the list
+// begins.  Enqueued by chopper_load_columns on side[2] once the spans are validated, so that it runs beside
+// chopper_align (whose host synchronizations would otherwise leave the gpu idle); every buffer it touches is
+// allocated here and kept for the step.
+chopper_status ch_span_sort_launch(chopper_ctx *ctx) {
+    ctx->span_pending = false;
+    ctx->span_launched = true;
     const int64_t S = ctx->S;
     const int n_lg = ctx->n_lg;
     const int n_lists = n_lg * 4;
@@ -453,44 +460,85 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
     ctx->P_orig = CH_ALLOC(ctx, int32_t, S);
     ctx->P_label = CH_ALLOC(ctx, int32_t, S);
     ctx->P_parent = CH_ALLOC(ctx, int32_t, S);
-    int32_t *Plist = CH_ALLOC(ctx, int32_t, S);
+    ctx->ss.Plist = CH_ALLOC(ctx, int32_t, S);
     CH_ALLOC_END(ctx);
-    CH_CUDA(ctx, cudaMemsetAsync(ctx->d_list_flags, 0, sizeof(int32_t) * (n_lists + 1), ctx->st));
+    if (n_lg == 0 || S == 0) return CHOPPER_OK;
+    int64_t smin = dec_i64(ctx->h_rep.s_min_enc), emax = dec_i64(ctx->h_rep.s_max_enc);
+    if (ctx->h_rep.s_min_enc == ~0ull) { smin = 0; emax = 0; }
+    const int rbits = bits_for((uint64_t)(emax - smin));
+    const int lbits = bits_for((uint64_t)n_lists);
+    if (rbits + lbits > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "span sort key exceeds 64 bits");
+    auto &q = ctx->ss;
+    q.smin = smin; q.emax = emax; q.rbits = rbits; q.lbits = lbits;
+    q.k1 = CH_ALLOC(ctx, unsigned long long, S); q.k2 = CH_ALLOC(ctx, unsigned long long, S);
+    q.v1 = CH_ALLOC(ctx, uint32_t, S); q.v2 = CH_ALLOC(ctx, uint32_t, S);
+    q.lb = CH_ALLOC(ctx, unsigned long long, n_lists + 1);
+    q.lb2 = CH_ALLOC(ctx, unsigned long long, n_lists + 1);
+    CH_ALLOC_END(ctx);
+    q.big = reinterpret_cast<unsigned int *>(q.lb + n_lists);
+    // side stream: ordered after everything chopper_load_columns enqueued
+    CH_CUDA(ctx, cudaEventRecord(ctx->span_fork, ctx->st));
+    CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[2], ctx->span_fork, 0));
+    cudaStream_t main_st = ctx->st;
+    ctx->st = ctx->side[2];
+    ctx->hold_scratch = true;                   // the sort's own scratch must outlive the launches
+    chopper_status st = [&]() -> chopper_status {
+        CH_CUDA(ctx, cudaMemsetAsync(ctx->d_list_flags, 0, sizeof(int32_t) * (n_lists + 1), ctx->st));
+        const unsigned g = (unsigned)ceil_div(S, NT);
+        bool alt;
+        k_span_key_fast<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, S, ctx->d_gpu_lg,
+                                               n_lg, smin, rbits, q.k1, q.v1);
+        CH_LAUNCHED(ctx);
+        CH_TRY(ch_radix_sort(ctx, q.k1, q.v1, q.k2, q.v2, S, 0, rbits + lbits, &alt));
+        q.order = alt ? q.v2 : q.v1;
+        q.okeys = alt ? q.k2 : q.k1;
+        CH_CUDA(ctx, cudaMemsetAsync(q.big, 0, 4, ctx->st));
+        k_fix_ties<<<g, NT, 0, ctx->st>>>(q.okeys, q.order, ctx->sp.end_ns, S, (unsigned long long)n_lists << rbits, q.big);
+        CH_LAUNCHED(ctx);
+        // gather speculatively (long equal-start runs are rare); one read-back for the flag and the list begins
+        CH_TRY(ch_fill_u64(ctx, q.lb2, n_lists + 1, ~0ull));
+        k_span_gather<<<g, NT, 0, ctx->st>>>(q.order, ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns,
+                                             ctx->sp.label, S, ctx->d_gpu_lg, n_lg, ctx->P_start, ctx->P_end,
+                                             ctx->P_orig, ctx->P_label, q.Plist, q.lb2);
+        CH_LAUNCHED(ctx);
+        return CHOPPER_OK;
+    }();
+    ctx->hold_scratch = false;
+    CH_CUDA(ctx, cudaEventRecord(ctx->span_join, ctx->st));
+    ctx->st = main_st;
+    CH_TRY(st);
+    ctx->span_pending = true;
+    return CHOPPER_OK;
+}
+
+chopper_status ch_build_spans(chopper_ctx *ctx) {
+    CH_ALLOC_BEGIN;
+    const int64_t S = ctx->S;
+    const int n_lg = ctx->n_lg;
+    const int n_lists = n_lg * 4;
+    if (!ctx->span_launched) CH_TRY(ch_span_sort_launch(ctx));     // (not launched by the load)
+    if (ctx->span_pending) {
+        CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->span_join, 0));
+        ctx->span_pending = false;
+    }
+    int32_t *Plist = ctx->ss.Plist;
     ctx->list_beg.assign(n_lists + 2, 0);
     ctx->S_loc = 0;
     if (n_lg == 0) {                 // a rank without events (its traced GPUs are empty): no span lists
         CH_CUDA(ctx, cudaMemsetAsync(ctx->d_list_beg, 0, sizeof(int64_t) * (n_lists + 2), ctx->st));
+        CH_CUDA(ctx, cudaMemsetAsync(ctx->d_list_flags, 0, sizeof(int32_t) * (n_lists + 1), ctx->st));
         ctx->et_ok = false;
         return CHOPPER_OK;
     }
+    if (S == 0) CH_CUDA(ctx, cudaMemsetAsync(ctx->d_list_flags, 0, sizeof(int32_t) * (n_lists + 1), ctx->st));
     if (S > 0) {
-        int64_t smin = dec_i64(ctx->h_rep.s_min_enc), emax = dec_i64(ctx->h_rep.s_max_enc);
-        if (ctx->h_rep.s_min_enc == ~0ull) { smin = 0; emax = 0; }
-        int rbits = bits_for((uint64_t)(emax - smin));
-        int lbits = bits_for((uint64_t)n_lists);
-        if (rbits + lbits > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "span sort key exceeds 64 bits");
-        size_t mark = ctx->used;
-        unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, S), *k2 = CH_ALLOC(ctx, unsigned long long, S);
-        uint32_t *v1 = CH_ALLOC(ctx, uint32_t, S), *v2 = CH_ALLOC(ctx, uint32_t, S);
-        unsigned long long *lb = CH_ALLOC(ctx, unsigned long long, n_lists + 1);
-        CH_ALLOC_END(ctx);
-        unsigned g = (unsigned)ceil_div(S, NT);
-        unsigned int *big = reinterpret_cast<unsigned int *>(lb + n_lists);   // reuses the EXCL slot until gather
+        auto &q = ctx->ss;
+        const int64_t emax = q.emax, smin = q.smin;
+        const int rbits = q.rbits, lbits = q.lbits;
+        const unsigned g = (unsigned)ceil_div(S, NT);
+        unsigned long long *k1 = q.k1, *k2 = q.k2, *lb2 = q.lb2;
+        uint32_t *v1 = q.v1, *v2 = q.v2, *order = q.order;
         bool alt;
-        // one stable (list, start) sort with input order as tie-break, then equal-start runs are reordered
-        // by (end desc, index desc) in place
-        k_span_key_fast<<<g, NT, 0, ctx->st>>>(ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns, S, ctx->d_gpu_lg,
-                                               n_lg, smin, rbits, k1, v1);
-        CH_LAUNCHED(ctx);
-        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, S, 0, rbits + lbits, &alt));
-        uint32_t *order = alt ? v2 : v1;
-        unsigned long long *okeys = alt ? k2 : k1;
-        CH_CUDA(ctx, cudaMemsetAsync(big, 0, 4, ctx->st));
-        k_fix_ties<<<g, NT, 0, ctx->st>>>(okeys, order, ctx->sp.end_ns, S, (unsigned long long)n_lists << rbits, big);
-        CH_LAUNCHED(ctx);
-        // gather speculatively (long equal-start runs are rare); one read-back for the flag and the list begins
-        unsigned long long *lb2 = CH_ALLOC(ctx, unsigned long long, n_lists + 1);
-        CH_ALLOC_END(ctx);
         auto gather = [&](const uint32_t *ord) -> chopper_status {
             CH_TRY(ch_fill_u64(ctx, lb2, n_lists + 1, ~0ull));
             k_span_gather<<<g, NT, 0, ctx->st>>>(ord, ctx->sp.gpu_level, ctx->sp.start_ns, ctx->sp.end_ns,
@@ -499,10 +547,9 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
             CH_LAUNCHED(ctx);
             return CHOPPER_OK;
         };
-        CH_TRY(gather(order));
         std::vector<unsigned long long> hb(n_lists + 1);
         unsigned int hbig = 0;
-        CH_CUDA(ctx, ch_d2h(ctx, &hbig, big, 4));
+        CH_CUDA(ctx, ch_d2h(ctx, &hbig, q.big, 4));
         CH_CUDA(ctx, ch_d2h(ctx, hb.data(), lb2, 8 * (n_lists + 1)));
         CH_CUDA(ctx, ch_sync(ctx));
         if (hbig) {
@@ -522,7 +569,6 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
             CH_CUDA(ctx, ch_d2h(ctx, hb.data(), lb2, 8 * (n_lists + 1)));
             CH_CUDA(ctx, ch_sync(ctx));
         }
-        ctx->used = mark;
         ctx->list_beg[n_lists + 1] = S;
         for (int l = n_lists; l >= 0; l--) ctx->list_beg[l] = hb[l] == ~0ull ? ctx->list_beg[l + 1] : (int64_t)hb[l];
         ctx->S_loc = ctx->list_beg[n_lists];
