@@ -150,6 +150,8 @@ struct chopper_ctx {
     int64_t *d_pred_end = nullptr;   // [N] end of chain predecessor or NONE
     bool full_sort = false;
     bool lean = false;               // one compute stream per gpu, start-monotone in dispatch order (lean a2)
+    bool counters_early = false;     // the counter pass was launched beside the event pass (ch_event_pass)
+    bool t_run_rank = false;         // d_t_run holds in-tile head ranks (k_tile_heads), not global run ids
     bool tables_radix = false;       // sticky: a trace of this ctx needed the radix instance sort (tables.cu)
     unsigned int *d_prefix_bad = nullptr;   // deferred instance-order check, read with the tables' row counts
 
@@ -511,6 +513,7 @@ chopper_status ch_load(chopper_ctx *ctx);
 // spans.cu
 chopper_status ch_build_spans(chopper_ctx *ctx);
 chopper_status ch_span_sort_launch(chopper_ctx *ctx);
+chopper_status ch_counters_launch(chopper_ctx *ctx, double *cnt, unsigned int *colbad, int t_rank);
 chopper_status ch_attr_pass(chopper_ctx *ctx, int32_t *span_idx);
 // events.cu
 chopper_status ch_overlap_prep(chopper_ctx *ctx);

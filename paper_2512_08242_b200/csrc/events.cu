@@ -1394,6 +1394,7 @@ __global__ void __launch_bounds__(W_NT) k_tile_heads(EvParams P, int64_t *__rest
     unsigned long long prevk = CH_INVALID_KEY, first = CH_INVALID_KEY;
     int64_t prevj = -1;
     int nh = 0;
+    unsigned hm = 0;                      // head mask of the thread's 8 events (the event pass's rule)
 #pragma unroll
     for (int k = 0; k < EV_IPT; k++) {
         if (k < nv) {
@@ -1402,7 +1403,7 @@ __global__ void __launch_bounds__(W_NT) k_tile_heads(EvParams P, int64_t *__rest
             wcur_seek(wk, ck, tl[k]);
             if (ck.j != prevj) {
                 const unsigned long long kk = key_at(wk, P, ck.j);
-                if (k > 0 && kk != prevk) nh++;
+                if (k > 0 && kk != prevk) { nh++; hm |= 1u << k; }
                 prevk = kk;
                 prevj = ck.j;
             }
@@ -1417,15 +1418,27 @@ __global__ void __launch_bounds__(W_NT) k_tile_heads(EvParams P, int64_t *__rest
     if (lane == 31) s_last[warp] = prevk;
     __syncthreads();
     if (lane == 0) pl = warp > 0 ? s_last[warp - 1] : CH_INVALID_KEY;
-    if (nv > 0 && (tid == 0 || first != pl)) nh++;
+    if (nv > 0 && (tid == 0 || first != pl)) { nh++; hm |= 1u; }
+    // in-tile exclusive head count before this thread (warp scan + warp totals)
+    int inc = nh;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nh += __shfl_xor_sync(CH_FULL, nh, o);
-    if (lane == 0) s_cnt[warp] = nh;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(CH_FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_cnt[warp] = inc;
     __syncthreads();
-    if (tid == 0) {
-        int64_t t = 0;
-        for (int w = 0; w < W_WARPS; w++) t += s_cnt[w];
-        tile_cnt[tile] = t;
+    int wb = 0, t = 0;
+#pragma unroll
+    for (int w = 0; w < W_WARPS; w++) {
+        const int c = s_cnt[w];
+        if (w < warp) wb += c;
+        t += c;
+    }
+    if (tid == 0) tile_cnt[tile] = t;
+    if (P.t_run) {                        // the counter pass's view: head mask + in-tile rank (plus the tile base there)
+        P.t_run[tile * (int64_t)W_NT + tid] = wb + inc - nh;
+        P.t_hm[tile * (int64_t)W_NT + tid] = (uint8_t)hm;
     }
 }
 
@@ -2252,6 +2265,11 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     const int64_t nthr = ceil_div(N, W_TILE) * W_NT;
     ctx->d_t_run = ctx->C > 0 ? CH_ALLOC(ctx, int32_t, nthr) : nullptr;
     ctx->d_t_hm = ctx->C > 0 ? CH_ALLOC(ctx, uint8_t, nthr) : nullptr;
+    // the counter pass's sums ([cap][C]) and non-finite flags: it can start once the head pre-count is scanned
+    double *sub_cnt = ctx->C > 0 ? CH_ALLOC(ctx, double, (int64_t)ctx->C * cap) : nullptr;
+    unsigned int *colbad = ctx->C > 0 ? CH_ALLOC(ctx, unsigned int, (int64_t)ctx->n_lg * ctx->C) : nullptr;
+    ctx->counters_early = false;
+    ctx->t_run_rank = false;
     ctx->d_tile_state = CH_ALLOC(ctx, unsigned long long, ceil_div(N, W_TILE));   // >= tiles of either pass
     ctx->d_tile_ticket = CH_ALLOC(ctx, unsigned int, 1);
     CH_ALLOC_END(ctx);
@@ -2335,10 +2353,18 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         CH_LAUNCHED(ctx);
         P.twin = twin;
         P.twinl = twinl;
-        k_tile_heads<<<(unsigned)ntile, W_NT, 0, ctx->st>>>(P, tcnt);
+        k_tile_heads<<<(unsigned)ntile, W_NT, 0, ctx->st>>>(P, tcnt);      // (+ head masks / ranks for counters)
         CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, tcnt, tbase, ntile, tbase + ntile));
         P.tile_base = tbase;
+        if (sub_cnt) {                        // the counter pass beside the event pass (side[0])
+            ctx->sub.cnt = sub_cnt;
+            CH_TRY(ch_counters_launch(ctx, sub_cnt, colbad, 1));
+            ctx->counters_early = true;
+        }
+        P.t_run = nullptr;                    // (already written by the pre-count)
+        P.t_hm = nullptr;
+        ctx->t_run_rank = true;
         const bool out = ovl || prep || call || phi || psi;
         ch_tick(ctx, 8, 0);
         if (out) k_events_l<true><<<(unsigned)ntile, W_NT, dsm, ctx->st>>>(P, tm[0], tm[1], tm[2], tm[3]);
@@ -2374,6 +2400,14 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, tcnt, tbase, ntile, tbase + ntile));
         P.tile_base = tbase;
+        if (sub_cnt) {
+            ctx->sub.cnt = sub_cnt;
+            CH_TRY(ch_counters_launch(ctx, sub_cnt, colbad, 1));
+            ctx->counters_early = true;
+        }
+        P.t_run = nullptr;
+        P.t_hm = nullptr;
+        ctx->t_run_rank = true;
         ch_tick(ctx, 8, 0);
         k_events_w<<<(unsigned)ntile, W_NT, dsm, ctx->st>>>(P, vec_ok);
         CH_LAUNCHED(ctx);

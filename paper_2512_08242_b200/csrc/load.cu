@@ -544,8 +544,6 @@ static chopper_status finish_load(chopper_ctx *ctx) {
     fill_public_report(ctx);
     if (ctx->h_rep.val_count[CV_STREAM_OVERLAP]) ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
     ctx->loaded_ok = true;
-    // the spans are validated: their push-order sort starts now, beside chopper_align (spans.cu)
-    CH_TRY(ch_span_sort_launch(ctx));
     ctx->mark_after_load = ctx->used;
     return CHOPPER_OK;
 }
@@ -706,6 +704,9 @@ chopper_status ch_load(chopper_ctx *ctx) {
     }
     CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_gpu_lg, ctx->gpu_lg_h, sizeof(int32_t) * CH_MAX_GPUS, cudaMemcpyHostToDevice,
                                  ctx->st));
+    // the spans are validated: their push-order sort starts now on a side stream, beside the rest of the load
+    // and chopper_align and their host synchronizations (spans.cu; chopper_attribute joins it)
+    CH_TRY(ch_span_sort_launch(ctx));
     // a2: partition by (lg, dense group); full radix sort only if a group is not start-monotone
     ctx->d_perm = CH_ALLOC(ctx, uint32_t, n);
     ctx->d_pred_end = nullptr;       // materialized by the general path only (k_chain); lean: derived (PredView)

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
                                                           const double *const *__restrict__ col, int C,
                                                           int64_t N, double *__restrict__ out, int64_t cap,
                                                           unsigned int *__restrict__ colbad, int vec_ok,
-                                                          int n_lg) {
+                                                          int n_lg, int t_rank) {
     extern __shared__ __align__(16) unsigned char ct_dsm[];
     CtSmem &S = *reinterpret_cast<CtSmem *>(ct_dsm);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(CT_NT, 3) k_counters_tiled(const uint32_t *__r
     // run id before its first event + head mask, and its non-MEMOP rank before its first event, give every run id
     // and counter position here (5 + 4 B per 8 events instead of 8 B per event)
     const int64_t th = (int64_t)blockIdx.x * CT_NT + tid;
-    const int32_t rrun = nv > 0 ? t_run[th] : 0;
+    // t_run: the run id before the thread's first event, or (t_rank, from k_tile_heads) the in-tile head rank
+    const int32_t rrun = nv > 0 ? (t_rank ? (int32_t)(tile_sub[blockIdx.x] - 1) + t_run[th] : t_run[th]) : 0;
     const unsigned hmask = nv > 0 ? (unsigned)t_hm[th] : 0u;
     const int32_t rnm = nv > 0 ? t_nm[th] : 0;
     uint32_t mt[CT_IPT];
@@ -1258,6 +1259,19 @@ __global__ void k_rates(const int64_t *__restrict__ n_dev, const int64_t *__rest
 }
 }  // namespace
 
+// Dynamic shared memory above 48 KB needs an opt-in per kernel.  The sizes vary with the trace (and several host
+// threads may drive contexts at once), so each such kernel is opted in once to the device maximum (minus its
+// static shared memory): every caller sets the same value, and any size the launch asks for is allowed.
+static cudaError_t allow_max_smem(const void *fn) {
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, fn);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    return e;
+}
+
 static chopper_status alloc_table(chopper_ctx *ctx, RowTable &t, int64_t cap, int C, bool identity) {
     CH_ALLOC_BEGIN;
     t.cap = cap;
@@ -1321,18 +1335,12 @@ static chopper_status sum_rows(chopper_ctx *ctx, const TabView &ch, const uint32
     if (mode == 1 && C > 32) mode = 2;
     if (mode == 0 && !perm && ch.rs == 1 && C <= 8 && fanout >= 2) {
         const size_t shc = (size_t)(RF_NFIELDS + C) * (RC_CH + PB) * 8;
-        static size_t attr_c = 0;
-        if (shc > attr_c) {                   // (static + dynamic must fit the limit: always set it)
-            CH_CUDA(ctx, cudaFuncSetAttribute(k_sum_rows_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shc));
-            attr_c = shc;
-        }
+        static bool opt_c = false;
+        if (!opt_c) { CH_CUDA(ctx, allow_max_smem((const void *)k_sum_rows_cols)); opt_c = true; }
         k_sum_rows_cols<<<grid_for(ng_upper / fanout, PB), RC_NT, shc, ctx->st>>>(ch, starts, ng_dev, shift, C, pa, PB);
     } else if (mode == 0) {
-        static size_t attr = 0;
-        if (shb > 48 * 1024 && shb > attr) {
-            CH_CUDA(ctx, cudaFuncSetAttribute(k_sum_rows_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
-            attr = shb;
-        }
+        static bool opt = false;
+        if (!opt) { CH_CUDA(ctx, allow_max_smem((const void *)k_sum_rows_chunked)); opt = true; }
         if (C > 8) CH_CUDA(ctx, cudaMemsetAsync(pa.cnt, 0, 8 * (size_t)C * pa.ccap, ctx->st));
         k_sum_rows_chunked<<<grid_for(ng_upper / std::max(fanout, 1), PB), RC_NT, shb, ctx->st>>>(ch, perm, starts, ng_dev,
                                                                                                  shift, C, pa, PB);
@@ -1418,6 +1426,27 @@ struct DbgTicks {
 };
 DbgTicks g_dbg;
 }
+// The counter pass (R8 finiteness of every value it reads included) on side[0], joined (join_ev[0]) before the
+// sub-run -> instance sum.  t_rank = 1: the per-thread run values are in-tile head ranks from k_tile_heads, so
+// the pass can start beside the event pass (ch_event_pass); 0: global run ids written by the event pass.
+chopper_status ch_counters_launch(chopper_ctx *ctx, double *cnt, unsigned int *colbad, int t_rank) {
+    const int C = ctx->C, n_lg = ctx->n_lg;
+    ctx->d_colbad = colbad;                   // [n_lg][C] non-finite flags, read with the tables' row counts
+    CH_CUDA(ctx, cudaMemsetAsync(ctx->d_colbad, 0, 4 * (size_t)n_lg * C, ctx->st));
+    const int vec_ok = (((uintptr_t)ctx->ev.meta) & 15u) == 0;
+    CH_CUDA(ctx, cudaFuncSetAttribute(k_counters_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CtSmem)));
+    CH_CUDA(ctx, cudaEventRecord(ctx->fork_ev, ctx->st));
+    CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[0], ctx->fork_ev, 0));
+    ch_tick_on(ctx, 9, 0, ctx->side[0]);
+    k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->side[0]>>>(
+        ctx->ev.meta, ctx->d_t_run, ctx->d_t_hm, ctx->d_t_nm, ctx->d_nm_base, ctx->d_tile_sub, ctx->d_gpu_lg,
+        ctx->d_col, C, ctx->N, cnt, 1, ctx->d_colbad, vec_ok, n_lg, t_rank);
+    CH_LAUNCHED(ctx);
+    ch_tick_on(ctx, 9, 1, ctx->side[0]);
+    CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[0], ctx->side[0]));
+    return CHOPPER_OK;
+}
+
 static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
     const int C = ctx->C;
     const int64_t R = ctx->R;
@@ -1427,35 +1456,25 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
     g_dbg.mark(ctx->st, "begin");
     CH_ALLOC_BEGIN;
     int32_t *lg_gpu_d = CH_ALLOC(ctx, int32_t, ctx->n_lg + 1);
-    ctx->sub.cnt = CH_ALLOC(ctx, double, (int64_t)(C > 0 ? C : 1) * std::max<int64_t>(R, 1));
     CH_ALLOC_END(ctx);
     ctx->h_lg_gpu.assign(ctx->lg_gpu, ctx->lg_gpu + ctx->n_lg);
     if (ctx->n_lg)
         CH_CUDA(ctx, cudaMemcpyAsync(lg_gpu_d, ctx->h_lg_gpu.data(), 4 * ctx->n_lg, cudaMemcpyHostToDevice, ctx->st));
     ctx->sub.cap = std::max<int64_t>(R, 1);
-    TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, 1, 1, 16, std::max(C, 1)};   // AoS sub-run rows and counters
-    bool counters_forked = false;
-    if (C > 0 && R > 0) {
-        const int n_lg = ctx->n_lg;
-        ctx->d_colbad = CH_ALLOC(ctx, unsigned int, (int64_t)n_lg * C);
+    // the counter pass may already run beside the event pass (ch_counters_launch from ch_event_pass)
+    bool counters_forked = ctx->counters_early;
+    if (!counters_forked) {
+        CH_ALLOC_BEGIN;
+        ctx->sub.cnt = CH_ALLOC(ctx, double, (int64_t)(C > 0 ? C : 1) * std::max<int64_t>(R, 1));
+        unsigned int *colbad = CH_ALLOC(ctx, unsigned int, (int64_t)ctx->n_lg * std::max(C, 1));
         CH_ALLOC_END(ctx);
-        CH_CUDA(ctx, cudaMemsetAsync(ctx->d_colbad, 0, 4 * (size_t)n_lg * C, ctx->st));
-        const int vec_ok = (((uintptr_t)ctx->ev.meta) & 15u) == 0;
-        CH_CUDA(ctx, cudaFuncSetAttribute(k_counters_tiled, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)sizeof(CtSmem)));
-        // the counter pass runs on a side stream, concurrently with the instance ordering below (which never
-        // touches the counter sums); it is joined before the sub-run -> instance sum
-        CH_CUDA(ctx, cudaEventRecord(ctx->fork_ev, ctx->st));
-        CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[0], ctx->fork_ev, 0));
-        ch_tick_on(ctx, 9, 0, ctx->side[0]);
-        k_counters_tiled<<<(unsigned)ceil_div(ctx->N, CT_TILE), CT_NT, sizeof(CtSmem), ctx->side[0]>>>(
-            ctx->ev.meta, ctx->d_t_run, ctx->d_t_hm, ctx->d_t_nm, ctx->d_nm_base, ctx->d_tile_sub, ctx->d_gpu_lg,
-            ctx->d_col, C, ctx->N, subv.cnt, subv.ccap, ctx->d_colbad, vec_ok, n_lg);
-        CH_LAUNCHED(ctx);
-        ch_tick_on(ctx, 9, 1, ctx->side[0]);
-        CH_CUDA(ctx, cudaEventRecord(ctx->join_ev[0], ctx->side[0]));
-        counters_forked = true;
+        if (C > 0 && R > 0) {
+            CH_TRY(ch_counters_launch(ctx, ctx->sub.cnt, colbad, ctx->t_run_rank ? 1 : 0));
+            counters_forked = true;
+        }
     }
+    ctx->counters_early = false;              // (a redo of the tables forks its own pass)
+    TabView subv{ctx->sub.key, ctx->sub.f, ctx->sub.cnt, 1, 1, 16, std::max(C, 1)};   // AoS sub-run rows and counters
     g_dbg.mark(ctx->st, "fork");
     // instances: sort of sub-runs by key, then groups of equal keys
     unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, R + 1), *k2 = CH_ALLOC(ctx, unsigned long long, R + 1);
@@ -1561,11 +1580,8 @@ static chopper_status tables_body(chopper_ctx *ctx, unsigned int **ovf_out) {
             CH_CUDA(ctx, cudaMemsetAsync(dvalid, 0, 8 * (size_t)cells, ctx->st));
             CH_CUDA(ctx, cudaMemsetAsync(ovf, 0, 4, ctx->st));
             size_t shb = (size_t)(RF_NFIELDS + C) * (PT_CH + nL) * 8 + 4 * (2 * PT_CH + 11 * (size_t)nL);
-            static size_t attr_shb = 0;
-            if (shb > 48 * 1024 && shb > attr_shb) {
-                CH_CUDA(ctx, cudaFuncSetAttribute(k_points_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shb));
-                attr_shb = shb;
-            }
+            static bool opt_p = false;
+            if (!opt_p) { CH_CUDA(ctx, allow_max_smem((const void *)k_points_iter)); opt_p = true; }
             k_points_iter<<<grid_for(std::min<int64_t>(n, (int64_t)n_lg * R0), 1), 256, shb, ctx->st>>>(
                 view(ctx->inst), its, n_it, L, ctx->d_list_beg, ctx->P_label, nL, n_lg, R0, C, df, dc, dvalid, ovf);
             CH_LAUNCHED(ctx);
