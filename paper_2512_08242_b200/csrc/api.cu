@@ -205,6 +205,8 @@ static chopper_status load_columns(chopper_ctx *ctx, const chopper_events *ev, c
     ctx->C = 0;
     ctx->d_col = nullptr;
     ctx->d_nm_rank = nullptr;
+    ctx->d_bd = nullptr;            // (reduce_ranks reuses this step's local breakdown with one rank)
+    ctx->n_bd = 0;
     ctx->present.clear();
     ctx->err.clear();
     memset(&ctx->rep, 0, sizeof(ctx->rep));

@@ -1034,7 +1034,7 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
         ctx->d_exchanged = true;
         CH_TRY(ch_nccl_allgather(ctx, ctx->d_dense, all, sizeof(int64_t) * (size_t)slots * Ly.W));
     } else {
-        CH_CUDA(ctx, cudaMemcpyAsync(all, ctx->d_dense, 8 * (size_t)slots * Ly.W, cudaMemcpyDeviceToDevice, ctx->st));
+        all = ctx->d_dense;                   // one rank: the gathered block is the local one (read only from here)
     }
     int32_t *ord;
     CH_TRY(slot_order(ctx, all, nslots, Ly.W, &ord, poison));
@@ -1070,7 +1070,14 @@ chopper_status ch_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     CH_LAUNCHED(ctx);
     double *bd;
     int64_t nbd;
-    CH_TRY(run_breakdown(ctx, all, nslots, ord, &bd, &nbd));
+    if (ctx->nranks == 1 && ctx->d_bd) {
+        // one rank: the gathered block is the local one, so the global breakdown is the local one (same kernels on
+        // the same block, computed in chopper_breakdown) -- reused, not recomputed
+        bd = ctx->d_bd;
+        nbd = ctx->n_bd;
+    } else {
+        CH_TRY(run_breakdown(ctx, all, nslots, ord, &bd, &nbd));
+    }
     // report statistics per op label (O14)
     const int nL = ctx->cfg.n_labels;
     double *rep = nullptr;

@@ -463,9 +463,12 @@ __global__ void k_ss_check(const unsigned long long *__restrict__ key, const uin
     if (t == 0 || t >= M) return;
     if (key[t] == key[t - 1] && ks[val[t]] < ks[val[t - 1]]) atomicOr(fail, 2u);
 }
+// cl[cl_off[a] .. cl_off[a + 1]): the non-empty stream cells of segment a (built on the host at the fast-path
+// check's read-back), so an element searches only the streams present, not all SS_STREAMS cells
 __global__ void k_ss_rank(const unsigned long long *__restrict__ key, const uint32_t *__restrict__ val, int64_t M,
                           const int64_t *__restrict__ ks, const unsigned int *__restrict__ cnt,
                           const int64_t *__restrict__ cstart, const int64_t *__restrict__ lo,
+                          const int32_t *__restrict__ cl, const int32_t *__restrict__ cl_off,
                           uint32_t *__restrict__ perm) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= M) return;
@@ -474,9 +477,10 @@ __global__ void k_ss_rank(const unsigned long long *__restrict__ key, const uint
     const uint32_t x = val[t];
     const int64_t kx = ks[x];
     int64_t r = t - cstart[cell];
-    for (int c2 = a * SS_STREAMS; c2 < (a + 1) * SS_STREAMS; c2++) {
+    for (int q = cl_off[a]; q < cl_off[a + 1]; q++) {
+        const int c2 = cl[q];
         const unsigned int n2 = cnt[c2];
-        if (c2 == cell || n2 == 0) continue;
+        if (c2 == cell) continue;
         int64_t l = cstart[c2], h = l + n2;           // count of (ks, idx) < (kx, x) in list c2
         const int64_t l0 = l;
         while (l < h) {
@@ -591,11 +595,24 @@ static chopper_status sort_segments(chopper_ctx *ctx, std::vector<int64_t> seg_l
         CH_LAUNCHED(ctx);
         CH_TRY(ch_scan_excl_i64(ctx, c64, cst, cells, nullptr));
         unsigned int hfail = 0;
+        std::vector<unsigned int> hcnt((size_t)cells);
         CH_CUDA(ctx, ch_d2h(ctx, &hfail, fail, 4));
+        CH_CUDA(ctx, ch_d2h(ctx, hcnt.data(), cnt, 4 * (size_t)cells));
         CH_CUDA(ctx, ch_sync(ctx));
         if (!hfail) {
+            std::vector<int32_t> hcl, hoff(nseg + 1, 0);
+            for (int a = 0; a < nseg; a++) {
+                hoff[a] = (int32_t)hcl.size();
+                for (int c = 0; c < SS_STREAMS; c++)
+                    if (hcnt[(size_t)a * SS_STREAMS + c]) hcl.push_back(a * SS_STREAMS + c);
+            }
+            hoff[nseg] = (int32_t)hcl.size();
+            int32_t *dcl = CH_ALLOC(ctx, int32_t, (int64_t)hcl.size() + 1), *doff = CH_ALLOC(ctx, int32_t, nseg + 1);
+            CH_ALLOC_END(ctx);
+            CH_CUDA(ctx, cudaMemcpyAsync(dcl, hcl.data(), 4 * hcl.size(), cudaMemcpyHostToDevice, ctx->st));
+            CH_CUDA(ctx, cudaMemcpyAsync(doff, hoff.data(), 4 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
             k_ss_rank<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, cnt, cst, dlo,
-                                                                        ctx->d_perm);
+                                                                        dcl, doff, ctx->d_perm);
             CH_LAUNCHED(ctx);
             merged = true;
         }

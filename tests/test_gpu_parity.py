@@ -648,3 +648,58 @@ def test_scratch_plan_bounds_high_water(cid):
     used = ch.load_library().chopper_scratch_used(pipe.ctx)
     assert 0 < used <= plan["total"]
     pipe.close()
+
+
+def test_ctx_reuse_across_steps_with_side_streams():
+    """One context over several steps (DESIGN §5 concurrency): the span sort is forked by chopper_load_columns
+    onto a side stream and joined by chopper_attribute, chopper_overlap's preparation runs beside the span
+    tables, the counter pass beside the event pass.  A load whose step is abandoned before chopper_attribute
+    (its sort never joined) and a step with a fatal validation error must leave the next step exact; so must a
+    change of trace shape."""
+    import paper_2512_08242_b200 as ch
+    from paper_2512_08242_b200 import chopper_events, chopper_load_columns, chopper_samples, chopper_spans
+    c1 = tracegen.config(1)
+    c1.n_gpus = 3
+    ba = tracegen.generate(c1)                      # 8 counters
+    cfg = tracegen.config(3)
+    cfg.n_iters, cfg.n_layers, cfg.n_gpus, cfg.opt_kernels, cfg.warmup = 3, 4, 3, 600, 1
+    bb = tracegen.generate(cfg)                     # 20 counters, more spans and iterations
+    G = 3
+    L = max(len(ba.labels), len(bb.labels))
+    mi = max(8, ba.cfg.n_iters + 2, bb.cfg.n_iters + 2)
+    from parity import _max_coll
+    kc = int(max(16, 4 * max(_max_coll(ba), _max_coll(bb))))
+    pipe = ch.Pipeline(G, L, mi, kc, device=0)
+
+    def step(b, bare_load=False):
+        pipe.upload(b, b.n_counters)
+        p = oracle.default_params(b)
+        if bare_load:      # only chopper_load_columns: the side-stream span sort is left unjoined
+            d = pipe.d
+            ev = chopper_events(n=pipe.N, dispatch_ns=d["t_l"].data_ptr(), start_ns=d["t_ks"].data_ptr(),
+                                end_ns=d["t_ke"].data_ptr(), meta=d["meta"].data_ptr(), name_id=d["name_id"].data_ptr())
+            sp = chopper_spans(n=pipe.S, gpu_level=d["span_gl"].data_ptr(), start_ns=d["span_start"].data_ptr(),
+                               end_ns=d["span_end"].data_ptr(), label=d["span_label"].data_ptr())
+            smp = chopper_samples(n=pipe.M, gpu=d["smp_gpu"].data_ptr(), ts_ns=d["smp_ts"].data_ptr(),
+                                  freq_mhz=d["smp_freq"].data_ptr(), power_mw=d["smp_power"].data_ptr()) \
+                if pipe.M > 0 else None
+            assert chopper_load_columns(pipe.ctx, ev, sp, smp) == 0
+            return None
+        res = pipe.run(p, full=True, check=False)
+        got = pipe.to_numpy(res, n_ratios=len(p["ratio_num"]))
+        ref = oracle.run(b, p, max_iters=mi)
+        assert_parity(ref, got)
+        return got
+
+    step(ba)
+    step(bb, bare_load=True)           # abandoned after the load
+    step(ba)
+    ke = bb.t_ke.copy()
+    ke[7] = bb.t_ks[7] - 1             # fatal: t_ks > t_ke
+    bad = tracegen.dataclasses.replace(bb, t_ke=ke)
+    pipe.upload(bad, bad.n_counters)
+    res = pipe.run(oracle.default_params(bad), full=False, check=False)
+    assert res["load_status"] != 0
+    step(bb)
+    step(ba)
+    pipe.close()
