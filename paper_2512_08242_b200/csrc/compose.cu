@@ -88,24 +88,46 @@ __global__ void k_dense_points(int64_t *blk, Layout Ly, int64_t n, const int32_t
 
 // O16 cells: instance durations by (phase label, op type) and launch overhead by phase label, summed into
 // the gpu's iteration-rank row of the exchange block (integer atomics: exact in any order)
+// instances are in key order, so long runs of them share a (gpu, iteration, phase) row: each lane walks K of a
+// warp's 32 K instances (stride 32, coalesced) and accumulates per target cell, issuing the atomics only when the
+// row changes (integer sums: exact in any order).  K grows with the instance count once the grid is full
+// (a small table keeps K = 1: every lane one instance, all in parallel)
+constexpr int E2E_KMAX = 16;
 __global__ void k_dense_e2e(int64_t *blk, Layout Ly, const int64_t *__restrict__ n_dev, const int32_t *__restrict__ gpu,
                             const int32_t *__restrict__ rank, const int32_t *__restrict__ ph,
                             const int32_t *__restrict__ label, const int64_t *__restrict__ f, int64_t cap,
                             const int32_t *__restrict__ gpu_lg, const int32_t *__restrict__ span_label,
-                            const int32_t *__restrict__ op_type) {
+                            const int32_t *__restrict__ op_type, int E2E_K) {
     const int64_t n = *n_dev;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = rank[j];
-        if (r < 0 || r >= Ly.MI || ph[j] < 0) continue;
-        const int P = span_label[ph[j]];
-        if (P < 0 || P >= E2E_P) continue;
-        const int lab = label[j];
-        const int T = lab >= 0 && op_type[lab] == 1 ? 1 : lab >= 0 && op_type[lab] == 2 ? 2 : 0;
-        int64_t *b = blk + (int64_t)gpu_lg[gpu[j]] * Ly.W + Ly.e2e_off() + r * E2E_W + P * 4;
-        const int64_t busy = f[(int64_t)RF_BUSY * cap + j];
-        const int64_t launch = f[(int64_t)RF_PREP * cap + j] + f[(int64_t)RF_CALL * cap + j];
-        if (busy) atomicAdd(reinterpret_cast<unsigned long long *>(b + T), (unsigned long long)busy);
-        if (launch) atomicAdd(reinterpret_cast<unsigned long long *>(b + 3), (unsigned long long)launch);
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w0 = wid * 32 * E2E_K; w0 < n; w0 += nw * 32 * E2E_K) {
+        int64_t *cur = nullptr;
+        unsigned long long acc[4] = {0, 0, 0, 0};
+        for (int k = 0; k < E2E_K; k++) {
+            const int64_t j = w0 + (int64_t)k * 32 + lane;
+            if (j >= n) break;
+            const int64_t r = rank[j];
+            if (r < 0 || r >= Ly.MI || ph[j] < 0) continue;
+            const int P = span_label[ph[j]];
+            if (P < 0 || P >= E2E_P) continue;
+            const int lab = label[j];
+            const int T = lab >= 0 && op_type[lab] == 1 ? 1 : lab >= 0 && op_type[lab] == 2 ? 2 : 0;
+            int64_t *b = blk + (int64_t)gpu_lg[gpu[j]] * Ly.W + Ly.e2e_off() + r * E2E_W + P * 4;
+            if (b != cur) {
+                if (cur)
+                    for (int q = 0; q < 4; q++)
+                        if (acc[q]) atomicAdd(reinterpret_cast<unsigned long long *>(cur + q), acc[q]);
+                cur = b;
+                acc[0] = acc[1] = acc[2] = acc[3] = 0;
+            }
+            acc[T] += (unsigned long long)f[(int64_t)RF_BUSY * cap + j];
+            acc[3] += (unsigned long long)(f[(int64_t)RF_PREP * cap + j] + f[(int64_t)RF_CALL * cap + j]);
+        }
+        if (cur)
+            for (int q = 0; q < 4; q++)
+                if (acc[q]) atomicAdd(reinterpret_cast<unsigned long long *>(cur + q), acc[q]);
     }
 }
 
@@ -910,9 +932,11 @@ static chopper_status densify(chopper_ctx *ctx, int64_t **blk_out, int *slots_ou
         CH_LAUNCHED(ctx);
     }
     if (ctx->inst.n > 0 && ctx->cfg.n_labels > 0) {
-        k_dense_e2e<<<(unsigned)std::min<int64_t>(ceil_div(ctx->inst.n, 256), 148 * 8), 256, 0, ctx->st>>>(
+        const int64_t slots = (int64_t)148 * 8 * 256;   // threads of a full grid
+        const int kk = (int)std::max<int64_t>(1, std::min<int64_t>(E2E_KMAX, ctx->inst.n / slots));
+        k_dense_e2e<<<(unsigned)std::min<int64_t>(ceil_div(ctx->inst.n, 256 * kk), 148 * 8), 256, 0, ctx->st>>>(
             blk, Ly, ctx->inst.n_dev, ctx->inst.gpu, ctx->inst.rank, ctx->inst.ph, ctx->inst.label, ctx->inst.f,
-            ctx->inst.cap, ctx->d_gpu_lg, ctx->sp.label, ctx->d_op_type);
+            ctx->inst.cap, ctx->d_gpu_lg, ctx->sp.label, ctx->d_op_type, kk);
         CH_LAUNCHED(ctx);
     }
     ctx->d_dense_ovf = ovf;     // checked at chopper_reduce_ranks' read-back (no round trip here)

@@ -134,22 +134,33 @@ __global__ void k_span_gather(const uint32_t *__restrict__ order, const uint32_t
 }
 
 // per-chunk sequential stack: previous greater-or-equal end inside the chunk
-__global__ void k_chunk_stack(const int64_t *__restrict__ Pe, const int32_t *__restrict__ Plist, int64_t S,
-                              int32_t *__restrict__ parent, int32_t *__restrict__ cstack, int32_t *__restrict__ csp,
-                              int64_t *__restrict__ cmax, const int64_t *__restrict__ list_beg) {
-    int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int64_t lo = c * CHUNK;
+// 64 chunks per block: the block's 64 x CHUNK span ends are staged by coalesced loads (chunk-major, pitch
+// CHUNK + 1: conflict-free when 64 threads walk their chunks in step); list changes come from list_beg
+// (one read of the chunk's first list), not from a per-span list column
+constexpr int CS_NT = 64, CS_PITCH = CHUNK + 1;
+__global__ void __launch_bounds__(CS_NT) k_chunk_stack(const int64_t *__restrict__ Pe, const int32_t *__restrict__ Plist,
+                                                       int64_t S, int32_t *__restrict__ parent,
+                                                       int32_t *__restrict__ cstack, int32_t *__restrict__ csp,
+                                                       int64_t *__restrict__ cmax, const int64_t *__restrict__ list_beg) {
+    __shared__ int64_t s_e[CS_NT * CS_PITCH];
+    const int tid = threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * CS_NT * CHUNK;
+    const int nb = (int)min((int64_t)CS_NT * CHUNK, S - base);
+    for (int i = tid; i < nb; i += CS_NT) s_e[(i / CHUNK) * CS_PITCH + (i % CHUNK)] = Pe[base + i];
+    __syncthreads();
+    const int64_t c = (int64_t)blockIdx.x * CS_NT + tid;
+    const int64_t lo = c * CHUNK;
     if (lo >= S) return;
-    int64_t hi = lo + CHUNK < S ? lo + CHUNK : S;
+    const int64_t hi = lo + CHUNK < S ? lo + CHUNK : S;
+    const int64_t *e_s = s_e + tid * CS_PITCH;
     int32_t si[CHUNK];                 // the stack (indices and ends) stays thread-local
     int64_t se[CHUNK];
     int sp = 0;
-    int cur = -1;
-    int64_t lbeg = 0;
+    int list = Plist[lo];
+    int64_t lbeg = list_beg[list], lnext = list_beg[list + 1];
     for (int64_t q = lo; q < hi; q++) {
-        int list = Plist[q];
-        if (list != cur) { sp = 0; cur = list; lbeg = list_beg[list]; }
-        int64_t e = Pe[q];
+        while (q >= lnext) { list++; lbeg = lnext; lnext = list_beg[list + 1]; sp = 0; }
+        const int64_t e = e_s[q - lo];
         while (sp > 0 && se[sp - 1] < e) sp--;
         if (sp > 0) parent[q] = si[sp - 1];
         else parent[q] = (lbeg >= lo) ? -1 : UNRES;
@@ -609,7 +620,7 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         int32_t *csp = CH_ALLOC(ctx, int32_t, nch);
         int64_t *sparse = CH_ALLOC(ctx, int64_t, (int64_t)levels * nch);
         CH_ALLOC_END(ctx);
-        k_chunk_stack<<<(unsigned)ceil_div(nch, 64), 64, 0, ctx->st>>>(ctx->P_end, Plist, SL, ctx->P_parent, cstack, csp,
+        k_chunk_stack<<<(unsigned)ceil_div(nch, CS_NT), CS_NT, 0, ctx->st>>>(ctx->P_end, Plist, SL, ctx->P_parent, cstack, csp,
                                                                       sparse, ctx->d_list_beg);
         CH_LAUNCHED(ctx);
         for (int k = 1; k < levels; k += 3) {
