@@ -770,6 +770,9 @@ __global__ void __launch_bounds__(256) k_sum_rows(TabView ch, const uint32_t *__
 // warp per parent (groups averaging several children: layer / phase / iteration / gpu roll-ups and
 // points): lanes take consecutive children (coalesced on field-major tables), every field and counter
 // in one pass, then a butterfly.
+// CMAX: the counter accumulators held per lane (0 without counters, 8, 32): sized to the trace, so a run without
+// counters keeps its registers (and occupancy) for the row fields
+template <int CMAX>
 __global__ void __launch_bounds__(256) k_sum_rows_warp(TabView ch, const uint32_t *__restrict__ perm,
                                                        const int64_t *__restrict__ starts,
                                                        const int64_t *__restrict__ ng_dev, int shift, int C,
@@ -781,8 +784,7 @@ __global__ void __launch_bounds__(256) k_sum_rows_warp(TabView ch, const uint32_
     const int64_t qlo = starts[q], qhi = starts[q + 1];
     RowAcc a;
     a.zero();
-    constexpr int CMAX = 32;
-    double acc[CMAX];
+    double acc[CMAX > 0 ? CMAX : 1];
 #pragma unroll
     for (int s = 0; s < CMAX; s++) acc[s] = 0.0;
     for (int64_t j = qlo + lane; j < qhi; j += 32) {
@@ -1345,7 +1347,9 @@ static chopper_status sum_rows(chopper_ctx *ctx, const TabView &ch, const uint32
         k_sum_rows_chunked<<<grid_for(ng_upper / std::max(fanout, 1), PB), RC_NT, shb, ctx->st>>>(ch, perm, starts, ng_dev,
                                                                                                  shift, C, pa, PB);
     } else if (mode == 1) {
-        k_sum_rows_warp<<<grid_for(ng_upper, NT / 32), NT, 0, ctx->st>>>(ch, perm, starts, ng_dev, shift, C, pa);
+        if (C == 0) k_sum_rows_warp<0><<<grid_for(ng_upper, NT / 32), NT, 0, ctx->st>>>(ch, perm, starts, ng_dev, shift, C, pa);
+        else if (C <= 8) k_sum_rows_warp<8><<<grid_for(ng_upper, NT / 32), NT, 0, ctx->st>>>(ch, perm, starts, ng_dev, shift, C, pa);
+        else k_sum_rows_warp<32><<<grid_for(ng_upper, NT / 32), NT, 0, ctx->st>>>(ch, perm, starts, ng_dev, shift, C, pa);
     } else {
         k_sum_rows<<<grid_for(ng_upper, NT), NT, 0, ctx->st>>>(ch, perm, starts, ng_dev, shift, C, pa);
     }
