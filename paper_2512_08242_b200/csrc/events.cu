@@ -1332,7 +1332,7 @@ __device__ __forceinline__ TlEnt tl_ent(const WinR &w, const EvParams &P, int64_
 // look-back chain that any slow tile would stall for all later ones.  Columns are read straight from global
 // memory (8 consecutive events per thread, 16 B loads); only the key-table window is staged.
 constexpr int HD_POOL = 28672;
-__global__ void __launch_bounds__(W_NT) k_tile_heads(EvParams P, int64_t *__restrict__ tile_cnt) {
+__global__ void __launch_bounds__(W_NT, 4) k_tile_heads(EvParams P, int64_t *__restrict__ tile_cnt) {
     __shared__ __align__(16) unsigned char pool[HD_POOL];
     __shared__ int64_t s_lo, s_next;
     __shared__ int s_n, s_lg;
