@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(RC_NT, 3) k_sum_rows_chunked(TabView ch, const
 // k_sum_rows_chunked, but the fold is split by (column, parent) so that all threads work -- thread task
 // (f, i) folds column f of parent i over its children in order (counter sums keep the sequential child
 // order); running values live in shared memory across chunks.  C <= 8.
-__global__ void __launch_bounds__(RC_NT, 3) k_sum_rows_cols(TabView ch, const int64_t *__restrict__ starts,
+__global__ void __launch_bounds__(RC_NT, 4) k_sum_rows_cols(TabView ch, const int64_t *__restrict__ starts,
                                                          const int64_t *__restrict__ ng_dev, int shift, int C,
                                                          TabView pa, int PB) {
     extern __shared__ int64_t rsm[];
