@@ -450,15 +450,19 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         int64_t ntile = ceil_div(N, MR_TILE);
         ctx->d_mg = CH_ALLOC(ctx, int64_t, n_lg + 1);
         CH_ALLOC_END(ctx);
-        int64_t *tc = CH_ALLOC(ctx, int64_t, 3 * ntile), *tex = CH_ALLOC(ctx, int64_t, 3 * ntile);
+        static_assert(MR_TILE == 2048, "the lean a2's tile counts use 2048-event tiles");
+        int64_t *tc = ctx->d_meta_tc ? ctx->d_meta_tc : CH_ALLOC(ctx, int64_t, 3 * ntile);
+        int64_t *tex = CH_ALLOC(ctx, int64_t, 3 * ntile);
         int64_t *base = CH_ALLOC(ctx, int64_t, 3 * (n_lg + 1));
         ctx->d_nm_base = base;           // component 0: non-MEMOP rank of each local gpu's first event
         int32_t *dlg = CH_ALLOC(ctx, int32_t, n_lg + 1);
         CH_ALLOC_END(ctx);
         std::vector<int32_t> hlg(ctx->lg_gpu, ctx->lg_gpu + n_lg);
         CH_CUDA(ctx, cudaMemcpyAsync(dlg, hlg.data(), 4 * n_lg, cudaMemcpyHostToDevice, ctx->st));
-        k_meta_tiles<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, N, tc, ntile);
-        CH_LAUNCHED(ctx);
+        if (!ctx->d_meta_tc) {            // (the general a2 path: a count pass of its own)
+            k_meta_tiles<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, N, tc, ntile);
+            CH_LAUNCHED(ctx);
+        }
         for (int c = 0; c < 3; c++) CH_TRY(ch_scan_excl_i64(ctx, tc + c * ntile, tex + c * ntile, ntile, nullptr));
         k_gpu_bases<<<1, 1024, 0, ctx->st>>>(
             ctx->ev.meta, N, tex, ntile, dgbeg, n_lg, base, dlg, ctx->d_xsend, ctx->xW);
@@ -654,6 +658,7 @@ chopper_status ch_offsets_launch(chopper_ctx *ctx) {
     CH_CUDA(ctx, ch_d2h(ctx, ctx->off_hs, mskew, 16));
     CH_CUDA(ctx, ch_d2h(ctx, &ctx->off_ovf, ctx->d_xovf, 4));
     CH_CUDA(ctx, ch_d2h_2d(ctx, ctx->off_hdr.data(), 16, all, 8 * (size_t)W, 16, nslots));
+    if (ctx->ss_pending) CH_CUDA(ctx, ch_d2h(ctx, &ctx->h_ss_fail, ctx->d_ss_fail, 4));   // (load's deferred check)
     ctx->off_pending = true;
     return CHOPPER_OK;
 }
@@ -663,6 +668,7 @@ chopper_status ch_offsets_finish(chopper_ctx *ctx) {
     if (!ctx->off_pending) CH_TRY(ch_offsets_launch(ctx));
     CH_CUDA(ctx, ch_sync(ctx));          // (already reached when ch_align synchronized)
     ctx->off_pending = false;
+    CH_TRY(ch_comm_sort_settle(ctx));
     const int nslots = (int)(ctx->off_hdr.size() / 2);
     // gpus absent from every rank keep flag 1 (no events)
     ctx->gpu_present.assign(G, 0);

@@ -150,6 +150,13 @@ struct chopper_ctx {
     int64_t *d_pred_end = nullptr;   // [N] end of chain predecessor or NONE
     bool full_sort = false;
     bool lean = false;               // one compute stream per gpu, start-monotone in dispatch order (lean a2)
+    // lean a2's communication sort, checked late (load.cu ch_comm_sort_settle)
+    bool ss_pending = false;
+    unsigned int *d_ss_fail = nullptr, h_ss_fail = 0;
+    uint32_t *d_ss_save = nullptr;
+    std::vector<int64_t> ss_seg_lo, ss_seg_pre;
+    int64_t ss_M = 0;
+    int64_t *d_meta_tc = nullptr;    // [3][N / 2048] non-MEMOP / AG / RS tile counts from the lean a2 (align reuses)
     bool counters_early = false;     // the counter pass was launched beside the event pass (ch_event_pass)
     bool t_run_rank = false;         // d_t_run holds in-tile head ranks (k_tile_heads), not global run ids
     bool tables_radix = false;       // sticky: a trace of this ctx needed the radix instance sort (tables.cu)
@@ -513,6 +520,7 @@ chopper_status ch_load(chopper_ctx *ctx);
 // spans.cu
 chopper_status ch_build_spans(chopper_ctx *ctx);
 chopper_status ch_span_sort_launch(chopper_ctx *ctx);
+chopper_status ch_comm_sort_settle(chopper_ctx *ctx);
 chopper_status ch_counters_launch(chopper_ctx *ctx, double *cnt, unsigned int *colbad, int t_rank);
 chopper_status ch_attr_pass(chopper_ctx *ctx, int32_t *span_idx);
 // events.cu

@@ -209,25 +209,55 @@ __global__ void __launch_bounds__(LN_NT) k_lean_tiles(const uint32_t *__restrict
                                                       const int32_t *__restrict__ gpu_lg, int NG, int other,
                                                       int64_t *__restrict__ t_comm, int64_t *__restrict__ t_comp,
                                                       int64_t *__restrict__ t_last, unsigned long long *__restrict__ bcnt,
-                                                      int nb) {
+                                                      int nb, int64_t *__restrict__ mtc, int64_t ntile) {
     extern __shared__ unsigned int ln_h[];               // [nb]
     __shared__ int64_t sm[33];
     for (int b = threadIdx.x; b < nb; b += LN_NT) ln_h[b] = 0;
     __syncthreads();
     const int64_t i0 = (int64_t)blockIdx.x * LN_TILE + (int64_t)threadIdx.x * LN_IPT;
     int64_t cc = 0, cp = 0, last = -1;
+    unsigned long long c3 = 0;           // non-MEMOP / AG / RS counts packed 21 bits apart (chopper_align's ranks)
+    int hb = -1;                         // bucket histogram: one shared atomic per run of equal bucket
+    unsigned hc = 0;
+    uint32_t mv[LN_IPT];
+    if (i0 + LN_IPT <= n && ((uintptr_t)(meta + i0) & 15u) == 0) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4 *>(meta + i0)), b = __ldg(reinterpret_cast<const uint4 *>(meta + i0) + 1);
+        mv[0] = a.x; mv[1] = a.y; mv[2] = a.z; mv[3] = a.w; mv[4] = b.x; mv[5] = b.y; mv[6] = b.z; mv[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < LN_IPT; k++) mv[k] = i0 + k < n ? meta[i0 + k] : 0u;
+    }
+#pragma unroll
     for (int k = 0; k < LN_IPT; k++) {
         const int64_t i = i0 + k;
         if (i >= n) break;
-        const uint32_t m = meta[i];
+        const uint32_t m = mv[k];
         const int kd = kind_of(m);
         if (is_comm(kd)) cc++;
         else if (kd == CK_COMPUTE) { cp++; last = i; }
-        atomicAdd(&ln_h[bucket_of(m, gpu_lg, NG, other)], 1u);
+        c3 += (kd != CK_MEMOP ? 1ull : 0ull) | (kd == CK_AG ? 1ull << 21 : 0ull) | (kd == CK_RS ? 1ull << 42 : 0ull);
+        const int b = bucket_of(m, gpu_lg, NG, other);
+        if (b != hb) {
+            if (hc) atomicAdd(&ln_h[hb], hc);
+            hb = b;
+            hc = 0;
+        }
+        hc++;
     }
+    if (hc) atomicAdd(&ln_h[hb], hc);
     int64_t tc, tp;
     block_excl_sum<LN_NT>(cc, &tc, sm);
     block_excl_sum<LN_NT>(cp, &tp, sm);
+    if (mtc) {                           // the tile counts of chopper_align's rank pass (its tiles are these)
+        int64_t t3;
+        block_excl_sum<LN_NT>((int64_t)c3, &t3, sm);
+        if (threadIdx.x == 0) {
+            const unsigned long long t = (unsigned long long)t3;
+            mtc[blockIdx.x] = (int64_t)(t & 0x1FFFFF);
+            mtc[ntile + blockIdx.x] = (int64_t)((t >> 21) & 0x1FFFFF);
+            mtc[2 * ntile + blockIdx.x] = (int64_t)(t >> 42);
+        }
+    }
     // block max of last
     int64_t x = last;
 #pragma unroll
@@ -463,12 +493,23 @@ __global__ void k_ss_check(const unsigned long long *__restrict__ key, const uin
     if (t == 0 || t >= M) return;
     if (key[t] == key[t - 1] && ks[val[t]] < ks[val[t - 1]]) atomicOr(fail, 2u);
 }
-// cl[cl_off[a] .. cl_off[a + 1]): the non-empty stream cells of segment a (built on the host at the fast-path
-// check's read-back), so an element searches only the streams present, not all SS_STREAMS cells
+// the non-empty stream cells of each segment (block a, thread = cell): cl[a * SS_STREAMS + k], k < cl_n[a], so an
+// element's rank searches only the streams present, not all SS_STREAMS cells
+__global__ void __launch_bounds__(SS_STREAMS) k_ss_cells(const unsigned int *__restrict__ cnt, int32_t *__restrict__ cl,
+                                                         int32_t *__restrict__ cl_n) {
+    __shared__ int64_t sm[33];
+    const int a = blockIdx.x, c = threadIdx.x;
+    const int cell = a * SS_STREAMS + c;
+    const bool on = cnt[cell] != 0;
+    int64_t tot;
+    const int64_t pos = block_excl_sum<SS_STREAMS>(on ? 1 : 0, &tot, sm);
+    if (on) cl[a * SS_STREAMS + pos] = cell;
+    if (c == 0) cl_n[a] = (int32_t)tot;
+}
 __global__ void k_ss_rank(const unsigned long long *__restrict__ key, const uint32_t *__restrict__ val, int64_t M,
                           const int64_t *__restrict__ ks, const unsigned int *__restrict__ cnt,
                           const int64_t *__restrict__ cstart, const int64_t *__restrict__ lo,
-                          const int32_t *__restrict__ cl, const int32_t *__restrict__ cl_off,
+                          const int32_t *__restrict__ cl, const int32_t *__restrict__ cl_n,
                           uint32_t *__restrict__ perm) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= M) return;
@@ -477,8 +518,8 @@ __global__ void k_ss_rank(const unsigned long long *__restrict__ key, const uint
     const uint32_t x = val[t];
     const int64_t kx = ks[x];
     int64_t r = t - cstart[cell];
-    for (int q = cl_off[a]; q < cl_off[a + 1]; q++) {
-        const int c2 = cl[q];
+    for (int q = 0; q < cl_n[a]; q++) {
+        const int c2 = cl[a * SS_STREAMS + q];
         const unsigned int n2 = cnt[c2];
         if (c2 == cell) continue;
         int64_t l = cstart[c2], h = l + n2;           // count of (ks, idx) < (kx, x) in list c2
@@ -556,79 +597,122 @@ static chopper_status finish_load(chopper_ctx *ctx) {
 // runs the full partition + chain, which resets the overlap report it recomputes)
 // stable timestamp sort of the permutation segments [seg_lo[s], seg_lo[s] + size) (D1): a stream-merge fast
 // path (partition by stream + binary-search ranks), else a radix sort on (segment, t_ks - t0)
-static chopper_status sort_segments(chopper_ctx *ctx, std::vector<int64_t> seg_lo, std::vector<int64_t> seg_pre,
-                                    int64_t Mseg) {
-    const int64_t n = ctx->N;
-    CH_ALLOC_BEGIN;
-    const int nseg = (int)seg_lo.size();
-    seg_pre.push_back(Mseg);
-    int tsbits = bits_for((uint64_t)(ctx->t_max - ctx->t0));
-    int sb = bits_for((uint64_t)nseg);
+// the radix path: a stable sort of the segments by (segment, t_ks - t0)
+static chopper_status sort_segments_radix(chopper_ctx *ctx, const std::vector<int64_t> &seg_lo,
+                                          const std::vector<int64_t> &seg_pre, int64_t Mseg) {
+    const int nseg = (int)seg_lo.size() - 1;         // (both arrays carry their end entry)
+    const int tsbits = bits_for((uint64_t)(ctx->t_max - ctx->t0)), sb = bits_for((uint64_t)nseg);
     if (tsbits + sb > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "sort key exceeds 64 bits");
-    size_t mk = ctx->used;
+    const size_t mk = ctx->used;
+    CH_ALLOC_BEGIN;
     unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, Mseg), *k2 = CH_ALLOC(ctx, unsigned long long, Mseg);
     uint32_t *v1 = CH_ALLOC(ctx, uint32_t, Mseg), *v2 = CH_ALLOC(ctx, uint32_t, Mseg);
     int64_t *dlo = CH_ALLOC(ctx, int64_t, nseg + 1), *dpre = CH_ALLOC(ctx, int64_t, nseg + 1);
     CH_ALLOC_END(ctx);
-    seg_lo.push_back(n);
     CH_CUDA(ctx, cudaMemcpyAsync(dlo, seg_lo.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(dpre, seg_pre.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
-    // stream-merge fast path (1-2 digit partition + binary-search ranks), else the full radix sort
-    bool merged = false;
-    {
-        const int64_t cells = (int64_t)nseg * SS_STREAMS;
-        unsigned int *cnt = CH_ALLOC(ctx, unsigned int, cells), *fail = CH_ALLOC(ctx, unsigned int, 1);
-        int64_t *c64 = CH_ALLOC(ctx, int64_t, cells), *cst = CH_ALLOC(ctx, int64_t, cells);
-        CH_ALLOC_END(ctx);
-        CH_CUDA(ctx, cudaMemsetAsync(cnt, 0, 4 * (size_t)cells, ctx->st));
-        CH_CUDA(ctx, cudaMemsetAsync(fail, 0, 4, ctx->st));
-        k_ss_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, dlo, dpre, nseg, Mseg,
-                                                                    k1, v1, cnt, fail);
-        CH_LAUNCHED(ctx);
-        bool alt2;
-        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, sb + 8, &alt2));
-        unsigned long long *ksd = alt2 ? k2 : k1;
-        uint32_t *vsd = alt2 ? v2 : v1;
-        k_ss_check<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, fail);
-        CH_LAUNCHED(ctx);
-        k_u32_i64<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(cnt, c64, cells);
-        CH_LAUNCHED(ctx);
-        CH_TRY(ch_scan_excl_i64(ctx, c64, cst, cells, nullptr));
-        unsigned int hfail = 0;
-        std::vector<unsigned int> hcnt((size_t)cells);
-        CH_CUDA(ctx, ch_d2h(ctx, &hfail, fail, 4));
-        CH_CUDA(ctx, ch_d2h(ctx, hcnt.data(), cnt, 4 * (size_t)cells));
-        CH_CUDA(ctx, ch_sync(ctx));
-        if (!hfail) {
-            std::vector<int32_t> hcl, hoff(nseg + 1, 0);
-            for (int a = 0; a < nseg; a++) {
-                hoff[a] = (int32_t)hcl.size();
-                for (int c = 0; c < SS_STREAMS; c++)
-                    if (hcnt[(size_t)a * SS_STREAMS + c]) hcl.push_back(a * SS_STREAMS + c);
-            }
-            hoff[nseg] = (int32_t)hcl.size();
-            int32_t *dcl = CH_ALLOC(ctx, int32_t, (int64_t)hcl.size() + 1), *doff = CH_ALLOC(ctx, int32_t, nseg + 1);
-            CH_ALLOC_END(ctx);
-            CH_CUDA(ctx, cudaMemcpyAsync(dcl, hcl.data(), 4 * hcl.size(), cudaMemcpyHostToDevice, ctx->st));
-            CH_CUDA(ctx, cudaMemcpyAsync(doff, hoff.data(), 4 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
-            k_ss_rank<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, cnt, cst, dlo,
-                                                                        dcl, doff, ctx->d_perm);
-            CH_LAUNCHED(ctx);
-            merged = true;
-        }
-    }
-    if (!merged) {
-        k_seg_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.start_ns, dlo, dpre, nseg,
-                                                                     Mseg, ctx->t0, tsbits, k1, v1);
-        CH_LAUNCHED(ctx);
-        bool alt;
-        CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, tsbits + sb, &alt));
-        k_seg_scatter<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(alt ? v2 : v1, dlo, dpre, nseg, Mseg,
-                                                                        ctx->d_perm);
-        CH_LAUNCHED(ctx);
-    }
+    k_seg_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.start_ns, dlo, dpre, nseg, Mseg,
+                                                                 ctx->t0, tsbits, k1, v1);
+    CH_LAUNCHED(ctx);
+    bool alt;
+    CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, tsbits + sb, &alt));
+    k_seg_scatter<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(alt ? v2 : v1, dlo, dpre, nseg, Mseg, ctx->d_perm);
+    CH_LAUNCHED(ctx);
     ctx->used = mk;
     return CHOPPER_OK;
+}
+
+// Stable timestamp sort of the permutation segments [seg_lo[s], seg_lo[s] + size) (D1): the stream-merge fast
+// path (partition by stream + binary-search ranks), else the radix path.  defer: the fast path's validity flag is
+// not waited for here -- it is read with chopper_align's read-back (ch_comm_sort_settle), and a failed check then
+// restores the saved unsorted segments and takes the radix path before anything reads them (the communication
+// buckets are first read by chopper_overlap's preparation)
+static chopper_status sort_segments(chopper_ctx *ctx, std::vector<int64_t> seg_lo, std::vector<int64_t> seg_pre,
+                                    int64_t Mseg, bool defer = false) {
+    const int64_t n = ctx->N;
+    CH_ALLOC_BEGIN;
+    const int nseg = (int)seg_lo.size();
+    seg_pre.push_back(Mseg);
+    seg_lo.push_back(n);
+    const int sb = bits_for((uint64_t)nseg);
+    if (bits_for((uint64_t)(ctx->t_max - ctx->t0)) + sb > 64) return ch_fail(ctx, CHOPPER_E_RANGE, "sort key exceeds 64 bits");
+    unsigned int *fail = nullptr;
+    if (defer) {
+        // kept until chopper_align: the flag and the unsorted segments (for a redo)
+        fail = CH_ALLOC(ctx, unsigned int, 1);
+        ctx->d_ss_save = CH_ALLOC(ctx, uint32_t, Mseg);
+        CH_ALLOC_END(ctx);
+        for (int a = 0; a < nseg; a++)
+            CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_ss_save + seg_pre[a], ctx->d_perm + seg_lo[a],
+                                         4 * (size_t)(seg_pre[a + 1] - seg_pre[a]), cudaMemcpyDeviceToDevice, ctx->st));
+    }
+    size_t mk = ctx->used;
+    unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, Mseg), *k2 = CH_ALLOC(ctx, unsigned long long, Mseg);
+    uint32_t *v1 = CH_ALLOC(ctx, uint32_t, Mseg), *v2 = CH_ALLOC(ctx, uint32_t, Mseg);
+    int64_t *dlo = CH_ALLOC(ctx, int64_t, nseg + 1), *dpre = CH_ALLOC(ctx, int64_t, nseg + 1);
+    const int64_t cells = (int64_t)nseg * SS_STREAMS;
+    unsigned int *cnt = CH_ALLOC(ctx, unsigned int, cells);
+    if (!fail) fail = CH_ALLOC(ctx, unsigned int, 1);
+    int64_t *c64 = CH_ALLOC(ctx, int64_t, cells), *cst = CH_ALLOC(ctx, int64_t, cells);
+    int32_t *dcl = CH_ALLOC(ctx, int32_t, cells), *dcn = CH_ALLOC(ctx, int32_t, nseg + 1);
+    CH_ALLOC_END(ctx);
+    CH_CUDA(ctx, cudaMemcpyAsync(dlo, seg_lo.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
+    CH_CUDA(ctx, cudaMemcpyAsync(dpre, seg_pre.data(), 8 * (nseg + 1), cudaMemcpyHostToDevice, ctx->st));
+    CH_CUDA(ctx, cudaMemsetAsync(cnt, 0, 4 * (size_t)cells, ctx->st));
+    CH_CUDA(ctx, cudaMemsetAsync(fail, 0, 4, ctx->st));
+    k_ss_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, dlo, dpre, nseg, Mseg,
+                                                                k1, v1, cnt, fail);
+    CH_LAUNCHED(ctx);
+    bool alt2;
+    CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, sb + 8, &alt2));
+    unsigned long long *ksd = alt2 ? k2 : k1;
+    uint32_t *vsd = alt2 ? v2 : v1;
+    k_ss_check<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, fail);
+    CH_LAUNCHED(ctx);
+    k_u32_i64<<<(unsigned)ceil_div(cells, NT), NT, 0, ctx->st>>>(cnt, c64, cells);
+    CH_LAUNCHED(ctx);
+    CH_TRY(ch_scan_excl_i64(ctx, c64, cst, cells, nullptr));
+    k_ss_cells<<<nseg, SS_STREAMS, 0, ctx->st>>>(cnt, dcl, dcn);
+    CH_LAUNCHED(ctx);
+    if (defer) {
+        // speculative: valid unless the flag is set (then ch_comm_sort_settle redoes the segments)
+        k_ss_rank<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, cnt, cst, dlo,
+                                                                    dcl, dcn, ctx->d_perm);
+        CH_LAUNCHED(ctx);
+        ctx->d_ss_fail = fail;
+        ctx->ss_seg_lo = seg_lo;
+        ctx->ss_seg_pre = seg_pre;
+        ctx->ss_M = Mseg;
+        ctx->ss_pending = true;
+        ctx->used = mk;
+        return CHOPPER_OK;
+    }
+    unsigned int hfail = 0;
+    CH_CUDA(ctx, ch_d2h(ctx, &hfail, fail, 4));
+    CH_CUDA(ctx, ch_sync(ctx));
+    if (!hfail) {
+        k_ss_rank<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ksd, vsd, Mseg, ctx->ev.start_ns, cnt, cst, dlo,
+                                                                    dcl, dcn, ctx->d_perm);
+        CH_LAUNCHED(ctx);
+        ctx->used = mk;
+        return CHOPPER_OK;
+    }
+    ctx->used = mk;
+    return sort_segments_radix(ctx, seg_lo, seg_pre, Mseg);
+}
+
+// the deferred check of the lean path's communication sort (called right after chopper_align's synchronization,
+// which also brought h_ss_fail): a failed stream-merge check restores the unsorted segments and sorts by radix
+chopper_status ch_comm_sort_settle(chopper_ctx *ctx) {
+    if (!ctx->ss_pending) return CHOPPER_OK;
+    ctx->ss_pending = false;
+    if (!ctx->h_ss_fail) return CHOPPER_OK;
+    const int nseg = (int)ctx->ss_seg_lo.size() - 1;
+    for (int a = 0; a < nseg; a++)
+        CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_perm + ctx->ss_seg_lo[a], ctx->d_ss_save + ctx->ss_seg_pre[a],
+                                     4 * (size_t)(ctx->ss_seg_pre[a + 1] - ctx->ss_seg_pre[a]), cudaMemcpyDeviceToDevice,
+                                     ctx->st));
+    return sort_segments_radix(ctx, ctx->ss_seg_lo, ctx->ss_seg_pre, ctx->ss_M);
 }
 
 static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back);
@@ -643,6 +727,8 @@ chopper_status ch_load(chopper_ctx *ctx) {
         ctx->span_pending = false;
     }
     ctx->span_launched = false;
+    ctx->d_meta_tc = nullptr;
+    ctx->ss_pending = false;
     if (ctx->prep_pending) {                    // likewise chopper_overlap's preparation
         CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->prep_join, 0));
         ctx->prep_pending = false;
@@ -815,6 +901,8 @@ static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back) {
     *fell_back = false;
     const int64_t ntile = ceil_div(n, LN_TILE);
     CH_ALLOC_BEGIN;
+    ctx->d_meta_tc = CH_ALLOC(ctx, int64_t, 3 * ntile);       // kept for chopper_align (no separate count pass)
+    CH_ALLOC_END(ctx);
     const size_t keep = ctx->used;
     int64_t *tcm = CH_ALLOC(ctx, int64_t, ntile + 1), *tcp = CH_ALLOC(ctx, int64_t, ntile + 1);
     int64_t *tla = CH_ALLOC(ctx, int64_t, ntile + 1), *tcme = CH_ALLOC(ctx, int64_t, ntile + 1);
@@ -828,7 +916,7 @@ static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back) {
     CH_CUDA(ctx, cudaMemsetAsync(nonmono, 0, 4, ctx->st));
     CH_CUDA(ctx, cudaMemcpyAsync(gb, ctx->g_beg, 8 * (n_lg + 1), cudaMemcpyHostToDevice, ctx->st));
     k_lean_tiles<<<(unsigned)ntile, LN_NT, 4 * nb, ctx->st>>>(ctx->ev.meta, n, ctx->d_gpu_lg, NG, other, tcm, tcp, tla,
-                                                              bcnt, nb);
+                                                              bcnt, nb, ctx->d_meta_tc, ntile);
     CH_LAUNCHED(ctx);
     CH_TRY(ch_scan_excl_i64(ctx, tcm, tcme, ntile, nullptr));
     CH_TRY(ch_scan_excl_i64(ctx, tcp, tcpe, ntile, nullptr));
@@ -866,7 +954,7 @@ static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back) {
         }
     }
     if (Mseg > 0) {
-        CH_TRY(sort_segments(ctx, seg_lo, seg_pre, Mseg));
+        CH_TRY(sort_segments(ctx, seg_lo, seg_pre, Mseg, true));
         ctx->full_sort = true;
     }
     return CHOPPER_OK;

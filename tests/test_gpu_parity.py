@@ -703,3 +703,23 @@ def test_ctx_reuse_across_steps_with_side_streams():
     step(bb)
     step(ba)
     pipe.close()
+
+
+def test_comm_stream_out_of_start_order_lean():
+    """Lean a2 (one compute stream) with a communication stream whose starts are not in dispatch order: the
+    stream-merge fast path's check fails, which the lean path reads only at chopper_align's read-back; the
+    communication buckets are then restored and radix-sorted before chopper_overlap reads them (D1)."""
+    tt = TinyTrace(n_gpus=2).span(0, 0, 0, 10_000, 1).span(1, 0, 0, 10_000, 1)
+    for g in range(2):
+        t = 0
+        for k in range(40):
+            tt.ev(g, t, t + 5, t + 60)                                        # compute, stream 0
+            t += 70
+        # all-gathers dispatched in this order, started out of order; reduce-scatters in order
+        for k, ks in enumerate([300, 100, 900, 500, 700, 200]):
+            tt.ev(g, 50 + 10 * k, ks, ks + 150, kind=AG, stream=1)
+        for k in range(5):
+            tt.ev(g, 60 + 10 * k, 1000 + 300 * k, 1100 + 300 * k, kind=RS, stream=2)
+    ref, got, _, _ = _tiny(tt)
+    _check_status(ref, got)
+    assert_parity(ref, got)
