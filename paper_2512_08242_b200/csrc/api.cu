@@ -75,8 +75,11 @@ size_t chopper_scratch_plan(const chopper_config *cfg, const chopper_shape *sh, 
     const size_t Rb = std::min(N, 2 * S + tiles + G + 1) + 1;          // instance runs / instance rows
     const size_t row = 8 + 8 * RF_NFIELDS + 8 * std::max<size_t>(C, 1) + 7 * 4 + 8;   // RowTable with identity
     // events: permutation + chain predecessor end; counter-pass position + run id (counters); the exact
-    // sweep's [4][N] span table (non-laminar); the explicit compute union + its permutation (several streams)
-    it.events = N * 12 + (C ? N * 8 : 0) + (laminar ? 0 : N * 16) + (multi ? N * 28 : 0);
+    // sweep's [4][N] span table (non-laminar); the explicit compute union + its permutation (several streams);
+    // the head pre-count's key-table index per event (4 B, whole tiles) and, without counters, its per-thread
+    // head masks / ranks
+    it.events = N * 12 + (C ? N * 8 : 0) + (laminar ? 0 : N * 16) + (multi ? N * 28 : 0) + tiles * 2048 * 4 +
+                (C ? 0 : tiles * 256 * 5);
     // push-order span arrays (32 B), Euler tables (12 B per endpoint), merged key table (16 B per endpoint),
     // chunk stacks and sparse tables (~8 B)
     it.spans = S * 32 + (2 * S + 4 * G + 2) * 28 + S * 8 + 4096 * (G + 1);
@@ -122,6 +125,8 @@ size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_
     sh.laminar = 0;
     return chopper_scratch_plan(cfg, &sh, nullptr);
 }
+
+HostProf g_hprof;
 
 chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int device, void *cuda_stream,
                               void *nccl_comm, int rank, int nranks, void *scratch, size_t scratch_bytes) {
@@ -174,6 +179,7 @@ static chopper_status load_columns(chopper_ctx *ctx, const chopper_events *ev, c
                                    const chopper_samples *smp);
 chopper_status chopper_load_columns(chopper_ctx *ctx, const chopper_events *ev, const chopper_spans *sp,
                                     const chopper_samples *smp) {
+    g_hprof.dump();
     if (!ctx) return CHOPPER_E_INVALID_ARG;
     ctx->poison = CHOPPER_OK;             // a new step
     ctx->x_exchanged = ctx->d_exchanged = false;

@@ -7,7 +7,10 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -313,8 +316,40 @@ struct chopper_ctx {
         if (s_ != CHOPPER_OK) return s_;      \
     } while (0)
 
+// development aid (CHOPPER_DBG_HOST=1): host time from each stream synchronization's return to the next
+// kernel launch -- the stretch in which the GPU idles waiting for the host -- attributed to that launch's line
+struct HostProf {
+    bool on = getenv("CHOPPER_DBG_HOST") != nullptr;
+    bool armed = false;
+    double t_sync = 0.0, t_wait = 0.0;
+    std::vector<std::pair<std::string, double>> gaps;     // (launch site, gap us)
+    std::vector<double> waits;                            // sync wait us
+    static double now_us() {
+        return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
+    void launch(const char *f, int line) {
+        if (!on || !armed) return;
+        armed = false;
+        const char *b = strrchr(f, '/');
+        gaps.push_back({std::string(b ? b + 1 : f) + ":" + std::to_string(line), now_us() - t_sync});
+    }
+    void dump() {
+        if (!on || gaps.empty()) return;
+        double s = 0, w = 0;
+        for (auto &g : gaps) s += g.second;
+        for (double x : waits) w += x;
+        fprintf(stderr, "[host] syncs %zu wait %.1f us, sync->launch gaps %.1f us:", waits.size(), w, s);
+        for (auto &g : gaps) fprintf(stderr, " %s=%.1f", g.first.c_str(), g.second);
+        fprintf(stderr, "\n");
+        gaps.clear();
+        waits.clear();
+    }
+};
+extern HostProf g_hprof;
+
 #define CH_LAUNCHED(ctx)                                                                   \
     do {                                                                                   \
+        g_hprof.launch(__FILE__, __LINE__);                                                \
         (ctx)->launches++;                                                                 \
         cudaError_t e_ = cudaGetLastError();                                               \
         if (e_ != cudaSuccess) {                                                           \
@@ -329,7 +364,13 @@ chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &ms
 // host synchronization with the ctx stream (counted: chopper_host_syncs)
 inline cudaError_t ch_sync(chopper_ctx *ctx) {
     ctx->syncs++;
+    const double t_a = g_hprof.on ? HostProf::now_us() : 0.0;
     const cudaError_t e = cudaStreamSynchronize(ctx->st);
+    if (g_hprof.on) {
+        g_hprof.t_sync = HostProf::now_us();
+        g_hprof.waits.push_back(g_hprof.t_sync - t_a);
+        g_hprof.armed = true;
+    }
     if (e == cudaSuccess)
         for (const auto &p : ctx->pin_pending) memcpy(p.dst, p.src, p.n);
     ctx->pin_pending.clear();

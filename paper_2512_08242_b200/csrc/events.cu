@@ -298,6 +298,10 @@ struct EvParams {
     const int64_t *tile_base;     // [ntile + 1] first sub-run id of each tile
     const struct TileWin *twin;   // [ntile] placed windows
     const struct TileWinL *twinl; // [ntile] placed windows of the lean pass
+    // lean pass: the head pre-count's results, so the event pass does no key lookups of its own
+    uint32_t *kidx;               // [ntile * 2048] key-table index of each event (written by k_tile_heads)
+    const int32_t *h_run;         // [ntile][256] in-tile head rank before each thread's first event
+    const uint8_t *h_hm;          // [ntile][256] head mask of each thread's 8 events
 };
 
 
@@ -1395,12 +1399,15 @@ __global__ void __launch_bounds__(W_NT, 4) k_tile_heads(EvParams P, int64_t *__r
     int64_t prevj = -1;
     int nh = 0;
     unsigned hm = 0;                      // head mask of the thread's 8 events (the event pass's rule)
+    uint32_t kx[EV_IPT];                  // key-table index of each event (the lean event pass reads it)
 #pragma unroll
     for (int k = 0; k < EV_IPT; k++) {
+        kx[k] = KIDX_NONE;
         if (k < nv) {
             const int lg = P.gpu_lg[gpu_of(mt[k])];
             if (lg != lgc) { wk = win_global(P, 0, lg); wcur_init(ck); lgc = lg; }
             wcur_seek(wk, ck, tl[k]);
+            kx[k] = (uint32_t)ck.j;
             if (ck.j != prevj) {
                 const unsigned long long kk = key_at(wk, P, ck.j);
                 if (k > 0 && kk != prevk) { nh++; hm |= 1u << k; }
@@ -1439,6 +1446,11 @@ __global__ void __launch_bounds__(W_NT, 4) k_tile_heads(EvParams P, int64_t *__r
     if (P.t_run) {                        // the counter pass's view: head mask + in-tile rank (plus the tile base there)
         P.t_run[tile * (int64_t)W_NT + tid] = wb + inc - nh;
         P.t_hm[tile * (int64_t)W_NT + tid] = (uint8_t)hm;
+    }
+    if (P.kidx) {                         // (the column has whole tiles: no bounds check)
+        uint4 *o = reinterpret_cast<uint4 *>(P.kidx + i0);
+        o[0] = make_uint4(kx[0], kx[1], kx[2], kx[3]);
+        o[1] = make_uint4(kx[4], kx[5], kx[6], kx[7]);
     }
 }
 
@@ -1622,8 +1634,7 @@ struct EvSmemL {
     static constexpr int NT = W_NT, TILE = W_TILE, WARPS = W_WARPS;
     longlong2 col[3][W_TILE / 2];         // t_l, t_ks, t_ke (48 KB), 64 B-swizzled rows (TMA)
     uint4 meta[W_TILE / 4];               // 8 KB, 32 B-swizzled rows (TMA)
-    uint32_t kidx[EV_IPT][W_NT];          // key of each event as a key-table index (8 KB)
-    unsigned long long lastk[W_NT];
+    uint32_t kidx[W_TILE];                // key of each event as a key-table index (8 KB, k_tile_heads; bulk copy)
     Acc wagg[W_WARPS], wcarry[W_WARPS];
     int wflag[W_WARPS], wcflag[W_WARPS];
     int wheads[W_WARPS];
@@ -1858,12 +1869,13 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_l(EvParams P, const __grid_c
     __syncthreads();
     const TileWinL *twp = P.twinl + tile;
     if (tid == 0) {
-        mbar_arrive_tx(&S.bar[0], 3u * 16384u + 8192u);
+        mbar_arrive_tx(&S.bar[0], 3u * 16384u + 8192u + 8192u);
         const int row = (int)(base >> 3);
         tma_2d(&S.col[0][0], &tm_tl, 0, row, &S.bar[0]);
         tma_2d(&S.col[1][0], &tm_ks, 0, row, &S.bar[0]);
         tma_2d(&S.col[2][0], &tm_ke, 0, row, &S.bar[0]);
         tma_2d(&S.meta[0], &tm_meta, 0, row, &S.bar[0]);
+        bulk_g2s(&S.kidx[0], P.kidx + base, 8192u, &S.bar[0]);     // (the column has whole tiles)
         S.excl = P.tile_base[tile];
         S.tot = (int)(P.tile_base[tile + 1] - P.tile_base[tile]);
     } else if (tid == 32) {
@@ -1909,44 +1921,16 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_l(EvParams P, const __grid_c
     }
     const WinL wkP = winl_reg(twp->tw[0], S, 0, P);
 
-    // ---- phase A: instance key per event (a5) and the thread's last COMPUTE kernel (a7 chain) ----
-    unsigned hmask = 0;
-    unsigned long long firstk = CH_INVALID_KEY;
+    // ---- phase A: the thread's last COMPUTE kernel (a7 chain).  The instance keys (a5) -- each event's
+    // key-table index, the head masks and the in-tile head ranks -- come from the head pre-count ----
+    const int64_t th = tile * (int64_t)W_NT + tid;
+    unsigned hmask = P.h_hm[th];
+    const int32_t hrank = P.h_run[th];
     int32_t lpos = -1;                         // tile offset of the thread's last COMPUTE event
     int64_t lend = 0;
-    {
-        WinL wk = wkP;
-        int gc = gP;
-        WCur ck;
-        wcur_init(ck);
-        unsigned long long prevk = CH_INVALID_KEY;
-        int64_t prevj = -1;
-#pragma unroll 1
-        for (int k = 0; k < EV_IPT; k++) {
-            uint32_t v = KIDX_NONE;
-            if (k < nv) {
-                const int64_t t = rcol(S, 0, tid, x64, k);
-                const uint32_t m = rmeta(S, tid, x32, k);
-                const int g = gpu_of(m);
-                if (g != gc) { wk = winl_for(P, 0, g, lgP, wkP); wcur_init(ck); gc = g; }
-                if (!(t < ck.b && t >= ck.a)) winl_seek(wk, ck, t);
-                v = (uint32_t)ck.j;
-                if (ck.j != prevj) {                  // same entry => same key; else compare the keys
-                    const unsigned long long kk = keyl_at(wk, P, ck.j);
-                    if (k > 0 && kk != prevk) hmask |= 1u << k;
-                    prevk = kk;
-                    prevj = ck.j;
-                }
-                if (kind_of(m) == CK_COMPUTE) { lpos = tid * EV_IPT + k; lend = rcol(S, 2, tid, x64, k); }
-            } else {
-                prevk = CH_INVALID_KEY;
-                prevj = -1;
-            }
-            if (k == 0) firstk = prevk;
-            S.kidx[k][tid] = v;
-        }
-        S.lastk[tid] = prevk;
-    }
+#pragma unroll
+    for (int k = 0; k < EV_IPT; k++)
+        if (k < nv && kind_of(rmeta(S, tid, x32, k)) == CK_COMPUTE) { lpos = tid * EV_IPT + k; lend = rcol(S, 2, tid, x64, k); }
     // chain scan: the last COMPUTE event before this thread (position, end); the later position wins
     int32_t xpos = lpos;
     int64_t xend = lend;
@@ -1958,13 +1942,7 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_l(EvParams P, const __grid_c
     }
     if (lane == 31) { S.wpos[warp] = xpos; S.wend[warp] = xend; }
     __syncthreads();
-    int tot;
-    const int ex = tile_head_scan_h(S, hmask, nv > 0 && (tid == 0 || firstk != S.lastk[tid - 1]), &tot);
-    const int64_t run0 = S.excl + ex;
-    if (P.t_run) {                        // the counter pass's view of the runs: 5 B per thread
-        P.t_run[tile * (int64_t)blockDim.x + threadIdx.x] = (int32_t)(run0 - 1);    // (k_events: ticketed tiles)
-        P.t_hm[tile * (int64_t)blockDim.x + threadIdx.x] = (uint8_t)hmask;
-    }
+    const int64_t run0 = S.excl + hrank;
     int32_t ppos = __shfl_up_sync(CH_FULL, xpos, 1);
     int64_t pend = __shfl_up_sync(CH_FULL, xend, 1);
     if (lane == 0) { ppos = -1; pend = 0; }
@@ -2005,7 +1983,7 @@ __global__ void __launch_bounds__(W_NT, 2) k_events_l(EvParams P, const __grid_c
                 else write_subrun(P, curid, cur, base);
                 curid++;
                 cur.zero();
-                const uint32_t v = S.kidx[k][tid];
+                const uint32_t v = S.kidx[tid * EV_IPT + k];
                 if (curid < cap) {
                     P.sr_key[curid] = keyl_at(g == gP ? wkP : winl_for(P, 0, g, lgP, wkP), P, (int64_t)v);
                     P.sr_first[curid] = i;
@@ -2301,6 +2279,9 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
     P.o_run = nullptr;
     P.t_run = ctx->d_t_run;
     P.t_hm = ctx->d_t_hm;
+    P.kidx = nullptr;
+    P.h_run = nullptr;
+    P.h_hm = nullptr;
     P.sr_key = ctx->sub.key; P.sr_first = ctx->sub.first_event; P.sr_f = ctx->sub.f; P.cap = cap;
     P.tile_state = ctx->d_tile_state; P.ticket = ctx->d_tile_ticket;
     P.KTt = ctx->KT_t; P.KTk = ctx->KT_k; P.kt_beg = ctx->d_kt_beg;
@@ -2335,7 +2316,15 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         int64_t *tcnt = CH_ALLOC(ctx, int64_t, ntile + 1), *tbase = ctx->d_tile_sub;
         TileWin *twin = CH_ALLOC(ctx, TileWin, ntile);
         TileWinL *twinl = CH_ALLOC(ctx, TileWinL, ntile);
+        // the head pre-count's per-event key indices and per-thread head masks / ranks, read by the event pass
+        P.kidx = CH_ALLOC(ctx, uint32_t, ntile * W_TILE);
+        if (!P.t_run) {                       // (without counters the counter pass's copies do not exist)
+            P.t_run = CH_ALLOC(ctx, int32_t, ntile * W_NT);
+            P.t_hm = CH_ALLOC(ctx, uint8_t, ntile * W_NT);
+        }
         CH_ALLOC_END(ctx);
+        P.h_run = P.t_run;
+        P.h_hm = P.t_hm;
         P.seeds = seeds;
         const size_t dsm = sizeof(EvSmemL);
         static bool attr_l = false;

@@ -474,11 +474,12 @@ __device__ __forceinline__ int seg_of(const int64_t *__restrict__ pre, int nseg,
 __global__ void k_ss_keys(const uint32_t *__restrict__ perm, const uint32_t *__restrict__ meta,
                           const int64_t *__restrict__ lo, const int64_t *__restrict__ pre, int nseg, int64_t M,
                           unsigned long long *__restrict__ key, uint32_t *__restrict__ val, unsigned int *__restrict__ cnt,
-                          unsigned int *__restrict__ fail) {
+                          unsigned int *__restrict__ fail, uint32_t *__restrict__ save) {
     int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= M) return;
     const int a = seg_of(pre, nseg, t);
     const uint32_t i = perm[lo[a] + (t - pre[a])];
+    if (save) save[t] = i;                    // the unsorted segments, for a redo by the radix path
     const int st = stream_of(meta[i]);
     if (st >= SS_STREAMS) atomicOr(fail, 1u);
     const int cell = a * SS_STREAMS + (st & (SS_STREAMS - 1));
@@ -641,10 +642,7 @@ static chopper_status sort_segments(chopper_ctx *ctx, std::vector<int64_t> seg_l
         // kept until chopper_align: the flag and the unsorted segments (for a redo)
         fail = CH_ALLOC(ctx, unsigned int, 1);
         ctx->d_ss_save = CH_ALLOC(ctx, uint32_t, Mseg);
-        CH_ALLOC_END(ctx);
-        for (int a = 0; a < nseg; a++)
-            CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_ss_save + seg_pre[a], ctx->d_perm + seg_lo[a],
-                                         4 * (size_t)(seg_pre[a + 1] - seg_pre[a]), cudaMemcpyDeviceToDevice, ctx->st));
+        CH_ALLOC_END(ctx);                   // (filled by k_ss_keys)
     }
     size_t mk = ctx->used;
     unsigned long long *k1 = CH_ALLOC(ctx, unsigned long long, Mseg), *k2 = CH_ALLOC(ctx, unsigned long long, Mseg);
@@ -661,7 +659,7 @@ static chopper_status sort_segments(chopper_ctx *ctx, std::vector<int64_t> seg_l
     CH_CUDA(ctx, cudaMemsetAsync(cnt, 0, 4 * (size_t)cells, ctx->st));
     CH_CUDA(ctx, cudaMemsetAsync(fail, 0, 4, ctx->st));
     k_ss_keys<<<(unsigned)ceil_div(Mseg, NT), NT, 0, ctx->st>>>(ctx->d_perm, ctx->ev.meta, dlo, dpre, nseg, Mseg,
-                                                                k1, v1, cnt, fail);
+                                                                k1, v1, cnt, fail, defer ? ctx->d_ss_save : nullptr);
     CH_LAUNCHED(ctx);
     bool alt2;
     CH_TRY(ch_radix_sort(ctx, k1, v1, k2, v2, Mseg, 0, sb + 8, &alt2));
