@@ -32,6 +32,10 @@ def test_compute_sanitizer(tool):
     cmd += [sys.executable, os.path.join(HERE, "sanitize_run.py")]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=3000)
     out = p.stdout + p.stderr
+    if "compute-sanitizer is closed" in out:
+        # the pool's operators closed the tool (a wrapper refuses to run); the last runs under it are in
+        # profiles/r02_gpu_tests_p.txt (all three tools green)
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     summ = re.findall(r"ERROR SUMMARY: (\d+) error", out) + re.findall(r"RACECHECK SUMMARY: \d+ hazards? displayed \((\d+) error", out)
     assert p.returncode == 0 and "sanitize workload ok" in out, out[-4000:]
     assert summ and all(int(x) == 0 for x in summ), out[-4000:]
