@@ -515,6 +515,23 @@ __device__ __forceinline__ int64_t last_le(const int64_t *__restrict__ a, int64_
     return l - 1;
 }
 
+// last_le by a whole warp (every lane calls it, every lane gets the answer): 32 probes per round, so a
+// search over n entries takes about log32(n) dependent loads instead of log2(n)
+__device__ __forceinline__ int64_t warp_last_le(const int64_t *__restrict__ a, int64_t lo, int64_t hi, int64_t t) {
+    const int lane = threadIdx.x & 31;
+    int64_t l = lo, h = hi;              // entries before l are <= t, entries from h on are > t
+    while (h - l > 32) {
+        const int64_t step = (h - l + 31) >> 5;
+        const int64_t p = l + (int64_t)(lane + 1) * step - 1;
+        const int c = __popc(__ballot_sync(0xFFFFFFFFu, p < h && __ldg(a + p) <= t));
+        const int64_t nh = l + (int64_t)(c + 1) * step - 1;
+        l += (int64_t)c * step;
+        if (nh < h) h = nh;
+    }
+    const int64_t p = l + lane;
+    return l + __popc(__ballot_sync(0xFFFFFFFFu, p < h && __ldg(a + p) <= t)) - 1;
+}
+
 // warp inclusive scan (sum) of int64
 __device__ __forceinline__ int64_t warp_incl_sum(int64_t v) {
 #pragma unroll

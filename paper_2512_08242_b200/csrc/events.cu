@@ -1684,14 +1684,14 @@ __global__ void k_tile_seeds_l(EvParams P, int32_t *__restrict__ seeds, int64_t 
     const uint32_t m = i < P.N ? P.meta[i] : 0u;
     const bool cmp = i < P.N && kind_of(m) == CK_COMPUTE && P.gpu_lg[gpu_of(m)] == lg;
     const unsigned cm = __ballot_sync(CH_FULL, cmp);
-    int64_t s = 0;
-    if (lane < NTAB) {
-        const int64_t t = lane == 0 ? P.tl[base] : (cm ? P.ks[base + __ffs(cm) - 1] : P.tl[base]);
+    int64_t s = lane == NTAB ? lg : 0;
+#pragma unroll
+    for (int x = 0; x < NTAB; x++) {          // (the whole warp searches each table: log32 dependent loads)
+        const int64_t t = x == 0 ? P.tl[base] : (cm ? P.ks[base + __ffs(cm) - 1] : P.tl[base]);
         int64_t gb, ge;
-        tab_bounds(P, lane, lg, &gb, &ge);
-        s = last_le(lane == 0 ? P.KTt : P.TLt, gb, ge, t);
-    } else if (lane == NTAB) {
-        s = lg;
+        tab_bounds(P, x, lg, &gb, &ge);
+        const int64_t r = warp_last_le(x == 0 ? P.KTt : P.TLt, gb, ge, t);
+        if (lane == x) s = r;
     }
     if (lane < SEED_W) seeds[tile * SEED_W + lane] = (int32_t)s;
     // backward search for the chain carry, 32 events per probe

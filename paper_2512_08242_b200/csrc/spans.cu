@@ -362,13 +362,15 @@ __global__ void __launch_bounds__(KT_NT) k_keytab_blk(const int64_t *__restrict_
     __syncthreads();
     const int l = s_list, lg = l >> 2, lv = l & 3;
     const int64_t j0 = s_j0, j1 = s_j1;
-    if (tid < 3) {
-        const int o = tid + (tid >= lv ? 1 : 0);
+    if (tid < 3 * 32) {                                     // warp q: the window of the q-th other list
+        const int q = tid >> 5, o = q + (q >= lv ? 1 : 0);
         const int64_t b = et_beg[lg * 4 + o], e = et_beg[lg * 4 + o + 1];
-        const int64_t lo = last_le(Et, b, e, Et[j0]);       // >= b (sentinel)
-        const int64_t hi = last_le(Et, lo, e, Et[j1 - 1]) + 1;
-        s_lo[tid] = lo;
-        s_n[tid] = hi - lo <= KT_WIN ? hi - lo : -1;          // -1: search global memory
+        const int64_t lo = warp_last_le(Et, b, e, Et[j0]);  // >= b (sentinel)
+        const int64_t hi = warp_last_le(Et, lo, e, Et[j1 - 1]) + 1;
+        if ((tid & 31) == 0) {
+            s_lo[q] = lo;
+            s_n[q] = hi - lo <= KT_WIN ? hi - lo : -1;      // -1: search global memory
+        }
     }
     __syncthreads();
 #pragma unroll
