@@ -15,6 +15,7 @@ chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &ms
 
 // failure protocol (chopper.h): remember this rank's first failure of the step (several ranks only)
 static chopper_status step(chopper_ctx *ctx, chopper_status s) {
+    g_marks.mark(ctx->st, "call_end");
     if (s != CHOPPER_OK) ctx->pin_pending.clear();
     if (s != CHOPPER_OK && ctx->nranks > 1 && ctx->poison == CHOPPER_OK) ctx->poison = s;
     return s;
@@ -127,6 +128,7 @@ size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_
 }
 
 HostProf g_hprof;
+DevMarks g_marks;
 
 chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int device, void *cuda_stream,
                               void *nccl_comm, int rank, int nranks, void *scratch, size_t scratch_bytes) {
@@ -180,7 +182,9 @@ static chopper_status load_columns(chopper_ctx *ctx, const chopper_events *ev, c
 chopper_status chopper_load_columns(chopper_ctx *ctx, const chopper_events *ev, const chopper_spans *sp,
                                     const chopper_samples *smp) {
     g_hprof.dump();
+    g_marks.dump();
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    g_marks.mark(ctx->st, "begin");
     ctx->poison = CHOPPER_OK;             // a new step
     ctx->x_exchanged = ctx->d_exchanged = false;
     ctx->stage = 0;
@@ -301,6 +305,7 @@ static chopper_status overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_n
         CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->prep_join, 0));
         ctx->prep_pending = false;
     }
+    g_marks.mark(ctx->st, "ov_prep_join");
     if (!ctx->prep_done) CH_TRY(ch_overlap_prep(ctx));
     ctx->prep_done = false;
     ch_tick(ctx, 3, 1);

@@ -346,6 +346,33 @@ struct HostProf {
     }
 };
 extern HostProf g_hprof;
+// development aid (CHOPPER_DBG_MARKS=1): device timestamps at marked points of the ctx stream, printed (deltas)
+// at the next chopper_load_columns
+struct DevMarks {
+    bool on = getenv("CHOPPER_DBG_MARKS") != nullptr;
+    cudaEvent_t ev[64] = {};
+    const char *lab[64] = {};
+    int n = 0;
+    void mark(cudaStream_t st, const char *l) {
+        if (!on || n >= 64) return;
+        if (!ev[n]) cudaEventCreate(&ev[n]);
+        cudaEventRecord(ev[n], st);
+        lab[n++] = l;
+    }
+    void dump() {
+        if (!on || n < 2) { n = 0; return; }
+        cudaEventSynchronize(ev[n - 1]);
+        fprintf(stderr, "[marks]");
+        for (int i = 1; i < n; i++) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, " %s %.3f", lab[i], ms);
+        }
+        fprintf(stderr, "\n");
+        n = 0;
+    }
+};
+extern DevMarks g_marks;
 
 #define CH_LAUNCHED(ctx)                                                                   \
     do {                                                                                   \

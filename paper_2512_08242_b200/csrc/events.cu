@@ -2333,6 +2333,7 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
             CH_CUDA(ctx, cudaFuncSetAttribute(k_events_l<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
             attr_l = true;
         }
+        g_marks.mark(ctx->st, "ev_prologue");
         ch_tick(ctx, 4, 0);
         k_tile_seeds_l<<<(unsigned)ceil_div(ntile * 32, NT), NT, 0, ctx->st>>>(P, seeds, tpe);
         CH_LAUNCHED(ctx);
@@ -2342,8 +2343,10 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         CH_LAUNCHED(ctx);
         P.twin = twin;
         P.twinl = twinl;
+        g_marks.mark(ctx->st, "seeds_windows");
         k_tile_heads<<<(unsigned)ntile, W_NT, 0, ctx->st>>>(P, tcnt);      // (+ head masks / ranks for counters)
         CH_LAUNCHED(ctx);
+        g_marks.mark(ctx->st, "heads");
         CH_TRY(ch_scan_excl_i64(ctx, tcnt, tbase, ntile, tbase + ntile));
         P.tile_base = tbase;
         if (sub_cnt) {                        // the counter pass beside the event pass (side[0])
@@ -2356,9 +2359,11 @@ chopper_status ch_event_pass(chopper_ctx *ctx, int64_t *ovl, int64_t *prep, int6
         ctx->t_run_rank = true;
         const bool out = ovl || prep || call || phi || psi;
         ch_tick(ctx, 8, 0);
+        g_marks.mark(ctx->st, "scan_counters_fork");
         if (out) k_events_l<true><<<(unsigned)ntile, W_NT, dsm, ctx->st>>>(P, tm[0], tm[1], tm[2], tm[3]);
         else k_events_l<false><<<(unsigned)ntile, W_NT, dsm, ctx->st>>>(P, tm[0], tm[1], tm[2], tm[3]);
         CH_LAUNCHED(ctx);
+        g_marks.mark(ctx->st, "events_l");
         ch_tick(ctx, 8, 1);
         ch_tick(ctx, 4, 1);
         CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_tile_state + ntile - 1, tbase + ntile, 8, cudaMemcpyDeviceToDevice, ctx->st));
