@@ -127,6 +127,23 @@ size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_
     return chopper_scratch_plan(cfg, &sh, nullptr);
 }
 
+// orders a call's work after the caller's stream and the caller's stream after the call's work
+struct CallJoin {
+    chopper_ctx *c;
+    explicit CallJoin(chopper_ctx *ctx) : c(ctx) {
+        if (c && c->st) {
+            cudaEventRecord(c->call_in, c->user_st);
+            cudaStreamWaitEvent(c->st, c->call_in, 0);
+        }
+    }
+    ~CallJoin() {
+        if (c && c->st) {
+            cudaEventRecord(c->call_out, c->st);
+            cudaStreamWaitEvent(c->user_st, c->call_out, 0);
+        }
+    }
+};
+
 HostProf g_hprof;
 DevMarks g_marks;
 
@@ -139,7 +156,7 @@ chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int 
     chopper_ctx *c = new chopper_ctx();
     c->cfg = *cfg;
     c->device = device;
-    c->st = (cudaStream_t)cuda_stream;
+    c->user_st = (cudaStream_t)cuda_stream;
     c->nccl = nccl_comm;
     c->rank = rank;
     c->nranks = nranks;
@@ -148,6 +165,20 @@ chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int 
     if (cudaSetDevice(device) != cudaSuccess) {
         delete c;
         return CHOPPER_E_CUDA;
+    }
+    // the library's work runs on a stream of the device's greatest priority: the block scheduler then dispatches
+    // the main path's kernels ahead of pending blocks of the side streams (the counter pass, the span sort), which
+    // fill the SMs the main path leaves idle.  Every call is ordered after the caller's stream and the caller's
+    // stream after the call (CallJoin).
+    {
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        if (cudaStreamCreateWithPriority(&c->st, cudaStreamNonBlocking, greatest) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->call_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->call_out, cudaEventDisableTiming) != cudaSuccess) {
+            delete c;
+            return CHOPPER_E_CUDA;
+        }
     }
     for (int q = 0; q < 3; q++) {
         if (cudaStreamCreateWithFlags(&c->side[q], cudaStreamNonBlocking) != cudaSuccess ||
@@ -184,6 +215,7 @@ chopper_status chopper_load_columns(chopper_ctx *ctx, const chopper_events *ev, 
     g_hprof.dump();
     g_marks.dump();
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    CallJoin join_(ctx);
     g_marks.mark(ctx->st, "begin");
     ctx->poison = CHOPPER_OK;             // a new step
     ctx->x_exchanged = ctx->d_exchanged = false;
@@ -248,6 +280,7 @@ static chopper_status align(chopper_ctx *ctx, const chopper_counter_pass *passes
 chopper_status chopper_align(chopper_ctx *ctx, const chopper_counter_pass *passes, int32_t n_passes,
                              int32_t n_counters, double *counters_out, int64_t *offsets_ns) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    CallJoin join_(ctx);
     ctx->C = n_counters > 0 ? n_counters : 0;     // fixes the shape of exchange #2 even if this call fails
     if (ctx->poison != CHOPPER_OK) {
         chopper_status s = ch_exchange_poison(ctx, 1);
@@ -293,6 +326,7 @@ static chopper_status attribute(chopper_ctx *ctx, int32_t *span_idx) {
 
 chopper_status chopper_attribute(chopper_ctx *ctx, int32_t *span_idx) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    CallJoin join_(ctx);
     if (ctx->poison != CHOPPER_OK) return dead_call(ctx);
     return step(ctx, attribute(ctx, span_idx));
 }
@@ -317,6 +351,7 @@ static chopper_status overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_n
 chopper_status chopper_overlap(chopper_ctx *ctx, int64_t *ovl_ns, int64_t *prep_ns, int64_t *call_ns, int64_t *phi,
                                int64_t *psi) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    CallJoin join_(ctx);
     if (ctx->poison != CHOPPER_OK) return dead_call(ctx);
     return step(ctx, overlap(ctx, ovl_ns, prep_ns, call_ns, phi, psi));
 }
@@ -410,6 +445,7 @@ static chopper_status breakdown(chopper_ctx *ctx, const chopper_bd_params *p, ch
 
 chopper_status chopper_breakdown(chopper_ctx *ctx, const chopper_bd_params *p, chopper_tables *out) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    CallJoin join_(ctx);
     if (ctx->poison != CHOPPER_OK) return dead_call(ctx);
     return step(ctx, breakdown(ctx, p, out));
 }
@@ -427,6 +463,7 @@ static chopper_status reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
 
 chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    CallJoin join_(ctx);
     if (ctx->poison != CHOPPER_OK) {
         chopper_status s = ch_exchange_poison(ctx, 2);
         return s != CHOPPER_OK ? s : dead_call(ctx);
@@ -438,6 +475,7 @@ chopper_status chopper_reduce_ranks(chopper_ctx *ctx, chopper_global *out) {
 
 chopper_status chopper_report_cdf(chopper_ctx *ctx, double *out, int64_t cap, int64_t *n_rows) {
     if (!ctx || !n_rows || cap < 0 || (cap > 0 && !out)) return CHOPPER_E_INVALID_ARG;
+    CallJoin join_(ctx);
     if (ctx->stage != 6) return ch_fail(ctx, CHOPPER_E_STATE, "chopper_report_cdf before chopper_reduce_ranks");
     return ch_report_cdf(ctx, out, cap, n_rows);
 }
@@ -446,6 +484,7 @@ size_t chopper_ingest_scratch_bytes(int64_t n_bytes) { return n_bytes < 0 ? 0 : 
 
 chopper_status chopper_ingest_chrome(chopper_ctx *ctx, const char *json, int64_t n_bytes, void *scratch,
                                      size_t scratch_bytes, const chopper_ingest_out *out, chopper_ingest_report *rep) {
+    CallJoin join_(ctx);
     if (!ctx || n_bytes < 0 || (n_bytes > 0 && !json) || !scratch || !out || !rep || out->ev_cap < 0 ||
         out->span_cap < 0 || (out->ev_cap > 0 && (!out->t_l || !out->t_ks || !out->t_ke || !out->meta || !out->name_id)) ||
         (out->span_cap > 0 && (!out->span_gl || !out->span_start || !out->span_end || !out->span_label)))
@@ -456,12 +495,14 @@ chopper_status chopper_ingest_chrome(chopper_ctx *ctx, const char *json, int64_t
 chopper_status chopper_set_metrics(chopper_ctx *ctx, int32_t n, const char *const *exprs, int32_t n_names,
                                    const char *const *names, int32_t *bad_expr) {
     if (!ctx || n < 0 || n_names < 0 || (n > 0 && !exprs) || (n_names > 0 && !names)) return CHOPPER_E_INVALID_ARG;
+    CallJoin join_(ctx);
     return ch_compile_metrics(ctx, n, exprs, n_names, names, bad_expr);
 }
 
 chopper_status chopper_cpu_util(chopper_ctx *ctx, const chopper_cpu_samples *samples, const int32_t *topology,
                                 int32_t n_logical, int64_t *c_active, double *c_min, int64_t cap,
                                 chopper_cpu_summary *out) {
+    CallJoin join_(ctx);
     if (!ctx || !samples || !out || samples->n < 0 || n_logical <= 0 || !topology || cap < 0 ||
         (samples->n > 0 && (!samples->ts_ns || !samples->logical_core || !samples->util_pct)))
         return CHOPPER_E_INVALID_ARG;
@@ -513,6 +554,7 @@ chopper_status chopper_get_report(const chopper_ctx *ctx, chopper_report *out) {
 
 chopper_status chopper_status_sync(chopper_ctx *ctx, uint32_t *mask) {
     if (!ctx) return CHOPPER_E_INVALID_ARG;
+    CallJoin join_(ctx);
     uint32_t m = ctx->latched_host;
     unsigned int dl = 0;
     if (ctx->d_rep && ch_d2h(ctx, &dl, &ctx->d_rep->latched, 4) != cudaSuccess) m |= 1u << CHOPPER_E_CUDA;
@@ -543,6 +585,9 @@ void chopper_destroy(chopper_ctx *ctx) {
     if (ctx->prep_join) cudaEventDestroy(ctx->prep_join);
     if (ctx->span_join) cudaEventDestroy(ctx->span_join);
     if (ctx->h_pin) cudaFreeHost(ctx->h_pin);
+    if (ctx->st) cudaStreamDestroy(ctx->st);
+    if (ctx->call_in) cudaEventDestroy(ctx->call_in);
+    if (ctx->call_out) cudaEventDestroy(ctx->call_out);
     delete ctx;
 }
 

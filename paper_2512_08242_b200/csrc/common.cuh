@@ -78,7 +78,9 @@ struct PassDesc {          // device copy of one counter pass
 struct chopper_ctx {
     chopper_config cfg{};
     int device = 0;
-    cudaStream_t st = nullptr;
+    cudaStream_t st = nullptr;             // the library's own stream (greatest priority), joined to user_st per call
+    cudaStream_t user_st = nullptr;        // the caller's stream (chopper_create)
+    cudaEvent_t call_in = nullptr, call_out = nullptr;
     cudaStream_t side[3] = {nullptr, nullptr, nullptr};   // fork / join of independent small kernels
     cudaEvent_t fork_ev = nullptr, join_ev[3] = {nullptr, nullptr, nullptr};
     // span push-order sort enqueued on side[2] at the end of chopper_load_columns (spans.cu), so that it runs
