@@ -18,7 +18,11 @@
  *    chopper_destroy (or the next chopper_load_columns).
  *  - The library never allocates device memory: all intermediates live in
  *    the caller's scratch buffer of chopper_scratch_bytes() bytes.
- *  - Every call enqueues work on the ctx stream.  Host-detectable errors
+ *  - Every call enqueues work on the ctx stream: the library's own stream of
+ *    the device's greatest priority, ordered after the caller's stream
+ *    (chopper_create's cuda_stream) at the call's start, and the caller's
+ *    stream ordered after the call's work at its end, so to the caller the
+ *    work behaves as if it were enqueued on its stream.  Host-detectable errors
  *    (bad arguments, call order) are returned immediately; device-detected
  *    errors latch into a status mask read by chopper_status_sync().  Some
  *    calls synchronize the stream internally (documented per call).
@@ -249,7 +253,9 @@ size_t chopper_scratch_bytes(const chopper_config *cfg, int64_t n_events, int64_
 
 /* nccl_comm: ncclComm_t of the process group (borrowed), NULL when nranks == 1 (or when a transport is
  * installed with chopper_set_allgather before chopper_align).
- * cuda_stream: cudaStream_t (borrowed), NULL = legacy default stream. */
+ * cuda_stream: cudaStream_t (borrowed), NULL = legacy default stream: every call is ordered after the work
+ * already on it and before the work enqueued on it afterwards (the calls run on an internal stream of the
+ * greatest priority, whose kernels the block scheduler places ahead of the library's side-stream work). */
 chopper_status chopper_create(chopper_ctx **out, const chopper_config *cfg, int device, void *cuda_stream,
                               void *nccl_comm, int rank, int nranks, void *scratch, size_t scratch_bytes);
 
