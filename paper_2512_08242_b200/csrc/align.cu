@@ -490,6 +490,7 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
             CH_CUDA(ctx, cudaMemcpyAsync(didx, idx.data(), 4 * n_passes, cudaMemcpyHostToDevice, ctx->st));
             CH_TRY(ch_fill_u64(ctx, mis, n_passes, ~0ull));
         }
+        g_marks.mark(ctx->st, "al_pre_rank");
         k_meta_apply<<<(unsigned)ntile, MR_NT, 0, ctx->st>>>(ctx->ev.meta, ctx->ev.start_ns, ctx->ev.end_ns, N,
                                                              ctx->d_gpu_lg, tex, ntile, base, n_lg, ctx->d_nm_rank,
                                                              ctx->d_xsend, K, ctx->xW, ctx->d_xovf, ctx->ev.name_id,
@@ -497,7 +498,9 @@ chopper_status ch_align(chopper_ctx *ctx, const chopper_counter_pass *passes, in
         CH_LAUNCHED(ctx);
         k_mg<<<1, 256, 0, ctx->st>>>(base, n_lg, ctx->d_mg);
         CH_LAUNCHED(ctx);
+        g_marks.mark(ctx->st, "al_rank");
         CH_TRY(ch_offsets_launch(ctx));                 // the exchange block is complete: a4 shares the read-back
+        g_marks.mark(ctx->st, "al_offsets");
 
         if (n_passes > 0) {
             // one read-back: the name-sequence divergences and the per-gpu non-MEMOP counts

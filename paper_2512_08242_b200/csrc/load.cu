@@ -765,6 +765,7 @@ chopper_status ch_load(chopper_ctx *ctx) {
         k_validate_samples<<<gs, NT, 0, ctx->st>>>(ctx->smp.gpu, ctx->smp.ts_ns, ctx->M, G, ctx->d_rep);
         CH_LAUNCHED(ctx);
     }
+    g_marks.mark(ctx->st, "ld_validate");
     CH_TRY(read_report(ctx));
     DevReport &h = ctx->h_rep;
     ctx->t0 = n > 0 ? dec_i64(h.t_min_enc) : 0;
