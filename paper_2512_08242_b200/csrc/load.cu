@@ -246,8 +246,12 @@ __global__ void __launch_bounds__(LN_NT) k_lean_tiles(const uint32_t *__restrict
     }
     if (hc) atomicAdd(&ln_h[hb], hc);
     int64_t tc, tp;
-    block_excl_sum<LN_NT>(cc, &tc, sm);
-    block_excl_sum<LN_NT>(cp, &tp, sm);
+    {                                    // (tile counts < 2^32: both totals from one packed scan)
+        int64_t t2;
+        block_excl_sum<LN_NT>(cc | (cp << 32), &t2, sm);
+        tc = t2 & 0xFFFFFFFFll;
+        tp = t2 >> 32;
+    }
     if (mtc) {                           // the tile counts of chopper_align's rank pass (its tiles are these)
         int64_t t3;
         block_excl_sum<LN_NT>((int64_t)c3, &t3, sm);
@@ -375,8 +379,9 @@ __global__ void __launch_bounds__(LN_NT) k_lean_chain(const uint32_t *__restrict
         if (k < nv && is_comm(kd)) cc++;
         else if (k < nv && kd == CK_COMPUTE) { cp++; last = i0 + k; }
     }
-    int64_t ex_c = block_excl_sum<LN_NT>(cc, nullptr, sm) + t_comm_ex[blockIdx.x];
-    int64_t ex_p = block_excl_sum<LN_NT>(cp, nullptr, sm) + t_comp_ex[blockIdx.x];
+    const int64_t ex2 = block_excl_sum<LN_NT>(cc | (cp << 32), nullptr, sm);   // (tile counts < 2^32: one packed scan)
+    int64_t ex_c = (ex2 & 0xFFFFFFFFll) + t_comm_ex[blockIdx.x];
+    int64_t ex_p = (ex2 >> 32) + t_comp_ex[blockIdx.x];
     // the last compute index before this thread
     int64_t x = last;
 #pragma unroll
