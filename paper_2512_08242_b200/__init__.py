@@ -265,9 +265,21 @@ def chopper_load_columns(ctx, ev: chopper_events, sp: chopper_spans, smp: Option
                                                ctypes.byref(smp) if smp is not None else None)
 
 
-def chopper_align(ctx, passes: List[chopper_counter_pass], n_counters: int, counters_out=None, offsets=None) -> int:
-    arr = (chopper_counter_pass * max(len(passes), 1))(*passes)
-    return load_library().chopper_align(ctx, arr, len(passes), n_counters, _ptr(counters_out),
+class PassArray:
+    """A prebuilt ctypes array of chopper_counter_pass (the Pipeline keeps one per input set)."""
+    __slots__ = ("arr", "n")
+
+    def __init__(self, arr, n: int):
+        self.arr, self.n = arr, n
+
+
+def chopper_align(ctx, passes, n_counters: int, counters_out=None, offsets=None) -> int:
+    """passes: a list of chopper_counter_pass, or a PassArray"""
+    if isinstance(passes, PassArray):
+        arr, n = passes.arr, passes.n
+    else:
+        arr, n = (chopper_counter_pass * max(len(passes), 1))(*passes), len(passes)
+    return load_library().chopper_align(ctx, arr, n, n_counters, _ptr(counters_out),
                                         offsets.ctypes.data if offsets is not None else None)
 
 

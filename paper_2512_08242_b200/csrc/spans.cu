@@ -530,10 +530,12 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
     const int n_lg = ctx->n_lg;
     const int n_lists = n_lg * 4;
     if (!ctx->span_launched) CH_TRY(ch_span_sort_launch(ctx));     // (not launched by the load)
+    g_marks.mark(ctx->st, "at_begin");
     if (ctx->span_pending) {
         CH_CUDA(ctx, cudaStreamWaitEvent(ctx->st, ctx->span_join, 0));
         ctx->span_pending = false;
     }
+    g_marks.mark(ctx->st, "at_span_join");
     int32_t *Plist = ctx->ss.Plist;
     ctx->list_beg.assign(n_lists + 2, 0);
     ctx->S_loc = 0;

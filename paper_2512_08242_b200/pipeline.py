@@ -12,7 +12,7 @@ from typing import Dict, Optional
 
 import numpy as np
 
-from . import (chopper_set_allgather_loopback, chopper_scratch_plan, chopper_shape, chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
+from . import (PassArray, chopper_set_allgather_loopback, chopper_scratch_plan, chopper_shape, chopper_align, chopper_attribute, chopper_breakdown, chopper_config, chopper_counter_pass,
                chopper_cpu_util, chopper_create, chopper_set_metrics, chopper_destroy, chopper_events, chopper_get_report, chopper_global, chopper_report_cdf,
                chopper_kernel_launches, chopper_load_columns, chopper_overlap, chopper_reduce_ranks,
                chopper_samples, chopper_scratch_bytes, chopper_spans, chopper_status_sync, chopper_tables,
@@ -125,6 +125,8 @@ class Pipeline:
         self.ctx = None
         self.scratch = None
         self.d = {}
+        self.passes_dev = []
+        self._mcache = {}
         self.cpu = None
 
     def set_metrics(self, exprs, names) -> None:
@@ -172,6 +174,7 @@ class Pipeline:
                                         np.ascontiguousarray(slots, np.int32),
                                         torch.from_numpy(np.ascontiguousarray(vals, np.float64)).to(dev)))
         self.d = d
+        self._mcache = {}
         self.n_counters = n_counters
         self.N, self.S, self.M = len(src["t_l"]), len(src["span_gl"]), len(src["smp_gpu"])
         if plan_laminar is None:
@@ -229,18 +232,38 @@ class Pipeline:
             self.stream.wait_event(ready)
         self.d, self.passes_dev, self.cpu = s["d"], s["passes"], s["cpu"]
 
-    # ---- run ----
-    def run(self, params: dict, full: bool = False, check: bool = True) -> dict:
-        """All six ABI calls.  full=True also writes the per-event outputs (parity mode)."""
-        torch = self.torch
-        d, N = self.d, self.N
-        ev = chopper_events(n=N, dispatch_ns=d["t_l"].data_ptr(), start_ns=d["t_ks"].data_ptr(),
+    def _marshal(self):
+        """The ABI structs of the current input set: events / spans / samples and the counter-pass array.  Built
+        once per input set (upload, or each set `use_inputs` alternates between) -- the set's tensors are kept
+        in the cache entry, so an entry's device pointers stay valid while it is cached."""
+        key = (id(self.d), id(self.passes_dev), id(self.cpu))
+        hit = self._mcache.get(key)
+        if hit is not None and hit[0] is self.d and hit[1] is self.passes_dev:
+            return hit[2]
+        d = self.d
+        ev = chopper_events(n=self.N, dispatch_ns=d["t_l"].data_ptr(), start_ns=d["t_ks"].data_ptr(),
                             end_ns=d["t_ke"].data_ptr(), meta=d["meta"].data_ptr(), name_id=d["name_id"].data_ptr())
         sp = chopper_spans(n=self.S, gpu_level=d["span_gl"].data_ptr(), start_ns=d["span_start"].data_ptr(),
                            end_ns=d["span_end"].data_ptr(), label=d["span_label"].data_ptr())
         smp = chopper_samples(n=self.M, gpu=d["smp_gpu"].data_ptr(), ts_ns=d["smp_ts"].data_ptr(),
                               freq_mhz=d["smp_freq"].data_ptr(), power_mw=d["smp_power"].data_ptr()) \
             if self.M > 0 else None
+        passes = [chopper_counter_pass(gpu=g, n=names.numel(), name_id=names.data_ptr(), k=len(slots),
+                                       slot=slots.ctypes.data, values=vals.data_ptr())
+                  for (g, names, slots, vals) in self.passes_dev]
+        arr = (chopper_counter_pass * max(len(passes), 1))(*passes)
+        m = (ev, sp, smp, PassArray(arr, len(passes)))
+        if len(self._mcache) >= 4:
+            self._mcache.clear()
+        self._mcache[key] = (self.d, self.passes_dev, m)     # (the slots arrays live in passes_dev)
+        return m
+
+    # ---- run ----
+    def run(self, params: dict, full: bool = False, check: bool = True) -> dict:
+        """All six ABI calls.  full=True also writes the per-event outputs (parity mode)."""
+        torch = self.torch
+        N = self.N
+        ev, sp, smp, passes = self._marshal()
         res = {"full": full}
         allow = () if check else tuple(range(1, 10))
         s = chopper_load_columns(self.ctx, ev, sp, smp)
@@ -253,12 +276,6 @@ class Pipeline:
             _check(self.ctx, s, "chopper_load_columns", allow=allow)
             return res
         C = self.n_counters
-        passes = []
-        self._slot_keep = []
-        for (g, names, slots, vals) in self.passes_dev:
-            self._slot_keep.append(slots)
-            passes.append(chopper_counter_pass(gpu=g, n=names.numel(), name_id=names.data_ptr(), k=len(slots),
-                                               slot=slots.ctypes.data, values=vals.data_ptr()))
         dev = torch.device("cuda", self.device)
         out = {}
         if full:
