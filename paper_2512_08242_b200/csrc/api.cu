@@ -291,6 +291,26 @@ chopper_status chopper_align(chopper_ctx *ctx, const chopper_counter_pass *passe
     return s;
 }
 
+}  // extern "C"
+// chopper_overlap's preparation on side[1] (see attribute)
+chopper_status ch_prep_side(chopper_ctx *ctx) {
+    ctx->prep_deferred = false;
+    // ordered after the main stream's work at chopper_attribute's start (span_fork, recorded there; the load's
+    // span sort consumed its previous record), not after the span kernels enqueued since
+    CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[1], ctx->span_fork, 0));
+    cudaStream_t main_st = ctx->st;
+    ctx->st = ctx->side[1];
+    ctx->hold_scratch = true;
+    const chopper_status ps = ch_overlap_prep(ctx);
+    ctx->hold_scratch = false;
+    CH_CUDA(ctx, cudaEventRecord(ctx->prep_join, ctx->st));
+    ctx->st = main_st;
+    CH_TRY(ps);
+    ctx->prep_done = ctx->prep_pending = true;
+    return CHOPPER_OK;
+}
+extern "C" {
+
 static chopper_status attribute(chopper_ctx *ctx, int32_t *span_idx) {
     if (ctx->stage == 1 && ctx->nranks == 1) {
         // align may be skipped on one rank without counters
@@ -303,21 +323,12 @@ static chopper_status attribute(chopper_ctx *ctx, int32_t *span_idx) {
     ch_tick(ctx, 2, 0);
     // chopper_overlap's preparation (comm union, sample integrals, timeline) needs nothing from the span tables:
     // it runs on side[1] beside the span build, whose kernels are small and whose host synchronizations would
-    // leave the gpu idle; chopper_overlap joins it
-    {
-        CH_CUDA(ctx, cudaEventRecord(ctx->fork_ev, ctx->st));
-        CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[1], ctx->fork_ev, 0));
-        cudaStream_t main_st = ctx->st;
-        ctx->st = ctx->side[1];
-        ctx->hold_scratch = true;
-        const chopper_status ps = ch_overlap_prep(ctx);
-        ctx->hold_scratch = false;
-        CH_CUDA(ctx, cudaEventRecord(ctx->prep_join, ctx->st));
-        ctx->st = main_st;
-        CH_TRY(ps);
-        ctx->prep_done = ctx->prep_pending = true;
-    }
+    // leave the gpu idle; chopper_overlap joins it.  Its host part is done inside the span build, once the
+    // Euler-table kernels are enqueued (ch_prep_side), so that the gpu runs them meanwhile
+    CH_CUDA(ctx, cudaEventRecord(ctx->span_fork, ctx->st));
+    ctx->prep_deferred = true;
     CH_TRY(ch_build_spans(ctx));
+    if (ctx->prep_deferred) CH_TRY(ch_prep_side(ctx));
     CH_TRY(ch_attr_pass(ctx, span_idx));
     ch_tick(ctx, 2, 1);
     ctx->stage = 3;

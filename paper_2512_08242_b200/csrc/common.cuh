@@ -80,6 +80,7 @@ struct chopper_ctx {
     int device = 0;
     cudaStream_t st = nullptr;             // the library's own stream (greatest priority), joined to user_st per call
     cudaStream_t user_st = nullptr;        // the caller's stream (chopper_create)
+    bool prep_deferred = false;            // chopper_attribute: the overlap preparation is still to be enqueued
     cudaEvent_t call_in = nullptr, call_out = nullptr;
     cudaStream_t side[3] = {nullptr, nullptr, nullptr};   // fork / join of independent small kernels
     cudaEvent_t fork_ev = nullptr, join_ev[3] = {nullptr, nullptr, nullptr};
@@ -390,6 +391,7 @@ extern DevMarks g_marks;
     } while (0)
 
 chopper_status ch_fail(chopper_ctx *ctx, chopper_status s, const std::string &msg);
+chopper_status ch_prep_side(chopper_ctx *ctx);   // api.cu: chopper_overlap's preparation on side[1]
 // host synchronization with the ctx stream (counted: chopper_host_syncs)
 inline cudaError_t ch_sync(chopper_ctx *ctx) {
     ctx->syncs++;

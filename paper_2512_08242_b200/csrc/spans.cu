@@ -651,8 +651,13 @@ chopper_status ch_build_spans(chopper_ctx *ctx) {
         // one read-back: laminarity flags and the tour check
         CH_CUDA(ctx, ch_d2h(ctx, ctx->list_flags.data(), ctx->d_list_flags, 4 * n_lists));
         CH_CUDA(ctx, ch_d2h(ctx, &h_et_bad, et_bad, 4));
+        // chopper_overlap's preparation: its host work while the gpu runs the kernels above.  Its buffers are
+        // allocated above this block's transients, which therefore stay allocated for the step (the scratch plan
+        // counts the chunk stacks and sparse tables per span)
+        const bool prep_here = ctx->prep_deferred;
+        if (prep_here) CH_TRY(ch_prep_side(ctx));
         CH_CUDA(ctx, ch_sync(ctx));
-        ctx->used = mark;
+        if (!prep_here) ctx->used = mark;
     }
     // exact sweep for non-laminar lists
     std::vector<int> sweep;
