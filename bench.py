@@ -402,7 +402,7 @@ def main():
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "traffic_source": traffic_src or "no committed ncu capture for this config",
-            "kernel": "k_events_w (fused event pass, a5-a9 time part; time = its own CUDA-event bracket)",
+            "kernel": "k_events_l (fused lean event pass, a5-a9 time part; k_events_w / k_events on the general paths; time = its own CUDA-event bracket)",
             "peak_source": peak_src, "frac_of_nominal_8TBs": (achieved / NOMINAL_HBM_GBS) if achieved else None,
             "alg_bytes_per_launch": alg, "alg_formula": "28 B/event (t_l, t_ks, t_ke, meta) + 96 B/instance row",
             "avg_launch_ms": ev_avg, "event_pass_phase_ms": ev_phase_avg, "phase_ms_last_step": phase_ms}
