@@ -81,8 +81,6 @@ struct chopper_ctx {
     cudaStream_t st = nullptr;             // the library's own stream (greatest priority), joined to user_st per call
     cudaStream_t user_st = nullptr;        // the caller's stream (chopper_create)
     bool prep_deferred = false;            // chopper_attribute: the overlap preparation is still to be enqueued
-    bool span_sort_deferred = false;       // chopper_load_columns: the span push-order sort is still to be enqueued
-    bool span_fork_recorded = false;       // span_fork already marks where that sort may start
     cudaEvent_t call_in = nullptr, call_out = nullptr;
     cudaStream_t side[3] = {nullptr, nullptr, nullptr};   // fork / join of independent small kernels
     cudaEvent_t fork_ev = nullptr, join_ev[3] = {nullptr, nullptr, nullptr};

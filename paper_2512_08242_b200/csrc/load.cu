@@ -591,13 +591,6 @@ static void fill_public_report(chopper_ctx *ctx) {
 }
 
 static chopper_status finish_load(chopper_ctx *ctx) {
-    if (ctx->span_sort_deferred) {          // (not enqueued inside the lean a2)
-        ctx->span_sort_deferred = false;
-        // forked from here, not from the early mark: its buffers may reuse scratch that the a2 path's queued
-        // kernels released only on the host
-        ctx->span_fork_recorded = false;
-        CH_TRY(ch_span_sort_launch(ctx));
-    }
     // same-stream overlaps are data: reported, processing continues
     fill_public_report(ctx);
     if (ctx->h_rep.val_count[CV_STREAM_OVERLAP]) ctx->latched_host |= 1u << CHOPPER_E_VALIDATION;
@@ -737,8 +730,6 @@ chopper_status ch_load(chopper_ctx *ctx) {
         ctx->span_pending = false;
     }
     ctx->span_launched = false;
-    ctx->span_sort_deferred = false;
-    ctx->span_fork_recorded = false;
     ctx->d_meta_tc = nullptr;
     ctx->ss_pending = false;
     if (ctx->prep_pending) {                    // likewise chopper_overlap's preparation
@@ -820,12 +811,9 @@ chopper_status ch_load(chopper_ctx *ctx) {
     }
     CH_CUDA(ctx, cudaMemcpyAsync(ctx->d_gpu_lg, ctx->gpu_lg_h, sizeof(int32_t) * CH_MAX_GPUS, cudaMemcpyHostToDevice,
                                  ctx->st));
-    // the spans are validated: their push-order sort runs on a side stream, beside the rest of the load and
-    // chopper_align and their host synchronizations (spans.cu; chopper_attribute joins it).  It is enqueued inside
-    // the lean a2 once that pass's kernels are queued, so that its host work overlaps them (else at the load's end)
-    ctx->span_sort_deferred = true;
-    CH_CUDA(ctx, cudaEventRecord(ctx->span_fork, ctx->st));   // (its start: after the validation and gpu map)
-    ctx->span_fork_recorded = true;
+    // the spans are validated: their push-order sort starts now on a side stream, beside the rest of the load
+    // and chopper_align and their host synchronizations (spans.cu; chopper_attribute joins it)
+    CH_TRY(ch_span_sort_launch(ctx));
     // a2: partition by (lg, dense group); full radix sort only if a group is not start-monotone
     ctx->d_perm = CH_ALLOC(ctx, uint32_t, n);
     ctx->d_pred_end = nullptr;       // materialized by the general path only (k_chain); lean: derived (PredView)
@@ -946,16 +934,8 @@ static chopper_status lean_a2(chopper_ctx *ctx, bool *fell_back) {
     unsigned int hnm = 0;
     CH_CUDA(ctx, ch_d2h(ctx, ctx->bucket_beg.data(), ctx->d_bucket_beg, 8 * (nb + 1)));
     CH_CUDA(ctx, ch_d2h(ctx, &hnm, nonmono, 4));
-    // the span push-order sort (side[2]): its host work while the gpu runs the kernels above.  Its buffers sit
-    // above this pass's transients, which then stay allocated for the step (tile-count arrays, ~40 B per tile);
-    // nothing allocated since the load's validation was released, so the sort may start from the early mark
-    const bool sort_here = ctx->span_sort_deferred;
-    if (sort_here) {
-        ctx->span_sort_deferred = false;
-        CH_TRY(ch_span_sort_launch(ctx));
-    }
     CH_TRY(read_report(ctx));
-    if (!sort_here) ctx->used = keep;
+    ctx->used = keep;
     if (hnm) {
         // a compute group out of start order: the full path (it resets and recomputes the overlap report)
         unsigned long long zero = 0, none = ~0ull;

@@ -490,8 +490,7 @@ chopper_status ch_span_sort_launch(chopper_ctx *ctx) {
     CH_ALLOC_END(ctx);
     q.big = reinterpret_cast<unsigned int *>(q.lb + n_lists);
     // side stream: ordered after everything chopper_load_columns enqueued
-    if (!ctx->span_fork_recorded) CH_CUDA(ctx, cudaEventRecord(ctx->span_fork, ctx->st));   // (else recorded by
-    ctx->span_fork_recorded = false;                                                        //  the load earlier)
+    CH_CUDA(ctx, cudaEventRecord(ctx->span_fork, ctx->st));
     CH_CUDA(ctx, cudaStreamWaitEvent(ctx->side[2], ctx->span_fork, 0));
     cudaStream_t main_st = ctx->st;
     ctx->st = ctx->side[2];
